@@ -1,0 +1,125 @@
+/*
+ * vlcache.h -- C ABI of the B200 (sm_100a) VLCache cache-reuse prefill kernels.
+ *
+ * The reference (`kvreuse` 0.1.0, /root/reference/pkg/src/kvreuse) is a pure
+ * Python/NumPy package with no FFI: its plugin boundary is the Python API
+ * (`prefill_with_reuse`, `CacheStore`, `plan_greedy`, ...; __init__.py:3-16).
+ * The drop-in keeps that Python API (package `paper_2512_12977_b200`) and moves
+ * every NumPy op of the hot path behind this C ABI; each entry point names the
+ * reference lines it replaces.  The Python binding is ctypes
+ * (paper_2512_12977_b200/_native.py); see INTEGRATION.md.
+ *
+ * Conventions: every function returns 0 (VLC_OK) or a VLC_ERR_* status and never
+ * throws; vlc_last_error() gives a thread-local message.  All tensor arguments
+ * are caller-owned DEVICE pointers; nothing synchronises the host; every call is
+ * stream-ordered on `stream` and re-entrant across streams.  Dtypes: "bf16" =
+ * IEEE bfloat16 stored as uint16, "f32" = float.
+ */
+#ifndef VLCACHE_H
+#define VLCACHE_H
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VLC_OK 0
+#define VLC_ERR_INVALID 1     /* bad argument (maps to InputError)           */
+#define VLC_ERR_UNSUPPORTED 2 /* shape the kernels do not handle             */
+#define VLC_ERR_CUDA 3        /* CUDA runtime / driver failure               */
+
+/* GEMM epilogue kinds (vlc_gemm_bf16). */
+#define VLC_EPI_F32 0       /* out[map1?map1[j]:j][f] = acc            (engine.py:187 logits)   */
+#define VLC_EPI_RESID 1     /* out[j][f] += acc, fp32 residual          (engine.py:183, 185)     */
+#define VLC_EPI_BF16 2      /* out[j][f] = bf16(acc)                                              */
+#define VLC_EPI_BIAS_ADD 3  /* out[j][f] = acc + bias[f] + add[j][f]    (model.py:316)           */
+#define VLC_EPI_SWIGLU 4    /* rows interleaved gate/up: out[j][f/2] = silu(g)*u (model.py:262)  */
+#define VLC_EPI_QKV_PLAIN 5 /* q/k/v sections -> out/out2/out3          (model.py:318)           */
+#define VLC_EPI_QKV_ROPE 6  /* q rot -> out[map1[j]], k -> out4[j] (pre-RoPE) and rot -> out2
+                               [map2[j]], v -> out3[map2[j]]            (engine.py:176-180)       */
+
+typedef struct vlc_epilogue {
+  int kind;
+  int n_valid;   /* valid weight rows (output features)            */
+  int m_tokens;  /* valid token rows                                */
+  void* out;  int ldo;
+  void* out2; int ld2;
+  void* out3; int ld3;
+  void* out4; int ld4;
+  const int* map1;   /* token -> destination row of `out` (NULL = identity) */
+  const int* map2;   /* token -> KV-cache row                                 */
+  const int* pos;    /* token -> absolute position in its request           */
+  const float* cos_tab; /* [positions][tab_ld] f32 RoPE tables (model.py:129-134) */
+  const float* sin_tab;
+  int tab_ld;
+  int hd;            /* head_dim                                             */
+  int seg;           /* features per q / k / v section (= kv_dim)            */
+  const float* bias;
+  const float* add;  int ld_add;
+} vlc_epilogue;
+
+/* Mixed attention over cached + recomputed KV (engine.py:181-182, model.py:268-291).
+ * Work items: int32[n_items][8] = {q_row0, n_q<=128, head, kv_row0, key_begin,
+ * key_end, slot, 0}; slot<0 writes normalised bf16 rows to out[rowof[q]], slot>=0
+ * writes an unnormalised fp32 partial to ws_o/ws_ml for vlc_attn_combine.
+ * Combine items: int32[n_comb][8] = {q_row0, n_q, head, slot0, nslots, 0,0,0}.   */
+typedef struct vlc_attn_args {
+  const void* q; int q_rows_cap;                 /* bf16 [q_rows_cap][kv]            */
+  const void* kc; const void* vc;                /* bf16 [layers][kv_rows_cap][kv]   */
+  int layers_cap; int kv_rows_cap; int layer;
+  int kv; int heads; int head_dim;
+  const int* items; int n_items;
+  const int* qpos;                               /* [q] position within request       */
+  const int* rowof;                              /* [q] packed output row             */
+  void* out; int ldo;                            /* bf16 [rows][ldo]                  */
+  float* ws_o; float* ws_ml; int ws_slots;
+  const int* comb; int n_comb;
+  float scale_log2;                              /* log2(e) / sqrt(head_dim)          */
+} vlc_attn_args;
+
+const char* vlc_last_error(void);
+int vlc_version(void);
+
+/* Layer-0 hidden rows of the computed set (model.py:339-359, engine.py:167):
+ * src[r] >= 0: text token id -> bf16 embed row; src[r] < 0: fp32 encoder row (-src-1). */
+int vlc_embed_assemble(float* x, int ldx, const void* embed_bf16, int d, const float* enc_rows,
+                       const int* src, int rows, cudaStream_t stream);
+
+/* RMSNorm eps (model.py:257-259) of rows (optionally gathered via row_map) -> bf16 or f32. */
+int vlc_rmsnorm(const float* x, int ldx, const float* gamma, void* out, int ldo, int out_f32,
+                int rows, int d, const int* row_map, float eps, cudaStream_t stream);
+
+/* Fused gather + RoPE re-rotation + scatter of cached pre-RoPE K and copy of V from
+ * the paged store into the request KV cache (engine.py:153-155 + engine.py:180).
+ * descs int32[n][8] = {layer, page_tab_off, tok0, ntok, dst_row0, pos0, 0, 0};
+ * blocks int32[n_blocks][2] = {desc, token offset}; kc/vc bf16 [layers][kv_rows_cap][kv]. */
+int vlc_kv_relocate(const void* kpool, const void* vpool, int page_tokens, const int* page_table,
+                    int kv, int head_dim, void* kc, void* vc, int kv_rows_cap, const int* descs,
+                    const int* blocks, int n_blocks, const float* cos_tab, const float* sin_tab,
+                    int tab_ld, cudaStream_t stream);
+
+/* Store write (store.py:140-147 put_kv): src [layers][T][kv] (f32 or bf16) -> bf16 pages. */
+int vlc_store_write_pages(const void* src, int src_f32, int layers, int tokens, int kv,
+                          const int* page_table, int pages_per_layer, void* pool,
+                          int page_tokens, cudaStream_t stream);
+
+/* Fused-epilogue tcgen05 GEMM: acc[f][j] = sum_k W[f][k] X[j][k]; W bf16 [n_pad][k_pad]
+ * K-major, X bf16 [x_rows_cap][k_pad].  n_pad % 128 == 0, k_pad % 64 == 0. */
+int vlc_gemm_bf16(const void* w, int n_pad, int k_pad, const void* x, int x_rows_cap,
+                  int m_tokens, const vlc_epilogue* epi, int splits, float* ws, size_t ws_bytes,
+                  int* counters, cudaStream_t stream);
+
+int vlc_attn_mixed(const vlc_attn_args* args, cudaStream_t stream);
+int vlc_attn_combine(const vlc_attn_args* args, cudaStream_t stream);
+
+/* Patchify (model.py:312-314): pixels f32 [side][side] -> bf16 [T][ldo] patches. */
+int vlc_patchify(const float* pixels, int side, int patch, void* out, int ldo,
+                 cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VLCACHE_H */

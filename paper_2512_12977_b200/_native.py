@@ -1,0 +1,90 @@
+"""ctypes binding of libvlcache.so (include/vlcache.h).
+
+The library is the only compute path: if it is missing, or no CUDA device is
+present, every device entry point raises -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .exceptions import InputError, KVReuseError
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libvlcache.so")
+
+VLC_OK, VLC_ERR_INVALID, VLC_ERR_UNSUPPORTED, VLC_ERR_CUDA = 0, 1, 2, 3
+EPI_F32, EPI_RESID, EPI_BF16, EPI_BIAS_ADD, EPI_SWIGLU, EPI_QKV_PLAIN, EPI_QKV_ROPE = range(7)
+
+EXPORTS = ("vlc_last_error", "vlc_version", "vlc_embed_assemble", "vlc_rmsnorm", "vlc_kv_relocate",
+           "vlc_store_write_pages", "vlc_gemm_bf16", "vlc_attn_mixed", "vlc_attn_combine",
+           "vlc_patchify")
+
+
+class NativeError(KVReuseError):
+    """A CUDA-side failure reported by libvlcache (status VLC_ERR_CUDA / UNSUPPORTED)."""
+
+
+class Epilogue(C.Structure):
+    _fields_ = [("kind", C.c_int), ("n_valid", C.c_int), ("m_tokens", C.c_int),
+                ("out", C.c_void_p), ("ldo", C.c_int), ("out2", C.c_void_p), ("ld2", C.c_int),
+                ("out3", C.c_void_p), ("ld3", C.c_int), ("out4", C.c_void_p), ("ld4", C.c_int),
+                ("map1", C.c_void_p), ("map2", C.c_void_p), ("pos", C.c_void_p),
+                ("cos_tab", C.c_void_p), ("sin_tab", C.c_void_p), ("tab_ld", C.c_int),
+                ("hd", C.c_int), ("seg", C.c_int), ("bias", C.c_void_p), ("add", C.c_void_p),
+                ("ld_add", C.c_int)]
+
+
+class AttnArgs(C.Structure):
+    _fields_ = [("q", C.c_void_p), ("q_rows_cap", C.c_int), ("kc", C.c_void_p), ("vc", C.c_void_p),
+                ("layers_cap", C.c_int), ("kv_rows_cap", C.c_int), ("layer", C.c_int),
+                ("kv", C.c_int), ("heads", C.c_int), ("head_dim", C.c_int),
+                ("items", C.c_void_p), ("n_items", C.c_int), ("qpos", C.c_void_p),
+                ("rowof", C.c_void_p), ("out", C.c_void_p), ("ldo", C.c_int),
+                ("ws_o", C.c_void_p), ("ws_ml", C.c_void_p), ("ws_slots", C.c_int),
+                ("comb", C.c_void_p), ("n_comb", C.c_int), ("scale_log2", C.c_float)]
+
+
+_lib = None
+
+
+def load():
+    """Load (not build) the library; raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback)")
+        lib = C.CDLL(LIB_PATH)
+        vp, i, f = C.c_void_p, C.c_int, C.c_float
+        lib.vlc_last_error.restype = C.c_char_p
+        lib.vlc_version.restype = i
+        lib.vlc_embed_assemble.argtypes = [vp, i, vp, i, vp, vp, i, vp]
+        lib.vlc_rmsnorm.argtypes = [vp, i, vp, vp, i, i, i, i, vp, f, vp]
+        lib.vlc_kv_relocate.argtypes = [vp, vp, i, vp, i, i, vp, vp, i, vp, vp, i, vp, vp, i, vp]
+        lib.vlc_store_write_pages.argtypes = [vp, i, i, i, i, vp, i, vp, i, vp]
+        lib.vlc_gemm_bf16.argtypes = [vp, i, i, vp, i, i, C.POINTER(Epilogue), i, vp, C.c_size_t, vp, vp]
+        lib.vlc_attn_mixed.argtypes = [C.POINTER(AttnArgs), vp]
+        lib.vlc_attn_combine.argtypes = [C.POINTER(AttnArgs), vp]
+        lib.vlc_patchify.argtypes = [vp, i, i, vp, i, vp]
+        for name in EXPORTS:
+            getattr(lib, name).restype = C.c_char_p if name == "vlc_last_error" else i
+        _lib = lib
+    return _lib
+
+
+def check(status: int, what: str) -> None:
+    if status == VLC_OK:
+        return
+    msg = load().vlc_last_error().decode(errors="replace")
+    if status == VLC_ERR_INVALID:
+        raise InputError(f"{what}: {msg}")
+    raise NativeError(f"{what}: {msg} (status {status})")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)
+
+
+def ptr(t) -> int:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    return 0 if t is None else int(t.data_ptr())

@@ -1,0 +1,352 @@
+// Mixed attention of the reuse prefill (engine.py:179-182, model.py:268-291):
+// the recomputed queries of one request attend, causally by ABSOLUTE position,
+// over every key of the request -- cached keys re-rotated by kv_relocate and
+// fresh keys written by the QKV epilogue.  Flash-style on tcgen05:
+//   S = Q K^T  (UMMA 128x128xHD, accumulator in TMEM)
+//   softmax in registers (one thread per query row, exp2 domain, lazy rescale)
+//   O += P V   (P staged in smem K-major, V consumed MN-major, O in TMEM)
+// One CTA = (request, head, <=128 queries, key range); key ranges may be split
+// across CTAs, merged by attn_combine.
+#include "vlc_internal.h"
+
+namespace vlc {
+
+constexpr int ATT_THREADS = 192;
+constexpr int ATT_STAGES = 2;
+
+template <int HD>
+struct AttnCfg {
+  static constexpr int ATOM_E = HD < 64 ? HD : 64;        // elements per swizzled row
+  static constexpr int SWZ = ATOM_E * 2;                  // swizzle width in bytes
+  static constexpr int N_ATOMS = HD / ATOM_E;
+  static constexpr int TILE_BYTES = 128 * HD * 2;         // 128 rows x HD
+  static constexpr int ATOM_BYTES = 128 * SWZ;
+  static constexpr int P_BYTES = 128 * 128 * 2;
+  static constexpr int SMEM = 1024 + TILE_BYTES * (1 + 2 * ATT_STAGES) + P_BYTES + 256;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(ATT_THREADS, 1)
+    attn_fwd_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                const __grid_constant__ CUtensorMap map_v, vlc_attn_args a) {
+  using C = AttnCfg<HD>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + C::TILE_BYTES;
+  uint8_t* sV = sK + ATT_STAGES * C::TILE_BYTES;
+  uint8_t* sP = sV + ATT_STAGES * C::TILE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::P_BYTES);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + ATT_STAGES;
+  uint64_t* s_full = kv_empty + ATT_STAGES;
+  uint64_t* s_free = s_full + 1;
+  uint64_t* p_full = s_free + 1;
+  uint64_t* o_done = p_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
+
+  const int* it = a.items + blockIdx.x * 8;
+  const int q_row0 = it[0], n_q = it[1], head = it[2], kv_row0 = it[3];
+  const int key_begin = it[4], key_end = it[5], slot = it[6];
+  const int n_kt = (key_end - key_begin + 127) / 128;
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_k);
+    tma_prefetch(&map_v);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < ATT_STAGES; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 128);
+    mbar_init(p_full, 128);
+    mbar_init(o_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem_s = tmem, tmem_o = tmem + 128;
+
+  if (warp == 0) {
+    if (lane == 0 && n_kt > 0) {
+      const uint64_t pol_q = policy_evict_first();
+      const uint64_t pol_kv = policy_evict_normal();
+      mbar_expect_tx(q_full, C::TILE_BYTES);
+#pragma unroll
+      for (int at = 0; at < C::N_ATOMS; ++at)
+        tma_load_2d(sQ + at * C::ATOM_BYTES, &map_q, q_full, head * HD + at * C::ATOM_E, q_row0, pol_q);
+      for (int j = 0; j < n_kt; ++j) {
+        const int st = j % ATT_STAGES;
+        mbar_wait(&kv_empty[st], ((j / ATT_STAGES) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], 2 * C::TILE_BYTES);
+        const int krow = kv_row0 + key_begin + j * 128;
+#pragma unroll
+        for (int at = 0; at < C::N_ATOMS; ++at) {
+          tma_load_3d(sK + st * C::TILE_BYTES + at * C::ATOM_BYTES, &map_k, &kv_full[st],
+                      head * HD + at * C::ATOM_E, krow, a.layer, pol_kv);
+          tma_load_3d(sV + st * C::TILE_BYTES + at * C::ATOM_BYTES, &map_v, &kv_full[st],
+                      head * HD + at * C::ATOM_E, krow, a.layer, pol_kv);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && n_kt > 0) {
+      const uint32_t idesc_s = make_idesc_bf16(128, 128, 0, 0);
+      const uint32_t idesc_o = make_idesc_bf16(128, HD, 0, 1);
+      const uint32_t q_addr = smem_u32(sQ);
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int j) {
+        const int st = j % ATT_STAGES;
+        mbar_wait(&kv_full[st], (j / ATT_STAGES) & 1);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + st * C::TILE_BYTES);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const int at = (k * 16) / C::ATOM_E;
+          const uint32_t off = at * C::ATOM_BYTES + ((k * 16) % C::ATOM_E) * 2;
+          const uint64_t ad = make_sdesc(q_addr + off, 16, 8 * C::SWZ, C::SWZ);
+          const uint64_t bd = make_sdesc(k_addr + off, 16, 8 * C::SWZ, C::SWZ);
+          tc_mma_f16(tmem_s, ad, bd, idesc_s, k > 0 ? 1u : 0u);
+        }
+        tc_commit(s_full);
+      };
+      issue_s(0);
+      const uint32_t p_addr = smem_u32(sP);
+      for (int j = 0; j < n_kt; ++j) {
+        if (j + 1 < n_kt) {
+          mbar_wait(s_free, j & 1);
+          tc_fence_after();
+          issue_s(j + 1);
+        }
+        mbar_wait(p_full, j & 1);
+        tc_fence_after();
+        const int st = j % ATT_STAGES;
+        const uint32_t v_addr = smem_u32(sV + st * C::TILE_BYTES);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint64_t ad = make_sdesc(p_addr + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, 128);
+          const uint64_t bd = make_sdesc(v_addr + k * 16 * C::SWZ, C::ATOM_BYTES, 8 * C::SWZ, C::SWZ);
+          tc_mma_f16(tmem_o, ad, bd, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+        }
+        tc_commit(o_done);
+        tc_commit(&kv_empty[st]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- softmax / correction / epilogue warps
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const bool q_valid = r < n_q;
+    const int qp = q_valid ? a.qpos[q_row0 + r] : -1;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const float NEG_INF = -INFINITY;
+    float m_run = NEG_INF, l_run = 0.f;
+    uint8_t* prow = sP + r * 128;
+    const int sw = r & 7;
+    for (int j = 0; j < n_kt; ++j) {
+      const int k0 = key_begin + j * 128;
+      float s[128];
+      mbar_wait(s_full, j & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tmem_s + lane_off + c * 32, s + c * 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(s_free);
+      float tmax = NEG_INF;
+      const int lim = min(qp, key_end - 1) - k0;  // columns <= lim are visible
+#pragma unroll
+      for (int i = 0; i < 128; ++i) {
+        s[i] = (i <= lim) ? s[i] * a.scale_log2 : NEG_INF;
+        tmax = fmaxf(tmax, s[i]);
+      }
+      if (j > 0) {
+        mbar_wait(o_done, (j - 1) & 1);
+        tc_fence_after();
+      }
+      const float m_new = fmaxf(m_run, tmax);
+      const bool need = m_new > m_run + 8.0f;  // lazy rescale (true when m_run = -inf)
+      const bool has_o = m_run != NEG_INF;
+      if (__any_sync(0xffffffffu, need && has_o)) {
+        const float sc = (need && has_o) ? exp2f(m_run - m_new) : 1.0f;
+#pragma unroll
+        for (int c = 0; c < HD / 16; ++c) {
+          float o[16];
+          tmem_ld16(tmem_o + lane_off + c * 16, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] *= sc;
+          tmem_st16(tmem_o + lane_off + c * 16, o);
+        }
+        tmem_wait_st();
+      }
+      if (need) {
+        l_run = has_o ? l_run * exp2f(m_run - m_new) : 0.f;
+        m_run = m_new;
+      }
+      const bool any = m_run != NEG_INF;
+      float lsum = 0.f;
+#pragma unroll
+      for (int c16 = 0; c16 < 16; ++c16) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float p0 = any ? exp2f(s[c16 * 8 + 2 * q] - m_run) : 0.f;
+          const float p1 = any ? exp2f(s[c16 * 8 + 2 * q + 1] - m_run) : 0.f;
+          lsum += p0 + p1;
+          pk[q] = pack_bf16(p0, p1);
+        }
+        const int atom = c16 >> 3, ch = (c16 & 7) ^ sw;
+        *reinterpret_cast<uint4*>(prow + atom * 16384 + ch * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      }
+      l_run += lsum;
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    if (n_kt > 0) {
+      mbar_wait(o_done, (n_kt - 1) & 1);
+      tc_fence_after();
+    }
+    if (slot < 0) {
+      const float inv = (l_run > 0.f) ? 1.0f / l_run : 0.f;
+      __nv_bfloat16* orow = q_valid ? reinterpret_cast<__nv_bfloat16*>(a.out) +
+                                          (long)a.rowof[q_row0 + r] * a.ldo + head * HD
+                                    : nullptr;
+#pragma unroll
+      for (int c = 0; c < HD / 16; ++c) {
+        float o[16];
+        if (n_kt > 0) {
+          tmem_ld16(tmem_o + lane_off + c * 16, o);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = 0.f;
+        }
+        if (q_valid) {
+          uint32_t pk[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) pk[q] = pack_bf16(o[2 * q] * inv, o[2 * q + 1] * inv);
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+          dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+      }
+    } else {
+      float* wo = a.ws_o + ((long)slot * 128 + r) * HD;
+#pragma unroll
+      for (int c = 0; c < HD / 16; ++c) {
+        float o[16];
+        if (n_kt > 0) {
+          tmem_ld16(tmem_o + lane_off + c * 16, o);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = 0.f;
+        }
+        if (q_valid) {
+          float4* dst = reinterpret_cast<float4*>(wo + c * 16);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dst[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        }
+      }
+      if (q_valid) {
+        a.ws_ml[((long)slot * 128 + r) * 2] = m_run;
+        a.ws_ml[((long)slot * 128 + r) * 2 + 1] = l_run;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
+// Merge split-KV partials: O = sum_s 2^(m_s-M) O_s / sum_s 2^(m_s-M) l_s.
+template <int HD>
+__global__ void attn_combine_kernel(vlc_attn_args a) {
+  const int* it = a.comb + blockIdx.x * 8;
+  const int q_row0 = it[0], n_q = it[1], head = it[2], slot0 = it[3], ns = it[4];
+  const int r = threadIdx.x;
+  if (r >= n_q) return;
+  float M = -INFINITY;
+  for (int s = 0; s < ns; ++s) M = fmaxf(M, a.ws_ml[((long)(slot0 + s) * 128 + r) * 2]);
+  float L = 0.f;
+  float acc[HD];
+#pragma unroll
+  for (int d = 0; d < HD; ++d) acc[d] = 0.f;
+  for (int s = 0; s < ns; ++s) {
+    const long base = (long)(slot0 + s) * 128 + r;
+    const float m = a.ws_ml[base * 2], l = a.ws_ml[base * 2 + 1];
+    const float w = (m == -INFINITY) ? 0.f : exp2f(m - M);
+    L += w * l;
+    const float4* src = reinterpret_cast<const float4*>(a.ws_o + base * HD);
+#pragma unroll
+    for (int d4 = 0; d4 < HD / 4; ++d4) {
+      const float4 v = src[d4];
+      acc[4 * d4] += w * v.x; acc[4 * d4 + 1] += w * v.y; acc[4 * d4 + 2] += w * v.z; acc[4 * d4 + 3] += w * v.w;
+    }
+  }
+  const float inv = L > 0.f ? 1.0f / L : 0.f;
+  __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(a.out) + (long)a.rowof[q_row0 + r] * a.ldo + head * HD;
+#pragma unroll
+  for (int d = 0; d < HD; d += 2) {
+    *reinterpret_cast<uint32_t*>(orow + d) = pack_bf16(acc[d] * inv, acc[d + 1] * inv);
+  }
+}
+
+template <int HD>
+static cudaError_t launch_attn_hd(const vlc_attn_args& a, cudaStream_t stream) {
+  using C = AttnCfg<HD>;
+  CUtensorMap mq, mk, mv;
+  cudaError_t e = make_tmap_2d(&mq, a.q, a.kv, a.q_rows_cap, (uint64_t)a.kv * 2, C::ATOM_E, 128, C::SWZ);
+  if (e != cudaSuccess) return e;
+  e = make_tmap_3d(&mk, a.kc, a.kv, a.kv_rows_cap, a.layers_cap, (uint64_t)a.kv * 2,
+                   (uint64_t)a.kv * 2 * a.kv_rows_cap, C::ATOM_E, 128, 1, C::SWZ);
+  if (e != cudaSuccess) return e;
+  e = make_tmap_3d(&mv, a.vc, a.kv, a.kv_rows_cap, a.layers_cap, (uint64_t)a.kv * 2,
+                   (uint64_t)a.kv * 2 * a.kv_rows_cap, C::ATOM_E, 128, 1, C::SWZ);
+  if (e != cudaSuccess) return e;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_fwd_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  attn_fwd_tc<HD><<<a.n_items, ATT_THREADS, C::SMEM, stream>>>(mq, mk, mv, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attention(const vlc_attn_args& a, cudaStream_t stream) {
+  if (a.n_items <= 0) return cudaSuccess;
+  switch (a.head_dim) {
+    case 16: return launch_attn_hd<16>(a, stream);
+    case 32: return launch_attn_hd<32>(a, stream);
+    case 64: return launch_attn_hd<64>(a, stream);
+    case 128: return launch_attn_hd<128>(a, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_attn_combine(const vlc_attn_args& a, cudaStream_t stream) {
+  if (a.n_comb <= 0) return cudaSuccess;
+  switch (a.head_dim) {
+    case 16: attn_combine_kernel<16><<<a.n_comb, 128, 0, stream>>>(a); break;
+    case 32: attn_combine_kernel<32><<<a.n_comb, 128, 0, stream>>>(a); break;
+    case 64: attn_combine_kernel<64><<<a.n_comb, 128, 0, stream>>>(a); break;
+    case 128: attn_combine_kernel<128><<<a.n_comb, 128, 0, stream>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace vlc

@@ -1,0 +1,165 @@
+// extern "C" surface of libvlcache.so (see include/vlcache.h): argument checks,
+// status codes, thread-local error text and TMA descriptor construction.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "vlc_internal.h"
+
+namespace vlc {
+
+static thread_local char g_err[512] = "";
+
+static int fail(int code, const char* msg) {
+  std::snprintf(g_err, sizeof(g_err), "%s", msg);
+  return code;
+}
+static int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return VLC_OK;
+  std::snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+  return VLC_ERR_CUDA;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+static CUtensorMapSwizzle swz(int bytes) {
+  return bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+         : bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+         : bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                       : CU_TENSOR_MAP_SWIZZLE_NONE;
+}
+
+cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                         uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer,
+                         int swizzle_bytes) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz(swizzle_bytes), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t make_tmap_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                         uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1,
+                         uint32_t b2, int swizzle_bytes) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  cuuint32_t box[3] = {b0, b1, b2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz(swizzle_bytes), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+}  // namespace vlc
+
+using namespace vlc;
+
+extern "C" {
+
+int vlc_embed_assemble_impl(float*, int, const void*, int, const float*, const int*, int, cudaStream_t);
+int vlc_rmsnorm_impl(const float*, int, const float*, void*, int, int, int, int, const int*, float, cudaStream_t);
+int vlc_kv_relocate_impl(const void*, const void*, int, const int*, int, int, void*, void*, int, const int*,
+                         const int*, int, const float*, const float*, int, cudaStream_t);
+int vlc_store_write_pages_impl(const void*, int, int, int, int, const int*, int, void*, int, cudaStream_t);
+int vlc_patchify_impl(const float*, int, int, void*, int, cudaStream_t);
+
+const char* vlc_last_error(void) { return g_err; }
+int vlc_version(void) { return 100; }
+
+int vlc_embed_assemble(float* x, int ldx, const void* embed_bf16, int d, const float* enc_rows, const int* src,
+                       int rows, cudaStream_t stream) {
+  if (rows < 0 || d <= 0 || ldx < d || !x || !src) return fail(VLC_ERR_INVALID, "embed_assemble: bad args");
+  return cuda_status((cudaError_t)vlc_embed_assemble_impl(x, ldx, embed_bf16, d, enc_rows, src, rows, stream),
+                     "embed_assemble");
+}
+
+int vlc_rmsnorm(const float* x, int ldx, const float* gamma, void* out, int ldo, int out_f32, int rows, int d,
+                const int* row_map, float eps, cudaStream_t stream) {
+  if (rows < 0 || d <= 0 || ldx < d || ldo < d || !x || !gamma || !out)
+    return fail(VLC_ERR_INVALID, "rmsnorm: bad args");
+  return cuda_status(
+      (cudaError_t)vlc_rmsnorm_impl(x, ldx, gamma, out, ldo, out_f32, rows, d, row_map, eps, stream), "rmsnorm");
+}
+
+int vlc_kv_relocate(const void* kpool, const void* vpool, int page_tokens, const int* page_table, int kv,
+                    int head_dim, void* kc, void* vc, int kv_rows_cap, const int* descs, const int* blocks,
+                    int n_blocks, const float* cos_tab, const float* sin_tab, int tab_ld, cudaStream_t stream) {
+  if (n_blocks < 0 || page_tokens <= 0 || head_dim < 16 || head_dim % 16 || kv % head_dim || kv_rows_cap <= 0)
+    return fail(VLC_ERR_UNSUPPORTED, "kv_relocate: head_dim must be a multiple of 16 dividing kv");
+  if (tab_ld != head_dim / 2) return fail(VLC_ERR_INVALID, "kv_relocate: tab_ld must be head_dim/2");
+  return cuda_status((cudaError_t)vlc_kv_relocate_impl(kpool, vpool, page_tokens, page_table, kv, head_dim, kc, vc,
+                                                       kv_rows_cap, descs, blocks, n_blocks, cos_tab, sin_tab,
+                                                       tab_ld, stream),
+                     "kv_relocate");
+}
+
+int vlc_store_write_pages(const void* src, int src_f32, int layers, int tokens, int kv, const int* page_table,
+                          int pages_per_layer, void* pool, int page_tokens, cudaStream_t stream) {
+  if (!src || !pool || !page_table || layers <= 0 || tokens <= 0 || kv <= 0 || page_tokens <= 0)
+    return fail(VLC_ERR_INVALID, "store_write_pages: bad args");
+  return cuda_status((cudaError_t)vlc_store_write_pages_impl(src, src_f32, layers, tokens, kv, page_table,
+                                                             pages_per_layer, pool, page_tokens, stream),
+                     "store_write_pages");
+}
+
+int vlc_gemm_bf16(const void* w, int n_pad, int k_pad, const void* x, int x_rows_cap, int m_tokens,
+                  const vlc_epilogue* epi, int splits, float* ws, size_t ws_bytes, int* counters,
+                  cudaStream_t stream) {
+  if (!w || !x || !epi) return fail(VLC_ERR_INVALID, "gemm: null pointer");
+  if (n_pad % 128 || k_pad % 64 || n_pad <= 0 || k_pad <= 0)
+    return fail(VLC_ERR_UNSUPPORTED, "gemm: n_pad must be a multiple of 128 and k_pad of 64");
+  if (x_rows_cap < 256 || m_tokens > x_rows_cap)
+    return fail(VLC_ERR_INVALID, "gemm: x_rows_cap must be >= 256 and >= m_tokens");
+  if (epi->m_tokens != m_tokens) return fail(VLC_ERR_INVALID, "gemm: epilogue m_tokens mismatch");
+  if (epi->kind == VLC_EPI_QKV_ROPE && (!epi->map2 || !epi->pos || !epi->cos_tab || epi->hd % 2))
+    return fail(VLC_ERR_INVALID, "gemm: QKV_ROPE needs map2/pos/tables");
+  return cuda_status(launch_gemm(w, n_pad, k_pad, x, x_rows_cap, m_tokens, *epi, splits, ws, ws_bytes, counters,
+                                 stream),
+                     "gemm_bf16");
+}
+
+int vlc_attn_mixed(const vlc_attn_args* a, cudaStream_t stream) {
+  if (!a || !a->q || !a->kc || !a->vc || !a->items) return fail(VLC_ERR_INVALID, "attn: null pointer");
+  if (a->head_dim != 16 && a->head_dim != 32 && a->head_dim != 64 && a->head_dim != 128)
+    return fail(VLC_ERR_UNSUPPORTED, "attn: head_dim must be 16/32/64/128");
+  if (a->kv != a->heads * a->head_dim) return fail(VLC_ERR_INVALID, "attn: kv != heads*head_dim");
+  return cuda_status(launch_attention(*a, stream), "attn_mixed");
+}
+
+int vlc_attn_combine(const vlc_attn_args* a, cudaStream_t stream) {
+  if (!a) return fail(VLC_ERR_INVALID, "attn_combine: null");
+  return cuda_status(launch_attn_combine(*a, stream), "attn_combine");
+}
+
+int vlc_patchify(const float* pixels, int side, int patch, void* out, int ldo, cudaStream_t stream) {
+  if (!pixels || !out || patch <= 0 || side % patch || ldo < patch * patch)
+    return fail(VLC_ERR_INVALID, "patchify: bad args");
+  return cuda_status((cudaError_t)vlc_patchify_impl(pixels, side, patch, out, ldo, stream), "patchify");
+}
+
+}  // extern "C"

@@ -1,0 +1,286 @@
+// Weight-streaming tcgen05 GEMM for the recomputed rows of the reuse prefill.
+//
+//   acc[f, j] = sum_k W[f, k] * X[j, k]          (swap-AB: weights on UMMA M)
+//
+// W is the layer weight stored K-major on device ([n_out, k] with k contiguous),
+// X the activations of the c computed tokens ([rows, k], bf16).  A CTA owns a
+// 128-row weight tile and one <=256-token tile; the K range may be split across
+// CTAs (split-K, deterministic "last CTA reduces").  One elected thread issues
+// the TMA loads (warp 0) and another the tcgen05.mma chain into TMEM (warp 1);
+// four epilogue warps read TMEM with tcgen05.ld and apply the fused epilogue:
+//   QKV_ROPE  Q/K rotated at the token's position (engine.py:176-180), K/V scattered
+//             into the request KV cache rows, pre-RoPE K kept for the result
+//   RESID     x += acc (fp32 residual, engine.py:183,185)
+//   SWIGLU    silu(gate) * up -> bf16 (model.py:262-265)
+//   F32       logits (engine.py:187)
+//   BIAS_ADD  encoder patch embedding + bias + positional rows (model.py:316)
+//   QKV_PLAIN encoder projections (model.py:318)
+#include "vlc_internal.h"
+
+namespace vlc {
+
+constexpr int GEMM_THREADS = 192;
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BK = 64;
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g)); }
+
+__device__ __forceinline__ void store_bf16(void* base, long idx, float v) {
+  reinterpret_cast<__nv_bfloat16*>(base)[idx] = __float2bfloat16_rn(v);
+}
+
+// Apply the epilogue for 16 consecutive token columns of one weight row.
+__device__ __forceinline__ void epilogue_chunk(const GemmEpi& e, int f, int j0, const float* v) {
+  const bool row_ok = f < e.n_valid;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int j = j0 + i;
+    const float val = v[i];
+    float partner = 0.f;
+    if (e.kind == EPI_QKV_ROPE || e.kind == EPI_SWIGLU) partner = __shfl_xor_sync(0xffffffffu, val, 1);
+    if (!row_ok || j >= e.m_tokens) continue;
+    switch (e.kind) {
+      case EPI_F32: {
+        const long r = e.map1 ? e.map1[j] : j;
+        reinterpret_cast<float*>(e.out)[r * e.ldo + f] = val;
+        break;
+      }
+      case EPI_RESID: {
+        float* o = reinterpret_cast<float*>(e.out) + (long)j * e.ldo + f;
+        *o = *o + val;
+        break;
+      }
+      case EPI_BF16:
+        store_bf16(e.out, (long)j * e.ldo + f, val);
+        break;
+      case EPI_BIAS_ADD: {
+        const float b = e.bias ? e.bias[f] : 0.f;
+        const float a = e.add ? e.add[(long)j * e.ld_add + f] : 0.f;
+        reinterpret_cast<float*>(e.out)[(long)j * e.ldo + f] = (val + b) + a;
+        break;
+      }
+      case EPI_SWIGLU: {
+        if ((f & 1) == 0) store_bf16(e.out, (long)j * e.ldo + (f >> 1), silu_f(val) * partner);
+        break;
+      }
+      case EPI_QKV_PLAIN: {
+        const int sec = f / e.seg, r = f - sec * e.seg;
+        if (sec == 0) store_bf16(e.out, (long)j * e.ldo + r, val);
+        else if (sec == 1) store_bf16(e.out2, (long)j * e.ld2 + r, val);
+        else store_bf16(e.out3, (long)j * e.ld3 + r, val);
+        break;
+      }
+      case EPI_QKV_ROPE: {
+        const int sec = f / e.seg, r = f - sec * e.seg;
+        if (sec == 2) {  // V: not permuted, not rotated
+          store_bf16(e.out3, (long)e.map2[j] * e.ld3 + r, val);
+          break;
+        }
+        const int half = e.hd >> 1;
+        const int head = r / e.hd, w = r - head * e.hd, t = w >> 1, odd = w & 1;
+        const int feat = head * e.hd + (odd ? t + half : t);
+        const long tab = (long)e.pos[j] * e.tab_ld + t;
+        const float c = e.cos_tab[tab], s = e.sin_tab[tab];
+        const float a = odd ? partner : val, b = odd ? val : partner;
+        const float rot = odd ? (b * c + a * s) : (a * c - b * s);
+        if (sec == 0) {
+          const long qr = e.map1 ? e.map1[j] : j;
+          store_bf16(e.out, qr * e.ldo + feat, rot);
+        } else {
+          if (e.out4) store_bf16(e.out4, (long)j * e.ld4 + feat, val);
+          store_bf16(e.out2, (long)e.map2[j] * e.ld2 + feat, rot);
+        }
+        break;
+      }
+      default:
+        break;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_bf16_tc(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
+                 GemmEpi epi, int k_blocks, int splits, int n_tile, int stages, float* ws,
+                 int* counters) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int a_bytes = GEMM_BM * GEMM_BK * 2;
+  const int b_bytes = n_tile * GEMM_BK * 2;
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + stages * a_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + stages * b_bytes);
+  uint64_t* empty = full + stages;
+  uint64_t* accum_full = empty + stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_full + 1);
+  int* flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int m0 = blockIdx.x * GEMM_BM;
+  const int tok0 = blockIdx.y * n_tile;
+  const int split = blockIdx.z;
+  const int kb0 = (int)((long)k_blocks * split / splits);
+  const int kb1 = (int)((long)k_blocks * (split + 1) / splits);
+  const int nkb = kb1 - kb0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_w);
+    tma_prefetch(&map_x);
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accum_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_expect_tx(&full[stage], a_bytes + b_bytes);
+        tma_load_2d(sa + stage * a_bytes, &map_w, &full[stage], kb * GEMM_BK, m0, pol_w);
+        tma_load_2d(sb + stage * b_bytes, &map_x, &full[stage], kb * GEMM_BK, tok0, pol_x);
+        if (++stage == stages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc_bf16(GEMM_BM, n_tile, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t a_addr = smem_u32(sa + stage * a_bytes);
+        const uint32_t b_addr = smem_u32(sb + stage * b_bytes);
+#pragma unroll
+        for (int k = 0; k < GEMM_BK / 16; ++k) {
+          const uint64_t ad = make_sdesc(a_addr + k * 32, 16, 1024, 128);
+          const uint64_t bd = make_sdesc(b_addr + k * 32, 16, 1024, 128);
+          tc_mma_f16(tmem, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+        }
+        tc_commit(&empty[stage]);
+        if (++stage == stages) { stage = 0; phase ^= 1; }
+      }
+      tc_commit(accum_full);
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue warps 2..5
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;  // TMEM lane == weight row within the tile
+    const int f = m0 + row;
+    const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
+    mbar_wait(accum_full, 0);
+    tc_fence_after();
+    const int nchunks = n_tile / 16;
+    if (splits == 1) {
+      for (int c = 0; c < nchunks; ++c) {
+        float v[16];
+        tmem_ld16(t_lane + c * 16, v);
+        tmem_wait_ld();
+        epilogue_chunk(epi, f, tok0 + c * 16, v);
+      }
+    } else {
+      const long tile = (long)blockIdx.y * gridDim.x + blockIdx.x;
+      float* mine = ws + ((tile * splits + split) * GEMM_BM + row) * (long)n_tile;
+      for (int c = 0; c < nchunks; ++c) {
+        float v[16];
+        tmem_ld16(t_lane + c * 16, v);
+        tmem_wait_ld();
+        float4* dst = reinterpret_cast<float4*>(mine + c * 16);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
+      __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 64) {
+        const int prev = atomicAdd(&counters[tile], 1);
+        *flag = (prev == splits - 1);
+        if (prev == splits - 1) counters[tile] = 0;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (*flag) {
+        __threadfence();
+        const float* base = ws + (tile * splits * GEMM_BM + row) * (long)n_tile;
+        const long sstride = (long)GEMM_BM * n_tile;
+        for (int c = 0; c < nchunks; ++c) {
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          for (int s = 0; s < splits; ++s) {
+            const float4* src = reinterpret_cast<const float4*>(base + s * sstride + c * 16);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 p = __ldcg(src + q);
+              v[4 * q] += p.x; v[4 * q + 1] += p.y; v[4 * q + 2] += p.z; v[4 * q + 3] += p.w;
+            }
+          }
+          epilogue_chunk(epi, f, tok0 + c * 16, v);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
+int gemm_smem_bytes(int n_tile, int stages) {
+  return 1024 + stages * (GEMM_BM * GEMM_BK * 2 + n_tile * GEMM_BK * 2) + (2 * stages + 1) * 8 + 16;
+}
+
+int gemm_pick_stages(int n_tile) {
+  const int per = GEMM_BM * GEMM_BK * 2 + n_tile * GEMM_BK * 2;
+  int s = (200 * 1024) / per;
+  if (s > 8) s = 8;
+  if (s < 2) s = 2;
+  return s;
+}
+
+cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap,
+                        int m_tokens, const GemmEpi& epi, int splits, float* ws, size_t ws_bytes,
+                        int* counters, cudaStream_t stream) {
+  if (m_tokens <= 0) return cudaSuccess;
+  const int k_blocks = k_pad / GEMM_BK;
+  const int m_tiles = n_pad / GEMM_BM;
+  int n_tile = m_tokens >= 256 ? 256 : ((m_tokens + 15) / 16) * 16;
+  if (n_tile < 16) n_tile = 16;
+  const int tok_tiles = (m_tokens + n_tile - 1) / n_tile;
+  if (splits < 1) splits = 1;
+  if (splits > k_blocks) splits = k_blocks;
+  if (splits > 1) {
+    const size_t need = (size_t)m_tiles * tok_tiles * splits * GEMM_BM * n_tile * sizeof(float);
+    if (need > ws_bytes || counters == nullptr) splits = 1;
+  }
+  CUtensorMap mw, mx;
+  cudaError_t err = make_tmap_2d(&mw, W, k_pad, n_pad, (uint64_t)k_pad * 2, GEMM_BK, GEMM_BM, 128);
+  if (err != cudaSuccess) return err;
+  err = make_tmap_2d(&mx, X, k_pad, x_rows_cap, (uint64_t)k_pad * 2, GEMM_BK, n_tile, 128);
+  if (err != cudaSuccess) return err;
+  const int stages = gemm_pick_stages(n_tile);
+  const int smem = gemm_smem_bytes(n_tile, stages);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_bf16_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    attr_set = true;
+  }
+  dim3 grid(m_tiles, tok_tiles, splits);
+  gemm_bf16_tc<<<grid, GEMM_THREADS, smem, stream>>>(mw, mx, epi, k_blocks, splits, n_tile, stages,
+                                                     ws, counters);
+  return cudaGetLastError();
+}
+
+}  // namespace vlc

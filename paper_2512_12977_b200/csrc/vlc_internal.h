@@ -1,0 +1,38 @@
+// Internal declarations shared by the VLCache sm_100a kernels and the C-ABI layer.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/vlcache.h"
+#include "vlc_ptx.cuh"
+
+namespace vlc {
+
+enum EpiKind {
+  EPI_F32 = VLC_EPI_F32,
+  EPI_RESID = VLC_EPI_RESID,
+  EPI_BF16 = VLC_EPI_BF16,
+  EPI_BIAS_ADD = VLC_EPI_BIAS_ADD,
+  EPI_SWIGLU = VLC_EPI_SWIGLU,
+  EPI_QKV_PLAIN = VLC_EPI_QKV_PLAIN,
+  EPI_QKV_ROPE = VLC_EPI_QKV_ROPE,
+};
+
+using GemmEpi = vlc_epilogue;
+
+// tensor maps (driver entry point resolved through the runtime, no -lcuda)
+cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                         uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer,
+                         int swizzle_bytes);
+cudaError_t make_tmap_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                         uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1,
+                         uint32_t b2, int swizzle_bytes);
+
+cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap,
+                        int m_tokens, const GemmEpi& epi, int splits, float* ws, size_t ws_bytes,
+                        int* counters, cudaStream_t stream);
+
+cudaError_t launch_attention(const vlc_attn_args& a, cudaStream_t stream);
+cudaError_t launch_attn_combine(const vlc_attn_args& a, cudaStream_t stream);
+
+}  // namespace vlc

@@ -1,0 +1,249 @@
+// Bandwidth kernels of the reuse prefill: embedding assembly, RMSNorm, the
+// fused KV gather + RoPE re-rotation + scatter (kv_relocate), store page writes
+// and image patchify.
+#include "vlc_internal.h"
+
+namespace vlc {
+
+// ------------------------------------------------------------------ embed (K1)
+__global__ void embed_assemble_kernel(float* __restrict__ x, int ldx,
+                                      const __nv_bfloat16* __restrict__ embed, int d,
+                                      const float* __restrict__ enc_rows,
+                                      const int* __restrict__ src, int rows) {
+  const int r = blockIdx.x;
+  if (r >= rows) return;
+  const int s = src[r];
+  float* dst = x + (long)r * ldx;
+  if (s >= 0) {
+    const __nv_bfloat16* e = embed + (long)s * d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = __bfloat162float(e[i]);
+  } else {
+    const float* e = enc_rows + (long)(-s - 1) * d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = e[i];
+  }
+}
+
+// ------------------------------------------------------------------ rmsnorm (K4)
+template <bool OUT_F32>
+__global__ void rmsnorm_kernel(const float* __restrict__ x, int ldx, const float* __restrict__ g,
+                               void* __restrict__ out, int ldo, int rows, int d,
+                               const int* __restrict__ row_map, float eps) {
+  const int r = blockIdx.x;
+  if (r >= rows) return;
+  const int sr = row_map ? row_map[r] : r;
+  const float* xr = x + (long)sr * ldx;
+  float acc = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) acc += xr[i] * xr[i];
+  __shared__ float red[32];
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float denom = sqrtf(red[0] / (float)d + eps);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float y = (xr[i] / denom) * g[i];
+    if (OUT_F32) reinterpret_cast<float*>(out)[(long)r * ldo + i] = y;
+    else reinterpret_cast<__nv_bfloat16*>(out)[(long)r * ldo + i] = __float2bfloat16_rn(y);
+  }
+}
+
+// ------------------------------------------------------------------ kv_relocate (K2+K3)
+// One block = RELOC_TOK consecutive tokens of one (image, layer) descriptor.
+// K: thread (token, frequency chunk of 8, head group) rotates 8 pairs per head
+// with 128-bit loads of both halves; cos/sin for the token's position are
+// loaded once and reused across every head.  V: straight 128-bit copy.
+constexpr int RELOC_TOK = 8;
+constexpr int RELOC_THREADS = 256;
+
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void rotate8(const uint4& a, const uint4& b, const float* c,
+                                        const float* s, uint4& oa, uint4& ob) {
+  const uint32_t* pa = &a.x;
+  const uint32_t* pb = &b.x;
+  uint32_t* qa = &oa.x;
+  uint32_t* qb = &ob.x;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float a0 = bf16_lo(pa[i]), a1 = bf16_hi(pa[i]);
+    const float b0 = bf16_lo(pb[i]), b1 = bf16_hi(pb[i]);
+    const float c0 = c[2 * i], c1 = c[2 * i + 1], s0 = s[2 * i], s1 = s[2 * i + 1];
+    qa[i] = pack_bf16(a0 * c0 - b0 * s0, a1 * c1 - b1 * s1);
+    qb[i] = pack_bf16(b0 * c0 + a0 * s0, b1 * c1 + a1 * s1);
+  }
+}
+
+__global__ void __launch_bounds__(RELOC_THREADS)
+    kv_relocate_kernel(const __nv_bfloat16* __restrict__ kpool,
+                       const __nv_bfloat16* __restrict__ vpool, int page_tokens,
+                       const int* __restrict__ page_table, int kv, int hd,
+                       __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
+                       int kv_rows_cap, const int* __restrict__ descs,
+                       const int2* __restrict__ blocks, const float* __restrict__ cos_tab,
+                       const float* __restrict__ sin_tab, int tab_ld) {
+  const int2 blk = blocks[blockIdx.x];
+  const int* dsc = descs + blk.x * 8;
+  const int layer = dsc[0], pt_off = dsc[1], tok0 = dsc[2], ntok = dsc[3];
+  const int dst0 = dsc[4], pos0 = dsc[5];
+  const int t_begin = blk.y;
+  const int t_count = min(RELOC_TOK, ntok - t_begin);
+  const int heads = kv / hd;
+  const int fchunks = hd / 16;  // chunks of 8 frequencies
+  const long layer_off = (long)layer * kv_rows_cap;
+
+  // ---- K: rotate pairs (j, j + hd/2) of every head
+  const int group_threads = fchunks * RELOC_TOK;
+  const int n_groups = RELOC_THREADS / group_threads;
+  const int tid = threadIdx.x;
+  if (tid < n_groups * group_threads) {
+    const int fc = tid % fchunks;
+    const int tk = (tid / fchunks) % RELOC_TOK;
+    const int hg = tid / group_threads;
+    if (tk < t_count) {
+      const int t = tok0 + t_begin + tk;  // token index inside the image
+      const long src_row = (long)page_table[pt_off + t / page_tokens] * page_tokens + (t % page_tokens);
+      const long dst_row = layer_off + dst0 + t_begin + tk;
+      const int pos = pos0 + t_begin + tk;
+      float c[8], s[8];
+      const float4* cp = reinterpret_cast<const float4*>(cos_tab + (long)pos * tab_ld + fc * 8);
+      const float4* sp = reinterpret_cast<const float4*>(sin_tab + (long)pos * tab_ld + fc * 8);
+      *reinterpret_cast<float4*>(c) = __ldg(cp);
+      *reinterpret_cast<float4*>(c + 4) = __ldg(cp + 1);
+      *reinterpret_cast<float4*>(s) = __ldg(sp);
+      *reinterpret_cast<float4*>(s + 4) = __ldg(sp + 1);
+      const __nv_bfloat16* srow = kpool + src_row * kv;
+      __nv_bfloat16* drow = kc + dst_row * kv;
+      const int half = hd >> 1;
+#pragma unroll 4
+      for (int h = hg; h < heads; h += n_groups) {
+        const int ea = h * hd + fc * 8;
+        const uint4 a = ldg_stream(reinterpret_cast<const uint4*>(srow + ea));
+        const uint4 b = ldg_stream(reinterpret_cast<const uint4*>(srow + ea + half));
+        uint4 oa, ob;
+        rotate8(a, b, c, s, oa, ob);
+        *reinterpret_cast<uint4*>(drow + ea) = oa;
+        *reinterpret_cast<uint4*>(drow + ea + half) = ob;
+      }
+    }
+  }
+  // ---- V: 128-bit copy
+  const int vec_per_row = kv / 8;
+  const int total = t_count * vec_per_row;
+#pragma unroll 4
+  for (int i = tid; i < total; i += RELOC_THREADS) {
+    const int tk = i / vec_per_row, vi = i - tk * vec_per_row;
+    const int t = tok0 + t_begin + tk;
+    const long src_row = (long)page_table[pt_off + t / page_tokens] * page_tokens + (t % page_tokens);
+    const long dst_row = layer_off + dst0 + t_begin + tk;
+    const uint4 v = ldg_stream(reinterpret_cast<const uint4*>(vpool + src_row * kv) + vi);
+    reinterpret_cast<uint4*>(vc + dst_row * kv)[vi] = v;
+  }
+}
+
+// ------------------------------------------------------------------ store pages
+template <bool SRC_F32>
+__global__ void store_pages_kernel(const void* __restrict__ src, int layers, int tokens, int kv,
+                                   const int* __restrict__ page_table, int pages_per_layer,
+                                   __nv_bfloat16* __restrict__ pool, int page_tokens) {
+  const long row = blockIdx.x;  // layer * tokens + t
+  const int layer = (int)(row / tokens), t = (int)(row % tokens);
+  const long dst = (long)page_table[layer * pages_per_layer + t / page_tokens] * page_tokens + t % page_tokens;
+  __nv_bfloat16* d = pool + dst * kv;
+  if (SRC_F32) {
+    const float* s = reinterpret_cast<const float*>(src) + row * kv;
+    for (int i = threadIdx.x; i < kv; i += blockDim.x) d[i] = __float2bfloat16_rn(s[i]);
+  } else {
+    const __nv_bfloat16* s = reinterpret_cast<const __nv_bfloat16*>(src) + row * kv;
+    for (int i = threadIdx.x; i < kv; i += blockDim.x) d[i] = s[i];
+  }
+}
+
+// ------------------------------------------------------------------ patchify
+__global__ void patchify_kernel(const float* __restrict__ px, int side, int p,
+                                __nv_bfloat16* __restrict__ out, int ldo) {
+  const int t = blockIdx.x;  // patch index, row-major over the patch grid
+  const int per_row = side / p;
+  const int ty = t / per_row, tx = t % per_row;
+  for (int e = threadIdx.x; e < ldo; e += blockDim.x) {
+    float v = 0.f;
+    if (e < p * p) {
+      const int py = e / p, pxx = e % p;
+      v = px[(long)(ty * p + py) * side + tx * p + pxx];
+    }
+    out[(long)t * ldo + e] = __float2bfloat16_rn(v);
+  }
+}
+
+}  // namespace vlc
+
+using namespace vlc;
+
+extern "C" {
+
+int vlc_embed_assemble_impl(float* x, int ldx, const void* embed_bf16, int d, const float* enc_rows,
+                            const int* src, int rows, cudaStream_t stream) {
+  if (rows <= 0) return 0;
+  embed_assemble_kernel<<<rows, 256, 0, stream>>>(x, ldx, reinterpret_cast<const __nv_bfloat16*>(embed_bf16),
+                                                  d, enc_rows, src, rows);
+  return (int)cudaGetLastError();
+}
+
+int vlc_rmsnorm_impl(const float* x, int ldx, const float* gamma, void* out, int ldo, int out_f32,
+                     int rows, int d, const int* row_map, float eps, cudaStream_t stream) {
+  if (rows <= 0) return 0;
+  if (out_f32)
+    rmsnorm_kernel<true><<<rows, 256, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps);
+  else
+    rmsnorm_kernel<false><<<rows, 256, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps);
+  return (int)cudaGetLastError();
+}
+
+int vlc_kv_relocate_impl(const void* kpool, const void* vpool, int page_tokens, const int* page_table,
+                         int kv, int head_dim, void* kc, void* vc, int kv_rows_cap, const int* descs,
+                         const int* blocks, int n_blocks, const float* cos_tab, const float* sin_tab,
+                         int tab_ld, cudaStream_t stream) {
+  if (n_blocks <= 0) return 0;
+  kv_relocate_kernel<<<n_blocks, RELOC_THREADS, 0, stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(kpool), reinterpret_cast<const __nv_bfloat16*>(vpool),
+      page_tokens, page_table, kv, head_dim, reinterpret_cast<__nv_bfloat16*>(kc),
+      reinterpret_cast<__nv_bfloat16*>(vc), kv_rows_cap, descs, reinterpret_cast<const int2*>(blocks),
+      cos_tab, sin_tab, tab_ld);
+  return (int)cudaGetLastError();
+}
+
+int vlc_store_write_pages_impl(const void* src, int src_f32, int layers, int tokens, int kv,
+                               const int* page_table, int pages_per_layer, void* pool, int page_tokens,
+                               cudaStream_t stream) {
+  const long rows = (long)layers * tokens;
+  if (rows <= 0) return 0;
+  if (src_f32)
+    store_pages_kernel<true><<<(unsigned)rows, 256, 0, stream>>>(src, layers, tokens, kv, page_table,
+                                                                 pages_per_layer,
+                                                                 reinterpret_cast<__nv_bfloat16*>(pool),
+                                                                 page_tokens);
+  else
+    store_pages_kernel<false><<<(unsigned)rows, 256, 0, stream>>>(src, layers, tokens, kv, page_table,
+                                                                  pages_per_layer,
+                                                                  reinterpret_cast<__nv_bfloat16*>(pool),
+                                                                  page_tokens);
+  return (int)cudaGetLastError();
+}
+
+int vlc_patchify_impl(const float* pixels, int side, int patch, void* out, int ldo, cudaStream_t stream) {
+  const int T = (side / patch) * (side / patch);
+  patchify_kernel<<<T, 64, 0, stream>>>(pixels, side, patch, reinterpret_cast<__nv_bfloat16*>(out), ldo);
+  return (int)cudaGetLastError();
+}
+
+}  // extern "C"

@@ -1,0 +1,231 @@
+"""Kernel-level numerics of libvlcache against plain PyTorch fp32 references.
+
+Every op is checked through the C ABI (ctypes), on the same bf16 inputs the
+kernel sees, so the only differences are accumulation order and output rounding.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nat(cuda_ok):
+    from paper_2512_12977_b200 import _native
+    _native.load()
+    return _native
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _epi(nat, **kw):
+    e = nat.Epilogue()
+    for k, v in kw.items():
+        setattr(e, k, v)
+    return e
+
+
+def _gemm(nat, W, X, m, epi, splits=1):
+    ws = torch.zeros(64 << 20, dtype=torch.uint8, device="cuda")
+    cnt = torch.zeros(4096, dtype=torch.int32, device="cuda")
+    nat.check(nat.load().vlc_gemm_bf16(W.data_ptr(), W.shape[0], W.shape[1], X.data_ptr(), X.shape[0], m,
+                                       epi, splits, ws.data_ptr(), ws.numel(), cnt.data_ptr(), _stream()),
+              "gemm")
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("n_pad,k_pad,m,splits", [(128, 64, 16, 1), (256, 128, 40, 1), (384, 512, 100, 3),
+                                                  (256, 256, 300, 2), (128, 1024, 256, 4), (512, 192, 1000, 1)])
+def test_gemm_f32_matches_torch(nat, n_pad, k_pad, m, splits):
+    g = torch.Generator(device="cuda").manual_seed(n_pad + m)
+    W = torch.randn(n_pad, k_pad, device="cuda", generator=g).bfloat16()
+    X = torch.randn(max(256, m), k_pad, device="cuda", generator=g).bfloat16()
+    out = torch.full((m, n_pad), float("nan"), device="cuda")
+    epi = _epi(nat, kind=nat.EPI_F32, n_valid=n_pad, m_tokens=m, out=out.data_ptr(), ldo=n_pad)
+    _gemm(nat, W, X, m, epi, splits)
+    ref = X[:m].float() @ W.float().t()
+    err = (out - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-5, err
+
+
+def test_gemm_resid_and_swiglu(nat):
+    g = torch.Generator(device="cuda").manual_seed(1)
+    n, k, m = 256, 128, 50
+    W = torch.randn(n, k, device="cuda", generator=g).bfloat16()
+    X = torch.randn(256, k, device="cuda", generator=g).bfloat16()
+    x = torch.randn(m, n, device="cuda", generator=g)
+    x0 = x.clone()
+    _gemm(nat, W, X, m, _epi(nat, kind=nat.EPI_RESID, n_valid=n, m_tokens=m, out=x.data_ptr(), ldo=n), 2)
+    acc = X[:m].float() @ W.float().t()
+    assert torch.allclose(x, x0 + acc, atol=1e-4, rtol=1e-5)
+    h = torch.zeros(m, n // 2, device="cuda", dtype=torch.bfloat16)
+    _gemm(nat, W, X, m, _epi(nat, kind=nat.EPI_SWIGLU, n_valid=n, m_tokens=m, out=h.data_ptr(), ldo=n // 2))
+    gate, up = acc[:, 0::2], acc[:, 1::2]
+    ref = gate / (1 + torch.exp(-gate)) * up
+    assert (h.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item()
+
+
+def _rope_ref(x, pos, hd, base=10000.0):
+    half = hd // 2
+    inv = base ** (-torch.arange(half, dtype=torch.float32) * (2.0 / hd))
+    ang = pos.float().cpu()[:, None] * inv[None]
+    c, s = torch.cos(ang).cuda(), torch.sin(ang).cuda()
+    n = x.shape[0]
+    xh = x.reshape(n, -1, hd)
+    a, b = xh[..., :half], xh[..., half:]
+    return torch.cat([a * c[:, None] - b * s[:, None], b * c[:, None] + a * s[:, None]], -1).reshape(n, -1)
+
+
+def _tables(hd, npos, base=10000.0):
+    half = hd // 2
+    inv = (base ** (-np.arange(half, dtype=np.float32) * (2.0 / hd))).astype(np.float32)
+    ang = np.arange(npos, dtype=np.float32)[:, None] * inv
+    return (torch.from_numpy(np.cos(ang, dtype=np.float32)).cuda(),
+            torch.from_numpy(np.sin(ang, dtype=np.float32)).cuda())
+
+
+def _perm_rows(kv, hd):
+    """device row order for rope pairing: within a head, rows (t, t+hd/2) adjacent."""
+    idx = []
+    for h in range(kv // hd):
+        for t in range(hd // 2):
+            idx += [h * hd + t, h * hd + t + hd // 2]
+    return torch.tensor(idx)
+
+
+@pytest.mark.parametrize("hd,heads", [(128, 3), (32, 8), (16, 2)])
+def test_gemm_qkv_rope_epilogue(nat, hd, heads):
+    kv = hd * heads
+    d, m = 128, 37
+    g = torch.Generator(device="cuda").manual_seed(hd)
+    Wq, Wk, Wv = (torch.randn(kv, d, device="cuda", generator=g).bfloat16() for _ in range(3))
+    perm = _perm_rows(kv, hd).cuda()
+    n_pad = ((3 * kv + 127) // 128) * 128
+    W = torch.zeros(n_pad, d, device="cuda", dtype=torch.bfloat16)
+    W[:kv], W[kv:2 * kv], W[2 * kv:3 * kv] = Wq[perm], Wk[perm], Wv
+    X = torch.randn(256, d, device="cuda", generator=g).bfloat16()
+    pos = torch.randint(0, 500, (m,), device="cuda", generator=g, dtype=torch.int32)
+    qmap = torch.randperm(m, device="cuda", generator=g).int()
+    kvmap = (pos + 3).int()
+    cos, sin = _tables(hd, 600)
+    q = torch.zeros(m, kv, device="cuda", dtype=torch.bfloat16)
+    kc = torch.zeros(600, kv, device="cuda", dtype=torch.bfloat16)
+    vc = torch.zeros_like(kc)
+    kpre = torch.zeros(m, kv, device="cuda", dtype=torch.bfloat16)
+    epi = _epi(nat, kind=nat.EPI_QKV_ROPE, n_valid=3 * kv, m_tokens=m, out=q.data_ptr(), ldo=kv,
+               out2=kc.data_ptr(), ld2=kv, out3=vc.data_ptr(), ld3=kv, out4=kpre.data_ptr(), ld4=kv,
+               map1=qmap.data_ptr(), map2=kvmap.data_ptr(), pos=pos.data_ptr(), cos_tab=cos.data_ptr(),
+               sin_tab=sin.data_ptr(), tab_ld=hd // 2, hd=hd, seg=kv)
+    _gemm(nat, W, X, m, epi, 2)
+    Xf = X[:m].float()
+    qr = _rope_ref(Xf @ Wq.float().t(), pos, hd)
+    kr = _rope_ref(Xf @ Wk.float().t(), pos, hd)
+    v = Xf @ Wv.float().t()
+    tol = lambda r: 1e-2 * r.abs().max().item()
+    assert (q[qmap.long()].float() - qr).abs().max().item() < tol(qr)
+    assert (kc[kvmap.long()].float() - kr).abs().max().item() < tol(kr)
+    assert (vc[kvmap.long()].float() - v).abs().max().item() < tol(v)
+    assert (kpre.float() - Xf @ Wk.float().t()).abs().max().item() < tol(v)
+
+
+def _attn_ref(q, k, v, qpos, heads, hd, nkeys):
+    nq = q.shape[0]
+    qh = q.float().reshape(nq, heads, hd).transpose(0, 1)
+    kh = k.float()[:nkeys].reshape(nkeys, heads, hd).transpose(0, 1)
+    vh = v.float()[:nkeys].reshape(nkeys, heads, hd).transpose(0, 1)
+    s = qh @ kh.transpose(1, 2) / math.sqrt(hd)
+    vis = torch.arange(nkeys, device=q.device)[None, :] <= qpos.long()[:, None]
+    s = s.masked_fill(~vis[None], float("-inf"))
+    return (torch.softmax(s, -1) @ vh).transpose(0, 1).reshape(nq, -1)
+
+
+@pytest.mark.parametrize("hd,heads,nkeys,nq,split", [(128, 2, 1000, 150, 3), (128, 4, 300, 60, 1),
+                                                      (64, 2, 513, 200, 2), (32, 8, 288, 44, 1),
+                                                      (16, 2, 26, 10, 1), (128, 1, 4128, 236, 6)])
+def test_attention_matches_torch(nat, hd, heads, nkeys, nq, split):
+    kv = heads * hd
+    g = torch.Generator(device="cuda").manual_seed(nkeys)
+    layers, layer, kv_rows = 3, 1, nkeys + 64
+    kc = torch.randn(layers, kv_rows, kv, device="cuda", generator=g).bfloat16()
+    vc = torch.randn(layers, kv_rows, kv, device="cuda", generator=g).bfloat16()
+    qpos = torch.sort(torch.randperm(nkeys, device="cuda", generator=g)[:nq]).values.int()
+    qpos[-1] = nkeys - 1
+    q = torch.zeros(max(256, nq + 128), kv, device="cuda", dtype=torch.bfloat16)
+    q[:nq] = torch.randn(nq, kv, device="cuda", generator=g).bfloat16()
+    rowof = torch.randperm(nq, device="cuda", generator=g).int()
+    out = torch.zeros(nq, kv, device="cuda", dtype=torch.bfloat16)
+    items, comb, slot = [], [], 0
+    for h in range(heads):
+        for q0 in range(0, nq, 128):
+            n_q = min(128, nq - q0)
+            kend = int(qpos[q0 + n_q - 1]) + 1
+            ntile = (kend + 127) // 128
+            ns = min(split, ntile)
+            if ns == 1:
+                items.append([q0, n_q, h, 0, 0, kend, -1, 0])
+                continue
+            bounds = [round(ntile * i / ns) * 128 for i in range(ns + 1)]
+            bounds[-1] = kend
+            for s in range(ns):
+                items.append([q0, n_q, h, 0, bounds[s], bounds[s + 1], slot + s, 0])
+            comb.append([q0, n_q, h, slot, ns, 0, 0, 0])
+            slot += ns
+    it = torch.tensor(items, dtype=torch.int32, device="cuda")
+    cb = torch.tensor(comb or [[0] * 8], dtype=torch.int32, device="cuda")
+    ws_o = torch.zeros(max(slot, 1) * 128 * hd, device="cuda")
+    ws_ml = torch.zeros(max(slot, 1) * 256, device="cuda")
+    a = nat.AttnArgs(q=q.data_ptr(), q_rows_cap=q.shape[0], kc=kc.data_ptr(), vc=vc.data_ptr(),
+                     layers_cap=layers, kv_rows_cap=kv_rows, layer=layer, kv=kv, heads=heads, head_dim=hd,
+                     items=it.data_ptr(), n_items=len(items), qpos=qpos.data_ptr(), rowof=rowof.data_ptr(),
+                     out=out.data_ptr(), ldo=kv, ws_o=ws_o.data_ptr(), ws_ml=ws_ml.data_ptr(), ws_slots=slot,
+                     comb=cb.data_ptr(), n_comb=len(comb), scale_log2=math.log2(math.e) / math.sqrt(hd))
+    nat.check(nat.load().vlc_attn_mixed(a, _stream()), "attn")
+    nat.check(nat.load().vlc_attn_combine(a, _stream()), "comb")
+    torch.cuda.synchronize()
+    ref = _attn_ref(q[:nq], kc[layer], vc[layer], qpos, heads, hd, nkeys)
+    got = out[rowof.long()].float()
+    err = (got - ref).abs().max().item()
+    assert err < 2e-2, err
+
+
+def test_kv_relocate_matches_torch(nat):
+    g = torch.Generator(device="cuda").manual_seed(5)
+    L, T, kv, hd, P = 3, 100, 256, 128, 16
+    ppl = (T + P - 1) // P
+    npages = L * ppl + 5
+    kpool = torch.randn(npages * P, kv, device="cuda", generator=g).bfloat16()
+    vpool = torch.randn(npages * P, kv, device="cuda", generator=g).bfloat16()
+    ptab = torch.randperm(npages, device="cuda", generator=g)[:L * ppl].int()
+    kv_rows = 400
+    kc = torch.zeros(L, kv_rows, kv, device="cuda", dtype=torch.bfloat16)
+    vc = torch.zeros_like(kc)
+    cos, sin = _tables(hd, 1000)
+    start = 37
+    descs, blocks = [], []
+    keeps = [10, 5, 0]
+    for layer in range(L):
+        d = [layer, layer * ppl, keeps[layer], T - keeps[layer], start + keeps[layer], start + keeps[layer], 0, 0]
+        for off in range(0, d[3], 8):
+            blocks.append([len(descs), off])
+        descs.append(d)
+    dd = torch.tensor(descs, dtype=torch.int32, device="cuda")
+    bb = torch.tensor(blocks, dtype=torch.int32, device="cuda")
+    nat.check(nat.load().vlc_kv_relocate(kpool.data_ptr(), vpool.data_ptr(), P, ptab.data_ptr(), kv, hd,
+                                         kc.data_ptr(), vc.data_ptr(), kv_rows, dd.data_ptr(), bb.data_ptr(),
+                                         len(blocks), cos.data_ptr(), sin.data_ptr(), hd // 2, _stream()),
+              "relocate")
+    torch.cuda.synchronize()
+    for layer in range(L):
+        t = torch.arange(keeps[layer], T, device="cuda")
+        rows = ptab[layer * ppl + t // P].long() * P + t % P
+        pos = start + t
+        ref_k = _rope_ref(kpool[rows].float(), pos, hd)
+        assert (kc[layer, pos].float() - ref_k).abs().max().item() < 2e-2
+        assert torch.equal(vc[layer, pos], vpool[rows])
+        assert kc[layer, :start + keeps[layer]].abs().sum().item() == 0
