@@ -83,10 +83,12 @@ typedef struct vlc_attn_args {
 const char* vlc_last_error(void);
 int vlc_version(void);
 
-/* Layer-0 hidden rows of the computed set (model.py:339-359, engine.py:167):
- * src[r] >= 0: text token id -> bf16 embed row; src[r] < 0: fp32 encoder row (-src-1). */
-int vlc_embed_assemble(float* x, int ldx, const void* embed_bf16, int d, const float* enc_rows,
-                       const int* src, int rows, cudaStream_t stream);
+/* Layer-0 hidden rows of the computed set (model.py:339-359, engine.py:167).
+ * src int32[rows][2] = {kind, index}: kind 0 -> bf16 embed row `index` (text token id),
+ * kind 1 -> fp32 row `index` of enc_a (encoder-cache pool), kind 2 -> row of enc_b
+ * (freshly encoded images of a cache miss). */
+int vlc_embed_assemble(float* x, int ldx, const void* embed_bf16, int d, const float* enc_a,
+                       const float* enc_b, const int* src, int rows, cudaStream_t stream);
 
 /* RMSNorm eps (model.py:257-259) of rows (optionally gathered via row_map) -> bf16 or f32. */
 int vlc_rmsnorm(const float* x, int ldx, const float* gamma, void* out, int ldo, int out_f32,

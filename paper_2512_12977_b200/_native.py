@@ -58,7 +58,7 @@ def load():
         vp, i, f = C.c_void_p, C.c_int, C.c_float
         lib.vlc_last_error.restype = C.c_char_p
         lib.vlc_version.restype = i
-        lib.vlc_embed_assemble.argtypes = [vp, i, vp, i, vp, vp, i, vp]
+        lib.vlc_embed_assemble.argtypes = [vp, i, vp, i, vp, vp, vp, i, vp]
         lib.vlc_rmsnorm.argtypes = [vp, i, vp, vp, i, i, i, i, vp, f, vp]
         lib.vlc_kv_relocate.argtypes = [vp, vp, i, vp, i, i, vp, vp, i, vp, vp, i, vp, vp, i, vp]
         lib.vlc_store_write_pages.argtypes = [vp, i, i, i, i, vp, i, vp, i, vp]

@@ -81,7 +81,7 @@ using namespace vlc;
 
 extern "C" {
 
-int vlc_embed_assemble_impl(float*, int, const void*, int, const float*, const int*, int, cudaStream_t);
+int vlc_embed_assemble_impl(float*, int, const void*, int, const float*, const float*, const int*, int, cudaStream_t);
 int vlc_rmsnorm_impl(const float*, int, const float*, void*, int, int, int, int, const int*, float, cudaStream_t);
 int vlc_kv_relocate_impl(const void*, const void*, int, const int*, int, int, void*, void*, int, const int*,
                          const int*, int, const float*, const float*, int, cudaStream_t);
@@ -91,10 +91,10 @@ int vlc_patchify_impl(const float*, int, int, void*, int, cudaStream_t);
 const char* vlc_last_error(void) { return g_err; }
 int vlc_version(void) { return 100; }
 
-int vlc_embed_assemble(float* x, int ldx, const void* embed_bf16, int d, const float* enc_rows, const int* src,
-                       int rows, cudaStream_t stream) {
+int vlc_embed_assemble(float* x, int ldx, const void* embed_bf16, int d, const float* enc_a, const float* enc_b,
+                       const int* src, int rows, cudaStream_t stream) {
   if (rows < 0 || d <= 0 || ldx < d || !x || !src) return fail(VLC_ERR_INVALID, "embed_assemble: bad args");
-  return cuda_status((cudaError_t)vlc_embed_assemble_impl(x, ldx, embed_bf16, d, enc_rows, src, rows, stream),
+  return cuda_status((cudaError_t)vlc_embed_assemble_impl(x, ldx, embed_bf16, d, enc_a, enc_b, src, rows, stream),
                      "embed_assemble");
 }
 

@@ -8,17 +8,18 @@ namespace vlc {
 // ------------------------------------------------------------------ embed (K1)
 __global__ void embed_assemble_kernel(float* __restrict__ x, int ldx,
                                       const __nv_bfloat16* __restrict__ embed, int d,
-                                      const float* __restrict__ enc_rows,
-                                      const int* __restrict__ src, int rows) {
+                                      const float* __restrict__ enc_a,
+                                      const float* __restrict__ enc_b,
+                                      const int2* __restrict__ src, int rows) {
   const int r = blockIdx.x;
   if (r >= rows) return;
-  const int s = src[r];
+  const int2 s = src[r];
   float* dst = x + (long)r * ldx;
-  if (s >= 0) {
-    const __nv_bfloat16* e = embed + (long)s * d;
+  if (s.x == 0) {
+    const __nv_bfloat16* e = embed + (long)s.y * d;
     for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = __bfloat162float(e[i]);
   } else {
-    const float* e = enc_rows + (long)(-s - 1) * d;
+    const float* e = (s.x == 1 ? enc_a : enc_b) + (long)s.y * d;
     for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = e[i];
   }
 }
@@ -191,11 +192,11 @@ using namespace vlc;
 
 extern "C" {
 
-int vlc_embed_assemble_impl(float* x, int ldx, const void* embed_bf16, int d, const float* enc_rows,
-                            const int* src, int rows, cudaStream_t stream) {
+int vlc_embed_assemble_impl(float* x, int ldx, const void* embed_bf16, int d, const float* enc_a,
+                            const float* enc_b, const int* src, int rows, cudaStream_t stream) {
   if (rows <= 0) return 0;
   embed_assemble_kernel<<<rows, 256, 0, stream>>>(x, ldx, reinterpret_cast<const __nv_bfloat16*>(embed_bf16),
-                                                  d, enc_rows, src, rows);
+                                                  d, enc_a, enc_b, reinterpret_cast<const int2*>(src), rows);
   return (int)cudaGetLastError();
 }
 

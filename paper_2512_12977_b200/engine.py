@@ -1,0 +1,383 @@
+"""Reuse prefill on B200 behind the reference API (reference: engine.py:39-190).
+
+`prefill_with_reuse(model, request, store)` keeps the reference's validation
+order, error types, hit/miss/fallback semantics and result fields.  Compute runs
+on the device: embed assembly, kv_relocate (cached K gathered from the paged
+store, re-rotated to its new positions, V copied), then per layer RMSNorm ->
+fused QKV GEMM (RoPE + KV scatter epilogue) -> mixed attention -> O GEMM +
+residual -> RMSNorm -> gate/up GEMM (SwiGLU epilogue) -> down GEMM + residual,
+then final norm + LM head for the last layer's rows.
+
+Results are device-resident and materialise on access: `logits` and `kv.keys`
+/`kv.values` are numpy like the reference; `device_logits`, `last_logits()` and
+`kv.device_keys()` avoid the host copy.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .config import ModelConfig
+from .exceptions import InputError
+from .layout import SRC_SCRATCH, SRC_STORE, RequestSpec, build_layout
+from .model import KVTensors, ToyVLM
+from .plans import ComputationMask, RecomputePlan, build_masks, layer_keep, mean_ratio, require_valid
+from .sequence import TokenSequence, make_sequence
+from .store import CacheStore, EncoderCacheEntry, ImageHash, KVCacheEntry, hash_image
+
+
+# ---------------------------------------------------------------- analytic work (engine.py:39-85)
+
+@dataclass(frozen=True)
+class FlopsBreakdown:
+    encoder: int
+    attention: int
+    mlp: int
+
+    @property
+    def total(self) -> int:
+        return self.encoder + self.attention + self.mlp
+
+
+def _attn_flops(computed: int, keys: int, cfg: ModelConfig) -> int:
+    d, kv = cfg.model_dim, cfg.kv_dim
+    return 2 * (3 * computed * d * kv + 2 * computed * keys * kv + computed * kv * d)
+
+
+def _mlp_flops(computed: int, cfg: ModelConfig) -> int:
+    return 6 * computed * cfg.model_dim * cfg.mlp_hidden
+
+
+def encoder_flops(cfg: ModelConfig) -> int:
+    t = cfg.tokens_per_image
+    return 2 * t * cfg.patch_size ** 2 * cfg.model_dim + _attn_flops(t, t, cfg) + _mlp_flops(t, cfg)
+
+
+def flops_from_masks(masks: ComputationMask, seq_len: int, cfg: ModelConfig,
+                     images_encoded: int = 0) -> FlopsBreakdown:
+    counts = masks.computed_counts
+    return FlopsBreakdown(images_encoded * encoder_flops(cfg),
+                          sum(_attn_flops(c, seq_len, cfg) for c in counts),
+                          sum(_mlp_flops(c, cfg) for c in counts))
+
+
+def _flops_from_counts(counts, n, cfg, encoded):
+    return FlopsBreakdown(encoded * encoder_flops(cfg), sum(_attn_flops(c, n, cfg) for c in counts),
+                          sum(_mlp_flops(c, cfg) for c in counts))
+
+
+def count_flops(request, plan: RecomputePlan, config: ModelConfig, encoder_cached: bool = True) -> FlopsBreakdown:
+    seq = getattr(request, "seq", request)
+    require_valid(plan)
+    masks = build_masks(plan, seq)
+    return flops_from_masks(masks, len(seq), config, 0 if encoder_cached else len(seq.image_segments))
+
+
+# ---------------------------------------------------------------- request / result types
+
+@dataclass
+class ReuseRequest:
+    seq: TokenSequence
+    image_hashes: list[ImageHash]
+    plan: RecomputePlan
+    images: list | None = None  # pixels, for the cache-miss fallback
+
+
+class ReuseMetrics:
+    """Reference fields (engine.py:100-108); compute_seconds is device time (CUDA events),
+    resolved lazily so the prefill call itself never blocks the host."""
+
+    def __init__(self, mean_ratio: float = 0.0):
+        self.fallback_images = 0
+        self.encoder_misses = 0
+        self.computed_per_layer: list[int] = []
+        self.flops: FlopsBreakdown | None = None
+        self.resolve_seconds = 0.0
+        self.mean_ratio = mean_ratio
+        self._events = None
+        self._compute = None
+
+    @property
+    def compute_seconds(self) -> float:
+        if self._compute is None:
+            if self._events is None:
+                return 0.0
+            self._events[1].synchronize()
+            self._compute = self._events[0].elapsed_time(self._events[1]) / 1e3
+        return self._compute
+
+    @compute_seconds.setter
+    def compute_seconds(self, v: float) -> None:
+        self._compute = v
+
+
+class ReuseResult:
+    """positions (host), logits [len(positions), V] and merged pre-RoPE KV, device-backed."""
+
+    def __init__(self, positions, dev_logits, kv: KVTensors, metrics: ReuseMetrics):
+        self.positions = positions
+        self._dev_logits = dev_logits
+        self._logits = None
+        self.kv = kv
+        self.metrics = metrics
+
+    @property
+    def device_logits(self):
+        return self._dev_logits
+
+    @property
+    def logits(self) -> np.ndarray:
+        if self._logits is None:
+            self._logits = self._dev_logits.cpu().numpy()
+        return self._logits
+
+    def last_logits(self) -> np.ndarray:
+        return self._dev_logits[-1].cpu().numpy()
+
+    def _detach(self):
+        """The runner is about to reuse its workspace: take private copies."""
+        if self._logits is None:
+            self._dev_logits = self._dev_logits.clone()
+        if self.kv._dev is None and self.kv._keys is None:
+            self.kv._device()
+        if self.kv._dev is not None:
+            self.kv._dev = tuple(t.clone() for t in self.kv._dev)
+        self.kv._loader = None
+
+
+# ---------------------------------------------------------------- runner cache
+
+def _runner(model: ToyVLM):
+    from .runtime import Runner
+    r = getattr(model, "_runner", None)
+    if r is None:
+        r = Runner(model.device)
+        model._runner = r
+    return r
+
+
+def encode_image(model: ToyVLM, pixels) -> np.ndarray:
+    """GPU toy ViT (model.py:302-332); returns host fp32 [T, d] like the reference."""
+    _check_pixels(model.config, pixels)
+    return _runner(model).encode([pixels]).cpu().numpy()
+
+
+def encode_images_device(model: ToyVLM, pixels_list):
+    for px in pixels_list:
+        _check_pixels(model.config, px)
+    return _runner(model).encode(pixels_list)
+
+
+def _check_pixels(cfg: ModelConfig, pixels) -> None:
+    px = np.asarray(pixels)
+    if px.ndim != 2:
+        raise InputError(f"expected a 2-d pixel grid, got shape {px.shape}")
+    h, w = px.shape
+    p = cfg.patch_size
+    if h % p or w % p:
+        raise InputError(f"image dims {px.shape} not divisible by patch size {p}")
+    if (h // p) * (w // p) != cfg.tokens_per_image:
+        raise InputError(f"image yields {(h // p) * (w // p)} patches, model expects {cfg.tokens_per_image}")
+    if h != w:
+        raise InputError("the device patchify expects square images")
+
+
+# ---------------------------------------------------------------- the hot path
+
+def _text_tokens(seq: TokenSequence, cfg: ModelConfig):
+    pos, ids = [], []
+    for seg in seq.segments:
+        if seg.kind == "text":
+            for p in range(seg.start, seg.start + seg.length):
+                t = seq.ids[p]
+                if t >= cfg.vocab_size:
+                    raise InputError(f"token id {t} out of vocab")
+                if t >= 0:
+                    pos.append(p)
+                    ids.append(t)
+    return np.array(pos, dtype=np.int64), np.array(ids, dtype=np.int64)
+
+
+def prefill_with_reuse(model: ToyVLM, request: ReuseRequest, store: CacheStore) -> ReuseResult:
+    cfg = model.config
+    seq, plan = request.seq, request.plan
+    require_valid(plan)
+    if plan.num_layers != cfg.num_layers:
+        raise InputError(f"plan has {plan.num_layers} layers, model has {cfg.num_layers}")
+    seq.validate(cfg.tokens_per_image)
+    segs = seq.image_segments
+    if len(request.image_hashes) != len(segs):
+        raise InputError("one hash per image segment required")
+    metrics = ReuseMetrics(mean_ratio=mean_ratio(plan))
+    T, L = cfg.tokens_per_image, cfg.num_layers
+    keep = np.repeat(layer_keep(plan, T)[:, None], len(segs), axis=1).astype(np.int32)
+    runner = _runner(model)
+
+    t0 = time.perf_counter()
+    fp = model.fingerprint
+    enc_src, kv_hit, page_rows, miss_px = [], [], [], []
+    enc_pool = kv_pool = None
+    for m, seg in enumerate(segs):                               # engine.py:140-159
+        h = request.image_hashes[m]
+        enc = store.get_encoder(h, expected_fingerprint=fp)
+        if enc is not None:
+            if enc_pool is not None and enc._pool is not enc_pool:
+                raise InputError("encoder entries of one model must share a pool")
+            enc_pool = enc._pool
+            enc_src.append((SRC_STORE, enc.slot * T))
+        else:
+            metrics.encoder_misses += 1
+            if request.images is None or request.images[m] is None:
+                raise InputError(f"encoder cache miss for image {m} and no pixels supplied")
+            _check_pixels(cfg, request.images[m])
+            enc_src.append((SRC_SCRATCH, len(miss_px) * T))
+            miss_px.append(request.images[m])
+        entry = store.get_kv(h, expected_fingerprint=fp)
+        if entry is not None:
+            if entry.tokens != T or entry.layers != L:
+                raise InputError("cached KV shape does not match the model")
+            kv_pool = entry.pool
+            kv_hit.append(bool(keep[0, m] < T))
+            page_rows.append(entry.pages)
+        else:
+            kv_hit.append(False)
+            page_rows.append(None)
+            if (keep[:, m] < T).any():                            # reuse requested, nothing to reuse
+                metrics.fallback_images += 1
+                keep[:, m] = T
+    text_pos, text_ids = _text_tokens(seq, cfg)
+    counts = [len(text_pos) + int(keep[i].sum()) for i in range(L)]
+    metrics.computed_per_layer = counts
+    metrics.flops = _flops_from_counts(counts, len(seq), cfg, metrics.encoder_misses)
+    scratch = runner.encode(miss_px) if miss_px else None
+    metrics.resolve_seconds = time.perf_counter() - t0
+
+    spec = RequestSpec(n=len(seq), text_pos=text_pos, text_ids=text_ids,
+                       images=[(s.start, s.length) for s in segs], keep=keep, kv_hit=kv_hit,
+                       enc_src=enc_src, page_rows=page_rows)
+    lay = build_layout([spec], L, cfg.num_heads)
+    import torch
+    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    out = runner.prefill(lay, text_ids, enc_pool.rows.view(-1, cfg.model_dim) if enc_pool else None,
+                         scratch, kv_pool, events=ev)
+    metrics._events = ev
+    start, cnt = lay.logit_ranges[0]
+    dev_logits = out["logits"][start:start + cnt]
+    kv = KVTensors(loader=_merged_kv_loader(out, lay, spec, kv_pool, cfg))
+    res = ReuseResult(lay.positions[0], dev_logits, kv, metrics)
+    runner.ws.live.add(res)
+    return res
+
+
+def _merged_kv_loader(out, lay, spec: RequestSpec, kv_pool, cfg: ModelConfig, req: int = 0):
+    """Merged pre-RoPE KV [L, n, kv] of one request: computed rows from the QKV epilogue's
+    pre-RoPE copy, reused rows from the store pages (engine.py:153-155, 177-178)."""
+    L, n = cfg.num_layers, spec.n
+    kvoff = int(lay.kvoff[req])
+    sel = np.flatnonzero(lay.row_req == req)
+    pos = lay.row_pos[sel].astype(np.int64)
+    kpre_idx, kpre_dst, pool_idx, pool_dst = [], [], [], []
+    R = out["R"]
+    for i in range(L):
+        live = sel < lay.c[i]
+        kpre_idx.append(i * R + sel[live])
+        kpre_dst.append(i * n + pos[live])
+        for m, (start, T) in enumerate(spec.images):
+            if not spec.kv_hit[m]:
+                continue
+            t = np.arange(int(spec.keep[i, m]), T)
+            if not len(t):
+                continue
+            pages = spec.page_rows[m]
+            pool_idx.append(pages[i, t // kv_pool.P].astype(np.int64) * kv_pool.P + t % kv_pool.P)
+            pool_dst.append(i * n + start + t)
+    kpre, vc = out["kpre"], out["vc"]
+
+    def load():
+        import torch
+        kvd = cfg.kv_dim
+        K = torch.zeros(L * n, kvd, dtype=torch.bfloat16, device="cuda")
+        src = kpre.view(-1, kvd)
+        a = torch.from_numpy(np.concatenate(kpre_idx)).cuda()
+        b = torch.from_numpy(np.concatenate(kpre_dst)).cuda()
+        K[b] = src[a]
+        if pool_idx:
+            a = torch.from_numpy(np.concatenate(pool_idx)).cuda()
+            b = torch.from_numpy(np.concatenate(pool_dst)).cuda()
+            K[b] = kv_pool.k[a]
+        V = vc[:, kvoff:kvoff + n].clone()
+        return K.view(L, n, kvd), V
+    return load
+
+
+def prefill_full(model: ToyVLM, seq: TokenSequence, image_embeds) -> tuple[np.ndarray, KVTensors]:
+    """Dense causal prefill (model.py:362-389) on device: plan = 1.0 through the same kernels."""
+    res = _prefill_embeds(model, seq, image_embeds)
+    return res.logits, res.kv
+
+
+def _prefill_embeds(model: ToyVLM, seq: TokenSequence, image_embeds) -> ReuseResult:
+    """Full prefill with explicit image embeddings (host numpy or device rows)."""
+    import torch
+    cfg = model.config
+    seq.validate(cfg.tokens_per_image)
+    segs = seq.image_segments
+    if len(segs) != len(image_embeds):
+        raise InputError(f"sequence has {len(segs)} image segments but {len(image_embeds)} embedding blocks "
+                         "were supplied")
+    T, L, d = cfg.tokens_per_image, cfg.num_layers, cfg.model_dim
+    runner = _runner(model)
+    if segs:
+        blocks = []
+        for e in image_embeds:
+            t = e if isinstance(e, torch.Tensor) else torch.from_numpy(np.asarray(e, dtype=np.float32))
+            if tuple(t.shape) != (T, d):
+                raise InputError(f"embedding block shape {tuple(t.shape)} does not match model")
+            blocks.append(t.to(device="cuda", dtype=torch.float32))
+        scratch = torch.cat(blocks).contiguous()
+    else:
+        scratch = None
+    text_pos, text_ids = _text_tokens(seq, cfg)
+    keep = np.full((L, len(segs)), T, dtype=np.int32)
+    spec = RequestSpec(n=len(seq), text_pos=text_pos, text_ids=text_ids,
+                       images=[(s.start, s.length) for s in segs], keep=keep, kv_hit=[False] * len(segs),
+                       enc_src=[(SRC_SCRATCH, m * T) for m in range(len(segs))], page_rows=[None] * len(segs))
+    lay = build_layout([spec], L, cfg.num_heads)
+    metrics = ReuseMetrics(mean_ratio=1.0)
+    metrics.computed_per_layer = [len(seq)] * L
+    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    out = runner.prefill(lay, text_ids, None, scratch, None, events=ev)
+    metrics._events = ev
+    start, cnt = lay.logit_ranges[0]
+    res = ReuseResult(lay.positions[0], out["logits"][start:start + cnt],
+                      KVTensors(loader=_merged_kv_loader(out, lay, spec, None, cfg)), metrics)
+    res._scratch = scratch
+    runner.ws.live.add(res)
+    return res
+
+
+# ---------------------------------------------------------------- cache-miss fill (bench.py:82-104)
+
+def fill_store_request(model: ToyVLM, store: CacheStore, seq: TokenSequence, images) -> list:
+    """One full device prefill of the request, then one encoder entry and one per-layer
+    pre-RoPE KV slice per image written into the store (device to device)."""
+    embeds = encode_images_device(model, images) if images else None
+    T = model.config.tokens_per_image
+    blocks = [embeds[m * T:(m + 1) * T] for m in range(len(images))]
+    res = _prefill_embeds(model, seq, blocks)
+    K, V = res.kv.device_keys(), res.kv.device_values()
+    fp = model.fingerprint
+    for seg, px, emb in zip(seq.image_segments, images, blocks):
+        h = hash_image(px)
+        sl = slice(seg.start, seg.start + seg.length)
+        store.put_encoder(EncoderCacheEntry(h, emb, fp))
+        store.put_kv(KVCacheEntry(h, K[:, sl], V[:, sl], origin_position=seg.start, model_fingerprint=fp))
+    return blocks
+
+
+def fill_store(model: ToyVLM, store: CacheStore, images, prefix) -> None:
+    cfg = model.config
+    for px in images:
+        fill_store_request(model, store, make_sequence(prefix, 1, cfg.tokens_per_image), [px])

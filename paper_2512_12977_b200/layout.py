@@ -1,0 +1,207 @@
+"""Host planning of one reuse-prefill launch (pure numpy; no device needed).
+
+The reference recomputes, at layer i, the rows `flatnonzero(mask[i])` and keeps
+one hidden state per position (engine.py:166-186).  On the device the hidden
+states of the computed tokens are PACKED so that every layer's computed set is a
+PREFIX of one buffer: tokens are ordered by how many layers they survive
+(text: all L; image token t of image m: #{i : keep[i][m] > t}, a prefix of the
+layers because keep is non-increasing), then by (request, position).  Layer i
+then works on rows [0, c_i) -- no gathers or scatters of hidden states between
+layers.  Attention needs queries ordered by position per request (causal
+masking by absolute position, reference `rows[:, None] >= positions[None, :]`),
+so each layer also gets a sorted query order (qdst / qpos / rowof).
+
+Everything here depends only on (sequence layout, plan, which images hit the KV
+cache), so it is cached and reused across requests with the same structure.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+SRC_TEXT, SRC_STORE, SRC_SCRATCH = 0, 1, 2
+
+
+@dataclass
+class RequestSpec:
+    n: int                        # sequence length
+    text_pos: np.ndarray          # positions of text tokens
+    text_ids: np.ndarray          # their ids
+    images: list                  # [(start, T)] per image segment
+    keep: np.ndarray              # int32 [L, n_images] recomputed leading tokens per layer
+    kv_hit: list                  # per image: True if cached KV is reused (relocated)
+    enc_src: list                 # per image: (SRC_STORE|SRC_SCRATCH, row base)
+    page_rows: list = field(default_factory=list)  # per image: int32 [L, ppl] page ids (kv_hit only)
+
+
+@dataclass
+class Layout:
+    L: int
+    heads: int
+    c: np.ndarray                 # int32 [L] computed rows per layer (prefix lengths)
+    kv_rows: int                  # total KV-cache rows (sum of n)
+    kvoff: np.ndarray             # int32 [R] first KV row of each request
+    # per packed row (length c[0])
+    row_req: np.ndarray
+    row_pos: np.ndarray
+    row_kv: np.ndarray
+    row_src: np.ndarray           # int32 [c0, 2] (kind, index)
+    # per layer sorted query order: [L, c0] (only first c[i] meaningful)
+    qdst: np.ndarray
+    qpos: np.ndarray
+    rowof: np.ndarray
+    q_ranges: list                # per layer: list of (req, q0, count)
+    # attention work (per layer) + combine entries
+    attn_items: list              # per layer: int32 [n, 8]
+    comb_items: list              # per layer: int32 [m, 8]
+    attn_slots: int               # max partial slots over layers
+    # relocation
+    reloc_descs: np.ndarray       # int32 [d, 8]
+    reloc_blocks: np.ndarray      # int32 [b, 2]
+    reloc_layer_blocks: np.ndarray  # int32 [L+1] block offsets per layer (descs sorted by layer)
+    reloc_tokens: int             # total relocated token rows (all layers)
+    page_table: np.ndarray        # int32 flat page ids referenced by reloc_descs
+    # outputs
+    final_rows: np.ndarray        # int32 [c_L] packed rows in (req, pos) order
+    positions: list               # per request: int64 positions with logits (reference `rows`)
+    logit_ranges: list            # per request: (start, count) into the logits rows
+
+
+RELOC_TOK = 8
+
+
+def _depths(spec: RequestSpec, L: int):
+    """(positions, depth, src kind, src index) of every token computed at layer 0."""
+    pos = [spec.text_pos.astype(np.int64)]
+    dep = [np.full(len(spec.text_pos), L, dtype=np.int64)]
+    kind = [np.full(len(spec.text_pos), SRC_TEXT, dtype=np.int64)]
+    idx = [spec.text_ids.astype(np.int64)]
+    for m, (start, T) in enumerate(spec.images):
+        k0 = int(spec.keep[0, m])
+        if k0 == 0:
+            continue
+        t = np.arange(k0)
+        d = (spec.keep[:, m][None, :] > t[:, None]).sum(axis=1)
+        pos.append(start + t)
+        dep.append(d)
+        kind.append(np.full(k0, spec.enc_src[m][0], dtype=np.int64))
+        idx.append(spec.enc_src[m][1] + t)
+    return (np.concatenate(pos), np.concatenate(dep), np.concatenate(kind), np.concatenate(idx))
+
+
+def attention_work(q_ranges, qpos, n_req, heads, target_items: int):
+    """Split (request, head, 128-query tile) key ranges into <= target_items CTAs.
+
+    Returns (items int32 [n, 8], comb int32 [m, 8], slots)."""
+    tiles = []
+    for req, q0, cnt in q_ranges:
+        for t0 in range(q0, q0 + cnt, 128):
+            nq = min(128, q0 + cnt - t0)
+            kend = int(qpos[t0 + nq - 1]) + 1
+            kend = min(kend, int(n_req[req]))
+            tiles.append((req, t0, nq, kend))
+    total = sum((kend + 127) // 128 for _, _, _, kend in tiles) * heads
+    chunk = max(2, -(-total // max(1, target_items)))
+    items, comb, slot = [], [], 0
+    for h in range(heads):
+        for req, t0, nq, kend in tiles:
+            nt = (kend + 127) // 128
+            ns = -(-nt // chunk)
+            if ns <= 1:
+                items.append([t0, nq, h, 0, 0, kend, -1, req])
+                continue
+            bounds = [min(kend, (nt * s // ns) * 128) for s in range(ns)] + [kend]
+            for s in range(ns):
+                items.append([t0, nq, h, 0, bounds[s], bounds[s + 1], slot + s, req])
+            comb.append([t0, nq, h, slot, ns, 0, 0, 0])
+            slot += ns
+    it = np.array(items, dtype=np.int32).reshape(-1, 8)
+    cb = np.array(comb, dtype=np.int32).reshape(-1, 8)
+    return it, cb, slot
+
+
+def build_layout(specs: list[RequestSpec], L: int, heads: int, target_items: int = 296) -> Layout:
+    R = len(specs)
+    n_req = np.array([s.n for s in specs], dtype=np.int64)
+    kvoff = np.concatenate([[0], np.cumsum(n_req)[:-1]]).astype(np.int64)
+    P, D, K, I, Q = [], [], [], [], []
+    for r, spec in enumerate(specs):
+        pos, dep, kind, idx = _depths(spec, L)
+        P.append(pos); D.append(dep); K.append(kind); I.append(idx); Q.append(np.full(len(pos), r))
+    pos, dep, kind, idx, req = (np.concatenate(a) for a in (P, D, K, I, Q))
+    order = np.lexsort((pos, req, -dep))            # depth desc, then request, then position
+    pos, dep, kind, idx, req = pos[order], dep[order], kind[order], idx[order], req[order]
+    c0 = len(pos)
+    c = np.array([(dep > i).sum() for i in range(L)], dtype=np.int32)
+    row_kv = kvoff[req] + pos
+
+    qdst = np.zeros((L, c0), dtype=np.int32)
+    qpos = np.zeros((L, c0), dtype=np.int32)
+    rowof = np.zeros((L, c0), dtype=np.int32)
+    q_ranges, attn_items, comb_items = [], [], []
+    slots = 0
+    for i in range(L):
+        ci = int(c[i])
+        srt = np.lexsort((pos[:ci], req[:ci]))       # (req, pos) order of the active prefix
+        qdst[i, srt] = np.arange(ci)
+        qpos[i, :ci] = pos[srt]
+        rowof[i, :ci] = srt
+        rq = req[srt]
+        ranges = []
+        for r in range(R):
+            sel = np.flatnonzero(rq == r)
+            if len(sel):
+                ranges.append((r, int(sel[0]), len(sel)))
+        q_ranges.append(ranges)
+        it, cb, s = attention_work(ranges, qpos[i], n_req, heads, target_items)
+        it[:, 3] = kvoff[it[:, 7]]
+        attn_items.append(it)
+        comb_items.append(cb)
+        slots = max(slots, s)
+
+    # relocation descriptors, grouped by layer
+    descs, blocks, layer_blocks, pages, ntok_total = [], [], [0], [], 0
+    page_base = {}
+    for r, spec in enumerate(specs):
+        for m, (start, T) in enumerate(spec.images):
+            if spec.kv_hit[m]:
+                page_base[(r, m)] = sum(len(p) for p in pages)
+                pages.append(np.asarray(spec.page_rows[m], dtype=np.int32).reshape(-1))
+    for i in range(L):
+        for r, spec in enumerate(specs):
+            for m, (start, T) in enumerate(spec.images):
+                if not spec.kv_hit[m]:
+                    continue
+                k = int(spec.keep[i, m])
+                ntok = T - k
+                if ntok <= 0:
+                    continue
+                ppl = np.asarray(spec.page_rows[m]).shape[1]
+                d = [i, page_base[(r, m)] + i * ppl, k, ntok, int(kvoff[r]) + start + k, start + k, 0, 0]
+                for off in range(0, ntok, RELOC_TOK):
+                    blocks.append([len(descs), off])
+                descs.append(d)
+                ntok_total += ntok
+        layer_blocks.append(len(blocks))
+
+    last = int(c[L - 1])
+    final_rows = rowof[L - 1, :last].copy()
+    positions, logit_ranges = [], []
+    fr_req = req[final_rows]
+    for r in range(R):
+        sel = np.flatnonzero(fr_req == r)
+        positions.append(pos[final_rows[sel]].astype(np.int64))
+        logit_ranges.append((int(sel[0]) if len(sel) else 0, len(sel)))
+
+    src = np.stack([kind, idx], axis=1).astype(np.int32)
+    src[kind == SRC_TEXT, 1] = idx[kind == SRC_TEXT]
+    return Layout(L=L, heads=heads, c=c, kv_rows=int(n_req.sum()), kvoff=kvoff.astype(np.int32),
+                  row_req=req.astype(np.int32), row_pos=pos.astype(np.int32), row_kv=row_kv.astype(np.int32),
+                  row_src=src, qdst=qdst, qpos=qpos, rowof=rowof, q_ranges=q_ranges,
+                  attn_items=attn_items, comb_items=comb_items, attn_slots=slots,
+                  reloc_descs=np.array(descs, dtype=np.int32).reshape(-1, 8),
+                  reloc_blocks=np.array(blocks, dtype=np.int32).reshape(-1, 2),
+                  reloc_layer_blocks=np.array(layer_blocks, dtype=np.int32), reloc_tokens=ntok_total,
+                  page_table=(np.concatenate(pages) if pages else np.zeros(1, np.int32)).astype(np.int32),
+                  final_rows=final_rows, positions=positions, logit_ranges=logit_ranges)

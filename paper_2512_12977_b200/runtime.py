@@ -1,0 +1,280 @@
+"""Device executor of the reuse prefill: workspaces and the per-layer launch chain.
+
+All compute goes through libvlcache (include/vlcache.h); torch only allocates
+HBM, provides the stream and does host<->device copies.
+"""
+from __future__ import annotations
+
+import math
+import weakref
+
+import numpy as np
+
+from . import _native as N
+from .layout import Layout, attention_work
+from .model import RMS_EPS, DeviceWeights
+
+N_SMS = 148
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream() -> int:
+    return _torch().cuda.current_stream().cuda_stream
+
+
+def pick_splits(n_pad: int, k_pad: int, m_tokens: int) -> int:
+    """Split-K factor so a weight-streaming GEMM covers the 148 SMs."""
+    m_tiles = n_pad // 128
+    n_tile = 256 if m_tokens >= 256 else max(16, (m_tokens + 15) // 16 * 16)
+    tiles = m_tiles * ((m_tokens + n_tile - 1) // n_tile)
+    k_blocks = k_pad // 64
+    if tiles >= N_SMS:
+        return 1
+    s = min(max(1, k_blocks // 4), max(1, round(N_SMS / tiles)))
+    return max(1, s)
+
+
+class Workspace:
+    """Grow-only device buffers keyed by name."""
+
+    def __init__(self):
+        self.bufs: dict[str, object] = {}
+        self.live = weakref.WeakSet()
+
+    def get(self, name: str, shape: tuple, dtype, zero: bool = True):
+        torch = _torch()
+        t = self.bufs.get(name)
+        if t is None or t.dtype != dtype or t.dim() != len(shape) or any(a < b for a, b in zip(t.shape, shape)):
+            if t is not None:
+                shape = tuple(max(a, b) for a, b in zip(t.shape, shape)) if t.dim() == len(shape) else shape
+            t = (torch.zeros if zero else torch.empty)(shape, dtype=dtype, device="cuda")
+            self.bufs[name] = t
+        return t
+
+    def detach_live(self):
+        for r in list(self.live):
+            r._detach()
+        self.live = weakref.WeakSet()
+
+
+class IntPack:
+    """Concatenate int32 arrays into one host buffer -> one H2D copy; views by name."""
+
+    def __init__(self):
+        self.parts, self.off, self.n = [], {}, 0
+
+    def add(self, name, arr):
+        a = np.ascontiguousarray(np.asarray(arr, dtype=np.int32).reshape(-1))
+        self.off[name] = (self.n, a.size)
+        self.parts.append(a)
+        self.n += a.size + (-a.size) % 4   # keep 16-byte alignment of every view
+        if (-a.size) % 4:
+            self.parts.append(np.zeros((-a.size) % 4, np.int32))
+
+    def upload(self, ws: Workspace, key: str):
+        torch = _torch()
+        host = np.concatenate(self.parts) if self.parts else np.zeros(4, np.int32)
+        dev = ws.get(key, (max(4, host.size),), torch.int32, zero=False)
+        pinned = torch.from_numpy(host).pin_memory()
+        dev[:host.size].copy_(pinned, non_blocking=True)
+        self.dev = dev
+        return self
+
+    def ptr(self, name) -> int:
+        o, _ = self.off[name]
+        return int(self.dev.data_ptr()) + 4 * o
+
+
+def _epi(**kw) -> N.Epilogue:
+    e = N.Epilogue()
+    for k, v in kw.items():
+        setattr(e, k, v)
+    return e
+
+
+class Runner:
+    """Issues the kernel chain for one model on the current stream."""
+
+    def __init__(self, dw: DeviceWeights):
+        self.dw = dw
+        self.cfg = dw.cfg
+        self.ws = Workspace()
+        self.enc_ws = Workspace()
+        self.lib = N.load()
+        torch = _torch()
+        self.splitk = self.ws.get("splitk", (64 << 20,), torch.float32, zero=False)
+        self.counters = self.ws.get("counters", (1 << 16,), torch.int32)
+
+    # ---------------------------------------------------------------- primitives
+    def gemm(self, w, k_pad, x, m, epi: N.Epilogue, splits: int | None = None):
+        if m <= 0:
+            return
+        if splits is None:
+            splits = pick_splits(w.shape[0], k_pad, m)
+        epi.m_tokens = m
+        N.check(self.lib.vlc_gemm_bf16(w.data_ptr(), w.shape[0], k_pad, x.data_ptr(), x.shape[0], m, epi, splits,
+                                       self.splitk.data_ptr(), self.splitk.numel() * 4,
+                                       self.counters.data_ptr(), _stream()), "vlc_gemm_bf16")
+
+    def rmsnorm(self, x, gamma, out, rows, out_f32=False, row_map=0):
+        d = self.cfg.model_dim
+        N.check(self.lib.vlc_rmsnorm(x.data_ptr(), x.shape[1], gamma.data_ptr(), out.data_ptr(), out.shape[1],
+                                     int(out_f32), rows, d, row_map, RMS_EPS, _stream()), "vlc_rmsnorm")
+
+    def attention(self, q, kc, vc, layer, items_ptr, n_items, comb_ptr, n_comb, qpos_ptr, rowof_ptr, out,
+                  slots):
+        torch = _torch()
+        cfg = self.cfg
+        hd = cfg.head_dim
+        ws_o = self.ws.get("attn_ws_o", (max(1, slots) * 128 * hd,), torch.float32, zero=False)
+        ws_ml = self.ws.get("attn_ws_ml", (max(1, slots) * 256,), torch.float32, zero=False)
+        a = N.AttnArgs(q=q.data_ptr(), q_rows_cap=q.shape[0], kc=kc.data_ptr(), vc=vc.data_ptr(),
+                       layers_cap=kc.shape[0], kv_rows_cap=kc.shape[1], layer=layer, kv=cfg.kv_dim,
+                       heads=cfg.num_heads, head_dim=hd, items=items_ptr, n_items=n_items, qpos=qpos_ptr,
+                       rowof=rowof_ptr, out=out.data_ptr(), ldo=out.shape[1], ws_o=ws_o.data_ptr(),
+                       ws_ml=ws_ml.data_ptr(), ws_slots=slots, comb=comb_ptr, n_comb=n_comb,
+                       scale_log2=math.log2(math.e) / math.sqrt(hd))
+        N.check(self.lib.vlc_attn_mixed(a, _stream()), "vlc_attn_mixed")
+        if n_comb:
+            N.check(self.lib.vlc_attn_combine(a, _stream()), "vlc_attn_combine")
+
+    # ---------------------------------------------------------------- vision encoder (miss path)
+    def encode(self, pixels_list) -> "object":
+        """GPU toy ViT (model.py:302-332) for k images -> fp32 [k*T, d] (workspace scratch)."""
+        torch = _torch()
+        cfg, dw, ws = self.cfg, self.dw, self.enc_ws
+        T, d, kv, p = cfg.tokens_per_image, cfg.model_dim, cfg.kv_dim, cfg.patch_size
+        k = len(pixels_list)
+        M = k * T
+        cap = max(256, M) + 256
+        patches = ws.get("patches", (cap, dw.kp), torch.bfloat16)
+        xe = ws.get("xe", (cap, d), torch.float32)
+        xn = ws.get("xn", (cap, dw.kd), torch.bfloat16)
+        qe = ws.get("qe", (cap, kv), torch.bfloat16)
+        ke = ws.get("ke", (1, cap, kv), torch.bfloat16)
+        ve = ws.get("ve", (1, cap, kv), torch.bfloat16)
+        att = ws.get("att", (cap, dw.kkv), torch.bfloat16)
+        hb = ws.get("h", (cap, dw.kh), torch.bfloat16)
+        out = ws.get("out", (cap, d), torch.float32)
+        side = cfg.image_side
+        host = np.stack([np.asarray(px, dtype=np.float32).reshape(side, side) for px in pixels_list])
+        dev_px = ws.get("pixels", (k, side, side), torch.float32, zero=False)
+        dev_px[:k].copy_(torch.from_numpy(host).pin_memory(), non_blocking=True)
+        E = dw.enc
+        for m in range(k):
+            N.check(self.lib.vlc_patchify(dev_px[m].data_ptr(), side, p, patches[m * T].data_ptr(), dw.kp, _stream()),
+                    "vlc_patchify")
+        for m in range(k):
+            # per-image GEMM so the positional rows line up with token t
+            xm = patches[m * T:]
+            self.gemm(E["patch_w"], dw.kp, xm, T,
+                      _epi(kind=N.EPI_BIAS_ADD, n_valid=d, out=xe[m * T].data_ptr(), ldo=d,
+                           bias=E["patch_b"].data_ptr(), add=E["pos"].data_ptr(), ld_add=d))
+        self.rmsnorm(xe, E["attn_norm"], xn, M)
+        self.gemm(E["wqkv_plain"], dw.kd, xn, M,
+                  _epi(kind=N.EPI_QKV_PLAIN, n_valid=3 * kv, out=qe.data_ptr(), ldo=kv, out2=ke.data_ptr(), ld2=kv,
+                       out3=ve.data_ptr(), ld3=kv, seg=kv, hd=cfg.head_dim))
+        ranges = [(m, m * T, T) for m in range(k)]
+        qpos = np.full(M, T - 1, dtype=np.int32)
+        items, comb, slots = attention_work(ranges, qpos, np.full(k, T), cfg.num_heads, 296)
+        items[:, 3] = items[:, 7] * T
+        pack = IntPack()
+        pack.add("items", items)
+        pack.add("comb", comb if len(comb) else np.zeros((1, 8)))
+        pack.add("qpos", qpos)
+        pack.add("rowof", np.arange(M))
+        pack.upload(ws, "enc_ints")
+        self.attention(qe, ke, ve, 0, pack.ptr("items"), len(items), pack.ptr("comb"), len(comb),
+                       pack.ptr("qpos"), pack.ptr("rowof"), att, slots)
+        self.gemm(E["wo"], dw.kkv, att, M, _epi(kind=N.EPI_RESID, n_valid=d, out=xe.data_ptr(), ldo=d))
+        self.rmsnorm(xe, E["mlp_norm"], xn, M)
+        self.gemm(E["wgu"], dw.kd, xn, M,
+                  _epi(kind=N.EPI_SWIGLU, n_valid=2 * cfg.mlp_hidden, out=hb.data_ptr(), ldo=dw.kh))
+        self.gemm(E["wd"], dw.kh, hb, M, _epi(kind=N.EPI_RESID, n_valid=d, out=xe.data_ptr(), ldo=d))
+        self.rmsnorm(xe, E["out_norm"], out, M, out_f32=True)
+        return out[:M]
+
+    # ---------------------------------------------------------------- decoder
+    def prefill(self, lay: Layout, text_src: np.ndarray, enc_store_rows, enc_scratch_rows, kv_pool, events=None):
+        """Run embed -> relocate -> L layers -> final norm -> head for a built Layout.
+
+        Returns dict of device tensors (logits rows in final order, caches)."""
+        torch = _torch()
+        cfg, dw, ws = self.cfg, self.dw, self.ws
+        L, d, kv, V = cfg.num_layers, cfg.model_dim, cfg.kv_dim, cfg.vocab_size
+        c = lay.c
+        c0 = int(c[0])
+        R = max(256, (c0 + 127) // 128 * 128 + 128)
+        KVR = max(128, lay.kv_rows)
+        dw.ensure_positions(max(lay.kv_rows, 1) + 1)
+        ws.detach_live()
+        x = ws.get("x", (R, d), torch.float32)
+        xn = ws.get("xn", (R, dw.kd), torch.bfloat16)
+        q = ws.get("q", (R, kv), torch.bfloat16)
+        att = ws.get("att", (R, dw.kkv), torch.bfloat16)
+        hb = ws.get("h", (R, dw.kh), torch.bfloat16)
+        kc = ws.get("kc", (L, KVR, kv), torch.bfloat16)
+        vc = ws.get("vc", (L, KVR, kv), torch.bfloat16)
+        kpre = ws.get("kpre", (L, R, kv), torch.bfloat16)
+        cL = int(c[L - 1])
+        logits = ws.get("logits", (max(cL, 1), V), torch.float32, zero=False)
+
+        pack = IntPack()
+        pack.add("src", lay.row_src)
+        pack.add("row_pos", lay.row_pos)
+        pack.add("row_kv", lay.row_kv)
+        for i in range(L):
+            pack.add(f"qdst{i}", lay.qdst[i])
+            pack.add(f"qpos{i}", lay.qpos[i])
+            pack.add(f"rowof{i}", lay.rowof[i])
+            pack.add(f"items{i}", lay.attn_items[i])
+            pack.add(f"comb{i}", lay.comb_items[i] if len(lay.comb_items[i]) else np.zeros(8))
+        pack.add("descs", lay.reloc_descs if len(lay.reloc_descs) else np.zeros(8))
+        pack.add("blocks", lay.reloc_blocks if len(lay.reloc_blocks) else np.zeros(2))
+        pack.add("pages", lay.page_table)
+        pack.add("final", lay.final_rows)
+        pack.upload(ws, "ints")
+        s = _stream()
+        if events is not None:
+            events[0].record()
+
+        # layer-0 rows: text embeddings + cached / freshly encoded image rows
+        src = np.asarray(lay.row_src)
+        enc_a = enc_store_rows.data_ptr() if enc_store_rows is not None else 0
+        enc_b = enc_scratch_rows.data_ptr() if enc_scratch_rows is not None else 0
+        N.check(self.lib.vlc_embed_assemble(x.data_ptr(), d, dw.embed.data_ptr(), d, enc_a, enc_b,
+                                            pack.ptr("src"), c0, s), "vlc_embed_assemble")
+        # cached K/V of every reused image token, all layers, re-rotated to the new positions
+        nb = len(lay.reloc_blocks)
+        if nb:
+            N.check(self.lib.vlc_kv_relocate(kv_pool.k.data_ptr(), kv_pool.v.data_ptr(), kv_pool.P, pack.ptr("pages"),
+                                             kv, cfg.head_dim, kc.data_ptr(), vc.data_ptr(), kc.shape[1],
+                                             pack.ptr("descs"), pack.ptr("blocks"), nb, dw.cos.data_ptr(),
+                                             dw.sin.data_ptr(), cfg.head_dim // 2, s), "vlc_kv_relocate")
+        KVR = kc.shape[1]
+        for i in range(L):
+            ci = int(c[i])
+            W = dw.layers[i]
+            self.rmsnorm(x, W["attn_norm"], xn, ci)
+            self.gemm(W["wqkv"], dw.kd, xn, ci, _epi(
+                kind=N.EPI_QKV_ROPE, n_valid=3 * kv, out=q.data_ptr(), ldo=kv,
+                out2=kc[i].data_ptr(), ld2=kv, out3=vc[i].data_ptr(), ld3=kv, out4=kpre[i].data_ptr(), ld4=kv,
+                map1=pack.ptr(f"qdst{i}"), map2=pack.ptr("row_kv"), pos=pack.ptr("row_pos"),
+                cos_tab=dw.cos.data_ptr(), sin_tab=dw.sin.data_ptr(), tab_ld=cfg.head_dim // 2,
+                hd=cfg.head_dim, seg=kv))
+            self.attention(q, kc, vc, i, pack.ptr(f"items{i}"), len(lay.attn_items[i]), pack.ptr(f"comb{i}"),
+                           len(lay.comb_items[i]), pack.ptr(f"qpos{i}"), pack.ptr(f"rowof{i}"), att, lay.attn_slots)
+            self.gemm(W["wo"], dw.kkv, att, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d))
+            self.rmsnorm(x, W["mlp_norm"], xn, ci)
+            self.gemm(W["wgu"], dw.kd, xn, ci,
+                      _epi(kind=N.EPI_SWIGLU, n_valid=2 * cfg.mlp_hidden, out=hb.data_ptr(), ldo=dw.kh))
+            self.gemm(W["wd"], dw.kh, hb, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d))
+        self.rmsnorm(x, dw.final_norm, xn, cL, row_map=pack.ptr("final"))
+        self.gemm(dw.head, dw.kd, xn, cL, _epi(kind=N.EPI_F32, n_valid=V, out=logits.data_ptr(), ldo=V))
+        if events is not None:
+            events[1].record()
+        return {"logits": logits, "kc": kc, "vc": vc, "kpre": kpre, "R": kpre.shape[1], "KVR": KVR, "pack": pack}

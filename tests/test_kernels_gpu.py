@@ -110,7 +110,7 @@ def test_gemm_qkv_rope_epilogue(nat, hd, heads):
     W = torch.zeros(n_pad, d, device="cuda", dtype=torch.bfloat16)
     W[:kv], W[kv:2 * kv], W[2 * kv:3 * kv] = Wq[perm], Wk[perm], Wv
     X = torch.randn(256, d, device="cuda", generator=g).bfloat16()
-    pos = torch.randint(0, 500, (m,), device="cuda", generator=g, dtype=torch.int32)
+    pos = torch.randperm(500, device="cuda", generator=g)[:m].int()
     qmap = torch.randperm(m, device="cuda", generator=g).int()
     kvmap = (pos + 3).int()
     cos, sin = _tables(hd, 600)
