@@ -363,7 +363,11 @@ class ReuseOut:
 
 
 def reuse_prefill(cfg: Cfg, w, ids, segs, hashes, ratios, enc_store, kv_store,
-                  images=None):
+                  images=None, timings=None):
+    """`timings` (optional dict) receives wall seconds of resolve / embed / each layer / head
+    (used only by bench.py's bounded CPU-baseline sample)."""
+    import time
+    t_start = time.perf_counter()
     if plan_problem(ratios) is not None or len(ratios) != cfg.num_layers:
         raise ValueError("bad plan")
     spans = image_spans(segs)
@@ -388,7 +392,10 @@ def reuse_prefill(cfg: Cfg, w, ids, segs, hashes, ratios, enc_store, kv_store,
             fallbacks += 1
             mask[:, start:start + length] = True
     counts = [int(r.sum()) for r in mask]
+    t_res = time.perf_counter()
     x_all = embed(cfg, w, ids, segs, embs)
+    t_emb = time.perf_counter()
+    per_layer = []
     allpos = np.arange(n)
     hd, base = cfg.head_dim, cfg.rope_base
     rows = None
@@ -405,7 +412,13 @@ def reuse_prefill(cfg: Cfg, w, ids, segs, hashes, ratios, enc_store, kv_store,
         x = x + a @ wo
         x = x + mlp(rmsnorm(x, g2), wg, wu, wd)
         x_all[rows] = x
+        per_layer.append(time.perf_counter())
     logits = (rmsnorm(x_all[rows], w["final_norm"]) @ w["head"]).astype(F32)
+    if timings is not None:
+        marks = [t_emb] + per_layer
+        timings.update(resolve=t_res - t_start, embed=t_emb - t_res,
+                       layers=[b - a for a, b in zip(marks[:-1], marks[1:])],
+                       head=time.perf_counter() - marks[-1])
     return ReuseOut(rows, logits, Kc, Vc, counts, misses, fallbacks)
 
 

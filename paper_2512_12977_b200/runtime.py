@@ -108,25 +108,46 @@ class Runner:
         torch = _torch()
         self.splitk = self.ws.get("splitk", (64 << 20,), torch.float32, zero=False)
         self.counters = self.ws.get("counters", (1 << 16,), torch.int32)
+        self.launches = 0          # kernels issued by this runner (all entry points)
+        self.tracer = None         # list -> (name, ev0, ev1, algo_bytes, algo_flops) per launch
+
+    def _run(self, name, fn, nbytes=0, flops=0, kernels=1):
+        """Issue one C-ABI call; optionally bracket it with CUDA events on the current stream."""
+        if self.tracer is None:
+            fn()
+        else:
+            torch = _torch()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            self.tracer.append((name, e0, e1, nbytes, flops))
+        self.launches += kernels
 
     # ---------------------------------------------------------------- primitives
-    def gemm(self, w, k_pad, x, m, epi: N.Epilogue, splits: int | None = None):
+    def gemm(self, w, k_pad, x, m, epi: N.Epilogue, splits: int | None = None, name="gemm", k_valid=None):
         if m <= 0:
             return
         if splits is None:
             splits = pick_splits(w.shape[0], k_pad, m)
         epi.m_tokens = m
-        N.check(self.lib.vlc_gemm_bf16(w.data_ptr(), w.shape[0], k_pad, x.data_ptr(), x.shape[0], m, epi, splits,
-                                       self.splitk.data_ptr(), self.splitk.numel() * 4,
-                                       self.counters.data_ptr(), _stream()), "vlc_gemm_bf16")
+        kv_ = k_valid or k_pad
+        nbytes = 2 * epi.n_valid * kv_ + 2 * m * kv_
+        self._run(name, lambda: N.check(self.lib.vlc_gemm_bf16(
+            w.data_ptr(), w.shape[0], k_pad, x.data_ptr(), x.shape[0], m, epi, splits, self.splitk.data_ptr(),
+            self.splitk.numel() * 4, self.counters.data_ptr(), _stream()), "vlc_gemm_bf16"),
+            nbytes, 2 * m * epi.n_valid * kv_)
 
     def rmsnorm(self, x, gamma, out, rows, out_f32=False, row_map=0):
         d = self.cfg.model_dim
-        N.check(self.lib.vlc_rmsnorm(x.data_ptr(), x.shape[1], gamma.data_ptr(), out.data_ptr(), out.shape[1],
-                                     int(out_f32), rows, d, row_map, RMS_EPS, _stream()), "vlc_rmsnorm")
+        if rows <= 0:
+            return
+        self._run("rmsnorm", lambda: N.check(self.lib.vlc_rmsnorm(
+            x.data_ptr(), x.shape[1], gamma.data_ptr(), out.data_ptr(), out.shape[1], int(out_f32), rows, d,
+            row_map, RMS_EPS, _stream()), "vlc_rmsnorm"), rows * d * (4 + (4 if out_f32 else 2)))
 
     def attention(self, q, kc, vc, layer, items_ptr, n_items, comb_ptr, n_comb, qpos_ptr, rowof_ptr, out,
-                  slots):
+                  slots, nbytes=0, flops=0):
         torch = _torch()
         cfg = self.cfg
         hd = cfg.head_dim
@@ -138,9 +159,10 @@ class Runner:
                        rowof=rowof_ptr, out=out.data_ptr(), ldo=out.shape[1], ws_o=ws_o.data_ptr(),
                        ws_ml=ws_ml.data_ptr(), ws_slots=slots, comb=comb_ptr, n_comb=n_comb,
                        scale_log2=math.log2(math.e) / math.sqrt(hd))
-        N.check(self.lib.vlc_attn_mixed(a, _stream()), "vlc_attn_mixed")
+        self._run("attention", lambda: N.check(self.lib.vlc_attn_mixed(a, _stream()), "vlc_attn_mixed"),
+                  nbytes, flops)
         if n_comb:
-            N.check(self.lib.vlc_attn_combine(a, _stream()), "vlc_attn_combine")
+            self._run("attn_combine", lambda: N.check(self.lib.vlc_attn_combine(a, _stream()), "vlc_attn_combine"))
 
     # ---------------------------------------------------------------- vision encoder (miss path)
     def encode(self, pixels_list) -> "object":
@@ -166,8 +188,8 @@ class Runner:
         dev_px[:k].copy_(torch.from_numpy(host).pin_memory(), non_blocking=True)
         E = dw.enc
         for m in range(k):
-            N.check(self.lib.vlc_patchify(dev_px[m].data_ptr(), side, p, patches[m * T].data_ptr(), dw.kp, _stream()),
-                    "vlc_patchify")
+            self._run("patchify", lambda m=m: N.check(self.lib.vlc_patchify(
+                dev_px[m].data_ptr(), side, p, patches[m * T].data_ptr(), dw.kp, _stream()), "vlc_patchify"))
         for m in range(k):
             # per-image GEMM so the positional rows line up with token t
             xm = patches[m * T:]
@@ -246,15 +268,17 @@ class Runner:
         src = np.asarray(lay.row_src)
         enc_a = enc_store_rows.data_ptr() if enc_store_rows is not None else 0
         enc_b = enc_scratch_rows.data_ptr() if enc_scratch_rows is not None else 0
-        N.check(self.lib.vlc_embed_assemble(x.data_ptr(), d, dw.embed.data_ptr(), d, enc_a, enc_b,
-                                            pack.ptr("src"), c0, s), "vlc_embed_assemble")
+        self._run("embed", lambda: N.check(self.lib.vlc_embed_assemble(
+            x.data_ptr(), d, dw.embed.data_ptr(), d, enc_a, enc_b, pack.ptr("src"), c0, s), "vlc_embed_assemble"),
+            c0 * d * 6)
         # cached K/V of every reused image token, all layers, re-rotated to the new positions
         nb = len(lay.reloc_blocks)
         if nb:
-            N.check(self.lib.vlc_kv_relocate(kv_pool.k.data_ptr(), kv_pool.v.data_ptr(), kv_pool.P, pack.ptr("pages"),
-                                             kv, cfg.head_dim, kc.data_ptr(), vc.data_ptr(), kc.shape[1],
-                                             pack.ptr("descs"), pack.ptr("blocks"), nb, dw.cos.data_ptr(),
-                                             dw.sin.data_ptr(), cfg.head_dim // 2, s), "vlc_kv_relocate")
+            self._run("kv_relocate", lambda: N.check(self.lib.vlc_kv_relocate(
+                kv_pool.k.data_ptr(), kv_pool.v.data_ptr(), kv_pool.P, pack.ptr("pages"), kv, cfg.head_dim,
+                kc.data_ptr(), vc.data_ptr(), kc.shape[1], pack.ptr("descs"), pack.ptr("blocks"), nb,
+                dw.cos.data_ptr(), dw.sin.data_ptr(), cfg.head_dim // 2, s), "vlc_kv_relocate"),
+                lay.reloc_tokens * kv * 2 * 4)
         KVR = kc.shape[1]
         for i in range(L):
             ci = int(c[i])
@@ -265,16 +289,22 @@ class Runner:
                 out2=kc[i].data_ptr(), ld2=kv, out3=vc[i].data_ptr(), ld3=kv, out4=kpre[i].data_ptr(), ld4=kv,
                 map1=pack.ptr(f"qdst{i}"), map2=pack.ptr("row_kv"), pos=pack.ptr("row_pos"),
                 cos_tab=dw.cos.data_ptr(), sin_tab=dw.sin.data_ptr(), tab_ld=cfg.head_dim // 2,
-                hd=cfg.head_dim, seg=kv))
+                hd=cfg.head_dim, seg=kv), name="gemm_qkv", k_valid=d)
+            vis = int(lay.qpos[i, :ci].astype(np.int64).sum()) + ci
             self.attention(q, kc, vc, i, pack.ptr(f"items{i}"), len(lay.attn_items[i]), pack.ptr(f"comb{i}"),
-                           len(lay.comb_items[i]), pack.ptr(f"qpos{i}"), pack.ptr(f"rowof{i}"), att, lay.attn_slots)
-            self.gemm(W["wo"], dw.kkv, att, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d))
+                           len(lay.comb_items[i]), pack.ptr(f"qpos{i}"), pack.ptr(f"rowof{i}"), att, lay.attn_slots,
+                           nbytes=lay.kv_rows * kv * 4 + ci * kv * 4, flops=4 * cfg.head_dim * cfg.num_heads * vis)
+            self.gemm(W["wo"], dw.kkv, att, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d),
+                      name="gemm_o", k_valid=kv)
             self.rmsnorm(x, W["mlp_norm"], xn, ci)
             self.gemm(W["wgu"], dw.kd, xn, ci,
-                      _epi(kind=N.EPI_SWIGLU, n_valid=2 * cfg.mlp_hidden, out=hb.data_ptr(), ldo=dw.kh))
-            self.gemm(W["wd"], dw.kh, hb, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d))
+                      _epi(kind=N.EPI_SWIGLU, n_valid=2 * cfg.mlp_hidden, out=hb.data_ptr(), ldo=dw.kh),
+                      name="gemm_gate_up", k_valid=d)
+            self.gemm(W["wd"], dw.kh, hb, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d),
+                      name="gemm_down", k_valid=cfg.mlp_hidden)
         self.rmsnorm(x, dw.final_norm, xn, cL, row_map=pack.ptr("final"))
-        self.gemm(dw.head, dw.kd, xn, cL, _epi(kind=N.EPI_F32, n_valid=V, out=logits.data_ptr(), ldo=V))
+        self.gemm(dw.head, dw.kd, xn, cL, _epi(kind=N.EPI_F32, n_valid=V, out=logits.data_ptr(), ldo=V),
+                  name="gemm_head", k_valid=d)
         if events is not None:
             events[1].record()
         return {"logits": logits, "kc": kc, "vc": vc, "kpre": kpre, "R": kpre.shape[1], "KVR": KVR, "pack": pack}
