@@ -273,35 +273,31 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
 }
 
 // Merge split-KV partials: O = sum_s 2^(m_s-M) O_s / sum_s 2^(m_s-M) l_s.
+// Block = one combine item; thread = (query row, 4 output columns).
 template <int HD>
-__global__ void attn_combine_kernel(vlc_attn_args a) {
+__global__ void __launch_bounds__(256) attn_combine_kernel(vlc_attn_args a) {
   const int* it = a.comb + blockIdx.x * 8;
   const int q_row0 = it[0], n_q = it[1], head = it[2], slot0 = it[3], ns = it[4];
-  const int r = threadIdx.x;
-  if (r >= n_q) return;
-  float M = -INFINITY;
-  for (int s = 0; s < ns; ++s) M = fmaxf(M, a.ws_ml[((long)(slot0 + s) * 128 + r) * 2]);
-  float L = 0.f;
-  float acc[HD];
-#pragma unroll
-  for (int d = 0; d < HD; ++d) acc[d] = 0.f;
-  for (int s = 0; s < ns; ++s) {
-    const long base = (long)(slot0 + s) * 128 + r;
-    const float m = a.ws_ml[base * 2], l = a.ws_ml[base * 2 + 1];
-    const float w = (m == -INFINITY) ? 0.f : exp2f(m - M);
-    L += w * l;
-    const float4* src = reinterpret_cast<const float4*>(a.ws_o + base * HD);
-#pragma unroll
-    for (int d4 = 0; d4 < HD / 4; ++d4) {
-      const float4 v = src[d4];
-      acc[4 * d4] += w * v.x; acc[4 * d4 + 1] += w * v.y; acc[4 * d4 + 2] += w * v.z; acc[4 * d4 + 3] += w * v.w;
+  constexpr int C4 = HD / 4;
+  for (int w = threadIdx.x; w < 128 * C4; w += blockDim.x) {
+    const int r = w / C4, c4 = w - r * C4;
+    if (r >= n_q) break;
+    float M = -INFINITY;
+    for (int s = 0; s < ns; ++s) M = fmaxf(M, __ldg(a.ws_ml + ((long)(slot0 + s) * 128 + r) * 2));
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < ns; ++s) {
+      const long base = (long)(slot0 + s) * 128 + r;
+      const float m = __ldg(a.ws_ml + base * 2), l = __ldg(a.ws_ml + base * 2 + 1);
+      const float wgt = (m == -INFINITY) ? 0.f : exp2f(m - M);
+      L += wgt * l;
+      const float4 o = __ldg(reinterpret_cast<const float4*>(a.ws_o + base * HD) + c4);
+      acc.x += wgt * o.x; acc.y += wgt * o.y; acc.z += wgt * o.z; acc.w += wgt * o.w;
     }
-  }
-  const float inv = L > 0.f ? 1.0f / L : 0.f;
-  __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(a.out) + (long)a.rowof[q_row0 + r] * a.ldo + head * HD;
-#pragma unroll
-  for (int d = 0; d < HD; d += 2) {
-    *reinterpret_cast<uint32_t*>(orow + d) = pack_bf16(acc[d] * inv, acc[d + 1] * inv);
+    const float inv = L > 0.f ? 1.0f / L : 0.f;
+    __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(a.out) + (long)a.rowof[q_row0 + r] * a.ldo + head * HD;
+    uint2 pk = make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
+    *reinterpret_cast<uint2*>(orow + c4 * 4) = pk;
   }
 }
 
@@ -340,10 +336,10 @@ cudaError_t launch_attention(const vlc_attn_args& a, cudaStream_t stream) {
 cudaError_t launch_attn_combine(const vlc_attn_args& a, cudaStream_t stream) {
   if (a.n_comb <= 0) return cudaSuccess;
   switch (a.head_dim) {
-    case 16: attn_combine_kernel<16><<<a.n_comb, 128, 0, stream>>>(a); break;
-    case 32: attn_combine_kernel<32><<<a.n_comb, 128, 0, stream>>>(a); break;
-    case 64: attn_combine_kernel<64><<<a.n_comb, 128, 0, stream>>>(a); break;
-    case 128: attn_combine_kernel<128><<<a.n_comb, 128, 0, stream>>>(a); break;
+    case 16: attn_combine_kernel<16><<<a.n_comb, 256, 0, stream>>>(a); break;
+    case 32: attn_combine_kernel<32><<<a.n_comb, 256, 0, stream>>>(a); break;
+    case 64: attn_combine_kernel<64><<<a.n_comb, 256, 0, stream>>>(a); break;
+    case 128: attn_combine_kernel<128><<<a.n_comb, 256, 0, stream>>>(a); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -29,72 +29,117 @@ __device__ __forceinline__ void store_bf16(void* base, long idx, float v) {
   reinterpret_cast<__nv_bfloat16*>(base)[idx] = __float2bfloat16_rn(v);
 }
 
-// Apply the epilogue for 16 consecutive token columns of one weight row.
+// Apply the epilogue to 16 consecutive token columns (j0 .. j0+15) of this thread's
+// weight row f.  Per-token metadata is fetched once per warp (lane i loads token j0+i,
+// then broadcast with shuffles) and every global load of the chunk is issued before
+// any store, so the chunk costs ~one memory round trip instead of sixteen.
 __device__ __forceinline__ void epilogue_chunk(const GemmEpi& e, int f, int j0, const float* v) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int jl = j0 + (lane & 15);
+  const bool jl_ok = jl < e.m_tokens;
+  const int m1_l = (e.map1 && jl_ok) ? __ldg(e.map1 + jl) : jl;
+  const int m2_l = (e.map2 && jl_ok) ? __ldg(e.map2 + jl) : jl;
+  const int ps_l = (e.pos && jl_ok) ? __ldg(e.pos + jl) : 0;
+  const int nv = min(16, e.m_tokens - j0);
   const bool row_ok = f < e.n_valid;
+  switch (e.kind) {
+    case EPI_F32: {
+      float* __restrict__ o = reinterpret_cast<float*>(e.out) + f;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int j = j0 + i;
-    const float val = v[i];
-    float partner = 0.f;
-    if (e.kind == EPI_QKV_ROPE || e.kind == EPI_SWIGLU) partner = __shfl_xor_sync(0xffffffffu, val, 1);
-    if (!row_ok || j >= e.m_tokens) continue;
-    switch (e.kind) {
-      case EPI_F32: {
-        const long r = e.map1 ? e.map1[j] : j;
-        reinterpret_cast<float*>(e.out)[r * e.ldo + f] = val;
-        break;
+      for (int i = 0; i < 16; ++i) {
+        const int r = __shfl_sync(FULL, m1_l, i);
+        if (row_ok && i < nv) o[(long)r * e.ldo] = v[i];
       }
-      case EPI_RESID: {
-        float* o = reinterpret_cast<float*>(e.out) + (long)j * e.ldo + f;
-        *o = *o + val;
-        break;
-      }
-      case EPI_BF16:
-        store_bf16(e.out, (long)j * e.ldo + f, val);
-        break;
-      case EPI_BIAS_ADD: {
-        const float b = e.bias ? e.bias[f] : 0.f;
-        const float a = e.add ? e.add[(long)j * e.ld_add + f] : 0.f;
-        reinterpret_cast<float*>(e.out)[(long)j * e.ldo + f] = (val + b) + a;
-        break;
-      }
-      case EPI_SWIGLU: {
-        if ((f & 1) == 0) store_bf16(e.out, (long)j * e.ldo + (f >> 1), silu_f(val) * partner);
-        break;
-      }
-      case EPI_QKV_PLAIN: {
-        const int sec = f / e.seg, r = f - sec * e.seg;
-        if (sec == 0) store_bf16(e.out, (long)j * e.ldo + r, val);
-        else if (sec == 1) store_bf16(e.out2, (long)j * e.ld2 + r, val);
-        else store_bf16(e.out3, (long)j * e.ld3 + r, val);
-        break;
-      }
-      case EPI_QKV_ROPE: {
-        const int sec = f / e.seg, r = f - sec * e.seg;
-        if (sec == 2) {  // V: not permuted, not rotated
-          store_bf16(e.out3, (long)e.map2[j] * e.ld3 + r, val);
-          break;
-        }
-        const int half = e.hd >> 1;
-        const int head = r / e.hd, w = r - head * e.hd, t = w >> 1, odd = w & 1;
-        const int feat = head * e.hd + (odd ? t + half : t);
-        const long tab = (long)e.pos[j] * e.tab_ld + t;
-        const float c = e.cos_tab[tab], s = e.sin_tab[tab];
-        const float a = odd ? partner : val, b = odd ? val : partner;
-        const float rot = odd ? (b * c + a * s) : (a * c - b * s);
-        if (sec == 0) {
-          const long qr = e.map1 ? e.map1[j] : j;
-          store_bf16(e.out, qr * e.ldo + feat, rot);
-        } else {
-          if (e.out4) store_bf16(e.out4, (long)j * e.ld4 + feat, val);
-          store_bf16(e.out2, (long)e.map2[j] * e.ld2 + feat, rot);
-        }
-        break;
-      }
-      default:
-        break;
+      break;
     }
+    case EPI_RESID: {
+      float* __restrict__ o = reinterpret_cast<float*>(e.out) + f;
+      float old[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) old[i] = (row_ok && i < nv) ? o[(long)(j0 + i) * e.ldo] : 0.f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (row_ok && i < nv) o[(long)(j0 + i) * e.ldo] = old[i] + v[i];
+      break;
+    }
+    case EPI_BF16: {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (row_ok && i < nv) store_bf16(e.out, (long)(j0 + i) * e.ldo + f, v[i]);
+      break;
+    }
+    case EPI_BIAS_ADD: {
+      const float b = (e.bias && row_ok) ? __ldg(e.bias + f) : 0.f;
+      float a[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        a[i] = (e.add && row_ok && i < nv) ? __ldg(e.add + (long)(j0 + i) * e.ld_add + f) : 0.f;
+      float* __restrict__ o = reinterpret_cast<float*>(e.out) + f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (row_ok && i < nv) o[(long)(j0 + i) * e.ldo] = (v[i] + b) + a[i];
+      break;
+    }
+    case EPI_SWIGLU: {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float up = __shfl_xor_sync(FULL, v[i], 1);
+        if (row_ok && i < nv && (f & 1) == 0) store_bf16(e.out, (long)(j0 + i) * e.ldo + (f >> 1), silu_f(v[i]) * up);
+      }
+      break;
+    }
+    case EPI_QKV_PLAIN: {
+      const int sec = f / e.seg, r = f - sec * e.seg;
+      void* dst = sec == 0 ? e.out : sec == 1 ? e.out2 : e.out3;
+      const int ld = sec == 0 ? e.ldo : sec == 1 ? e.ld2 : e.ld3;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (row_ok && i < nv) store_bf16(dst, (long)(j0 + i) * ld + r, v[i]);
+      break;
+    }
+    case EPI_QKV_ROPE: {
+      const int sec = f / e.seg, r = f - sec * e.seg;
+      float partner[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) partner[i] = __shfl_xor_sync(FULL, v[i], 1);
+      if (sec == 2) {  // V: not permuted, not rotated
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int kr = __shfl_sync(FULL, m2_l, i);
+          if (row_ok && i < nv) store_bf16(e.out3, (long)kr * e.ld3 + r, v[i]);
+        }
+        break;
+      }
+      const int half = e.hd >> 1;
+      const int head = r / e.hd, w = r - head * e.hd, t = w >> 1, odd = w & 1;
+      const int feat = head * e.hd + (odd ? t + half : t);
+      float c[16], sn[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int p = __shfl_sync(FULL, ps_l, i);
+        const long tab = (long)p * e.tab_ld + t;
+        c[i] = row_ok ? __ldg(e.cos_tab + tab) : 0.f;
+        sn[i] = row_ok ? __ldg(e.sin_tab + tab) : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float a = odd ? partner[i] : v[i], b = odd ? v[i] : partner[i];
+        const float rot = odd ? (b * c[i] + a * sn[i]) : (a * c[i] - b * sn[i]);
+        const int q_row = __shfl_sync(FULL, m1_l, i);
+        const int kv_row = __shfl_sync(FULL, m2_l, i);
+        if (!(row_ok && i < nv)) continue;
+        if (sec == 0) {
+          store_bf16(e.out, (long)q_row * e.ldo + feat, rot);
+        } else {
+          if (e.out4) store_bf16(e.out4, (long)(j0 + i) * e.ld4 + feat, v[i]);
+          store_bf16(e.out2, (long)kv_row * e.ld2 + feat, rot);
+        }
+      }
+      break;
+    }
+    default:
+      break;
   }
 }
 

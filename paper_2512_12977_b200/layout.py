@@ -67,6 +67,19 @@ class Layout:
     positions: list               # per request: int64 positions with logits (reference `rows`)
     logit_ranges: list            # per request: (start, count) into the logits rows
 
+    def structure_key(self) -> bytes:
+        """Everything that shapes the launch chain (not the token ids / page ids it reads)."""
+        import hashlib
+        h = hashlib.sha1()
+        for a in (self.c, self.kvoff, self.row_pos, self.row_kv, self.qdst, self.qpos, self.rowof,
+                  self.reloc_descs, self.reloc_blocks, self.final_rows, self.row_src[:, 0]):
+            h.update(np.ascontiguousarray(a).tobytes())
+            h.update(b"|")
+        for a in self.attn_items + self.comb_items:
+            h.update(np.ascontiguousarray(a).tobytes())
+        h.update(f"{len(self.page_table)}|{self.kv_rows}|{self.attn_slots}".encode())
+        return h.digest()
+
 
 RELOC_TOK = 8
 

@@ -109,6 +109,8 @@ class Runner:
         self.splitk = self.ws.get("splitk", (64 << 20,), torch.float32, zero=False)
         self.counters = self.ws.get("counters", (1 << 16,), torch.int32)
         self.launches = 0          # kernels issued by this runner (all entry points)
+        self.graphs: dict = {}     # structure key -> captured CUDA graph of the prefill chain
+        self.graph_launches: dict = {}
         self.tracer = None         # list -> (name, ev0, ev1, algo_bytes, algo_flops) per launch
 
     def _run(self, name, fn, nbytes=0, flops=0, kernels=1):
@@ -221,10 +223,14 @@ class Runner:
         return out[:M]
 
     # ---------------------------------------------------------------- decoder
-    def prefill(self, lay: Layout, text_src: np.ndarray, enc_store_rows, enc_scratch_rows, kv_pool, events=None):
-        """Run embed -> relocate -> L layers -> final norm -> head for a built Layout.
+    def prefill(self, lay: Layout, text_src: np.ndarray, enc_store_rows, enc_scratch_rows, kv_pool, events=None,
+                use_graph: bool = True):
+        """Run embed -> kv_relocate -> L layers -> final norm -> head for a built Layout.
 
-        Returns dict of device tensors (logits rows in final order, caches)."""
+        The launch chain depends only on the layout STRUCTURE (row counts, work lists) and
+        on buffer addresses; per-request data (token ids, store pages) travels in one int32
+        upload.  The chain is therefore captured once per structure into a CUDA graph and
+        replayed: one launch instead of ~230.  Returns the device tensors of the result."""
         torch = _torch()
         cfg, dw, ws = self.cfg, self.dw, self.ws
         L, d, kv, V = cfg.num_layers, cfg.model_dim, cfg.kv_dim, cfg.vocab_size
@@ -234,16 +240,15 @@ class Runner:
         KVR = max(128, lay.kv_rows)
         dw.ensure_positions(max(lay.kv_rows, 1) + 1)
         ws.detach_live()
-        x = ws.get("x", (R, d), torch.float32)
-        xn = ws.get("xn", (R, dw.kd), torch.bfloat16)
-        q = ws.get("q", (R, kv), torch.bfloat16)
-        att = ws.get("att", (R, dw.kkv), torch.bfloat16)
-        hb = ws.get("h", (R, dw.kh), torch.bfloat16)
-        kc = ws.get("kc", (L, KVR, kv), torch.bfloat16)
-        vc = ws.get("vc", (L, KVR, kv), torch.bfloat16)
-        kpre = ws.get("kpre", (L, R, kv), torch.bfloat16)
-        cL = int(c[L - 1])
-        logits = ws.get("logits", (max(cL, 1), V), torch.float32, zero=False)
+        buf = dict(
+            x=ws.get("x", (R, d), torch.float32), xn=ws.get("xn", (R, dw.kd), torch.bfloat16),
+            q=ws.get("q", (R, kv), torch.bfloat16), att=ws.get("att", (R, dw.kkv), torch.bfloat16),
+            h=ws.get("h", (R, dw.kh), torch.bfloat16), kc=ws.get("kc", (L, KVR, kv), torch.bfloat16),
+            vc=ws.get("vc", (L, KVR, kv), torch.bfloat16), kpre=ws.get("kpre", (L, R, kv), torch.bfloat16),
+            logits=ws.get("logits", (max(int(c[L - 1]), 1), V), torch.float32, zero=False))
+        hd = cfg.head_dim
+        ws.get("attn_ws_o", (max(1, lay.attn_slots) * 128 * hd,), torch.float32, zero=False)
+        ws.get("attn_ws_ml", (max(1, lay.attn_slots) * 256,), torch.float32, zero=False)
 
         pack = IntPack()
         pack.add("src", lay.row_src)
@@ -260,14 +265,54 @@ class Runner:
         pack.add("pages", lay.page_table)
         pack.add("final", lay.final_rows)
         pack.upload(ws, "ints")
-        s = _stream()
+        ptrs = (enc_store_rows.data_ptr() if enc_store_rows is not None else 0,
+                enc_scratch_rows.data_ptr() if enc_scratch_rows is not None else 0,
+                kv_pool.k.data_ptr() if kv_pool is not None else 0,
+                kv_pool.v.data_ptr() if kv_pool is not None else 0, kv_pool.P if kv_pool is not None else 0,
+                pack.dev.data_ptr(), dw.cos.data_ptr(), self.splitk.data_ptr(),
+                ws.bufs["attn_ws_o"].data_ptr(), ws.bufs["attn_ws_ml"].data_ptr()) + tuple(
+                    t.data_ptr() for t in buf.values())
+        chain = lambda: self._chain(lay, pack, buf, ptrs)  # noqa: E731
         if events is not None:
             events[0].record()
+        if use_graph and self.tracer is None:
+            key = (lay.structure_key(), ptrs, tuple(pack.off.items()))
+            g = self.graphs.get(key)
+            if g is None:
+                chain()                                   # eager run serves this call
+                g = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream()
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    with torch.cuda.graph(g, stream=side):
+                        launches = self.launches
+                        chain()
+                        self.graph_launches[key] = self.launches - launches
+                        self.launches = launches
+                torch.cuda.current_stream().wait_stream(side)
+                if len(self.graphs) >= 16:
+                    self.graphs.pop(next(iter(self.graphs)))
+                self.graphs[key] = g
+            else:
+                g.replay()
+                self.launches += self.graph_launches[key]
+        else:
+            chain()
+        if events is not None:
+            events[1].record()
+        return {"logits": buf["logits"], "kc": buf["kc"], "vc": buf["vc"], "kpre": buf["kpre"],
+                "R": buf["kpre"].shape[1], "KVR": buf["kc"].shape[1], "pack": pack}
 
+    def _chain(self, lay: Layout, pack: "IntPack", buf: dict, ptrs):
+        cfg, dw = self.cfg, self.dw
+        L, d, kv, V = cfg.num_layers, cfg.model_dim, cfg.kv_dim, cfg.vocab_size
+        x, xn, q, att, hb = buf["x"], buf["xn"], buf["q"], buf["att"], buf["h"]
+        kc, vc, kpre, logits = buf["kc"], buf["vc"], buf["kpre"], buf["logits"]
+        c = lay.c
+        c0, cL = int(c[0]), int(c[L - 1])
+        enc_a, enc_b, kpool, vpool, P = ptrs[:5]
+        s = _stream()
         # layer-0 rows: text embeddings + cached / freshly encoded image rows
-        src = np.asarray(lay.row_src)
-        enc_a = enc_store_rows.data_ptr() if enc_store_rows is not None else 0
-        enc_b = enc_scratch_rows.data_ptr() if enc_scratch_rows is not None else 0
         self._run("embed", lambda: N.check(self.lib.vlc_embed_assemble(
             x.data_ptr(), d, dw.embed.data_ptr(), d, enc_a, enc_b, pack.ptr("src"), c0, s), "vlc_embed_assemble"),
             c0 * d * 6)
@@ -275,11 +320,9 @@ class Runner:
         nb = len(lay.reloc_blocks)
         if nb:
             self._run("kv_relocate", lambda: N.check(self.lib.vlc_kv_relocate(
-                kv_pool.k.data_ptr(), kv_pool.v.data_ptr(), kv_pool.P, pack.ptr("pages"), kv, cfg.head_dim,
-                kc.data_ptr(), vc.data_ptr(), kc.shape[1], pack.ptr("descs"), pack.ptr("blocks"), nb,
-                dw.cos.data_ptr(), dw.sin.data_ptr(), cfg.head_dim // 2, s), "vlc_kv_relocate"),
-                lay.reloc_tokens * kv * 2 * 4)
-        KVR = kc.shape[1]
+                kpool, vpool, P, pack.ptr("pages"), kv, cfg.head_dim, kc.data_ptr(), vc.data_ptr(), kc.shape[1],
+                pack.ptr("descs"), pack.ptr("blocks"), nb, dw.cos.data_ptr(), dw.sin.data_ptr(), cfg.head_dim // 2,
+                s), "vlc_kv_relocate"), lay.reloc_tokens * kv * 2 * 4)
         for i in range(L):
             ci = int(c[i])
             W = dw.layers[i]
@@ -305,6 +348,3 @@ class Runner:
         self.rmsnorm(x, dw.final_norm, xn, cL, row_map=pack.ptr("final"))
         self.gemm(dw.head, dw.kd, xn, cL, _epi(kind=N.EPI_F32, n_valid=V, out=logits.data_ptr(), ldo=V),
                   name="gemm_head", k_valid=d)
-        if events is not None:
-            events[1].record()
-        return {"logits": logits, "kc": kc, "vc": vc, "kpre": kpre, "R": kpre.shape[1], "KVR": KVR, "pack": pack}
