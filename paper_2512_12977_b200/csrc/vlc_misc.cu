@@ -25,12 +25,54 @@ __global__ void embed_assemble_kernel(float* __restrict__ x, int ldx,
 }
 
 // ------------------------------------------------------------------ rmsnorm (K4)
-template <bool OUT_F32>
-__global__ void rmsnorm_kernel(const float* __restrict__ x, int ldx, const float* __restrict__ g,
-                               void* __restrict__ out, int ldo, int rows, int d,
-                               const int* __restrict__ row_map, float eps) {
-  const int r = blockIdx.x;
+// One warp per row, the row held in registers as float4 (d <= 32*4*VPT), so x is
+// read once; 8 rows per 256-thread block.
+template <bool OUT_F32, int VPT>
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, int ldx,
+                                                      const float* __restrict__ g, void* __restrict__ out,
+                                                      int ldo, int rows, int d,
+                                                      const int* __restrict__ row_map, float eps) {
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (r >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const int sr = row_map ? __ldg(row_map + r) : r;
+  const float4* xr = reinterpret_cast<const float4*>(x + (long)sr * ldx);
+  const int n4 = d >> 2;
+  float4 v[VPT];
+  float acc = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int i = lane + 32 * k;
+    v[k] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) acc += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  const float denom = sqrtf(acc / (float)d + eps);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int i = lane + 32 * k;
+    if (i >= n4) break;
+    const float4 gg = __ldg(g4 + i);
+    const float4 y = make_float4((v[k].x / denom) * gg.x, (v[k].y / denom) * gg.y, (v[k].z / denom) * gg.z,
+                                 (v[k].w / denom) * gg.w);
+    if (OUT_F32) {
+      reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + (long)r * ldo)[i] = y;
+    } else {
+      uint2 pk = make_uint2(pack_bf16(y.x, y.y), pack_bf16(y.z, y.w));
+      reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + (long)r * ldo)[i] = pk;
+    }
+  }
+}
+
+// Generic fallback (any d): block per row.
+template <bool OUT_F32>
+__global__ void rmsnorm_generic(const float* __restrict__ x, int ldx, const float* __restrict__ g,
+                                void* __restrict__ out, int ldo, int rows, int d,
+                                const int* __restrict__ row_map, float eps) {
+  const int r = blockIdx.x;
   const int sr = row_map ? row_map[r] : r;
   const float* xr = x + (long)sr * ldx;
   float acc = 0.f;
@@ -203,10 +245,23 @@ int vlc_embed_assemble_impl(float* x, int ldx, const void* embed_bf16, int d, co
 int vlc_rmsnorm_impl(const float* x, int ldx, const float* gamma, void* out, int ldo, int out_f32,
                      int rows, int d, const int* row_map, float eps, cudaStream_t stream) {
   if (rows <= 0) return 0;
-  if (out_f32)
-    rmsnorm_kernel<true><<<rows, 256, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps);
-  else
-    rmsnorm_kernel<false><<<rows, 256, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps);
+  const bool vec = (d % 4 == 0) && (ldx % 4 == 0) && (ldo % 4 == 0) && d <= 32 * 4 * 32;
+  const unsigned blocks = (rows + 7) / 8;
+#define VLC_RMS(VPT)                                                                                   \
+  if (out_f32) rmsnorm_kernel<true, VPT><<<blocks, 256, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps); \
+  else rmsnorm_kernel<false, VPT><<<blocks, 256, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps);
+  if (vec) {
+    const int vpt = (d / 4 + 31) / 32;
+    if (vpt <= 2) { VLC_RMS(2) }
+    else if (vpt <= 8) { VLC_RMS(8) }
+    else if (vpt <= 16) { VLC_RMS(16) }
+    else { VLC_RMS(32) }
+  } else if (out_f32) {
+    rmsnorm_generic<true><<<rows, 256, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps);
+  } else {
+    rmsnorm_generic<false><<<rows, 256, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps);
+  }
+#undef VLC_RMS
   return (int)cudaGetLastError();
 }
 

@@ -21,7 +21,7 @@ import numpy as np
 
 from .config import ModelConfig
 from .exceptions import InputError
-from .layout import SRC_SCRATCH, SRC_STORE, RequestSpec, build_layout
+from .layout import SRC_SCRATCH, SRC_STORE, RequestSpec, build_layout, structure_of, with_data
 from .model import KVTensors, ToyVLM
 from .plans import ComputationMask, RecomputePlan, build_masks, layer_keep, mean_ratio, require_valid
 from .sequence import TokenSequence, make_sequence
@@ -149,6 +149,19 @@ class ReuseResult:
 
 # ---------------------------------------------------------------- runner cache
 
+def _layout(runner, specs, L, heads):
+    """Structural layouts are cached per runner; per-request data is patched in."""
+    key = structure_of(specs, L, heads)
+    lay = runner.layouts.get(key)
+    if lay is None:
+        lay = build_layout(specs, L, heads)
+        if len(runner.layouts) >= 64:
+            runner.layouts.pop(next(iter(runner.layouts)))
+        runner.layouts[key] = lay
+        return lay
+    return with_data(lay, specs)
+
+
 def _runner(model: ToyVLM):
     from .runtime import Runner
     r = getattr(model, "_runner", None)
@@ -257,7 +270,7 @@ def prefill_with_reuse(model: ToyVLM, request: ReuseRequest, store: CacheStore) 
     spec = RequestSpec(n=len(seq), text_pos=text_pos, text_ids=text_ids,
                        images=[(s.start, s.length) for s in segs], keep=keep, kv_hit=kv_hit,
                        enc_src=enc_src, page_rows=page_rows)
-    lay = build_layout([spec], L, cfg.num_heads)
+    lay = _layout(runner, [spec], L, cfg.num_heads)
     import torch
     ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
     out = runner.prefill(lay, text_ids, enc_pool.rows.view(-1, cfg.model_dim) if enc_pool else None,
@@ -273,36 +286,33 @@ def prefill_with_reuse(model: ToyVLM, request: ReuseRequest, store: CacheStore) 
 
 def _merged_kv_loader(out, lay, spec: RequestSpec, kv_pool, cfg: ModelConfig, req: int = 0):
     """Merged pre-RoPE KV [L, n, kv] of one request: computed rows from the QKV epilogue's
-    pre-RoPE copy, reused rows from the store pages (engine.py:153-155, 177-178)."""
-    L, n = cfg.num_layers, spec.n
-    kvoff = int(lay.kvoff[req])
-    sel = np.flatnonzero(lay.row_req == req)
-    pos = lay.row_pos[sel].astype(np.int64)
-    kpre_idx, kpre_dst, pool_idx, pool_dst = [], [], [], []
-    R = out["R"]
-    for i in range(L):
-        live = sel < lay.c[i]
-        kpre_idx.append(i * R + sel[live])
-        kpre_dst.append(i * n + pos[live])
-        for m, (start, T) in enumerate(spec.images):
-            if not spec.kv_hit[m]:
-                continue
-            t = np.arange(int(spec.keep[i, m]), T)
-            if not len(t):
-                continue
-            pages = spec.page_rows[m]
-            pool_idx.append(pages[i, t // kv_pool.P].astype(np.int64) * kv_pool.P + t % kv_pool.P)
-            pool_dst.append(i * n + start + t)
-    kpre, vc = out["kpre"], out["vc"]
+    pre-RoPE copy, reused rows from the store pages (engine.py:153-155, 177-178).
+    Index construction is deferred to the first access."""
+    kpre, vc, R = out["kpre"], out["vc"], out["R"]
 
     def load():
         import torch
-        kvd = cfg.kv_dim
+        L, n, kvd = cfg.num_layers, spec.n, cfg.kv_dim
+        kvoff = int(lay.kvoff[req])
+        sel = np.flatnonzero(lay.row_req == req)
+        pos = lay.row_pos[sel].astype(np.int64)
+        kpre_idx, kpre_dst, pool_idx, pool_dst = [], [], [], []
+        for i in range(L):
+            live = sel < lay.c[i]
+            kpre_idx.append(i * R + sel[live])
+            kpre_dst.append(i * n + pos[live])
+            for m, (start, T) in enumerate(spec.images):
+                if not spec.kv_hit[m]:
+                    continue
+                t = np.arange(int(spec.keep[i, m]), T)
+                if len(t):
+                    pages = spec.page_rows[m]
+                    pool_idx.append(pages[i, t // kv_pool.P].astype(np.int64) * kv_pool.P + t % kv_pool.P)
+                    pool_dst.append(i * n + start + t)
         K = torch.zeros(L * n, kvd, dtype=torch.bfloat16, device="cuda")
-        src = kpre.view(-1, kvd)
         a = torch.from_numpy(np.concatenate(kpre_idx)).cuda()
         b = torch.from_numpy(np.concatenate(kpre_dst)).cuda()
-        K[b] = src[a]
+        K[b] = kpre.view(-1, kvd)[a]
         if pool_idx:
             a = torch.from_numpy(np.concatenate(pool_idx)).cuda()
             b = torch.from_numpy(np.concatenate(pool_dst)).cuda()
@@ -344,7 +354,7 @@ def _prefill_embeds(model: ToyVLM, seq: TokenSequence, image_embeds) -> ReuseRes
     spec = RequestSpec(n=len(seq), text_pos=text_pos, text_ids=text_ids,
                        images=[(s.start, s.length) for s in segs], keep=keep, kv_hit=[False] * len(segs),
                        enc_src=[(SRC_SCRATCH, m * T) for m in range(len(segs))], page_rows=[None] * len(segs))
-    lay = build_layout([spec], L, cfg.num_heads)
+    lay = _layout(runner, [spec], L, cfg.num_heads)
     metrics = ReuseMetrics(mean_ratio=1.0)
     metrics.computed_per_layer = [len(seq)] * L
     ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))

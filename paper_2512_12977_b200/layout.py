@@ -63,6 +63,9 @@ class Layout:
     reloc_tokens: int             # total relocated token rows (all layers)
     page_table: np.ndarray        # int32 flat page ids referenced by reloc_descs
     # outputs
+    row_text: np.ndarray          # int32 [c0] index into the concatenated text ids (-1: image row)
+    row_img: np.ndarray           # int32 [c0] global image index (-1: text row)
+    row_t: np.ndarray             # int32 [c0] token index inside its image
     final_rows: np.ndarray        # int32 [c_L] packed rows in (req, pos) order
     positions: list               # per request: int64 positions with logits (reference `rows`)
     logit_ranges: list            # per request: (start, count) into the logits rows
@@ -84,12 +87,17 @@ class Layout:
 RELOC_TOK = 8
 
 
-def _depths(spec: RequestSpec, L: int):
-    """(positions, depth, src kind, src index) of every token computed at layer 0."""
+def _depths(spec: RequestSpec, L: int, text_base: int, img_base: int):
+    """(positions, depth, src kind, src index, text ref, image ref, t) of every token
+    computed at layer 0."""
+    nt = len(spec.text_pos)
     pos = [spec.text_pos.astype(np.int64)]
-    dep = [np.full(len(spec.text_pos), L, dtype=np.int64)]
-    kind = [np.full(len(spec.text_pos), SRC_TEXT, dtype=np.int64)]
+    dep = [np.full(nt, L, dtype=np.int64)]
+    kind = [np.full(nt, SRC_TEXT, dtype=np.int64)]
     idx = [spec.text_ids.astype(np.int64)]
+    tref = [text_base + np.arange(nt)]
+    iref = [np.full(nt, -1)]
+    tt = [np.zeros(nt, dtype=np.int64)]
     for m, (start, T) in enumerate(spec.images):
         k0 = int(spec.keep[0, m])
         if k0 == 0:
@@ -100,7 +108,10 @@ def _depths(spec: RequestSpec, L: int):
         dep.append(d)
         kind.append(np.full(k0, spec.enc_src[m][0], dtype=np.int64))
         idx.append(spec.enc_src[m][1] + t)
-    return (np.concatenate(pos), np.concatenate(dep), np.concatenate(kind), np.concatenate(idx))
+        tref.append(np.full(k0, -1))
+        iref.append(np.full(k0, img_base + m))
+        tt.append(t)
+    return tuple(np.concatenate(a) for a in (pos, dep, kind, idx, tref, iref, tt))
 
 
 def attention_work(q_ranges, qpos, n_req, heads, target_items: int):
@@ -138,13 +149,18 @@ def build_layout(specs: list[RequestSpec], L: int, heads: int, target_items: int
     R = len(specs)
     n_req = np.array([s.n for s in specs], dtype=np.int64)
     kvoff = np.concatenate([[0], np.cumsum(n_req)[:-1]]).astype(np.int64)
-    P, D, K, I, Q = [], [], [], [], []
+    cols = [[] for _ in range(8)]
+    tb = ib = 0
     for r, spec in enumerate(specs):
-        pos, dep, kind, idx = _depths(spec, L)
-        P.append(pos); D.append(dep); K.append(kind); I.append(idx); Q.append(np.full(len(pos), r))
-    pos, dep, kind, idx, req = (np.concatenate(a) for a in (P, D, K, I, Q))
+        parts = _depths(spec, L, tb, ib)
+        for k, a in enumerate(parts):
+            cols[k].append(a)
+        cols[7].append(np.full(len(parts[0]), r))
+        tb += len(spec.text_pos)
+        ib += len(spec.images)
+    pos, dep, kind, idx, tref, iref, tt, req = (np.concatenate(a) for a in cols)
     order = np.lexsort((pos, req, -dep))            # depth desc, then request, then position
-    pos, dep, kind, idx, req = pos[order], dep[order], kind[order], idx[order], req[order]
+    pos, dep, kind, idx, tref, iref, tt, req = (a[order] for a in (pos, dep, kind, idx, tref, iref, tt, req))
     c0 = len(pos)
     c = np.array([(dep > i).sum() for i in range(L)], dtype=np.int32)
     row_kv = kvoff[req] + pos
@@ -217,4 +233,35 @@ def build_layout(specs: list[RequestSpec], L: int, heads: int, target_items: int
                   reloc_blocks=np.array(blocks, dtype=np.int32).reshape(-1, 2),
                   reloc_layer_blocks=np.array(layer_blocks, dtype=np.int32), reloc_tokens=ntok_total,
                   page_table=(np.concatenate(pages) if pages else np.zeros(1, np.int32)).astype(np.int32),
+                  row_text=tref.astype(np.int32), row_img=iref.astype(np.int32), row_t=tt.astype(np.int32),
                   final_rows=final_rows, positions=positions, logit_ranges=logit_ranges)
+
+
+def structure_of(specs: list[RequestSpec], L: int, heads: int):
+    """Cache key of the launch structure of a batch (independent of ids and page ids)."""
+    key = [L, heads]
+    for s in specs:
+        key.append((s.n, np.asarray(s.text_pos, np.int64).tobytes(), tuple(s.images),
+                     np.asarray(s.keep, np.int32).tobytes(), tuple(bool(h) for h in s.kv_hit),
+                     tuple(int(k) for k, _ in s.enc_src),
+                     tuple(0 if p is None else np.asarray(p).shape[1] for p in s.page_rows)))
+    return tuple(key)
+
+
+def with_data(lay: Layout, specs: list[RequestSpec]) -> Layout:
+    """Copy of a cached structural layout carrying this batch's token ids, encoder rows
+    and store pages."""
+    import copy
+    out = copy.copy(lay)
+    text = np.concatenate([np.asarray(s.text_ids, np.int64) for s in specs]) if specs else np.zeros(0)
+    base = np.array([b for s in specs for _, b in s.enc_src], dtype=np.int64)
+    src = lay.row_src.copy()
+    t_rows = lay.row_text >= 0
+    src[t_rows, 1] = text[lay.row_text[t_rows]]
+    i_rows = ~t_rows
+    src[i_rows, 1] = base[lay.row_img[i_rows]] + lay.row_t[i_rows]
+    out.row_src = src
+    pages = [np.asarray(s.page_rows[m], np.int32).reshape(-1) for s in specs
+             for m in range(len(s.images)) if s.kv_hit[m]]
+    out.page_table = np.concatenate(pages) if pages else np.zeros(1, np.int32)
+    return out

@@ -77,7 +77,9 @@ class IntPack:
 
     def upload(self, ws: Workspace, key: str):
         torch = _torch()
-        host = np.concatenate(self.parts) if self.parts else np.zeros(4, np.int32)
+        host = getattr(self, "host", None)
+        if host is None:
+            host = np.concatenate(self.parts) if self.parts else np.zeros(4, np.int32)
         dev = ws.get(key, (max(4, host.size),), torch.int32, zero=False)
         pinned = torch.from_numpy(host).pin_memory()
         dev[:host.size].copy_(pinned, non_blocking=True)
@@ -110,6 +112,7 @@ class Runner:
         self.counters = self.ws.get("counters", (1 << 16,), torch.int32)
         self.launches = 0          # kernels issued by this runner (all entry points)
         self.graphs: dict = {}     # structure key -> captured CUDA graph of the prefill chain
+        self.layouts: dict = {}    # structure key -> Layout (engine._layout)
         self.graph_launches: dict = {}
         self.tracer = None         # list -> (name, ev0, ev1, algo_bytes, algo_flops) per launch
 
@@ -250,20 +253,7 @@ class Runner:
         ws.get("attn_ws_o", (max(1, lay.attn_slots) * 128 * hd,), torch.float32, zero=False)
         ws.get("attn_ws_ml", (max(1, lay.attn_slots) * 256,), torch.float32, zero=False)
 
-        pack = IntPack()
-        pack.add("src", lay.row_src)
-        pack.add("row_pos", lay.row_pos)
-        pack.add("row_kv", lay.row_kv)
-        for i in range(L):
-            pack.add(f"qdst{i}", lay.qdst[i])
-            pack.add(f"qpos{i}", lay.qpos[i])
-            pack.add(f"rowof{i}", lay.rowof[i])
-            pack.add(f"items{i}", lay.attn_items[i])
-            pack.add(f"comb{i}", lay.comb_items[i] if len(lay.comb_items[i]) else np.zeros(8))
-        pack.add("descs", lay.reloc_descs if len(lay.reloc_descs) else np.zeros(8))
-        pack.add("blocks", lay.reloc_blocks if len(lay.reloc_blocks) else np.zeros(2))
-        pack.add("pages", lay.page_table)
-        pack.add("final", lay.final_rows)
+        pack = self._pack(lay)
         pack.upload(ws, "ints")
         ptrs = (enc_store_rows.data_ptr() if enc_store_rows is not None else 0,
                 enc_scratch_rows.data_ptr() if enc_scratch_rows is not None else 0,
@@ -276,7 +266,10 @@ class Runner:
         if events is not None:
             events[0].record()
         if use_graph and self.tracer is None:
-            key = (lay.structure_key(), ptrs, tuple(pack.off.items()))
+            skey = getattr(lay, "_skey", None)
+            if skey is None:
+                skey = lay._skey = lay.structure_key()
+            key = (skey, ptrs)
             g = self.graphs.get(key)
             if g is None:
                 chain()                                   # eager run serves this call
@@ -302,6 +295,37 @@ class Runner:
             events[1].record()
         return {"logits": buf["logits"], "kc": buf["kc"], "vc": buf["vc"], "kpre": buf["kpre"],
                 "R": buf["kpre"].shape[1], "KVR": buf["kc"].shape[1], "pack": pack}
+
+    @staticmethod
+    def _pack(lay: Layout) -> "IntPack":
+        """int32 arrays of the launch chain in one host buffer.  The structural part is built
+        once per layout and cached on it; only token ids and page ids change per call."""
+        tpl = getattr(lay, "_pack_tpl", None)
+        if tpl is None:
+            pk = IntPack()
+            pk.add("src", lay.row_src)
+            pk.add("row_pos", lay.row_pos)
+            pk.add("row_kv", lay.row_kv)
+            for i in range(lay.L):
+                pk.add(f"qdst{i}", lay.qdst[i])
+                pk.add(f"qpos{i}", lay.qpos[i])
+                pk.add(f"rowof{i}", lay.rowof[i])
+                pk.add(f"items{i}", lay.attn_items[i])
+                pk.add(f"comb{i}", lay.comb_items[i] if len(lay.comb_items[i]) else np.zeros(8))
+            pk.add("descs", lay.reloc_descs if len(lay.reloc_descs) else np.zeros(8))
+            pk.add("blocks", lay.reloc_blocks if len(lay.reloc_blocks) else np.zeros(2))
+            pk.add("pages", lay.page_table)
+            pk.add("final", lay.final_rows)
+            tpl = lay._pack_tpl = (np.concatenate(pk.parts), dict(pk.off))
+        host, off = tpl
+        host = host.copy()
+        o, n = off["src"]
+        host[o:o + n] = lay.row_src.reshape(-1)
+        o, n = off["pages"]
+        host[o:o + n] = lay.page_table.reshape(-1)
+        pk = IntPack()
+        pk.host, pk.off = host, off
+        return pk
 
     def _chain(self, lay: Layout, pack: "IntPack", buf: dict, ptrs):
         cfg, dw = self.cfg, self.dw
