@@ -89,6 +89,13 @@ int vlc_store_write_pages_impl(const void*, int, int, int, int, const int*, int,
 int vlc_patchify_impl(const float*, int, int, void*, int, cudaStream_t);
 
 const char* vlc_last_error(void) { return g_err; }
+
+namespace vlc { extern int g_stage_override; }
+/* Experiment knobs (not part of the stable ABI): key 1 = GEMM pipeline stages (0 = auto). */
+int vlc_set_tuning(int key, int value) {
+  if (key == 1) { vlc::g_stage_override = value; return VLC_OK; }
+  return fail(VLC_ERR_INVALID, "set_tuning: unknown key");
+}
 int vlc_version(void) { return 100; }
 
 int vlc_embed_assemble(float* x, int ldx, const void* embed_bf16, int d, const float* enc_a, const float* enc_b,

@@ -287,7 +287,10 @@ int gemm_smem_bytes(int n_tile, int stages) {
   return 1024 + stages * (GEMM_BM * GEMM_BK * 2 + n_tile * GEMM_BK * 2) + (2 * stages + 1) * 8 + 16;
 }
 
+int g_stage_override = 0;
+
 int gemm_pick_stages(int n_tile) {
+  if (g_stage_override > 0) return g_stage_override;
   const int per = GEMM_BM * GEMM_BK * 2 + n_tile * GEMM_BK * 2;
   int s = (200 * 1024) / per;
   if (s > 8) s = 8;
