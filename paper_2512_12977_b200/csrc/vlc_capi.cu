@@ -90,7 +90,6 @@ int vlc_patchify_impl(const float*, int, int, void*, int, cudaStream_t);
 
 const char* vlc_last_error(void) { return g_err; }
 
-namespace vlc { extern int g_stage_override; }
 /* Experiment knobs (not part of the stable ABI): key 1 = GEMM pipeline stages (0 = auto). */
 int vlc_set_tuning(int key, int value) {
   if (key == 1) { vlc::g_stage_override = value; return VLC_OK; }

@@ -20,6 +20,8 @@ enum EpiKind {
 
 using GemmEpi = vlc_epilogue;
 
+extern int g_stage_override;  // experiment knob (vlc_set_tuning key 1)
+
 // tensor maps (driver entry point resolved through the runtime, no -lcuda)
 cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                          uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer,
