@@ -111,9 +111,13 @@ int vlc_store_write_pages(const void* src, int src_f32, int layers, int tokens, 
                           int page_tokens, cudaStream_t stream);
 
 /* Fused-epilogue tcgen05 GEMM: acc[f][j] = sum_k W[f][k] X[j][k]; W bf16 [n_pad][k_pad]
- * K-major, X bf16 [x_rows_cap][k_pad].  n_pad % 128 == 0, k_pad % 64 == 0. */
+ * K-major, X bf16 [x_rows_cap][k_pad].  n_pad % 128 == 0, k_pad % 64 == 0.
+ * Stream-K schedule over (128-row weight tile x token tile x 64-wide k-block) units on
+ * max_ctas co-resident CTAs (0 = one per SM); tiles shared by several CTAs are reduced in
+ * parallel through `ws` (>= ctas*8*128*256 floats) with `counters` (>= 2*ctas ints, zeroed
+ * once; the kernel leaves them zeroed).  Replaces engine.py:176-178, 183-185, 187. */
 int vlc_gemm_bf16(const void* w, int n_pad, int k_pad, const void* x, int x_rows_cap,
-                  int m_tokens, const vlc_epilogue* epi, int splits, float* ws, size_t ws_bytes,
+                  int m_tokens, const vlc_epilogue* epi, int max_ctas, float* ws, size_t ws_bytes,
                   int* counters, cudaStream_t stream);
 
 int vlc_attn_mixed(const vlc_attn_args* args, cudaStream_t stream);

@@ -134,7 +134,7 @@ int vlc_store_write_pages(const void* src, int src_f32, int layers, int tokens, 
 }
 
 int vlc_gemm_bf16(const void* w, int n_pad, int k_pad, const void* x, int x_rows_cap, int m_tokens,
-                  const vlc_epilogue* epi, int splits, float* ws, size_t ws_bytes, int* counters,
+                  const vlc_epilogue* epi, int max_ctas, float* ws, size_t ws_bytes, int* counters,
                   cudaStream_t stream) {
   if (!w || !x || !epi) return fail(VLC_ERR_INVALID, "gemm: null pointer");
   if (n_pad % 128 || k_pad % 64 || n_pad <= 0 || k_pad <= 0)
@@ -144,7 +144,7 @@ int vlc_gemm_bf16(const void* w, int n_pad, int k_pad, const void* x, int x_rows
   if (epi->m_tokens != m_tokens) return fail(VLC_ERR_INVALID, "gemm: epilogue m_tokens mismatch");
   if (epi->kind == VLC_EPI_QKV_ROPE && (!epi->map2 || !epi->pos || !epi->cos_tab || epi->hd % 2))
     return fail(VLC_ERR_INVALID, "gemm: QKV_ROPE needs map2/pos/tables");
-  return cuda_status(launch_gemm(w, n_pad, k_pad, x, x_rows_cap, m_tokens, *epi, splits, ws, ws_bytes, counters,
+  return cuda_status(launch_gemm(w, n_pad, k_pad, x, x_rows_cap, m_tokens, *epi, max_ctas, ws, ws_bytes, counters,
                                  stream),
                      "gemm_bf16");
 }

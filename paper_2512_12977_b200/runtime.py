@@ -134,7 +134,7 @@ class Runner:
         if m <= 0:
             return
         if splits is None:
-            splits = pick_splits(w.shape[0], k_pad, m)
+            splits = 0                       # stream-K over all SMs
         epi.m_tokens = m
         kv_ = k_valid or k_pad
         nbytes = 2 * epi.n_valid * kv_ + 2 * m * kv_

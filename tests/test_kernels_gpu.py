@@ -32,7 +32,7 @@ def _epi(nat, **kw):
 
 
 def _gemm(nat, W, X, m, epi, splits=1):
-    ws = torch.zeros(64 << 20, dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
     cnt = torch.zeros(4096, dtype=torch.int32, device="cuda")
     nat.check(nat.load().vlc_gemm_bf16(W.data_ptr(), W.shape[0], W.shape[1], X.data_ptr(), X.shape[0], m,
                                        epi, splits, ws.data_ptr(), ws.numel(), cnt.data_ptr(), _stream()),
@@ -41,7 +41,9 @@ def _gemm(nat, W, X, m, epi, splits=1):
 
 
 @pytest.mark.parametrize("n_pad,k_pad,m,splits", [(128, 64, 16, 1), (256, 128, 40, 1), (384, 512, 100, 3),
-                                                  (256, 256, 300, 2), (128, 1024, 256, 4), (512, 192, 1000, 1)])
+                                                  (256, 256, 300, 2), (128, 1024, 256, 4), (512, 192, 1000, 1),
+                                                  (3584, 3584, 236, 0), (1024, 7168, 112, 0), (10752, 3584, 240, 0),
+                                                  (1280, 640, 600, 7), (512, 4096, 40, 0)])
 def test_gemm_f32_matches_torch(nat, n_pad, k_pad, m, splits):
     g = torch.Generator(device="cuda").manual_seed(n_pad + m)
     W = torch.randn(n_pad, k_pad, device="cuda", generator=g).bfloat16()

@@ -45,17 +45,12 @@ def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20):
 
 
 if __name__ == "__main__":
-    for m in (16, 64, 128, 240):
-        run(14336, 3584, m, 1)
-    for st in (2, 3, 4):
-        run(14336, 3584, 240, 1, stages=st)
-    run(14336, 3584, 240, 1, kind=N.EPI_RESID)
-    run(14336, 3584, 240, 1, kind=N.EPI_F32)
-    for sp in (1, 2, 4, 5, 8):
-        run(3584, 3584, 240, sp)
-    for sp in (1, 2, 4):
-        run(10752, 3584, 240, sp)
-    run(3584, 7168, 240, 4)
-    run(152064, 3584, 236, 1)
-    run(14336, 3584, 4128, 1)
-    run(10752, 3584, 4128, 1)
+    for m in (16, 112, 240):
+        for n, k in ((14336, 3584), (10752, 3584), (3584, 3584), (3584, 7168)):
+            run(n, k, m, 0, kind=N.EPI_RESID if n == 3584 else N.EPI_BF16)
+    for st in (3, 4):
+        run(14336, 3584, 240, 0, stages=st)
+    run(152064, 3584, 236, 0, kind=N.EPI_F32)
+    run(14336, 3584, 4128, 0)
+    run(10752, 3584, 4128, 0)
+    run(3584, 7168, 4128, 0, kind=N.EPI_RESID)
