@@ -25,116 +25,87 @@ constexpr int GEMM_BK = 64;
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g)); }
 
-__device__ __forceinline__ void store_bf16(void* base, long idx, float v) {
-  reinterpret_cast<__nv_bfloat16*>(base)[idx] = __float2bfloat16_rn(v);
+__device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) {
+  return make_uint2(pack_bf16(a, b), pack_bf16(c, d));
 }
 
-// Apply the epilogue to 16 consecutive token columns (j0 .. j0+15) of this thread's
-// weight row f.  Per-token metadata is fetched once per warp (lane i loads token j0+i,
-// then broadcast with shuffles) and every global load of the chunk is issued before
-// any store, so the chunk costs ~one memory round trip instead of sixteen.
-__device__ __forceinline__ void epilogue_chunk(const GemmEpi& e, int f, int j0, const float* v) {
-  const unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const int hb = lane & 16;  // metadata of token j0+i lives in lane hb+i (half-warps may differ in j0)
-  const int jl = j0 + (lane & 15);
-  const bool jl_ok = jl < e.m_tokens;
-  const int m1_l = (e.map1 && jl_ok) ? __ldg(e.map1 + jl) : jl;
-  const int m2_l = (e.map2 && jl_ok) ? __ldg(e.map2 + jl) : jl;
-  const int ps_l = (e.pos && jl_ok) ? __ldg(e.pos + jl) : 0;
-  const int nv = min(16, e.m_tokens - j0);
-  const bool row_ok = f < e.n_valid;
+// Final values of 4 consecutive DEVICE features [F, F+4) of token j (token-major group).
+// Device feature order: q/k rows permuted so RoPE pairs are adjacent (F, F+1), gate/up
+// interleaved (gate f at 2f, up f at 2f+1); see model.py DeviceWeights.
+__device__ __forceinline__ void write_group(const GemmEpi& e, int F, int j, float4 v) {
+  if (F >= e.n_valid) return;
+  const bool full4 = F + 4 <= e.n_valid;
   switch (e.kind) {
     case EPI_F32: {
-      float* __restrict__ o = reinterpret_cast<float*>(e.out) + f;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int r = __shfl_sync(FULL, m1_l, hb + i);
-        if (row_ok && i < nv) o[(long)r * e.ldo] = v[i];
+      const long r = e.map1 ? __ldg(e.map1 + j) : j;
+      float* o = reinterpret_cast<float*>(e.out) + r * e.ldo + F;
+      if (full4 && (e.ldo & 3) == 0) {
+        *reinterpret_cast<float4*>(o) = v;
+      } else {
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+        for (int i = 0; i < 4 && F + i < e.n_valid; ++i) o[i] = vv[i];
       }
       break;
     }
     case EPI_RESID: {
-      float* __restrict__ o = reinterpret_cast<float*>(e.out) + f;
-      float old[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) old[i] = (row_ok && i < nv) ? o[(long)(j0 + i) * e.ldo] : 0.f;
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (row_ok && i < nv) o[(long)(j0 + i) * e.ldo] = old[i] + v[i];
+      float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (long)j * e.ldo + F);
+      const float4 x = *o;
+      *o = make_float4(x.x + v.x, x.y + v.y, x.z + v.z, x.w + v.w);
       break;
     }
-    case EPI_BF16: {
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (row_ok && i < nv) store_bf16(e.out, (long)(j0 + i) * e.ldo + f, v[i]);
+    case EPI_BF16:
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(e.out) + (long)j * e.ldo + F) =
+          pack4_bf16(v.x, v.y, v.z, v.w);
       break;
-    }
     case EPI_BIAS_ADD: {
-      const float b = (e.bias && row_ok) ? __ldg(e.bias + f) : 0.f;
-      float a[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        a[i] = (e.add && row_ok && i < nv) ? __ldg(e.add + (long)(j0 + i) * e.ld_add + f) : 0.f;
-      float* __restrict__ o = reinterpret_cast<float*>(e.out) + f;
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (row_ok && i < nv) o[(long)(j0 + i) * e.ldo] = (v[i] + b) + a[i];
+      float4 b = e.bias ? __ldg(reinterpret_cast<const float4*>(e.bias + F)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 a = e.add ? __ldg(reinterpret_cast<const float4*>(e.add + (long)j * e.ld_add + F))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (long)j * e.ldo + F) =
+          make_float4((v.x + b.x) + a.x, (v.y + b.y) + a.y, (v.z + b.z) + a.z, (v.w + b.w) + a.w);
       break;
     }
-    case EPI_SWIGLU: {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float up = __shfl_xor_sync(FULL, v[i], 1);
-        if (row_ok && i < nv && (f & 1) == 0) store_bf16(e.out, (long)(j0 + i) * e.ldo + (f >> 1), silu_f(v[i]) * up);
-      }
+    case EPI_SWIGLU:
+      *reinterpret_cast<uint32_t*>(reinterpret_cast<__nv_bfloat16*>(e.out) + (long)j * e.ldo + (F >> 1)) =
+          pack_bf16(silu_f(v.x) * v.y, silu_f(v.z) * v.w);
       break;
-    }
     case EPI_QKV_PLAIN: {
-      const int sec = f / e.seg, r = f - sec * e.seg;
+      const int sec = F / e.seg, r = F - sec * e.seg;
       void* dst = sec == 0 ? e.out : sec == 1 ? e.out2 : e.out3;
       const int ld = sec == 0 ? e.ldo : sec == 1 ? e.ld2 : e.ld3;
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (row_ok && i < nv) store_bf16(dst, (long)(j0 + i) * ld + r, v[i]);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(dst) + (long)j * ld + r) = pack4_bf16(v.x, v.y, v.z, v.w);
       break;
     }
     case EPI_QKV_ROPE: {
-      const int sec = f / e.seg, r = f - sec * e.seg;
-      float partner[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) partner[i] = __shfl_xor_sync(FULL, v[i], 1);
-      if (sec == 2) {  // V: not permuted, not rotated
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int kr = __shfl_sync(FULL, m2_l, hb + i);
-          if (row_ok && i < nv) store_bf16(e.out3, (long)kr * e.ld3 + r, v[i]);
-        }
+      const int sec = F / e.seg, r = F - sec * e.seg;
+      if (sec == 2) {
+        const long kr = __ldg(e.map2 + j);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(e.out3) + kr * e.ld3 + r) =
+            pack4_bf16(v.x, v.y, v.z, v.w);
         break;
       }
       const int half = e.hd >> 1;
-      const int head = r / e.hd, w = r - head * e.hd, t = w >> 1, odd = w & 1;
-      const int feat = head * e.hd + (odd ? t + half : t);
-      float c[16], sn[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int p = __shfl_sync(FULL, ps_l, hb + i);
-        const long tab = (long)p * e.tab_ld + t;
-        c[i] = row_ok ? __ldg(e.cos_tab + tab) : 0.f;
-        sn[i] = row_ok ? __ldg(e.sin_tab + tab) : 0.f;
-      }
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float a = odd ? partner[i] : v[i], b = odd ? v[i] : partner[i];
-        const float rot = odd ? (b * c[i] + a * sn[i]) : (a * c[i] - b * sn[i]);
-        const int q_row = __shfl_sync(FULL, m1_l, hb + i);
-        const int kv_row = __shfl_sync(FULL, m2_l, hb + i);
-        if (!(row_ok && i < nv)) continue;
-        if (sec == 0) {
-          store_bf16(e.out, (long)q_row * e.ldo + feat, rot);
-        } else {
-          if (e.out4) store_bf16(e.out4, (long)(j0 + i) * e.ld4 + feat, v[i]);
-          store_bf16(e.out2, (long)kv_row * e.ld2 + feat, rot);
+      const int head = r / e.hd, t = (r - head * e.hd) >> 1;   // pairs (t, t+half), (t+1, t+1+half)
+      const long tab = (long)__ldg(e.pos + j) * e.tab_ld + t;
+      const float2 c = __ldg(reinterpret_cast<const float2*>(e.cos_tab + tab));
+      const float2 sn = __ldg(reinterpret_cast<const float2*>(e.sin_tab + tab));
+      const uint32_t lo = pack_bf16(v.x * c.x - v.y * sn.x, v.z * c.y - v.w * sn.y);
+      const uint32_t hi = pack_bf16(v.y * c.x + v.x * sn.x, v.w * c.y + v.z * sn.y);
+      const int fa = head * e.hd + t;
+      if (sec == 0) {
+        const long qr = e.map1 ? __ldg(e.map1 + j) : j;
+        __nv_bfloat16* q = reinterpret_cast<__nv_bfloat16*>(e.out) + qr * e.ldo;
+        *reinterpret_cast<uint32_t*>(q + fa) = lo;
+        *reinterpret_cast<uint32_t*>(q + fa + half) = hi;
+      } else {
+        const long kr = __ldg(e.map2 + j);
+        __nv_bfloat16* k = reinterpret_cast<__nv_bfloat16*>(e.out2) + kr * e.ld2;
+        *reinterpret_cast<uint32_t*>(k + fa) = lo;
+        *reinterpret_cast<uint32_t*>(k + fa + half) = hi;
+        if (e.out4) {
+          __nv_bfloat16* kp = reinterpret_cast<__nv_bfloat16*>(e.out4) + (long)j * e.ld4;
+          *reinterpret_cast<uint32_t*>(kp + fa) = pack_bf16(v.x, v.z);
+          *reinterpret_cast<uint32_t*>(kp + fa + half) = pack_bf16(v.y, v.w);
         }
       }
       break;
@@ -161,6 +132,14 @@ struct SkSched {
 
 constexpr int SK_MAX_PART = 8;  // participants per split tile
 
+__device__ unsigned long long* g_dbg = nullptr;  // phase timestamps (experiments only)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define DBG(slot) do { if (g_dbg) g_dbg[blockIdx.x * 8 + (slot)] = gtimer(); } while (0)
+
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
                  GemmEpi epi, SkSched sk, int n_tile, int stages, float* ws, int* counters) {
@@ -175,6 +154,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* acc_full = empty + stages;   // [2]
   uint64_t* acc_empty = acc_full + 2;    // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  float* stage_buf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(acc_empty) + 64);  // [32][128] fp32
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int g = blockIdx.x;
@@ -183,6 +163,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int t_last = (u_end > u_begin) ? (int)((u_end - 1) / sk.KB) : t_first - 1;
 
   if (warp == 0 && lane == 0) {
+    DBG(0);
     tma_prefetch(&map_w);
     tma_prefetch(&map_x);
     for (int s = 0; s < stages; ++s) {
@@ -203,6 +184,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      DBG(1);
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
       int stage = 0;
@@ -219,6 +201,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
       }
+      DBG(2);
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -253,10 +236,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     __syncwarp();
   } else {
     // ---------------- epilogue warps 2..5 (threads 64..191)
+    // TMEM (thread = weight row) -> smem stage [32 tokens][128 rows] -> token-major float4
+    // groups written coalesced (write_group), or raw partial rows for split tiles.
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const int nchunks = n_tile / 16;
     int seg = 0;
     for (int t = t_first; t <= t_last; ++t, ++seg) {
       const long long tb = (long long)t * sk.KB;
@@ -265,34 +249,42 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int slot = seg & 1;
       mbar_wait(&acc_full[slot], (seg >> 1) & 1);
       tc_fence_after();
+      if (threadIdx.x == 64) DBG(3);
       const uint32_t d = tmem + slot * 256 + lane_off;
-      if (gf == gl) {
-        for (int c = 0; c < nchunks; ++c) {
-          float v[16];
-          tmem_ld16(d + c * 16, v);
-          tmem_wait_ld();
-          epilogue_chunk(epi, m0 + row, tok0 + c * 16, v);
+      const bool split = gf != gl;
+      float* part = split ? ws + ((long)gf * SK_MAX_PART + (g - gf)) * (long)n_tile * GEMM_BM : nullptr;
+      for (int c = 0; c < n_tile; c += 32) {
+        float v[32];
+        tmem_ld32(d + c, v);
+        tmem_wait_ld();
+        if (c + 32 >= n_tile) {  // last TMEM read of this accumulator: release it to the MMA warp
+          tc_fence_before();
+          mbar_arrive(&acc_empty[slot]);
         }
-        tc_fence_before();
-        mbar_arrive(&acc_empty[slot]);
-      } else {
-        float* part = ws + (((long)gf * SK_MAX_PART + (g - gf)) * GEMM_BM + row) * (long)n_tile;
-        for (int c = 0; c < nchunks; ++c) {
-          float v[16];
-          tmem_ld16(d + c * 16, v);
-          tmem_wait_ld();
-          float4* dst = reinterpret_cast<float4*>(part + c * 16);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) __stcg(dst + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+        for (int jj = 0; jj < 32; ++jj) stage_buf[jj * 128 + row] = v[jj];
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (int jj = quad; jj < 32; jj += 4) {
+          const int jt = c + jj;   // token index inside the tile
+          if (jt >= n_tile) break;
+          const float4 val = *reinterpret_cast<const float4*>(stage_buf + jj * 128 + 4 * lane);
+          if (split) {
+            __stcg(reinterpret_cast<float4*>(part + (long)jt * GEMM_BM) + lane, val);
+          } else if (tok0 + jt < epi.m_tokens) {
+            write_group(epi, m0 + 4 * lane, tok0 + jt, val);
+          }
         }
-        tc_fence_before();
-        mbar_arrive(&acc_empty[slot]);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+      if (split) {
         __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (threadIdx.x == 64) atomicAdd(&counters[2 * gf], 1);
       }
     }
-    // ---- parallel fixup of the split tiles this CTA touched (first and/or last segment)
+    if (threadIdx.x == 64) DBG(4);
+    // ---- parallel fixup of the split tiles this CTA touched: participant p of nseg owns a
+    // contiguous token range of the tile; partials are token-major rows of 128 fp32.
     for (int t = t_first; t <= t_last; ++t) {
       const long long tb = (long long)t * sk.KB;
       const int gf = sk.cta_of(tb), gl = sk.cta_of(tb + sk.KB - 1);
@@ -300,36 +292,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int nseg = gl - gf + 1, p = g - gf;
       if (threadIdx.x == 64) {
         volatile int* cnt = counters + 2 * gf;
-        while (*cnt < nseg) __nanosleep(64);
+        while (*cnt < nseg) __nanosleep(32);
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       __threadfence();
+      if (threadIdx.x == 64) DBG(5);
       const int m0 = (t % sk.m_tiles) * GEMM_BM, tok0 = (t / sk.m_tiles) * n_tile;
-      const int u_lo = p * 8 / nseg, u_hi = (p + 1) * 8 / nseg;   // 16-row units owned by this CTA
-      const int nu = u_hi - u_lo;
-      const int total = nu * nchunks;
-      const int half = lane >> 4;
-      const float* base = ws + (long)gf * SK_MAX_PART * GEMM_BM * n_tile;
-      const long pstride = (long)GEMM_BM * n_tile;
-      for (int pr = quad; pr < (total + 1) / 2; pr += 4) {
-        const int w = 2 * pr + half;
-        const bool ok = w < total;
-        const int unit = u_lo + (ok ? w % nu : 0), chunk = ok ? w / nu : 0;
-        const int r = unit * 16 + (lane & 15);
-        float v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = 0.f;
-        if (ok) {
-          for (int s = 0; s < nseg; ++s) {
-            const float4* src = reinterpret_cast<const float4*>(base + s * pstride + (long)r * n_tile + chunk * 16);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float4 x = __ldcg(src + q);
-              v[4 * q] += x.x; v[4 * q + 1] += x.y; v[4 * q + 2] += x.z; v[4 * q + 3] += x.w;
-            }
-          }
+      const int j_lo = n_tile * p / nseg, j_hi = n_tile * (p + 1) / nseg;
+      const float* base = ws + (long)gf * SK_MAX_PART * n_tile * GEMM_BM;
+      const long pstride = (long)n_tile * GEMM_BM;
+      for (int jt = j_lo + quad; jt < j_hi; jt += 4) {
+        if (tok0 + jt >= epi.m_tokens) break;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int s2 = 0; s2 < nseg; ++s2) {
+          const float4 x = __ldcg(reinterpret_cast<const float4*>(base + s2 * pstride + (long)jt * GEMM_BM) + lane);
+          acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
         }
-        epilogue_chunk(epi, ok ? m0 + r : 0x7fffffff, tok0 + chunk * 16, v);
+        write_group(epi, m0 + 4 * lane, tok0 + jt, acc);
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (threadIdx.x == 64) {
@@ -340,27 +319,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   }
+  if (threadIdx.x == 64) DBG(6);
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
+  if (threadIdx.x == 0) DBG(7);
 }
 
 int g_stage_override = 0;
+void set_debug_buffer(unsigned long long* p) { cudaMemcpyToSymbol(g_dbg, &p, sizeof(p)); }
+int g_coop = 1;
 
 static int gemm_pick_stages(int n_tile) {
   if (g_stage_override > 0) return g_stage_override;
   const int per = GEMM_BM * GEMM_BK * 2 + n_tile * GEMM_BK * 2;
-  int s = (200 * 1024) / per;
+  int s = (200 * 1024 - 16 * 1024) / per;
   if (s > 8) s = 8;
   if (s < 2) s = 2;
   return s;
 }
 
 static int gemm_smem_bytes(int n_tile, int stages) {
-  return 1024 + stages * (GEMM_BM * GEMM_BK * 2 + n_tile * GEMM_BK * 2) + (2 * stages + 4) * 8 + 16;
+  // pipeline stages + barriers (64 B reserved) + 16 KB epilogue staging tile
+  return 1024 + stages * (GEMM_BM * GEMM_BK * 2 + n_tile * GEMM_BK * 2) + (2 * stages + 2) * 8 + 64 + 32 * 128 * 4;
 }
 
 static int num_sms() {
@@ -418,7 +402,7 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = g_coop ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, gemm_bf16_tc, mw, mx, epi, sk, n_tile, stages, ws, counters);
 }
 

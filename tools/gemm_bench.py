@@ -12,24 +12,26 @@ ws = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 cnt = torch.zeros(1 << 16, dtype=torch.int32, device="cuda")
 
 
-def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20):
-    W = torch.randn(n, k, device="cuda").bfloat16()
+def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1):
+    nw = max(2, min(8, (1 << 30) // (n * k * 2)))   # rotate > L2 worth of weights
+    Ws = [torch.randn(n, k, device="cuda").bfloat16() for _ in range(nw)]
     X = torch.randn(max(256, m + 256), k, device="cuda").bfloat16()
     out = torch.zeros(m + 256, n, device="cuda", dtype=torch.float32)
     e = N.Epilogue()
     e.kind, e.n_valid, e.m_tokens, e.out, e.ldo = kind, n, m, out.data_ptr(), n
     lib.vlc_set_tuning(1, stages)
+    lib.vlc_set_tuning(2, coop)
     s = torch.cuda.current_stream().cuda_stream
 
-    def go():
+    def go(W):
         N.check(lib.vlc_gemm_bf16(W.data_ptr(), n, k, X.data_ptr(), X.shape[0], m, e, splits, ws.data_ptr(),
                                   ws.numel() * 4, cnt.data_ptr(), torch.cuda.current_stream().cuda_stream), "g")
-    go()
+    go(Ws[0])
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
-        for _ in range(reps):
-            go()
+        for r in range(reps):
+            go(Ws[r % nw])
     g.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
@@ -40,17 +42,56 @@ def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20):
     us = e0.elapsed_time(e1) * 1e3 / reps
     gbs = (n * k * 2 + m * k * 2) / us / 1e3
     tf = 2 * n * k * m / us / 1e6
-    print(f"N={n:6d} K={k:5d} M={m:4d} splits={splits} kind={kind} stages={stages}: {us:8.2f} us  "
+    print(f"N={n:6d} K={k:5d} M={m:4d} ctas={splits} coop={coop} kind={kind} st={stages}: {us:8.2f} us  "
           f"{gbs:7.1f} GB/s  {tf:7.1f} TF/s", flush=True)
 
 
+def phases(n, k, m, ctas):
+    """Per-CTA phase timestamps of one launch (DRAM-cold weights)."""
+    W = torch.randn(n, k, device="cuda").bfloat16()
+    X = torch.randn(max(256, m + 256), k, device="cuda").bfloat16()
+    out = torch.zeros(m + 256, n, device="cuda", dtype=torch.float32)
+    e = N.Epilogue()
+    e.kind, e.n_valid, e.m_tokens, e.out, e.ldo = N.EPI_BF16, n, m, out.data_ptr(), n
+    dbg = torch.zeros(148 * 8, dtype=torch.int64, device="cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    for it in range(3):
+        flush.add_(1)
+        lib.vlc_set_debug_buffer(dbg.data_ptr() if it == 2 else None)
+        N.check(lib.vlc_gemm_bf16(W.data_ptr(), n, k, X.data_ptr(), X.shape[0], m, e, ctas, ws.data_ptr(),
+                                  ws.numel() * 4, cnt.data_ptr(), torch.cuda.current_stream().cuda_stream), "g")
+        torch.cuda.synchronize()
+    lib.vlc_set_debug_buffer(None)
+    d = dbg.view(148, 8).cpu().numpy().astype("float64")
+    g = d[:, 0] > 0
+    d = d[g]
+    t0 = d[:, 0].min()
+    d = np.where(d > 0, (d - t0) / 1e3, -1.0)
+    names = ["start", "prod_go", "prod_done", "acc_full(last)", "partials_done", "fixup_go", "epi_end", "exit"]
+    print(f"--- N={n} K={k} M={m} ctas={ctas}: {len(d)} CTAs; us rel. to first start")
+    for i, nm in enumerate(names):
+        col = d[:, i]
+        col = col[col >= 0]
+        if not len(col):
+            continue
+        print(f"  {nm:16s} min {col.min():7.2f} med {np.median(col):7.2f} max {col.max():7.2f}")
+
+
 if __name__ == "__main__":
-    for m in (16, 112, 240):
-        for n, k in ((14336, 3584), (10752, 3584), (3584, 3584), (3584, 7168)):
-            run(n, k, m, 0, kind=N.EPI_RESID if n == 3584 else N.EPI_BF16)
-    for st in (3, 4):
-        run(14336, 3584, 240, 0, stages=st)
-    run(152064, 3584, 236, 0, kind=N.EPI_F32)
-    run(14336, 3584, 4128, 0)
-    run(10752, 3584, 4128, 0)
-    run(3584, 7168, 4128, 0, kind=N.EPI_RESID)
+    import numpy as np  # noqa: F811
+    mode = sys.argv[1] if len(sys.argv) > 1 else "sweep"
+    if mode == "phases":
+        for (n, kk, m, c) in ((3584, 3584, 16, 28), (3584, 3584, 16, 148), (3584, 3584, 240, 28),
+                              (3584, 3584, 240, 148), (14336, 3584, 240, 112), (14336, 3584, 240, 148)):
+            phases(n, kk, m, c)
+    elif mode == "ctas":
+        for (n, k) in ((14336, 3584), (10752, 3584), (3584, 3584), (3584, 7168)):
+            for m in (16, 240):
+                for ctas in sorted({n // 128, 74, 148}):
+                    run(n, k, m, ctas)
+    else:
+        for m in (16, 112, 240):
+            for n, k in ((14336, 3584), (10752, 3584), (3584, 3584), (3584, 7168)):
+                run(n, k, m, 0, kind=N.EPI_RESID if n == 3584 else N.EPI_BF16)
+        run(152064, 3584, 236, 0, kind=N.EPI_F32)
+        run(14336, 3584, 4128, 0)
