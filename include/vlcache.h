@@ -78,7 +78,15 @@ typedef struct vlc_attn_args {
   float* ws_o; float* ws_ml; int ws_slots;
   const int* comb; int n_comb;
   float scale_log2;                              /* log2(e) / sqrt(head_dim)          */
+  int* counters;                                 /* >= 2*ws_slots ints, zeroed (pp)   */
 } vlc_attn_args;
+
+/* Ping-pong attention (vlc_attn_pp): one CTA = up to 256 queries of one request and head
+ * (two 128-query tiles with their own softmax warpgroups sharing each K/V tile) over a key
+ * range.  Items int32[n][8] = {q_row0, n_q<=256, head, kv_row0, key_begin, key_end, group,
+ * (part << 8) | nsplit}; group < 0 writes normalised rows directly, otherwise the nsplit
+ * CTAs of a group merge their partials in parallel (all CTAs must be co-resident: the
+ * launch is cooperative when any group is split, so n_items <= #SMs then). */
 
 const char* vlc_last_error(void);
 int vlc_version(void);
@@ -123,6 +131,7 @@ int vlc_gemm_bf16(const void* w, int n_pad, int k_pad, const void* x, int x_rows
 
 int vlc_attn_mixed(const vlc_attn_args* args, cudaStream_t stream);
 int vlc_attn_combine(const vlc_attn_args* args, cudaStream_t stream);
+int vlc_attn_pp(const vlc_attn_args* args, cudaStream_t stream);
 
 /* Patchify (model.py:312-314): pixels f32 [side][side] -> bf16 [T][ldo] patches. */
 int vlc_patchify(const float* pixels, int side, int patch, void* out, int ldo,

@@ -17,7 +17,7 @@ VLC_OK, VLC_ERR_INVALID, VLC_ERR_UNSUPPORTED, VLC_ERR_CUDA = 0, 1, 2, 3
 EPI_F32, EPI_RESID, EPI_BF16, EPI_BIAS_ADD, EPI_SWIGLU, EPI_QKV_PLAIN, EPI_QKV_ROPE = range(7)
 
 EXPORTS = ("vlc_last_error", "vlc_version", "vlc_embed_assemble", "vlc_rmsnorm", "vlc_kv_relocate",
-           "vlc_store_write_pages", "vlc_gemm_bf16", "vlc_attn_mixed", "vlc_attn_combine",
+           "vlc_store_write_pages", "vlc_gemm_bf16", "vlc_attn_mixed", "vlc_attn_combine", "vlc_attn_pp",
            "vlc_patchify", "vlc_set_tuning", "vlc_set_debug_buffer")
 
 
@@ -42,7 +42,8 @@ class AttnArgs(C.Structure):
                 ("items", C.c_void_p), ("n_items", C.c_int), ("qpos", C.c_void_p),
                 ("rowof", C.c_void_p), ("out", C.c_void_p), ("ldo", C.c_int),
                 ("ws_o", C.c_void_p), ("ws_ml", C.c_void_p), ("ws_slots", C.c_int),
-                ("comb", C.c_void_p), ("n_comb", C.c_int), ("scale_log2", C.c_float)]
+                ("comb", C.c_void_p), ("n_comb", C.c_int), ("scale_log2", C.c_float),
+                ("counters", C.c_void_p)]
 
 
 _lib = None
@@ -65,6 +66,7 @@ def load():
         lib.vlc_gemm_bf16.argtypes = [vp, i, i, vp, i, i, C.POINTER(Epilogue), i, vp, C.c_size_t, vp, vp]
         lib.vlc_attn_mixed.argtypes = [C.POINTER(AttnArgs), vp]
         lib.vlc_attn_combine.argtypes = [C.POINTER(AttnArgs), vp]
+        lib.vlc_attn_pp.argtypes = [C.POINTER(AttnArgs), vp]
         lib.vlc_patchify.argtypes = [vp, i, i, vp, i, vp]
         lib.vlc_set_tuning.argtypes = [i, i]
         lib.vlc_set_debug_buffer.argtypes = [vp]

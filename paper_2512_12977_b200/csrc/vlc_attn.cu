@@ -322,6 +322,368 @@ static cudaError_t launch_attn_hd(const vlc_attn_args& a, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// ===================================================================== ping-pong kernel
+// CTA = (request, head, key range) for up to 256 queries = two 128-query tiles A and B.
+// Warp 0: TMA (Q once, then 64-key K/V tiles through a 3-stage ring); warp 1: tcgen05.mma
+// issue; warps 2-5 softmax A, warps 6-9 softmax B.  While one group runs its softmax the
+// tensor core works on the other group's S / PV.  TMEM: S_A, S_B (64 cols fp32), P_A, P_B
+// (32 cols of packed bf16 pairs, the A operand of the PV MMA), O_A, O_B (HD cols fp32).
+constexpr int PP_THREADS = 320;
+constexpr int PP_KT = 64;
+constexpr int PP_ST = 3;
+
+template <int HD>
+struct PPCfg {
+  static constexpr int ATOM_E = HD < 64 ? HD : 64;
+  static constexpr int SWZ = ATOM_E * 2;
+  static constexpr int N_ATOMS = HD / ATOM_E;
+  static constexpr int Q_BYTES = 128 * HD * 2;
+  static constexpr int Q_ATOM = 128 * SWZ;
+  static constexpr int KV_BYTES = PP_KT * HD * 2;
+  static constexpr int KV_ATOM = PP_KT * SWZ;
+  static constexpr int SMEM = 1024 + 2 * Q_BYTES + PP_ST * 2 * KV_BYTES + 256;
+  __device__ static constexpr uint32_t s_col(int x) { return 64u * x; }
+  __device__ static constexpr uint32_t p_col(int x) { return 128u + 32u * x; }
+  __device__ static constexpr uint32_t o_col(int x) { return 256u + (uint32_t)(HD > 64 ? HD : 64) * x; }
+};
+
+template <int HD>
+__global__ void __launch_bounds__(PP_THREADS, 1)
+    attn_pp_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                   const __grid_constant__ CUtensorMap map_v, vlc_attn_args a) {
+  using C = PPCfg<HD>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                                   // [2][Q_BYTES]
+  uint8_t* sK = sQ + 2 * C::Q_BYTES;                    // [ST][KV_BYTES]
+  uint8_t* sV = sK + PP_ST * C::KV_BYTES;               // [ST][KV_BYTES]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + PP_ST * C::KV_BYTES);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + PP_ST;
+  uint64_t* s_full = kv_empty + PP_ST;   // [2]
+  uint64_t* p_full = s_full + 2;         // [2]
+  uint64_t* o_done = p_full + 2;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+
+  const int* it = a.items + blockIdx.x * 8;
+  const int q_row0 = it[0], nq = it[1], head = it[2], kv_row0 = it[3];
+  const int kb = it[4], ke = it[5], group = it[6];
+  const int part = it[7] >> 8, nsplit = it[7] & 0xff;
+  const int nq_t[2] = {min(nq, 128), max(0, nq - 128)};
+  int nt_t[2];
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    int e = -1;
+    if (nq_t[x] > 0) e = min(ke, a.qpos[q_row0 + x * 128 + nq_t[x] - 1] + 1);
+    nt_t[x] = e > kb ? (e - kb + PP_KT - 1) / PP_KT : 0;
+  }
+  const int nt = max(nt_t[0], nt_t[1]);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_k);
+    tma_prefetch(&map_v);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < PP_ST; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&s_full[x], 1);
+      mbar_init(&p_full[x], 128);
+      mbar_init(&o_done[x], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && nt > 0) {
+      const uint64_t pol_q = policy_evict_first();
+      const uint64_t pol_kv = policy_evict_normal();
+      mbar_expect_tx(q_full, (nq_t[1] > 0 ? 2 : 1) * C::Q_BYTES);
+      for (int x = 0; x < 2; ++x) {
+        if (nq_t[x] == 0) continue;
+#pragma unroll
+        for (int at = 0; at < C::N_ATOMS; ++at)
+          tma_load_2d(sQ + x * C::Q_BYTES + at * C::Q_ATOM, &map_q, q_full, head * HD + at * C::ATOM_E,
+                      q_row0 + x * 128, pol_q);
+      }
+      for (int j = 0; j < nt; ++j) {
+        const int st = j % PP_ST;
+        mbar_wait(&kv_empty[st], ((j / PP_ST) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], 2 * C::KV_BYTES);
+        const int krow = kv_row0 + kb + j * PP_KT;
+#pragma unroll
+        for (int at = 0; at < C::N_ATOMS; ++at) {
+          tma_load_3d(sK + st * C::KV_BYTES + at * C::KV_ATOM, &map_k, &kv_full[st], head * HD + at * C::ATOM_E,
+                      krow, a.layer, pol_kv);
+          tma_load_3d(sV + st * C::KV_BYTES + at * C::KV_ATOM, &map_v, &kv_full[st], head * HD + at * C::ATOM_E,
+                      krow, a.layer, pol_kv);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && nt > 0) {
+      const uint32_t idesc_s = make_idesc_bf16(128, PP_KT, 0, 0);
+      const uint32_t idesc_o = make_idesc_bf16(128, HD, 0, 1);
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int x, int j) {
+        const int st = j % PP_ST;
+        mbar_wait(&kv_full[st], (j / PP_ST) & 1);
+        tc_fence_after();
+        const uint32_t q_addr = smem_u32(sQ + x * C::Q_BYTES);
+        const uint32_t k_addr = smem_u32(sK + st * C::KV_BYTES);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const int at = (k * 16) / C::ATOM_E;
+          const uint32_t eoff = ((k * 16) % C::ATOM_E) * 2;
+          const uint64_t ad = make_sdesc(q_addr + at * C::Q_ATOM + eoff, 16, 8 * C::SWZ, C::SWZ);
+          const uint64_t bd = make_sdesc(k_addr + at * C::KV_ATOM + eoff, 16, 8 * C::SWZ, C::SWZ);
+          tc_mma_f16(tmem + C::s_col(x), ad, bd, idesc_s, k > 0 ? 1u : 0u);
+        }
+        tc_commit(&s_full[x]);
+      };
+      auto issue_pv = [&](int x, int j) {
+        const int st = j % PP_ST;
+        const uint32_t v_addr = smem_u32(sV + st * C::KV_BYTES);
+#pragma unroll
+        for (int k = 0; k < PP_KT / 16; ++k) {
+          const uint64_t bd = make_sdesc(v_addr + k * 16 * C::SWZ, C::KV_ATOM, 8 * C::SWZ, C::SWZ);
+          tc_mma_f16_ts(tmem + C::o_col(x), tmem + C::p_col(x) + k * 8, bd, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+        }
+        tc_commit(&o_done[x]);
+      };
+      for (int x = 0; x < 2; ++x)
+        if (nt_t[x] > 0) issue_s(x, 0);
+      for (int j = 0; j < nt; ++j) {
+        for (int x = 0; x < 2; ++x) {
+          if (j >= nt_t[x]) continue;
+          mbar_wait(&p_full[x], j & 1);
+          tc_fence_after();
+          issue_pv(x, j);
+          if (j + 1 < nt_t[x]) issue_s(x, j + 1);
+        }
+        tc_commit(&kv_empty[j % PP_ST]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- softmax groups: warps 2-5 -> tile A, warps 6-9 -> tile B
+    const int x = (warp - 2) >> 2;
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const bool q_valid = r < nq_t[x];
+    const int qp = q_valid ? a.qpos[q_row0 + x * 128 + r] : -1;
+    const int ntx = nt_t[x];
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const uint32_t tS = tmem + C::s_col(x) + lane_off, tP = tmem + C::p_col(x) + lane_off;
+    const uint32_t tO = tmem + C::o_col(x) + lane_off;
+    const float NEG_INF = -INFINITY;
+    float m_run = NEG_INF, l_run = 0.f;
+    for (int j = 0; j < ntx; ++j) {
+      const int k0 = kb + j * PP_KT;
+      float s[PP_KT];
+      mbar_wait(&s_full[x], j & 1);
+      tc_fence_after();
+      tmem_ld32(tS, s);
+      tmem_ld32(tS + 32, s + 32);
+      tmem_wait_ld();
+      const int lim = min(qp, ke - 1) - k0;
+      float tmax = NEG_INF;
+#pragma unroll
+      for (int i = 0; i < PP_KT; ++i) {
+        s[i] = (i <= lim) ? s[i] * a.scale_log2 : NEG_INF;
+        tmax = fmaxf(tmax, s[i]);
+      }
+      if (j > 0) {
+        mbar_wait(&o_done[x], (j - 1) & 1);
+        tc_fence_after();
+      }
+      const float m_new = fmaxf(m_run, tmax);
+      const bool need = m_new > m_run + 8.0f;
+      const bool has_o = m_run != NEG_INF;
+      if (__any_sync(0xffffffffu, need && has_o)) {
+        const float sc = (need && has_o) ? exp2f(m_run - m_new) : 1.0f;
+#pragma unroll
+        for (int c = 0; c < HD / 16; ++c) {
+          float o[16];
+          tmem_ld16(tO + c * 16, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] *= sc;
+          tmem_st16(tO + c * 16, o);
+        }
+        tmem_wait_st();
+      }
+      if (need) {
+        l_run = has_o ? l_run * exp2f(m_run - m_new) : 0.f;
+        m_run = m_new;
+      }
+      const bool any = m_run != NEG_INF;
+      uint32_t pk[PP_KT / 2];
+      float lsum = 0.f;
+#pragma unroll
+      for (int i = 0; i < PP_KT / 2; ++i) {
+        const float p0 = any ? exp2f(s[2 * i] - m_run) : 0.f;
+        const float p1 = any ? exp2f(s[2 * i + 1] - m_run) : 0.f;
+        lsum += p0 + p1;
+        pk[i] = pack_bf16(p0, p1);
+      }
+      l_run += lsum;
+      tmem_st32(tP, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&p_full[x]);
+    }
+    if (ntx > 0) {
+      mbar_wait(&o_done[x], (ntx - 1) & 1);
+      tc_fence_after();
+    }
+    const int qrow = q_row0 + x * 128 + r;
+    if (group < 0) {
+      const float inv = (l_run > 0.f) ? 1.0f / l_run : 0.f;
+      __nv_bfloat16* orow = q_valid ? reinterpret_cast<__nv_bfloat16*>(a.out) + (long)a.rowof[qrow] * a.ldo + head * HD
+                                    : nullptr;
+#pragma unroll
+      for (int c = 0; c < HD / 16; ++c) {
+        float o[16];
+        if (ntx > 0) {
+          tmem_ld16(tO + c * 16, o);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = 0.f;
+        }
+        if (q_valid) {
+          uint32_t pkk[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) pkk[q] = pack_bf16(o[2 * q] * inv, o[2 * q + 1] * inv);
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+          dst[0] = make_uint4(pkk[0], pkk[1], pkk[2], pkk[3]);
+          dst[1] = make_uint4(pkk[4], pkk[5], pkk[6], pkk[7]);
+        }
+      }
+    } else {
+      const long prow = ((long)group * 8 + part) * 256 + x * 128 + r;
+      float* wo = a.ws_o + prow * HD;
+#pragma unroll
+      for (int c = 0; c < HD / 16; ++c) {
+        float o[16];
+        if (ntx > 0) {
+          tmem_ld16(tO + c * 16, o);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = 0.f;
+        }
+        if (q_valid) {
+          float4* dst = reinterpret_cast<float4*>(wo + c * 16);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) __stcg(dst + q, make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]));
+        }
+      }
+      if (q_valid) __stcg(reinterpret_cast<float2*>(a.ws_ml) + prow, make_float2(m_run, l_run));
+      __threadfence();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+  if (group < 0) return;
+  // ---------------- parallel merge of the nsplit partials (all CTAs of the group co-resident)
+  if (threadIdx.x == 0) {
+    atomicAdd(&a.counters[group], 1);
+    volatile int* cnt = a.counters + group;
+    while (*cnt < nsplit) __nanosleep(32);
+  }
+  __syncthreads();
+  __threadfence();
+  const int r_lo = 256 * part / nsplit, r_hi = min(nq, 256 * (part + 1) / nsplit);
+  constexpr int C4 = HD / 4;
+  for (int w = threadIdx.x; w < (r_hi - r_lo) * C4; w += PP_THREADS) {
+    const int rr = r_lo + w / C4, c4 = w % C4;
+    float mm[8];
+    float M = -INFINITY;
+    for (int s2 = 0; s2 < nsplit; ++s2) {
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.ws_ml) + ((long)group * 8 + s2) * 256 + rr);
+      mm[s2] = ml.x;
+      M = fmaxf(M, ml.x);
+    }
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s2 = 0; s2 < nsplit; ++s2) {
+      const long prow = ((long)group * 8 + s2) * 256 + rr;
+      const float wgt = (mm[s2] == -INFINITY) ? 0.f : exp2f(mm[s2] - M);
+      if (wgt == 0.f) continue;
+      L += wgt * __ldcg(reinterpret_cast<const float2*>(a.ws_ml) + prow).y;
+      const float4 o = __ldcg(reinterpret_cast<const float4*>(a.ws_o + prow * HD) + c4);
+      acc.x += wgt * o.x; acc.y += wgt * o.y; acc.z += wgt * o.z; acc.w += wgt * o.w;
+    }
+    const float inv = L > 0.f ? 1.0f / L : 0.f;
+    __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(a.out) + (long)a.rowof[q_row0 + rr] * a.ldo + head * HD;
+    *reinterpret_cast<uint2*>(orow + c4 * 4) =
+        make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(&a.counters[a.ws_slots + group], 1) == nsplit - 1) {
+      a.counters[group] = 0;
+      a.counters[a.ws_slots + group] = 0;
+    }
+  }
+}
+
+template <int HD>
+static cudaError_t launch_pp_hd(const vlc_attn_args& a, cudaStream_t stream, bool coop) {
+  using C = PPCfg<HD>;
+  CUtensorMap mq, mk, mv;
+  cudaError_t e = make_tmap_2d(&mq, a.q, a.kv, a.q_rows_cap, (uint64_t)a.kv * 2, C::ATOM_E, 128, C::SWZ);
+  if (e != cudaSuccess) return e;
+  e = make_tmap_3d(&mk, a.kc, a.kv, a.kv_rows_cap, a.layers_cap, (uint64_t)a.kv * 2,
+                   (uint64_t)a.kv * 2 * a.kv_rows_cap, C::ATOM_E, PP_KT, 1, C::SWZ);
+  if (e != cudaSuccess) return e;
+  e = make_tmap_3d(&mv, a.vc, a.kv, a.kv_rows_cap, a.layers_cap, (uint64_t)a.kv * 2,
+                   (uint64_t)a.kv * 2 * a.kv_rows_cap, C::ATOM_E, PP_KT, 1, C::SWZ);
+  if (e != cudaSuccess) return e;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_pp_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.n_items);
+  cfg.blockDim = dim3(PP_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr_c[1];
+  attr_c[0].id = cudaLaunchAttributeCooperative;
+  attr_c[0].val.cooperative = 1;
+  cfg.attrs = attr_c;
+  cfg.numAttrs = coop ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, attn_pp_kernel<HD>, mq, mk, mv, a);
+}
+
+cudaError_t launch_attention_pp(const vlc_attn_args& a, cudaStream_t stream, bool coop) {
+  if (a.n_items <= 0) return cudaSuccess;
+  switch (a.head_dim) {
+    case 16: return launch_pp_hd<16>(a, stream, coop);
+    case 32: return launch_pp_hd<32>(a, stream, coop);
+    case 64: return launch_pp_hd<64>(a, stream, coop);
+    case 128: return launch_pp_hd<128>(a, stream, coop);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t launch_attention(const vlc_attn_args& a, cudaStream_t stream) {
   if (a.n_items <= 0) return cudaSuccess;
   switch (a.head_dim) {

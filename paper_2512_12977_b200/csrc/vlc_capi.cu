@@ -164,6 +164,17 @@ int vlc_attn_mixed(const vlc_attn_args* a, cudaStream_t stream) {
   return cuda_status(launch_attention(*a, stream), "attn_mixed");
 }
 
+int vlc_attn_pp(const vlc_attn_args* a, cudaStream_t stream) {
+  if (!a || !a->q || !a->kc || !a->vc || !a->items) return fail(VLC_ERR_INVALID, "attn_pp: null pointer");
+  if (a->head_dim != 16 && a->head_dim != 32 && a->head_dim != 64 && a->head_dim != 128)
+    return fail(VLC_ERR_UNSUPPORTED, "attn_pp: head_dim must be 16/32/64/128");
+  if (a->kv != a->heads * a->head_dim) return fail(VLC_ERR_INVALID, "attn_pp: kv != heads*head_dim");
+  // split groups need every CTA resident at once (parallel merge); cooperative launch checks it
+  const bool coop = a->ws_slots > 0;
+  if (coop && !a->counters) return fail(VLC_ERR_INVALID, "attn_pp: split groups need counters");
+  return cuda_status(launch_attention_pp(*a, stream, coop), "attn_pp");
+}
+
 int vlc_attn_combine(const vlc_attn_args* a, cudaStream_t stream) {
   if (!a) return fail(VLC_ERR_INVALID, "attn_combine: null");
   return cuda_status(launch_attn_combine(*a, stream), "attn_combine");

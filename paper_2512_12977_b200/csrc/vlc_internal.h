@@ -38,5 +38,6 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
 
 cudaError_t launch_attention(const vlc_attn_args& a, cudaStream_t stream);
 cudaError_t launch_attn_combine(const vlc_attn_args& a, cudaStream_t stream);
+cudaError_t launch_attention_pp(const vlc_attn_args& a, cudaStream_t stream, bool coop);
 
 }  // namespace vlc

@@ -145,6 +145,37 @@ def attention_work(q_ranges, qpos, n_req, heads, target_items: int):
     return it, cb, slot
 
 
+def attention_work_pp(q_ranges, qpos, n_req, heads, max_ctas: int = 148):
+    """Work items of the ping-pong attention kernel (include/vlcache.h vlc_attn_pp): one CTA per
+    (request, head, <=256 sorted queries, key range).  When there are few (query-pair, head)
+    units the key range is split so the grid fills the SMs; split groups merge in-kernel, which
+    requires every CTA co-resident, hence total CTAs <= max_ctas whenever anything is split.
+
+    Returns (items int32 [n, 8], n_groups)."""
+    pairs = []
+    for req, q0, cnt in q_ranges:
+        for t0 in range(q0, q0 + cnt, 256):
+            nq = min(256, q0 + cnt - t0)
+            kend = min(int(qpos[t0 + nq - 1]) + 1, int(n_req[req]))
+            pairs.append((req, t0, nq, kend))
+    units = len(pairs) * heads
+    ns_max = max(1, min(8, max_ctas // max(1, units)))
+    items, group = [], 0
+    for h in range(heads):
+        for req, t0, nq, kend in pairs:
+            tiles = (kend + 63) // 64
+            ns = max(1, min(ns_max, tiles // 2))
+            if ns == 1:
+                items.append([t0, nq, h, 0, 0, kend, -1, (0 << 8) | 1, req])
+                continue
+            bounds = [min(kend, (tiles * s // ns) * 64) for s in range(ns)] + [kend]
+            for s in range(ns):
+                items.append([t0, nq, h, 0, bounds[s], bounds[s + 1], group, (s << 8) | ns, req])
+            group += 1
+    it = np.array(items, dtype=np.int32).reshape(-1, 9)
+    return it, group
+
+
 def build_layout(specs: list[RequestSpec], L: int, heads: int, target_items: int = 296) -> Layout:
     R = len(specs)
     n_req = np.array([s.n for s in specs], dtype=np.int64)
@@ -183,11 +214,11 @@ def build_layout(specs: list[RequestSpec], L: int, heads: int, target_items: int
             if len(sel):
                 ranges.append((r, int(sel[0]), len(sel)))
         q_ranges.append(ranges)
-        it, cb, s = attention_work(ranges, qpos[i], n_req, heads, target_items)
-        it[:, 3] = kvoff[it[:, 7]]
-        attn_items.append(it)
-        comb_items.append(cb)
-        slots = max(slots, s)
+        it9, groups = attention_work_pp(ranges, qpos[i], n_req, heads)
+        it9[:, 3] = kvoff[it9[:, 8]]
+        attn_items.append(np.ascontiguousarray(it9[:, :8]))
+        comb_items.append(np.zeros((0, 8), dtype=np.int32))
+        slots = max(slots, groups)
 
     # relocation descriptors, grouped by layer
     descs, blocks, layer_blocks, pages, ntok_total = [], [], [0], [], 0

@@ -11,7 +11,7 @@ import weakref
 import numpy as np
 
 from . import _native as N
-from .layout import Layout, attention_work
+from .layout import Layout, attention_work_pp
 from .model import RMS_EPS, DeviceWeights
 
 N_SMS = 148
@@ -110,6 +110,7 @@ class Runner:
         torch = _torch()
         self.splitk = self.ws.get("splitk", (64 << 20,), torch.float32, zero=False)
         self.counters = self.ws.get("counters", (1 << 16,), torch.int32)
+        self.attn_counters = self.ws.get("attn_counters", (1 << 14,), torch.int32)
         self.launches = 0          # kernels issued by this runner (all entry points)
         self.graphs: dict = {}     # structure key -> captured CUDA graph of the prefill chain
         self.layouts: dict = {}    # structure key -> Layout (engine._layout)
@@ -156,18 +157,16 @@ class Runner:
         torch = _torch()
         cfg = self.cfg
         hd = cfg.head_dim
-        ws_o = self.ws.get("attn_ws_o", (max(1, slots) * 128 * hd,), torch.float32, zero=False)
-        ws_ml = self.ws.get("attn_ws_ml", (max(1, slots) * 256,), torch.float32, zero=False)
+        ws_o = self.ws.get("attn_ws_o", (max(1, slots) * 8 * 256 * hd,), torch.float32, zero=False)
+        ws_ml = self.ws.get("attn_ws_ml", (max(1, slots) * 8 * 256 * 2,), torch.float32, zero=False)
         a = N.AttnArgs(q=q.data_ptr(), q_rows_cap=q.shape[0], kc=kc.data_ptr(), vc=vc.data_ptr(),
                        layers_cap=kc.shape[0], kv_rows_cap=kc.shape[1], layer=layer, kv=cfg.kv_dim,
                        heads=cfg.num_heads, head_dim=hd, items=items_ptr, n_items=n_items, qpos=qpos_ptr,
                        rowof=rowof_ptr, out=out.data_ptr(), ldo=out.shape[1], ws_o=ws_o.data_ptr(),
                        ws_ml=ws_ml.data_ptr(), ws_slots=slots, comb=comb_ptr, n_comb=n_comb,
-                       scale_log2=math.log2(math.e) / math.sqrt(hd))
-        self._run("attention", lambda: N.check(self.lib.vlc_attn_mixed(a, _stream()), "vlc_attn_mixed"),
+                       scale_log2=math.log2(math.e) / math.sqrt(hd), counters=self.attn_counters.data_ptr())
+        self._run("attention", lambda: N.check(self.lib.vlc_attn_pp(a, _stream()), "vlc_attn_pp"),
                   nbytes, flops)
-        if n_comb:
-            self._run("attn_combine", lambda: N.check(self.lib.vlc_attn_combine(a, _stream()), "vlc_attn_combine"))
 
     # ---------------------------------------------------------------- vision encoder (miss path)
     def encode(self, pixels_list) -> "object":
@@ -207,11 +206,12 @@ class Runner:
                        out3=ve.data_ptr(), ld3=kv, seg=kv, hd=cfg.head_dim))
         ranges = [(m, m * T, T) for m in range(k)]
         qpos = np.full(M, T - 1, dtype=np.int32)
-        items, comb, slots = attention_work(ranges, qpos, np.full(k, T), cfg.num_heads, 296)
-        items[:, 3] = items[:, 7] * T
+        it9, slots = attention_work_pp(ranges, qpos, np.full(k, T), cfg.num_heads)
+        it9[:, 3] = it9[:, 8] * T
+        items, comb = np.ascontiguousarray(it9[:, :8]), np.zeros((0, 8), np.int32)
         pack = IntPack()
         pack.add("items", items)
-        pack.add("comb", comb if len(comb) else np.zeros((1, 8)))
+        pack.add("comb", np.zeros((1, 8)))
         pack.add("qpos", qpos)
         pack.add("rowof", np.arange(M))
         pack.upload(ws, "enc_ints")
@@ -250,8 +250,8 @@ class Runner:
             vc=ws.get("vc", (L, KVR, kv), torch.bfloat16), kpre=ws.get("kpre", (L, R, kv), torch.bfloat16),
             logits=ws.get("logits", (max(int(c[L - 1]), 1), V), torch.float32, zero=False))
         hd = cfg.head_dim
-        ws.get("attn_ws_o", (max(1, lay.attn_slots) * 128 * hd,), torch.float32, zero=False)
-        ws.get("attn_ws_ml", (max(1, lay.attn_slots) * 256,), torch.float32, zero=False)
+        ws.get("attn_ws_o", (max(1, lay.attn_slots) * 8 * 256 * hd,), torch.float32, zero=False)
+        ws.get("attn_ws_ml", (max(1, lay.attn_slots) * 8 * 256 * 2,), torch.float32, zero=False)
 
         pack = self._pack(lay)
         pack.upload(ws, "ints")

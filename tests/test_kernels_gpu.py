@@ -231,3 +231,44 @@ def test_kv_relocate_matches_torch(nat):
         assert (kc[layer, pos].float() - ref_k).abs().max().item() < 2e-2
         assert torch.equal(vc[layer, pos], vpool[rows])
         assert kc[layer, :start + keeps[layer]].abs().sum().item() == 0
+
+
+@pytest.mark.parametrize("hd,heads,nkeys,nq,causal", [(128, 28, 4128, 236, True), (128, 2, 1000, 150, True),
+                                                      (64, 2, 513, 200, True), (32, 8, 288, 44, True),
+                                                      (16, 2, 26, 10, True), (128, 4, 300, 300, True),
+                                                      (128, 3, 256, 256, False), (128, 1, 4128, 600, True)])
+def test_attention_pp_matches_torch(nat, hd, heads, nkeys, nq, causal):
+    from paper_2512_12977_b200.layout import attention_work_pp
+    kv = heads * hd
+    g = torch.Generator(device="cuda").manual_seed(nkeys + nq)
+    layers, layer, kv_rows = 2, 1, nkeys + 64
+    kc = torch.randn(layers, kv_rows, kv, device="cuda", generator=g).bfloat16()
+    vc = torch.randn(layers, kv_rows, kv, device="cuda", generator=g).bfloat16()
+    if causal:
+        qpos = torch.sort(torch.randperm(nkeys, device="cuda", generator=g)[:nq]).values.int()
+        qpos[-1] = nkeys - 1
+    else:
+        qpos = torch.full((nq,), nkeys - 1, dtype=torch.int32, device="cuda")
+    q = torch.zeros(max(256, nq + 256), kv, device="cuda", dtype=torch.bfloat16)
+    q[:nq] = torch.randn(nq, kv, device="cuda", generator=g).bfloat16()
+    rowof = torch.randperm(nq, device="cuda", generator=g).int()
+    out = torch.zeros(nq, kv, device="cuda", dtype=torch.bfloat16)
+    it9, groups = attention_work_pp([(0, 0, nq)], qpos.cpu().numpy(), np.array([nkeys]), heads)
+    it = torch.from_numpy(np.ascontiguousarray(it9[:, :8])).cuda()
+    ws_o = torch.zeros(max(groups, 1) * 8 * 256 * hd, device="cuda")
+    ws_ml = torch.zeros(max(groups, 1) * 8 * 256 * 2, device="cuda")
+    cnt = torch.zeros(4096, dtype=torch.int32, device="cuda")
+    a = nat.AttnArgs(q=q.data_ptr(), q_rows_cap=q.shape[0], kc=kc.data_ptr(), vc=vc.data_ptr(),
+                     layers_cap=layers, kv_rows_cap=kv_rows, layer=layer, kv=kv, heads=heads, head_dim=hd,
+                     items=it.data_ptr(), n_items=it.shape[0], qpos=qpos.data_ptr(), rowof=rowof.data_ptr(),
+                     out=out.data_ptr(), ldo=kv, ws_o=ws_o.data_ptr(), ws_ml=ws_ml.data_ptr(), ws_slots=groups,
+                     comb=0, n_comb=0, scale_log2=math.log2(math.e) / math.sqrt(hd), counters=cnt.data_ptr())
+    for _ in range(2):   # twice: counters must be left zeroed for the next launch
+        out.zero_()
+        nat.check(nat.load().vlc_attn_pp(a, _stream()), "attn_pp")
+        torch.cuda.synchronize()
+        ref = _attn_ref(q[:nq], kc[layer], vc[layer], qpos, heads, hd, nkeys)
+        got = out[rowof.long()].float()
+        err = (got - ref).abs().max().item()
+        assert err < 2e-2, err
+    assert int(cnt.abs().sum()) == 0
