@@ -25,16 +25,14 @@ __global__ void embed_assemble_kernel(float* __restrict__ x, int ldx,
 }
 
 // ------------------------------------------------------------------ rmsnorm (K4)
-// One warp per row, the row held in registers as float4 (d <= 32*4*VPT), so x is
-// read once; 8 rows per 256-thread block.
+// One 128-thread block per row, the row held in registers as float4 (VPT per thread), so x
+// is read once; cross-warp sum through shared memory.
 template <bool OUT_F32, int VPT>
-__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, int ldx,
+__global__ void __launch_bounds__(128) rmsnorm_kernel(const float* __restrict__ x, int ldx,
                                                       const float* __restrict__ g, void* __restrict__ out,
                                                       int ldo, int rows, int d,
                                                       const int* __restrict__ row_map, float eps) {
-  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (r >= rows) return;
-  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x;
   const int sr = row_map ? __ldg(row_map + r) : r;
   const float4* xr = reinterpret_cast<const float4*>(x + (long)sr * ldx);
   const int n4 = d >> 2;
@@ -42,18 +40,21 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
   float acc = 0.f;
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
-    const int i = lane + 32 * k;
-    v[k] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int i = threadIdx.x + 128 * k;
+    v[k] = i < n4 ? __ldg(xr + i) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
 #pragma unroll
   for (int k = 0; k < VPT; ++k) acc += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
 #pragma unroll
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  const float denom = sqrtf(acc / (float)d + eps);
+  __shared__ float red[4];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  const float denom = sqrtf((red[0] + red[1] + red[2] + red[3]) / (float)d + eps);
   const float4* g4 = reinterpret_cast<const float4*>(g);
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
-    const int i = lane + 32 * k;
+    const int i = threadIdx.x + 128 * k;
     if (i >= n4) break;
     const float4 gg = __ldg(g4 + i);
     const float4 y = make_float4((v[k].x / denom) * gg.x, (v[k].y / denom) * gg.y, (v[k].z / denom) * gg.z,
@@ -245,17 +246,18 @@ int vlc_embed_assemble_impl(float* x, int ldx, const void* embed_bf16, int d, co
 int vlc_rmsnorm_impl(const float* x, int ldx, const float* gamma, void* out, int ldo, int out_f32,
                      int rows, int d, const int* row_map, float eps, cudaStream_t stream) {
   if (rows <= 0) return 0;
-  const bool vec = (d % 4 == 0) && (ldx % 4 == 0) && (ldo % 4 == 0) && d <= 32 * 4 * 32;
-  const unsigned blocks = (rows + 7) / 8;
+  const bool vec = (d % 4 == 0) && (ldx % 4 == 0) && (ldo % 4 == 0) && d <= 128 * 4 * 16;
+  const unsigned blocks = rows;
 #define VLC_RMS(VPT)                                                                                   \
-  if (out_f32) rmsnorm_kernel<true, VPT><<<blocks, 256, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps); \
-  else rmsnorm_kernel<false, VPT><<<blocks, 256, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps);
+  if (out_f32) rmsnorm_kernel<true, VPT><<<blocks, 128, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps); \
+  else rmsnorm_kernel<false, VPT><<<blocks, 128, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps);
   if (vec) {
-    const int vpt = (d / 4 + 31) / 32;
-    if (vpt <= 2) { VLC_RMS(2) }
+    const int vpt = (d / 4 + 127) / 128;
+    if (vpt <= 1) { VLC_RMS(1) }
+    else if (vpt <= 2) { VLC_RMS(2) }
+    else if (vpt <= 4) { VLC_RMS(4) }
     else if (vpt <= 8) { VLC_RMS(8) }
-    else if (vpt <= 16) { VLC_RMS(16) }
-    else { VLC_RMS(32) }
+    else { VLC_RMS(16) }
   } else if (out_f32) {
     rmsnorm_generic<true><<<rows, 256, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps);
   } else {
