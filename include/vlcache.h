@@ -129,6 +129,13 @@ int vlc_gemm_bf16(const void* w, int n_pad, int k_pad, const void* x, int x_rows
                   int m_tokens, const vlc_epilogue* epi, int max_ctas, float* ws, size_t ws_bytes,
                   int* counters, cudaStream_t stream);
 
+/* Same GEMM with the weight pre-packed for streaming: tile (m, kb) of 128 rows x 64 bf16 at
+ * byte offset (m * (k_pad/64) + kb) * 16384, rows 128 B each, 16-byte chunk c of row r stored
+ * at chunk c ^ (r & 7) (the SWIZZLE_128B image) -- one contiguous 16 KB bulk copy per stage. */
+int vlc_gemm_bf16_packed(const void* w_packed, int n_pad, int k_pad, const void* x, int x_rows_cap,
+                         int m_tokens, const vlc_epilogue* epi, int max_ctas, float* ws,
+                         size_t ws_bytes, int* counters, cudaStream_t stream);
+
 int vlc_attn_mixed(const vlc_attn_args* args, cudaStream_t stream);
 int vlc_attn_combine(const vlc_attn_args* args, cudaStream_t stream);
 int vlc_attn_pp(const vlc_attn_args* args, cudaStream_t stream);

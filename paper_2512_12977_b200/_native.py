@@ -17,7 +17,7 @@ VLC_OK, VLC_ERR_INVALID, VLC_ERR_UNSUPPORTED, VLC_ERR_CUDA = 0, 1, 2, 3
 EPI_F32, EPI_RESID, EPI_BF16, EPI_BIAS_ADD, EPI_SWIGLU, EPI_QKV_PLAIN, EPI_QKV_ROPE = range(7)
 
 EXPORTS = ("vlc_last_error", "vlc_version", "vlc_embed_assemble", "vlc_rmsnorm", "vlc_kv_relocate",
-           "vlc_store_write_pages", "vlc_gemm_bf16", "vlc_attn_mixed", "vlc_attn_combine", "vlc_attn_pp",
+           "vlc_store_write_pages", "vlc_gemm_bf16", "vlc_gemm_bf16_packed", "vlc_attn_mixed", "vlc_attn_combine", "vlc_attn_pp",
            "vlc_patchify", "vlc_set_tuning", "vlc_set_debug_buffer")
 
 
@@ -64,6 +64,7 @@ def load():
         lib.vlc_kv_relocate.argtypes = [vp, vp, i, vp, i, i, vp, vp, i, vp, vp, i, vp, vp, i, vp]
         lib.vlc_store_write_pages.argtypes = [vp, i, i, i, i, vp, i, vp, i, vp]
         lib.vlc_gemm_bf16.argtypes = [vp, i, i, vp, i, i, C.POINTER(Epilogue), i, vp, C.c_size_t, vp, vp]
+        lib.vlc_gemm_bf16_packed.argtypes = [vp, i, i, vp, i, i, C.POINTER(Epilogue), i, vp, C.c_size_t, vp, vp]
         lib.vlc_attn_mixed.argtypes = [C.POINTER(AttnArgs), vp]
         lib.vlc_attn_combine.argtypes = [C.POINTER(AttnArgs), vp]
         lib.vlc_attn_pp.argtypes = [C.POINTER(AttnArgs), vp]
@@ -92,3 +93,15 @@ def call(name: str, *args) -> None:
 def ptr(t) -> int:
     """Device pointer of a torch tensor (None -> NULL)."""
     return 0 if t is None else int(t.data_ptr())
+
+
+def pack_weight(w):
+    """[n_pad, k_pad] bf16 K-major (cuda) -> the vlc_gemm_bf16_packed streaming image."""
+    import torch
+    n, k = w.shape
+    t = w.view(n // 128, 128, k // 64, 8, 8).permute(0, 2, 1, 3, 4)          # [mt, kb, row, chunk, 8]
+    r = torch.arange(128, device=w.device).view(1, 1, 128, 1)
+    c = torch.arange(8, device=w.device).view(1, 1, 1, 8)
+    idx = (c ^ (r % 8)).expand(t.shape[0], t.shape[1], 128, 8)              # physical p <- logical p ^ (r&7)
+    out = torch.gather(t, 3, idx.unsqueeze(-1).expand(*idx.shape, 8))
+    return out.contiguous().view(n, k)

@@ -156,6 +156,20 @@ int vlc_gemm_bf16(const void* w, int n_pad, int k_pad, const void* x, int x_rows
                      "gemm_bf16");
 }
 
+int vlc_gemm_bf16_packed(const void* w_packed, int n_pad, int k_pad, const void* x, int x_rows_cap, int m_tokens,
+                         const vlc_epilogue* epi, int max_ctas, float* ws, size_t ws_bytes, int* counters,
+                         cudaStream_t stream) {
+  if (!w_packed || !x || !epi) return fail(VLC_ERR_INVALID, "gemm_packed: null pointer");
+  if (n_pad % 128 || k_pad % 64 || n_pad <= 0 || k_pad <= 0)
+    return fail(VLC_ERR_UNSUPPORTED, "gemm_packed: n_pad must be a multiple of 128 and k_pad of 64");
+  if (x_rows_cap < 256 || m_tokens > x_rows_cap)
+    return fail(VLC_ERR_INVALID, "gemm_packed: x_rows_cap must be >= 256 and >= m_tokens");
+  if (epi->m_tokens != m_tokens) return fail(VLC_ERR_INVALID, "gemm_packed: epilogue m_tokens mismatch");
+  return cuda_status(launch_gemm(w_packed, n_pad, k_pad, x, x_rows_cap, m_tokens, *epi, max_ctas, ws, ws_bytes,
+                                 counters, stream, true),
+                     "gemm_bf16_packed");
+}
+
 int vlc_attn_mixed(const vlc_attn_args* a, cudaStream_t stream) {
   if (!a || !a->q || !a->kc || !a->vc || !a->items) return fail(VLC_ERR_INVALID, "attn: null pointer");
   if (a->head_dim != 16 && a->head_dim != 32 && a->head_dim != 64 && a->head_dim != 128)

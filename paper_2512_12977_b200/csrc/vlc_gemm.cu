@@ -142,7 +142,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
-                 GemmEpi epi, SkSched sk, int n_tile, int stages, float* ws, int* counters) {
+                 GemmEpi epi, SkSched sk, int n_tile, int stages, float* ws, int* counters,
+                 const uint8_t* __restrict__ w_packed) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int a_bytes = GEMM_BM * GEMM_BK * 2;
@@ -196,7 +197,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], a_bytes + b_bytes);
-          tma_load_2d(sa + stage * a_bytes, &map_w, &full[stage], kb * GEMM_BK, m0, pol_w);
+          if (w_packed)   // tile (m-tile, kb) stored pre-swizzled and contiguous: one 16 KB bulk copy
+            bulk_load(sa + stage * a_bytes, w_packed + ((long)(m0 / GEMM_BM) * sk.KB + kb) * a_bytes, a_bytes,
+                      &full[stage], pol_w);
+          else
+            tma_load_2d(sa + stage * a_bytes, &map_w, &full[stage], kb * GEMM_BK, m0, pol_w);
           tma_load_2d(sb + stage * b_bytes, &map_x, &full[stage], kb * GEMM_BK, tok0, pol_x);
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
@@ -337,7 +342,7 @@ static int gemm_pick_stages(int n_tile) {
   if (g_stage_override > 0) return g_stage_override;
   const int per = GEMM_BM * GEMM_BK * 2 + n_tile * GEMM_BK * 2;
   int s = (200 * 1024 - 16 * 1024) / per;
-  if (s > 8) s = 8;
+  if (s > 12) s = 12;
   if (s < 2) s = 2;
   return s;
 }
@@ -361,7 +366,7 @@ static int num_sms() {
 // ws must hold G * SK_MAX_PART * 128 * n_tile floats; counters 2 * G ints (zero).
 cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap,
                         int m_tokens, const GemmEpi& epi, int max_ctas, float* ws, size_t ws_bytes,
-                        int* counters, cudaStream_t stream) {
+                        int* counters, cudaStream_t stream, bool packed) {
   if (m_tokens <= 0) return cudaSuccess;
   const int KB = k_pad / GEMM_BK;
   const int m_tiles = n_pad / GEMM_BM;
@@ -381,8 +386,9 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
     else return cudaErrorInvalidValue;
   }
   CUtensorMap mw, mx;
-  cudaError_t err = make_tmap_2d(&mw, W, k_pad, n_pad, (uint64_t)k_pad * 2, GEMM_BK, GEMM_BM, 128);
+  cudaError_t err = packed ? cudaSuccess : make_tmap_2d(&mw, W, k_pad, n_pad, (uint64_t)k_pad * 2, GEMM_BK, GEMM_BM, 128);
   if (err != cudaSuccess) return err;
+  if (packed) mw = CUtensorMap{};
   err = make_tmap_2d(&mx, X, k_pad, x_rows_cap, (uint64_t)k_pad * 2, GEMM_BK, n_tile, 128);
   if (err != cudaSuccess) return err;
   const int stages = gemm_pick_stages(n_tile);
@@ -403,7 +409,8 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = g_coop ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, gemm_bf16_tc, mw, mx, epi, sk, n_tile, stages, ws, counters);
+  return cudaLaunchKernelEx(&cfg, gemm_bf16_tc, mw, mx, epi, sk, n_tile, stages, ws, counters,
+                            packed ? reinterpret_cast<const uint8_t*>(W) : nullptr);
 }
 
 }  // namespace vlc

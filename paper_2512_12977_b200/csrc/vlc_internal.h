@@ -34,7 +34,7 @@ cudaError_t make_tmap_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64
 
 cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap,
                         int m_tokens, const GemmEpi& epi, int max_ctas, float* ws, size_t ws_bytes,
-                        int* counters, cudaStream_t stream);
+                        int* counters, cudaStream_t stream, bool packed = false);
 
 cudaError_t launch_attention(const vlc_attn_args& a, cudaStream_t stream);
 cudaError_t launch_attn_combine(const vlc_attn_args& a, cudaStream_t stream);

@@ -12,9 +12,12 @@ ws = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 cnt = torch.zeros(1 << 16, dtype=torch.int32, device="cuda")
 
 
-def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1):
+def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1, packed=False):
     nw = max(2, min(8, (1 << 30) // (n * k * 2)))   # rotate > L2 worth of weights
     Ws = [torch.randn(n, k, device="cuda").bfloat16() for _ in range(nw)]
+    if packed:
+        Ws = [N.pack_weight(w) for w in Ws]
+    fn = lib.vlc_gemm_bf16_packed if packed else lib.vlc_gemm_bf16
     X = torch.randn(max(256, m + 256), k, device="cuda").bfloat16()
     out = torch.zeros(m + 256, n, device="cuda", dtype=torch.float32)
     e = N.Epilogue()
@@ -24,8 +27,8 @@ def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1):
     s = torch.cuda.current_stream().cuda_stream
 
     def go(W):
-        N.check(lib.vlc_gemm_bf16(W.data_ptr(), n, k, X.data_ptr(), X.shape[0], m, e, splits, ws.data_ptr(),
-                                  ws.numel() * 4, cnt.data_ptr(), torch.cuda.current_stream().cuda_stream), "g")
+        N.check(fn(W.data_ptr(), n, k, X.data_ptr(), X.shape[0], m, e, splits, ws.data_ptr(),
+                   ws.numel() * 4, cnt.data_ptr(), torch.cuda.current_stream().cuda_stream), "g")
     go(Ws[0])
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
@@ -42,7 +45,7 @@ def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1):
     us = e0.elapsed_time(e1) * 1e3 / reps
     gbs = (n * k * 2 + m * k * 2) / us / 1e3
     tf = 2 * n * k * m / us / 1e6
-    print(f"N={n:6d} K={k:5d} M={m:4d} ctas={splits} coop={coop} kind={kind} st={stages}: {us:8.2f} us  "
+    print(f"N={n:6d} K={k:5d} M={m:4d} ctas={splits} pk={int(packed)} kind={kind} st={stages}: {us:8.2f} us  "
           f"{gbs:7.1f} GB/s  {tf:7.1f} TF/s", flush=True)
 
 
@@ -84,6 +87,14 @@ if __name__ == "__main__":
         for (n, kk, m, c) in ((3584, 3584, 16, 28), (3584, 3584, 16, 148), (3584, 3584, 240, 28),
                               (3584, 3584, 240, 148), (14336, 3584, 240, 112), (14336, 3584, 240, 148)):
             phases(n, kk, m, c)
+    elif mode == "packed":
+        for (n, k) in ((14336, 3584), (10752, 3584), (3584, 3584), (3584, 7168)):
+            for m in (16, 240):
+                for pk in (False, True):
+                    run(n, k, m, n // 128, packed=pk)
+        for pk in (False, True):
+            run(3584, 3584, 16, 148, packed=pk)
+            run(14336, 3584, 16, 112, packed=pk, stages=12)
     elif mode == "ctas":
         for (n, k) in ((14336, 3584), (10752, 3584), (3584, 3584), (3584, 7168)):
             for m in (16, 240):
