@@ -133,6 +133,7 @@ struct SkSched {
 constexpr int SK_MAX_PART = 8;  // participants per split tile
 
 __device__ unsigned long long* g_dbg = nullptr;  // phase timestamps (experiments only)
+__device__ int g_exp_mode = 0;                     // experiments: 1 = no MMA, 2 = no loads
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -196,6 +197,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int m0 = (t % sk.m_tiles) * GEMM_BM, tok0 = (t / sk.m_tiles) * n_tile;
         for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
+          if (g_exp_mode == 2) {
+            mbar_arrive(&full[stage]);
+            if (++stage == stages) { stage = 0; phase ^= 1; }
+            continue;
+          }
           mbar_expect_tx(&full[stage], a_bytes + b_bytes);
           if (w_packed)   // tile (m-tile, kb) stored pre-swizzled and contiguous: one 16 KB bulk copy
             bulk_load(sa + stage * a_bytes, w_packed + ((long)(m0 / GEMM_BM) * sk.KB + kb) * a_bytes, a_bytes,
@@ -226,6 +232,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sa + stage * a_bytes);
           const uint32_t b_addr = smem_u32(sb + stage * b_bytes);
+          if (g_exp_mode == 1) {
+            mbar_arrive(&empty[stage]);
+            if (++stage == stages) { stage = 0; phase ^= 1; }
+            continue;
+          }
 #pragma unroll
           for (int k = 0; k < GEMM_BK / 16; ++k) {
             const uint64_t ad = make_sdesc(a_addr + k * 32, 16, 1024, 128);
@@ -336,6 +347,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
 int g_stage_override = 0;
 void set_debug_buffer(unsigned long long* p) { cudaMemcpyToSymbol(g_dbg, &p, sizeof(p)); }
+void set_exp_mode(int m) { cudaMemcpyToSymbol(g_exp_mode, &m, sizeof(m)); }
 int g_coop = 1;
 
 static int gemm_pick_stages(int n_tile) {

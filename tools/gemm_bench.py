@@ -12,7 +12,7 @@ ws = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 cnt = torch.zeros(1 << 16, dtype=torch.int32, device="cuda")
 
 
-def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1, packed=False):
+def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1, packed=False, mode=0):
     nw = max(2, min(8, (1 << 30) // (n * k * 2)))   # rotate > L2 worth of weights
     Ws = [torch.randn(n, k, device="cuda").bfloat16() for _ in range(nw)]
     if packed:
@@ -24,6 +24,7 @@ def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1, packed=Fals
     e.kind, e.n_valid, e.m_tokens, e.out, e.ldo = kind, n, m, out.data_ptr(), n
     lib.vlc_set_tuning(1, stages)
     lib.vlc_set_tuning(2, coop)
+    lib.vlc_set_tuning(3, mode)
     s = torch.cuda.current_stream().cuda_stream
 
     def go(W):
@@ -45,7 +46,7 @@ def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1, packed=Fals
     us = e0.elapsed_time(e1) * 1e3 / reps
     gbs = (n * k * 2 + m * k * 2) / us / 1e3
     tf = 2 * n * k * m / us / 1e6
-    print(f"N={n:6d} K={k:5d} M={m:4d} ctas={splits} pk={int(packed)} kind={kind} st={stages}: {us:8.2f} us  "
+    print(f"N={n:6d} K={k:5d} M={m:4d} ctas={splits} pk={int(packed)} mode={mode} st={stages}: {us:8.2f} us  "
           f"{gbs:7.1f} GB/s  {tf:7.1f} TF/s", flush=True)
 
 
@@ -87,6 +88,13 @@ if __name__ == "__main__":
         for (n, kk, m, c) in ((3584, 3584, 16, 28), (3584, 3584, 16, 148), (3584, 3584, 240, 28),
                               (3584, 3584, 240, 148), (14336, 3584, 240, 112), (14336, 3584, 240, 148)):
             phases(n, kk, m, c)
+    elif mode == "modes":
+        for (n, k, m, c) in ((3584, 3584, 16, 28), (3584, 3584, 240, 28), (14336, 3584, 240, 112),
+                             (14336, 3584, 16, 112), (3584, 3584, 16, 148)):
+            for md in (0, 1, 2):
+                for st in (0, 4):
+                    run(n, k, m, c, mode=md, stages=st)
+        lib.vlc_set_tuning(3, 0)
     elif mode == "packed":
         for (n, k) in ((14336, 3584), (10752, 3584), (3584, 3584), (3584, 7168)):
             for m in (16, 240):
