@@ -21,7 +21,8 @@ namespace vlc {
 
 constexpr int GEMM_THREADS = 192;
 constexpr int GEMM_BM = 128;
-constexpr int GEMM_BK = 64;
+constexpr int GEMM_BK = 128;   // one stage = two 64-element (128 B) swizzle atoms along K
+constexpr int GEMM_ATOM_K = 64;
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g)); }
 
@@ -203,12 +204,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             continue;
           }
           mbar_expect_tx(&full[stage], a_bytes + b_bytes);
-          if (w_packed)   // tile (m-tile, kb) stored pre-swizzled and contiguous: one 16 KB bulk copy
-            bulk_load(sa + stage * a_bytes, w_packed + ((long)(m0 / GEMM_BM) * sk.KB + kb) * a_bytes, a_bytes,
-                      &full[stage], pol_w);
-          else
-            tma_load_2d(sa + stage * a_bytes, &map_w, &full[stage], kb * GEMM_BK, m0, pol_w);
-          tma_load_2d(sb + stage * b_bytes, &map_x, &full[stage], kb * GEMM_BK, tok0, pol_x);
+          // one TMA op per operand per stage: 3-D view {64 elems, rows, k-atom} -> [atom][rows][128 B]
+          tma_load_3d(sa + stage * a_bytes, &map_w, &full[stage], 0, m0, kb * 2, pol_w);
+          tma_load_3d(sb + stage * b_bytes, &map_x, &full[stage], 0, tok0, kb * 2, pol_x);
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
       }
@@ -239,8 +237,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
 #pragma unroll
           for (int k = 0; k < GEMM_BK / 16; ++k) {
-            const uint64_t ad = make_sdesc(a_addr + k * 32, 16, 1024, 128);
-            const uint64_t bd = make_sdesc(b_addr + k * 32, 16, 1024, 128);
+            const int at = k >> 2;
+            const uint64_t ad = make_sdesc(a_addr + at * (GEMM_BM * 128) + (k & 3) * 32, 16, 1024, 128);
+            const uint64_t bd = make_sdesc(b_addr + at * (n_tile * 128) + (k & 3) * 32, 16, 1024, 128);
             tc_mma_f16(d, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
           }
           tc_commit(&empty[stage]);
@@ -353,8 +352,8 @@ int g_coop = 1;
 static int gemm_pick_stages(int n_tile) {
   if (g_stage_override > 0) return g_stage_override;
   const int per = GEMM_BM * GEMM_BK * 2 + n_tile * GEMM_BK * 2;
-  int s = (200 * 1024 - 16 * 1024) / per;
-  if (s > 12) s = 12;
+  int s = (210 * 1024 - 16 * 1024) / per;
+  if (s > 8) s = 8;
   if (s < 2) s = 2;
   return s;
 }
@@ -380,7 +379,7 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
                         int m_tokens, const GemmEpi& epi, int max_ctas, float* ws, size_t ws_bytes,
                         int* counters, cudaStream_t stream, bool packed) {
   if (m_tokens <= 0) return cudaSuccess;
-  const int KB = k_pad / GEMM_BK;
+  const int KB = (k_pad + GEMM_BK - 1) / GEMM_BK;   // odd atom counts zero-fill (TMA OOB)
   const int m_tiles = n_pad / GEMM_BM;
   int n_tile = m_tokens >= 256 ? 256 : ((m_tokens + 15) / 16) * 16;
   if (n_tile < 16) n_tile = 16;
@@ -397,11 +396,14 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
     if (U / KB <= num_sms()) G = (int)(U / KB);
     else return cudaErrorInvalidValue;
   }
+  if (packed) return cudaErrorNotSupported;  // superseded by the 3-D atom boxes below
   CUtensorMap mw, mx;
-  cudaError_t err = packed ? cudaSuccess : make_tmap_2d(&mw, W, k_pad, n_pad, (uint64_t)k_pad * 2, GEMM_BK, GEMM_BM, 128);
+  // dims {64 (k within atom), rows, k atoms}; strides {row pitch, 128 B}; box {64, rows, 2}
+  cudaError_t err = make_tmap_3d(&mw, W, GEMM_ATOM_K, n_pad, k_pad / GEMM_ATOM_K, (uint64_t)k_pad * 2, 128,
+                                 GEMM_ATOM_K, GEMM_BM, 2, 128);
   if (err != cudaSuccess) return err;
-  if (packed) mw = CUtensorMap{};
-  err = make_tmap_2d(&mx, X, k_pad, x_rows_cap, (uint64_t)k_pad * 2, GEMM_BK, n_tile, 128);
+  err = make_tmap_3d(&mx, X, GEMM_ATOM_K, x_rows_cap, k_pad / GEMM_ATOM_K, (uint64_t)k_pad * 2, 128, GEMM_ATOM_K,
+                     n_tile, 2, 128);
   if (err != cudaSuccess) return err;
   const int stages = gemm_pick_stages(n_tile);
   const int smem = gemm_smem_bytes(n_tile, stages);

@@ -272,20 +272,3 @@ def test_attention_pp_matches_torch(nat, hd, heads, nkeys, nq, causal):
         err = (got - ref).abs().max().item()
         assert err < 2e-2, err
     assert int(cnt.abs().sum()) == 0
-
-
-@pytest.mark.parametrize("n_pad,k_pad,m", [(256, 128, 40), (3584, 3584, 236), (1280, 640, 600)])
-def test_gemm_packed_weight_matches_torch(nat, n_pad, k_pad, m):
-    g = torch.Generator(device="cuda").manual_seed(n_pad * 7 + m)
-    W = torch.randn(n_pad, k_pad, device="cuda", generator=g).bfloat16()
-    X = torch.randn(max(256, m), k_pad, device="cuda", generator=g).bfloat16()
-    out = torch.full((m, n_pad), float("nan"), device="cuda")
-    epi = _epi(nat, kind=nat.EPI_F32, n_valid=n_pad, m_tokens=m, out=out.data_ptr(), ldo=n_pad)
-    ws = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
-    cnt = torch.zeros(4096, dtype=torch.int32, device="cuda")
-    Wp = nat.pack_weight(W)
-    nat.check(nat.load().vlc_gemm_bf16_packed(Wp.data_ptr(), n_pad, k_pad, X.data_ptr(), X.shape[0], m, epi, 0,
-                                              ws.data_ptr(), ws.numel(), cnt.data_ptr(), _stream()), "gemm_packed")
-    torch.cuda.synchronize()
-    ref = X[:m].float() @ W.float().t()
-    assert (out - ref).abs().max().item() / ref.abs().max().item() < 1e-5
