@@ -134,7 +134,7 @@ struct SkSched {
 constexpr int SK_MAX_PART = 8;  // participants per split tile
 
 __device__ unsigned long long* g_dbg = nullptr;  // phase timestamps (experiments only)
-__device__ int g_exp_mode = 0;                     // experiments: 1 = no MMA, 2 = no loads
+__device__ int g_exp_mode = 0;  // experiments: 1 = no MMA, 2 = no loads, 3 = no loads + 2 accumulators
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int m0 = (t % sk.m_tiles) * GEMM_BM, tok0 = (t / sk.m_tiles) * n_tile;
         for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (g_exp_mode == 2) {
+          if (g_exp_mode >= 2) {
             mbar_arrive(&full[stage]);
             if (++stage == stages) { stage = 0; phase ^= 1; }
             continue;
@@ -240,7 +240,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const int at = k >> 2;
             const uint64_t ad = make_sdesc(a_addr + at * (GEMM_BM * 128) + (k & 3) * 32, 16, 1024, 128);
             const uint64_t bd = make_sdesc(b_addr + at * (n_tile * 128) + (k & 3) * 32, 16, 1024, 128);
-            tc_mma_f16(d, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            const uint32_t dd = (g_exp_mode == 3) ? (tmem + ((k & 1) ? 256 : 0)) : d;
+            tc_mma_f16(dd, ad, bd, idesc, (kb > 0 || k > 1) ? 1u : 0u);
           }
           tc_commit(&empty[stage]);
           if (++stage == stages) { stage = 0; phase ^= 1; }

@@ -90,9 +90,8 @@ if __name__ == "__main__":
             phases(n, kk, m, c)
     elif mode == "modes":
         for (n, k, m, c) in ((3584, 3584, 16, 28), (3584, 3584, 240, 28), (14336, 3584, 240, 112),
-                             (14336, 3584, 16, 112), (3584, 3584, 16, 148), (10752, 3584, 240, 84),
-                             (3584, 3584, 240, 148), (3584, 7168, 240, 148), (14336, 3584, 240, 148)):
-            for md in (0, 1):
+                             (14336, 3584, 128, 112), (14336, 3584, 16, 112)):
+            for md in (0, 1, 2, 3):
                 run(n, k, m, c, mode=md)
         lib.vlc_set_tuning(3, 0)
     elif mode == "packed":

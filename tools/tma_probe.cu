@@ -58,3 +58,49 @@ extern "C" int probe_ldg(const void* src, long bytes_per_cta, int ctas, int thre
   ldg_stream<<<ctas, threads, 0, s>>>((const uint4*)src, bytes_per_cta / 16, (unsigned long long*)sink);
   return (int)cudaGetLastError();
 }
+
+// ---------------------------------------------------------------- tcgen05 issue-rate probe
+// One CTA, operands = whatever is in smem (timing only).  variant bits:
+//  1: commit to an mbarrier after every group of 8 MMAs (else once at the end)
+//  2: wait that mbarrier before the next group (serialising, like a 1-deep pipeline)
+__global__ void mma_probe(int n, int groups, int variant, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  if (threadIdx.x == 32) { mbar_init(&bar, 1); fence_barrier_init(); }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (warp == 1 && lane == 0) {
+    const uint32_t idesc = make_idesc_bf16(128, n, 0, 0);
+    const uint32_t a = smem_u32(sm), b = smem_u32(sm + 32768);
+    long long t0 = clock64();
+    for (int g = 0; g < groups; ++g) {
+      for (int k = 0; k < 8; ++k) {
+        const uint64_t ad = make_sdesc(a + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, 128);
+        const uint64_t bd = make_sdesc(b + (k >> 2) * 32768 + (k & 3) * 32, 16, 1024, 128);
+        tc_mma_f16(tmem, ad, bd, idesc, (g | k) ? 1u : 0u);
+      }
+      if (variant & 1) tc_commit(&bar);
+      if (variant & 2) { mbar_wait(&bar, g & 1); tc_fence_after(); }
+    }
+    long long t1 = clock64();
+    tc_commit(&bar);
+    mbar_wait(&bar, (variant & 1) ? (groups & 1) : 0);
+    long long t2 = clock64();
+    out[0] = t1 - t0;  // issue loop
+    out[1] = t2 - t0;  // until all MMAs complete
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tmem); }
+}
+
+extern "C" int probe_mma(int n, int groups, int variant, void* out, cudaStream_t s) {
+  cudaFuncSetAttribute(mma_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  mma_probe<<<1, 128, 100 * 1024, s>>>(n, groups, variant, (unsigned long long*)out);
+  return (int)cudaGetLastError();
+}
