@@ -31,6 +31,19 @@ extern "C" {
 #define VLC_ERR_UNSUPPORTED 2 /* shape the kernels do not handle             */
 #define VLC_ERR_CUDA 3        /* CUDA runtime / driver failure               */
 
+/* PACKED OPERAND LAYOUT (inputs of vlc_gemm_bf16).  A bf16 matrix [rows][K] is stored as
+ * row tiles of R rows x 128-wide K blocks; block (rt, kb) is contiguous: two 64-column atoms,
+ * each R rows x 128 B, and inside an atom the 16-byte chunk c of row r sits at chunk c^(r&7)
+ * (the SWIZZLE_128B image UMMA expects).  Element (row, k), KB = ceil(K/128):
+ *   ((((rt*KB + kb)*2 + atom)*R + r)*64 + ((c ^ (r&7)) << 3) + e),
+ *   rt = row/R, r = row%R, kb = k>>7, atom = (k>>6)&1, c = (k>>3)&7, e = k&7.
+ * Weights use R = 128; activations use R = vlc_gemm_row_tile(m_tokens) of the consuming GEMM.
+ * One (rt, kb) block is one cp.async.bulk copy, which is what lets a CTA stream at HBM speed. */
+int vlc_gemm_row_tile(int m_tokens);
+/* Row-major bf16 [rows][cols] (leading dimension ld) -> packed (R, KB); padding is untouched. */
+int vlc_pack_operand(const void* src, int rows, int cols, int ld, void* dst, int R, int KB,
+                     cudaStream_t stream);
+
 /* GEMM epilogue kinds (vlc_gemm_bf16). */
 #define VLC_EPI_F32 0       /* out[map1?map1[j]:j][f] = acc            (engine.py:187 logits)   */
 #define VLC_EPI_RESID 1     /* out[j][f] += acc, fp32 residual          (engine.py:183, 185)     */
@@ -59,6 +72,8 @@ typedef struct vlc_epilogue {
   int seg;           /* features per q / k / v section (= kv_dim)            */
   const float* bias;
   const float* add;  int ld_add;
+  int pk_rows;       /* > 0: BF16 / SWIGLU output written PACKED (row tile pk_rows, pk_kb blocks) */
+  int pk_kb;
 } vlc_epilogue;
 
 /* Mixed attention over cached + recomputed KV (engine.py:181-182, model.py:268-291).
@@ -79,6 +94,7 @@ typedef struct vlc_attn_args {
   const int* comb; int n_comb;
   float scale_log2;                              /* log2(e) / sqrt(head_dim)          */
   int* counters;                                 /* >= 2*ws_slots ints, zeroed (pp)   */
+  int pk_rows; int pk_kb;                        /* > 0: output rows written PACKED   */
 } vlc_attn_args;
 
 /* Ping-pong attention (vlc_attn_pp): one CTA = up to 256 queries of one request and head
@@ -101,9 +117,11 @@ int vlc_set_debug_buffer(void* device_ptr);
 int vlc_embed_assemble(float* x, int ldx, const void* embed_bf16, int d, const float* enc_a,
                        const float* enc_b, const int* src, int rows, cudaStream_t stream);
 
-/* RMSNorm eps (model.py:257-259) of rows (optionally gathered via row_map) -> bf16 or f32. */
+/* RMSNorm eps (model.py:257-259) of rows (optionally gathered via row_map) -> bf16 or f32;
+ * bf16 output is PACKED when pk_rows > 0 (then ldo is ignored). */
 int vlc_rmsnorm(const float* x, int ldx, const float* gamma, void* out, int ldo, int out_f32,
-                int rows, int d, const int* row_map, float eps, cudaStream_t stream);
+                int rows, int d, const int* row_map, float eps, int pk_rows, int pk_kb,
+                cudaStream_t stream);
 
 /* Fused gather + RoPE re-rotation + scatter of cached pre-RoPE K and copy of V from
  * the paged store into the request KV cache (engine.py:153-155 + engine.py:180).
@@ -119,8 +137,9 @@ int vlc_store_write_pages(const void* src, int src_f32, int layers, int tokens, 
                           const int* page_table, int pages_per_layer, void* pool,
                           int page_tokens, cudaStream_t stream);
 
-/* Fused-epilogue tcgen05 GEMM: acc[f][j] = sum_k W[f][k] X[j][k]; W bf16 [n_pad][k_pad]
- * K-major, X bf16 [x_rows_cap][k_pad].  n_pad % 128 == 0, k_pad % 64 == 0.
+/* Fused-epilogue tcgen05 GEMM: acc[f][j] = sum_k W[f][k] X[j][k]; W PACKED (R = 128) with
+ * n_pad rows, X PACKED with R = vlc_gemm_row_tile(m_tokens) and >= ceil(m/R)*R rows (x_rows_cap),
+ * both with K = k_pad (% 128 == 0).  n_pad % 128 == 0.
  * Stream-K schedule over (128-row weight tile x token tile x 64-wide k-block) units on
  * max_ctas co-resident CTAs (0 = one per SM); tiles shared by several CTAs are reduced in
  * parallel through `ws` (>= ctas*8*128*256 floats) with `counters` (>= 2*ctas ints, zeroed
@@ -129,20 +148,14 @@ int vlc_gemm_bf16(const void* w, int n_pad, int k_pad, const void* x, int x_rows
                   int m_tokens, const vlc_epilogue* epi, int max_ctas, float* ws, size_t ws_bytes,
                   int* counters, cudaStream_t stream);
 
-/* Same GEMM with the weight pre-packed for streaming: tile (m, kb) of 128 rows x 64 bf16 at
- * byte offset (m * (k_pad/64) + kb) * 16384, rows 128 B each, 16-byte chunk c of row r stored
- * at chunk c ^ (r & 7) (the SWIZZLE_128B image) -- one contiguous 16 KB bulk copy per stage. */
-int vlc_gemm_bf16_packed(const void* w_packed, int n_pad, int k_pad, const void* x, int x_rows_cap,
-                         int m_tokens, const vlc_epilogue* epi, int max_ctas, float* ws,
-                         size_t ws_bytes, int* counters, cudaStream_t stream);
-
 int vlc_attn_mixed(const vlc_attn_args* args, cudaStream_t stream);
 int vlc_attn_combine(const vlc_attn_args* args, cudaStream_t stream);
 int vlc_attn_pp(const vlc_attn_args* args, cudaStream_t stream);
 
-/* Patchify (model.py:312-314): pixels f32 [side][side] -> bf16 [T][ldo] patches. */
-int vlc_patchify(const float* pixels, int side, int patch, void* out, int ldo,
-                 cudaStream_t stream);
+/* Patchify (model.py:312-314): pixels f32 [side][side] -> bf16 patches, PACKED with row tile
+ * pk_rows (patch rows start at row `row0`), K = patch^2 (kb blocks pk_kb). */
+int vlc_patchify(const float* pixels, int side, int patch, void* out, int row0, int pk_rows,
+                 int pk_kb, cudaStream_t stream);
 
 #ifdef __cplusplus
 }

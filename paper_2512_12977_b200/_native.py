@@ -17,7 +17,7 @@ VLC_OK, VLC_ERR_INVALID, VLC_ERR_UNSUPPORTED, VLC_ERR_CUDA = 0, 1, 2, 3
 EPI_F32, EPI_RESID, EPI_BF16, EPI_BIAS_ADD, EPI_SWIGLU, EPI_QKV_PLAIN, EPI_QKV_ROPE = range(7)
 
 EXPORTS = ("vlc_last_error", "vlc_version", "vlc_embed_assemble", "vlc_rmsnorm", "vlc_kv_relocate",
-           "vlc_store_write_pages", "vlc_gemm_bf16", "vlc_gemm_bf16_packed", "vlc_attn_mixed", "vlc_attn_combine", "vlc_attn_pp",
+           "vlc_store_write_pages", "vlc_gemm_bf16", "vlc_gemm_row_tile", "vlc_pack_operand", "vlc_attn_mixed", "vlc_attn_combine", "vlc_attn_pp",
            "vlc_patchify", "vlc_set_tuning", "vlc_set_debug_buffer")
 
 
@@ -32,7 +32,7 @@ class Epilogue(C.Structure):
                 ("map1", C.c_void_p), ("map2", C.c_void_p), ("pos", C.c_void_p),
                 ("cos_tab", C.c_void_p), ("sin_tab", C.c_void_p), ("tab_ld", C.c_int),
                 ("hd", C.c_int), ("seg", C.c_int), ("bias", C.c_void_p), ("add", C.c_void_p),
-                ("ld_add", C.c_int)]
+                ("ld_add", C.c_int), ("pk_rows", C.c_int), ("pk_kb", C.c_int)]
 
 
 class AttnArgs(C.Structure):
@@ -43,7 +43,7 @@ class AttnArgs(C.Structure):
                 ("rowof", C.c_void_p), ("out", C.c_void_p), ("ldo", C.c_int),
                 ("ws_o", C.c_void_p), ("ws_ml", C.c_void_p), ("ws_slots", C.c_int),
                 ("comb", C.c_void_p), ("n_comb", C.c_int), ("scale_log2", C.c_float),
-                ("counters", C.c_void_p)]
+                ("counters", C.c_void_p), ("pk_rows", C.c_int), ("pk_kb", C.c_int)]
 
 
 _lib = None
@@ -60,15 +60,16 @@ def load():
         lib.vlc_last_error.restype = C.c_char_p
         lib.vlc_version.restype = i
         lib.vlc_embed_assemble.argtypes = [vp, i, vp, i, vp, vp, vp, i, vp]
-        lib.vlc_rmsnorm.argtypes = [vp, i, vp, vp, i, i, i, i, vp, f, vp]
+        lib.vlc_rmsnorm.argtypes = [vp, i, vp, vp, i, i, i, i, vp, f, i, i, vp]
         lib.vlc_kv_relocate.argtypes = [vp, vp, i, vp, i, i, vp, vp, i, vp, vp, i, vp, vp, i, vp]
         lib.vlc_store_write_pages.argtypes = [vp, i, i, i, i, vp, i, vp, i, vp]
         lib.vlc_gemm_bf16.argtypes = [vp, i, i, vp, i, i, C.POINTER(Epilogue), i, vp, C.c_size_t, vp, vp]
-        lib.vlc_gemm_bf16_packed.argtypes = [vp, i, i, vp, i, i, C.POINTER(Epilogue), i, vp, C.c_size_t, vp, vp]
+        lib.vlc_gemm_row_tile.argtypes = [i]
+        lib.vlc_pack_operand.argtypes = [vp, i, i, i, vp, i, i, vp]
         lib.vlc_attn_mixed.argtypes = [C.POINTER(AttnArgs), vp]
         lib.vlc_attn_combine.argtypes = [C.POINTER(AttnArgs), vp]
         lib.vlc_attn_pp.argtypes = [C.POINTER(AttnArgs), vp]
-        lib.vlc_patchify.argtypes = [vp, i, i, vp, i, vp]
+        lib.vlc_patchify.argtypes = [vp, i, i, vp, i, i, i, vp]
         lib.vlc_set_tuning.argtypes = [i, i]
         lib.vlc_set_debug_buffer.argtypes = [vp]
         for name in EXPORTS:
@@ -95,13 +96,36 @@ def ptr(t) -> int:
     return 0 if t is None else int(t.data_ptr())
 
 
-def pack_weight(w):
-    """[n_pad, k_pad] bf16 K-major (cuda) -> the vlc_gemm_bf16_packed streaming image."""
+def row_tile(m_tokens: int) -> int:
+    """Row tile R of the packed activations consumed by a GEMM over m_tokens rows."""
+    return 256 if m_tokens >= 256 else max(16, (m_tokens + 15) // 16 * 16)
+
+
+def packed_numel(rows: int, K: int, R: int) -> int:
+    return -(-rows // R) * R * -(-K // 128) * 128
+
+
+def pack(t, R: int, K: int | None = None, rows_cap: int | None = None):
+    """Row-major bf16 cuda tensor [rows, cols] -> flat packed buffer (include/vlcache.h)."""
     import torch
-    n, k = w.shape
-    t = w.view(n // 128, 128, k // 64, 8, 8).permute(0, 2, 1, 3, 4)          # [mt, kb, row, chunk, 8]
-    r = torch.arange(128, device=w.device).view(1, 1, 128, 1)
-    c = torch.arange(8, device=w.device).view(1, 1, 1, 8)
-    idx = (c ^ (r % 8)).expand(t.shape[0], t.shape[1], 128, 8)              # physical p <- logical p ^ (r&7)
-    out = torch.gather(t, 3, idx.unsqueeze(-1).expand(*idx.shape, 8))
-    return out.contiguous().view(n, k)
+    rows, cols = t.shape
+    K = K or cols
+    KB = -(-K // 128)
+    rcap = max(rows, rows_cap or 0)
+    out = torch.zeros(packed_numel(rcap, K, R), dtype=torch.bfloat16, device=t.device)
+    src = t.contiguous()
+    call("vlc_pack_operand", src.data_ptr(), rows, cols, src.shape[1], out.data_ptr(), R, KB,
+         torch.cuda.current_stream().cuda_stream)
+    return out
+
+
+def unpack(p, rows: int, cols: int, R: int, K: int | None = None):
+    """Inverse of pack() (torch indexing; test / result helper)."""
+    import torch
+    K = K or cols
+    KB = -(-K // 128)
+    row = torch.arange(rows, device=p.device).view(-1, 1)
+    k = torch.arange(cols, device=p.device).view(1, -1)
+    rt, r = row // R, row % R
+    off = ((((rt * KB + (k >> 7)) * 2 + ((k >> 6) & 1)) * R + r) * 64 + ((((k >> 3) & 7) ^ (r & 7)) << 3) + (k & 7))
+    return p.view(-1)[off]

@@ -549,8 +549,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     const int qrow = q_row0 + x * 128 + r;
     if (group < 0) {
       const float inv = (l_run > 0.f) ? 1.0f / l_run : 0.f;
-      __nv_bfloat16* orow = q_valid ? reinterpret_cast<__nv_bfloat16*>(a.out) + (long)a.rowof[qrow] * a.ldo + head * HD
-                                    : nullptr;
+      const int orow_i = q_valid ? a.rowof[qrow] : 0;
+      __nv_bfloat16* obase = reinterpret_cast<__nv_bfloat16*>(a.out);
 #pragma unroll
       for (int c = 0; c < HD / 16; ++c) {
         float o[16];
@@ -565,9 +565,11 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
           uint32_t pkk[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q) pkk[q] = pack_bf16(o[2 * q] * inv, o[2 * q + 1] * inv);
-          uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
-          dst[0] = make_uint4(pkk[0], pkk[1], pkk[2], pkk[3]);
-          dst[1] = make_uint4(pkk[4], pkk[5], pkk[6], pkk[7]);
+          const int col = head * HD + c * 16;
+          const long o0 = a.pk_rows > 0 ? packed_off(orow_i, col, a.pk_rows, a.pk_kb) : (long)orow_i * a.ldo + col;
+          const long o1 = a.pk_rows > 0 ? packed_off(orow_i, col + 8, a.pk_rows, a.pk_kb) : o0 + 8;
+          *reinterpret_cast<uint4*>(obase + o0) = make_uint4(pkk[0], pkk[1], pkk[2], pkk[3]);
+          *reinterpret_cast<uint4*>(obase + o1) = make_uint4(pkk[4], pkk[5], pkk[6], pkk[7]);
         }
       }
     } else {
@@ -630,8 +632,9 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       acc.x += wgt * o.x; acc.y += wgt * o.y; acc.z += wgt * o.z; acc.w += wgt * o.w;
     }
     const float inv = L > 0.f ? 1.0f / L : 0.f;
-    __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(a.out) + (long)a.rowof[q_row0 + rr] * a.ldo + head * HD;
-    *reinterpret_cast<uint2*>(orow + c4 * 4) =
+    const int orow_i = a.rowof[q_row0 + rr], col = head * HD + c4 * 4;
+    const long off = a.pk_rows > 0 ? packed_off(orow_i, col, a.pk_rows, a.pk_kb) : (long)orow_i * a.ldo + col;
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.out) + off) =
         make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
   }
   __syncthreads();

@@ -82,11 +82,12 @@ using namespace vlc;
 extern "C" {
 
 int vlc_embed_assemble_impl(float*, int, const void*, int, const float*, const float*, const int*, int, cudaStream_t);
-int vlc_rmsnorm_impl(const float*, int, const float*, void*, int, int, int, int, const int*, float, cudaStream_t);
+int vlc_rmsnorm_impl(const float*, int, const float*, void*, int, int, int, int, const int*, float, int, int,
+                     cudaStream_t);
 int vlc_kv_relocate_impl(const void*, const void*, int, const int*, int, int, void*, void*, int, const int*,
                          const int*, int, const float*, const float*, int, cudaStream_t);
 int vlc_store_write_pages_impl(const void*, int, int, int, int, const int*, int, void*, int, cudaStream_t);
-int vlc_patchify_impl(const float*, int, int, void*, int, cudaStream_t);
+int vlc_patchify_impl(const float*, int, int, void*, int, int, int, cudaStream_t);
 
 const char* vlc_last_error(void) { return g_err; }
 
@@ -94,7 +95,6 @@ const char* vlc_last_error(void) { return g_err; }
 int vlc_set_tuning(int key, int value) {
   if (key == 1) { vlc::g_stage_override = value; return VLC_OK; }
   if (key == 2) { vlc::g_coop = value; return VLC_OK; }
-  if (key == 3) { vlc::set_exp_mode(value); return VLC_OK; }
   return fail(VLC_ERR_INVALID, "set_tuning: unknown key");
 }
 /* Experiments only: device buffer receiving per-CTA phase timestamps of the GEMM (NULL = off). */
@@ -113,11 +113,14 @@ int vlc_embed_assemble(float* x, int ldx, const void* embed_bf16, int d, const f
 }
 
 int vlc_rmsnorm(const float* x, int ldx, const float* gamma, void* out, int ldo, int out_f32, int rows, int d,
-                const int* row_map, float eps, cudaStream_t stream) {
-  if (rows < 0 || d <= 0 || ldx < d || ldo < d || !x || !gamma || !out)
+                const int* row_map, float eps, int pk_rows, int pk_kb, cudaStream_t stream) {
+  if (rows < 0 || d <= 0 || ldx < d || (pk_rows <= 0 && ldo < d) || !x || !gamma || !out)
     return fail(VLC_ERR_INVALID, "rmsnorm: bad args");
-  return cuda_status(
-      (cudaError_t)vlc_rmsnorm_impl(x, ldx, gamma, out, ldo, out_f32, rows, d, row_map, eps, stream), "rmsnorm");
+  if (pk_rows > 0 && (out_f32 || pk_rows % 8 || pk_kb * 128 < d))
+    return fail(VLC_ERR_INVALID, "rmsnorm: packed output needs bf16, pk_rows % 8 == 0, pk_kb*128 >= d");
+  return cuda_status((cudaError_t)vlc_rmsnorm_impl(x, ldx, gamma, out, ldo, out_f32, rows, d, row_map, eps, pk_rows,
+                                                   pk_kb, stream),
+                     "rmsnorm");
 }
 
 int vlc_kv_relocate(const void* kpool, const void* vpool, int page_tokens, const int* page_table, int kv,
@@ -141,34 +144,31 @@ int vlc_store_write_pages(const void* src, int src_f32, int layers, int tokens, 
                      "store_write_pages");
 }
 
+int vlc_gemm_row_tile(int m_tokens) { return gemm_row_tile(m_tokens); }
+
+int vlc_pack_operand(const void* src, int rows, int cols, int ld, void* dst, int R, int KB, cudaStream_t stream) {
+  if (!src || !dst || rows < 0 || cols <= 0 || ld < cols || R <= 0 || R % 8 || KB * 128 < cols)
+    return fail(VLC_ERR_INVALID, "pack_operand: bad args");
+  return cuda_status(launch_pack(src, rows, cols, ld, dst, R, KB, stream), "pack_operand");
+}
+
 int vlc_gemm_bf16(const void* w, int n_pad, int k_pad, const void* x, int x_rows_cap, int m_tokens,
                   const vlc_epilogue* epi, int max_ctas, float* ws, size_t ws_bytes, int* counters,
                   cudaStream_t stream) {
   if (!w || !x || !epi) return fail(VLC_ERR_INVALID, "gemm: null pointer");
-  if (n_pad % 128 || k_pad % 64 || n_pad <= 0 || k_pad <= 0)
-    return fail(VLC_ERR_UNSUPPORTED, "gemm: n_pad must be a multiple of 128 and k_pad of 64");
-  if (x_rows_cap < 256 || m_tokens > x_rows_cap)
-    return fail(VLC_ERR_INVALID, "gemm: x_rows_cap must be >= 256 and >= m_tokens");
+  if (n_pad % 128 || k_pad % 128 || n_pad <= 0 || k_pad <= 0)
+    return fail(VLC_ERR_UNSUPPORTED, "gemm: n_pad and k_pad must be multiples of 128");
+  const int rt = gemm_row_tile(m_tokens);
+  if (m_tokens > 0 && x_rows_cap < (m_tokens + rt - 1) / rt * rt)
+    return fail(VLC_ERR_INVALID, "gemm: x_rows_cap must cover whole row tiles of the packed activations");
+  if ((epi->kind == VLC_EPI_BF16 || epi->kind == VLC_EPI_SWIGLU) && epi->pk_rows > 0 && epi->pk_rows % 8)
+    return fail(VLC_ERR_INVALID, "gemm: packed epilogue output needs pk_rows % 8 == 0");
   if (epi->m_tokens != m_tokens) return fail(VLC_ERR_INVALID, "gemm: epilogue m_tokens mismatch");
   if (epi->kind == VLC_EPI_QKV_ROPE && (!epi->map2 || !epi->pos || !epi->cos_tab || epi->hd % 2))
     return fail(VLC_ERR_INVALID, "gemm: QKV_ROPE needs map2/pos/tables");
   return cuda_status(launch_gemm(w, n_pad, k_pad, x, x_rows_cap, m_tokens, *epi, max_ctas, ws, ws_bytes, counters,
                                  stream),
                      "gemm_bf16");
-}
-
-int vlc_gemm_bf16_packed(const void* w_packed, int n_pad, int k_pad, const void* x, int x_rows_cap, int m_tokens,
-                         const vlc_epilogue* epi, int max_ctas, float* ws, size_t ws_bytes, int* counters,
-                         cudaStream_t stream) {
-  if (!w_packed || !x || !epi) return fail(VLC_ERR_INVALID, "gemm_packed: null pointer");
-  if (n_pad % 128 || k_pad % 64 || n_pad <= 0 || k_pad <= 0)
-    return fail(VLC_ERR_UNSUPPORTED, "gemm_packed: n_pad must be a multiple of 128 and k_pad of 64");
-  if (x_rows_cap < 256 || m_tokens > x_rows_cap)
-    return fail(VLC_ERR_INVALID, "gemm_packed: x_rows_cap must be >= 256 and >= m_tokens");
-  if (epi->m_tokens != m_tokens) return fail(VLC_ERR_INVALID, "gemm_packed: epilogue m_tokens mismatch");
-  return cuda_status(launch_gemm(w_packed, n_pad, k_pad, x, x_rows_cap, m_tokens, *epi, max_ctas, ws, ws_bytes,
-                                 counters, stream, true),
-                     "gemm_bf16_packed");
 }
 
 int vlc_attn_mixed(const vlc_attn_args* a, cudaStream_t stream) {
@@ -195,10 +195,12 @@ int vlc_attn_combine(const vlc_attn_args* a, cudaStream_t stream) {
   return cuda_status(launch_attn_combine(*a, stream), "attn_combine");
 }
 
-int vlc_patchify(const float* pixels, int side, int patch, void* out, int ldo, cudaStream_t stream) {
-  if (!pixels || !out || patch <= 0 || side % patch || ldo < patch * patch)
+int vlc_patchify(const float* pixels, int side, int patch, void* out, int row0, int pk_rows, int pk_kb,
+                 cudaStream_t stream) {
+  if (!pixels || !out || patch <= 0 || side % patch || pk_rows <= 0 || pk_rows % 8 || pk_kb * 128 < patch * patch)
     return fail(VLC_ERR_INVALID, "patchify: bad args");
-  return cuda_status((cudaError_t)vlc_patchify_impl(pixels, side, patch, out, ldo, stream), "patchify");
+  return cuda_status((cudaError_t)vlc_patchify_impl(pixels, side, patch, out, row0, pk_rows, pk_kb, stream),
+                     "patchify");
 }
 
 }  // extern "C"

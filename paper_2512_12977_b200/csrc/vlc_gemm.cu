@@ -2,8 +2,10 @@
 //
 //   acc[f, j] = sum_k W[f, k] * X[j, k]          (swap-AB: weights on UMMA M)
 //
-// W is the layer weight stored K-major on device ([n_out, k] with k contiguous),
-// X the activations of the c computed tokens ([rows, k], bf16).  A CTA owns a
+// W (the layer weight, [n_out, k]) and X (the c computed tokens, [rows, k]) are both in the
+// PACKED operand layout of include/vlcache.h, so each pipeline stage is two contiguous
+// cp.async.bulk copies (32 KB of weights, n_tile*256 B of activations): TMA tensor boxes cost
+// ~3 cycles per 128 B row per SM, bulk copies ~190 ns per op (tools/tma_probe.py).  A CTA owns a
 // 128-row weight tile and one <=256-token tile; the K range may be split across
 // CTAs (split-K, deterministic "last CTA reduces").  One elected thread issues
 // the TMA loads (warp 0) and another the tcgen05.mma chain into TMEM (warp 1);
@@ -54,10 +56,11 @@ __device__ __forceinline__ void write_group(const GemmEpi& e, int F, int j, floa
       *o = make_float4(x.x + v.x, x.y + v.y, x.z + v.z, x.w + v.w);
       break;
     }
-    case EPI_BF16:
-      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(e.out) + (long)j * e.ldo + F) =
-          pack4_bf16(v.x, v.y, v.z, v.w);
+    case EPI_BF16: {
+      const long off = e.pk_rows > 0 ? packed_off(j, F, e.pk_rows, e.pk_kb) : (long)j * e.ldo + F;
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(e.out) + off) = pack4_bf16(v.x, v.y, v.z, v.w);
       break;
+    }
     case EPI_BIAS_ADD: {
       float4 b = e.bias ? __ldg(reinterpret_cast<const float4*>(e.bias + F)) : make_float4(0.f, 0.f, 0.f, 0.f);
       float4 a = e.add ? __ldg(reinterpret_cast<const float4*>(e.add + (long)j * e.ld_add + F))
@@ -66,10 +69,12 @@ __device__ __forceinline__ void write_group(const GemmEpi& e, int F, int j, floa
           make_float4((v.x + b.x) + a.x, (v.y + b.y) + a.y, (v.z + b.z) + a.z, (v.w + b.w) + a.w);
       break;
     }
-    case EPI_SWIGLU:
-      *reinterpret_cast<uint32_t*>(reinterpret_cast<__nv_bfloat16*>(e.out) + (long)j * e.ldo + (F >> 1)) =
+    case EPI_SWIGLU: {
+      const long off = e.pk_rows > 0 ? packed_off(j, F >> 1, e.pk_rows, e.pk_kb) : (long)j * e.ldo + (F >> 1);
+      *reinterpret_cast<uint32_t*>(reinterpret_cast<__nv_bfloat16*>(e.out) + off) =
           pack_bf16(silu_f(v.x) * v.y, silu_f(v.z) * v.w);
       break;
+    }
     case EPI_QKV_PLAIN: {
       const int sec = F / e.seg, r = F - sec * e.seg;
       void* dst = sec == 0 ? e.out : sec == 1 ? e.out2 : e.out3;
@@ -134,7 +139,6 @@ struct SkSched {
 constexpr int SK_MAX_PART = 8;  // participants per split tile
 
 __device__ unsigned long long* g_dbg = nullptr;  // phase timestamps (experiments only)
-__device__ int g_exp_mode = 0;  // experiments: 1 = no MMA, 2 = no loads, 3 = no loads + 2 accumulators
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -143,9 +147,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define DBG(slot) do { if (g_dbg) g_dbg[blockIdx.x * 8 + (slot)] = gtimer(); } while (0)
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-    gemm_bf16_tc(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
-                 GemmEpi epi, SkSched sk, int n_tile, int stages, float* ws, int* counters,
-                 const uint8_t* __restrict__ w_packed) {
+    gemm_bf16_tc(const uint8_t* __restrict__ wp, const uint8_t* __restrict__ xp, GemmEpi epi, SkSched sk,
+                 int n_tile, int stages, float* ws, int* counters) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int a_bytes = GEMM_BM * GEMM_BK * 2;
@@ -167,8 +170,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     DBG(0);
-    tma_prefetch(&map_w);
-    tma_prefetch(&map_x);
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -196,17 +197,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const long long tb = (long long)t * sk.KB;
         const int kb_lo = (int)(max(u_begin, tb) - tb), kb_hi = (int)(min(u_end, tb + sk.KB) - tb);
         const int m0 = (t % sk.m_tiles) * GEMM_BM, tok0 = (t / sk.m_tiles) * n_tile;
+        const uint8_t* wsrc = wp + (long)(m0 / GEMM_BM) * sk.KB * a_bytes;
+        const uint8_t* xsrc = xp + (long)(tok0 / n_tile) * sk.KB * b_bytes;
         for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (g_exp_mode >= 2) {
-            mbar_arrive(&full[stage]);
-            if (++stage == stages) { stage = 0; phase ^= 1; }
-            continue;
-          }
           mbar_expect_tx(&full[stage], a_bytes + b_bytes);
-          // one TMA op per operand per stage: 3-D view {64 elems, rows, k-atom} -> [atom][rows][128 B]
-          tma_load_3d(sa + stage * a_bytes, &map_w, &full[stage], 0, m0, kb * 2, pol_w);
-          tma_load_3d(sb + stage * b_bytes, &map_x, &full[stage], 0, tok0, kb * 2, pol_x);
+          bulk_load(sa + stage * a_bytes, wsrc + (long)kb * a_bytes, a_bytes, &full[stage], pol_w);
+          bulk_load(sb + stage * b_bytes, xsrc + (long)kb * b_bytes, b_bytes, &full[stage], pol_x);
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
       }
@@ -230,18 +227,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sa + stage * a_bytes);
           const uint32_t b_addr = smem_u32(sb + stage * b_bytes);
-          if (g_exp_mode == 1) {
-            mbar_arrive(&empty[stage]);
-            if (++stage == stages) { stage = 0; phase ^= 1; }
-            continue;
-          }
 #pragma unroll
           for (int k = 0; k < GEMM_BK / 16; ++k) {
             const int at = k >> 2;
             const uint64_t ad = make_sdesc(a_addr + at * (GEMM_BM * 128) + (k & 3) * 32, 16, 1024, 128);
             const uint64_t bd = make_sdesc(b_addr + at * (n_tile * 128) + (k & 3) * 32, 16, 1024, 128);
-            const uint32_t dd = (g_exp_mode == 3) ? (tmem + ((k & 1) ? 256 : 0)) : d;
-            tc_mma_f16(dd, ad, bd, idesc, (kb > 0 || k > 1) ? 1u : 0u);
+            tc_mma_f16(d, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
           }
           tc_commit(&empty[stage]);
           if (++stage == stages) { stage = 0; phase ^= 1; }
@@ -347,7 +338,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
 int g_stage_override = 0;
 void set_debug_buffer(unsigned long long* p) { cudaMemcpyToSymbol(g_dbg, &p, sizeof(p)); }
-void set_exp_mode(int m) { cudaMemcpyToSymbol(g_exp_mode, &m, sizeof(m)); }
+
 int g_coop = 1;
 
 static int gemm_pick_stages(int n_tile) {
@@ -375,16 +366,22 @@ static int num_sms() {
   return n;
 }
 
+int gemm_row_tile(int m_tokens) {
+  if (m_tokens >= 256) return 256;
+  int t = ((m_tokens + 15) / 16) * 16;
+  return t < 16 ? 16 : t;
+}
+
 // ws must hold G * SK_MAX_PART * 128 * n_tile floats; counters 2 * G ints (zero).
 cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap,
                         int m_tokens, const GemmEpi& epi, int max_ctas, float* ws, size_t ws_bytes,
-                        int* counters, cudaStream_t stream, bool packed) {
+                        int* counters, cudaStream_t stream) {
   if (m_tokens <= 0) return cudaSuccess;
-  const int KB = (k_pad + GEMM_BK - 1) / GEMM_BK;   // odd atom counts zero-fill (TMA OOB)
+  const int KB = k_pad / GEMM_BK;
   const int m_tiles = n_pad / GEMM_BM;
-  int n_tile = m_tokens >= 256 ? 256 : ((m_tokens + 15) / 16) * 16;
-  if (n_tile < 16) n_tile = 16;
+  const int n_tile = gemm_row_tile(m_tokens);
   const int tok_tiles = (m_tokens + n_tile - 1) / n_tile;
+  if (x_rows_cap < tok_tiles * n_tile) return cudaErrorInvalidValue;
   const long long U = (long long)m_tiles * tok_tiles * KB;
   int G = num_sms();
   if (max_ctas > 0 && max_ctas < G) G = max_ctas;
@@ -393,19 +390,9 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   if (G < 1) G = 1;
   const size_t need = (size_t)G * SK_MAX_PART * GEMM_BM * n_tile * sizeof(float);
   if (need > ws_bytes || counters == nullptr) {
-    // no workspace: one CTA per tile, never split
-    if (U / KB <= num_sms()) G = (int)(U / KB);
+    if (U / KB <= num_sms()) G = (int)(U / KB);   // no workspace: one CTA per tile, never split
     else return cudaErrorInvalidValue;
   }
-  if (packed) return cudaErrorNotSupported;  // superseded by the 3-D atom boxes below
-  CUtensorMap mw, mx;
-  // dims {64 (k within atom), rows, k atoms}; strides {row pitch, 128 B}; box {64, rows, 2}
-  cudaError_t err = make_tmap_3d(&mw, W, GEMM_ATOM_K, n_pad, k_pad / GEMM_ATOM_K, (uint64_t)k_pad * 2, 128,
-                                 GEMM_ATOM_K, GEMM_BM, 2, 128);
-  if (err != cudaSuccess) return err;
-  err = make_tmap_3d(&mx, X, GEMM_ATOM_K, x_rows_cap, k_pad / GEMM_ATOM_K, (uint64_t)k_pad * 2, 128, GEMM_ATOM_K,
-                     n_tile, 2, 128);
-  if (err != cudaSuccess) return err;
   const int stages = gemm_pick_stages(n_tile);
   const int smem = gemm_smem_bytes(n_tile, stages);
   static bool attr_set = false;
@@ -424,8 +411,30 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = g_coop ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, gemm_bf16_tc, mw, mx, epi, sk, n_tile, stages, ws, counters,
-                            packed ? reinterpret_cast<const uint8_t*>(W) : nullptr);
+  return cudaLaunchKernelEx(&cfg, gemm_bf16_tc, reinterpret_cast<const uint8_t*>(W),
+                            reinterpret_cast<const uint8_t*>(X), epi, sk, n_tile, stages, ws, counters);
+}
+
+// ------------------------------------------------------------------ operand packing
+__global__ void pack_operand_kernel(const __nv_bfloat16* __restrict__ src, int rows, int cols, int ld,
+                                    __nv_bfloat16* __restrict__ dst, int R, int KB) {
+  const int row = blockIdx.x;
+  if (row >= rows) return;
+  for (int c8 = threadIdx.x * 8; c8 < cols; c8 += blockDim.x * 8) {
+    if (c8 + 8 <= cols && (ld & 7) == 0) {
+      *reinterpret_cast<uint4*>(dst + packed_off(row, c8, R, KB)) =
+          *reinterpret_cast<const uint4*>(src + (long)row * ld + c8);
+    } else {
+      for (int k = c8; k < c8 + 8 && k < cols; ++k) dst[packed_off(row, k, R, KB)] = src[(long)row * ld + k];
+    }
+  }
+}
+
+cudaError_t launch_pack(const void* src, int rows, int cols, int ld, void* dst, int R, int KB, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  pack_operand_kernel<<<rows, 128, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(src), rows, cols, ld,
+                                           reinterpret_cast<__nv_bfloat16*>(dst), R, KB);
+  return cudaGetLastError();
 }
 
 }  // namespace vlc

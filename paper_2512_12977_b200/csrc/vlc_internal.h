@@ -23,7 +23,7 @@ using GemmEpi = vlc_epilogue;
 extern int g_stage_override;  // experiment knob (vlc_set_tuning key 1)
 extern int g_coop;            // key 2: cooperative launch of the stream-K GEMM
 void set_debug_buffer(unsigned long long* p);
-void set_exp_mode(int m);
+
 
 // tensor maps (driver entry point resolved through the runtime, no -lcuda)
 cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
@@ -35,7 +35,9 @@ cudaError_t make_tmap_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64
 
 cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap,
                         int m_tokens, const GemmEpi& epi, int max_ctas, float* ws, size_t ws_bytes,
-                        int* counters, cudaStream_t stream, bool packed = false);
+                        int* counters, cudaStream_t stream);
+int gemm_row_tile(int m_tokens);
+cudaError_t launch_pack(const void* src, int rows, int cols, int ld, void* dst, int R, int KB, cudaStream_t s);
 
 cudaError_t launch_attention(const vlc_attn_args& a, cudaStream_t stream);
 cudaError_t launch_attn_combine(const vlc_attn_args& a, cudaStream_t stream);

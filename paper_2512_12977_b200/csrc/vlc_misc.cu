@@ -31,7 +31,8 @@ template <bool OUT_F32, int VPT>
 __global__ void __launch_bounds__(128) rmsnorm_kernel(const float* __restrict__ x, int ldx,
                                                       const float* __restrict__ g, void* __restrict__ out,
                                                       int ldo, int rows, int d,
-                                                      const int* __restrict__ row_map, float eps) {
+                                                      const int* __restrict__ row_map, float eps,
+                                                      int pk_rows, int pk_kb) {
   const int r = blockIdx.x;
   const int sr = row_map ? __ldg(row_map + r) : r;
   const float4* xr = reinterpret_cast<const float4*>(x + (long)sr * ldx);
@@ -63,7 +64,8 @@ __global__ void __launch_bounds__(128) rmsnorm_kernel(const float* __restrict__ 
       reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + (long)r * ldo)[i] = y;
     } else {
       uint2 pk = make_uint2(pack_bf16(y.x, y.y), pack_bf16(y.z, y.w));
-      reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + (long)r * ldo)[i] = pk;
+      const long off = pk_rows > 0 ? packed_off(r, 4 * i, pk_rows, pk_kb) : (long)r * ldo + 4 * i;
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + off) = pk;
     }
   }
 }
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(128) rmsnorm_kernel(const float* __restrict__ 
 template <bool OUT_F32>
 __global__ void rmsnorm_generic(const float* __restrict__ x, int ldx, const float* __restrict__ g,
                                 void* __restrict__ out, int ldo, int rows, int d,
-                                const int* __restrict__ row_map, float eps) {
+                                const int* __restrict__ row_map, float eps, int pk_rows, int pk_kb) {
   const int r = blockIdx.x;
   const int sr = row_map ? row_map[r] : r;
   const float* xr = x + (long)sr * ldx;
@@ -92,7 +94,8 @@ __global__ void rmsnorm_generic(const float* __restrict__ x, int ldx, const floa
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     const float y = (xr[i] / denom) * g[i];
     if (OUT_F32) reinterpret_cast<float*>(out)[(long)r * ldo + i] = y;
-    else reinterpret_cast<__nv_bfloat16*>(out)[(long)r * ldo + i] = __float2bfloat16_rn(y);
+    else reinterpret_cast<__nv_bfloat16*>(out)[pk_rows > 0 ? packed_off(r, i, pk_rows, pk_kb) : (long)r * ldo + i] =
+        __float2bfloat16_rn(y);
   }
 }
 
@@ -215,17 +218,13 @@ __global__ void store_pages_kernel(const void* __restrict__ src, int layers, int
 
 // ------------------------------------------------------------------ patchify
 __global__ void patchify_kernel(const float* __restrict__ px, int side, int p,
-                                __nv_bfloat16* __restrict__ out, int ldo) {
+                                __nv_bfloat16* __restrict__ out, int row0, int pk_rows, int pk_kb) {
   const int t = blockIdx.x;  // patch index, row-major over the patch grid
   const int per_row = side / p;
   const int ty = t / per_row, tx = t % per_row;
-  for (int e = threadIdx.x; e < ldo; e += blockDim.x) {
-    float v = 0.f;
-    if (e < p * p) {
-      const int py = e / p, pxx = e % p;
-      v = px[(long)(ty * p + py) * side + tx * p + pxx];
-    }
-    out[(long)t * ldo + e] = __float2bfloat16_rn(v);
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    const int py = e / p, pxx = e % p;
+    out[packed_off(row0 + t, e, pk_rows, pk_kb)] = __float2bfloat16_rn(px[(long)(ty * p + py) * side + tx * p + pxx]);
   }
 }
 
@@ -244,13 +243,13 @@ int vlc_embed_assemble_impl(float* x, int ldx, const void* embed_bf16, int d, co
 }
 
 int vlc_rmsnorm_impl(const float* x, int ldx, const float* gamma, void* out, int ldo, int out_f32,
-                     int rows, int d, const int* row_map, float eps, cudaStream_t stream) {
+                     int rows, int d, const int* row_map, float eps, int pk_rows, int pk_kb, cudaStream_t stream) {
   if (rows <= 0) return 0;
-  const bool vec = (d % 4 == 0) && (ldx % 4 == 0) && (ldo % 4 == 0) && d <= 128 * 4 * 16;
+  const bool vec = (d % 4 == 0) && (ldx % 4 == 0) && (pk_rows > 0 || ldo % 4 == 0) && d <= 128 * 4 * 16;
   const unsigned blocks = rows;
 #define VLC_RMS(VPT)                                                                                   \
-  if (out_f32) rmsnorm_kernel<true, VPT><<<blocks, 128, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps); \
-  else rmsnorm_kernel<false, VPT><<<blocks, 128, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps);
+  if (out_f32) rmsnorm_kernel<true, VPT><<<blocks, 128, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps, pk_rows, pk_kb); \
+  else rmsnorm_kernel<false, VPT><<<blocks, 128, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps, pk_rows, pk_kb);
   if (vec) {
     const int vpt = (d / 4 + 127) / 128;
     if (vpt <= 1) { VLC_RMS(1) }
@@ -259,9 +258,9 @@ int vlc_rmsnorm_impl(const float* x, int ldx, const float* gamma, void* out, int
     else if (vpt <= 8) { VLC_RMS(8) }
     else { VLC_RMS(16) }
   } else if (out_f32) {
-    rmsnorm_generic<true><<<rows, 256, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps);
+    rmsnorm_generic<true><<<rows, 256, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps, pk_rows, pk_kb);
   } else {
-    rmsnorm_generic<false><<<rows, 256, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps);
+    rmsnorm_generic<false><<<rows, 256, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps, pk_rows, pk_kb);
   }
 #undef VLC_RMS
   return (int)cudaGetLastError();
@@ -298,9 +297,11 @@ int vlc_store_write_pages_impl(const void* src, int src_f32, int layers, int tok
   return (int)cudaGetLastError();
 }
 
-int vlc_patchify_impl(const float* pixels, int side, int patch, void* out, int ldo, cudaStream_t stream) {
+int vlc_patchify_impl(const float* pixels, int side, int patch, void* out, int row0, int pk_rows, int pk_kb,
+                      cudaStream_t stream) {
   const int T = (side / patch) * (side / patch);
-  patchify_kernel<<<T, 64, 0, stream>>>(pixels, side, patch, reinterpret_cast<__nv_bfloat16*>(out), ldo);
+  patchify_kernel<<<T, 64, 0, stream>>>(pixels, side, patch, reinterpret_cast<__nv_bfloat16*>(out), row0, pk_rows,
+                                        pk_kb);
   return (int)cudaGetLastError();
 }
 

@@ -227,4 +227,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// Element offset of (row, k) in the PACKED operand layout (include/vlcache.h).
+__host__ __device__ __forceinline__ long packed_off(int row, int k, int R, int KB) {
+  const int rt = row / R, r = row - rt * R;
+  const int kb = k >> 7, atom = (k >> 6) & 1, c = (k >> 3) & 7, e = k & 7;
+  return ((((long)rt * KB + kb) * 2 + atom) * R + r) * 64 + ((c ^ (r & 7)) << 3) + e;
+}
+
 }  // namespace vlc

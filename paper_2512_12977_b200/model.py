@@ -5,8 +5,9 @@ draw order of model.py:165-210) so fingerprints and cache staleness checks are
 bit-identical to the reference.  `DeviceWeights` is the sm_100a layout the
 kernels consume:
   * every projection stored K-major (W^T, [out, in]) in bf16, `out` padded to a
-    multiple of 128 (one UMMA M tile), `in` padded to a multiple of 64 (one
-    128-byte TMA/UMMA swizzle row);
+    multiple of 128 (one UMMA M tile), `in` padded to a multiple of 128 (one
+    pipeline stage), then PACKED (include/vlcache.h): each 128 x 128 tile is one
+    contiguous, pre-swizzled 32 KB block streamed with a single bulk copy;
   * Q and K rows permuted inside each head so the RoPE pair (j, j + hd/2) lands
     in adjacent TMEM lanes (the epilogue exchanges them with one shuffle);
   * gate / up rows interleaved so the SwiGLU pair is adjacent the same way;
@@ -237,10 +238,10 @@ class DeviceWeights:
         _native.load()
         self.cfg = cfg
         d, kv, h = cfg.model_dim, cfg.kv_dim, cfg.mlp_hidden
-        self.kd = _round_up(d, 64)          # K of projections fed by d-wide rows
-        self.kkv = _round_up(kv, 64)        # K of the O projection
-        self.kh = _round_up(h, 64)          # K of the down projection
-        self.kp = _round_up(cfg.patch_size ** 2, 64)
+        self.kd = _round_up(d, 128)         # K of projections fed by d-wide rows
+        self.kkv = _round_up(kv, 128)       # K of the O projection
+        self.kh = _round_up(h, 128)         # K of the down projection
+        self.kp = _round_up(cfg.patch_size ** 2, 128)
         self.n_qkv = _round_up(3 * kv, 128)
         self.n_d = _round_up(d, 128)
         self.n_gu = _round_up(2 * h, 128)
@@ -281,9 +282,9 @@ class DeviceWeights:
         def norm(x):
             t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
             return t.float().cuda().contiguous()
-        return {"wqkv": wqkv, "wqkv_plain": wqkv_plain,
-                "wo": self._kmajor(torch, get("wo"), self.n_d, self.kkv),
-                "wgu": gu, "wd": self._kmajor(torch, get("w_down"), self.n_d, self.kh),
+        return {"wqkv": PackedWeight(wqkv), "wqkv_plain": PackedWeight(wqkv_plain),
+                "wo": PackedWeight(self._kmajor(torch, get("wo"), self.n_d, self.kkv)),
+                "wgu": PackedWeight(gu), "wd": PackedWeight(self._kmajor(torch, get("w_down"), self.n_d, self.kh)),
                 "attn_norm": norm(get("attn_norm")), "mlp_norm": norm(get("mlp_norm"))}
 
     @classmethod
@@ -295,13 +296,13 @@ class DeviceWeights:
             blk.pop("wqkv_plain")
             self.layers.append(blk)
         self.enc = self._block(torch, lambda n: w[f"enc_{n}"])
-        self.enc["patch_w"] = self._kmajor(torch, w["enc_patch_w"], self.n_d, self.kp)
+        self.enc["patch_w"] = PackedWeight(self._kmajor(torch, w["enc_patch_w"], self.n_d, self.kp))
         self.enc["patch_b"] = torch.from_numpy(w["enc_patch_b"]).cuda()
         self.enc["pos"] = torch.from_numpy(np.ascontiguousarray(w["enc_pos"])).cuda()
         self.enc["out_norm"] = torch.from_numpy(w["enc_out_norm"]).cuda()
         self.embed = torch.from_numpy(w["embed"]).cuda().to(torch.bfloat16)
         self.final_norm = torch.from_numpy(w["final_norm"]).cuda()
-        self.head = self._kmajor(torch, w["head"], self.n_vocab, self.kd)
+        self.head = PackedWeight(self._kmajor(torch, w["head"], self.n_vocab, self.kd))
         torch.cuda.synchronize()
         return self
 
@@ -325,18 +326,20 @@ class DeviceWeights:
             blk.pop("wqkv_plain")
             self.layers.append(blk)
         self.enc = self._block(torch, gen)
-        self.enc["patch_w"] = self._kmajor(torch, torch.randn(pp, d, device="cuda", generator=g) / float(np.sqrt(pp)),
-                                           self.n_d, self.kp)
+        self.enc["patch_w"] = PackedWeight(self._kmajor(
+            torch, torch.randn(pp, d, device="cuda", generator=g) / float(np.sqrt(pp)), self.n_d, self.kp))
         self.enc["patch_b"] = torch.randn(d, device="cuda", generator=g) / float(np.sqrt(d))
         self.enc["pos"] = torch.randn(cfg.tokens_per_image, d, device="cuda", generator=g)
         self.enc["out_norm"] = torch.ones(d, device="cuda")
         self.embed = torch.randn(cfg.vocab_size, d, device="cuda", generator=g).to(torch.bfloat16)
         self.final_norm = torch.ones(d, device="cuda")
-        self.head = torch.zeros(self.n_vocab, self.kd, dtype=torch.bfloat16, device="cuda")
+        head = torch.zeros(self.n_vocab, self.kd, dtype=torch.bfloat16, device="cuda")
         for r0 in range(0, cfg.vocab_size, 16384):   # chunked to bound the fp32 transient
             r1 = min(cfg.vocab_size, r0 + 16384)
-            self.head[r0:r1, :d] = (torch.randn(r1 - r0, d, device="cuda", generator=g)
-                                    / float(np.sqrt(d))).to(torch.bfloat16)
+            head[r0:r1, :d] = (torch.randn(r1 - r0, d, device="cuda", generator=g)
+                               / float(np.sqrt(d))).to(torch.bfloat16)
+        self.head = PackedWeight(head)
+        del head
         torch.cuda.synchronize()
         return self
 
@@ -353,4 +356,16 @@ class DeviceWeights:
 
     def bytes_per_layer(self) -> int:
         l0 = self.layers[0]
-        return sum(int(l0[k].numel()) * 2 for k in ("wqkv", "wo", "wgu", "wd"))
+        return sum(int(l0[k].t.numel()) * 2 for k in ("wqkv", "wo", "wgu", "wd"))
+
+
+class PackedWeight:
+    """A [n, k] K-major bf16 weight in the packed streaming layout (row tile 128)."""
+
+    def __init__(self, dense):
+        from . import _native
+        self.n, self.k = int(dense.shape[0]), int(dense.shape[1])
+        self.t = _native.pack(dense, 128)
+
+    def data_ptr(self) -> int:
+        return self.t.data_ptr()

@@ -132,28 +132,32 @@ class Runner:
 
     # ---------------------------------------------------------------- primitives
     def gemm(self, w, k_pad, x, m, epi: N.Epilogue, splits: int | None = None, name="gemm", k_valid=None):
+        """w: PackedWeight; x: packed activations (row tile N.row_tile(m)), flat bf16 tensor."""
         if m <= 0:
             return
         if splits is None:
             splits = 0                       # stream-K over all SMs
         epi.m_tokens = m
+        R = N.row_tile(m)
         kv_ = k_valid or k_pad
         nbytes = 2 * epi.n_valid * kv_ + 2 * m * kv_
         self._run(name, lambda: N.check(self.lib.vlc_gemm_bf16(
-            w.data_ptr(), w.shape[0], k_pad, x.data_ptr(), x.shape[0], m, epi, splits, self.splitk.data_ptr(),
+            w.data_ptr(), w.n, w.k, x.data_ptr(), -(-m // R) * R, m, epi, splits, self.splitk.data_ptr(),
             self.splitk.numel() * 4, self.counters.data_ptr(), _stream()), "vlc_gemm_bf16"),
             nbytes, 2 * m * epi.n_valid * kv_)
 
-    def rmsnorm(self, x, gamma, out, rows, out_f32=False, row_map=0):
+    def rmsnorm(self, x, gamma, out, rows, out_f32=False, row_map=0, pk=(0, 0)):
+        """out: fp32 row-major [rows, ld] (out_f32) or flat packed bf16 with geometry pk=(R, KB)."""
         d = self.cfg.model_dim
         if rows <= 0:
             return
+        ldo = out.shape[1] if out.dim() == 2 else d
         self._run("rmsnorm", lambda: N.check(self.lib.vlc_rmsnorm(
-            x.data_ptr(), x.shape[1], gamma.data_ptr(), out.data_ptr(), out.shape[1], int(out_f32), rows, d,
-            row_map, RMS_EPS, _stream()), "vlc_rmsnorm"), rows * d * (4 + (4 if out_f32 else 2)))
+            x.data_ptr(), x.shape[1], gamma.data_ptr(), out.data_ptr(), ldo, int(out_f32), rows, d,
+            row_map, RMS_EPS, pk[0], pk[1], _stream()), "vlc_rmsnorm"), rows * d * (4 + (4 if out_f32 else 2)))
 
     def attention(self, q, kc, vc, layer, items_ptr, n_items, comb_ptr, n_comb, qpos_ptr, rowof_ptr, out,
-                  slots, nbytes=0, flops=0):
+                  slots, nbytes=0, flops=0, pk=(0, 0)):
         torch = _torch()
         cfg = self.cfg
         hd = cfg.head_dim
@@ -162,29 +166,34 @@ class Runner:
         a = N.AttnArgs(q=q.data_ptr(), q_rows_cap=q.shape[0], kc=kc.data_ptr(), vc=vc.data_ptr(),
                        layers_cap=kc.shape[0], kv_rows_cap=kc.shape[1], layer=layer, kv=cfg.kv_dim,
                        heads=cfg.num_heads, head_dim=hd, items=items_ptr, n_items=n_items, qpos=qpos_ptr,
-                       rowof=rowof_ptr, out=out.data_ptr(), ldo=out.shape[1], ws_o=ws_o.data_ptr(),
+                       rowof=rowof_ptr, out=out.data_ptr(), ldo=cfg.kv_dim, ws_o=ws_o.data_ptr(),
                        ws_ml=ws_ml.data_ptr(), ws_slots=slots, comb=comb_ptr, n_comb=n_comb,
-                       scale_log2=math.log2(math.e) / math.sqrt(hd), counters=self.attn_counters.data_ptr())
+                       scale_log2=math.log2(math.e) / math.sqrt(hd), counters=self.attn_counters.data_ptr(),
+                       pk_rows=pk[0], pk_kb=pk[1])
         self._run("attention", lambda: N.check(self.lib.vlc_attn_pp(a, _stream()), "vlc_attn_pp"),
                   nbytes, flops)
 
     # ---------------------------------------------------------------- vision encoder (miss path)
     def encode(self, pixels_list) -> "object":
-        """GPU toy ViT (model.py:302-332) for k images -> fp32 [k*T, d] (workspace scratch)."""
+        """GPU toy ViT (model.py:302-332) for k images -> fp32 [k*T, d] (workspace scratch).
+        GEMM inputs (patches, normed rows, attention output, SwiGLU output) are PACKED."""
         torch = _torch()
         cfg, dw, ws = self.cfg, self.dw, self.enc_ws
         T, d, kv, p = cfg.tokens_per_image, cfg.model_dim, cfg.kv_dim, cfg.patch_size
         k = len(pixels_list)
         M = k * T
-        cap = max(256, M) + 256
-        patches = ws.get("patches", (cap, dw.kp), torch.bfloat16)
+        cap = -(-max(256, M) // 256) * 256
+        Rp = N.row_tile(T)
+        rows_img = -(-T // Rp) * Rp
+        RM = N.row_tile(M)
+        patches = ws.get("patches", (k * rows_img * dw.kp,), torch.bfloat16)
         xe = ws.get("xe", (cap, d), torch.float32)
-        xn = ws.get("xn", (cap, dw.kd), torch.bfloat16)
+        xn = ws.get("xn", (cap * dw.kd,), torch.bfloat16)
         qe = ws.get("qe", (cap, kv), torch.bfloat16)
         ke = ws.get("ke", (1, cap, kv), torch.bfloat16)
         ve = ws.get("ve", (1, cap, kv), torch.bfloat16)
-        att = ws.get("att", (cap, dw.kkv), torch.bfloat16)
-        hb = ws.get("h", (cap, dw.kh), torch.bfloat16)
+        att = ws.get("att", (cap * dw.kkv,), torch.bfloat16)
+        hb = ws.get("h", (cap * dw.kh,), torch.bfloat16)
         out = ws.get("out", (cap, d), torch.float32)
         side = cfg.image_side
         host = np.stack([np.asarray(px, dtype=np.float32).reshape(side, side) for px in pixels_list])
@@ -193,14 +202,15 @@ class Runner:
         E = dw.enc
         for m in range(k):
             self._run("patchify", lambda m=m: N.check(self.lib.vlc_patchify(
-                dev_px[m].data_ptr(), side, p, patches[m * T].data_ptr(), dw.kp, _stream()), "vlc_patchify"))
+                dev_px[m].data_ptr(), side, p, patches.data_ptr(), m * rows_img, Rp, dw.kp // 128, _stream()),
+                "vlc_patchify"))
         for m in range(k):
             # per-image GEMM so the positional rows line up with token t
-            xm = patches[m * T:]
-            self.gemm(E["patch_w"], dw.kp, xm, T,
+            self.gemm(E["patch_w"], dw.kp, patches[m * rows_img * dw.kp:], T,
                       _epi(kind=N.EPI_BIAS_ADD, n_valid=d, out=xe[m * T].data_ptr(), ldo=d,
                            bias=E["patch_b"].data_ptr(), add=E["pos"].data_ptr(), ld_add=d))
-        self.rmsnorm(xe, E["attn_norm"], xn, M)
+        pkd, pkkv, pkh = (RM, dw.kd // 128), (RM, dw.kkv // 128), (RM, dw.kh // 128)
+        self.rmsnorm(xe, E["attn_norm"], xn, M, pk=pkd)
         self.gemm(E["wqkv_plain"], dw.kd, xn, M,
                   _epi(kind=N.EPI_QKV_PLAIN, n_valid=3 * kv, out=qe.data_ptr(), ldo=kv, out2=ke.data_ptr(), ld2=kv,
                        out3=ve.data_ptr(), ld3=kv, seg=kv, hd=cfg.head_dim))
@@ -208,19 +218,20 @@ class Runner:
         qpos = np.full(M, T - 1, dtype=np.int32)
         it9, slots = attention_work_pp(ranges, qpos, np.full(k, T), cfg.num_heads)
         it9[:, 3] = it9[:, 8] * T
-        items, comb = np.ascontiguousarray(it9[:, :8]), np.zeros((0, 8), np.int32)
+        items = np.ascontiguousarray(it9[:, :8])
         pack = IntPack()
         pack.add("items", items)
         pack.add("comb", np.zeros((1, 8)))
         pack.add("qpos", qpos)
         pack.add("rowof", np.arange(M))
         pack.upload(ws, "enc_ints")
-        self.attention(qe, ke, ve, 0, pack.ptr("items"), len(items), pack.ptr("comb"), len(comb),
-                       pack.ptr("qpos"), pack.ptr("rowof"), att, slots)
+        self.attention(qe, ke, ve, 0, pack.ptr("items"), len(items), pack.ptr("comb"), 0,
+                       pack.ptr("qpos"), pack.ptr("rowof"), att, slots, pk=pkkv)
         self.gemm(E["wo"], dw.kkv, att, M, _epi(kind=N.EPI_RESID, n_valid=d, out=xe.data_ptr(), ldo=d))
-        self.rmsnorm(xe, E["mlp_norm"], xn, M)
+        self.rmsnorm(xe, E["mlp_norm"], xn, M, pk=pkd)
         self.gemm(E["wgu"], dw.kd, xn, M,
-                  _epi(kind=N.EPI_SWIGLU, n_valid=2 * cfg.mlp_hidden, out=hb.data_ptr(), ldo=dw.kh))
+                  _epi(kind=N.EPI_SWIGLU, n_valid=2 * cfg.mlp_hidden, out=hb.data_ptr(), ldo=dw.kh,
+                       pk_rows=pkh[0], pk_kb=pkh[1]))
         self.gemm(E["wd"], dw.kh, hb, M, _epi(kind=N.EPI_RESID, n_valid=d, out=xe.data_ptr(), ldo=d))
         self.rmsnorm(xe, E["out_norm"], out, M, out_f32=True)
         return out[:M]
@@ -239,14 +250,14 @@ class Runner:
         L, d, kv, V = cfg.num_layers, cfg.model_dim, cfg.kv_dim, cfg.vocab_size
         c = lay.c
         c0 = int(c[0])
-        R = max(256, (c0 + 127) // 128 * 128 + 128)
+        R = -(-max(256, c0) // 256) * 256          # row capacity (whole 256-row tiles)
         KVR = max(128, lay.kv_rows)
         dw.ensure_positions(max(lay.kv_rows, 1) + 1)
         ws.detach_live()
         buf = dict(
-            x=ws.get("x", (R, d), torch.float32), xn=ws.get("xn", (R, dw.kd), torch.bfloat16),
-            q=ws.get("q", (R, kv), torch.bfloat16), att=ws.get("att", (R, dw.kkv), torch.bfloat16),
-            h=ws.get("h", (R, dw.kh), torch.bfloat16), kc=ws.get("kc", (L, KVR, kv), torch.bfloat16),
+            x=ws.get("x", (R, d), torch.float32), xn=ws.get("xn", (R * dw.kd,), torch.bfloat16),
+            q=ws.get("q", (R + 256, kv), torch.bfloat16), att=ws.get("att", (R * dw.kkv,), torch.bfloat16),
+            h=ws.get("h", (R * dw.kh,), torch.bfloat16), kc=ws.get("kc", (L, KVR, kv), torch.bfloat16),
             vc=ws.get("vc", (L, KVR, kv), torch.bfloat16), kpre=ws.get("kpre", (L, R, kv), torch.bfloat16),
             logits=ws.get("logits", (max(int(c[L - 1]), 1), V), torch.float32, zero=False))
         hd = cfg.head_dim
@@ -350,7 +361,8 @@ class Runner:
         for i in range(L):
             ci = int(c[i])
             W = dw.layers[i]
-            self.rmsnorm(x, W["attn_norm"], xn, ci)
+            Ri = N.row_tile(ci)
+            self.rmsnorm(x, W["attn_norm"], xn, ci, pk=(Ri, dw.kd // 128))
             self.gemm(W["wqkv"], dw.kd, xn, ci, _epi(
                 kind=N.EPI_QKV_ROPE, n_valid=3 * kv, out=q.data_ptr(), ldo=kv,
                 out2=kc[i].data_ptr(), ld2=kv, out3=vc[i].data_ptr(), ld3=kv, out4=kpre[i].data_ptr(), ld4=kv,
@@ -360,15 +372,17 @@ class Runner:
             vis = int(lay.qpos[i, :ci].astype(np.int64).sum()) + ci
             self.attention(q, kc, vc, i, pack.ptr(f"items{i}"), len(lay.attn_items[i]), pack.ptr(f"comb{i}"),
                            len(lay.comb_items[i]), pack.ptr(f"qpos{i}"), pack.ptr(f"rowof{i}"), att, lay.attn_slots,
-                           nbytes=lay.kv_rows * kv * 4 + ci * kv * 4, flops=4 * cfg.head_dim * cfg.num_heads * vis)
+                           nbytes=lay.kv_rows * kv * 4 + ci * kv * 4, flops=4 * cfg.head_dim * cfg.num_heads * vis,
+                           pk=(Ri, dw.kkv // 128))
             self.gemm(W["wo"], dw.kkv, att, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d),
                       name="gemm_o", k_valid=kv)
-            self.rmsnorm(x, W["mlp_norm"], xn, ci)
+            self.rmsnorm(x, W["mlp_norm"], xn, ci, pk=(Ri, dw.kd // 128))
             self.gemm(W["wgu"], dw.kd, xn, ci,
-                      _epi(kind=N.EPI_SWIGLU, n_valid=2 * cfg.mlp_hidden, out=hb.data_ptr(), ldo=dw.kh),
+                      _epi(kind=N.EPI_SWIGLU, n_valid=2 * cfg.mlp_hidden, out=hb.data_ptr(), ldo=dw.kh,
+                           pk_rows=Ri, pk_kb=dw.kh // 128),
                       name="gemm_gate_up", k_valid=d)
             self.gemm(W["wd"], dw.kh, hb, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d),
                       name="gemm_down", k_valid=cfg.mlp_hidden)
-        self.rmsnorm(x, dw.final_norm, xn, cL, row_map=pack.ptr("final"))
+        self.rmsnorm(x, dw.final_norm, xn, cL, row_map=pack.ptr("final"), pk=(N.row_tile(cL), dw.kd // 128))
         self.gemm(dw.head, dw.kd, xn, cL, _epi(kind=N.EPI_F32, n_valid=V, out=logits.data_ptr(), ldo=V),
                   name="gemm_head", k_valid=d)

@@ -32,18 +32,22 @@ def _epi(nat, **kw):
 
 
 def _gemm(nat, W, X, m, epi, splits=1):
+    """W [n_pad, k_pad] and X [rows, k_pad] row-major bf16 -> packed operands -> vlc_gemm_bf16."""
     ws = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
     cnt = torch.zeros(4096, dtype=torch.int32, device="cuda")
-    nat.check(nat.load().vlc_gemm_bf16(W.data_ptr(), W.shape[0], W.shape[1], X.data_ptr(), X.shape[0], m,
+    R = nat.row_tile(m)
+    Wp = nat.pack(W, 128)
+    Xp = nat.pack(X[:m], R, rows_cap=-(-m // R) * R)
+    nat.check(nat.load().vlc_gemm_bf16(Wp.data_ptr(), W.shape[0], W.shape[1], Xp.data_ptr(), -(-m // R) * R, m,
                                        epi, splits, ws.data_ptr(), ws.numel(), cnt.data_ptr(), _stream()),
               "gemm")
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("n_pad,k_pad,m,splits", [(128, 64, 16, 1), (256, 128, 40, 1), (384, 512, 100, 3),
-                                                  (256, 256, 300, 2), (128, 1024, 256, 4), (512, 192, 1000, 1),
+@pytest.mark.parametrize("n_pad,k_pad,m,splits", [(128, 128, 16, 1), (256, 128, 40, 1), (384, 512, 100, 3),
+                                                  (256, 256, 300, 2), (128, 1024, 256, 4), (512, 256, 1000, 1),
                                                   (3584, 3584, 236, 0), (1024, 7168, 112, 0), (10752, 3584, 240, 0),
-                                                  (1280, 640, 600, 7), (512, 4096, 40, 0)])
+                                                  (1280, 768, 600, 7), (512, 4096, 40, 0)])
 def test_gemm_f32_matches_torch(nat, n_pad, k_pad, m, splits):
     g = torch.Generator(device="cuda").manual_seed(n_pad + m)
     W = torch.randn(n_pad, k_pad, device="cuda", generator=g).bfloat16()
@@ -68,6 +72,11 @@ def test_gemm_resid_and_swiglu(nat):
     assert torch.allclose(x, x0 + acc, atol=1e-4, rtol=1e-5)
     h = torch.zeros(m, n // 2, device="cuda", dtype=torch.bfloat16)
     _gemm(nat, W, X, m, _epi(nat, kind=nat.EPI_SWIGLU, n_valid=n, m_tokens=m, out=h.data_ptr(), ldo=n // 2))
+    R = nat.row_tile(m)   # packed SwiGLU output (as consumed by the down projection)
+    hp = torch.zeros(nat.packed_numel(m, n // 2, R), device="cuda", dtype=torch.bfloat16)
+    _gemm(nat, W, X, m, _epi(nat, kind=nat.EPI_SWIGLU, n_valid=n, m_tokens=m, out=hp.data_ptr(), ldo=n // 2,
+                             pk_rows=R, pk_kb=-(-(n // 2) // 128)))
+    assert torch.equal(nat.unpack(hp, m, n // 2, R), h)
     gate, up = acc[:, 0::2], acc[:, 1::2]
     ref = gate / (1 + torch.exp(-gate)) * up
     assert (h.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item()
@@ -272,3 +281,10 @@ def test_attention_pp_matches_torch(nat, hd, heads, nkeys, nq, causal):
         err = (got - ref).abs().max().item()
         assert err < 2e-2, err
     assert int(cnt.abs().sum()) == 0
+    # packed output (the O-projection's input layout)
+    R = nat.row_tile(nq)
+    outp = torch.zeros(nat.packed_numel(nq, kv, R), device="cuda", dtype=torch.bfloat16)
+    a.out, a.pk_rows, a.pk_kb = outp.data_ptr(), R, -(-kv // 128)
+    nat.check(nat.load().vlc_attn_pp(a, _stream()), "attn_pp packed")
+    torch.cuda.synchronize()
+    assert torch.equal(nat.unpack(outp, nq, kv, R), out)

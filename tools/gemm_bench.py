@@ -14,21 +14,19 @@ cnt = torch.zeros(1 << 16, dtype=torch.int32, device="cuda")
 
 def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1, packed=False, mode=0):
     nw = max(2, min(8, (1 << 30) // (n * k * 2)))   # rotate > L2 worth of weights
-    Ws = [torch.randn(n, k, device="cuda").bfloat16() for _ in range(nw)]
-    if packed:
-        Ws = [N.pack_weight(w) for w in Ws]
-    fn = lib.vlc_gemm_bf16_packed if packed else lib.vlc_gemm_bf16
-    X = torch.randn(max(256, m + 256), k, device="cuda").bfloat16()
+    Ws = [N.pack(torch.randn(n, k, device="cuda").bfloat16(), 128) for _ in range(nw)]
+    R = N.row_tile(m)
+    fn = lib.vlc_gemm_bf16
+    X = N.pack(torch.randn(m, k, device="cuda").bfloat16(), R, rows_cap=-(-m // R) * R)
     out = torch.zeros(m + 256, n, device="cuda", dtype=torch.float32)
     e = N.Epilogue()
     e.kind, e.n_valid, e.m_tokens, e.out, e.ldo = kind, n, m, out.data_ptr(), n
     lib.vlc_set_tuning(1, stages)
     lib.vlc_set_tuning(2, coop)
-    lib.vlc_set_tuning(3, mode)
     s = torch.cuda.current_stream().cuda_stream
 
     def go(W):
-        N.check(fn(W.data_ptr(), n, k, X.data_ptr(), X.shape[0], m, e, splits, ws.data_ptr(),
+        N.check(fn(W.data_ptr(), n, k, X.data_ptr(), -(-m // R) * R, m, e, splits, ws.data_ptr(),
                    ws.numel() * 4, cnt.data_ptr(), torch.cuda.current_stream().cuda_stream), "g")
     go(Ws[0])
     torch.cuda.synchronize()
@@ -52,8 +50,9 @@ def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1, packed=Fals
 
 def phases(n, k, m, ctas):
     """Per-CTA phase timestamps of one launch (DRAM-cold weights)."""
-    W = torch.randn(n, k, device="cuda").bfloat16()
-    X = torch.randn(max(256, m + 256), k, device="cuda").bfloat16()
+    R = N.row_tile(m)
+    W = N.pack(torch.randn(n, k, device="cuda").bfloat16(), 128)
+    X = N.pack(torch.randn(m, k, device="cuda").bfloat16(), R, rows_cap=-(-m // R) * R)
     out = torch.zeros(m + 256, n, device="cuda", dtype=torch.float32)
     e = N.Epilogue()
     e.kind, e.n_valid, e.m_tokens, e.out, e.ldo = N.EPI_BF16, n, m, out.data_ptr(), n
@@ -62,7 +61,7 @@ def phases(n, k, m, ctas):
     for it in range(3):
         flush.add_(1)
         lib.vlc_set_debug_buffer(dbg.data_ptr() if it == 2 else None)
-        N.check(lib.vlc_gemm_bf16(W.data_ptr(), n, k, X.data_ptr(), X.shape[0], m, e, ctas, ws.data_ptr(),
+        N.check(lib.vlc_gemm_bf16(W.data_ptr(), n, k, X.data_ptr(), -(-m // R) * R, m, e, ctas, ws.data_ptr(),
                                   ws.numel() * 4, cnt.data_ptr(), torch.cuda.current_stream().cuda_stream), "g")
         torch.cuda.synchronize()
     lib.vlc_set_debug_buffer(None)
@@ -90,9 +89,10 @@ if __name__ == "__main__":
             phases(n, kk, m, c)
     elif mode == "modes":
         for (n, k, m, c) in ((3584, 3584, 16, 28), (3584, 3584, 240, 28), (14336, 3584, 240, 112),
-                             (14336, 3584, 128, 112), (14336, 3584, 16, 112)):
-            for md in (0, 1, 2, 3):
-                run(n, k, m, c, mode=md)
+                             (14336, 3584, 128, 112), (14336, 3584, 16, 112), (10752, 3584, 240, 84),
+                             (14336, 3584, 240, 148), (10752, 3584, 240, 148), (3584, 3584, 240, 148),
+                             (3584, 7168, 240, 148), (152064, 3584, 236, 0), (14336, 3584, 4128, 0)):
+            run(n, k, m, c)
         lib.vlc_set_tuning(3, 0)
     elif mode == "packed":
         for (n, k) in ((14336, 3584), (10752, 3584), (3584, 3584), (3584, 7168)):
