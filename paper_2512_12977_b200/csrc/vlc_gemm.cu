@@ -21,7 +21,8 @@
 
 namespace vlc {
 
-constexpr int GEMM_THREADS = 192;
+constexpr int GEMM_EPI_WARPS = 8;                  // two groups of 4 (one warp per TMEM lane quadrant)
+constexpr int GEMM_THREADS = 64 + 32 * GEMM_EPI_WARPS;
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 128;   // one stage = two 64-element (128 B) swizzle atoms along K
 constexpr int GEMM_ATOM_K = 64;
@@ -35,10 +36,11 @@ __device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) 
 // Final values of 4 consecutive DEVICE features [F, F+4) of token j (token-major group).
 // Device feature order: q/k rows permuted so RoPE pairs are adjacent (F, F+1), gate/up
 // interleaved (gate f at 2f, up f at 2f+1); see model.py DeviceWeights.
+template <int KIND>
 __device__ __forceinline__ void write_group(const GemmEpi& e, int F, int j, float4 v) {
   if (F >= e.n_valid) return;
   const bool full4 = F + 4 <= e.n_valid;
-  switch (e.kind) {
+  switch (KIND) {
     case EPI_F32: {
       const long r = e.map1 ? __ldg(e.map1 + j) : j;
       float* o = reinterpret_cast<float*>(e.out) + r * e.ldo + F;
@@ -146,6 +148,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define DBG(slot) do { if (g_dbg) g_dbg[blockIdx.x * 8 + (slot)] = gtimer(); } while (0)
 
+template <int KIND>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc(const uint8_t* __restrict__ wp, const uint8_t* __restrict__ xp, GemmEpi epi, SkSched sk,
                  int n_tile, int stages, float* ws, int* counters) {
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* acc_full = empty + stages;   // [2]
   uint64_t* acc_empty = acc_full + 2;    // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  float* stage_buf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(acc_empty) + 64);  // [32][128] fp32
+  float* stage_all = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(acc_empty) + 64);  // [2][32][128] fp32
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int g = blockIdx.x;
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&acc_full[s], 1);
-      mbar_init(&acc_empty[s], 128);
+      mbar_init(&acc_empty[s], 32 * GEMM_EPI_WARPS);
     }
     fence_barrier_init();
   }
@@ -242,12 +245,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     __syncwarp();
   } else {
-    // ---------------- epilogue warps 2..5 (threads 64..191)
+    // ---------------- epilogue warps 2..9: group eg = 0/1 takes alternate 32-column chunks.
     // TMEM (thread = weight row) -> smem stage [32 tokens][128 rows] -> token-major float4
     // groups written coalesced (write_group), or raw partial rows for split tiles.
     const int quad = warp & 3;
+    const int eg = (warp - 2) >> 2;
     const int row = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    float* stage_buf = stage_all + eg * 32 * 128;
+    const int bar_id = 1 + eg;
+    const bool leader = (threadIdx.x == 64);
     int seg = 0;
     for (int t = t_first; t <= t_last; ++t, ++seg) {
       const long long tb = (long long)t * sk.KB;
@@ -256,69 +263,73 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int slot = seg & 1;
       mbar_wait(&acc_full[slot], (seg >> 1) & 1);
       tc_fence_after();
-      if (threadIdx.x == 64) DBG(3);
+      if (leader) DBG(3);
       const uint32_t d = tmem + slot * 256 + lane_off;
       const bool split = gf != gl;
       float* part = split ? ws + ((long)gf * SK_MAX_PART + (g - gf)) * (long)n_tile * GEMM_BM : nullptr;
-      for (int c = 0; c < n_tile; c += 32) {
+      const int nch = (n_tile + 31) / 32;
+      for (int ci = eg; ci < nch; ci += 2) {
+        const int c = ci * 32;
         float v[32];
         tmem_ld32(d + c, v);
         tmem_wait_ld();
-        if (c + 32 >= n_tile) {  // last TMEM read of this accumulator: release it to the MMA warp
-          tc_fence_before();
-          mbar_arrive(&acc_empty[slot]);
-        }
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) stage_buf[jj * 128 + row] = v[jj];
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        for (int jj = quad; jj < 32; jj += 4) {
-          const int jt = c + jj;   // token index inside the tile
-          if (jt >= n_tile) break;
-          const float4 val = *reinterpret_cast<const float4*>(stage_buf + jj * 128 + 4 * lane);
-          if (split) {
-            __stcg(reinterpret_cast<float4*>(part + (long)jt * GEMM_BM) + lane, val);
-          } else if (tok0 + jt < epi.m_tokens) {
-            write_group(epi, m0 + 4 * lane, tok0 + jt, val);
-          }
+        asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+        const int jmax = min(32, n_tile - c);
+        if (split) {
+          for (int jj = quad; jj < jmax; jj += 4)
+            __stcg(reinterpret_cast<float4*>(part + (long)(c + jj) * GEMM_BM) + lane,
+                   *reinterpret_cast<const float4*>(stage_buf + jj * 128 + 4 * lane));
+        } else {
+          const int jv = min(jmax, epi.m_tokens - tok0 - c);
+          for (int jj = quad; jj < jv; jj += 4)
+            write_group<KIND>(epi, m0 + 4 * lane, tok0 + c + jj,
+                              *reinterpret_cast<const float4*>(stage_buf + jj * 128 + 4 * lane));
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
       }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[slot]);   // this thread's TMEM reads of the accumulator are done
       if (split) {
         __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (threadIdx.x == 64) atomicAdd(&counters[2 * gf], 1);
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+        if (leader) atomicAdd(&counters[2 * gf], 1);
       }
     }
-    if (threadIdx.x == 64) DBG(4);
+    if (leader) DBG(4);
     // ---- parallel fixup of the split tiles this CTA touched: participant p of nseg owns a
     // contiguous token range of the tile; partials are token-major rows of 128 fp32.
+    const int ew = warp - 2;   // 0..7
     for (int t = t_first; t <= t_last; ++t) {
       const long long tb = (long long)t * sk.KB;
       const int gf = sk.cta_of(tb), gl = sk.cta_of(tb + sk.KB - 1);
       if (gf == gl) continue;
       const int nseg = gl - gf + 1, p = g - gf;
-      if (threadIdx.x == 64) {
+      if (leader) {
         volatile int* cnt = counters + 2 * gf;
         while (*cnt < nseg) __nanosleep(32);
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 3, 256;" ::: "memory");
       __threadfence();
-      if (threadIdx.x == 64) DBG(5);
+      if (leader) DBG(5);
       const int m0 = (t % sk.m_tiles) * GEMM_BM, tok0 = (t / sk.m_tiles) * n_tile;
-      const int j_lo = n_tile * p / nseg, j_hi = n_tile * (p + 1) / nseg;
+      const int j_lo = n_tile * p / nseg, j_hi = min(n_tile * (p + 1) / nseg, epi.m_tokens - tok0);
       const float* base = ws + (long)gf * SK_MAX_PART * n_tile * GEMM_BM;
       const long pstride = (long)n_tile * GEMM_BM;
-      for (int jt = j_lo + quad; jt < j_hi; jt += 4) {
-        if (tok0 + jt >= epi.m_tokens) break;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int s2 = 0; s2 < nseg; ++s2) {
-          const float4 x = __ldcg(reinterpret_cast<const float4*>(base + s2 * pstride + (long)jt * GEMM_BM) + lane);
-          acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
-        }
-        write_group(epi, m0 + 4 * lane, tok0 + jt, acc);
+      for (int jt = j_lo + ew; jt < j_hi; jt += GEMM_EPI_WARPS) {
+        float4 x[SK_MAX_PART];
+#pragma unroll
+        for (int s2 = 0; s2 < SK_MAX_PART; ++s2)
+          if (s2 < nseg) x[s2] = __ldcg(reinterpret_cast<const float4*>(base + s2 * pstride + (long)jt * GEMM_BM) + lane);
+        float4 acc = x[0];
+#pragma unroll
+        for (int s2 = 1; s2 < SK_MAX_PART; ++s2)
+          if (s2 < nseg) { acc.x += x[s2].x; acc.y += x[s2].y; acc.z += x[s2].z; acc.w += x[s2].w; }
+        write_group<KIND>(epi, m0 + 4 * lane, tok0 + jt, acc);
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (threadIdx.x == 64) {
+      asm volatile("bar.sync 3, 256;" ::: "memory");
+      if (leader) {
         if (atomicAdd(&counters[2 * gf + 1], 1) == nseg - 1) {
           counters[2 * gf] = 0;
           counters[2 * gf + 1] = 0;
@@ -344,15 +355,15 @@ int g_coop = 1;
 static int gemm_pick_stages(int n_tile) {
   if (g_stage_override > 0) return g_stage_override;
   const int per = GEMM_BM * GEMM_BK * 2 + n_tile * GEMM_BK * 2;
-  int s = (210 * 1024 - 16 * 1024) / per;
+  int s = (222 * 1024 - 32 * 1024) / per;
   if (s > 8) s = 8;
   if (s < 2) s = 2;
   return s;
 }
 
 static int gemm_smem_bytes(int n_tile, int stages) {
-  // pipeline stages + barriers (64 B reserved) + 16 KB epilogue staging tile
-  return 1024 + stages * (GEMM_BM * GEMM_BK * 2 + n_tile * GEMM_BK * 2) + (2 * stages + 2) * 8 + 64 + 32 * 128 * 4;
+  // pipeline stages + barriers (64 B reserved) + two 16 KB epilogue staging tiles
+  return 1024 + stages * (GEMM_BM * GEMM_BK * 2 + n_tile * GEMM_BK * 2) + (2 * stages + 2) * 8 + 64 + 2 * 32 * 128 * 4;
 }
 
 static int num_sms() {
@@ -395,11 +406,6 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   }
   const int stages = gemm_pick_stages(n_tile);
   const int smem = gemm_smem_bytes(n_tile, stages);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm_bf16_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    attr_set = true;
-  }
   SkSched sk{U, G, KB, m_tiles};
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(G);
@@ -411,8 +417,29 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = g_coop ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, gemm_bf16_tc, reinterpret_cast<const uint8_t*>(W),
-                            reinterpret_cast<const uint8_t*>(X), epi, sk, n_tile, stages, ws, counters);
+  const uint8_t* wpp = reinterpret_cast<const uint8_t*>(W);
+  const uint8_t* xpp = reinterpret_cast<const uint8_t*>(X);
+#define VLC_GEMM_KIND(K)                                                                              \
+  case K: {                                                                                           \
+    static bool attr = false;                                                                         \
+    if (!attr) {                                                                                      \
+      cudaFuncSetAttribute(gemm_bf16_tc<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);     \
+      attr = true;                                                                                    \
+    }                                                                                                 \
+    return cudaLaunchKernelEx(&cfg, gemm_bf16_tc<K>, wpp, xpp, epi, sk, n_tile, stages, ws, counters); \
+  }
+  switch (epi.kind) {
+    VLC_GEMM_KIND(EPI_F32)
+    VLC_GEMM_KIND(EPI_RESID)
+    VLC_GEMM_KIND(EPI_BF16)
+    VLC_GEMM_KIND(EPI_BIAS_ADD)
+    VLC_GEMM_KIND(EPI_SWIGLU)
+    VLC_GEMM_KIND(EPI_QKV_PLAIN)
+    VLC_GEMM_KIND(EPI_QKV_ROPE)
+    default:
+      return cudaErrorInvalidValue;
+  }
+#undef VLC_GEMM_KIND
 }
 
 // ------------------------------------------------------------------ operand packing

@@ -84,8 +84,8 @@ if __name__ == "__main__":
     import numpy as np  # noqa: F811
     mode = sys.argv[1] if len(sys.argv) > 1 else "sweep"
     if mode == "phases":
-        for (n, kk, m, c) in ((3584, 3584, 16, 28), (3584, 3584, 16, 148), (3584, 3584, 240, 28),
-                              (3584, 3584, 240, 148), (14336, 3584, 240, 112), (14336, 3584, 240, 148)):
+        for (n, kk, m, c) in ((14336, 3584, 240, 112), (14336, 3584, 16, 112), (3584, 3584, 240, 148),
+                              (14336, 3584, 240, 148)):
             phases(n, kk, m, c)
     elif mode == "modes":
         for (n, k, m, c) in ((3584, 3584, 16, 28), (3584, 3584, 240, 28), (14336, 3584, 240, 112),
