@@ -396,6 +396,10 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   const long long U = (long long)m_tiles * tok_tiles * KB;
   int G = num_sms();
   if (max_ctas > 0 && max_ctas < G) G = max_ctas;
+  // automatic schedule: enough weight tiles -> one CTA per tile (no split-K fixup); few tiles
+  // (the d x d projections) -> stream-K over every SM
+  const long long tiles = (long long)m_tiles * tok_tiles;
+  if (max_ctas == 0 && tiles >= 64 && tiles <= G) G = (int)tiles;
   const int min_units = (KB + 5) / 6;  // keeps <= 8 participants per split tile
   if ((long long)G * min_units > U) G = (int)(U / min_units);
   if (G < 1) G = 1;
