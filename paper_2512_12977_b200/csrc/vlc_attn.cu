@@ -329,6 +329,15 @@ static cudaError_t launch_attn_hd(const vlc_attn_args& a, cudaStream_t stream) {
 // tensor core works on the other group's S / PV.  TMEM: S_A, S_B (64 cols fp32), P_A, P_B
 // (32 cols of packed bf16 pairs, the A operand of the PV MMA), O_A, O_B (HD cols fp32).
 constexpr int PP_THREADS = 320;
+__device__ unsigned long long* g_attn_dbg = nullptr;  // per-CTA phase timestamps (experiments)
+__device__ __forceinline__ void adbg(int slot) {
+  if (g_attn_dbg) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_attn_dbg[blockIdx.x * 8 + slot] = t;
+  }
+}
+void set_attn_debug_buffer(unsigned long long* p) { cudaMemcpyToSymbol(g_attn_dbg, &p, sizeof(p)); }
 constexpr int PP_KT = 64;
 constexpr int PP_ST = 3;
 
@@ -382,6 +391,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
 
   const uint32_t warp = warp_id(), lane = lane_id();
   if (warp == 0 && lane == 0) {
+    adbg(0);
     tma_prefetch(&map_q);
     tma_prefetch(&map_k);
     tma_prefetch(&map_v);
@@ -434,6 +444,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       const uint32_t idesc_s = make_idesc_bf16(128, PP_KT, 0, 0);
       const uint32_t idesc_o = make_idesc_bf16(128, HD, 0, 1);
       mbar_wait(q_full, 0);
+      adbg(1);
       auto issue_s = [&](int x, int j) {
         const int st = j % PP_ST;
         mbar_wait(&kv_full[st], (j / PP_ST) & 1);
@@ -472,6 +483,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         }
         tc_commit(&kv_empty[j % PP_ST]);
       }
+      adbg(2);
     }
     __syncwarp();
   } else {
@@ -546,6 +558,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       mbar_wait(&o_done[x], (ntx - 1) & 1);
       tc_fence_after();
     }
+    if (r == 0) adbg(3 + x);
     const int qrow = q_row0 + x * 128 + r;
     if (group < 0) {
       const float inv = (l_run > 0.f) ? 1.0f / l_run : 0.f;
@@ -610,6 +623,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   }
   __syncthreads();
   __threadfence();
+  if (threadIdx.x == 0) adbg(5);
   const int r_lo = 256 * part / nsplit, r_hi = min(nq, 256 * (part + 1) / nsplit);
   constexpr int C4 = HD / 4;
   for (int w = threadIdx.x; w < (r_hi - r_lo) * C4; w += PP_THREADS) {
@@ -638,6 +652,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
   }
   __syncthreads();
+  if (threadIdx.x == 0) adbg(6);
   if (threadIdx.x == 0) {
     if (atomicAdd(&a.counters[a.ws_slots + group], 1) == nsplit - 1) {
       a.counters[group] = 0;

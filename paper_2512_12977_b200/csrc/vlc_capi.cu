@@ -95,11 +95,13 @@ const char* vlc_last_error(void) { return g_err; }
 int vlc_set_tuning(int key, int value) {
   if (key == 1) { vlc::g_stage_override = value; return VLC_OK; }
   if (key == 2) { vlc::g_coop = value; return VLC_OK; }
+  if (key == 4) { vlc::set_attn_debug_buffer(nullptr); return VLC_OK; }
   return fail(VLC_ERR_INVALID, "set_tuning: unknown key");
 }
 /* Experiments only: device buffer receiving per-CTA phase timestamps of the GEMM (NULL = off). */
 int vlc_set_debug_buffer(void* p) {
   vlc::set_debug_buffer(reinterpret_cast<unsigned long long*>(p));
+  vlc::set_attn_debug_buffer(reinterpret_cast<unsigned long long*>(p));
   return VLC_OK;
   return fail(VLC_ERR_INVALID, "set_tuning: unknown key");
 }

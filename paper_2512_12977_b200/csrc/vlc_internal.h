@@ -23,6 +23,7 @@ using GemmEpi = vlc_epilogue;
 extern int g_stage_override;  // experiment knob (vlc_set_tuning key 1)
 extern int g_coop;            // key 2: cooperative launch of the stream-K GEMM
 void set_debug_buffer(unsigned long long* p);
+void set_attn_debug_buffer(unsigned long long* p);
 
 
 // tensor maps (driver entry point resolved through the runtime, no -lcuda)
