@@ -351,8 +351,8 @@ struct PPCfg {
   static constexpr int KV_BYTES = PP_KT * HD * 2;
   static constexpr int KV_ATOM = PP_KT * SWZ;
   static constexpr int SMEM = 1024 + 2 * Q_BYTES + PP_ST * 2 * KV_BYTES + 256;
-  __device__ static constexpr uint32_t s_col(int x) { return 64u * x; }
-  __device__ static constexpr uint32_t p_col(int x) { return 128u + 32u * x; }
+  // TMEM: S[x][buf] (64 fp32 cols; P bf16 pairs aliased in its first 32 cols), O[x] (HD cols)
+  __device__ static constexpr uint32_t s_col(int x, int b) { return 64u * (2 * x + b); }
   __device__ static constexpr uint32_t o_col(int x) { return 256u + (uint32_t)(HD > 64 ? HD : 64) * x; }
 };
 
@@ -370,8 +370,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + PP_ST;
-  uint64_t* s_full = kv_empty + PP_ST;   // [2]
-  uint64_t* p_full = s_full + 2;         // [2]
+  uint64_t* s_full = kv_empty + PP_ST;   // [2 tiles][2 buffers]
+  uint64_t* p_full = s_full + 4;         // [2]
   uint64_t* o_done = p_full + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
@@ -400,8 +400,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
+    for (int x = 0; x < 4; ++x) mbar_init(&s_full[x], 1);
     for (int x = 0; x < 2; ++x) {
-      mbar_init(&s_full[x], 1);
       mbar_init(&p_full[x], 128);
       mbar_init(&o_done[x], 1);
     }
@@ -418,25 +418,16 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_normal();
       mbar_expect_tx(q_full, (nq_t[1] > 0 ? 2 : 1) * C::Q_BYTES);
-      for (int x = 0; x < 2; ++x) {
-        if (nq_t[x] == 0) continue;
-#pragma unroll
-        for (int at = 0; at < C::N_ATOMS; ++at)
-          tma_load_2d(sQ + x * C::Q_BYTES + at * C::Q_ATOM, &map_q, q_full, head * HD + at * C::ATOM_E,
-                      q_row0 + x * 128, pol_q);
-      }
+      for (int x = 0; x < 2; ++x)   // one op per Q tile: 3-D view {atom elems, rows, atoms}
+        if (nq_t[x] > 0)
+          tma_load_3d(sQ + x * C::Q_BYTES, &map_q, q_full, 0, q_row0 + x * 128, head * C::N_ATOMS, pol_q);
       for (int j = 0; j < nt; ++j) {
         const int st = j % PP_ST;
         mbar_wait(&kv_empty[st], ((j / PP_ST) & 1) ^ 1);
         mbar_expect_tx(&kv_full[st], 2 * C::KV_BYTES);
-        const int krow = kv_row0 + kb + j * PP_KT;
-#pragma unroll
-        for (int at = 0; at < C::N_ATOMS; ++at) {
-          tma_load_3d(sK + st * C::KV_BYTES + at * C::KV_ATOM, &map_k, &kv_full[st], head * HD + at * C::ATOM_E,
-                      krow, a.layer, pol_kv);
-          tma_load_3d(sV + st * C::KV_BYTES + at * C::KV_ATOM, &map_v, &kv_full[st], head * HD + at * C::ATOM_E,
-                      krow, a.layer, pol_kv);
-        }
+        const int krow = kv_row0 + kb + j * PP_KT;   // one op per K / V tile: 4-D {elems, keys, atoms, layer}
+        tma_load_4d(sK + st * C::KV_BYTES, &map_k, &kv_full[st], 0, krow, head * C::N_ATOMS, a.layer, pol_kv);
+        tma_load_4d(sV + st * C::KV_BYTES, &map_v, &kv_full[st], 0, krow, head * C::N_ATOMS, a.layer, pol_kv);
       }
     }
   } else if (warp == 1) {
@@ -445,7 +436,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       const uint32_t idesc_o = make_idesc_bf16(128, HD, 0, 1);
       mbar_wait(q_full, 0);
       adbg(1);
-      auto issue_s = [&](int x, int j) {
+      auto issue_s = [&](int x, int j) {   // S[x][j&1] = Q_x K_j^T
         const int st = j % PP_ST;
         mbar_wait(&kv_full[st], (j / PP_ST) & 1);
         tc_fence_after();
@@ -457,29 +448,32 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
           const uint32_t eoff = ((k * 16) % C::ATOM_E) * 2;
           const uint64_t ad = make_sdesc(q_addr + at * C::Q_ATOM + eoff, 16, 8 * C::SWZ, C::SWZ);
           const uint64_t bd = make_sdesc(k_addr + at * C::KV_ATOM + eoff, 16, 8 * C::SWZ, C::SWZ);
-          tc_mma_f16(tmem + C::s_col(x), ad, bd, idesc_s, k > 0 ? 1u : 0u);
+          tc_mma_f16(tmem + C::s_col(x, j & 1), ad, bd, idesc_s, k > 0 ? 1u : 0u);
         }
-        tc_commit(&s_full[x]);
+        tc_commit(&s_full[2 * x + (j & 1)]);
       };
-      auto issue_pv = [&](int x, int j) {
+      auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j, P from TMEM (aliased in S[x][j&1])
         const int st = j % PP_ST;
         const uint32_t v_addr = smem_u32(sV + st * C::KV_BYTES);
 #pragma unroll
         for (int k = 0; k < PP_KT / 16; ++k) {
           const uint64_t bd = make_sdesc(v_addr + k * 16 * C::SWZ, C::KV_ATOM, 8 * C::SWZ, C::SWZ);
-          tc_mma_f16_ts(tmem + C::o_col(x), tmem + C::p_col(x) + k * 8, bd, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+          tc_mma_f16_ts(tmem + C::o_col(x), tmem + C::s_col(x, j & 1) + k * 8, bd, idesc_o,
+                        (j > 0 || k > 0) ? 1u : 0u);
         }
         tc_commit(&o_done[x]);
       };
-      for (int x = 0; x < 2; ++x)
-        if (nt_t[x] > 0) issue_s(x, 0);
+      // S runs two tiles ahead of the softmax (double-buffered per query tile)
+      for (int j = 0; j < 2; ++j)
+        for (int x = 0; x < 2; ++x)
+          if (j < nt_t[x]) issue_s(x, j);
       for (int j = 0; j < nt; ++j) {
         for (int x = 0; x < 2; ++x) {
           if (j >= nt_t[x]) continue;
           mbar_wait(&p_full[x], j & 1);
           tc_fence_after();
           issue_pv(x, j);
-          if (j + 1 < nt_t[x]) issue_s(x, j + 1);
+          if (j + 2 < nt_t[x]) issue_s(x, j + 2);   // in-order after PV(j): reuses P(j)'s columns
         }
         tc_commit(&kv_empty[j % PP_ST]);
       }
@@ -495,14 +489,14 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     const int qp = q_valid ? a.qpos[q_row0 + x * 128 + r] : -1;
     const int ntx = nt_t[x];
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const uint32_t tS = tmem + C::s_col(x) + lane_off, tP = tmem + C::p_col(x) + lane_off;
     const uint32_t tO = tmem + C::o_col(x) + lane_off;
     const float NEG_INF = -INFINITY;
     float m_run = NEG_INF, l_run = 0.f;
     for (int j = 0; j < ntx; ++j) {
       const int k0 = kb + j * PP_KT;
+      const uint32_t tS = tmem + C::s_col(x, j & 1) + lane_off;
       float s[PP_KT];
-      mbar_wait(&s_full[x], j & 1);
+      mbar_wait(&s_full[2 * x + (j & 1)], (j >> 1) & 1);
       tc_fence_after();
       tmem_ld32(tS, s);
       tmem_ld32(tS + 32, s + 32);
@@ -549,7 +543,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         pk[i] = pack_bf16(p0, p1);
       }
       l_run += lsum;
-      tmem_st32(tP, pk);
+      tmem_st32(tS, pk);   // P(j) overwrites the first 32 columns of S[x][j&1]
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&p_full[x]);
@@ -615,7 +609,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     tmem_dealloc<512>(tmem);
   }
   if (group < 0) return;
-  // ---------------- parallel merge of the nsplit partials (all CTAs of the group co-resident)
+  // ---------------- parallel merge of the nsplit partials (all CTAs of the group co-resident):
+  // one warp per output row, lane = 4 head dims, all split loads issued together
   if (threadIdx.x == 0) {
     atomicAdd(&a.counters[group], 1);
     volatile int* cnt = a.counters + group;
@@ -625,31 +620,36 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   __threadfence();
   if (threadIdx.x == 0) adbg(5);
   const int r_lo = 256 * part / nsplit, r_hi = min(nq, 256 * (part + 1) / nsplit);
-  constexpr int C4 = HD / 4;
-  for (int w = threadIdx.x; w < (r_hi - r_lo) * C4; w += PP_THREADS) {
-    const int rr = r_lo + w / C4, c4 = w % C4;
-    float mm[8];
-    float M = -INFINITY;
-    for (int s2 = 0; s2 < nsplit; ++s2) {
-      const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.ws_ml) + ((long)group * 8 + s2) * 256 + rr);
-      mm[s2] = ml.x;
-      M = fmaxf(M, ml.x);
-    }
-    float L = 0.f;
+  for (int rr = r_lo + (int)warp; rr < r_hi; rr += PP_THREADS / 32) {
+    const long pbase = (long)group * 8 * 256 + rr;
+    float2 ml = make_float2(-INFINITY, 0.f);
+    if ((int)lane < nsplit) ml = __ldcg(reinterpret_cast<const float2*>(a.ws_ml) + pbase + lane * 256);
+    float M = ml.x;
+#pragma unroll
+    for (int o = 4; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    const float wgt = (ml.x == -INFINITY) ? 0.f : exp2f(ml.x - M);
+    float L = wgt * ml.y;
+#pragma unroll
+    for (int o = 4; o; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s2 = 0; s2 < nsplit; ++s2) {
-      const long prow = ((long)group * 8 + s2) * 256 + rr;
-      const float wgt = (mm[s2] == -INFINITY) ? 0.f : exp2f(mm[s2] - M);
-      if (wgt == 0.f) continue;
-      L += wgt * __ldcg(reinterpret_cast<const float2*>(a.ws_ml) + prow).y;
-      const float4 o = __ldcg(reinterpret_cast<const float4*>(a.ws_o + prow * HD) + c4);
-      acc.x += wgt * o.x; acc.y += wgt * o.y; acc.z += wgt * o.z; acc.w += wgt * o.w;
+    for (int c4 = lane; c4 < HD / 4; c4 += 32) {
+      float4 xs[8];
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2)
+        if (s2 < nsplit) xs[s2] = __ldcg(reinterpret_cast<const float4*>(a.ws_o + (pbase + s2 * 256) * HD) + c4);
+      acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2) {
+        if (s2 >= nsplit) break;
+        const float w = __shfl_sync(0xffffffffu, wgt, s2);
+        acc.x += w * xs[s2].x; acc.y += w * xs[s2].y; acc.z += w * xs[s2].z; acc.w += w * xs[s2].w;
+      }
+      const float inv = L > 0.f ? 1.0f / L : 0.f;
+      const int orow_i = a.rowof[q_row0 + rr], col = head * HD + c4 * 4;
+      const long off = a.pk_rows > 0 ? packed_off(orow_i, col, a.pk_rows, a.pk_kb) : (long)orow_i * a.ldo + col;
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.out) + off) =
+          make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
     }
-    const float inv = L > 0.f ? 1.0f / L : 0.f;
-    const int orow_i = a.rowof[q_row0 + rr], col = head * HD + c4 * 4;
-    const long off = a.pk_rows > 0 ? packed_off(orow_i, col, a.pk_rows, a.pk_kb) : (long)orow_i * a.ldo + col;
-    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.out) + off) =
-        make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
   }
   __syncthreads();
   if (threadIdx.x == 0) adbg(6);
@@ -665,13 +665,17 @@ template <int HD>
 static cudaError_t launch_pp_hd(const vlc_attn_args& a, cudaStream_t stream, bool coop) {
   using C = PPCfg<HD>;
   CUtensorMap mq, mk, mv;
-  cudaError_t e = make_tmap_2d(&mq, a.q, a.kv, a.q_rows_cap, (uint64_t)a.kv * 2, C::ATOM_E, 128, C::SWZ);
+  // Q: {atom elems, rows, atoms} box {ATOM_E, 128, N_ATOMS}: one op = both swizzle atoms of a tile
+  cudaError_t e = make_tmap_3d(&mq, a.q, C::ATOM_E, a.q_rows_cap, a.kv / C::ATOM_E, (uint64_t)a.kv * 2,
+                               (uint64_t)C::SWZ, C::ATOM_E, 128, C::N_ATOMS, C::SWZ);
   if (e != cudaSuccess) return e;
-  e = make_tmap_3d(&mk, a.kc, a.kv, a.kv_rows_cap, a.layers_cap, (uint64_t)a.kv * 2,
-                   (uint64_t)a.kv * 2 * a.kv_rows_cap, C::ATOM_E, PP_KT, 1, C::SWZ);
+  const uint64_t dims[4] = {(uint64_t)C::ATOM_E, (uint64_t)a.kv_rows_cap, (uint64_t)(a.kv / C::ATOM_E),
+                            (uint64_t)a.layers_cap};
+  const uint64_t strides[3] = {(uint64_t)a.kv * 2, (uint64_t)C::SWZ, (uint64_t)a.kv * 2 * a.kv_rows_cap};
+  const uint32_t box[4] = {(uint32_t)C::ATOM_E, (uint32_t)PP_KT, (uint32_t)C::N_ATOMS, 1};
+  e = make_tmap_4d(&mk, a.kc, dims, strides, box, C::SWZ);
   if (e != cudaSuccess) return e;
-  e = make_tmap_3d(&mv, a.vc, a.kv, a.kv_rows_cap, a.layers_cap, (uint64_t)a.kv * 2,
-                   (uint64_t)a.kv * 2 * a.kv_rows_cap, C::ATOM_E, PP_KT, 1, C::SWZ);
+  e = make_tmap_4d(&mv, a.vc, dims, strides, box, C::SWZ);
   if (e != cudaSuccess) return e;
   static bool attr = false;
   if (!attr) {

@@ -34,6 +34,9 @@ cudaError_t make_tmap_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64
                          uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0, uint32_t b1,
                          uint32_t b2, int swizzle_bytes);
 
+cudaError_t make_tmap_4d(CUtensorMap* map, const void* base, const uint64_t* dims, const uint64_t* strides_bytes,
+                         const uint32_t* box, int swizzle_bytes);
+
 cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap,
                         int m_tokens, const GemmEpi& epi, int max_ctas, float* ws, size_t ws_bytes,
                         int* counters, cudaStream_t stream);
