@@ -7,7 +7,8 @@ tcgen05 / TMA kernels) through a C ABI; there is no CPU fallback.
 """
 from .config import ModelConfig
 from .engine import (FlopsBreakdown, ReuseMetrics, ReuseRequest, ReuseResult, count_flops, encode_image,
-                     fill_store, fill_store_request, flops_from_masks, prefill_full, prefill_with_reuse)
+                     fill_store, fill_store_request, flops_from_masks, prefill_batch_with_reuse, prefill_full,
+                     prefill_with_reuse)
 from .exceptions import (ConfigError, InputError, IntegrityError, KVReuseError, ParseError, PlanError,
                          SetupError, StaleCacheError)
 from .model import KVTensors, ToyVLM, init_model, load_model, save_weights, weight_checksum

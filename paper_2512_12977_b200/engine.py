@@ -213,7 +213,16 @@ def _text_tokens(seq: TokenSequence, cfg: ModelConfig):
     return np.array(pos, dtype=np.int64), np.array(ids, dtype=np.int64)
 
 
-def prefill_with_reuse(model: ToyVLM, request: ReuseRequest, store: CacheStore) -> ReuseResult:
+class _Resolved:
+    """Host result of the resolve phase of one request (engine.py:121-163)."""
+
+    def __init__(self, spec, metrics, enc_pool, kv_pool, miss_px):
+        self.spec, self.metrics, self.enc_pool, self.kv_pool, self.miss_px = spec, metrics, enc_pool, kv_pool, miss_px
+
+
+def _resolve(model: ToyVLM, request: ReuseRequest, store: CacheStore, miss_base: int = 0) -> _Resolved:
+    """Validation (reference order: PlanError, layer count, sequence/hash count), then per
+    image: encoder-cache lookup, KV-cache lookup, miss / fallback bookkeeping."""
     cfg = model.config
     seq, plan = request.seq, request.plan
     require_valid(plan)
@@ -226,9 +235,7 @@ def prefill_with_reuse(model: ToyVLM, request: ReuseRequest, store: CacheStore) 
     metrics = ReuseMetrics(mean_ratio=mean_ratio(plan))
     T, L = cfg.tokens_per_image, cfg.num_layers
     keep = np.repeat(layer_keep(plan, T)[:, None], len(segs), axis=1).astype(np.int32)
-    runner = _runner(model)
 
-    t0 = time.perf_counter()
     fp = model.fingerprint
     enc_src, kv_hit, page_rows, miss_px = [], [], [], []
     enc_pool = kv_pool = None
@@ -245,7 +252,7 @@ def prefill_with_reuse(model: ToyVLM, request: ReuseRequest, store: CacheStore) 
             if request.images is None or request.images[m] is None:
                 raise InputError(f"encoder cache miss for image {m} and no pixels supplied")
             _check_pixels(cfg, request.images[m])
-            enc_src.append((SRC_SCRATCH, len(miss_px) * T))
+            enc_src.append((SRC_SCRATCH, (miss_base + len(miss_px)) * T))
             miss_px.append(request.images[m])
         entry = store.get_kv(h, expected_fingerprint=fp)
         if entry is not None:
@@ -264,24 +271,59 @@ def prefill_with_reuse(model: ToyVLM, request: ReuseRequest, store: CacheStore) 
     counts = [len(text_pos) + int(keep[i].sum()) for i in range(L)]
     metrics.computed_per_layer = counts
     metrics.flops = _flops_from_counts(counts, len(seq), cfg, metrics.encoder_misses)
-    scratch = runner.encode(miss_px) if miss_px else None
-    metrics.resolve_seconds = time.perf_counter() - t0
-
     spec = RequestSpec(n=len(seq), text_pos=text_pos, text_ids=text_ids,
                        images=[(s.start, s.length) for s in segs], keep=keep, kv_hit=kv_hit,
                        enc_src=enc_src, page_rows=page_rows)
-    lay = _layout(runner, [spec], L, cfg.num_heads)
+    return _Resolved(spec, metrics, enc_pool, kv_pool, miss_px)
+
+
+def prefill_with_reuse(model: ToyVLM, request: ReuseRequest, store: CacheStore) -> ReuseResult:
+    return prefill_batch_with_reuse(model, [request], store)[0]
+
+
+def prefill_batch_with_reuse(model: ToyVLM, requests: list, store: CacheStore) -> list:
+    """Several independent reuse prefills in ONE device pass (BASELINE configs[4]): the
+    computed rows of all requests are concatenated (varlen), so every layer's GEMMs stream
+    the weights once for the whole batch; attention stays per request (own KV rows,
+    causal by position).  Result i equals prefill_with_reuse(model, requests[i], store)."""
+    if not requests:
+        return []
+    cfg = model.config
+    L = cfg.num_layers
+    runner = _runner(model)
+    t0 = time.perf_counter()
+    resolved, miss_px = [], []
+    for req in requests:
+        r = _resolve(model, req, store, miss_base=len(miss_px))
+        resolved.append(r)
+        miss_px.extend(r.miss_px)
+    enc_pools = {id(r.enc_pool): r.enc_pool for r in resolved if r.enc_pool is not None}
+    kv_pools = {id(r.kv_pool): r.kv_pool for r in resolved if r.kv_pool is not None}
+    if len(enc_pools) > 1 or len(kv_pools) > 1:
+        raise InputError("requests of one batch must resolve to one encoder pool and one KV pool")
+    enc_pool = next(iter(enc_pools.values()), None)
+    kv_pool = next(iter(kv_pools.values()), None)
+    scratch = runner.encode(miss_px) if miss_px else None
+    dt = time.perf_counter() - t0
+    for r in resolved:
+        r.metrics.resolve_seconds = dt
+
+    specs = [r.spec for r in resolved]
+    lay = _layout(runner, specs, L, cfg.num_heads)
     import torch
     ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    text_ids = np.concatenate([s.text_ids for s in specs])
     out = runner.prefill(lay, text_ids, enc_pool.rows.view(-1, cfg.model_dim) if enc_pool else None,
                          scratch, kv_pool, events=ev)
-    metrics._events = ev
-    start, cnt = lay.logit_ranges[0]
-    dev_logits = out["logits"][start:start + cnt]
-    kv = KVTensors(loader=_merged_kv_loader(out, lay, spec, kv_pool, cfg))
-    res = ReuseResult(lay.positions[0], dev_logits, kv, metrics)
-    runner.ws.live.add(res)
-    return res
+    results = []
+    for i, r in enumerate(resolved):
+        r.metrics._events = ev
+        start, cnt = lay.logit_ranges[i]
+        kv = KVTensors(loader=_merged_kv_loader(out, lay, r.spec, kv_pool, cfg, req=i))
+        res = ReuseResult(lay.positions[i], out["logits"][start:start + cnt], kv, r.metrics)
+        runner.ws.live.add(res)
+        results.append(res)
+    return results
 
 
 def _merged_kv_loader(out, lay, spec: RequestSpec, kv_pool, cfg: ModelConfig, req: int = 0):
