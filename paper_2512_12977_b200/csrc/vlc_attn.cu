@@ -412,6 +412,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();                 // Q / K / V / work lists come from the previous kernels
+  if (threadIdx.x == 0) pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0 && nt > 0) {
@@ -631,17 +633,20 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     float L = wgt * ml.y;
 #pragma unroll
     for (int o = 4; o; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    L = __shfl_sync(0xffffffffu, L, 0);            // lanes >= 8 reduced their own (empty) octet
+    float w8[8];                                   // split weights, broadcast to every lane
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2) w8[s2] = __shfl_sync(0xffffffffu, wgt, s2);
     for (int c4 = lane; c4 < HD / 4; c4 += 32) {
       float4 xs[8];
 #pragma unroll
       for (int s2 = 0; s2 < 8; ++s2)
         if (s2 < nsplit) xs[s2] = __ldcg(reinterpret_cast<const float4*>(a.ws_o + (pbase + s2 * 256) * HD) + c4);
-      acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int s2 = 0; s2 < 8; ++s2) {
         if (s2 >= nsplit) break;
-        const float w = __shfl_sync(0xffffffffu, wgt, s2);
+        const float w = w8[s2];
         acc.x += w * xs[s2].x; acc.y += w * xs[s2].y; acc.z += w * xs[s2].z; acc.w += w * xs[s2].w;
       }
       const float inv = L > 0.f ? 1.0f / L : 0.f;
@@ -661,6 +666,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   }
 }
 
+int g_attn_min_smem = 0;
+
 template <int HD>
 static cudaError_t launch_pp_hd(const vlc_attn_args& a, cudaStream_t stream, bool coop) {
   using C = PPCfg<HD>;
@@ -679,20 +686,11 @@ static cudaError_t launch_pp_hd(const vlc_attn_args& a, cudaStream_t stream, boo
   if (e != cudaSuccess) return e;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_pp_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(attn_pp_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     attr = true;
   }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(a.n_items);
-  cfg.blockDim = dim3(PP_THREADS);
-  cfg.dynamicSmemBytes = C::SMEM;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr_c[1];
-  attr_c[0].id = cudaLaunchAttributeCooperative;
-  attr_c[0].val.cooperative = 1;
-  cfg.attrs = attr_c;
-  cfg.numAttrs = coop ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, attn_pp_kernel<HD>, mq, mk, mv, a);
+  const int smem = C::SMEM > g_attn_min_smem ? C::SMEM : g_attn_min_smem;
+  return launch_chain(attn_pp_kernel<HD>, dim3(a.n_items), dim3(PP_THREADS), smem, stream, coop, mq, mk, mv, a);
 }
 
 cudaError_t launch_attention_pp(const vlc_attn_args& a, cudaStream_t stream, bool coop) {

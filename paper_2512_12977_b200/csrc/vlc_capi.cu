@@ -110,6 +110,8 @@ int vlc_set_tuning(int key, int value) {
   if (key == 1) { vlc::g_stage_override = value; return VLC_OK; }
   if (key == 2) { vlc::g_coop = value; return VLC_OK; }
   if (key == 4) { vlc::set_attn_debug_buffer(nullptr); return VLC_OK; }
+  if (key == 5) { vlc::g_attn_min_smem = value; return VLC_OK; }
+  if (key == 6) { vlc::g_pdl = value; return VLC_OK; }
   return fail(VLC_ERR_INVALID, "set_tuning: unknown key");
 }
 /* Experiments only: device buffer receiving per-CTA phase timestamps of the GEMM (NULL = off). */

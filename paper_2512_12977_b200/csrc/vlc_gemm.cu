@@ -194,7 +194,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       DBG(1);
       const uint64_t pol_w = policy_evict_first();
       const uint64_t pol_x = policy_evict_last();
-      int stage = 0;
+      // The weights do not depend on the previous kernel: fill the first ring pass with weight
+      // copies before waiting on it (programmatic dependent launch), activations after.
+      int pre = 0;
+      for (int t = t_first; t <= t_last && pre < stages; ++t) {
+        const long long tb = (long long)t * sk.KB;
+        const int kb_lo = (int)(max(u_begin, tb) - tb), kb_hi = (int)(min(u_end, tb + sk.KB) - tb);
+        const uint8_t* wsrc = wp + (long)(t % sk.m_tiles) * sk.KB * a_bytes;
+        for (int kb = kb_lo; kb < kb_hi && pre < stages; ++kb, ++pre) {
+          mbar_expect_tx(&full[pre], a_bytes + b_bytes);
+          bulk_load(sa + pre * a_bytes, wsrc + (long)kb * a_bytes, a_bytes, &full[pre], pol_w);
+        }
+      }
+      pdl_wait();
+      int stage = 0, u = 0;
       uint32_t phase = 0;
       for (int t = t_first; t <= t_last; ++t) {
         const long long tb = (long long)t * sk.KB;
@@ -202,10 +215,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int m0 = (t % sk.m_tiles) * GEMM_BM, tok0 = (t / sk.m_tiles) * n_tile;
         const uint8_t* wsrc = wp + (long)(m0 / GEMM_BM) * sk.KB * a_bytes;
         const uint8_t* xsrc = xp + (long)(tok0 / n_tile) * sk.KB * b_bytes;
-        for (int kb = kb_lo; kb < kb_hi; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], a_bytes + b_bytes);
-          bulk_load(sa + stage * a_bytes, wsrc + (long)kb * a_bytes, a_bytes, &full[stage], pol_w);
+        for (int kb = kb_lo; kb < kb_hi; ++kb, ++u) {
+          if (u >= pre) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], a_bytes + b_bytes);
+            bulk_load(sa + stage * a_bytes, wsrc + (long)kb * a_bytes, a_bytes, &full[stage], pol_w);
+          }
           bulk_load(sb + stage * b_bytes, xsrc + (long)kb * b_bytes, b_bytes, &full[stage], pol_x);
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
@@ -245,6 +260,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     __syncwarp();
   } else {
+    pdl_wait();                     // outputs / residual rows belong to the previous kernels
+    if (threadIdx.x == 64) pdl_trigger();
     // ---------------- epilogue warps 2..9: group eg = 0/1 takes alternate 32-column chunks.
     // TMEM (thread = weight row) -> smem stage [32 tokens][128 rows] -> token-major float4
     // groups written coalesced (write_group), or raw partial rows for split tiles.
@@ -351,6 +368,7 @@ int g_stage_override = 0;
 void set_debug_buffer(unsigned long long* p) { cudaMemcpyToSymbol(g_dbg, &p, sizeof(p)); }
 
 int g_coop = 1;
+int g_pdl = 1;
 
 static int gemm_pick_stages(int n_tile) {
   if (g_stage_override > 0) return g_stage_override;
@@ -411,16 +429,6 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   const int stages = gemm_pick_stages(n_tile);
   const int smem = gemm_smem_bytes(n_tile, stages);
   SkSched sk{U, G, KB, m_tiles};
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(G);
-  cfg.blockDim = dim3(GEMM_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = g_coop ? 1 : 0;
   const uint8_t* wpp = reinterpret_cast<const uint8_t*>(W);
   const uint8_t* xpp = reinterpret_cast<const uint8_t*>(X);
 #define VLC_GEMM_KIND(K)                                                                              \
@@ -430,7 +438,8 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
       cudaFuncSetAttribute(gemm_bf16_tc<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);     \
       attr = true;                                                                                    \
     }                                                                                                 \
-    return cudaLaunchKernelEx(&cfg, gemm_bf16_tc<K>, wpp, xpp, epi, sk, n_tile, stages, ws, counters); \
+    return launch_chain(gemm_bf16_tc<K>, dim3(G), dim3(GEMM_THREADS), smem, stream, g_coop != 0, wpp, xpp, epi, \
+                        sk, n_tile, stages, ws, counters);                                            \
   }
   switch (epi.kind) {
     VLC_GEMM_KIND(EPI_F32)

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <utility>
 
 #include "../../include/vlcache.h"
 #include "vlc_ptx.cuh"
@@ -21,8 +22,36 @@ enum EpiKind {
 using GemmEpi = vlc_epilogue;
 
 extern int g_stage_override;  // experiment knob (vlc_set_tuning key 1)
+extern int g_attn_min_smem;   // key 5: lower bound on the attention kernel's dynamic smem
 extern int g_coop;            // key 2: cooperative launch of the stream-K GEMM
+extern int g_pdl;             // key 6: programmatic dependent launch of the chain kernels (default 1)
 void set_debug_buffer(unsigned long long* p);
+
+// Launch with programmatic stream serialization (g_pdl) and optionally cooperative residency
+// (only when PDL is off: the kernels that rely on co-residency size their grids to <= #SMs).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_chain(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                         bool coop, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (g_pdl) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  } else if (coop) {
+    at[n].id = cudaLaunchAttributeCooperative;
+    at[n].val.cooperative = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 void set_attn_debug_buffer(unsigned long long* p);
 
 

@@ -11,6 +11,8 @@ __global__ void embed_assemble_kernel(float* __restrict__ x, int ldx,
                                       const float* __restrict__ enc_a,
                                       const float* __restrict__ enc_b,
                                       const int2* __restrict__ src, int rows) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   if (r >= rows) return;
   const int2 s = src[r];
@@ -33,6 +35,8 @@ __global__ void __launch_bounds__(128) rmsnorm_kernel(const float* __restrict__ 
                                                       int ldo, int rows, int d,
                                                       const int* __restrict__ row_map, float eps,
                                                       int pk_rows, int pk_kb) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   const int sr = row_map ? __ldg(row_map + r) : r;
   const float4* xr = reinterpret_cast<const float4*>(x + (long)sr * ldx);
@@ -75,6 +79,8 @@ template <bool OUT_F32>
 __global__ void rmsnorm_generic(const float* __restrict__ x, int ldx, const float* __restrict__ g,
                                 void* __restrict__ out, int ldo, int rows, int d,
                                 const int* __restrict__ row_map, float eps, int pk_rows, int pk_kb) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   const int sr = row_map ? row_map[r] : r;
   const float* xr = x + (long)sr * ldx;
@@ -139,6 +145,8 @@ __global__ void __launch_bounds__(RELOC_THREADS)
                        int kv_rows_cap, const int* __restrict__ descs,
                        const int2* __restrict__ blocks, const float* __restrict__ cos_tab,
                        const float* __restrict__ sin_tab, int tab_ld) {
+  pdl_wait();
+  pdl_trigger();
   const int2 blk = blocks[blockIdx.x];
   const int* dsc = descs + blk.x * 8;
   const int layer = dsc[0], pt_off = dsc[1], tok0 = dsc[2], ntok = dsc[3];
@@ -237,9 +245,9 @@ extern "C" {
 int vlc_embed_assemble_impl(float* x, int ldx, const void* embed_bf16, int d, const float* enc_a,
                             const float* enc_b, const int* src, int rows, cudaStream_t stream) {
   if (rows <= 0) return 0;
-  embed_assemble_kernel<<<rows, 256, 0, stream>>>(x, ldx, reinterpret_cast<const __nv_bfloat16*>(embed_bf16),
-                                                  d, enc_a, enc_b, reinterpret_cast<const int2*>(src), rows);
-  return (int)cudaGetLastError();
+  return (int)launch_chain(embed_assemble_kernel, dim3(rows), dim3(256), 0, stream, false, x, ldx,
+                           reinterpret_cast<const __nv_bfloat16*>(embed_bf16), d, enc_a, enc_b,
+                           reinterpret_cast<const int2*>(src), rows);
 }
 
 int vlc_rmsnorm_impl(const float* x, int ldx, const float* gamma, void* out, int ldo, int out_f32,
@@ -247,9 +255,10 @@ int vlc_rmsnorm_impl(const float* x, int ldx, const float* gamma, void* out, int
   if (rows <= 0) return 0;
   const bool vec = (d % 4 == 0) && (ldx % 4 == 0) && (pk_rows > 0 || ldo % 4 == 0) && d <= 128 * 4 * 16;
   const unsigned blocks = rows;
+  cudaError_t e = cudaSuccess;
 #define VLC_RMS(VPT)                                                                                   \
-  if (out_f32) rmsnorm_kernel<true, VPT><<<blocks, 128, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps, pk_rows, pk_kb); \
-  else rmsnorm_kernel<false, VPT><<<blocks, 128, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps, pk_rows, pk_kb);
+  e = launch_chain(out_f32 ? rmsnorm_kernel<true, VPT> : rmsnorm_kernel<false, VPT>, dim3(blocks), dim3(128), 0, \
+                   stream, false, x, ldx, gamma, out, ldo, rows, d, row_map, eps, pk_rows, pk_kb);
   if (vec) {
     const int vpt = (d / 4 + 127) / 128;
     if (vpt <= 1) { VLC_RMS(1) }
@@ -257,13 +266,12 @@ int vlc_rmsnorm_impl(const float* x, int ldx, const float* gamma, void* out, int
     else if (vpt <= 4) { VLC_RMS(4) }
     else if (vpt <= 8) { VLC_RMS(8) }
     else { VLC_RMS(16) }
-  } else if (out_f32) {
-    rmsnorm_generic<true><<<rows, 256, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps, pk_rows, pk_kb);
   } else {
-    rmsnorm_generic<false><<<rows, 256, 0, stream>>>(x, ldx, gamma, out, ldo, rows, d, row_map, eps, pk_rows, pk_kb);
+    e = launch_chain(out_f32 ? rmsnorm_generic<true> : rmsnorm_generic<false>, dim3(rows), dim3(256), 0, stream,
+                     false, x, ldx, gamma, out, ldo, rows, d, row_map, eps, pk_rows, pk_kb);
   }
 #undef VLC_RMS
-  return (int)cudaGetLastError();
+  return (int)e;
 }
 
 int vlc_kv_relocate_impl(const void* kpool, const void* vpool, int page_tokens, const int* page_table,
@@ -271,12 +279,11 @@ int vlc_kv_relocate_impl(const void* kpool, const void* vpool, int page_tokens, 
                          const int* blocks, int n_blocks, const float* cos_tab, const float* sin_tab,
                          int tab_ld, cudaStream_t stream) {
   if (n_blocks <= 0) return 0;
-  kv_relocate_kernel<<<n_blocks, RELOC_THREADS, 0, stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(kpool), reinterpret_cast<const __nv_bfloat16*>(vpool),
-      page_tokens, page_table, kv, head_dim, reinterpret_cast<__nv_bfloat16*>(kc),
-      reinterpret_cast<__nv_bfloat16*>(vc), kv_rows_cap, descs, reinterpret_cast<const int2*>(blocks),
-      cos_tab, sin_tab, tab_ld);
-  return (int)cudaGetLastError();
+  return (int)launch_chain(kv_relocate_kernel, dim3(n_blocks), dim3(RELOC_THREADS), 0, stream, false,
+                           reinterpret_cast<const __nv_bfloat16*>(kpool), reinterpret_cast<const __nv_bfloat16*>(vpool),
+                           page_tokens, page_table, kv, head_dim, reinterpret_cast<__nv_bfloat16*>(kc),
+                           reinterpret_cast<__nv_bfloat16*>(vc), kv_rows_cap, descs,
+                           reinterpret_cast<const int2*>(blocks), cos_tab, sin_tab, tab_ld);
 }
 
 int vlc_store_write_pages_impl(const void* src, int src_f32, int layers, int tokens, int kv,

@@ -15,6 +15,7 @@ from .layout import Layout, attention_work_pp
 from .model import RMS_EPS, DeviceWeights
 
 N_SMS = 148
+_DEBUG_SYNC = bool(int(__import__("os").environ.get("VLC_DEBUG_SYNC", "0")))  # sync + log every launch
 
 
 def _torch():
@@ -119,7 +120,17 @@ class Runner:
 
     def _run(self, name, fn, nbytes=0, flops=0, kernels=1):
         """Issue one C-ABI call; optionally bracket it with CUDA events on the current stream."""
-        if self.tracer is None:
+        if _DEBUG_SYNC:
+            import sys
+            import time
+            sys.stderr.write(f"[vlc] {name} ...")
+            sys.stderr.flush()
+            t0 = time.perf_counter()
+            fn()
+            _torch().cuda.synchronize()
+            sys.stderr.write(f" {1e3 * (time.perf_counter() - t0):.3f} ms\n")
+            sys.stderr.flush()
+        elif self.tracer is None:
             fn()
         else:
             torch = _torch()
@@ -276,7 +287,7 @@ class Runner:
         chain = lambda: self._chain(lay, pack, buf, ptrs)  # noqa: E731
         if events is not None:
             events[0].record()
-        if use_graph and self.tracer is None:
+        if use_graph and self.tracer is None and not _DEBUG_SYNC:
             skey = getattr(lay, "_skey", None)
             if skey is None:
                 skey = lay._skey = lay.structure_key()
