@@ -510,14 +510,19 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         s[i] = (i <= lim) ? s[i] * a.scale_log2 : NEG_INF;
         tmax = fmaxf(tmax, s[i]);
       }
-      if (j > 0) {
-        mbar_wait(&o_done[x], (j - 1) & 1);
-        tc_fence_after();
-      }
       const float m_new = fmaxf(m_run, tmax);
       const bool need = m_new > m_run + 8.0f;
       const bool has_o = m_run != NEG_INF;
-      if (__any_sync(0xffffffffu, need && has_o)) {
+      // O is only touched when some row rescales; P(j) goes to S buffer j&1, whose previous P
+      // (PV(j-2)) is complete because S(j) was issued after it.  So PV(j-1) is waited for only
+      // when rescaling, and on the last tile (so that the final wait below is unambiguous):
+      // o_done has completed j-1 or j phases here (S(j) done => PV(j-2) done).
+      const bool resc = __any_sync(0xffffffffu, need && has_o);
+      if (j > 0 && (resc || j == ntx - 1)) {
+        mbar_wait(&o_done[x], (j - 1) & 1);
+        tc_fence_after();
+      }
+      if (resc) {
         const float sc = (need && has_o) ? exp2f(m_run - m_new) : 1.0f;
 #pragma unroll
         for (int c = 0; c < HD / 16; ++c) {
@@ -550,7 +555,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       tc_fence_before();
       mbar_arrive(&p_full[x]);
     }
-    if (ntx > 0) {
+    if (ntx > 0) {   // o_done has completed ntx-1 or ntx phases here
       mbar_wait(&o_done[x], (ntx - 1) & 1);
       tc_fence_after();
     }

@@ -105,13 +105,18 @@ class Runner:
     def __init__(self, dw: DeviceWeights):
         self.dw = dw
         self.cfg = dw.cfg
-        self.ws = Workspace()
+        # Two output/workspace sets used alternately: a result keeps pointing at its set (no copy)
+        # and is only detached (copied out) if it is still alive when its set comes round again.
+        self.sets = [Workspace(), Workspace()]
+        self._cur = 0
+        self.ws = self.sets[0]
+        self.shared = Workspace()    # per-call scratch (split-K partials, counters, attention merge)
         self.enc_ws = Workspace()
         self.lib = N.load()
         torch = _torch()
-        self.splitk = self.ws.get("splitk", (64 << 20,), torch.float32, zero=False)
-        self.counters = self.ws.get("counters", (1 << 16,), torch.int32)
-        self.attn_counters = self.ws.get("attn_counters", (1 << 14,), torch.int32)
+        self.splitk = self.shared.get("splitk", (64 << 20,), torch.float32, zero=False)
+        self.counters = self.shared.get("counters", (1 << 16,), torch.int32)
+        self.attn_counters = self.shared.get("attn_counters", (1 << 14,), torch.int32)
         self.launches = 0          # kernels issued by this runner (all entry points)
         self.graphs: dict = {}     # structure key -> captured CUDA graph of the prefill chain
         self.layouts: dict = {}    # structure key -> Layout (engine._layout)
@@ -172,8 +177,8 @@ class Runner:
         torch = _torch()
         cfg = self.cfg
         hd = cfg.head_dim
-        ws_o = self.ws.get("attn_ws_o", (max(1, slots) * 8 * 256 * hd,), torch.float32, zero=False)
-        ws_ml = self.ws.get("attn_ws_ml", (max(1, slots) * 8 * 256 * 2,), torch.float32, zero=False)
+        ws_o = self.shared.get("attn_ws_o", (max(1, slots) * 8 * 256 * hd,), torch.float32, zero=False)
+        ws_ml = self.shared.get("attn_ws_ml", (max(1, slots) * 8 * 256 * 2,), torch.float32, zero=False)
         a = N.AttnArgs(q=q.data_ptr(), q_rows_cap=q.shape[0], kc=kc.data_ptr(), vc=vc.data_ptr(),
                        layers_cap=kc.shape[0], kv_rows_cap=kc.shape[1], layer=layer, kv=cfg.kv_dim,
                        heads=cfg.num_heads, head_dim=hd, items=items_ptr, n_items=n_items, qpos=qpos_ptr,
@@ -248,6 +253,19 @@ class Runner:
         return out[:M]
 
     # ---------------------------------------------------------------- decoder
+    def _pick_set(self) -> Workspace:
+        """The output set for this call: one no live result points into (preferring the set not
+        used last), else detach the results of the older set."""
+        for k in (self._cur ^ 1, self._cur):
+            if len(self.sets[k].live) == 0:
+                self._cur = k
+                break
+        else:
+            self._cur ^= 1
+            self.sets[self._cur].detach_live()
+        self.ws = self.sets[self._cur]
+        return self.ws
+
     def prefill(self, lay: Layout, text_src: np.ndarray, enc_store_rows, enc_scratch_rows, kv_pool, events=None,
                 use_graph: bool = True):
         """Run embed -> kv_relocate -> L layers -> final norm -> head for a built Layout.
@@ -257,14 +275,14 @@ class Runner:
         upload.  The chain is therefore captured once per structure into a CUDA graph and
         replayed: one launch instead of ~230.  Returns the device tensors of the result."""
         torch = _torch()
-        cfg, dw, ws = self.cfg, self.dw, self.ws
+        cfg, dw = self.cfg, self.dw
+        ws = self._pick_set()
         L, d, kv, V = cfg.num_layers, cfg.model_dim, cfg.kv_dim, cfg.vocab_size
         c = lay.c
         c0 = int(c[0])
         R = -(-max(256, c0) // 256) * 256          # row capacity (whole 256-row tiles)
         KVR = max(128, lay.kv_rows)
         dw.ensure_positions(max(lay.kv_rows, 1) + 1)
-        ws.detach_live()
         buf = dict(
             x=ws.get("x", (R, d), torch.float32), xn=ws.get("xn", (R * dw.kd,), torch.bfloat16),
             q=ws.get("q", (R + 256, kv), torch.bfloat16), att=ws.get("att", (R * dw.kkv,), torch.bfloat16),
@@ -272,8 +290,8 @@ class Runner:
             vc=ws.get("vc", (L, KVR, kv), torch.bfloat16), kpre=ws.get("kpre", (L, R, kv), torch.bfloat16),
             logits=ws.get("logits", (max(int(c[L - 1]), 1), V), torch.float32, zero=False))
         hd = cfg.head_dim
-        ws.get("attn_ws_o", (max(1, lay.attn_slots) * 8 * 256 * hd,), torch.float32, zero=False)
-        ws.get("attn_ws_ml", (max(1, lay.attn_slots) * 8 * 256 * 2,), torch.float32, zero=False)
+        self.shared.get("attn_ws_o", (max(1, lay.attn_slots) * 8 * 256 * hd,), torch.float32, zero=False)
+        self.shared.get("attn_ws_ml", (max(1, lay.attn_slots) * 8 * 256 * 2,), torch.float32, zero=False)
 
         pack = self._pack(lay)
         pack.upload(ws, "ints")
@@ -282,7 +300,7 @@ class Runner:
                 kv_pool.k.data_ptr() if kv_pool is not None else 0,
                 kv_pool.v.data_ptr() if kv_pool is not None else 0, kv_pool.P if kv_pool is not None else 0,
                 pack.dev.data_ptr(), dw.cos.data_ptr(), self.splitk.data_ptr(),
-                ws.bufs["attn_ws_o"].data_ptr(), ws.bufs["attn_ws_ml"].data_ptr()) + tuple(
+                self.shared.bufs["attn_ws_o"].data_ptr(), self.shared.bufs["attn_ws_ml"].data_ptr()) + tuple(
                     t.data_ptr() for t in buf.values())
         chain = lambda: self._chain(lay, pack, buf, ptrs)  # noqa: E731
         if events is not None:
