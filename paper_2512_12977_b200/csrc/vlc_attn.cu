@@ -371,8 +371,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + PP_ST;
   uint64_t* s_full = kv_empty + PP_ST;   // [2 tiles][2 buffers]
-  uint64_t* p_full = s_full + 4;         // [2]
-  uint64_t* o_done = p_full + 2;         // [2]
+  uint64_t* p_full = s_full + 4;         // [2 tiles][2 S buffers]: P(j) of tile x in buffer j&1
+  uint64_t* o_done = p_full + 4;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const int* it = a.items + blockIdx.x * 8;
@@ -401,8 +401,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       mbar_init(&kv_empty[s], 1);
     }
     for (int x = 0; x < 4; ++x) mbar_init(&s_full[x], 1);
+    for (int x = 0; x < 4; ++x) mbar_init(&p_full[x], 128);
     for (int x = 0; x < 2; ++x) {
-      mbar_init(&p_full[x], 128);
       mbar_init(&o_done[x], 1);
     }
     fence_barrier_init();
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       for (int j = 0; j < nt; ++j) {
         for (int x = 0; x < 2; ++x) {
           if (j >= nt_t[x]) continue;
-          mbar_wait(&p_full[x], j & 1);
+          mbar_wait(&p_full[2 * x + (j & 1)], (j >> 1) & 1);
           tc_fence_after();
           issue_pv(x, j);
           if (j + 2 < nt_t[x]) issue_s(x, j + 2);   // in-order after PV(j): reuses P(j)'s columns
@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       tmem_st32(tS, pk);   // P(j) overwrites the first 32 columns of S[x][j&1]
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&p_full[x]);
+      mbar_arrive(&p_full[2 * x + (j & 1)]);   // per-buffer barrier: softmax may run a tile ahead
     }
     if (ntx > 0) {   // o_done has completed ntx-1 or ntx phases here
       mbar_wait(&o_done[x], (ntx - 1) & 1);

@@ -112,6 +112,7 @@ int vlc_set_tuning(int key, int value) {
   if (key == 4) { vlc::set_attn_debug_buffer(nullptr); return VLC_OK; }
   if (key == 5) { vlc::g_attn_min_smem = value; return VLC_OK; }
   if (key == 6) { vlc::g_pdl = value; return VLC_OK; }
+  if (key == 7) { vlc::g_wide = value; return VLC_OK; }
   return fail(VLC_ERR_INVALID, "set_tuning: unknown key");
 }
 /* Experiments only: device buffer receiving per-CTA phase timestamps of the GEMM (NULL = off). */

@@ -27,7 +27,7 @@ constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 128;   // one stage = two 64-element (128 B) swizzle atoms along K
 constexpr int GEMM_ATOM_K = 64;
 
-__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g)); }
+__device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 __device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) {
   return make_uint2(pack_bf16(a, b), pack_bf16(c, d));
@@ -52,10 +52,11 @@ __device__ __forceinline__ void write_group(const GemmEpi& e, int F, int j, floa
       }
       break;
     }
-    case EPI_RESID: {
-      float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (long)j * e.ldo + F);
-      const float4 x = *o;
-      *o = make_float4(x.x + v.x, x.y + v.y, x.z + v.z, x.w + v.w);
+    case EPI_RESID: {   // x += acc as an L2 vector reduction: split-K partials need no fixup
+      float* o = reinterpret_cast<float*>(e.out) + (long)j * e.ldo + F;
+      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(o), "f"(v.x), "f"(v.y), "f"(v.z),
+                   "f"(v.w)
+                   : "memory");
       break;
     }
     case EPI_BF16: {
@@ -123,6 +124,73 @@ __device__ __forceinline__ void write_group(const GemmEpi& e, int F, int j, floa
   }
 }
 
+// The up-to-8 tokens jj = quad + 4q (q < 8, jj < jv) of one 32-token chunk, features [F, F+4):
+// loads of per-token metadata / RoPE tables are issued for all tokens before any store, so the
+// epilogue is not a chain of dependent global-load latencies.  sb = stage + 4*lane (token stride
+// 128 floats).
+template <int KIND>
+__device__ __forceinline__ void write_chunk(const GemmEpi& e, int F, int j0, int quad, int jv, const float* sb) {
+  if constexpr (KIND == EPI_QKV_ROPE) {
+    if (F >= e.n_valid) return;
+    const int sec = F / e.seg, r = F - sec * e.seg;
+    float4 v[8];
+    int p[8];
+    long dr[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int jj = quad + 4 * q;
+      if (jj < jv) {
+        const int j = j0 + jj;
+        v[q] = *reinterpret_cast<const float4*>(sb + jj * 128);
+        p[q] = __ldg(e.pos + j);
+        dr[q] = sec == 0 ? (e.map1 ? __ldg(e.map1 + j) : j) : __ldg(e.map2 + j);
+      }
+    }
+    if (sec == 2) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (quad + 4 * q < jv)
+          *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(e.out3) + dr[q] * e.ld3 + r) =
+              pack4_bf16(v[q].x, v[q].y, v[q].z, v[q].w);
+      return;
+    }
+    const int half = e.hd >> 1;
+    const int head = r / e.hd, t = (r - head * e.hd) >> 1;   // pairs (t, t+half), (t+1, t+1+half)
+    const int fa = head * e.hd + t;
+    float2 cq[8], sq[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (quad + 4 * q < jv) {
+        const long tab = (long)p[q] * e.tab_ld + t;
+        cq[q] = __ldg(reinterpret_cast<const float2*>(e.cos_tab + tab));
+        sq[q] = __ldg(reinterpret_cast<const float2*>(e.sin_tab + tab));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (quad + 4 * q >= jv) continue;
+      const float2 c = cq[q], sn = sq[q];
+      const float4 x = v[q];
+      const uint32_t lo = pack_bf16(x.x * c.x - x.y * sn.x, x.z * c.y - x.w * sn.y);
+      const uint32_t hi = pack_bf16(x.y * c.x + x.x * sn.x, x.w * c.y + x.z * sn.y);
+      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(sec == 0 ? e.out : e.out2) + dr[q] * (sec == 0 ? e.ldo : e.ld2);
+      *reinterpret_cast<uint32_t*>(o + fa) = lo;
+      *reinterpret_cast<uint32_t*>(o + fa + half) = hi;
+      if (sec == 1 && e.out4) {
+        __nv_bfloat16* kp = reinterpret_cast<__nv_bfloat16*>(e.out4) + (long)(j0 + quad + 4 * q) * e.ld4;
+        *reinterpret_cast<uint32_t*>(kp + fa) = pack_bf16(x.x, x.z);
+        *reinterpret_cast<uint32_t*>(kp + fa + half) = pack_bf16(x.y, x.w);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int jj = quad + 4 * q;
+      if (jj < jv) write_group<KIND>(e, F, j0 + jj, *reinterpret_cast<const float4*>(sb + jj * 128));
+    }
+  }
+}
+
 // ------------------------------------------------------------------ stream-K schedule
 struct SkSched {
   long long U;   // total work units = tiles * KB
@@ -148,14 +216,22 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define DBG(slot) do { if (g_dbg) g_dbg[blockIdx.x * 8 + (slot)] = gtimer(); } while (0)
 
-template <int KIND>
+// H = 1: 128 weight rows per tile, 128-wide k-blocks (two swizzle atoms), double-buffered TMEM
+//        accumulator.
+// H = 2: 256 weight rows per tile (two M=128 UMMAs sharing each activation k-block), 64-wide
+//        k-blocks: the activation bytes per weight byte halve, which keeps the L2 traffic of
+//        c ~ 240-token GEMMs under the LTS cap.  Single accumulator of 2 x n_tile columns.
+// The A (weight) bytes of a stage are 32 KB in both cases.
+template <int KIND, int H>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc(const uint8_t* __restrict__ wp, const uint8_t* __restrict__ xp, GemmEpi epi, SkSched sk,
                  int n_tile, int stages, float* ws, int* counters) {
+  constexpr int BM = GEMM_BM * H;
+  constexpr int BK = GEMM_BK / H;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int a_bytes = GEMM_BM * GEMM_BK * 2;
-  const int b_bytes = n_tile * GEMM_BK * 2;
+  const int a_bytes = BM * BK * 2;          // 32 KB
+  const int b_bytes = n_tile * BK * 2;
   uint8_t* sa = smem;
   uint8_t* sb = smem + stages * a_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(sb + stages * b_bytes);
@@ -170,6 +246,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const long long u_begin = sk.u0(g), u_end = sk.u0(g + 1);
   const int t_first = (int)(u_begin / sk.KB);
   const int t_last = (u_end > u_begin) ? (int)((u_end - 1) / sk.KB) : t_first - 1;
+  const int kb128 = H == 1 ? sk.KB : sk.KB / 2;   // 128-wide blocks per packed row tile
 
   if (warp == 0 && lane == 0) {
     DBG(0);
@@ -189,6 +266,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // source of the weight half h of k-block kb of weight tile mt (PACKED layout, include/vlcache.h)
+  auto a_src = [&](int mt, int kb, int h) -> const uint8_t* {
+    if (H == 1) return wp + ((long)mt * kb128 + kb) * 32768;
+    return wp + ((((long)(2 * mt + h) * kb128 + (kb >> 1)) * 2 + (kb & 1)) << 14);
+  };
+  auto b_src = [&](int tt, int kb) -> const uint8_t* {
+    if (H == 1) return xp + ((long)tt * kb128 + kb) * b_bytes;
+    return xp + (((long)tt * kb128 + (kb >> 1)) * 2 + (kb & 1)) * (long)b_bytes;
+  };
+
   if (warp == 0) {
     if (lane == 0) {
       DBG(1);
@@ -200,10 +287,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int t = t_first; t <= t_last && pre < stages; ++t) {
         const long long tb = (long long)t * sk.KB;
         const int kb_lo = (int)(max(u_begin, tb) - tb), kb_hi = (int)(min(u_end, tb + sk.KB) - tb);
-        const uint8_t* wsrc = wp + (long)(t % sk.m_tiles) * sk.KB * a_bytes;
+        const int mt = t % sk.m_tiles;
         for (int kb = kb_lo; kb < kb_hi && pre < stages; ++kb, ++pre) {
           mbar_expect_tx(&full[pre], a_bytes + b_bytes);
-          bulk_load(sa + pre * a_bytes, wsrc + (long)kb * a_bytes, a_bytes, &full[pre], pol_w);
+#pragma unroll
+          for (int h = 0; h < H; ++h)
+            bulk_load(sa + pre * a_bytes + h * (a_bytes / H), a_src(mt, kb, h), a_bytes / H, &full[pre], pol_w);
         }
       }
       pdl_wait();
@@ -212,16 +301,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int t = t_first; t <= t_last; ++t) {
         const long long tb = (long long)t * sk.KB;
         const int kb_lo = (int)(max(u_begin, tb) - tb), kb_hi = (int)(min(u_end, tb + sk.KB) - tb);
-        const int m0 = (t % sk.m_tiles) * GEMM_BM, tok0 = (t / sk.m_tiles) * n_tile;
-        const uint8_t* wsrc = wp + (long)(m0 / GEMM_BM) * sk.KB * a_bytes;
-        const uint8_t* xsrc = xp + (long)(tok0 / n_tile) * sk.KB * b_bytes;
+        const int mt = t % sk.m_tiles, tt = t / sk.m_tiles;
         for (int kb = kb_lo; kb < kb_hi; ++kb, ++u) {
           if (u >= pre) {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_expect_tx(&full[stage], a_bytes + b_bytes);
-            bulk_load(sa + stage * a_bytes, wsrc + (long)kb * a_bytes, a_bytes, &full[stage], pol_w);
+#pragma unroll
+            for (int h = 0; h < H; ++h)
+              bulk_load(sa + stage * a_bytes + h * (a_bytes / H), a_src(mt, kb, h), a_bytes / H, &full[stage],
+                        pol_w);
           }
-          bulk_load(sb + stage * b_bytes, xsrc + (long)kb * b_bytes, b_bytes, &full[stage], pol_x);
+          bulk_load(sb + stage * b_bytes, b_src(tt, kb), b_bytes, &full[stage], pol_x);
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
       }
@@ -236,8 +326,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int t = t_first; t <= t_last; ++t, ++seg) {
         const long long tb = (long long)t * sk.KB;
         const int nkb = (int)(min(u_end, tb + sk.KB) - max(u_begin, tb));
-        const int slot = seg & 1;
-        mbar_wait(&acc_empty[slot], ((seg >> 1) & 1) ^ 1);
+        const int slot = H == 1 ? (seg & 1) : 0;
+        const uint32_t acc_phase = H == 1 ? (((seg >> 1) & 1) ^ 1) : ((seg & 1) ^ 1);
+        mbar_wait(&acc_empty[slot], acc_phase);
         tc_fence_after();
         const uint32_t d = tmem + slot * 256;
         for (int kb = 0; kb < nkb; ++kb) {
@@ -245,12 +336,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sa + stage * a_bytes);
           const uint32_t b_addr = smem_u32(sb + stage * b_bytes);
+          if (H == 1) {
 #pragma unroll
-          for (int k = 0; k < GEMM_BK / 16; ++k) {
-            const int at = k >> 2;
-            const uint64_t ad = make_sdesc(a_addr + at * (GEMM_BM * 128) + (k & 3) * 32, 16, 1024, 128);
-            const uint64_t bd = make_sdesc(b_addr + at * (n_tile * 128) + (k & 3) * 32, 16, 1024, 128);
-            tc_mma_f16(d, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < GEMM_BK / 16; ++k) {
+              const int at = k >> 2;
+              const uint64_t ad = make_sdesc(a_addr + at * (GEMM_BM * 128) + (k & 3) * 32, 16, 1024, 128);
+              const uint64_t bd = make_sdesc(b_addr + at * (n_tile * 128) + (k & 3) * 32, 16, 1024, 128);
+              tc_mma_f16(d, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t bd = make_sdesc(b_addr + k * 32, 16, 1024, 128);
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const uint64_t ad = make_sdesc(a_addr + h * 16384 + k * 32, 16, 1024, 128);
+                tc_mma_f16(d + h * 256, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              }
+            }
           }
           tc_commit(&empty[stage]);
           if (++stage == stages) { stage = 0; phase ^= 1; }
@@ -262,7 +365,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else {
     pdl_wait();                     // outputs / residual rows belong to the previous kernels
     if (threadIdx.x == 64) pdl_trigger();
-    // ---------------- epilogue warps 2..9: group eg = 0/1 takes alternate 32-column chunks.
+    // ---------------- epilogue warps 2..9 (quad = TMEM lane quadrant).  H == 1: group eg = 0/1
+    // takes alternate 32-column chunks; H == 2: group eg drains weight half eg.
     // TMEM (thread = weight row) -> smem stage [32 tokens][128 rows] -> token-major float4
     // groups written coalesced (write_group), or raw partial rows for split tiles.
     const int quad = warp & 3;
@@ -276,16 +380,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int t = t_first; t <= t_last; ++t, ++seg) {
       const long long tb = (long long)t * sk.KB;
       const int gf = sk.cta_of(tb), gl = sk.cta_of(tb + sk.KB - 1);
-      const int m0 = (t % sk.m_tiles) * GEMM_BM, tok0 = (t / sk.m_tiles) * n_tile;
-      const int slot = seg & 1;
-      mbar_wait(&acc_full[slot], (seg >> 1) & 1);
+      const int m0 = (t % sk.m_tiles) * BM, tok0 = (t / sk.m_tiles) * n_tile;
+      const int slot = H == 1 ? (seg & 1) : 0;
+      mbar_wait(&acc_full[slot], H == 1 ? ((seg >> 1) & 1) : (seg & 1));
       tc_fence_after();
       if (leader) DBG(3);
-      const uint32_t d = tmem + slot * 256 + lane_off;
-      const bool split = gf != gl;
-      float* part = split ? ws + ((long)gf * SK_MAX_PART + (g - gf)) * (long)n_tile * GEMM_BM : nullptr;
+      const uint32_t d = tmem + slot * 256 + (H == 2 ? eg * 256 : 0) + lane_off;
+      const int hoff = H == 2 ? eg * 128 : 0;                 // weight-row offset of this group
+      const bool split = gf != gl && KIND != EPI_RESID;   // RESID partials reduce in L2 (red.add)
+      float* part = split ? ws + (2L * g + (t == t_first ? 0 : 1)) * (long)n_tile * BM : nullptr;
       const int nch = (n_tile + 31) / 32;
-      for (int ci = eg; ci < nch; ci += 2) {
+      for (int ci = (H == 1 ? eg : 0); ci < nch; ci += (H == 1 ? 2 : 1)) {
         const int c = ci * 32;
         float v[32];
         tmem_ld32(d + c, v);
@@ -296,13 +401,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int jmax = min(32, n_tile - c);
         if (split) {
           for (int jj = quad; jj < jmax; jj += 4)
-            __stcg(reinterpret_cast<float4*>(part + (long)(c + jj) * GEMM_BM) + lane,
+            __stcg(reinterpret_cast<float4*>(part + (long)(c + jj) * BM + hoff) + lane,
                    *reinterpret_cast<const float4*>(stage_buf + jj * 128 + 4 * lane));
         } else {
           const int jv = min(jmax, epi.m_tokens - tok0 - c);
-          for (int jj = quad; jj < jv; jj += 4)
-            write_group<KIND>(epi, m0 + 4 * lane, tok0 + c + jj,
-                              *reinterpret_cast<const float4*>(stage_buf + jj * 128 + 4 * lane));
+          write_chunk<KIND>(epi, m0 + hoff + 4 * lane, tok0 + c, quad, jv, stage_buf + 4 * lane);
         }
         asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
       }
@@ -316,12 +419,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     if (leader) DBG(4);
     // ---- parallel fixup of the split tiles this CTA touched: participant p of nseg owns a
-    // contiguous token range of the tile; partials are token-major rows of 128 fp32.
+    // contiguous token range of the tile; partials are token-major rows of BM fp32, in the
+    // partial slot (2 per CTA: first / last tile of its unit range) of each participant.
     const int ew = warp - 2;   // 0..7
     for (int t = t_first; t <= t_last; ++t) {
       const long long tb = (long long)t * sk.KB;
       const int gf = sk.cta_of(tb), gl = sk.cta_of(tb + sk.KB - 1);
-      if (gf == gl) continue;
+      if (gf == gl || KIND == EPI_RESID) continue;
       const int nseg = gl - gf + 1, p = g - gf;
       if (leader) {
         volatile int* cnt = counters + 2 * gf;
@@ -330,20 +434,28 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       asm volatile("bar.sync 3, 256;" ::: "memory");
       __threadfence();
       if (leader) DBG(5);
-      const int m0 = (t % sk.m_tiles) * GEMM_BM, tok0 = (t / sk.m_tiles) * n_tile;
+      const int m0 = (t % sk.m_tiles) * BM, tok0 = (t / sk.m_tiles) * n_tile;
       const int j_lo = n_tile * p / nseg, j_hi = min(n_tile * (p + 1) / nseg, epi.m_tokens - tok0);
-      const float* base = ws + (long)gf * SK_MAX_PART * n_tile * GEMM_BM;
-      const long pstride = (long)n_tile * GEMM_BM;
+      const long pstride = (long)n_tile * BM;
+      const float* bases[SK_MAX_PART];
+#pragma unroll
+      for (int s2 = 0; s2 < SK_MAX_PART; ++s2) {
+        const int gp = gf + (s2 < nseg ? s2 : 0);
+        bases[s2] = ws + (2L * gp + ((int)(sk.u0(gp) / sk.KB) == t ? 0 : 1)) * pstride;
+      }
       for (int jt = j_lo + ew; jt < j_hi; jt += GEMM_EPI_WARPS) {
-        float4 x[SK_MAX_PART];
 #pragma unroll
-        for (int s2 = 0; s2 < SK_MAX_PART; ++s2)
-          if (s2 < nseg) x[s2] = __ldcg(reinterpret_cast<const float4*>(base + s2 * pstride + (long)jt * GEMM_BM) + lane);
-        float4 acc = x[0];
+        for (int hf = 0; hf < H; ++hf) {
+          float4 x[SK_MAX_PART];
 #pragma unroll
-        for (int s2 = 1; s2 < SK_MAX_PART; ++s2)
-          if (s2 < nseg) { acc.x += x[s2].x; acc.y += x[s2].y; acc.z += x[s2].z; acc.w += x[s2].w; }
-        write_group<KIND>(epi, m0 + 4 * lane, tok0 + jt, acc);
+          for (int s2 = 0; s2 < SK_MAX_PART; ++s2)
+            if (s2 < nseg) x[s2] = __ldcg(reinterpret_cast<const float4*>(bases[s2] + (long)jt * BM + hf * 128) + lane);
+          float4 acc = x[0];
+#pragma unroll
+          for (int s2 = 1; s2 < SK_MAX_PART; ++s2)
+            if (s2 < nseg) { acc.x += x[s2].x; acc.y += x[s2].y; acc.z += x[s2].z; acc.w += x[s2].w; }
+          write_group<KIND>(epi, m0 + hf * 128 + 4 * lane, tok0 + jt, acc);
+        }
       }
       asm volatile("bar.sync 3, 256;" ::: "memory");
       if (leader) {
@@ -370,18 +482,21 @@ void set_debug_buffer(unsigned long long* p) { cudaMemcpyToSymbol(g_dbg, &p, siz
 int g_coop = 1;
 int g_pdl = 1;
 
-static int gemm_pick_stages(int n_tile) {
+int g_wide = 1;   // tuning key 7: 0 auto, 1 never use 256-row tiles (default: measured slower), 2 always
+
+static int gemm_pick_stages(int n_tile, int H) {
   if (g_stage_override > 0) return g_stage_override;
-  const int per = GEMM_BM * GEMM_BK * 2 + n_tile * GEMM_BK * 2;
+  const int per = GEMM_BM * GEMM_BK * 2 + n_tile * (GEMM_BK / H) * 2;
   int s = (222 * 1024 - 32 * 1024) / per;
   if (s > 8) s = 8;
   if (s < 2) s = 2;
   return s;
 }
 
-static int gemm_smem_bytes(int n_tile, int stages) {
+static int gemm_smem_bytes(int n_tile, int stages, int H) {
   // pipeline stages + barriers (64 B reserved) + two 16 KB epilogue staging tiles
-  return 1024 + stages * (GEMM_BM * GEMM_BK * 2 + n_tile * GEMM_BK * 2) + (2 * stages + 2) * 8 + 64 + 2 * 32 * 128 * 4;
+  return 1024 + stages * (GEMM_BM * GEMM_BK * 2 + n_tile * (GEMM_BK / H) * 2) + (2 * stages + 2) * 8 + 64 +
+         2 * 32 * 128 * 4;
 }
 
 static int num_sms() {
@@ -401,14 +516,17 @@ int gemm_row_tile(int m_tokens) {
   return t < 16 ? 16 : t;
 }
 
-// ws must hold G * SK_MAX_PART * 128 * n_tile floats; counters 2 * G ints (zero).
+// ws must hold G * 2 * BM * n_tile floats; counters 2 * G ints (zero).
 cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap,
                         int m_tokens, const GemmEpi& epi, int max_ctas, float* ws, size_t ws_bytes,
                         int* counters, cudaStream_t stream) {
   if (m_tokens <= 0) return cudaSuccess;
-  const int KB = k_pad / GEMM_BK;
-  const int m_tiles = n_pad / GEMM_BM;
   const int n_tile = gemm_row_tile(m_tokens);
+  const bool wide_ok = n_pad % 256 == 0;
+  const int H = (g_wide == 2 && wide_ok) || (g_wide == 0 && wide_ok && n_tile >= 96) ? 2 : 1;
+  const int BM = GEMM_BM * H, BK = GEMM_BK / H;
+  const int KB = k_pad / BK;
+  const int m_tiles = n_pad / BM;
   const int tok_tiles = (m_tokens + n_tile - 1) / n_tile;
   if (x_rows_cap < tok_tiles * n_tile) return cudaErrorInvalidValue;
   const long long U = (long long)m_tiles * tok_tiles * KB;
@@ -418,16 +536,18 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   // (the d x d projections) -> stream-K over every SM
   const long long tiles = (long long)m_tiles * tok_tiles;
   if (max_ctas == 0 && tiles >= 64 && tiles <= G) G = (int)tiles;
-  const int min_units = (KB + 5) / 6;  // keeps <= 8 participants per split tile
+  // split tiles reduce through the workspace with <= 8 participants, except RESID (red.add into
+  // the residual, any number of participants; >= 2 k-blocks per CTA)
+  const int min_units = epi.kind == EPI_RESID ? 2 : (KB + 5) / 6;
   if ((long long)G * min_units > U) G = (int)(U / min_units);
   if (G < 1) G = 1;
-  const size_t need = (size_t)G * SK_MAX_PART * GEMM_BM * n_tile * sizeof(float);
-  if (need > ws_bytes || counters == nullptr) {
+  const size_t need = (size_t)G * 2 * BM * n_tile * sizeof(float);
+  if (epi.kind != EPI_RESID && (need > ws_bytes || counters == nullptr)) {
     if (U / KB <= num_sms()) G = (int)(U / KB);   // no workspace: one CTA per tile, never split
     else return cudaErrorInvalidValue;
   }
-  const int stages = gemm_pick_stages(n_tile);
-  const int smem = gemm_smem_bytes(n_tile, stages);
+  const int stages = gemm_pick_stages(n_tile, H);
+  const int smem = gemm_smem_bytes(n_tile, stages, H);
   SkSched sk{U, G, KB, m_tiles};
   const uint8_t* wpp = reinterpret_cast<const uint8_t*>(W);
   const uint8_t* xpp = reinterpret_cast<const uint8_t*>(X);
@@ -435,10 +555,14 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   case K: {                                                                                           \
     static bool attr = false;                                                                         \
     if (!attr) {                                                                                      \
-      cudaFuncSetAttribute(gemm_bf16_tc<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);     \
+      cudaFuncSetAttribute(gemm_bf16_tc<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);  \
+      cudaFuncSetAttribute(gemm_bf16_tc<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);  \
       attr = true;                                                                                    \
     }                                                                                                 \
-    return launch_chain(gemm_bf16_tc<K>, dim3(G), dim3(GEMM_THREADS), smem, stream, g_coop != 0, wpp, xpp, epi, \
+    if (H == 2)                                                                                       \
+      return launch_chain(gemm_bf16_tc<K, 2>, dim3(G), dim3(GEMM_THREADS), smem, stream, g_coop != 0, wpp, xpp, \
+                          epi, sk, n_tile, stages, ws, counters);                                     \
+    return launch_chain(gemm_bf16_tc<K, 1>, dim3(G), dim3(GEMM_THREADS), smem, stream, g_coop != 0, wpp, xpp, epi, \
                         sk, n_tile, stages, ws, counters);                                            \
   }
   switch (epi.kind) {

@@ -24,6 +24,7 @@ using GemmEpi = vlc_epilogue;
 extern int g_stage_override;  // experiment knob (vlc_set_tuning key 1)
 extern int g_attn_min_smem;   // key 5: lower bound on the attention kernel's dynamic smem
 extern int g_coop;            // key 2: cooperative launch of the stream-K GEMM
+extern int g_wide;            // key 7: 256-row GEMM tiles (0 auto, 1 never, 2 always)
 extern int g_pdl;             // key 6: programmatic dependent launch of the chain kernels (default 1)
 void set_debug_buffer(unsigned long long* p);
 

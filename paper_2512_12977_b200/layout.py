@@ -168,6 +168,9 @@ def attention_work_pp(q_ranges, qpos, n_req, heads, max_ctas: int = 148):
             if ns == 1:
                 items.append([t0, nq, h, 0, 0, kend, -1, (0 << 8) | 1, req])
                 continue
+            # even key-tile split: a CTA's time follows its key-tile count (each iteration serves
+            # both query tiles), not the query-tile x key-tile work (measured: work-balanced splits
+            # leave the single-tile tail CTAs 1.7x slower)
             bounds = [min(kend, (tiles * s // ns) * 64) for s in range(ns)] + [kend]
             for s in range(ns):
                 items.append([t0, nq, h, 0, bounds[s], bounds[s + 1], group, (s << 8) | ns, req])

@@ -16,6 +16,7 @@ from .model import RMS_EPS, DeviceWeights
 
 N_SMS = 148
 _DEBUG_SYNC = bool(int(__import__("os").environ.get("VLC_DEBUG_SYNC", "0")))  # sync + log every launch
+_OVERLAP_RELOC = bool(int(__import__("os").environ.get("VLC_RELOC_OVERLAP", "1")))
 
 
 def _torch():
@@ -122,6 +123,8 @@ class Runner:
         self.layouts: dict = {}    # structure key -> Layout (engine._layout)
         self.graph_launches: dict = {}
         self.tracer = None         # list -> (name, ev0, ev1, algo_bytes, algo_flops) per launch
+        self.overlap_reloc = _OVERLAP_RELOC
+        self._side = None          # side stream of the overlapped kv_relocate
 
     def _run(self, name, fn, nbytes=0, flops=0, kernels=1):
         """Issue one C-ABI call; optionally bracket it with CUDA events on the current stream."""
@@ -380,13 +383,36 @@ class Runner:
         self._run("embed", lambda: N.check(self.lib.vlc_embed_assemble(
             x.data_ptr(), d, dw.embed.data_ptr(), d, enc_a, enc_b, pack.ptr("src"), c0, s), "vlc_embed_assemble"),
             c0 * d * 6)
-        # cached K/V of every reused image token, all layers, re-rotated to the new positions
+        # cached K/V of every reused image token, re-rotated to the new positions.  The relocation
+        # is a pure HBM stream while the layer GEMMs are latency-bound, so by default it runs per
+        # layer on a side stream, overlapped with the layer chain; attention i waits for layer i.
         nb = len(lay.reloc_blocks)
-        if nb:
+        side_ev = None
+
+        def relocate(b0, n_b):
             self._run("kv_relocate", lambda: N.check(self.lib.vlc_kv_relocate(
                 kpool, vpool, P, pack.ptr("pages"), kv, cfg.head_dim, kc.data_ptr(), vc.data_ptr(), kc.shape[1],
-                pack.ptr("descs"), pack.ptr("blocks"), nb, dw.cos.data_ptr(), dw.sin.data_ptr(), cfg.head_dim // 2,
-                s), "vlc_kv_relocate"), lay.reloc_tokens * kv * 2 * 4)
+                pack.ptr("descs"), pack.ptr("blocks") + 8 * b0, n_b, dw.cos.data_ptr(), dw.sin.data_ptr(),
+                cfg.head_dim // 2, _stream()), "vlc_kv_relocate"), lay.reloc_tokens * kv * 2 * 4 * n_b // nb)
+
+        if nb and self.overlap_reloc:
+            torch = _torch()
+            main = torch.cuda.current_stream()
+            if self._side is None:
+                self._side = torch.cuda.Stream()
+            side = self._side
+            side.wait_stream(main)
+            side_ev = []
+            lb = lay.reloc_layer_blocks
+            with torch.cuda.stream(side):
+                for i in range(L):
+                    if lb[i + 1] > lb[i]:
+                        relocate(int(lb[i]), int(lb[i + 1] - lb[i]))
+                    ev = torch.cuda.Event()
+                    ev.record(side)
+                    side_ev.append(ev)
+        elif nb:
+            relocate(0, nb)
         for i in range(L):
             ci = int(c[i])
             W = dw.layers[i]
@@ -399,6 +425,8 @@ class Runner:
                 cos_tab=dw.cos.data_ptr(), sin_tab=dw.sin.data_ptr(), tab_ld=cfg.head_dim // 2,
                 hd=cfg.head_dim, seg=kv), name="gemm_qkv", k_valid=d)
             vis = int(lay.qpos[i, :ci].astype(np.int64).sum()) + ci
+            if side_ev is not None:
+                _torch().cuda.current_stream().wait_event(side_ev[i])
             self.attention(q, kc, vc, i, pack.ptr(f"items{i}"), len(lay.attn_items[i]), pack.ptr(f"comb{i}"),
                            len(lay.comb_items[i]), pack.ptr(f"qpos{i}"), pack.ptr(f"rowof{i}"), att, lay.attn_slots,
                            nbytes=lay.kv_rows * kv * 4 + ci * kv * 4, flops=4 * cfg.head_dim * cfg.num_heads * vis,
@@ -412,6 +440,8 @@ class Runner:
                       name="gemm_gate_up", k_valid=d)
             self.gemm(W["wd"], dw.kh, hb, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d),
                       name="gemm_down", k_valid=cfg.mlp_hidden)
+        if side_ev is not None:
+            _torch().cuda.current_stream().wait_stream(self._side)
         self.rmsnorm(x, dw.final_norm, xn, cL, row_map=pack.ptr("final"), pk=(N.row_tile(cL), dw.kd // 128))
         self.gemm(dw.head, dw.kd, xn, cL, _epi(kind=N.EPI_F32, n_valid=V, out=logits.data_ptr(), ldo=V),
                   name="gemm_head", k_valid=d)

@@ -288,3 +288,47 @@ def test_attention_pp_matches_torch(nat, hd, heads, nkeys, nq, causal):
     nat.check(nat.load().vlc_attn_pp(a, _stream()), "attn_pp packed")
     torch.cuda.synchronize()
     assert torch.equal(nat.unpack(outp, nq, kv, R), out)
+
+
+@pytest.fixture
+def gemm_mode(nat):
+    yield lambda mode: nat.load().vlc_set_tuning(7, mode)
+    nat.load().vlc_set_tuning(7, 1)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("n_pad,k_pad,m,ctas", [(256, 256, 40, 0), (512, 1024, 240, 0), (10752, 3584, 236, 0),
+                                                (3584, 7168, 236, 0), (768, 256, 44, 5), (1024, 512, 600, 0)])
+def test_gemm_tile_modes_f32_resid(nat, gemm_mode, mode, n_pad, k_pad, m, ctas):
+    """128-row (mode 1) and 256-row (mode 2) weight tiles, stream-K splits, F32 and RESID
+    (red.add) epilogues against torch."""
+    gemm_mode(mode)
+    g = torch.Generator(device="cuda").manual_seed(n_pad + k_pad + m)
+    W = torch.randn(n_pad, k_pad, device="cuda", generator=g).bfloat16()
+    X = torch.randn(max(256, m), k_pad, device="cuda", generator=g).bfloat16()
+    ref = X[:m].float() @ W.float().t()
+    out = torch.full((m, n_pad), float("nan"), device="cuda")
+    _gemm(nat, W, X, m, _epi(nat, kind=nat.EPI_F32, n_valid=n_pad, m_tokens=m, out=out.data_ptr(), ldo=n_pad), ctas)
+    assert (out - ref).abs().max().item() / ref.abs().max().item() < 1e-5
+    x = torch.randn(m, n_pad, device="cuda", generator=g)
+    x0 = x.clone()
+    _gemm(nat, W, X, m, _epi(nat, kind=nat.EPI_RESID, n_valid=n_pad, m_tokens=m, out=x.data_ptr(), ldo=n_pad), ctas)
+    assert ((x - x0) - ref).abs().max().item() / ref.abs().max().item() < 1e-5
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_gemm_tile_modes_swiglu_packed(nat, gemm_mode, mode):
+    gemm_mode(mode)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    n, k, m = 1024, 512, 236
+    W = torch.randn(n, k, device="cuda", generator=g).bfloat16()
+    X = torch.randn(256, k, device="cuda", generator=g).bfloat16()
+    acc = X[:m].float() @ W.float().t()
+    R = nat.row_tile(m)
+    hp = torch.zeros(nat.packed_numel(m, n // 2, R), device="cuda", dtype=torch.bfloat16)
+    _gemm(nat, W, X, m, _epi(nat, kind=nat.EPI_SWIGLU, n_valid=n, m_tokens=m, out=hp.data_ptr(), ldo=n // 2,
+                             pk_rows=R, pk_kb=-(-(n // 2) // 128)))
+    h = nat.unpack(hp, m, n // 2, R).float()
+    gate, up = acc[:, 0::2], acc[:, 1::2]
+    ref = gate / (1 + torch.exp(-gate)) * up
+    assert (h - ref).abs().max().item() <= 2e-2 * ref.abs().max().item()
