@@ -109,6 +109,7 @@ int vlc_version(void);
 /* Tuning knobs for experiments: key 1 = GEMM pipeline stages (0 = automatic). */
 int vlc_set_tuning(int key, int value);
 int vlc_set_debug_buffer(void* device_ptr);
+int vlc_set_trace_buffer(void* device_ptr);   /* experiments: attention CTA-0 event trace (>= 224 u64) */
 
 /* Layer-0 hidden rows of the computed set (model.py:339-359, engine.py:167).
  * src int32[rows][2] = {kind, index}: kind 0 -> bf16 embed row `index` (text token id),

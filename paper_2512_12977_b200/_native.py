@@ -18,7 +18,7 @@ EPI_F32, EPI_RESID, EPI_BF16, EPI_BIAS_ADD, EPI_SWIGLU, EPI_QKV_PLAIN, EPI_QKV_R
 
 EXPORTS = ("vlc_last_error", "vlc_version", "vlc_embed_assemble", "vlc_rmsnorm", "vlc_kv_relocate",
            "vlc_store_write_pages", "vlc_gemm_bf16", "vlc_gemm_row_tile", "vlc_pack_operand", "vlc_attn_mixed", "vlc_attn_combine", "vlc_attn_pp",
-           "vlc_patchify", "vlc_set_tuning", "vlc_set_debug_buffer")
+           "vlc_patchify", "vlc_set_tuning", "vlc_set_debug_buffer", "vlc_set_trace_buffer")
 
 
 class NativeError(KVReuseError):
@@ -72,6 +72,7 @@ def load():
         lib.vlc_patchify.argtypes = [vp, i, i, vp, i, i, i, vp]
         lib.vlc_set_tuning.argtypes = [i, i]
         lib.vlc_set_debug_buffer.argtypes = [vp]
+        lib.vlc_set_trace_buffer.argtypes = [vp]
         for name in EXPORTS:
             getattr(lib, name).restype = C.c_char_p if name == "vlc_last_error" else i
         _lib = lib

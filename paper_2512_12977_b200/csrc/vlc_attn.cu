@@ -338,8 +338,16 @@ __device__ __forceinline__ void adbg(int slot) {
   }
 }
 void set_attn_debug_buffer(unsigned long long* p) { cudaMemcpyToSymbol(g_attn_dbg, &p, sizeof(p)); }
+__device__ unsigned long long* g_attn_trace = nullptr;  // per-iteration event times of CTA 0 (experiments)
+__device__ __forceinline__ void atrace(int slot) {
+  if (g_attn_trace && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_attn_trace[slot] = t;
+  }
+}
+void set_attn_trace_buffer(unsigned long long* p) { cudaMemcpyToSymbol(g_attn_trace, &p, sizeof(p)); }
 constexpr int PP_KT = 64;
-constexpr int PP_ST = 3;
 
 template <int HD>
 struct PPCfg {
@@ -350,7 +358,11 @@ struct PPCfg {
   static constexpr int Q_ATOM = 128 * SWZ;
   static constexpr int KV_BYTES = PP_KT * HD * 2;
   static constexpr int KV_ATOM = PP_KT * SWZ;
-  static constexpr int SMEM = 1024 + 2 * Q_BYTES + PP_ST * 2 * KV_BYTES + 256;
+  // K/V ring as deep as shared memory allows (<= 8): the softmax warps wait on S, i.e. on K/V
+  // loads, when the ring is shallow (ncu: s_full wait was the top stall at 3 stages)
+  static constexpr int ST_FIT = (232448 - 1024 - 256 - 2 * Q_BYTES) / (2 * KV_BYTES);
+  static constexpr int ST = ST_FIT > 8 ? 8 : ST_FIT;
+  static constexpr int SMEM = 1024 + 2 * Q_BYTES + ST * 2 * KV_BYTES + 256;
   // TMEM: S[x][buf] (64 fp32 cols; P bf16 pairs aliased in its first 32 cols), O[x] (HD cols)
   __device__ static constexpr uint32_t s_col(int x, int b) { return 64u * (2 * x + b); }
   __device__ static constexpr uint32_t o_col(int x) { return 256u + (uint32_t)(HD > 64 ? HD : 64) * x; }
@@ -365,12 +377,12 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                                   // [2][Q_BYTES]
   uint8_t* sK = sQ + 2 * C::Q_BYTES;                    // [ST][KV_BYTES]
-  uint8_t* sV = sK + PP_ST * C::KV_BYTES;               // [ST][KV_BYTES]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + PP_ST * C::KV_BYTES);
+  uint8_t* sV = sK + C::ST * C::KV_BYTES;               // [ST][KV_BYTES]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + C::ST * C::KV_BYTES);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;
-  uint64_t* kv_empty = kv_full + PP_ST;
-  uint64_t* s_full = kv_empty + PP_ST;   // [2 tiles][2 buffers]
+  uint64_t* kv_empty = kv_full + C::ST;
+  uint64_t* s_full = kv_empty + C::ST;   // [2 tiles][2 buffers]
   uint64_t* p_full = s_full + 4;         // [2 tiles][2 S buffers]: P(j) of tile x in buffer j&1
   uint64_t* o_done = p_full + 4;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
@@ -396,7 +408,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     tma_prefetch(&map_k);
     tma_prefetch(&map_v);
     mbar_init(q_full, 1);
-    for (int s = 0; s < PP_ST; ++s) {
+    for (int s = 0; s < C::ST; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
@@ -424,8 +436,9 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         if (nq_t[x] > 0)
           tma_load_3d(sQ + x * C::Q_BYTES, &map_q, q_full, 0, q_row0 + x * 128, head * C::N_ATOMS, pol_q);
       for (int j = 0; j < nt; ++j) {
-        const int st = j % PP_ST;
-        mbar_wait(&kv_empty[st], ((j / PP_ST) & 1) ^ 1);
+        const int st = j % C::ST;
+        mbar_wait(&kv_empty[st], ((j / C::ST) & 1) ^ 1);
+        if (j < 32) atrace(128 + j);
         mbar_expect_tx(&kv_full[st], 2 * C::KV_BYTES);
         const int krow = kv_row0 + kb + j * PP_KT;   // one op per K / V tile: 4-D {elems, keys, atoms, layer}
         tma_load_4d(sK + st * C::KV_BYTES, &map_k, &kv_full[st], 0, krow, head * C::N_ATOMS, a.layer, pol_kv);
@@ -439,8 +452,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       mbar_wait(q_full, 0);
       adbg(1);
       auto issue_s = [&](int x, int j) {   // S[x][j&1] = Q_x K_j^T
-        const int st = j % PP_ST;
-        mbar_wait(&kv_full[st], (j / PP_ST) & 1);
+        const int st = j % C::ST;
+        mbar_wait(&kv_full[st], (j / C::ST) & 1);
         tc_fence_after();
         const uint32_t q_addr = smem_u32(sQ + x * C::Q_BYTES);
         const uint32_t k_addr = smem_u32(sK + st * C::KV_BYTES);
@@ -455,7 +468,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         tc_commit(&s_full[2 * x + (j & 1)]);
       };
       auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j, P from TMEM (aliased in S[x][j&1])
-        const int st = j % PP_ST;
+        const int st = j % C::ST;
         const uint32_t v_addr = smem_u32(sV + st * C::KV_BYTES);
 #pragma unroll
         for (int k = 0; k < PP_KT / 16; ++k) {
@@ -474,10 +487,12 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
           if (j >= nt_t[x]) continue;
           mbar_wait(&p_full[2 * x + (j & 1)], (j >> 1) & 1);
           tc_fence_after();
+          if (j < 16) atrace(64 + j * 4 + 2 * x);
           issue_pv(x, j);
           if (j + 2 < nt_t[x]) issue_s(x, j + 2);   // in-order after PV(j): reuses P(j)'s columns
+          if (j < 16) atrace(64 + j * 4 + 2 * x + 1);
         }
-        tc_commit(&kv_empty[j % PP_ST]);
+        tc_commit(&kv_empty[j % C::ST]);
       }
       adbg(2);
     }
@@ -500,16 +515,23 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       float s[PP_KT];
       mbar_wait(&s_full[2 * x + (j & 1)], (j >> 1) & 1);
       tc_fence_after();
+      const bool tr = (r == 0 && j < 16);
+      if (tr) atrace((x ? 160 : 0) + j * 4);
       tmem_ld32(tS, s);
       tmem_ld32(tS + 32, s + 32);
       tmem_wait_ld();
+      if (tr) atrace((x ? 160 : 0) + j * 4 + 1);
+      // scores stay raw (scale folded into the exp2 FFMA); masked keys -> -inf; reductions in
+      // 4 independent chains (only 2 softmax warps per scheduler: latency, not issue, binds)
       const int lim = min(qp, ke - 1) - k0;
-      float tmax = NEG_INF;
+      if (lim < PP_KT - 1) {
 #pragma unroll
-      for (int i = 0; i < PP_KT; ++i) {
-        s[i] = (i <= lim) ? s[i] * a.scale_log2 : NEG_INF;
-        tmax = fmaxf(tmax, s[i]);
+        for (int i = 0; i < PP_KT; ++i) s[i] = (i <= lim) ? s[i] : NEG_INF;
       }
+      float mx4[4] = {NEG_INF, NEG_INF, NEG_INF, NEG_INF};
+#pragma unroll
+      for (int i = 0; i < PP_KT; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], s[i]);
+      const float tmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * a.scale_log2;
       const float m_new = fmaxf(m_run, tmax);
       const bool need = m_new > m_run + 8.0f;
       const bool has_o = m_run != NEG_INF;
@@ -523,7 +545,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         tc_fence_after();
       }
       if (resc) {
-        const float sc = (need && has_o) ? exp2f(m_run - m_new) : 1.0f;
+        const float sc = (need && has_o) ? fast_exp2(m_run - m_new) : 1.0f;
 #pragma unroll
         for (int c = 0; c < HD / 16; ++c) {
           float o[16];
@@ -536,24 +558,27 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         tmem_wait_st();
       }
       if (need) {
-        l_run = has_o ? l_run * exp2f(m_run - m_new) : 0.f;
+        l_run = has_o ? l_run * fast_exp2(m_run - m_new) : 0.f;
         m_run = m_new;
       }
       const bool any = m_run != NEG_INF;
+      const float nm = any ? -m_run : NEG_INF;     // all-masked row: every p = exp2(-inf) = 0
       uint32_t pk[PP_KT / 2];
-      float lsum = 0.f;
+      float ls4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int i = 0; i < PP_KT / 2; ++i) {
-        const float p0 = any ? exp2f(s[2 * i] - m_run) : 0.f;
-        const float p1 = any ? exp2f(s[2 * i + 1] - m_run) : 0.f;
-        lsum += p0 + p1;
+        const float p0 = fast_exp2(fmaf(s[2 * i], a.scale_log2, nm));
+        const float p1 = fast_exp2(fmaf(s[2 * i + 1], a.scale_log2, nm));
+        ls4[i & 3] += p0 + p1;
         pk[i] = pack_bf16(p0, p1);
       }
-      l_run += lsum;
+      l_run += (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
+      if (tr) atrace((x ? 160 : 0) + j * 4 + 2);
       tmem_st32(tS, pk);   // P(j) overwrites the first 32 columns of S[x][j&1]
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&p_full[2 * x + (j & 1)]);   // per-buffer barrier: softmax may run a tile ahead
+      if (tr) atrace((x ? 160 : 0) + j * 4 + 3);
     }
     if (ntx > 0) {   // o_done has completed ntx-1 or ntx phases here
       mbar_wait(&o_done[x], (ntx - 1) & 1);

@@ -115,6 +115,11 @@ int vlc_set_tuning(int key, int value) {
   if (key == 7) { vlc::g_wide = value; return VLC_OK; }
   return fail(VLC_ERR_INVALID, "set_tuning: unknown key");
 }
+/* Experiments only: device buffer (>= 224 u64) receiving per-iteration event times of attention CTA 0. */
+int vlc_set_trace_buffer(void* p) {
+  vlc::set_attn_trace_buffer(reinterpret_cast<unsigned long long*>(p));
+  return VLC_OK;
+}
 /* Experiments only: device buffer receiving per-CTA phase timestamps of the GEMM (NULL = off). */
 int vlc_set_debug_buffer(void* p) {
   vlc::set_debug_buffer(reinterpret_cast<unsigned long long*>(p));

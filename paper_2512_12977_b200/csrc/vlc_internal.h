@@ -54,6 +54,7 @@ cudaError_t launch_chain(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t s
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 void set_attn_debug_buffer(unsigned long long* p);
+void set_attn_trace_buffer(unsigned long long* p);
 
 
 // tensor maps (driver entry point resolved through the runtime, no -lcuda)

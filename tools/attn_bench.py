@@ -67,5 +67,6 @@ def run(max_ctas):
             print(f"   {nm:14s} min {col.min():7.2f} med {np.median(col):7.2f} max {col.max():7.2f}")
 
 
-for mc in (148, 28):
+if __name__ == "__main__":
+  for mc in (148, 28):
     run(mc)
