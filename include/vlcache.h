@@ -124,6 +124,12 @@ int vlc_rmsnorm(const float* x, int ldx, const float* gamma, void* out, int ldo,
                 int rows, int d, const int* row_map, float eps, int pk_rows, int pk_kb,
                 cudaStream_t stream);
 
+/* Head-parallel attention: x[r] += add[r] (the all-reduced O projection),
+ * written back, then RMSNorm of x[r] -> bf16 (PACKED when pk_rows > 0).  Replaces the residual add
+ * of engine.py:183 + the MLP norm of engine.py:184 on each rank. */
+int vlc_add_rmsnorm(float* x, int ldx, const float* add, int ld_add, const float* gamma, void* out, int ldo,
+                    int rows, int d, float eps, int pk_rows, int pk_kb, cudaStream_t stream);
+
 /* Fused gather + RoPE re-rotation + scatter of cached pre-RoPE K and copy of V from
  * the paged store into the request KV cache (engine.py:153-155 + engine.py:180).
  * descs int32[n][8] = {layer, page_tab_off, tok0, ntok, dst_row0, pos0, 0, 0};

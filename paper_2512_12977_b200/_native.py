@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_PKG, "libvlcache.so")
 VLC_OK, VLC_ERR_INVALID, VLC_ERR_UNSUPPORTED, VLC_ERR_CUDA = 0, 1, 2, 3
 EPI_F32, EPI_RESID, EPI_BF16, EPI_BIAS_ADD, EPI_SWIGLU, EPI_QKV_PLAIN, EPI_QKV_ROPE = range(7)
 
-EXPORTS = ("vlc_last_error", "vlc_version", "vlc_embed_assemble", "vlc_rmsnorm", "vlc_kv_relocate",
+EXPORTS = ("vlc_last_error", "vlc_version", "vlc_embed_assemble", "vlc_rmsnorm", "vlc_add_rmsnorm", "vlc_kv_relocate",
            "vlc_store_write_pages", "vlc_gemm_bf16", "vlc_gemm_row_tile", "vlc_pack_operand", "vlc_attn_mixed", "vlc_attn_combine", "vlc_attn_pp",
            "vlc_patchify", "vlc_set_tuning", "vlc_set_debug_buffer", "vlc_set_trace_buffer")
 
@@ -61,6 +61,7 @@ def load():
         lib.vlc_version.restype = i
         lib.vlc_embed_assemble.argtypes = [vp, i, vp, i, vp, vp, vp, i, vp]
         lib.vlc_rmsnorm.argtypes = [vp, i, vp, vp, i, i, i, i, vp, f, i, i, vp]
+        lib.vlc_add_rmsnorm.argtypes = [vp, i, vp, i, vp, vp, i, i, i, f, i, i, vp]
         lib.vlc_kv_relocate.argtypes = [vp, vp, i, vp, i, i, vp, vp, i, vp, vp, i, vp, vp, i, vp]
         lib.vlc_store_write_pages.argtypes = [vp, i, i, i, i, vp, i, vp, i, vp]
         lib.vlc_gemm_bf16.argtypes = [vp, i, i, vp, i, i, C.POINTER(Epilogue), i, vp, C.c_size_t, vp, vp]

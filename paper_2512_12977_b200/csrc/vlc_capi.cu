@@ -96,8 +96,8 @@ using namespace vlc;
 extern "C" {
 
 int vlc_embed_assemble_impl(float*, int, const void*, int, const float*, const float*, const int*, int, cudaStream_t);
-int vlc_rmsnorm_impl(const float*, int, const float*, void*, int, int, int, int, const int*, float, int, int,
-                     cudaStream_t);
+int vlc_rmsnorm_impl(float*, int, const float*, void*, int, int, int, int, const int*, float, int, int,
+                     cudaStream_t, const float*, int);
 int vlc_kv_relocate_impl(const void*, const void*, int, const int*, int, int, void*, void*, int, const int*,
                          const int*, int, const float*, const float*, int, cudaStream_t);
 int vlc_store_write_pages_impl(const void*, int, int, int, int, const int*, int, void*, int, cudaStream_t);
@@ -142,9 +142,20 @@ int vlc_rmsnorm(const float* x, int ldx, const float* gamma, void* out, int ldo,
     return fail(VLC_ERR_INVALID, "rmsnorm: bad args");
   if (pk_rows > 0 && (out_f32 || pk_rows % 8 || pk_kb * 128 < d))
     return fail(VLC_ERR_INVALID, "rmsnorm: packed output needs bf16, pk_rows % 8 == 0, pk_kb*128 >= d");
-  return cuda_status((cudaError_t)vlc_rmsnorm_impl(x, ldx, gamma, out, ldo, out_f32, rows, d, row_map, eps, pk_rows,
-                                                   pk_kb, stream),
+  return cuda_status((cudaError_t)vlc_rmsnorm_impl(const_cast<float*>(x), ldx, gamma, out, ldo, out_f32, rows, d,
+                                                   row_map, eps, pk_rows, pk_kb, stream, nullptr, 0),
                      "rmsnorm");
+}
+
+int vlc_add_rmsnorm(float* x, int ldx, const float* add, int ld_add, const float* gamma, void* out, int ldo,
+                    int rows, int d, float eps, int pk_rows, int pk_kb, cudaStream_t stream) {
+  if (rows < 0 || d <= 0 || ldx < d || ld_add < d || (pk_rows <= 0 && ldo < d) || !x || !add || !gamma || !out)
+    return fail(VLC_ERR_INVALID, "add_rmsnorm: bad args");
+  if (pk_rows > 0 && (pk_rows % 8 || pk_kb * 128 < d))
+    return fail(VLC_ERR_INVALID, "add_rmsnorm: packed output needs pk_rows % 8 == 0, pk_kb*128 >= d");
+  return cuda_status((cudaError_t)vlc_rmsnorm_impl(x, ldx, gamma, out, ldo, 0, rows, d, nullptr, eps, pk_rows, pk_kb,
+                                                   stream, add, ld_add),
+                     "add_rmsnorm");
 }
 
 int vlc_kv_relocate(const void* kpool, const void* vpool, int page_tokens, const int* page_table, int kv,

@@ -29,24 +29,39 @@ __global__ void embed_assemble_kernel(float* __restrict__ x, int ldx,
 // ------------------------------------------------------------------ rmsnorm (K4)
 // One 128-thread block per row, the row held in registers as float4 (VPT per thread), so x
 // is read once; cross-warp sum through shared memory.
+// With `add` (head-parallel attention): x[row] += add[row] first (the all-reduced O projection),
+// written back, then normalised.
 template <bool OUT_F32, int VPT>
-__global__ void __launch_bounds__(128) rmsnorm_kernel(const float* __restrict__ x, int ldx,
+__global__ void __launch_bounds__(128) rmsnorm_kernel(float* __restrict__ x, int ldx,
                                                       const float* __restrict__ g, void* __restrict__ out,
                                                       int ldo, int rows, int d,
                                                       const int* __restrict__ row_map, float eps,
-                                                      int pk_rows, int pk_kb) {
+                                                      int pk_rows, int pk_kb, const float* __restrict__ add,
+                                                      int ld_add) {
   pdl_wait();
   pdl_trigger();
   const int r = blockIdx.x;
   const int sr = row_map ? __ldg(row_map + r) : r;
-  const float4* xr = reinterpret_cast<const float4*>(x + (long)sr * ldx);
+  float4* xr = reinterpret_cast<float4*>(x + (long)sr * ldx);
   const int n4 = d >> 2;
   float4 v[VPT];
   float acc = 0.f;
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
     const int i = threadIdx.x + 128 * k;
-    v[k] = i < n4 ? __ldg(xr + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    v[k] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (add) {
+    const float4* ar = reinterpret_cast<const float4*>(add + (long)sr * ld_add);
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int i = threadIdx.x + 128 * k;
+      if (i < n4) {
+        const float4 a = ar[i];
+        v[k] = make_float4(v[k].x + a.x, v[k].y + a.y, v[k].z + a.z, v[k].w + a.w);
+        xr[i] = v[k];
+      }
+    }
   }
 #pragma unroll
   for (int k = 0; k < VPT; ++k) acc += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
@@ -76,14 +91,19 @@ __global__ void __launch_bounds__(128) rmsnorm_kernel(const float* __restrict__ 
 
 // Generic fallback (any d): block per row.
 template <bool OUT_F32>
-__global__ void rmsnorm_generic(const float* __restrict__ x, int ldx, const float* __restrict__ g,
+__global__ void rmsnorm_generic(float* __restrict__ x, int ldx, const float* __restrict__ g,
                                 void* __restrict__ out, int ldo, int rows, int d,
-                                const int* __restrict__ row_map, float eps, int pk_rows, int pk_kb) {
+                                const int* __restrict__ row_map, float eps, int pk_rows, int pk_kb,
+                                const float* __restrict__ add, int ld_add) {
   pdl_wait();
   pdl_trigger();
   const int r = blockIdx.x;
   const int sr = row_map ? row_map[r] : r;
-  const float* xr = x + (long)sr * ldx;
+  float* xr = x + (long)sr * ldx;
+  if (add) {
+    for (int i = threadIdx.x; i < d; i += blockDim.x) xr[i] += add[(long)sr * ld_add + i];
+    __syncthreads();
+  }
   float acc = 0.f;
   for (int i = threadIdx.x; i < d; i += blockDim.x) acc += xr[i] * xr[i];
   __shared__ float red[32];
@@ -250,15 +270,17 @@ int vlc_embed_assemble_impl(float* x, int ldx, const void* embed_bf16, int d, co
                            reinterpret_cast<const int2*>(src), rows);
 }
 
-int vlc_rmsnorm_impl(const float* x, int ldx, const float* gamma, void* out, int ldo, int out_f32,
-                     int rows, int d, const int* row_map, float eps, int pk_rows, int pk_kb, cudaStream_t stream) {
+int vlc_rmsnorm_impl(float* x, int ldx, const float* gamma, void* out, int ldo, int out_f32,
+                     int rows, int d, const int* row_map, float eps, int pk_rows, int pk_kb, cudaStream_t stream,
+                     const float* add, int ld_add) {
   if (rows <= 0) return 0;
-  const bool vec = (d % 4 == 0) && (ldx % 4 == 0) && (pk_rows > 0 || ldo % 4 == 0) && d <= 128 * 4 * 16;
+  const bool vec = (d % 4 == 0) && (ldx % 4 == 0) && (pk_rows > 0 || ldo % 4 == 0) && d <= 128 * 4 * 16 &&
+                   (add == nullptr || ld_add % 4 == 0);
   const unsigned blocks = rows;
   cudaError_t e = cudaSuccess;
 #define VLC_RMS(VPT)                                                                                   \
   e = launch_chain(out_f32 ? rmsnorm_kernel<true, VPT> : rmsnorm_kernel<false, VPT>, dim3(blocks), dim3(128), 0, \
-                   stream, false, x, ldx, gamma, out, ldo, rows, d, row_map, eps, pk_rows, pk_kb);
+                   stream, false, x, ldx, gamma, out, ldo, rows, d, row_map, eps, pk_rows, pk_kb, add, ld_add);
   if (vec) {
     const int vpt = (d / 4 + 127) / 128;
     if (vpt <= 1) { VLC_RMS(1) }
@@ -268,7 +290,7 @@ int vlc_rmsnorm_impl(const float* x, int ldx, const float* gamma, void* out, int
     else { VLC_RMS(16) }
   } else {
     e = launch_chain(out_f32 ? rmsnorm_generic<true> : rmsnorm_generic<false>, dim3(rows), dim3(256), 0, stream,
-                     false, x, ldx, gamma, out, ldo, rows, d, row_map, eps, pk_rows, pk_kb);
+                     false, x, ldx, gamma, out, ldo, rows, d, row_map, eps, pk_rows, pk_kb, add, ld_add);
   }
 #undef VLC_RMS
   return (int)e;

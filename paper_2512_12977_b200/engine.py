@@ -167,6 +167,7 @@ def _runner(model: ToyVLM):
     r = getattr(model, "_runner", None)
     if r is None:
         r = Runner(model.device)
+        r.tp_group = model.tp_group
         model._runner = r
     return r
 
@@ -309,7 +310,7 @@ def prefill_batch_with_reuse(model: ToyVLM, requests: list, store: CacheStore) -
         r.metrics.resolve_seconds = dt
 
     specs = [r.spec for r in resolved]
-    lay = _layout(runner, specs, L, cfg.num_heads)
+    lay = _layout(runner, specs, L, runner.dw.heads)
     import torch
     ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
     text_ids = np.concatenate([s.text_ids for s in specs])
@@ -334,7 +335,7 @@ def _merged_kv_loader(out, lay, spec: RequestSpec, kv_pool, cfg: ModelConfig, re
 
     def load():
         import torch
-        L, n, kvd = cfg.num_layers, spec.n, cfg.kv_dim
+        L, n, kvd = cfg.num_layers, spec.n, out["kc"].shape[2]   # this rank's heads under head-parallel
         kvoff = int(lay.kvoff[req])
         sel = np.flatnonzero(lay.row_req == req)
         pos = lay.row_pos[sel].astype(np.int64)
@@ -396,7 +397,7 @@ def _prefill_embeds(model: ToyVLM, seq: TokenSequence, image_embeds) -> ReuseRes
     spec = RequestSpec(n=len(seq), text_pos=text_pos, text_ids=text_ids,
                        images=[(s.start, s.length) for s in segs], keep=keep, kv_hit=[False] * len(segs),
                        enc_src=[(SRC_SCRATCH, m * T) for m in range(len(segs))], page_rows=[None] * len(segs))
-    lay = _layout(runner, [spec], L, cfg.num_heads)
+    lay = _layout(runner, [spec], L, runner.dw.heads)
     metrics = ReuseMetrics(mean_ratio=1.0)
     metrics.computed_per_layer = [len(seq)] * L
     ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))

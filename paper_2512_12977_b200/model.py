@@ -94,11 +94,31 @@ class ToyVLM:
     @property
     def device(self) -> "DeviceWeights":
         if self._device is None:
-            self._device = DeviceWeights.from_host(self.config, self.w)
+            self._device = DeviceWeights.from_host(self.config, self.w, self._heads())
         return self._device
 
+    # -- head-parallel attention: one process per GPU, this rank keeps
+    # its share of the heads; one all-reduce of the O-projection per layer.
+    tp_group = None
+
+    def head_parallel(self, group=None) -> "ToyVLM":
+        """Split attention heads over the ranks of `group` (torch.distributed; NCCL on B200)."""
+        import torch.distributed as dist
+        if self._device is not None:
+            raise InputError("head_parallel() must be called before the device weights are built")
+        self.tp_group = group if group is not None else dist.group.WORLD
+        return self
+
+    def _heads(self):
+        if self.tp_group is None:
+            return None
+        import torch.distributed as dist
+        from .sharding import head_split
+        return head_split(self.config.num_heads, dist.get_world_size(self.tp_group))[
+            dist.get_rank(self.tp_group)]
+
     @classmethod
-    def device_random(cls, config: ModelConfig, seed: int | None = None) -> "ToyVLM":
+    def device_random(cls, config: ModelConfig, seed: int | None = None, tp_group=None) -> "ToyVLM":
         """Random-init weights generated directly on the GPU (benchmarks at 7B shape, where the
         reference's 125 s host init would dominate).  Not bit-identical to init_model."""
         m = cls.__new__(cls)
@@ -107,7 +127,9 @@ class ToyVLM:
         s = config.seed if seed is None else seed
         m._fingerprint = int.from_bytes(hashlib.sha256(
             (_config_json(config) + f"|device-random|{s}").encode()).digest()[:8], "big")
-        m._device = DeviceWeights.random(config, s)
+        if tp_group is not None:
+            m.tp_group = tp_group
+        m._device = DeviceWeights.random(config, s, m._heads())
         return m
 
 
@@ -229,7 +251,10 @@ def rope_row_perm(kv: int, hd: int) -> np.ndarray:
 class DeviceWeights:
     """bf16 K-major weights + fp32 norms + RoPE tables on cuda:0 (see module doc)."""
 
-    def __init__(self, cfg: ModelConfig):
+    def __init__(self, cfg: ModelConfig, heads: tuple[int, int] | None = None):
+        """heads = (first head, count) of this rank under head-parallel attention (None = all):
+        Q/K/V keep only those heads' output rows, O only their input columns; the MLP, head and
+        vision encoder stay whole."""
         import torch
         from . import _native
 
@@ -237,7 +262,10 @@ class DeviceWeights:
             raise _native.NativeError("no CUDA device: the B200 path has no CPU fallback")
         _native.load()
         self.cfg = cfg
-        d, kv, h = cfg.model_dim, cfg.kv_dim, cfg.mlp_hidden
+        self.h0, self.heads = heads if heads is not None else (0, cfg.num_heads)
+        self.kv = self.heads * cfg.head_dim                 # local K/V width (this rank's heads)
+        self.c0, self.c1 = self.h0 * cfg.head_dim, self.h0 * cfg.head_dim + self.kv
+        d, kv, h = cfg.model_dim, self.kv, cfg.mlp_hidden
         self.kd = _round_up(d, 128)         # K of projections fed by d-wide rows
         self.kkv = _round_up(kv, 128)       # K of the O projection
         self.kh = _round_up(h, 128)         # K of the down projection
@@ -247,6 +275,9 @@ class DeviceWeights:
         self.n_gu = _round_up(2 * h, 128)
         self.n_vocab = _round_up(cfg.vocab_size, 128)
         self.perm = rope_row_perm(kv, cfg.head_dim)
+        self.enc_kv = cfg.kv_dim            # the encoder is never head-split
+        self.n_qkv_enc = _round_up(3 * cfg.kv_dim, 128)
+        self.kkv_enc = _round_up(cfg.kv_dim, 128)
         self.layers: list[dict] = []
         self.cos = self.sin = None
         self.tab_rows = 0
@@ -263,13 +294,28 @@ class DeviceWeights:
         out[:t.shape[0], :t.shape[1]] = t.to(torch.bfloat16)
         return out
 
-    def _block(self, torch, get):
-        """Device tensors of one transformer block; `get(name)` returns [in, out] fp32."""
+    def _block(self, torch, get, whole: bool = False):
+        """Device tensors of one transformer block; `get(name)` returns [in, out] fp32.  Unless
+        `whole`, attention weights are cut to this rank's heads."""
         cfg = self.cfg
-        kv, h = cfg.kv_dim, cfg.mlp_hidden
-        wqkv = torch.zeros(self.n_qkv, self.kd, dtype=torch.bfloat16, device="cuda")
-        wqkv[0:kv] = self._kmajor(torch, get("wq"), kv, self.kd, self.perm)
-        wqkv[kv:2 * kv] = self._kmajor(torch, get("wk"), kv, self.kd, self.perm)
+        h = cfg.mlp_hidden
+        if whole:
+            kv, n_qkv, kkv, perm = cfg.kv_dim, self.n_qkv_enc, self.kkv_enc, rope_row_perm(cfg.kv_dim, cfg.head_dim)
+            c0, c1 = 0, cfg.kv_dim
+        else:
+            kv, n_qkv, kkv, perm, c0, c1 = self.kv, self.n_qkv, self.kkv, self.perm, self.c0, self.c1
+        full_get = get
+
+        def get(name):                      # noqa: F811 -- head slice of the attention weights
+            w = full_get(name)
+            if name in ("wq", "wk", "wv"):
+                return w[:, c0:c1]
+            if name == "wo":
+                return w[c0:c1, :]
+            return w
+        wqkv = torch.zeros(n_qkv, self.kd, dtype=torch.bfloat16, device="cuda")
+        wqkv[0:kv] = self._kmajor(torch, get("wq"), kv, self.kd, perm)
+        wqkv[kv:2 * kv] = self._kmajor(torch, get("wk"), kv, self.kd, perm)
         wqkv[2 * kv:3 * kv] = self._kmajor(torch, get("wv"), kv, self.kd)
         wqkv_plain = torch.zeros_like(wqkv)
         wqkv_plain[0:kv] = self._kmajor(torch, get("wq"), kv, self.kd)
@@ -283,19 +329,19 @@ class DeviceWeights:
             t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
             return t.float().cuda().contiguous()
         return {"wqkv": PackedWeight(wqkv), "wqkv_plain": PackedWeight(wqkv_plain),
-                "wo": PackedWeight(self._kmajor(torch, get("wo"), self.n_d, self.kkv)),
+                "wo": PackedWeight(self._kmajor(torch, get("wo"), self.n_d, kkv)),
                 "wgu": PackedWeight(gu), "wd": PackedWeight(self._kmajor(torch, get("w_down"), self.n_d, self.kh)),
                 "attn_norm": norm(get("attn_norm")), "mlp_norm": norm(get("mlp_norm"))}
 
     @classmethod
-    def from_host(cls, cfg: ModelConfig, w: dict[str, np.ndarray]) -> "DeviceWeights":
+    def from_host(cls, cfg: ModelConfig, w: dict[str, np.ndarray], heads=None) -> "DeviceWeights":
         import torch
-        self = cls(cfg)
+        self = cls(cfg, heads)
         for i in range(cfg.num_layers):
             blk = self._block(torch, lambda n, i=i: w[f"l{i}_{n}"])
             blk.pop("wqkv_plain")
             self.layers.append(blk)
-        self.enc = self._block(torch, lambda n: w[f"enc_{n}"])
+        self.enc = self._block(torch, lambda n: w[f"enc_{n}"], whole=True)
         self.enc["patch_w"] = PackedWeight(self._kmajor(torch, w["enc_patch_w"], self.n_d, self.kp))
         self.enc["patch_b"] = torch.from_numpy(w["enc_patch_b"]).cuda()
         self.enc["pos"] = torch.from_numpy(np.ascontiguousarray(w["enc_pos"])).cuda()
@@ -307,10 +353,11 @@ class DeviceWeights:
         return self
 
     @classmethod
-    def random(cls, cfg: ModelConfig, seed: int) -> "DeviceWeights":
-        """Same distributions as model.py:165-210 (N(0,1)/sqrt(fan_in), unit norms), drawn on device."""
+    def random(cls, cfg: ModelConfig, seed: int, heads=None) -> "DeviceWeights":
+        """Same distributions as model.py:165-210 (N(0,1)/sqrt(fan_in), unit norms), drawn on device
+        (the full tensors are drawn on every rank, so head slices agree across ranks)."""
         import torch
-        self = cls(cfg)
+        self = cls(cfg, heads)
         g = torch.Generator(device="cuda").manual_seed(int(seed))
         d, kv, h, pp = cfg.model_dim, cfg.kv_dim, cfg.mlp_hidden, cfg.patch_size ** 2
         shapes = {"wq": (d, kv), "wk": (d, kv), "wv": (d, kv), "wo": (kv, d), "w_gate": (d, h),
@@ -325,7 +372,7 @@ class DeviceWeights:
             blk = self._block(torch, gen)
             blk.pop("wqkv_plain")
             self.layers.append(blk)
-        self.enc = self._block(torch, gen)
+        self.enc = self._block(torch, gen, whole=True)
         self.enc["patch_w"] = PackedWeight(self._kmajor(
             torch, torch.randn(pp, d, device="cuda", generator=g) / float(np.sqrt(pp)), self.n_d, self.kp))
         self.enc["patch_b"] = torch.randn(d, device="cuda", generator=g) / float(np.sqrt(d))

@@ -124,6 +124,7 @@ class Runner:
         self.graph_launches: dict = {}
         self.tracer = None         # list -> (name, ev0, ev1, algo_bytes, algo_flops) per launch
         self.overlap_reloc = _OVERLAP_RELOC
+        self.tp_group = None       # head-parallel process group (engine sets it from the model)
         self._side = None          # side stream of the overlapped kv_relocate
 
     def _run(self, name, fn, nbytes=0, flops=0, kernels=1):
@@ -176,16 +177,19 @@ class Runner:
             row_map, RMS_EPS, pk[0], pk[1], _stream()), "vlc_rmsnorm"), rows * d * (4 + (4 if out_f32 else 2)))
 
     def attention(self, q, kc, vc, layer, items_ptr, n_items, comb_ptr, n_comb, qpos_ptr, rowof_ptr, out,
-                  slots, nbytes=0, flops=0, pk=(0, 0)):
+                  slots, nbytes=0, flops=0, pk=(0, 0), kv=None, heads=None):
+        """kv / heads: this rank's K/V width and head count (default: the decoder's, head-split)."""
         torch = _torch()
         cfg = self.cfg
         hd = cfg.head_dim
+        kv = kv or self.dw.kv
+        heads = heads or self.dw.heads
         ws_o = self.shared.get("attn_ws_o", (max(1, slots) * 8 * 256 * hd,), torch.float32, zero=False)
         ws_ml = self.shared.get("attn_ws_ml", (max(1, slots) * 8 * 256 * 2,), torch.float32, zero=False)
         a = N.AttnArgs(q=q.data_ptr(), q_rows_cap=q.shape[0], kc=kc.data_ptr(), vc=vc.data_ptr(),
-                       layers_cap=kc.shape[0], kv_rows_cap=kc.shape[1], layer=layer, kv=cfg.kv_dim,
-                       heads=cfg.num_heads, head_dim=hd, items=items_ptr, n_items=n_items, qpos=qpos_ptr,
-                       rowof=rowof_ptr, out=out.data_ptr(), ldo=cfg.kv_dim, ws_o=ws_o.data_ptr(),
+                       layers_cap=kc.shape[0], kv_rows_cap=kc.shape[1], layer=layer, kv=kv,
+                       heads=heads, head_dim=hd, items=items_ptr, n_items=n_items, qpos=qpos_ptr,
+                       rowof=rowof_ptr, out=out.data_ptr(), ldo=kv, ws_o=ws_o.data_ptr(),
                        ws_ml=ws_ml.data_ptr(), ws_slots=slots, comb=comb_ptr, n_comb=n_comb,
                        scale_log2=math.log2(math.e) / math.sqrt(hd), counters=self.attn_counters.data_ptr(),
                        pk_rows=pk[0], pk_kb=pk[1])
@@ -211,7 +215,7 @@ class Runner:
         qe = ws.get("qe", (cap, kv), torch.bfloat16)
         ke = ws.get("ke", (1, cap, kv), torch.bfloat16)
         ve = ws.get("ve", (1, cap, kv), torch.bfloat16)
-        att = ws.get("att", (cap * dw.kkv,), torch.bfloat16)
+        att = ws.get("att", (cap * dw.kkv_enc,), torch.bfloat16)
         hb = ws.get("h", (cap * dw.kh,), torch.bfloat16)
         out = ws.get("out", (cap, d), torch.float32)
         side = cfg.image_side
@@ -228,7 +232,7 @@ class Runner:
             self.gemm(E["patch_w"], dw.kp, patches[m * rows_img * dw.kp:], T,
                       _epi(kind=N.EPI_BIAS_ADD, n_valid=d, out=xe[m * T].data_ptr(), ldo=d,
                            bias=E["patch_b"].data_ptr(), add=E["pos"].data_ptr(), ld_add=d))
-        pkd, pkkv, pkh = (RM, dw.kd // 128), (RM, dw.kkv // 128), (RM, dw.kh // 128)
+        pkd, pkkv, pkh = (RM, dw.kd // 128), (RM, dw.kkv_enc // 128), (RM, dw.kh // 128)
         self.rmsnorm(xe, E["attn_norm"], xn, M, pk=pkd)
         self.gemm(E["wqkv_plain"], dw.kd, xn, M,
                   _epi(kind=N.EPI_QKV_PLAIN, n_valid=3 * kv, out=qe.data_ptr(), ldo=kv, out2=ke.data_ptr(), ld2=kv,
@@ -245,8 +249,8 @@ class Runner:
         pack.add("rowof", np.arange(M))
         pack.upload(ws, "enc_ints")
         self.attention(qe, ke, ve, 0, pack.ptr("items"), len(items), pack.ptr("comb"), 0,
-                       pack.ptr("qpos"), pack.ptr("rowof"), att, slots, pk=pkkv)
-        self.gemm(E["wo"], dw.kkv, att, M, _epi(kind=N.EPI_RESID, n_valid=d, out=xe.data_ptr(), ldo=d))
+                       pack.ptr("qpos"), pack.ptr("rowof"), att, slots, pk=pkkv, kv=kv, heads=cfg.num_heads)
+        self.gemm(E["wo"], dw.kkv_enc, att, M, _epi(kind=N.EPI_RESID, n_valid=d, out=xe.data_ptr(), ldo=d))
         self.rmsnorm(xe, E["mlp_norm"], xn, M, pk=pkd)
         self.gemm(E["wgu"], dw.kd, xn, M,
                   _epi(kind=N.EPI_SWIGLU, n_valid=2 * cfg.mlp_hidden, out=hb.data_ptr(), ldo=dw.kh,
@@ -280,7 +284,7 @@ class Runner:
         torch = _torch()
         cfg, dw = self.cfg, self.dw
         ws = self._pick_set()
-        L, d, kv, V = cfg.num_layers, cfg.model_dim, cfg.kv_dim, cfg.vocab_size
+        L, d, kv, V = cfg.num_layers, cfg.model_dim, dw.kv, cfg.vocab_size
         c = lay.c
         c0 = int(c[0])
         R = -(-max(256, c0) // 256) * 256          # row capacity (whole 256-row tiles)
@@ -292,6 +296,8 @@ class Runner:
             h=ws.get("h", (R * dw.kh,), torch.bfloat16), kc=ws.get("kc", (L, KVR, kv), torch.bfloat16),
             vc=ws.get("vc", (L, KVR, kv), torch.bfloat16), kpre=ws.get("kpre", (L, R, kv), torch.bfloat16),
             logits=ws.get("logits", (max(int(c[L - 1]), 1), V), torch.float32, zero=False))
+        if self.tp_group is not None:
+            buf["y"] = ws.get("y", (R, d), torch.float32)      # this rank's O-projection partial
         hd = cfg.head_dim
         self.shared.get("attn_ws_o", (max(1, lay.attn_slots) * 8 * 256 * hd,), torch.float32, zero=False)
         self.shared.get("attn_ws_ml", (max(1, lay.attn_slots) * 8 * 256 * 2,), torch.float32, zero=False)
@@ -308,7 +314,7 @@ class Runner:
         chain = lambda: self._chain(lay, pack, buf, ptrs)  # noqa: E731
         if events is not None:
             events[0].record()
-        if use_graph and self.tracer is None and not _DEBUG_SYNC:
+        if use_graph and self.tracer is None and not _DEBUG_SYNC and self._graph_ok():
             skey = getattr(lay, "_skey", None)
             if skey is None:
                 skey = lay._skey = lay.structure_key()
@@ -370,9 +376,28 @@ class Runner:
         pk.host, pk.off = host, off
         return pk
 
+    def _allreduce(self, t):
+        import torch.distributed as dist
+        if self.tracer is None:
+            dist.all_reduce(t, group=self.tp_group)
+        else:
+            torch = _torch()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dist.all_reduce(t, group=self.tp_group)
+            e1.record()
+            self.tracer.append(("allreduce", e0, e1, t.numel() * 4, 0))
+
+    def _graph_ok(self) -> bool:
+        """The chain is graph-captured unless it contains a non-capturable collective (gloo)."""
+        if self.tp_group is None:
+            return True
+        import torch.distributed as dist
+        return dist.get_backend(self.tp_group) == "nccl"
+
     def _chain(self, lay: Layout, pack: "IntPack", buf: dict, ptrs):
         cfg, dw = self.cfg, self.dw
-        L, d, kv, V = cfg.num_layers, cfg.model_dim, cfg.kv_dim, cfg.vocab_size
+        L, d, kv, V = cfg.num_layers, cfg.model_dim, dw.kv, cfg.vocab_size
         x, xn, q, att, hb = buf["x"], buf["xn"], buf["q"], buf["att"], buf["h"]
         kc, vc, kpre, logits = buf["kc"], buf["vc"], buf["kpre"], buf["logits"]
         c = lay.c
@@ -429,11 +454,23 @@ class Runner:
                 _torch().cuda.current_stream().wait_event(side_ev[i])
             self.attention(q, kc, vc, i, pack.ptr(f"items{i}"), len(lay.attn_items[i]), pack.ptr(f"comb{i}"),
                            len(lay.comb_items[i]), pack.ptr(f"qpos{i}"), pack.ptr(f"rowof{i}"), att, lay.attn_slots,
-                           nbytes=lay.kv_rows * kv * 4 + ci * kv * 4, flops=4 * cfg.head_dim * cfg.num_heads * vis,
+                           nbytes=lay.kv_rows * kv * 4 + ci * kv * 4, flops=4 * cfg.head_dim * dw.heads * vis,
                            pk=(Ri, dw.kkv // 128))
-            self.gemm(W["wo"], dw.kkv, att, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d),
-                      name="gemm_o", k_valid=kv)
-            self.rmsnorm(x, W["mlp_norm"], xn, ci, pk=(Ri, dw.kd // 128))
+            if self.tp_group is None:
+                self.gemm(W["wo"], dw.kkv, att, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d),
+                          name="gemm_o", k_valid=kv)
+                self.rmsnorm(x, W["mlp_norm"], xn, ci, pk=(Ri, dw.kd // 128))
+            else:
+                # head-parallel: row-parallel O projection of this rank's heads -> y, one all-reduce
+                # of y over the group (NCCL / NVLink), then x += y fused into the MLP norm
+                y = buf["y"]
+                y[:ci].zero_()
+                self.gemm(W["wo"], dw.kkv, att, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=y.data_ptr(), ldo=d),
+                          name="gemm_o", k_valid=kv)
+                self._allreduce(y[:ci])
+                self._run("rmsnorm", lambda: N.check(self.lib.vlc_add_rmsnorm(
+                    x.data_ptr(), d, y.data_ptr(), d, W["mlp_norm"].data_ptr(), xn.data_ptr(), d, ci, d, RMS_EPS,
+                    Ri, dw.kd // 128, _stream()), "vlc_add_rmsnorm"), ci * d * 14)
             self.gemm(W["wgu"], dw.kd, xn, ci,
                       _epi(kind=N.EPI_SWIGLU, n_valid=2 * cfg.mlp_hidden, out=hb.data_ptr(), ldo=dw.kh,
                            pk_rows=Ri, pk_kb=dw.kh // 128),
