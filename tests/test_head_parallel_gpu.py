@@ -1,0 +1,115 @@
+"""Head-parallel attention against the CPU oracle on configs[0].
+
+* 2 ranks sharing one GPU over gloo (eager chain): each rank keeps half of the heads (Q/K/V
+  rows, O columns, cached K/V columns), the O projection is all-reduced once per layer; logits
+  must match the oracle and both ranks must agree.
+* 1 rank over NCCL: the same chain captured in a CUDA graph with the collective inside.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+KW = dict(num_layers=4, num_heads=8, model_dim=256, kv_dim=256, vocab_size=4096, patch_size=4,
+          tokens_per_image=256, seed=0)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _scene():
+    from oracle import kvreuse_oracle as O
+    oc = O.Cfg(**KW)
+    w = {k: O.bf16_round(v) for k, v in O.make_weights(oc).items()}
+    V, T = oc.vocab_size, oc.tokens_per_image
+    img = O.images(1, oc.side, 1)
+    enc, kv = {}, {}
+    ids0, segs0 = O.layout(O.prompt(V, 8, 11), 1, T)
+    O.fill_one(oc, w, ids0, segs0, img, enc, kv)
+    h = O.sha256_hex(img[0])
+    text = O.prompt(V, 32, 12)
+    ids, segs = O.layout(text[:16], 1, T, text[16:])
+    ref = O.reuse_prefill(oc, w, ids, segs, [h], (0.05, 0.05, 0.04, 0.02), enc, kv)
+    return O, oc, w, enc, kv, h, text, ref
+
+
+def _run_rank(rank, world, backend, port, q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2512_12977_b200 as P
+        from paper_2512_12977_b200.sharding import head_split
+        O, oc, w, enc, kv, h, text, ref = _scene()
+        model = P.ToyVLM(P.ModelConfig(**KW), w).head_parallel()
+        h0, hk = head_split(KW["num_heads"], world)[rank]
+        c0, c1 = h0 * oc.head_dim, (h0 + hk) * oc.head_dim
+        store = P.CacheStore()
+        store.put_encoder(P.EncoderCacheEntry(P.ImageHash(h), enc[h], model.fingerprint))
+        store.put_kv(P.KVCacheEntry(P.ImageHash(h), np.ascontiguousarray(kv[h].keys[:, :, c0:c1]),
+                                    np.ascontiguousarray(kv[h].values[:, :, c0:c1]), 8, model.fingerprint))
+        T = oc.tokens_per_image
+        req = P.ReuseRequest(P.make_sequence(text[:16], 1, T, text[16:]), [P.ImageHash(h)],
+                             P.RecomputePlan((0.05, 0.05, 0.04, 0.02)))
+        for _ in range(2):                       # second call replays the captured graph (NCCL)
+            res = P.prefill_with_reuse(model, req, store)
+        out = dict(rows=np.asarray(res.positions), counts=res.metrics.computed_per_layer, logits=res.logits,
+                   keys=res.kv.keys, values=res.kv.values, c0=c0, c1=c1)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn(world, backend):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_run_rank, args=(r, world, backend, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return outs
+
+
+def _check(outs, ref):
+    from conftest import rel_err
+    for rank, o in outs.items():
+        assert np.array_equal(o["rows"], ref.rows)
+        assert o["counts"] == ref.counts
+        assert rel_err(o["logits"], ref.logits) <= 2e-2, rank
+        assert int(np.argmax(o["logits"][-1])) == int(np.argmax(ref.logits[-1]))
+        # this rank's head slice of the merged pre-RoPE KV
+        assert rel_err(o["keys"], ref.keys[:, :, o["c0"]:o["c1"]]) <= 2e-2
+        assert rel_err(o["values"], ref.values[:, :, o["c0"]:o["c1"]]) <= 2e-2
+
+
+@pytest.mark.timeout(600)
+def test_head_parallel_two_ranks_gloo(cuda_ok):
+    outs = _spawn(2, "gloo")
+    ref = _scene()[-1]
+    _check(outs, ref)
+    assert np.allclose(outs[0]["logits"], outs[1]["logits"], atol=1e-5)
+
+
+@pytest.mark.timeout(600)
+def test_head_parallel_one_rank_nccl_graph(cuda_ok):
+    outs = _spawn(1, "nccl")
+    _check(outs, _scene()[-1])
