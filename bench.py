@@ -349,17 +349,23 @@ def main():
                         "TFps": round(fl / s / 1e12, 2) if fl else None})
     dom = kernels[0]
     dname = dom["name"]
+    try:   # DRAM bytes per launch from the committed ncu --set full capture (tools/ncu_traffic.py)
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh)
+    except (OSError, ValueError):
+        traffic = {}
     ms_d, cnt_d, nb_d, fl_d = agg[dname]
     if dname.startswith("gemm") or dname in ("kv_relocate", "rmsnorm", "embed"):
         ach = nb_d / (ms_d / 1e3) / 1e9
         roof = {"kernel": dname, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(ach / hbm, 4), "traffic": None,
+                "frac": round(ach / hbm, 4), "traffic": traffic.get(dname, {}).get("dram_bytes"),
                 "algorithmic": f"{nb_d / cnt_d / 1e6:.2f} MB per launch (bf16 weights + activations)",
                 "peak_source": f"{peak_src} hbm_gbs"}
     else:
         ach = fl_d / (ms_d / 1e3) / 1e12
         roof = {"kernel": dname, "bound": "tensor", "achieved": round(ach, 2), "peak": tf_burst, "unit": "TFLOP/s",
-                "frac": round(ach / tf_burst, 4), "traffic": None, "peak_source": f"{peak_src} bf16_tflops"}
+                "frac": round(ach / tf_burst, 4), "traffic": traffic.get(dname, {}).get("dram_bytes"),
+                "peak_source": f"{peak_src} bf16_tflops"}
     others = {}
     for k in ("kv_relocate", "attention"):
         if k in agg:

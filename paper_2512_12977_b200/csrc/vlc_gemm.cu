@@ -18,6 +18,7 @@
 //   BIAS_ADD  encoder patch embedding + bias + positional rows (model.py:316)
 //   QKV_PLAIN encoder projections (model.py:318)
 #include "vlc_internal.h"
+#include "vlc_gemm_epi.cuh"
 
 namespace vlc {
 
@@ -26,170 +27,6 @@ constexpr int GEMM_THREADS = 64 + 32 * GEMM_EPI_WARPS;
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 128;   // one stage = two 64-element (128 B) swizzle atoms along K
 constexpr int GEMM_ATOM_K = 64;
-
-__device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
-
-__device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) {
-  return make_uint2(pack_bf16(a, b), pack_bf16(c, d));
-}
-
-// Final values of 4 consecutive DEVICE features [F, F+4) of token j (token-major group).
-// Device feature order: q/k rows permuted so RoPE pairs are adjacent (F, F+1), gate/up
-// interleaved (gate f at 2f, up f at 2f+1); see model.py DeviceWeights.
-template <int KIND>
-__device__ __forceinline__ void write_group(const GemmEpi& e, int F, int j, float4 v) {
-  if (F >= e.n_valid) return;
-  const bool full4 = F + 4 <= e.n_valid;
-  switch (KIND) {
-    case EPI_F32: {
-      const long r = e.map1 ? __ldg(e.map1 + j) : j;
-      float* o = reinterpret_cast<float*>(e.out) + r * e.ldo + F;
-      if (full4 && (e.ldo & 3) == 0) {
-        *reinterpret_cast<float4*>(o) = v;
-      } else {
-        const float vv[4] = {v.x, v.y, v.z, v.w};
-        for (int i = 0; i < 4 && F + i < e.n_valid; ++i) o[i] = vv[i];
-      }
-      break;
-    }
-    case EPI_RESID: {   // x += acc as an L2 vector reduction: split-K partials need no fixup
-      float* o = reinterpret_cast<float*>(e.out) + (long)j * e.ldo + F;
-      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(o), "f"(v.x), "f"(v.y), "f"(v.z),
-                   "f"(v.w)
-                   : "memory");
-      break;
-    }
-    case EPI_BF16: {
-      const long off = e.pk_rows > 0 ? packed_off(j, F, e.pk_rows, e.pk_kb) : (long)j * e.ldo + F;
-      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(e.out) + off) = pack4_bf16(v.x, v.y, v.z, v.w);
-      break;
-    }
-    case EPI_BIAS_ADD: {
-      float4 b = e.bias ? __ldg(reinterpret_cast<const float4*>(e.bias + F)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      float4 a = e.add ? __ldg(reinterpret_cast<const float4*>(e.add + (long)j * e.ld_add + F))
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
-      *reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (long)j * e.ldo + F) =
-          make_float4((v.x + b.x) + a.x, (v.y + b.y) + a.y, (v.z + b.z) + a.z, (v.w + b.w) + a.w);
-      break;
-    }
-    case EPI_SWIGLU: {
-      const long off = e.pk_rows > 0 ? packed_off(j, F >> 1, e.pk_rows, e.pk_kb) : (long)j * e.ldo + (F >> 1);
-      *reinterpret_cast<uint32_t*>(reinterpret_cast<__nv_bfloat16*>(e.out) + off) =
-          pack_bf16(silu_f(v.x) * v.y, silu_f(v.z) * v.w);
-      break;
-    }
-    case EPI_QKV_PLAIN: {
-      const int sec = F / e.seg, r = F - sec * e.seg;
-      void* dst = sec == 0 ? e.out : sec == 1 ? e.out2 : e.out3;
-      const int ld = sec == 0 ? e.ldo : sec == 1 ? e.ld2 : e.ld3;
-      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(dst) + (long)j * ld + r) = pack4_bf16(v.x, v.y, v.z, v.w);
-      break;
-    }
-    case EPI_QKV_ROPE: {
-      const int sec = F / e.seg, r = F - sec * e.seg;
-      if (sec == 2) {
-        const long kr = __ldg(e.map2 + j);
-        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(e.out3) + kr * e.ld3 + r) =
-            pack4_bf16(v.x, v.y, v.z, v.w);
-        break;
-      }
-      const int half = e.hd >> 1;
-      const int head = r / e.hd, t = (r - head * e.hd) >> 1;   // pairs (t, t+half), (t+1, t+1+half)
-      const long tab = (long)__ldg(e.pos + j) * e.tab_ld + t;
-      const float2 c = __ldg(reinterpret_cast<const float2*>(e.cos_tab + tab));
-      const float2 sn = __ldg(reinterpret_cast<const float2*>(e.sin_tab + tab));
-      const uint32_t lo = pack_bf16(v.x * c.x - v.y * sn.x, v.z * c.y - v.w * sn.y);
-      const uint32_t hi = pack_bf16(v.y * c.x + v.x * sn.x, v.w * c.y + v.z * sn.y);
-      const int fa = head * e.hd + t;
-      if (sec == 0) {
-        const long qr = e.map1 ? __ldg(e.map1 + j) : j;
-        __nv_bfloat16* q = reinterpret_cast<__nv_bfloat16*>(e.out) + qr * e.ldo;
-        *reinterpret_cast<uint32_t*>(q + fa) = lo;
-        *reinterpret_cast<uint32_t*>(q + fa + half) = hi;
-      } else {
-        const long kr = __ldg(e.map2 + j);
-        __nv_bfloat16* k = reinterpret_cast<__nv_bfloat16*>(e.out2) + kr * e.ld2;
-        *reinterpret_cast<uint32_t*>(k + fa) = lo;
-        *reinterpret_cast<uint32_t*>(k + fa + half) = hi;
-        if (e.out4) {
-          __nv_bfloat16* kp = reinterpret_cast<__nv_bfloat16*>(e.out4) + (long)j * e.ld4;
-          *reinterpret_cast<uint32_t*>(kp + fa) = pack_bf16(v.x, v.z);
-          *reinterpret_cast<uint32_t*>(kp + fa + half) = pack_bf16(v.y, v.w);
-        }
-      }
-      break;
-    }
-    default:
-      break;
-  }
-}
-
-// The up-to-8 tokens jj = quad + 4q (q < 8, jj < jv) of one 32-token chunk, features [F, F+4):
-// loads of per-token metadata / RoPE tables are issued for all tokens before any store, so the
-// epilogue is not a chain of dependent global-load latencies.  sb = stage + 4*lane (token stride
-// 128 floats).
-template <int KIND>
-__device__ __forceinline__ void write_chunk(const GemmEpi& e, int F, int j0, int quad, int jv, const float* sb) {
-  if constexpr (KIND == EPI_QKV_ROPE) {
-    if (F >= e.n_valid) return;
-    const int sec = F / e.seg, r = F - sec * e.seg;
-    float4 v[8];
-    int p[8];
-    long dr[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int jj = quad + 4 * q;
-      if (jj < jv) {
-        const int j = j0 + jj;
-        v[q] = *reinterpret_cast<const float4*>(sb + jj * 128);
-        p[q] = __ldg(e.pos + j);
-        dr[q] = sec == 0 ? (e.map1 ? __ldg(e.map1 + j) : j) : __ldg(e.map2 + j);
-      }
-    }
-    if (sec == 2) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (quad + 4 * q < jv)
-          *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(e.out3) + dr[q] * e.ld3 + r) =
-              pack4_bf16(v[q].x, v[q].y, v[q].z, v[q].w);
-      return;
-    }
-    const int half = e.hd >> 1;
-    const int head = r / e.hd, t = (r - head * e.hd) >> 1;   // pairs (t, t+half), (t+1, t+1+half)
-    const int fa = head * e.hd + t;
-    float2 cq[8], sq[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      if (quad + 4 * q < jv) {
-        const long tab = (long)p[q] * e.tab_ld + t;
-        cq[q] = __ldg(reinterpret_cast<const float2*>(e.cos_tab + tab));
-        sq[q] = __ldg(reinterpret_cast<const float2*>(e.sin_tab + tab));
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      if (quad + 4 * q >= jv) continue;
-      const float2 c = cq[q], sn = sq[q];
-      const float4 x = v[q];
-      const uint32_t lo = pack_bf16(x.x * c.x - x.y * sn.x, x.z * c.y - x.w * sn.y);
-      const uint32_t hi = pack_bf16(x.y * c.x + x.x * sn.x, x.w * c.y + x.z * sn.y);
-      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(sec == 0 ? e.out : e.out2) + dr[q] * (sec == 0 ? e.ldo : e.ld2);
-      *reinterpret_cast<uint32_t*>(o + fa) = lo;
-      *reinterpret_cast<uint32_t*>(o + fa + half) = hi;
-      if (sec == 1 && e.out4) {
-        __nv_bfloat16* kp = reinterpret_cast<__nv_bfloat16*>(e.out4) + (long)(j0 + quad + 4 * q) * e.ld4;
-        *reinterpret_cast<uint32_t*>(kp + fa) = pack_bf16(x.x, x.z);
-        *reinterpret_cast<uint32_t*>(kp + fa + half) = pack_bf16(x.y, x.w);
-      }
-    }
-  } else {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int jj = quad + 4 * q;
-      if (jj < jv) write_group<KIND>(e, F, j0 + jj, *reinterpret_cast<const float4*>(sb + jj * 128));
-    }
-  }
-}
 
 // ------------------------------------------------------------------ stream-K schedule
 struct SkSched {
@@ -482,6 +319,8 @@ void set_debug_buffer(unsigned long long* p) { cudaMemcpyToSymbol(g_dbg, &p, siz
 int g_coop = 1;
 int g_pdl = 1;
 
+int g_pair = 96;          // tuning key 10: CTA-pair GEMM for non-RESID kinds when n_tile >= this (0 = off)
+int g_unsplit_min = 64;   // tuning key 9: tile count from which each tile gets its own CTA (no split-K)
 int g_wide = 1;   // tuning key 7: 0 auto, 1 never use 256-row tiles (default: measured slower), 2 always
 
 static int gemm_pick_stages(int n_tile, int H) {
@@ -522,6 +361,16 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
                         int* counters, cudaStream_t stream) {
   if (m_tokens <= 0) return cudaSuccess;
   const int n_tile = gemm_row_tile(m_tokens);
+  // token-heavy non-residual GEMMs: CTA-pair kernel (halves the activation bytes per SM)
+  // (multi-wave GEMMs only -- the LM head: measured 7% faster there, no gain at <= 1 wave)
+  //  g_pair < 0: force the pair kernel from n_tile >= -g_pair (tests)
+  const int pair_min = g_pair < 0 ? -g_pair : g_pair;
+  if (g_pair != 0 && epi.kind != EPI_RESID && n_tile >= pair_min &&
+      (g_pair < 0 || (long long)(n_pad / 128) * ((m_tokens + n_tile - 1) / n_tile) >= 2LL * num_sms())) {
+    const cudaError_t e = launch_gemm_pair(W, n_pad, k_pad, X, x_rows_cap, m_tokens, epi,
+                                           max_ctas > 0 ? max_ctas / 2 : 0, stream);
+    if (e != cudaErrorNotSupported) return e;
+  }
   const bool wide_ok = n_pad % 256 == 0;
   const int H = (g_wide == 2 && wide_ok) || (g_wide == 0 && wide_ok && n_tile >= 96) ? 2 : 1;
   const int BM = GEMM_BM * H, BK = GEMM_BK / H;
@@ -535,7 +384,7 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   // automatic schedule: enough weight tiles -> one CTA per tile (no split-K fixup); few tiles
   // (the d x d projections) -> stream-K over every SM
   const long long tiles = (long long)m_tiles * tok_tiles;
-  if (max_ctas == 0 && tiles >= 64 && tiles <= G) G = (int)tiles;
+  if (max_ctas == 0 && tiles >= g_unsplit_min && tiles <= G) G = (int)tiles;
   // split tiles reduce through the workspace with <= 8 participants, except RESID (red.add into
   // the residual, any number of participants; >= 2 k-blocks per CTA)
   const int min_units = epi.kind == EPI_RESID ? 2 : (KB + 5) / 6;

@@ -24,6 +24,8 @@ using GemmEpi = vlc_epilogue;
 extern int g_stage_override;  // experiment knob (vlc_set_tuning key 1)
 extern int g_attn_min_smem;   // key 5: lower bound on the attention kernel's dynamic smem
 extern int g_coop;            // key 2: cooperative launch of the stream-K GEMM
+extern int g_pair;            // key 10: CTA-pair GEMM threshold on the token tile (0 = off)
+extern int g_unsplit_min;     // key 9: tiles >= this (and <= #SMs) -> one CTA per tile
 extern int g_wide;            // key 7: 256-row GEMM tiles (0 auto, 1 never, 2 always)
 extern int g_pdl;             // key 6: programmatic dependent launch of the chain kernels (default 1)
 void set_debug_buffer(unsigned long long* p);
@@ -72,6 +74,8 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
                         int m_tokens, const GemmEpi& epi, int max_ctas, float* ws, size_t ws_bytes,
                         int* counters, cudaStream_t stream);
 int gemm_row_tile(int m_tokens);
+cudaError_t launch_gemm_pair(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap, int m_tokens,
+                             const GemmEpi& epi, int max_pairs, cudaStream_t stream);
 cudaError_t launch_pack(const void* src, int rows, int cols, int ld, void* dst, int R, int KB, cudaStream_t s);
 
 cudaError_t launch_attention(const vlc_attn_args& a, cudaStream_t stream);

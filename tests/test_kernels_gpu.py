@@ -332,3 +332,39 @@ def test_gemm_tile_modes_swiglu_packed(nat, gemm_mode, mode):
     gate, up = acc[:, 0::2], acc[:, 1::2]
     ref = gate / (1 + torch.exp(-gate)) * up
     assert (h - ref).abs().max().item() <= 2e-2 * ref.abs().max().item()
+
+
+@pytest.fixture
+def pair_mode(nat):
+    nat.load().vlc_set_tuning(10, -32)     # force the CTA-pair kernel from 32-token tiles
+    yield
+    nat.load().vlc_set_tuning(10, 96)
+
+
+@pytest.mark.parametrize("n_pad,k_pad,m", [(256, 128, 32), (512, 256, 100), (10752, 3584, 236), (2048, 256, 600),
+                                           (512, 384, 48)])
+def test_gemm_cta_pair_f32(nat, pair_mode, n_pad, k_pad, m):
+    """cta_group::2 GEMM (M = 256 over an SM pair, token rows split between the two SMs)."""
+    g = torch.Generator(device="cuda").manual_seed(n_pad + m)
+    W = torch.randn(n_pad, k_pad, device="cuda", generator=g).bfloat16()
+    X = torch.randn(max(256, m), k_pad, device="cuda", generator=g).bfloat16()
+    ref = X[:m].float() @ W.float().t()
+    out = torch.full((m, n_pad), float("nan"), device="cuda")
+    _gemm(nat, W, X, m, _epi(nat, kind=nat.EPI_F32, n_valid=n_pad, m_tokens=m, out=out.data_ptr(), ldo=n_pad), 0)
+    assert (out - ref).abs().max().item() / ref.abs().max().item() < 1e-5
+
+
+def test_gemm_cta_pair_swiglu_packed(nat, pair_mode):
+    g = torch.Generator(device="cuda").manual_seed(9)
+    n, k, m = 1024, 512, 236
+    W = torch.randn(n, k, device="cuda", generator=g).bfloat16()
+    X = torch.randn(256, k, device="cuda", generator=g).bfloat16()
+    acc = X[:m].float() @ W.float().t()
+    R = nat.row_tile(m)
+    hp = torch.zeros(nat.packed_numel(m, n // 2, R), device="cuda", dtype=torch.bfloat16)
+    _gemm(nat, W, X, m, _epi(nat, kind=nat.EPI_SWIGLU, n_valid=n, m_tokens=m, out=hp.data_ptr(), ldo=n // 2,
+                             pk_rows=R, pk_kb=-(-(n // 2) // 128)))
+    h = nat.unpack(hp, m, n // 2, R).float()
+    gate, up = acc[:, 0::2], acc[:, 1::2]
+    ref = gate / (1 + torch.exp(-gate)) * up
+    assert (h - ref).abs().max().item() <= 2e-2 * ref.abs().max().item()

@@ -84,8 +84,11 @@ def main():
                       tab_ld=half, hd=hd, seg=kv).items():
         setattr(rope, kk, v)
     for name, e in (("qkv bf16", plain), ("qkv rope", rope)):
-        print(f"{name}: {timed(Ws, n, k, X, R, e):.2f} us", flush=True)
-        phases(Ws[0], n, k, X, R, e)
+        for um in (64, 1000):
+            lib.vlc_set_tuning(9, um)
+            print(f"{name} unsplit_min={um}: {timed(Ws, n, k, X, R, e):.2f} us", flush=True)
+            phases(Ws[0], n, k, X, R, e)
+        lib.vlc_set_tuning(9, 64)
     # gate/up
     n = 14336
     Ws = [N.pack(torch.randn(n, k, device="cuda").bfloat16(), 128) for _ in range(3)]
@@ -95,8 +98,11 @@ def main():
     sw = N.Epilogue()
     sw.kind, sw.n_valid, sw.m_tokens, sw.out, sw.ldo, sw.pk_rows, sw.pk_kb = N.EPI_SWIGLU, n, m, h.data_ptr(), n // 2, R, n // 256
     for name, e in (("gu bf16", plain), ("gu swiglu", sw)):
-        print(f"{name}: {timed(Ws, n, k, X, R, e):.2f} us", flush=True)
-        phases(Ws[0], n, k, X, R, e)
+        for um in (64, 1000):
+            lib.vlc_set_tuning(9, um)
+            print(f"{name} unsplit_min={um}: {timed(Ws, n, k, X, R, e):.2f} us", flush=True)
+            phases(Ws[0], n, k, X, R, e)
+        lib.vlc_set_tuning(9, 64)
 
 
 main()
