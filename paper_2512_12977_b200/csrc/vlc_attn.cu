@@ -347,32 +347,40 @@ __device__ __forceinline__ void atrace(int slot) {
   }
 }
 void set_attn_trace_buffer(unsigned long long* p) { cudaMemcpyToSymbol(g_attn_trace, &p, sizeof(p)); }
-constexpr int PP_KT = 64;
+// KT = keys per tile.  KT = 64: S double-buffered per query tile (S runs two tiles ahead).
+// KT = 128 (hd 128): one 128-column S buffer per query tile (TMEM: S_A, S_B, O_A, O_B = 512
+// columns), half the MMA instructions and barrier round trips per key; the ping-pong between
+// the two query tiles hides the S(j) -> softmax -> PV(j) -> S(j+1) chain of each tile.
+int g_attn_kt = 128;   // tuning key 12: key tile of the hd-128 kernel (64 or 128)
 
-template <int HD>
+template <int HD, int KT>
 struct PPCfg {
+  static constexpr bool DB = KT == 64;
   static constexpr int ATOM_E = HD < 64 ? HD : 64;
   static constexpr int SWZ = ATOM_E * 2;
   static constexpr int N_ATOMS = HD / ATOM_E;
   static constexpr int Q_BYTES = 128 * HD * 2;
   static constexpr int Q_ATOM = 128 * SWZ;
-  static constexpr int KV_BYTES = PP_KT * HD * 2;
-  static constexpr int KV_ATOM = PP_KT * SWZ;
+  static constexpr int KV_BYTES = KT * HD * 2;
+  static constexpr int KV_ATOM = KT * SWZ;
   // K/V ring as deep as shared memory allows (<= 8): the softmax warps wait on S, i.e. on K/V
   // loads, when the ring is shallow (ncu: s_full wait was the top stall at 3 stages)
   static constexpr int ST_FIT = (232448 - 1024 - 256 - 2 * Q_BYTES) / (2 * KV_BYTES);
   static constexpr int ST = ST_FIT > 8 ? 8 : ST_FIT;
   static constexpr int SMEM = 1024 + 2 * Q_BYTES + ST * 2 * KV_BYTES + 256;
-  // TMEM: S[x][buf] (64 fp32 cols; P bf16 pairs aliased in its first 32 cols), O[x] (HD cols)
-  __device__ static constexpr uint32_t s_col(int x, int b) { return 64u * (2 * x + b); }
+  // TMEM: S[x][buf] (KT fp32 cols; P bf16 pairs aliased in its first KT/2 cols), O[x] (HD cols)
+  __device__ static constexpr uint32_t s_col(int x, int b) { return DB ? 64u * (2 * x + b) : 128u * x; }
   __device__ static constexpr uint32_t o_col(int x) { return 256u + (uint32_t)(HD > 64 ? HD : 64) * x; }
+  __device__ static constexpr int sbuf(int j) { return DB ? (j & 1) : 0; }          // S buffer of tile j
+  __device__ static constexpr uint32_t sphase(int j) { return DB ? ((j >> 1) & 1) : (j & 1); }
 };
 
-template <int HD>
+template <int HD, int KT>
 __global__ void __launch_bounds__(PP_THREADS, 1)
     attn_pp_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                    const __grid_constant__ CUtensorMap map_v, vlc_attn_args a) {
-  using C = PPCfg<HD>;
+  using C = PPCfg<HD, KT>;
+  constexpr int PP_KT = KT;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                                   // [2][Q_BYTES]
@@ -463,9 +471,9 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
           const uint32_t eoff = ((k * 16) % C::ATOM_E) * 2;
           const uint64_t ad = make_sdesc(q_addr + at * C::Q_ATOM + eoff, 16, 8 * C::SWZ, C::SWZ);
           const uint64_t bd = make_sdesc(k_addr + at * C::KV_ATOM + eoff, 16, 8 * C::SWZ, C::SWZ);
-          tc_mma_f16(tmem + C::s_col(x, j & 1), ad, bd, idesc_s, k > 0 ? 1u : 0u);
+          tc_mma_f16(tmem + C::s_col(x, C::sbuf(j)), ad, bd, idesc_s, k > 0 ? 1u : 0u);
         }
-        tc_commit(&s_full[2 * x + (j & 1)]);
+        tc_commit(&s_full[2 * x + C::sbuf(j)]);
       };
       auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j, P from TMEM (aliased in S[x][j&1])
         const int st = j % C::ST;
@@ -473,23 +481,25 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
 #pragma unroll
         for (int k = 0; k < PP_KT / 16; ++k) {
           const uint64_t bd = make_sdesc(v_addr + k * 16 * C::SWZ, C::KV_ATOM, 8 * C::SWZ, C::SWZ);
-          tc_mma_f16_ts(tmem + C::o_col(x), tmem + C::s_col(x, j & 1) + k * 8, bd, idesc_o,
+          tc_mma_f16_ts(tmem + C::o_col(x), tmem + C::s_col(x, C::sbuf(j)) + k * 8, bd, idesc_o,
                         (j > 0 || k > 0) ? 1u : 0u);
         }
         tc_commit(&o_done[x]);
       };
-      // S runs two tiles ahead of the softmax (double-buffered per query tile)
-      for (int j = 0; j < 2; ++j)
+      // DB: S runs two tiles ahead of the softmax (double-buffered per query tile); otherwise one
+      // tile ahead: S(j+1) is issued right after PV(j), which frees the single S/P buffer
+      constexpr int AHEAD = C::DB ? 2 : 1;
+      for (int j = 0; j < AHEAD; ++j)
         for (int x = 0; x < 2; ++x)
           if (j < nt_t[x]) issue_s(x, j);
       for (int j = 0; j < nt; ++j) {
         for (int x = 0; x < 2; ++x) {
           if (j >= nt_t[x]) continue;
-          mbar_wait(&p_full[2 * x + (j & 1)], (j >> 1) & 1);
+          mbar_wait(&p_full[2 * x + C::sbuf(j)], C::sphase(j));
           tc_fence_after();
           if (j < 16) atrace(64 + j * 4 + 2 * x);
           issue_pv(x, j);
-          if (j + 2 < nt_t[x]) issue_s(x, j + 2);   // in-order after PV(j): reuses P(j)'s columns
+          if (j + AHEAD < nt_t[x]) issue_s(x, j + AHEAD);   // in-order after PV(j): reuses P(j)'s columns
           if (j < 16) atrace(64 + j * 4 + 2 * x + 1);
         }
         tc_commit(&kv_empty[j % C::ST]);
@@ -511,14 +521,14 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     float m_run = NEG_INF, l_run = 0.f;
     for (int j = 0; j < ntx; ++j) {
       const int k0 = kb + j * PP_KT;
-      const uint32_t tS = tmem + C::s_col(x, j & 1) + lane_off;
+      const uint32_t tS = tmem + C::s_col(x, C::sbuf(j)) + lane_off;
       float s[PP_KT];
-      mbar_wait(&s_full[2 * x + (j & 1)], (j >> 1) & 1);
+      mbar_wait(&s_full[2 * x + C::sbuf(j)], C::sphase(j));
       tc_fence_after();
       const bool tr = (r == 0 && j < 16);
       if (tr) atrace((x ? 160 : 0) + j * 4);
-      tmem_ld32(tS, s);
-      tmem_ld32(tS + 32, s + 32);
+#pragma unroll
+      for (int c = 0; c < PP_KT / 32; ++c) tmem_ld32(tS + 32 * c, s + 32 * c);
       tmem_wait_ld();
       if (tr) atrace((x ? 160 : 0) + j * 4 + 1);
       // scores stay raw (scale folded into the exp2 FFMA); masked keys -> -inf; reductions in
@@ -540,7 +550,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       // when rescaling, and on the last tile (so that the final wait below is unambiguous):
       // o_done has completed j-1 or j phases here (S(j) done => PV(j-2) done).
       const bool resc = __any_sync(0xffffffffu, need && has_o);
-      if (j > 0 && (resc || j == ntx - 1)) {
+      if (C::DB && j > 0 && (resc || j == ntx - 1)) {   // !DB: S(j) done => PV(j-1) done already
         mbar_wait(&o_done[x], (j - 1) & 1);
         tc_fence_after();
       }
@@ -563,21 +573,22 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       }
       const bool any = m_run != NEG_INF;
       const float nm = any ? -m_run : NEG_INF;     // all-masked row: every p = exp2(-inf) = 0
-      uint32_t pk[PP_KT / 2];
+      // P packed in place into s[0, KT/2) (slot i is free once pairs 2i, 2i+1 are read)
       float ls4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int i = 0; i < PP_KT / 2; ++i) {
         const float p0 = fast_exp2(fmaf(s[2 * i], a.scale_log2, nm));
         const float p1 = fast_exp2(fmaf(s[2 * i + 1], a.scale_log2, nm));
         ls4[i & 3] += p0 + p1;
-        pk[i] = pack_bf16(p0, p1);
+        s[i] = __uint_as_float(pack_bf16(p0, p1));
       }
       l_run += (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
       if (tr) atrace((x ? 160 : 0) + j * 4 + 2);
-      tmem_st32(tS, pk);   // P(j) overwrites the first 32 columns of S[x][j&1]
+#pragma unroll
+      for (int c = 0; c < PP_KT / 64; ++c) tmem_st32f(tS + 32 * c, s + 32 * c);   // P(j) over S(j)'s first cols
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&p_full[2 * x + (j & 1)]);   // per-buffer barrier: softmax may run a tile ahead
+      mbar_arrive(&p_full[2 * x + C::sbuf(j)]);   // per-buffer barrier: softmax may run a tile ahead
       if (tr) atrace((x ? 160 : 0) + j * 4 + 3);
     }
     if (ntx > 0) {   // o_done has completed ntx-1 or ntx phases here
@@ -698,9 +709,9 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
 
 int g_attn_min_smem = 0;
 
-template <int HD>
+template <int HD, int KT>
 static cudaError_t launch_pp_hd(const vlc_attn_args& a, cudaStream_t stream, bool coop) {
-  using C = PPCfg<HD>;
+  using C = PPCfg<HD, KT>;
   CUtensorMap mq, mk, mv;
   // Q: {atom elems, rows, atoms} box {ATOM_E, 128, N_ATOMS}: one op = both swizzle atoms of a tile
   cudaError_t e = make_tmap_3d(&mq, a.q, C::ATOM_E, a.q_rows_cap, a.kv / C::ATOM_E, (uint64_t)a.kv * 2,
@@ -709,27 +720,27 @@ static cudaError_t launch_pp_hd(const vlc_attn_args& a, cudaStream_t stream, boo
   const uint64_t dims[4] = {(uint64_t)C::ATOM_E, (uint64_t)a.kv_rows_cap, (uint64_t)(a.kv / C::ATOM_E),
                             (uint64_t)a.layers_cap};
   const uint64_t strides[3] = {(uint64_t)a.kv * 2, (uint64_t)C::SWZ, (uint64_t)a.kv * 2 * a.kv_rows_cap};
-  const uint32_t box[4] = {(uint32_t)C::ATOM_E, (uint32_t)PP_KT, (uint32_t)C::N_ATOMS, 1};
+  const uint32_t box[4] = {(uint32_t)C::ATOM_E, (uint32_t)KT, (uint32_t)C::N_ATOMS, 1};
   e = make_tmap_4d(&mk, a.kc, dims, strides, box, C::SWZ);
   if (e != cudaSuccess) return e;
   e = make_tmap_4d(&mv, a.vc, dims, strides, box, C::SWZ);
   if (e != cudaSuccess) return e;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_pp_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaFuncSetAttribute(attn_pp_kernel<HD, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     attr = true;
   }
   const int smem = C::SMEM > g_attn_min_smem ? C::SMEM : g_attn_min_smem;
-  return launch_chain(attn_pp_kernel<HD>, dim3(a.n_items), dim3(PP_THREADS), smem, stream, coop, mq, mk, mv, a);
+  return launch_chain(attn_pp_kernel<HD, KT>, dim3(a.n_items), dim3(PP_THREADS), smem, stream, coop, mq, mk, mv, a);
 }
 
 cudaError_t launch_attention_pp(const vlc_attn_args& a, cudaStream_t stream, bool coop) {
   if (a.n_items <= 0) return cudaSuccess;
   switch (a.head_dim) {
-    case 16: return launch_pp_hd<16>(a, stream, coop);
-    case 32: return launch_pp_hd<32>(a, stream, coop);
-    case 64: return launch_pp_hd<64>(a, stream, coop);
-    case 128: return launch_pp_hd<128>(a, stream, coop);
+    case 16: return launch_pp_hd<16, 64>(a, stream, coop);
+    case 32: return launch_pp_hd<32, 64>(a, stream, coop);
+    case 64: return launch_pp_hd<64, 64>(a, stream, coop);
+    case 128: return g_attn_kt == 128 ? launch_pp_hd<128, 128>(a, stream, coop) : launch_pp_hd<128, 64>(a, stream, coop);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -22,6 +22,7 @@ enum EpiKind {
 using GemmEpi = vlc_epilogue;
 
 extern int g_stage_override;  // experiment knob (vlc_set_tuning key 1)
+extern int g_attn_kt;         // key 12: key tile of the hd-128 attention kernel (64 / 128)
 extern int g_attn_min_smem;   // key 5: lower bound on the attention kernel's dynamic smem
 extern int g_coop;            // key 2: cooperative launch of the stream-K GEMM
 extern int g_pair;            // key 10: CTA-pair GEMM threshold on the token tile (0 = off)

@@ -68,5 +68,8 @@ def run(max_ctas):
 
 
 if __name__ == "__main__":
-  for mc in (148, 28):
-    run(mc)
+  for kt in (64, 128):
+    lib.vlc_set_tuning(12, kt)
+    print(f"== key tile {kt}", flush=True)
+    for mc in (148, 28):
+      run(mc)
