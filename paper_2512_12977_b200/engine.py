@@ -113,6 +113,9 @@ class ReuseMetrics:
         self._compute = v
 
 
+_PINNED: dict = {}   # numel -> pinned host staging row for last_logits()
+
+
 class ReuseResult:
     """positions (host), logits [len(positions), V] and merged pre-RoPE KV, device-backed."""
 
@@ -134,7 +137,15 @@ class ReuseResult:
         return self._logits
 
     def last_logits(self) -> np.ndarray:
-        return self._dev_logits[-1].cpu().numpy()
+        """Last row's logits (the next-token distribution) via a pinned staging buffer."""
+        import torch
+        row = self._dev_logits[-1]
+        buf = _PINNED.get(row.numel())
+        if buf is None:
+            buf = _PINNED[row.numel()] = torch.empty(row.numel(), dtype=row.dtype, pin_memory=True)
+        buf.copy_(row, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return buf.numpy().copy()
 
     def _detach(self):
         """The runner is about to reuse its workspace: take private copies."""

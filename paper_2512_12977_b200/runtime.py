@@ -45,6 +45,7 @@ class Workspace:
 
     def __init__(self):
         self.bufs: dict[str, object] = {}
+        self.pinned: dict[str, tuple] = {}     # key -> (pinned host staging tensor, last copy event)
         self.live = weakref.WeakSet()
 
     def get(self, name: str, shape: tuple, dtype, zero: bool = True):
@@ -78,13 +79,25 @@ class IntPack:
             self.parts.append(np.zeros((-a.size) % 4, np.int32))
 
     def upload(self, ws: Workspace, key: str):
+        """One async H2D copy through a persistent pinned staging buffer of the workspace (no
+        per-call pinned allocation); the staging buffer is reused once its last copy completed."""
         torch = _torch()
         host = getattr(self, "host", None)
         if host is None:
             host = np.concatenate(self.parts) if self.parts else np.zeros(4, np.int32)
-        dev = ws.get(key, (max(4, host.size),), torch.int32, zero=False)
-        pinned = torch.from_numpy(host).pin_memory()
-        dev[:host.size].copy_(pinned, non_blocking=True)
+        n = max(4, host.size)
+        dev = ws.get(key, (n,), torch.int32, zero=False)
+        pin, ev = ws.pinned.get(key, (None, None))
+        if pin is None or pin.numel() < n:
+            pin = torch.empty(max(n, 1 << 16), dtype=torch.int32, pin_memory=True)
+            ev = None
+        elif ev is not None:
+            ev.synchronize()              # the previous copy out of this staging buffer is done
+        pin.numpy()[:host.size] = host
+        dev[:host.size].copy_(pin[:host.size], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        ws.pinned[key] = (pin, ev)
         self.dev = dev
         return self
 
