@@ -425,6 +425,53 @@ def reuse_prefill(cfg: Cfg, w, ids, segs, hashes, ratios, enc_store, kv_store,
 # --------------------------------------------------------------------------
 # work accounting (engine.py:39-85)
 
+# --------------------------------------------------------------------------
+# decode over merged KV (engine.py:204-232, model.py:392-464)
+
+def decode(cfg: Cfg, w, keys, values, tail_ids=(), max_new=0, initial_logits=None):
+    """Greedy decode attending over merged pre-RoPE KV [L, n0, kv]: keys rotated at their request
+    positions once (model.py:403-411), each step appends one token at the next position
+    (model.py:413-439); tail tokens teacher-forced first, then greedy (engine.py:204-232,
+    model.py:442-456).  Returns (ids, step_logits, tail_logits)."""
+    L, n0 = keys.shape[0], keys.shape[1]
+    cap = n0 + len(tail_ids) + max_new
+    hd, base = cfg.head_dim, cfg.rope_base
+    k_rot = np.zeros((L, cap, cfg.kv_dim), F32)
+    v = np.zeros_like(k_rot)
+    for i in range(L):
+        k_rot[i, :n0] = rope(keys[i], np.arange(n0), hd, base)
+        v[i, :n0] = values[i]
+    state = {"n": n0}
+
+    def step(tok):
+        pos = state["n"]
+        x = w["embed"][tok].astype(F32).copy()
+        for i in range(L):
+            an, wq, wk, wv, wo, mn, wg, wu, wd = _layer_w(w, i)
+            xn = rmsnorm(x, an)
+            k_rot[i, pos] = rope((xn @ wk)[None], [pos], hd, base)[0]
+            v[i, pos] = xn @ wv
+            q = rope((xn @ wq)[None], [pos], hd, base)
+            a = attend(q, k_rot[i, :pos + 1], v[i, :pos + 1], np.ones((1, pos + 1), dtype=bool), cfg.num_heads)[0]
+            x = x + a @ wo
+            x = x + mlp(rmsnorm(x, mn), wg, wu, wd)
+        state["n"] += 1
+        return (rmsnorm(x, w["final_norm"]) @ w["head"]).astype(F32)
+
+    tail_logits = np.empty((len(tail_ids), cfg.vocab_size), F32)
+    cur = initial_logits
+    for j, tok in enumerate(tail_ids):
+        cur = step(int(tok))
+        tail_logits[j] = cur
+    ids, step_logits = [], np.empty((max_new, cfg.vocab_size), F32)
+    for t in range(max_new):
+        step_logits[t] = cur
+        tok = int(np.argmax(cur))
+        ids.append(tok)
+        cur = step(tok)
+    return ids, step_logits, tail_logits
+
+
 def flops(cfg: Cfg, counts, n, encoded_images=0):
     d, kv, h, T = cfg.model_dim, cfg.kv_dim, cfg.hidden, cfg.tokens_per_image
 

@@ -6,7 +6,8 @@ allocator and `prefill_with_reuse`.  Compute runs in libvlcache.so (hand-written
 tcgen05 / TMA kernels) through a C ABI; there is no CPU fallback.
 """
 from .config import ModelConfig
-from .engine import (FlopsBreakdown, ReuseMetrics, ReuseRequest, ReuseResult, count_flops, encode_image,
+from .engine import (DecodeResult, FlopsBreakdown, ReuseMetrics, ReuseRequest, ReuseResult, count_flops,
+                     decode_with_merged_kv, encode_image,
                      fill_store, fill_store_request, flops_from_masks, prefill_batch_with_reuse, prefill_full,
                      prefill_with_reuse)
 from .exceptions import (ConfigError, InputError, IntegrityError, KVReuseError, ParseError, PlanError,

@@ -422,6 +422,58 @@ def _prefill_embeds(model: ToyVLM, seq: TokenSequence, image_embeds) -> ReuseRes
     return res
 
 
+# ---------------------------------------------------------------- decode over merged KV (engine.py:195-232)
+
+@dataclass
+class DecodeResult:
+    ids: list
+    step_logits: np.ndarray   # distribution each generated id was taken from
+    tail_logits: np.ndarray   # logits after each teacher-forced tail token
+
+
+def decode_with_merged_kv(model: ToyVLM, merged_kv: KVTensors, tail_ids=(), max_new: int = 0,
+                          initial_logits=None) -> DecodeResult:
+    """Greedy decode attending over merged KV (reference engine.py:204-232): tail tokens are
+    teacher-forced first, then generation continues from the last tail logits or from
+    `initial_logits` (e.g. the reuse prefill's last row).  Every step runs on the device
+    (runtime.DeviceDecoder); ids are chosen on the host (argmax of the returned row)."""
+    import torch
+    if max_new < 0:
+        raise InputError("max_new must be >= 0")
+    cfg = model.config
+    V = cfg.vocab_size
+    tail_logits = np.empty((len(tail_ids), V), dtype=np.float32)
+    if not len(tail_ids) and max_new == 0:
+        return DecodeResult([], np.empty((0, V), np.float32), tail_logits)
+    if max_new > 0 and not len(tail_ids) and initial_logits is None:
+        raise InputError("decoding needs a starting distribution: supply tail tokens or "
+                         "initial_logits from the prefill")
+    runner = _runner(model)
+    if merged_kv._loader is not None or merged_kv._dev is not None:
+        keys, values = merged_kv.device_keys(), merged_kv.device_values()
+    else:
+        keys = torch.from_numpy(np.ascontiguousarray(merged_kv.keys, np.float32)).cuda().to(torch.bfloat16)
+        values = torch.from_numpy(np.ascontiguousarray(merged_kv.values, np.float32)).cuda().to(torch.bfloat16)
+    state = runner.decoder(keys, values, capacity=len(tail_ids) + max_new)
+
+    def step(tok):
+        if not 0 <= tok < V:
+            raise InputError(f"token id {tok} out of vocab")
+        return state.step(tok)[0].cpu().numpy()
+
+    cur = None if initial_logits is None else np.asarray(initial_logits, dtype=np.float32)
+    for j, tok in enumerate(tail_ids):
+        cur = step(int(tok))
+        tail_logits[j] = cur
+    ids, step_logits = [], np.empty((max_new, V), dtype=np.float32)
+    for t in range(max_new):
+        step_logits[t] = cur
+        tok = int(np.argmax(cur))
+        ids.append(tok)
+        cur = step(tok)
+    return DecodeResult(ids, step_logits, tail_logits)
+
+
 # ---------------------------------------------------------------- cache-miss fill (bench.py:82-104)
 
 def fill_store_request(model: ToyVLM, store: CacheStore, seq: TokenSequence, images) -> list:

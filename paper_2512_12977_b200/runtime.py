@@ -272,6 +272,11 @@ class Runner:
         self.rmsnorm(xe, E["out_norm"], out, M, out_f32=True)
         return out[:M]
 
+    # ---------------------------------------------------------------- token-by-token decode
+    def decoder(self, keys, values, capacity: int) -> "DeviceDecoder":
+        """Decode state over merged pre-RoPE KV (device bf16 [L, n0, kv]), model.py:392-411."""
+        return DeviceDecoder(self, keys, values, capacity)
+
     # ---------------------------------------------------------------- decoder
     def _pick_set(self) -> Workspace:
         """The output set for this call: one no live result points into (preferring the set not
@@ -495,3 +500,88 @@ class Runner:
         self.rmsnorm(x, dw.final_norm, xn, cL, row_map=pack.ptr("final"), pk=(N.row_tile(cL), dw.kd // 128))
         self.gemm(dw.head, dw.kd, xn, cL, _epi(kind=N.EPI_F32, n_valid=V, out=logits.data_ptr(), ldo=V),
                   name="gemm_head", k_valid=d)
+
+
+class DeviceDecoder:
+    """Growable request KV on the device for greedy decoding (reference DecoderState,
+    model.py:392-439): keys held ROTATED at their positions, values as is; each step runs the
+    layer chain for one token at the next position through the same kernels as the prefill
+    (QKV GEMM with RoPE + KV-append epilogue, attention over all previous keys, O / MLP / head)."""
+
+    def __init__(self, runner: Runner, keys, values, capacity: int):
+        torch = _torch()
+        if runner.tp_group is not None:
+            raise NotImplementedError("decode under head-parallel attention is not supported")
+        self.r, cfg, dw = runner, runner.cfg, runner.dw
+        L, n0, kv = keys.shape
+        self.n, self.cap = int(n0), int(n0 + capacity)
+        d = cfg.model_dim
+        dw.ensure_positions(self.cap + 1)
+        self.kc = torch.zeros(L, self.cap, kv, dtype=torch.bfloat16, device="cuda")
+        self.vc = torch.zeros_like(self.kc)
+        R = N.row_tile(1)
+        self.x = torch.zeros(R, d, dtype=torch.float32, device="cuda")
+        self.xn = torch.zeros(N.packed_numel(R, d, R), dtype=torch.bfloat16, device="cuda")
+        self.q = torch.zeros(R + 256, kv, dtype=torch.bfloat16, device="cuda")
+        self.att = torch.zeros(N.packed_numel(R, dw.kkv, R), dtype=torch.bfloat16, device="cuda")
+        self.h = torch.zeros(N.packed_numel(R, dw.kh, R), dtype=torch.bfloat16, device="cuda")
+        self.logits = torch.zeros(1, cfg.vocab_size, dtype=torch.float32, device="cuda")
+        if n0:
+            # rotate every cached key to its position: kv_relocate with the merged KV as a pool of
+            # one-token pages (page table = row index), destination rows = positions
+            kf = keys.reshape(L * n0, kv).contiguous()
+            vf = values.reshape(L * n0, kv).contiguous()
+            pt = torch.arange(L * n0, dtype=torch.int32, device="cuda")
+            descs = np.array([[i, i * n0, 0, n0, 0, 0, 0, 0] for i in range(L)], dtype=np.int32)
+            blocks = np.array([[i, t] for i in range(L) for t in range(0, n0, 8)], dtype=np.int32)
+            dd = torch.from_numpy(descs).cuda()
+            bb = torch.from_numpy(blocks).cuda()
+            N.call("vlc_kv_relocate", kf.data_ptr(), vf.data_ptr(), 1, pt.data_ptr(), kv, cfg.head_dim,
+                   self.kc.data_ptr(), self.vc.data_ptr(), self.cap, dd.data_ptr(), bb.data_ptr(), len(blocks),
+                   dw.cos.data_ptr(), dw.sin.data_ptr(), cfg.head_dim // 2, _stream())
+            _torch().cuda.current_stream().synchronize()
+
+    def step(self, token: int):
+        """Append `token` at the next position; device logits row [1, V] (model.py:413-439)."""
+        torch = _torch()
+        r, cfg, dw = self.r, self.r.cfg, self.r.dw
+        if self.n >= self.cap:
+            raise RuntimeError("decode capacity exhausted")
+        L, d, kv, V = cfg.num_layers, cfg.model_dim, dw.kv, cfg.vocab_size
+        pos = self.n
+        R = N.row_tile(1)
+        it9, groups = attention_work_pp([(0, 0, 1)], np.array([pos], np.int32), np.array([pos + 1]), dw.heads)
+        items = np.ascontiguousarray(it9[:, :8])
+        pack = IntPack()
+        pack.add("src", np.array([[0, token]]))
+        pack.add("pos", np.array([pos]))
+        pack.add("zero", np.array([0]))
+        pack.add("items", items)
+        pack.upload(r.shared, "dec_ints")
+        s = _stream()
+        r._run("embed", lambda: N.check(r.lib.vlc_embed_assemble(
+            self.x.data_ptr(), d, dw.embed.data_ptr(), d, 0, 0, pack.ptr("src"), 1, s), "vlc_embed_assemble"))
+        for i in range(L):
+            W = dw.layers[i]
+            r.rmsnorm(self.x, W["attn_norm"], self.xn, 1, pk=(R, dw.kd // 128))
+            r.gemm(W["wqkv"], dw.kd, self.xn, 1, _epi(
+                kind=N.EPI_QKV_ROPE, n_valid=3 * kv, out=self.q.data_ptr(), ldo=kv,
+                out2=self.kc[i].data_ptr(), ld2=kv, out3=self.vc[i].data_ptr(), ld3=kv,
+                map1=pack.ptr("zero"), map2=pack.ptr("pos"), pos=pack.ptr("pos"),
+                cos_tab=dw.cos.data_ptr(), sin_tab=dw.sin.data_ptr(), tab_ld=cfg.head_dim // 2,
+                hd=cfg.head_dim, seg=kv), name="gemm_qkv", k_valid=d)
+            r.attention(self.q, self.kc, self.vc, i, pack.ptr("items"), len(items), pack.ptr("zero"), 0,
+                        pack.ptr("pos"), pack.ptr("zero"), self.att, groups, pk=(R, dw.kkv // 128))
+            r.gemm(W["wo"], dw.kkv, self.att, 1, _epi(kind=N.EPI_RESID, n_valid=d, out=self.x.data_ptr(), ldo=d),
+                   name="gemm_o", k_valid=kv)
+            r.rmsnorm(self.x, W["mlp_norm"], self.xn, 1, pk=(R, dw.kd // 128))
+            r.gemm(W["wgu"], dw.kd, self.xn, 1,
+                   _epi(kind=N.EPI_SWIGLU, n_valid=2 * cfg.mlp_hidden, out=self.h.data_ptr(), ldo=dw.kh,
+                        pk_rows=R, pk_kb=dw.kh // 128), name="gemm_gate_up", k_valid=d)
+            r.gemm(W["wd"], dw.kh, self.h, 1, _epi(kind=N.EPI_RESID, n_valid=d, out=self.x.data_ptr(), ldo=d),
+                   name="gemm_down", k_valid=cfg.mlp_hidden)
+        r.rmsnorm(self.x, dw.final_norm, self.xn, 1, pk=(R, dw.kd // 128))
+        r.gemm(dw.head, dw.kd, self.xn, 1, _epi(kind=N.EPI_F32, n_valid=V, out=self.logits.data_ptr(), ldo=V),
+               name="gemm_head", k_valid=d)
+        self.n += 1
+        return self.logits

@@ -123,3 +123,30 @@ def test_masks_and_planner_match_reference():
                 assert O.brute(g[t + "_scores"], grid, base, p) == tuple(g[t + "_brute"])
     grid = tuple(float(x) for x in g["c2_grid"])
     assert O.greedy(g["c2_table"], grid, 1.0, 0.03 * 28) == tuple(g["c2_plan"])
+
+
+def test_decode_pins(small):
+    """Oracle decode (engine.py:204-232) against the reference: generate golden of the small scene
+    (full prefill + 8 greedy steps) and the pinned continuation after the mismatched-prefix r=0
+    reuse (test_engine.py:177-184)."""
+    g, w, enc, kv = small
+    ids, segs = O.layout(list(g["prefix"]), 1, 16, list(g["suffix"]))
+    logits, K, V = O.dense_prefill(SMALL, w, ids, segs, [g["emb"]])
+    got, step_logits, _ = O.decode(SMALL, w, K, V, max_new=8, initial_logits=logits[-1])
+    assert got == list(g["generate_ids"])
+    assert [int(np.argmax(r)) for r in step_logits] == got
+    got2, _, _ = O.decode(SMALL, w, g["r0_mis_keys"], g["r0_mis_values"], max_new=8,
+                          initial_logits=g["r0_mis_logits"][-1])
+    assert got2 == [92, 3, 88, 83, 83, 83, 83, 83]
+
+
+def test_decode_teacher_forced_tail_matches_prefill(small):
+    """Tail tokens teacher-forced over a shorter prefill reproduce the longer prefill's rows."""
+    g, w, _, _ = small
+    suffix = list(g["suffix"])
+    ids, segs = O.layout(list(g["prefix"]), 1, 16)
+    _, K, V = O.dense_prefill(SMALL, w, ids, segs, [g["emb"]])
+    _, _, tail = O.decode(SMALL, w, K, V, tail_ids=suffix)
+    ids_full, segs_full = O.layout(list(g["prefix"]), 1, 16, suffix)
+    full, _, _ = O.dense_prefill(SMALL, w, ids_full, segs_full, [g["emb"]])
+    assert rel_err(tail, full[-len(suffix):]) <= 1e-5
