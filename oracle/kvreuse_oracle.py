@@ -426,6 +426,88 @@ def reuse_prefill(cfg: Cfg, w, ids, segs, hashes, ratios, enc_store, kv_store,
 # work accounting (engine.py:39-85)
 
 # --------------------------------------------------------------------------
+# dense forward with injected KV and the sensitivity protocol (engine.py:239-292,
+# sensitivity.py:88-178)
+
+def forward_injected(cfg: Cfg, w, ids, segs, image_embeds, inject_k=None, inject_v=None, use_cached=None,
+                     capture_layers=()):
+    """Teacher-forced dense forward; at (layer, position) with use_cached, attention sees the
+    injected pre-RoPE K/V (rotated to the current position) instead of the fresh projections
+    (engine.py:239-283).  Returns (logits [n, V], {layer: attention block output [n, d]})."""
+    x = embed(cfg, w, ids, segs, image_embeds)
+    n = x.shape[0]
+    pos = np.arange(n)
+    L = cfg.num_layers
+    if use_cached is None:
+        use_cached = np.zeros((L, n), dtype=bool)
+    vis = np.tril(np.ones((n, n), dtype=bool))
+    hd, base = cfg.head_dim, cfg.rope_base
+    caps = {}
+    for i in range(L):
+        an, wq, wk, wv, wo, mn, wg, wu, wd = _layer_w(w, i)
+        xn = rmsnorm(x, an)
+        q, k, v = xn @ wq, xn @ wk, xn @ wv
+        if use_cached[i].any():
+            sel = use_cached[i][:, None]
+            k = np.where(sel, inject_k[i], k)
+            v = np.where(sel, inject_v[i], v)
+        a = attend(rope(q, pos, hd, base), rope(k, pos, hd, base), v, vis, cfg.num_heads) @ wo
+        if i in capture_layers or (i - L) in capture_layers:
+            caps[i] = a
+        x = x + a
+        x = x + mlp(rmsnorm(x, mn), wg, wu, wd)
+    return (rmsnorm(x, w["final_norm"]) @ w["head"]).astype(F32), caps
+
+
+def neutral_prompt(V, length):
+    """toydata.py:36-38 (fixed seed 0xD00D)."""
+    return prompt(V, length, 0xD00D)
+
+
+def profile(cfg: Cfg, w, samples, grid, max_new=8):
+    """sensitivity.py:88-178: per sample, the image's KV under the neutral prompt, the greedy
+    baseline under the original prompt, then teacher-forced logits with the neutral KV injected at
+    every layer except the first floor(r*T) image tokens of the probed layer; mean logit MSE per
+    (layer, ratio).  samples: [(image, original_prompt, neutral_prompt)].
+    Returns (scores [L, |grid|] f64, baseline f64)."""
+    grid = tuple(sorted(float(g) for g in grid))
+    L, T = cfg.num_layers, cfg.tokens_per_image
+    totals = np.zeros((L, len(grid)), np.float64)
+    base_total = 0.0
+    for img, orig, neutral in samples:
+        emb = encode(cfg, w, img)
+        ids_n, segs_n = layout(list(neutral), 1, T)
+        _, Kn, Vn = dense_prefill(cfg, w, ids_n, segs_n, [emb])          # build_mismatched_kv
+        s0 = image_spans(segs_n)[0][0]
+        mk, mv = Kn[:, s0:s0 + T], Vn[:, s0:s0 + T]
+        ids_o, segs_o = layout(list(orig), 1, T)                       # baseline_decode
+        lo, Ko, Vo = dense_prefill(cfg, w, ids_o, segs_o, [emb])
+        gen, z_orig, _ = decode(cfg, w, Ko, Vo, max_new=max_new, initial_logits=lo[-1])
+
+        def reuse(layer, r):                                           # reuse_logits
+            ids, segs = layout(list(orig), 1, T, gen)
+            n = len(ids)
+            start = image_spans(segs)[0][0]
+            ik = np.zeros((L, n, cfg.kv_dim), F32)
+            iv = np.zeros_like(ik)
+            ik[:, start:start + T], iv[:, start:start + T] = mk, mv
+            uc = np.zeros((L, n), dtype=bool)
+            uc[:, start:start + T] = True
+            uc[layer, start:start + keep_count(r, T)] = False
+            lg, _ = forward_injected(cfg, w, ids, segs, [emb], ik, iv, uc)
+            first = start + T - 1
+            return lg[first:first + len(gen)]
+
+        def mse(a, b):
+            return float(np.mean(np.square(np.asarray(a, np.float64) - np.asarray(b, np.float64))))
+        base_total += mse(z_orig, reuse(0, 0.0))
+        for i in range(L):
+            for j, r in enumerate(grid):
+                totals[i, j] += mse(z_orig, reuse(i, r))
+    return totals / len(samples), base_total / len(samples)
+
+
+# --------------------------------------------------------------------------
 # decode over merged KV (engine.py:204-232, model.py:392-464)
 
 def decode(cfg: Cfg, w, keys, values, tail_ids=(), max_new=0, initial_logits=None):

@@ -7,7 +7,7 @@ tcgen05 / TMA kernels) through a C ABI; there is no CPU fallback.
 """
 from .config import ModelConfig
 from .engine import (DecodeResult, FlopsBreakdown, ReuseMetrics, ReuseRequest, ReuseResult, count_flops,
-                     decode_with_merged_kv, encode_image,
+                     decode_with_merged_kv, encode_image, forward_injected, plan_to_use_cached,
                      fill_store, fill_store_request, flops_from_masks, prefill_batch_with_reuse, prefill_full,
                      prefill_with_reuse)
 from .exceptions import (ConfigError, InputError, IntegrityError, KVReuseError, ParseError, PlanError,

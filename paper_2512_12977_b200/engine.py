@@ -379,10 +379,13 @@ def _merged_kv_loader(out, lay, spec: RequestSpec, kv_pool, cfg: ModelConfig, re
 def prefill_full(model: ToyVLM, seq: TokenSequence, image_embeds) -> tuple[np.ndarray, KVTensors]:
     """Dense causal prefill (model.py:362-389) on device: plan = 1.0 through the same kernels."""
     res = _prefill_embeds(model, seq, image_embeds)
-    return res.logits, res.kv
+    # the result object is dropped here: give the returned KV its own device copy so that it stays
+    # valid when the runner's output buffers are reused
+    k, v = (t.clone() for t in res.kv._device())
+    return res.logits, KVTensors(loader=lambda: (k, v))
 
 
-def _prefill_embeds(model: ToyVLM, seq: TokenSequence, image_embeds) -> ReuseResult:
+def _prefill_embeds(model: ToyVLM, seq: TokenSequence, image_embeds, inject=None, capture=()) -> ReuseResult:
     """Full prefill with explicit image embeddings (host numpy or device rows)."""
     import torch
     cfg = model.config
@@ -412,14 +415,66 @@ def _prefill_embeds(model: ToyVLM, seq: TokenSequence, image_embeds) -> ReuseRes
     metrics = ReuseMetrics(mean_ratio=1.0)
     metrics.computed_per_layer = [len(seq)] * L
     ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-    out = runner.prefill(lay, text_ids, None, scratch, None, events=ev)
+    out = runner.prefill(lay, text_ids, None, scratch, None, events=ev, inject=inject, capture=capture)
     metrics._events = ev
     start, cnt = lay.logit_ranges[0]
     res = ReuseResult(lay.positions[0], out["logits"][start:start + cnt],
                       KVTensors(loader=_merged_kv_loader(out, lay, spec, None, cfg)), metrics)
     res._scratch = scratch
+    res._capture = out["capture"]
     runner.ws.live.add(res)
     return res
+
+
+# ---------------------------------------------------------------- dense forward with injected KV (engine.py:239-292)
+
+def forward_injected(model: ToyVLM, seq: TokenSequence, image_embeds, inject_keys=None, inject_values=None,
+                     use_cached=None, capture_layers=()):
+    """Teacher-forced dense forward with per-layer KV substitution (reference engine.py:239-283): at
+    (layer i, position p) with use_cached[i, p], attention sees inject_keys/values[i, p] (pre-RoPE,
+    rotated to p on the device) instead of the fresh projections; hidden states are still computed
+    everywhere.  Returns (logits [n, V] numpy, {layer: attention block output [n, d]})."""
+    import torch
+    cfg = model.config
+    L, n, kvd = cfg.num_layers, len(seq), cfg.kv_dim
+    if use_cached is None:
+        use_cached = np.zeros((L, n), dtype=bool)
+    use_cached = np.asarray(use_cached, dtype=bool)
+    if use_cached.shape != (L, n):
+        raise InputError(f"use_cached must be [{L}, {n}]")
+    if use_cached.any() and (inject_keys is None or inject_values is None):
+        raise InputError("use_cached set but no injected KV supplied")
+    caps = sorted({int(c) % L for c in capture_layers})
+    runner = _runner(model)
+    if runner.tp_group is not None:
+        raise NotImplementedError("forward_injected under head-parallel attention is not supported")
+    inject = None
+    if use_cached.any():
+        def dev(a):
+            t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a, np.float32))
+            return t.to(device="cuda", dtype=torch.bfloat16).reshape(L * n, kvd).contiguous()
+        descs, blocks, layer_blocks = [], [], [0]
+        for i in range(L):
+            row = use_cached[i]
+            edges = np.flatnonzero(np.diff(np.concatenate([[0], row.astype(np.int8), [0]])))
+            for s0, s1 in zip(edges[0::2], edges[1::2]):        # runs of injected positions
+                for off in range(0, int(s1 - s0), 8):
+                    blocks.append([len(descs), off])
+                descs.append([i, i * n + int(s0), 0, int(s1 - s0), int(s0), int(s0), 0, 0])
+            layer_blocks.append(len(blocks))
+        inject = dict(k=dev(inject_keys), v=dev(inject_values), descs=np.array(descs, np.int32),
+                      blocks=np.array(blocks, np.int32), layer_blocks=np.array(layer_blocks))
+    res = _prefill_embeds(model, seq, image_embeds, inject=inject, capture=caps)
+    captured = {i: res._capture[i][:n].cpu().numpy() for i in caps}
+    return res.logits, captured
+
+
+def plan_to_use_cached(plan: RecomputePlan, seq: TokenSequence) -> np.ndarray:
+    """The injected-path mask equivalent to a plan: stale wherever the skip path reuses cached KV
+    (engine.py:286-292)."""
+    use_cached = ~build_masks(plan, seq).layers
+    use_cached[:, ~seq.image_mask()] = False
+    return use_cached
 
 
 # ---------------------------------------------------------------- decode over merged KV (engine.py:195-232)

@@ -292,7 +292,7 @@ class Runner:
         return self.ws
 
     def prefill(self, lay: Layout, text_src: np.ndarray, enc_store_rows, enc_scratch_rows, kv_pool, events=None,
-                use_graph: bool = True):
+                use_graph: bool = True, inject=None, capture=()):
         """Run embed -> kv_relocate -> L layers -> final norm -> head for a built Layout.
 
         The launch chain depends only on the layout STRUCTURE (row counts, work lists) and
@@ -329,6 +329,18 @@ class Runner:
                 pack.dev.data_ptr(), dw.cos.data_ptr(), self.splitk.data_ptr(),
                 self.shared.bufs["attn_ws_o"].data_ptr(), self.shared.bufs["attn_ws_ml"].data_ptr()) + tuple(
                     t.data_ptr() for t in buf.values())
+        if inject is not None or capture:
+            # measurement path (forward_injected): per-layer KV substitution after the QKV GEMM and
+            # captured attention-block outputs; eager launches
+            use_graph = False
+            buf["capture"] = {i: torch.zeros(max(c0, 1), d, dtype=torch.float32, device="cuda") for i in capture}
+            if inject is not None:
+                ipk = IntPack()
+                ipk.add("descs", inject["descs"])
+                ipk.add("blocks", inject["blocks"])
+                ipk.add("pages", np.arange(inject["k"].shape[0], dtype=np.int32))
+                ipk.upload(self.shared, "inj_ints")
+                buf["inject"] = (inject, ipk)
         chain = lambda: self._chain(lay, pack, buf, ptrs)  # noqa: E731
         if events is not None:
             events[0].record()
@@ -361,7 +373,8 @@ class Runner:
         if events is not None:
             events[1].record()
         return {"logits": buf["logits"], "kc": buf["kc"], "vc": buf["vc"], "kpre": buf["kpre"],
-                "R": buf["kpre"].shape[1], "KVR": buf["kc"].shape[1], "pack": pack}
+                "R": buf["kpre"].shape[1], "KVR": buf["kc"].shape[1], "pack": pack,
+                "capture": buf.get("capture", {})}
 
     @staticmethod
     def _pack(lay: Layout) -> "IntPack":
@@ -467,6 +480,15 @@ class Runner:
                 map1=pack.ptr(f"qdst{i}"), map2=pack.ptr("row_kv"), pos=pack.ptr("row_pos"),
                 cos_tab=dw.cos.data_ptr(), sin_tab=dw.sin.data_ptr(), tab_ld=cfg.head_dim // 2,
                 hd=cfg.head_dim, seg=kv), name="gemm_qkv", k_valid=d)
+            if "inject" in buf:
+                inj, ipk = buf["inject"]
+                lb = inj["layer_blocks"]
+                if lb[i + 1] > lb[i]:    # injected pre-RoPE K (rotated to the row positions) / V overwrite
+                    self._run("kv_inject", lambda i=i, lb=lb, inj=inj, ipk=ipk: N.check(self.lib.vlc_kv_relocate(
+                        inj["k"].data_ptr(), inj["v"].data_ptr(), 1, ipk.ptr("pages"), kv, cfg.head_dim,
+                        kc.data_ptr(), vc.data_ptr(), kc.shape[1], ipk.ptr("descs"),
+                        ipk.ptr("blocks") + 8 * int(lb[i]), int(lb[i + 1] - lb[i]), dw.cos.data_ptr(),
+                        dw.sin.data_ptr(), cfg.head_dim // 2, _stream()), "vlc_kv_relocate"))
             vis = int(lay.qpos[i, :ci].astype(np.int64).sum()) + ci
             if side_ev is not None:
                 _torch().cuda.current_stream().wait_event(side_ev[i])
@@ -474,7 +496,16 @@ class Runner:
                            len(lay.comb_items[i]), pack.ptr(f"qpos{i}"), pack.ptr(f"rowof{i}"), att, lay.attn_slots,
                            nbytes=lay.kv_rows * kv * 4 + ci * kv * 4, flops=4 * cfg.head_dim * dw.heads * vis,
                            pk=(Ri, dw.kkv // 128))
-            if self.tp_group is None:
+            if i in buf.get("capture", {}):
+                # captured attention block output (engine.py:273-275): O projection alone, then
+                # x += it fused with the MLP norm
+                cap = buf["capture"][i]
+                self.gemm(W["wo"], dw.kkv, att, ci, _epi(kind=N.EPI_F32, n_valid=d, out=cap.data_ptr(), ldo=d),
+                          name="gemm_o", k_valid=kv)
+                self._run("rmsnorm", lambda cap=cap, W=W: N.check(self.lib.vlc_add_rmsnorm(
+                    x.data_ptr(), d, cap.data_ptr(), d, W["mlp_norm"].data_ptr(), xn.data_ptr(), d, ci, d, RMS_EPS,
+                    Ri, dw.kd // 128, _stream()), "vlc_add_rmsnorm"))
+            elif self.tp_group is None:
                 self.gemm(W["wo"], dw.kkv, att, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d),
                           name="gemm_o", k_valid=kv)
                 self.rmsnorm(x, W["mlp_norm"], xn, ci, pk=(Ri, dw.kd // 128))

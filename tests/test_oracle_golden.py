@@ -150,3 +150,36 @@ def test_decode_teacher_forced_tail_matches_prefill(small):
     ids_full, segs_full = O.layout(list(g["prefix"]), 1, 16, suffix)
     full, _, _ = O.dense_prefill(SMALL, w, ids_full, segs_full, [g["emb"]])
     assert rel_err(tail, full[-len(suffix):]) <= 1e-5
+
+
+def test_forward_injected_matches_reuse_golden(small):
+    """engine.py:239-283 restated: the dense injected path with the plan's stale mask reproduces the
+    reference's skip-path logits at the computed rows (test_engine.py:65-80)."""
+    g, w, enc, kv = small
+    ids, segs = O.layout(O.prompt(97, 6, 99), 1, 16, list(g["suffix"]))
+    n = len(ids)
+    h = O.sha256_hex(g["img"])
+    ik = np.zeros((4, n, 32), np.float32)
+    iv = np.zeros_like(ik)
+    start = O.image_spans(segs)[0][0]
+    ik[:, start:start + 16], iv[:, start:start + 16] = kv[h].keys, kv[h].values
+    uc = ~O.compute_masks((0.3, 0.2, 0.1, 0.0), n, segs)
+    uc[:, :start] = False
+    uc[:, start + 16:] = False
+    logits, caps = O.forward_injected(SMALL, w, ids, segs, [g["emb"]], ik, iv, uc, capture_layers=(1, -1))
+    rows = g["mixed_mis_rows"]
+    assert rel_err(logits[rows], g["mixed_mis_logits"]) <= 1e-5
+    assert sorted(caps) == [1, 3] and caps[1].shape == (n, 32)
+
+
+def test_profile_fixture_pinned():
+    """sensitivity.py:156-178 restated; the reference's regression pin (test_sensitivity.py:127-139)."""
+    w = O.make_weights(SMALL)
+    samples = [(O.image(16, 400 + k), O.prompt(97, 10, 500 + k), O.neutral_prompt(97, 10)) for k in range(5)]
+    scores, base = O.profile(SMALL, w, samples, (0.1, 0.2, 0.3), max_new=6)
+    assert base == pytest.approx(0.05434575974372617, rel=1e-6)
+    expected = [[0.05434575974372617, 0.05434575974372617, 0.05434575974372617],
+                [0.053952849361164124, 0.05491019159272694, 0.05474442593760177],
+                [0.05204071848618812, 0.04659527542216396, 0.04360329238478551],
+                [0.051986565840154916, 0.04302598720114376, 0.04084225128826289]]
+    assert np.allclose(scores, expected, rtol=1e-6)
