@@ -115,6 +115,7 @@ int vlc_set_tuning(int key, int value) {
   if (key == 7) { vlc::g_wide = value; return VLC_OK; }
   if (key == 9) { vlc::g_unsplit_min = value; return VLC_OK; }
   if (key == 10) { vlc::g_pair = value; return VLC_OK; }
+  if (key == 13) { vlc::g_deterministic = value != 0; return VLC_OK; }
   if (key == 12) { vlc::g_attn_kt = value == 64 ? 64 : 128; return VLC_OK; }
   return fail(VLC_ERR_INVALID, "set_tuning: unknown key");
 }

@@ -34,6 +34,7 @@ struct SkSched {
   int G;         // CTAs (all co-resident: cooperative launch)
   int KB;        // k-blocks per tile
   int m_tiles;
+  int red;       // RESID split partials reduced with red.add (1) or through the ordered fix-up (0)
   __device__ __forceinline__ long long u0(int g) const { return U * g / G; }
   __device__ __forceinline__ int cta_of(long long u) const {
     int g = (int)((u * G) / U);
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (leader) DBG(3);
       const uint32_t d = tmem + slot * 256 + (H == 2 ? eg * 256 : 0) + lane_off;
       const int hoff = H == 2 ? eg * 128 : 0;                 // weight-row offset of this group
-      const bool split = gf != gl && KIND != EPI_RESID;   // RESID partials reduce in L2 (red.add)
+      const bool split = gf != gl && !(KIND == EPI_RESID && sk.red);   // RESID partials: red.add in L2
       float* part = split ? ws + (2L * g + (t == t_first ? 0 : 1)) * (long)n_tile * BM : nullptr;
       const int nch = (n_tile + 31) / 32;
       for (int ci = (H == 1 ? eg : 0); ci < nch; ci += (H == 1 ? 2 : 1)) {
@@ -262,7 +263,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int t = t_first; t <= t_last; ++t) {
       const long long tb = (long long)t * sk.KB;
       const int gf = sk.cta_of(tb), gl = sk.cta_of(tb + sk.KB - 1);
-      if (gf == gl || KIND == EPI_RESID) continue;
+      if (gf == gl || (KIND == EPI_RESID && sk.red)) continue;
       const int nseg = gl - gf + 1, p = g - gf;
       if (leader) {
         volatile int* cnt = counters + 2 * gf;
@@ -319,6 +320,7 @@ void set_debug_buffer(unsigned long long* p) { cudaMemcpyToSymbol(g_dbg, &p, siz
 int g_coop = 1;
 int g_pdl = 1;
 
+int g_deterministic = 0;  // tuning key 13: 1 = RESID split-K partials through the ordered fix-up
 int g_pair = 96;          // tuning key 10: CTA-pair GEMM for non-RESID kinds when n_tile >= this (0 = off)
 int g_unsplit_min = 64;   // tuning key 9: tile count from which each tile gets its own CTA (no split-K)
 int g_wide = 1;   // tuning key 7: 0 auto, 1 never use 256-row tiles (default: measured slower), 2 always
@@ -387,17 +389,18 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   if (max_ctas == 0 && tiles >= g_unsplit_min && tiles <= G) G = (int)tiles;
   // split tiles reduce through the workspace with <= 8 participants, except RESID (red.add into
   // the residual, any number of participants; >= 2 k-blocks per CTA)
-  const int min_units = epi.kind == EPI_RESID ? 2 : (KB + 5) / 6;
+  const bool red = epi.kind == EPI_RESID && !g_deterministic;
+  const int min_units = red ? 2 : (KB + 5) / 6;
   if ((long long)G * min_units > U) G = (int)(U / min_units);
   if (G < 1) G = 1;
   const size_t need = (size_t)G * 2 * BM * n_tile * sizeof(float);
-  if (epi.kind != EPI_RESID && (need > ws_bytes || counters == nullptr)) {
+  if (!red && (need > ws_bytes || counters == nullptr)) {
     if (U / KB <= num_sms()) G = (int)(U / KB);   // no workspace: one CTA per tile, never split
     else return cudaErrorInvalidValue;
   }
   const int stages = gemm_pick_stages(n_tile, H);
   const int smem = gemm_smem_bytes(n_tile, stages, H);
-  SkSched sk{U, G, KB, m_tiles};
+  SkSched sk{U, G, KB, m_tiles, red ? 1 : 0};
   const uint8_t* wpp = reinterpret_cast<const uint8_t*>(W);
   const uint8_t* xpp = reinterpret_cast<const uint8_t*>(X);
 #define VLC_GEMM_KIND(K)                                                                              \

@@ -25,6 +25,7 @@ extern int g_stage_override;  // experiment knob (vlc_set_tuning key 1)
 extern int g_attn_kt;         // key 12: key tile of the hd-128 attention kernel (64 / 128)
 extern int g_attn_min_smem;   // key 5: lower bound on the attention kernel's dynamic smem
 extern int g_coop;            // key 2: cooperative launch of the stream-K GEMM
+extern int g_deterministic;   // key 13: bitwise run-to-run reproducible RESID GEMMs (slower)
 extern int g_pair;            // key 10: CTA-pair GEMM threshold on the token tile (0 = off)
 extern int g_unsplit_min;     // key 9: tiles >= this (and <= #SMs) -> one CTA per tile
 extern int g_wide;            // key 7: 256-row GEMM tiles (0 auto, 1 never, 2 always)

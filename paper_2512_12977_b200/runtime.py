@@ -127,6 +127,9 @@ class Runner:
         self.shared = Workspace()    # per-call scratch (split-K partials, counters, attention merge)
         self.enc_ws = Workspace()
         self.lib = N.load()
+        # VLC_DETERMINISTIC=1: split-K partials of the residual GEMMs reduced in a fixed order
+        # (bitwise reproducible runs) instead of red.add in arrival order (faster)
+        self.lib.vlc_set_tuning(13, int(__import__("os").environ.get("VLC_DETERMINISTIC", "0")))
         torch = _torch()
         self.splitk = self.shared.get("splitk", (64 << 20,), torch.float32, zero=False)
         self.counters = self.shared.get("counters", (1 << 16,), torch.int32)

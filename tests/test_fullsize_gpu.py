@@ -117,3 +117,23 @@ def test_c3_page_placement_invariance(c3):
     run_to_run = rel_err(a2, a)
     assert rel_err(b, a) <= 2e-2 and run_to_run <= 2e-2, (rel_err(b, a), run_to_run)
     assert int(np.argmax(a[-1])) == int(np.argmax(b[-1]))
+
+
+@pytest.mark.timeout(900)
+def test_c3_deterministic_mode_is_bitwise_reproducible(c3):
+    """vlc_set_tuning(13, 1) (env VLC_DETERMINISTIC=1): residual split-K partials reduced in a fixed
+    order -> two runs (and two page placements) give identical logits."""
+    from paper_2512_12977_b200 import _native as N
+    P, cfg, model, imgs, store = c3
+    req = _req(P, cfg, imgs, 12, 0.05)
+    lib = N.load()
+    lib.vlc_set_tuning(13, 1)
+    try:
+        model._runner.graphs.clear()          # re-capture with the deterministic kernels
+        a = P.prefill_with_reuse(model, req, store).logits
+        b = P.prefill_with_reuse(model, req, store).logits
+        c = P.prefill_with_reuse(model, req, store).logits
+    finally:
+        lib.vlc_set_tuning(13, 0)
+        model._runner.graphs.clear()
+    assert np.array_equal(a, b) and np.array_equal(b, c)
