@@ -508,13 +508,23 @@ def layer_aware_vs_uniform(P, model, seq, hashes, store, L, timed):
     GPU.  The sensitivity table is synthetic and pinned (the reference's CPU profiling costs
     L*|grid|+1 dense passes per sample at this size): layer i's score decays with the ratio as
     w_i * exp(-r / 0.04), w_i = 1 / (1 + i / 4) -- shallow layers more sensitive (sec. 3)."""
-    grid = tuple(round(0.002 * k, 3) for k in range(1, 151))
-    w = 1.0 / (1.0 + np.arange(L) / 4.0)
-    scores = w[:, None] * np.exp(-np.asarray(grid)[None, :] / 0.04)
-    table = P.SensitivityTable(scores, grid, float(w.max()), 1, model.fingerprint)
+    source = "synthetic"
+    try:       # device-profiled table for this model (tools/profile_table.py), if committed
+        with open(os.path.join(ROOT, "profiles", "c3_sensitivity_table.json")) as fh:
+            prof = json.load(fh)
+        if int(prof["model_fingerprint"]) != model.fingerprint:
+            raise ValueError("table profiled for another model")
+        table = P.SensitivityTable(np.asarray(prof["scores"]), tuple(prof["grid"]), float(prof["baseline"]),
+                                   int(prof["samples"]), model.fingerprint)
+        source = f"device-profiled ({prof['samples']} proxy samples, profiles/c3_sensitivity_table.json)"
+    except (OSError, ValueError, KeyError):
+        grid = tuple(round(0.002 * k, 3) for k in range(1, 151))
+        w = 1.0 / (1.0 + np.arange(L) / 4.0)
+        scores = w[:, None] * np.exp(-np.asarray(grid)[None, :] / 0.04)
+        table = P.SensitivityTable(scores, grid, float(w.max()), 1, model.fingerprint)
     plans = {"uniform": P.plan_static(0.05, L), "layer_aware": P.plan_greedy(table, P.BudgetSpec(0.05 * L))}
     full = prefill_last(P, model, P.ReuseRequest(seq, hashes, P.plan_static(1.0, L)), store)
-    out = {}
+    out = {"table": source}
     for name, plan in plans.items():
         req = P.ReuseRequest(seq, hashes, plan)
         last = prefill_last(P, model, req, store)
