@@ -172,7 +172,9 @@ def cpu_cores() -> int:
 def run_reference(args, wl):
     cfg_kw = CONFIGS[wl["cfg"]]
     times = []
-    sample = CpuSample(cfg_kw, wl["images"], wl["ratio"])
+    # one sampled layer per step (the per-layer time x L extrapolation) keeps a default run of the
+    # arm within a few minutes on the host cores
+    sample = CpuSample(cfg_kw, wl["images"], wl["ratio"], sample_layers=1)
     for step in range(args.warmup + args.steps):
         ms, det = sample.run()
         if step >= args.warmup:
