@@ -101,6 +101,25 @@ class IntPack:
         self.dev = dev
         return self
 
+    def upload_segments(self, ws: Workspace, key: str, names):
+        """Refresh only the named segments of an already uploaded pack of the same layout
+        structure (per-call token ids / page ids); the structural arrays stay resident."""
+        torch = _torch()
+        pin, ev = ws.pinned[key]
+        if ev is not None:
+            ev.synchronize()
+        dev = ws.bufs[key]
+        pn = pin.numpy()
+        for name in names:
+            o, n = self.off[name]
+            pn[o:o + n] = self.host[o:o + n]
+            dev[o:o + n].copy_(pin[o:o + n], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        ws.pinned[key] = (pin, ev)
+        self.dev = dev
+        return self
+
     def ptr(self, name) -> int:
         o, _ = self.off[name]
         return int(self.dev.data_ptr()) + 4 * o
@@ -324,7 +343,14 @@ class Runner:
         self.shared.get("attn_ws_ml", (max(1, lay.attn_slots) * 8 * 256 * 2,), torch.float32, zero=False)
 
         pack = self._pack(lay)
-        pack.upload(ws, "ints")
+        skey = getattr(lay, "_skey", None)
+        if skey is None:
+            skey = lay._skey = lay.structure_key()
+        if getattr(ws, "ints_key", None) == skey:       # structure resident: only ids / pages change
+            pack.upload_segments(ws, "ints", ("src", "pages"))
+        else:
+            pack.upload(ws, "ints")
+            ws.ints_key = skey
         ptrs = (enc_store_rows.data_ptr() if enc_store_rows is not None else 0,
                 enc_scratch_rows.data_ptr() if enc_scratch_rows is not None else 0,
                 kv_pool.k.data_ptr() if kv_pool is not None else 0,
