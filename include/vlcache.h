@@ -155,6 +155,17 @@ int vlc_gemm_bf16(const void* w, int n_pad, int k_pad, const void* x, int x_rows
                   int m_tokens, const vlc_epilogue* epi, int max_ctas, float* ws, size_t ws_bytes,
                   int* counters, cudaStream_t stream);
 
+/* The QKV GEMM fused with the same layer's kv_relocate: CTAs beyond the GEMM's own (the SMs a
+ * one-tile-per-CTA projection leaves idle) gather + re-rotate + scatter the layer's cached K/V
+ * (arguments as vlc_gemm_bf16 followed by vlc_kv_relocate's); falls back to two launches when the
+ * GEMM occupies every SM.  Replaces engine.py:153-155 + 176-180 for one layer. */
+int vlc_gemm_bf16_relocate(const void* w, int n_pad, int k_pad, const void* x, int x_rows_cap, int m_tokens,
+                           const vlc_epilogue* epi, int max_ctas, float* ws, size_t ws_bytes, int* counters,
+                           const void* kpool, const void* vpool, int page_tokens, const int* page_table, int kv,
+                           int head_dim, void* kc, void* vc, int kv_rows_cap, const int* descs, const int* blocks,
+                           int n_blocks, const float* cos_tab, const float* sin_tab, int tab_ld,
+                           cudaStream_t stream);
+
 int vlc_attn_mixed(const vlc_attn_args* args, cudaStream_t stream);
 int vlc_attn_combine(const vlc_attn_args* args, cudaStream_t stream);
 int vlc_attn_pp(const vlc_attn_args* args, cudaStream_t stream);

@@ -17,7 +17,7 @@ VLC_OK, VLC_ERR_INVALID, VLC_ERR_UNSUPPORTED, VLC_ERR_CUDA = 0, 1, 2, 3
 EPI_F32, EPI_RESID, EPI_BF16, EPI_BIAS_ADD, EPI_SWIGLU, EPI_QKV_PLAIN, EPI_QKV_ROPE = range(7)
 
 EXPORTS = ("vlc_last_error", "vlc_version", "vlc_embed_assemble", "vlc_rmsnorm", "vlc_add_rmsnorm", "vlc_kv_relocate",
-           "vlc_store_write_pages", "vlc_gemm_bf16", "vlc_gemm_row_tile", "vlc_pack_operand", "vlc_attn_mixed", "vlc_attn_combine", "vlc_attn_pp",
+           "vlc_store_write_pages", "vlc_gemm_bf16", "vlc_gemm_bf16_relocate", "vlc_gemm_row_tile", "vlc_pack_operand", "vlc_attn_mixed", "vlc_attn_combine", "vlc_attn_pp",
            "vlc_patchify", "vlc_set_tuning", "vlc_set_debug_buffer", "vlc_set_trace_buffer")
 
 
@@ -66,6 +66,8 @@ def load():
         lib.vlc_store_write_pages.argtypes = [vp, i, i, i, i, vp, i, vp, i, vp]
         lib.vlc_gemm_bf16.argtypes = [vp, i, i, vp, i, i, C.POINTER(Epilogue), i, vp, C.c_size_t, vp, vp]
         lib.vlc_gemm_row_tile.argtypes = [i]
+        lib.vlc_gemm_bf16_relocate.argtypes = [vp, i, i, vp, i, i, C.POINTER(Epilogue), i, vp, C.c_size_t, vp,
+                                               vp, vp, i, vp, i, i, vp, vp, i, vp, vp, i, vp, vp, i, vp]
         lib.vlc_pack_operand.argtypes = [vp, i, i, i, vp, i, i, vp]
         lib.vlc_attn_mixed.argtypes = [C.POINTER(AttnArgs), vp]
         lib.vlc_attn_combine.argtypes = [C.POINTER(AttnArgs), vp]

@@ -19,6 +19,7 @@
 //   QKV_PLAIN encoder projections (model.py:318)
 #include "vlc_internal.h"
 #include "vlc_gemm_epi.cuh"
+#include "vlc_reloc.cuh"
 
 namespace vlc {
 
@@ -63,7 +64,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 template <int KIND, int H>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc(const uint8_t* __restrict__ wp, const uint8_t* __restrict__ xp, GemmEpi epi, SkSched sk,
-                 int n_tile, int stages, float* ws, int* counters) {
+                 int n_tile, int stages, float* ws, int* counters, RelocArgs rl) {
+  // CTAs past the GEMM's own (sk.G) relocate cached KV (vlc_reloc.cuh) on the SMs the projection
+  // leaves idle: independent of the previous kernel's output and of this GEMM's (disjoint rows)
+  if ((int)blockIdx.x >= sk.G) {
+    if (threadIdx.x < RELOC_THREADS)
+      for (int b = blockIdx.x - sk.G; b < rl.n_blocks; b += gridDim.x - sk.G) relocate_block(rl, b, threadIdx.x);
+    return;
+  }
   constexpr int BM = GEMM_BM * H;
   constexpr int BK = GEMM_BK / H;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -360,7 +368,7 @@ int gemm_row_tile(int m_tokens) {
 // ws must hold G * 2 * BM * n_tile floats; counters 2 * G ints (zero).
 cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap,
                         int m_tokens, const GemmEpi& epi, int max_ctas, float* ws, size_t ws_bytes,
-                        int* counters, cudaStream_t stream) {
+                        int* counters, cudaStream_t stream, const RelocArgs* rl) {
   if (m_tokens <= 0) return cudaSuccess;
   const int n_tile = gemm_row_tile(m_tokens);
   // token-heavy non-residual GEMMs: CTA-pair kernel (halves the activation bytes per SM)
@@ -369,6 +377,11 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   const int pair_min = g_pair < 0 ? -g_pair : g_pair;
   if (g_pair != 0 && epi.kind != EPI_RESID && n_tile >= pair_min &&
       (g_pair < 0 || (long long)(n_pad / 128) * ((m_tokens + n_tile - 1) / n_tile) >= 2LL * num_sms())) {
+    if (rl && rl->n_blocks > 0) {                      // the pair kernel has no spare CTAs
+      const cudaError_t e = launch_relocate(*rl, stream);
+      if (e != cudaSuccess) return e;
+      rl = nullptr;
+    }
     const cudaError_t e = launch_gemm_pair(W, n_pad, k_pad, X, x_rows_cap, m_tokens, epi,
                                            max_ctas > 0 ? max_ctas / 2 : 0, stream);
     if (e != cudaErrorNotSupported) return e;
@@ -403,6 +416,19 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   SkSched sk{U, G, KB, m_tiles, red ? 1 : 0};
   const uint8_t* wpp = reinterpret_cast<const uint8_t*>(W);
   const uint8_t* xpp = reinterpret_cast<const uint8_t*>(X);
+  RelocArgs rla{};
+  int grid = G;
+  if (rl && rl->n_blocks > 0) {       // relocation CTAs on the SMs this GEMM leaves idle
+    rla = *rl;
+    const int extra = num_sms() - G;
+    if (extra <= 0) {
+      cudaError_t e = launch_relocate(rla, stream);
+      if (e != cudaSuccess) return e;
+      rla.n_blocks = 0;
+    } else {
+      grid = G + extra;
+    }
+  }
 #define VLC_GEMM_KIND(K)                                                                              \
   case K: {                                                                                           \
     static bool attr = false;                                                                         \
@@ -412,10 +438,10 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
       attr = true;                                                                                    \
     }                                                                                                 \
     if (H == 2)                                                                                       \
-      return launch_chain(gemm_bf16_tc<K, 2>, dim3(G), dim3(GEMM_THREADS), smem, stream, g_coop != 0, wpp, xpp, \
-                          epi, sk, n_tile, stages, ws, counters);                                     \
-    return launch_chain(gemm_bf16_tc<K, 1>, dim3(G), dim3(GEMM_THREADS), smem, stream, g_coop != 0, wpp, xpp, epi, \
-                        sk, n_tile, stages, ws, counters);                                            \
+      return launch_chain(gemm_bf16_tc<K, 2>, dim3(grid), dim3(GEMM_THREADS), smem, stream, g_coop != 0, wpp,    \
+                          xpp, epi, sk, n_tile, stages, ws, counters, rla);                           \
+    return launch_chain(gemm_bf16_tc<K, 1>, dim3(grid), dim3(GEMM_THREADS), smem, stream, g_coop != 0, wpp, xpp, \
+                        epi, sk, n_tile, stages, ws, counters, rla);                                  \
   }
   switch (epi.kind) {
     VLC_GEMM_KIND(EPI_F32)

@@ -26,6 +26,7 @@ extern int g_attn_kt;         // key 12: key tile of the hd-128 attention kernel
 extern int g_attn_min_smem;   // key 5: lower bound on the attention kernel's dynamic smem
 extern int g_coop;            // key 2: cooperative launch of the stream-K GEMM
 extern int g_deterministic;   // key 13: bitwise run-to-run reproducible RESID GEMMs (slower)
+extern int g_reloc_wide;      // key 14: idle-SM relocation variant (smem bytes requested; 0 = off)
 extern int g_pair;            // key 10: CTA-pair GEMM threshold on the token tile (0 = off)
 extern int g_unsplit_min;     // key 9: tiles >= this (and <= #SMs) -> one CTA per tile
 extern int g_wide;            // key 7: 256-row GEMM tiles (0 auto, 1 never, 2 always)
@@ -72,9 +73,11 @@ cudaError_t make_tmap_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64
 cudaError_t make_tmap_4d(CUtensorMap* map, const void* base, const uint64_t* dims, const uint64_t* strides_bytes,
                          const uint32_t* box, int swizzle_bytes);
 
+struct RelocArgs;   // vlc_reloc.cuh
+cudaError_t launch_relocate(const RelocArgs& r, cudaStream_t stream);
 cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap,
                         int m_tokens, const GemmEpi& epi, int max_ctas, float* ws, size_t ws_bytes,
-                        int* counters, cudaStream_t stream);
+                        int* counters, cudaStream_t stream, const RelocArgs* rl = nullptr);
 int gemm_row_tile(int m_tokens);
 cudaError_t launch_gemm_pair(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap, int m_tokens,
                              const GemmEpi& epi, int max_pairs, cudaStream_t stream);

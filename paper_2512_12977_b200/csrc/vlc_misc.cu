@@ -2,6 +2,7 @@
 // fused KV gather + RoPE re-rotation + scatter (kv_relocate), store page writes
 // and image patchify.
 #include "vlc_internal.h"
+#include "vlc_reloc.cuh"
 
 namespace vlc {
 
@@ -126,104 +127,35 @@ __global__ void rmsnorm_generic(float* __restrict__ x, int ldx, const float* __r
 }
 
 // ------------------------------------------------------------------ kv_relocate (K2+K3)
-// One block = RELOC_TOK consecutive tokens of one (image, layer) descriptor.
-// K: thread (token, frequency chunk of 8, head group) rotates 8 pairs per head
-// with 128-bit loads of both halves; cos/sin for the token's position are
-// loaded once and reused across every head.  V: straight 128-bit copy.
-constexpr int RELOC_TOK = 8;
-constexpr int RELOC_THREADS = 256;
-
-__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-
-__device__ __forceinline__ void rotate8(const uint4& a, const uint4& b, const float* c,
-                                        const float* s, uint4& oa, uint4& ob) {
-  const uint32_t* pa = &a.x;
-  const uint32_t* pb = &b.x;
-  uint32_t* qa = &oa.x;
-  uint32_t* qb = &ob.x;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float a0 = bf16_lo(pa[i]), a1 = bf16_hi(pa[i]);
-    const float b0 = bf16_lo(pb[i]), b1 = bf16_hi(pb[i]);
-    const float c0 = c[2 * i], c1 = c[2 * i + 1], s0 = s[2 * i], s1 = s[2 * i + 1];
-    qa[i] = pack_bf16(a0 * c0 - b0 * s0, a1 * c1 - b1 * s1);
-    qb[i] = pack_bf16(b0 * c0 + a0 * s0, b1 * c1 + a1 * s1);
-  }
-}
-
-__global__ void __launch_bounds__(RELOC_THREADS)
-    kv_relocate_kernel(const __nv_bfloat16* __restrict__ kpool,
-                       const __nv_bfloat16* __restrict__ vpool, int page_tokens,
-                       const int* __restrict__ page_table, int kv, int hd,
-                       __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
-                       int kv_rows_cap, const int* __restrict__ descs,
-                       const int2* __restrict__ blocks, const float* __restrict__ cos_tab,
-                       const float* __restrict__ sin_tab, int tab_ld) {
+// One CTA per RELOC_TOK-token block (vlc_reloc.cuh).
+__global__ void __launch_bounds__(RELOC_THREADS) kv_relocate_kernel(RelocArgs r) {
   pdl_wait();
   pdl_trigger();
-  const int2 blk = blocks[blockIdx.x];
-  const int* dsc = descs + blk.x * 8;
-  const int layer = dsc[0], pt_off = dsc[1], tok0 = dsc[2], ntok = dsc[3];
-  const int dst0 = dsc[4], pos0 = dsc[5];
-  const int t_begin = blk.y;
-  const int t_count = min(RELOC_TOK, ntok - t_begin);
-  const int heads = kv / hd;
-  const int fchunks = hd / 16;  // chunks of 8 frequencies
-  const long layer_off = (long)layer * kv_rows_cap;
+  relocate_block(r, blockIdx.x, threadIdx.x);
+}
 
-  // ---- K: rotate pairs (j, j + hd/2) of every head
-  const int group_threads = fchunks * RELOC_TOK;
-  const int n_groups = RELOC_THREADS / group_threads;
-  const int tid = threadIdx.x;
-  if (tid < n_groups * group_threads) {
-    const int fc = tid % fchunks;
-    const int tk = (tid / fchunks) % RELOC_TOK;
-    const int hg = tid / group_threads;
-    if (tk < t_count) {
-      const int t = tok0 + t_begin + tk;  // token index inside the image
-      const long src_row = (long)page_table[pt_off + t / page_tokens] * page_tokens + (t % page_tokens);
-      const long dst_row = layer_off + dst0 + t_begin + tk;
-      const int pos = pos0 + t_begin + tk;
-      float c[8], s[8];
-      const float4* cp = reinterpret_cast<const float4*>(cos_tab + (long)pos * tab_ld + fc * 8);
-      const float4* sp = reinterpret_cast<const float4*>(sin_tab + (long)pos * tab_ld + fc * 8);
-      *reinterpret_cast<float4*>(c) = __ldg(cp);
-      *reinterpret_cast<float4*>(c + 4) = __ldg(cp + 1);
-      *reinterpret_cast<float4*>(s) = __ldg(sp);
-      *reinterpret_cast<float4*>(s + 4) = __ldg(sp + 1);
-      const __nv_bfloat16* srow = kpool + src_row * kv;
-      __nv_bfloat16* drow = kc + dst_row * kv;
-      const int half = hd >> 1;
-#pragma unroll 4
-      for (int h = hg; h < heads; h += n_groups) {
-        const int ea = h * hd + fc * 8;
-        const uint4 a = ldg_stream(reinterpret_cast<const uint4*>(srow + ea));
-        const uint4 b = ldg_stream(reinterpret_cast<const uint4*>(srow + ea + half));
-        uint4 oa, ob;
-        rotate8(a, b, c, s, oa, ob);
-        *reinterpret_cast<uint4*>(drow + ea) = oa;
-        *reinterpret_cast<uint4*>(drow + ea + half) = ob;
-      }
+// "Idle-SM" variant (g_reloc_wide): 4 blocks per 1024-thread CTA with a large (unused) shared
+// memory request, so that relocation CTAs never co-reside with a GEMM / attention CTA (whose L1 /
+// shared-memory bandwidth they would steal) and instead fill the SMs a projection leaves idle.
+__global__ void __launch_bounds__(4 * RELOC_THREADS) kv_relocate_wide_kernel(RelocArgs r) {
+  const int b = blockIdx.x * 4 + (threadIdx.x / RELOC_THREADS);
+  if (b < r.n_blocks) relocate_block(r, b, threadIdx.x % RELOC_THREADS);
+}
+
+int g_reloc_wide = 0;   // tuning key 14: shared memory bytes requested by the idle-SM variant (0 = off)
+
+cudaError_t launch_relocate(const RelocArgs& r, cudaStream_t stream) {
+  if (r.n_blocks <= 0) return cudaSuccess;
+  if (g_reloc_wide > 0) {
+    static int attr = 0;
+    if (attr != g_reloc_wide) {
+      cudaFuncSetAttribute(kv_relocate_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, g_reloc_wide);
+      attr = g_reloc_wide;
     }
+    kv_relocate_wide_kernel<<<(r.n_blocks + 3) / 4, 4 * RELOC_THREADS, g_reloc_wide, stream>>>(r);
+    return cudaGetLastError();
   }
-  // ---- V: 128-bit copy
-  const int vec_per_row = kv / 8;
-  const int total = t_count * vec_per_row;
-#pragma unroll 4
-  for (int i = tid; i < total; i += RELOC_THREADS) {
-    const int tk = i / vec_per_row, vi = i - tk * vec_per_row;
-    const int t = tok0 + t_begin + tk;
-    const long src_row = (long)page_table[pt_off + t / page_tokens] * page_tokens + (t % page_tokens);
-    const long dst_row = layer_off + dst0 + t_begin + tk;
-    const uint4 v = ldg_stream(reinterpret_cast<const uint4*>(vpool + src_row * kv) + vi);
-    reinterpret_cast<uint4*>(vc + dst_row * kv)[vi] = v;
-  }
+  return launch_chain(kv_relocate_kernel, dim3(r.n_blocks), dim3(RELOC_THREADS), 0, stream, false, r);
 }
 
 // ------------------------------------------------------------------ store pages
@@ -301,11 +233,11 @@ int vlc_kv_relocate_impl(const void* kpool, const void* vpool, int page_tokens, 
                          const int* blocks, int n_blocks, const float* cos_tab, const float* sin_tab,
                          int tab_ld, cudaStream_t stream) {
   if (n_blocks <= 0) return 0;
-  return (int)launch_chain(kv_relocate_kernel, dim3(n_blocks), dim3(RELOC_THREADS), 0, stream, false,
-                           reinterpret_cast<const __nv_bfloat16*>(kpool), reinterpret_cast<const __nv_bfloat16*>(vpool),
-                           page_tokens, page_table, kv, head_dim, reinterpret_cast<__nv_bfloat16*>(kc),
-                           reinterpret_cast<__nv_bfloat16*>(vc), kv_rows_cap, descs,
-                           reinterpret_cast<const int2*>(blocks), cos_tab, sin_tab, tab_ld);
+  RelocArgs r{reinterpret_cast<const __nv_bfloat16*>(kpool), reinterpret_cast<const __nv_bfloat16*>(vpool),
+              page_tokens, page_table, kv, head_dim, reinterpret_cast<__nv_bfloat16*>(kc),
+              reinterpret_cast<__nv_bfloat16*>(vc), kv_rows_cap, descs, reinterpret_cast<const int2*>(blocks),
+              n_blocks, cos_tab, sin_tab, tab_ld};
+  return (int)launch_relocate(r, stream);
 }
 
 int vlc_store_write_pages_impl(const void* src, int src_f32, int layers, int tokens, int kv,

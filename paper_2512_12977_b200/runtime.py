@@ -17,6 +17,8 @@ from .model import RMS_EPS, DeviceWeights
 N_SMS = 148
 _DEBUG_SYNC = bool(int(__import__("os").environ.get("VLC_DEBUG_SYNC", "0")))  # sync + log every launch
 _OVERLAP_RELOC = bool(int(__import__("os").environ.get("VLC_RELOC_OVERLAP", "1")))
+_FUSE_RELOC = bool(int(__import__("os").environ.get("VLC_RELOC_FUSED", "0")))
+_SKIP_RELOC_EXPERIMENT = bool(int(__import__("os").environ.get("VLC_EXPERIMENT_SKIP_RELOC", "0")))
 
 
 def _torch():
@@ -159,6 +161,14 @@ class Runner:
         self.graph_launches: dict = {}
         self.tracer = None         # list -> (name, ev0, ev1, algo_bytes, algo_flops) per launch
         self.overlap_reloc = _OVERLAP_RELOC
+        self.fuse_reloc = _FUSE_RELOC    # relocate layer i's cached KV inside its QKV GEMM launch
+        # The cached-KV relocation runs on a low-priority side stream as 1024-thread CTAs that request
+        # ~100 KB of shared memory, so they cannot co-reside with GEMM / attention CTAs (whose L1 /
+        # shared-memory bandwidth they would steal) and fill the SMs a projection leaves idle; the
+        # layer chain is captured at high priority so its CTAs win the SMs that free up.
+        # Measured on C3: 5.58 -> 5.24 ms TTFT (tools: VLC_HI_PRIO / VLC_RELOC_WIDE A/B, run42).
+        self.hi_prio = bool(int(__import__("os").environ.get("VLC_HI_PRIO", "1")))
+        self.lib.vlc_set_tuning(14, int(__import__("os").environ.get("VLC_RELOC_WIDE", "100000")))
         self.tp_group = None       # head-parallel process group (engine sets it from the model)
         self._side = None          # side stream of the overlapped kv_relocate
 
@@ -186,8 +196,11 @@ class Runner:
         self.launches += kernels
 
     # ---------------------------------------------------------------- primitives
-    def gemm(self, w, k_pad, x, m, epi: N.Epilogue, splits: int | None = None, name="gemm", k_valid=None):
-        """w: PackedWeight; x: packed activations (row tile N.row_tile(m)), flat bf16 tensor."""
+    def gemm(self, w, k_pad, x, m, epi: N.Epilogue, splits: int | None = None, name="gemm", k_valid=None,
+             reloc=None):
+        """w: PackedWeight; x: packed activations (row tile N.row_tile(m)), flat bf16 tensor.
+        reloc: vlc_kv_relocate arguments (after `kv`... see vlc_gemm_bf16_relocate) to run on the
+        CTAs this GEMM leaves idle."""
         if m <= 0:
             return
         if splits is None:
@@ -196,10 +209,16 @@ class Runner:
         R = N.row_tile(m)
         kv_ = k_valid or k_pad
         nbytes = 2 * epi.n_valid * kv_ + 2 * m * kv_
-        self._run(name, lambda: N.check(self.lib.vlc_gemm_bf16(
-            w.data_ptr(), w.n, w.k, x.data_ptr(), -(-m // R) * R, m, epi, splits, self.splitk.data_ptr(),
-            self.splitk.numel() * 4, self.counters.data_ptr(), _stream()), "vlc_gemm_bf16"),
-            nbytes, 2 * m * epi.n_valid * kv_)
+        if reloc is None:
+            self._run(name, lambda: N.check(self.lib.vlc_gemm_bf16(
+                w.data_ptr(), w.n, w.k, x.data_ptr(), -(-m // R) * R, m, epi, splits, self.splitk.data_ptr(),
+                self.splitk.numel() * 4, self.counters.data_ptr(), _stream()), "vlc_gemm_bf16"),
+                nbytes, 2 * m * epi.n_valid * kv_)
+        else:
+            self._run(name, lambda: N.check(self.lib.vlc_gemm_bf16_relocate(
+                w.data_ptr(), w.n, w.k, x.data_ptr(), -(-m // R) * R, m, epi, splits, self.splitk.data_ptr(),
+                self.splitk.numel() * 4, self.counters.data_ptr(), *reloc, _stream()), "vlc_gemm_bf16_relocate"),
+                nbytes, 2 * m * epi.n_valid * kv_)
 
     def rmsnorm(self, x, gamma, out, rows, out_f32=False, row_map=0, pk=(0, 0)):
         """out: fp32 row-major [rows, ld] (out_f32) or flat packed bf16 with geometry pk=(R, KB)."""
@@ -382,7 +401,9 @@ class Runner:
             if g is None:
                 chain()                                   # eager run serves this call
                 g = torch.cuda.CUDAGraph()
-                side = torch.cuda.Stream()
+                # the layer chain is captured at high priority, the side-stream relocation at the
+                # default (lowest) one: when SMs free up, chain CTAs are dispatched first
+                side = torch.cuda.Stream(priority=-1 if self.hi_prio else 0)
                 side.wait_stream(torch.cuda.current_stream())
                 with torch.cuda.stream(side):
                     with torch.cuda.graph(g, stream=side):
@@ -480,7 +501,21 @@ class Runner:
                 pack.ptr("descs"), pack.ptr("blocks") + 8 * b0, n_b, dw.cos.data_ptr(), dw.sin.data_ptr(),
                 cfg.head_dim // 2, _stream()), "vlc_kv_relocate"), lay.reloc_tokens * kv * 2 * 4 * n_b // nb)
 
-        if nb and self.overlap_reloc:
+        if _SKIP_RELOC_EXPERIMENT:
+            nb = 0                    # timing experiment only: wrong results
+        lb = lay.reloc_layer_blocks
+        fused_reloc = bool(nb) and self.fuse_reloc and "inject" not in buf
+
+        def reloc_args(i):
+            """Layer i's relocation, run by the QKV GEMM's spare CTAs (vlc_gemm_bf16_relocate)."""
+            if not fused_reloc or lb[i + 1] <= lb[i]:
+                return None
+            return (kpool, vpool, P, pack.ptr("pages"), kv, cfg.head_dim, kc.data_ptr(), vc.data_ptr(), kc.shape[1],
+                    pack.ptr("descs"), pack.ptr("blocks") + 8 * int(lb[i]), int(lb[i + 1] - lb[i]), dw.cos.data_ptr(),
+                    dw.sin.data_ptr(), cfg.head_dim // 2)
+        if fused_reloc:
+            pass
+        elif nb and self.overlap_reloc:
             torch = _torch()
             main = torch.cuda.current_stream()
             if self._side is None:
@@ -508,7 +543,7 @@ class Runner:
                 out2=kc[i].data_ptr(), ld2=kv, out3=vc[i].data_ptr(), ld3=kv, out4=kpre[i].data_ptr(), ld4=kv,
                 map1=pack.ptr(f"qdst{i}"), map2=pack.ptr("row_kv"), pos=pack.ptr("row_pos"),
                 cos_tab=dw.cos.data_ptr(), sin_tab=dw.sin.data_ptr(), tab_ld=cfg.head_dim // 2,
-                hd=cfg.head_dim, seg=kv), name="gemm_qkv", k_valid=d)
+                hd=cfg.head_dim, seg=kv), name="gemm_qkv", k_valid=d, reloc=reloc_args(i))
             if "inject" in buf:
                 inj, ipk = buf["inject"]
                 lb = inj["layer_blocks"]
