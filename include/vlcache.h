@@ -106,7 +106,8 @@ typedef struct vlc_attn_args {
 
 const char* vlc_last_error(void);
 int vlc_version(void);
-/* Tuning knobs for experiments: key 1 = GEMM pipeline stages (0 = automatic). */
+/* Tuning knobs for experiments: key 1 = GEMM pipeline stages (0 = automatic); keys 2-15 see
+   vlc_capi.cu (e.g. 15 = softmax variant of the hd-128 attention). */
 int vlc_set_tuning(int key, int value);
 int vlc_set_debug_buffer(void* device_ptr);
 int vlc_set_trace_buffer(void* device_ptr);   /* experiments: attention CTA-0 event trace (>= 224 u64) */

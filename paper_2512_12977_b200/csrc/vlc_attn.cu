@@ -329,33 +329,50 @@ static cudaError_t launch_attn_hd(const vlc_attn_args& a, cudaStream_t stream) {
 // tensor core works on the other group's S / PV.  TMEM: S_A, S_B (64 cols fp32), P_A, P_B
 // (32 cols of packed bf16 pairs, the A operand of the PV MMA), O_A, O_B (HD cols fp32).
 constexpr int PP_THREADS = 320;
-__device__ unsigned long long* g_attn_dbg = nullptr;  // per-CTA phase timestamps (experiments)
-__device__ __forceinline__ void adbg(int slot) {
-  if (g_attn_dbg) {
+// Experiment instrumentation.  The buffers travel as kernel parameters (constant bank), so a
+// disabled trace costs a predicated branch, not a global load on the softmax critical path.
+static unsigned long long* h_attn_dbg = nullptr;    // per-CTA phase timestamps
+static unsigned long long* h_attn_trace = nullptr;  // per-iteration event times of CTA 0
+__device__ __forceinline__ void adbg(unsigned long long* dbgp, int slot) {
+  if (dbgp) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    g_attn_dbg[blockIdx.x * 8 + slot] = t;
+    dbgp[blockIdx.x * 8 + slot] = t;
   }
 }
-void set_attn_debug_buffer(unsigned long long* p) { cudaMemcpyToSymbol(g_attn_dbg, &p, sizeof(p)); }
-__device__ unsigned long long* g_attn_trace = nullptr;  // per-iteration event times of CTA 0 (experiments)
-__device__ __forceinline__ void atrace(int slot) {
-  if (g_attn_trace && blockIdx.x == 0) {
+void set_attn_debug_buffer(unsigned long long* p) { h_attn_dbg = p; }
+__device__ __forceinline__ void atrace(unsigned long long* trc, int slot) {
+  if (trc && blockIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    g_attn_trace[slot] = t;
+    trc[slot] = t;
   }
 }
-void set_attn_trace_buffer(unsigned long long* p) { cudaMemcpyToSymbol(g_attn_trace, &p, sizeof(p)); }
+void set_attn_trace_buffer(unsigned long long* p) { h_attn_trace = p; }
+// VAR 0x400: per-phase cycle counts summed over all CTAs into g_attn_trace[256 + slot]
+__device__ __forceinline__ long long clk() { long long c; asm volatile("mov.u64 %0, %%clock64;" : "=l"(c)); return c; }
+#define PH(on, slot, t)                                                               \
+  do {                                                                                \
+    if (on) {                                                                         \
+      const long long t2_ = clk();                                                    \
+      atomicAdd(&trc[256 + (slot)], (unsigned long long)(t2_ - (t)));        \
+      t = t2_;                                                                        \
+    }                                                                                 \
+  } while (0)
 // KT = keys per tile.  KT = 64: S double-buffered per query tile (S runs two tiles ahead).
 // KT = 128 (hd 128): one 128-column S buffer per query tile (TMEM: S_A, S_B, O_A, O_B = 512
 // columns), half the MMA instructions and barrier round trips per key; the ping-pong between
 // the two query tiles hides the S(j) -> softmax -> PV(j) -> S(j+1) chain of each tile.
 int g_attn_kt = 128;   // tuning key 12: key tile of the hd-128 kernel (64 or 128)
+int g_attn_var = 0;    // tuning key 15: softmax variant of the hd-128 / 128-key kernel (see VAR below)
 
-template <int HD, int KT>
+template <int HD, int KT, bool PSM_ = false>
 struct PPCfg {
   static constexpr bool DB = KT == 64;
+  // PSM: P staged in shared memory (SS MMA for PV) instead of aliased over S in TMEM, so S(j+1)
+  // can be issued as soon as the softmax has read S(j) into registers (KT = 128 only)
+  static constexpr bool PSM = PSM_ && KT == 128;
+  static constexpr int P_BYTES = PSM ? 128 * KT * 2 : 0;
   static constexpr int ATOM_E = HD < 64 ? HD : 64;
   static constexpr int SWZ = ATOM_E * 2;
   static constexpr int N_ATOMS = HD / ATOM_E;
@@ -365,9 +382,11 @@ struct PPCfg {
   static constexpr int KV_ATOM = KT * SWZ;
   // K/V ring as deep as shared memory allows (<= 8): the softmax warps wait on S, i.e. on K/V
   // loads, when the ring is shallow (ncu: s_full wait was the top stall at 3 stages)
-  static constexpr int ST_FIT = (232448 - 1024 - 256 - 2 * Q_BYTES) / (2 * KV_BYTES);
+  static constexpr int ST_FIT = (232448 - 1024 - 320 - 2 * Q_BYTES - P_BYTES) / (2 * KV_BYTES);
   static constexpr int ST = ST_FIT > 8 ? 8 : ST_FIT;
-  static constexpr int SMEM = 1024 + 2 * Q_BYTES + ST * 2 * KV_BYTES + 256;
+  static constexpr int SMEM = 1024 + 2 * Q_BYTES + ST * 2 * KV_BYTES + P_BYTES + 320;
+  static_assert(ST * 2 * KV_BYTES >= 2 * 128 * HD * 4, "split partials are staged in the K/V ring");
+  static_assert(ST * 2 * KV_BYTES >= 256 * 8 * 12 + 256 * 4, "merge tables live in the K/V ring");
   // TMEM: S[x][buf] (KT fp32 cols; P bf16 pairs aliased in its first KT/2 cols), O[x] (HD cols)
   __device__ static constexpr uint32_t s_col(int x, int b) { return DB ? 64u * (2 * x + b) : 128u * x; }
   __device__ static constexpr uint32_t o_col(int x) { return 256u + (uint32_t)(HD > 64 ? HD : 64) * x; }
@@ -375,25 +394,35 @@ struct PPCfg {
   __device__ static constexpr uint32_t sphase(int j) { return DB ? ((j >> 1) & 1) : (j & 1); }
 };
 
-template <int HD, int KT>
+// VAR (softmax variants, tuning key 15): bit 0 = three-input max, bits 4-6 = pairs of every 8 whose
+// exponentials run as poly_exp2 on the FMA pipe; bits 1 / 2 = timing experiments only (no exp2 /
+// no O rescale: wrong results).
+template <int HD, int KT, int VAR = 0>
 __global__ void __launch_bounds__(PP_THREADS, 1)
     attn_pp_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
-                   const __grid_constant__ CUtensorMap map_v, vlc_attn_args a) {
-  using C = PPCfg<HD, KT>;
+                   const __grid_constant__ CUtensorMap map_v, vlc_attn_args a, unsigned long long* dbgp,
+                   unsigned long long* trc) {
+  using C = PPCfg<HD, KT, (VAR & 0x1000) != 0>;
+  constexpr bool PSM = C::PSM;
   constexpr int PP_KT = KT;
+  constexpr int POLY = (VAR >> 4) & 7;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                                   // [2][Q_BYTES]
   uint8_t* sK = sQ + 2 * C::Q_BYTES;                    // [ST][KV_BYTES]
   uint8_t* sV = sK + C::ST * C::KV_BYTES;               // [ST][KV_BYTES]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + C::ST * C::KV_BYTES);
+  uint8_t* sP = sV + C::ST * C::KV_BYTES;               // [P_BYTES] (PSM)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::P_BYTES);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + C::ST;
   uint64_t* s_full = kv_empty + C::ST;   // [2 tiles][2 buffers]
   uint64_t* p_full = s_full + 4;         // [2 tiles][2 S buffers]: P(j) of tile x in buffer j&1
   uint64_t* o_done = p_full + 4;         // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  uint64_t* all_done = o_done + 2;       // every MMA of the CTA complete (K/V ring reusable)
+  uint64_t* s_free = all_done + 1;       // [2] PSM: S(j) of tile x read into registers
+  uint64_t* p_free = s_free + 2;         // [2] PSM: PV of P-buffer use u complete (alternating)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_free + 2);
 
   const int* it = a.items + blockIdx.x * 8;
   const int q_row0 = it[0], nq = it[1], head = it[2], kv_row0 = it[3];
@@ -408,10 +437,12 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     nt_t[x] = e > kb ? (e - kb + PP_KT - 1) / PP_KT : 0;
   }
   const int nt = max(nt_t[0], nt_t[1]);
+  // PSM: the single P buffer is used in the order (j, tile A), (j, tile B), ...; use index of (x, j)
+  auto p_use = [&](int x, int j) { return min(j, nt_t[0]) + min(j, nt_t[1]) + ((x == 1 && j < nt_t[0]) ? 1 : 0); };
 
   const uint32_t warp = warp_id(), lane = lane_id();
   if (warp == 0 && lane == 0) {
-    adbg(0);
+    adbg(dbgp, 0);
     tma_prefetch(&map_q);
     tma_prefetch(&map_k);
     tma_prefetch(&map_v);
@@ -424,6 +455,11 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     for (int x = 0; x < 4; ++x) mbar_init(&p_full[x], 128);
     for (int x = 0; x < 2; ++x) {
       mbar_init(&o_done[x], 1);
+    }
+    mbar_init(all_done, 1);
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&s_free[x], 128);
+      mbar_init(&p_free[x], 1);
     }
     fence_barrier_init();
   }
@@ -446,7 +482,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       for (int j = 0; j < nt; ++j) {
         const int st = j % C::ST;
         mbar_wait(&kv_empty[st], ((j / C::ST) & 1) ^ 1);
-        if (j < 32) atrace(128 + j);
+        if (j < 32) atrace(trc, 128 + j);
         mbar_expect_tx(&kv_full[st], 2 * C::KV_BYTES);
         const int krow = kv_row0 + kb + j * PP_KT;   // one op per K / V tile: 4-D {elems, keys, atoms, layer}
         tma_load_4d(sK + st * C::KV_BYTES, &map_k, &kv_full[st], 0, krow, head * C::N_ATOMS, a.layer, pol_kv);
@@ -458,7 +494,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       const uint32_t idesc_s = make_idesc_bf16(128, PP_KT, 0, 0);
       const uint32_t idesc_o = make_idesc_bf16(128, HD, 0, 1);
       mbar_wait(q_full, 0);
-      adbg(1);
+      adbg(dbgp, 1);
       auto issue_s = [&](int x, int j) {   // S[x][j&1] = Q_x K_j^T
         const int st = j % C::ST;
         mbar_wait(&kv_full[st], (j / C::ST) & 1);
@@ -471,7 +507,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
           const uint32_t eoff = ((k * 16) % C::ATOM_E) * 2;
           const uint64_t ad = make_sdesc(q_addr + at * C::Q_ATOM + eoff, 16, 8 * C::SWZ, C::SWZ);
           const uint64_t bd = make_sdesc(k_addr + at * C::KV_ATOM + eoff, 16, 8 * C::SWZ, C::SWZ);
-          tc_mma_f16(tmem + C::s_col(x, C::sbuf(j)), ad, bd, idesc_s, k > 0 ? 1u : 0u);
+          if (!(VAR & 0x200)) tc_mma_f16(tmem + C::s_col(x, C::sbuf(j)), ad, bd, idesc_s, k > 0 ? 1u : 0u);
         }
         tc_commit(&s_full[2 * x + C::sbuf(j)]);
       };
@@ -481,30 +517,72 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
 #pragma unroll
         for (int k = 0; k < PP_KT / 16; ++k) {
           const uint64_t bd = make_sdesc(v_addr + k * 16 * C::SWZ, C::KV_ATOM, 8 * C::SWZ, C::SWZ);
-          tc_mma_f16_ts(tmem + C::o_col(x), tmem + C::s_col(x, C::sbuf(j)) + k * 8, bd, idesc_o,
-                        (j > 0 || k > 0) ? 1u : 0u);
+          if (!(VAR & 0x200))
+            tc_mma_f16_ts(tmem + C::o_col(x), tmem + C::s_col(x, C::sbuf(j)) + k * 8, bd, idesc_o,
+                          (j > 0 || k > 0) ? 1u : 0u);
         }
         tc_commit(&o_done[x]);
       };
+      if constexpr (PSM) {
+        // S_x(j+1) as soon as the softmax has read S_x(j); PV_x(j) (P from smem) when P_x(j) is
+        // written; P-buffer use u releases the buffer through p_free[u & 1]
+        for (int x = 0; x < 2; ++x)
+          if (0 < nt_t[x]) issue_s(x, 0);
+        const uint32_t p_addr = smem_u32(sP);
+        for (int j = 0; j < nt; ++j) {
+          for (int x = 0; x < 2; ++x)
+            if (j + 1 < nt_t[x]) {
+              mbar_wait(&s_free[x], j & 1);
+              tc_fence_after();
+              issue_s(x, j + 1);
+            }
+          const int st = j % C::ST;
+          const uint32_t v_addr = smem_u32(sV + st * C::KV_BYTES);
+          for (int x = 0; x < 2; ++x) {
+            if (j >= nt_t[x]) continue;
+            mbar_wait(&p_full[2 * x], j & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < PP_KT / 16; ++k) {
+              const uint64_t ad = make_sdesc(p_addr + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, 128);
+              const uint64_t bd = make_sdesc(v_addr + k * 16 * C::SWZ, C::KV_ATOM, 8 * C::SWZ, C::SWZ);
+              tc_mma_f16(tmem + C::o_col(x), ad, bd, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+            }
+            tc_commit(&p_free[p_use(x, j) & 1]);
+            tc_commit(&o_done[x]);
+          }
+          tc_commit(&kv_empty[st]);
+        }
+        tc_commit(all_done);
+        adbg(dbgp, 2);
+      }
       // DB: S runs two tiles ahead of the softmax (double-buffered per query tile); otherwise one
       // tile ahead: S(j+1) is issued right after PV(j), which frees the single S/P buffer
       constexpr int AHEAD = C::DB ? 2 : 1;
+      if (!PSM) {
       for (int j = 0; j < AHEAD; ++j)
         for (int x = 0; x < 2; ++x)
           if (j < nt_t[x]) issue_s(x, j);
       for (int j = 0; j < nt; ++j) {
         for (int x = 0; x < 2; ++x) {
           if (j >= nt_t[x]) continue;
+          const bool ph = (VAR & 0x400) && trc;
+          long long tph = ph ? clk() : 0;
           mbar_wait(&p_full[2 * x + C::sbuf(j)], C::sphase(j));
           tc_fence_after();
-          if (j < 16) atrace(64 + j * 4 + 2 * x);
+          PH(ph, 16 + x * 4 + 0, tph);
+          if (j < 16) atrace(trc, 64 + j * 4 + 2 * x);
           issue_pv(x, j);
+          PH(ph, 16 + x * 4 + 1, tph);
           if (j + AHEAD < nt_t[x]) issue_s(x, j + AHEAD);   // in-order after PV(j): reuses P(j)'s columns
-          if (j < 16) atrace(64 + j * 4 + 2 * x + 1);
+          PH(ph, 16 + x * 4 + 2, tph);
+          if (j < 16) atrace(trc, 64 + j * 4 + 2 * x + 1);
         }
         tc_commit(&kv_empty[j % C::ST]);
       }
-      adbg(2);
+      tc_commit(all_done);
+      adbg(dbgp, 2);
+      }
     }
     __syncwarp();
   } else {
@@ -523,14 +601,28 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       const int k0 = kb + j * PP_KT;
       const uint32_t tS = tmem + C::s_col(x, C::sbuf(j)) + lane_off;
       float s[PP_KT];
+      const bool ph = (VAR & 0x400) && r == 0 && trc;
+      long long tph = ph ? clk() : 0;
       mbar_wait(&s_full[2 * x + C::sbuf(j)], C::sphase(j));
       tc_fence_after();
-      const bool tr = (r == 0 && j < 16);
-      if (tr) atrace((x ? 160 : 0) + j * 4);
+      PH(ph, x * 8 + 0, tph);
+      if (VAR & 0x100) {                      // experiment: no softmax work at all
+        tc_fence_before();
+        if (PSM) mbar_arrive(&s_free[x]);
+        mbar_arrive(&p_full[2 * x + C::sbuf(j)]);
+        continue;
+      }
+      const bool tr = trc && r == 0 && j < 16;
+      if (tr) atrace(trc, (x ? 160 : 0) + j * 4);
 #pragma unroll
       for (int c = 0; c < PP_KT / 32; ++c) tmem_ld32(tS + 32 * c, s + 32 * c);
       tmem_wait_ld();
-      if (tr) atrace((x ? 160 : 0) + j * 4 + 1);
+      if (PSM) {                                  // S(j) is in registers: S(j+1) may overwrite it
+        tc_fence_before();
+        mbar_arrive(&s_free[x]);
+      }
+      PH(ph, x * 8 + 1, tph);
+      if (tr) atrace(trc, (x ? 160 : 0) + j * 4 + 1);
       // scores stay raw (scale folded into the exp2 FFMA); masked keys -> -inf; reductions in
       // 4 independent chains (only 2 softmax warps per scheduler: latency, not issue, binds)
       const int lim = min(qp, ke - 1) - k0;
@@ -539,8 +631,13 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         for (int i = 0; i < PP_KT; ++i) s[i] = (i <= lim) ? s[i] : NEG_INF;
       }
       float mx4[4] = {NEG_INF, NEG_INF, NEG_INF, NEG_INF};
+      if (VAR & 1) {
 #pragma unroll
-      for (int i = 0; i < PP_KT; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], s[i]);
+        for (int i = 0; i < PP_KT; i += 2) mx4[(i >> 1) & 3] = fmax3(mx4[(i >> 1) & 3], s[i], s[i + 1]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < PP_KT; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], s[i]);
+      }
       const float tmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * a.scale_log2;
       const float m_new = fmaxf(m_run, tmax);
       const bool need = m_new > m_run + 8.0f;
@@ -549,8 +646,14 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       // (PV(j-2)) is complete because S(j) was issued after it.  So PV(j-1) is waited for only
       // when rescaling, and on the last tile (so that the final wait below is unambiguous):
       // o_done has completed j-1 or j phases here (S(j) done => PV(j-2) done).
-      const bool resc = __any_sync(0xffffffffu, need && has_o);
+      PH(ph, x * 8 + 2, tph);
+      const bool resc = (VAR & 4) ? false : __any_sync(0xffffffffu, need && has_o);
       if (C::DB && j > 0 && (resc || j == ntx - 1)) {   // !DB: S(j) done => PV(j-1) done already
+        mbar_wait(&o_done[x], (j - 1) & 1);
+        tc_fence_after();
+      }
+      // PSM: S(j) done => PV(j-2) done (issued earlier), so o_done has j-1 or j completions here
+      if (PSM && j > 0 && resc) {
         mbar_wait(&o_done[x], (j - 1) & 1);
         tc_fence_after();
       }
@@ -571,31 +674,59 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         l_run = has_o ? l_run * fast_exp2(m_run - m_new) : 0.f;
         m_run = m_new;
       }
+      PH(ph, x * 8 + 3, tph);
       const bool any = m_run != NEG_INF;
       const float nm = any ? -m_run : NEG_INF;     // all-masked row: every p = exp2(-inf) = 0
       // P packed in place into s[0, KT/2) (slot i is free once pairs 2i, 2i+1 are read)
       float ls4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int i = 0; i < PP_KT / 2; ++i) {
-        const float p0 = fast_exp2(fmaf(s[2 * i], a.scale_log2, nm));
-        const float p1 = fast_exp2(fmaf(s[2 * i + 1], a.scale_log2, nm));
+        // POLY of every 8 pairs on the FMA pipe, the rest on the MUFU (both pipes busy)
+        const float x0 = fmaf(s[2 * i], a.scale_log2, nm), x1 = fmaf(s[2 * i + 1], a.scale_log2, nm);
+        float p0, p1;
+        if (VAR & 2) {
+          p0 = x0; p1 = x1;                                   // experiment: no exponential at all
+        } else if ((i & 7) < POLY) {
+          p0 = poly_exp2(x0); p1 = poly_exp2(x1);
+        } else {
+          p0 = fast_exp2(x0); p1 = fast_exp2(x1);
+        }
         ls4[i & 3] += p0 + p1;
         s[i] = __uint_as_float(pack_bf16(p0, p1));
       }
       l_run += (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
-      if (tr) atrace((x ? 160 : 0) + j * 4 + 2);
+      PH(ph, x * 8 + 4, tph);
+      if (tr) atrace(trc, (x ? 160 : 0) + j * 4 + 2);
+      if constexpr (PSM) {
+        // P(j) -> the shared P buffer (SW128 K-major: 2 atoms of 64 keys, 16-byte chunk c of row r
+        // at c ^ (r & 7)) once its previous use (the other tile's or own PV) has completed.  Use
+        // u-1 shares p_free[(u-1) & 1] only with u-3, which this thread has already seen complete.
+        const int u = p_use(x, j);
+        if (u > 0) mbar_wait(&p_free[(u - 1) & 1], ((u - 1) >> 1) & 1);
+        uint8_t* prow = sP + r * 128;
 #pragma unroll
-      for (int c = 0; c < PP_KT / 64; ++c) tmem_st32f(tS + 32 * c, s + 32 * c);   // P(j) over S(j)'s first cols
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&p_full[2 * x + C::sbuf(j)]);   // per-buffer barrier: softmax may run a tile ahead
-      if (tr) atrace((x ? 160 : 0) + j * 4 + 3);
+        for (int c = 0; c < PP_KT / 8; ++c)
+          *reinterpret_cast<uint4*>(prow + (c >> 3) * 16384 + (((c & 7) ^ (r & 7)) << 4)) =
+              make_uint4(__float_as_uint(s[4 * c]), __float_as_uint(s[4 * c + 1]), __float_as_uint(s[4 * c + 2]),
+                         __float_as_uint(s[4 * c + 3]));
+        fence_proxy_async_smem();
+        mbar_arrive(&p_full[2 * x]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < PP_KT / 64; ++c) tmem_st32f(tS + 32 * c, s + 32 * c);   // P(j) over S(j)'s first cols
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&p_full[2 * x + C::sbuf(j)]);   // per-buffer barrier: softmax may run a tile ahead
+      }
+      PH(ph, x * 8 + 5, tph);
+      if (ph) atomicAdd(&trc[256 + x * 8 + 7], 1ull);
+      if (tr) atrace(trc, (x ? 160 : 0) + j * 4 + 3);
     }
     if (ntx > 0) {   // o_done has completed ntx-1 or ntx phases here
       mbar_wait(&o_done[x], (ntx - 1) & 1);
       tc_fence_after();
     }
-    if (r == 0) adbg(3 + x);
+    if (r == 0) adbg(dbgp, 3 + x);
     const int qrow = q_row0 + x * 128 + r;
     if (group < 0) {
       const float inv = (l_run > 0.f) ? 1.0f / l_run : 0.f;
@@ -623,25 +754,36 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         }
       }
     } else {
-      const long prow = ((long)group * 8 + part) * 256 + x * 128 + r;
-      float* wo = a.ws_o + prow * HD;
+      // Split partial: once every MMA of the CTA is complete the K/V ring is free; stage this
+      // tile's fp32 O rows there (row-major, float4 slot c4 stored at c4 ^ (row & 7): bank-conflict
+      // free, same layout in ws_o) and write them with one bulk copy (full-line writes; per-thread
+      // 16-byte row stores at a 512-byte stride were L2-transaction bound).
+      const long prow0 = ((long)group * 8 + part) * 256 + x * 128;
+      {
+        if (nt > 0) mbar_wait(all_done, 0);
+        tc_fence_after();
+        float4* stg = reinterpret_cast<float4*>(sK) + x * 128 * (HD / 4) + r * (HD / 4);
 #pragma unroll
-      for (int c = 0; c < HD / 16; ++c) {
-        float o[16];
-        if (ntx > 0) {
-          tmem_ld16(tO + c * 16, o);
-          tmem_wait_ld();
-        } else {
+        for (int c = 0; c < HD / 16; ++c) {
+          float o[16];
+          if (ntx > 0) {
+            tmem_ld16(tO + c * 16, o);
+            tmem_wait_ld();
+          } else {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) o[i] = 0.f;
+            for (int i = 0; i < 16; ++i) o[i] = 0.f;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            stg[(c * 4 + q) ^ (r & 7)] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
         }
-        if (q_valid) {
-          float4* dst = reinterpret_cast<float4*>(wo + c * 16);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) __stcg(dst + q, make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]));
-        }
+        fence_proxy_async_smem();
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + x) : "memory");
+        if (quad == 0 && lane == 0 && nq_t[x] > 0)
+          bulk_store_wait(a.ws_o + prow0 * HD, reinterpret_cast<float4*>(sK) + x * 128 * (HD / 4),
+                          (uint32_t)(nq_t[x] * HD * 4));
       }
-      if (q_valid) __stcg(reinterpret_cast<float2*>(a.ws_ml) + prow, make_float2(m_run, l_run));
+      if (q_valid) __stcg(reinterpret_cast<float2*>(a.ws_ml) + prow0 + r, make_float2(m_run, l_run));
       __threadfence();
     }
   }
@@ -652,8 +794,11 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     tmem_dealloc<512>(tmem);
   }
   if (group < 0) return;
-  // ---------------- parallel merge of the nsplit partials (all CTAs of the group co-resident):
-  // one warp per output row, lane = 4 head dims, all split loads issued together
+  // ---------------- parallel merge of the nsplit partials (all CTAs of the group co-resident).
+  // This CTA merges rows [r_lo, r_hi) of the group.  Pass 1: one thread per (row, split) reads
+  // (m, l); one thread per row turns them into normalised split weights (smem, in the K/V ring,
+  // free once this CTA's partials are written).  Pass 2: one thread per (row, float4 of the head), all split loads independent --
+  // no dependent L2 round trips per row.
   if (threadIdx.x == 0) {
     atomicAdd(&a.counters[group], 1);
     volatile int* cnt = a.counters + group;
@@ -661,44 +806,59 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   }
   __syncthreads();
   __threadfence();
-  if (threadIdx.x == 0) adbg(5);
+  if (threadIdx.x == 0) adbg(dbgp, 5);
   const int r_lo = 256 * part / nsplit, r_hi = min(nq, 256 * (part + 1) / nsplit);
-  for (int rr = r_lo + (int)warp; rr < r_hi; rr += PP_THREADS / 32) {
-    const long pbase = (long)group * 8 * 256 + rr;
-    float2 ml = make_float2(-INFINITY, 0.f);
-    if ((int)lane < nsplit) ml = __ldcg(reinterpret_cast<const float2*>(a.ws_ml) + pbase + lane * 256);
-    float M = ml.x;
+  const int nr = max(0, r_hi - r_lo);
+  float2* s_ml = reinterpret_cast<float2*>(sK);                 // [nr][8]
+  float* s_w = reinterpret_cast<float*>(s_ml + 256 * 8);        // [nr][8] weight / L
+  int* s_orow = reinterpret_cast<int*>(s_w + 256 * 8);          // [nr]
+  const long gbase = (long)group * 8 * 256;
+  for (int t = threadIdx.x; t < nr * 8; t += PP_THREADS) {
+    const int rr = t >> 3, s2 = t & 7;
+    s_ml[t] = s2 < nsplit ? __ldcg(reinterpret_cast<const float2*>(a.ws_ml) + gbase + s2 * 256 + r_lo + rr)
+                          : make_float2(-INFINITY, 0.f);
+  }
+  for (int rr = threadIdx.x; rr < nr; rr += PP_THREADS) s_orow[rr] = a.rowof[q_row0 + r_lo + rr];
+  __syncthreads();
+  for (int rr = threadIdx.x; rr < nr; rr += PP_THREADS) {
+    float M = -INFINITY;
 #pragma unroll
-    for (int o = 4; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    const float wgt = (ml.x == -INFINITY) ? 0.f : exp2f(ml.x - M);
-    float L = wgt * ml.y;
+    for (int s2 = 0; s2 < 8; ++s2) M = fmaxf(M, s_ml[rr * 8 + s2].x);
+    float w[8], L = 0.f;
 #pragma unroll
-    for (int o = 4; o; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-    L = __shfl_sync(0xffffffffu, L, 0);            // lanes >= 8 reduced their own (empty) octet
-    float w8[8];                                   // split weights, broadcast to every lane
-#pragma unroll
-    for (int s2 = 0; s2 < 8; ++s2) w8[s2] = __shfl_sync(0xffffffffu, wgt, s2);
-    for (int c4 = lane; c4 < HD / 4; c4 += 32) {
-      float4 xs[8];
-#pragma unroll
-      for (int s2 = 0; s2 < 8; ++s2)
-        if (s2 < nsplit) xs[s2] = __ldcg(reinterpret_cast<const float4*>(a.ws_o + (pbase + s2 * 256) * HD) + c4);
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int s2 = 0; s2 < 8; ++s2) {
-        if (s2 >= nsplit) break;
-        const float w = w8[s2];
-        acc.x += w * xs[s2].x; acc.y += w * xs[s2].y; acc.z += w * xs[s2].z; acc.w += w * xs[s2].w;
-      }
-      const float inv = L > 0.f ? 1.0f / L : 0.f;
-      const int orow_i = a.rowof[q_row0 + rr], col = head * HD + c4 * 4;
-      const long off = a.pk_rows > 0 ? packed_off(orow_i, col, a.pk_rows, a.pk_kb) : (long)orow_i * a.ldo + col;
-      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.out) + off) =
-          make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
+    for (int s2 = 0; s2 < 8; ++s2) {
+      const float2 ml = s_ml[rr * 8 + s2];
+      w[s2] = ml.x == -INFINITY ? 0.f : exp2f(ml.x - M);
+      L += w[s2] * ml.y;
     }
+    const float inv = L > 0.f ? 1.0f / L : 0.f;
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2) s_w[rr * 8 + s2] = w[s2] * inv;
   }
   __syncthreads();
-  if (threadIdx.x == 0) adbg(6);
+  constexpr int C4 = HD / 4;
+  for (int t = threadIdx.x; t < nr * C4; t += PP_THREADS) {
+    const int rr = t / C4, c4 = t % C4;
+    const int row = r_lo + rr;                                   // row within the group's 256
+    const float4* src = reinterpret_cast<const float4*>(a.ws_o) + (gbase + row) * C4 + (c4 ^ (row & 7));
+    float4 xs[8];
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2)
+      if (s2 < nsplit) xs[s2] = __ldcg(src + (long)s2 * 256 * C4);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2) {
+      if (s2 >= nsplit) break;
+      const float w = s_w[rr * 8 + s2];
+      acc.x += w * xs[s2].x; acc.y += w * xs[s2].y; acc.z += w * xs[s2].z; acc.w += w * xs[s2].w;
+    }
+    const int orow_i = s_orow[rr], col = head * HD + c4 * 4;
+    const long off = a.pk_rows > 0 ? packed_off(orow_i, col, a.pk_rows, a.pk_kb) : (long)orow_i * a.ldo + col;
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.out) + off) =
+        make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) adbg(dbgp, 6);
   if (threadIdx.x == 0) {
     if (atomicAdd(&a.counters[a.ws_slots + group], 1) == nsplit - 1) {
       a.counters[group] = 0;
@@ -709,9 +869,9 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
 
 int g_attn_min_smem = 0;
 
-template <int HD, int KT>
+template <int HD, int KT, int VAR = 0>
 static cudaError_t launch_pp_hd(const vlc_attn_args& a, cudaStream_t stream, bool coop) {
-  using C = PPCfg<HD, KT>;
+  using C = PPCfg<HD, KT, (VAR & 0x1000) != 0>;
   CUtensorMap mq, mk, mv;
   // Q: {atom elems, rows, atoms} box {ATOM_E, 128, N_ATOMS}: one op = both swizzle atoms of a tile
   cudaError_t e = make_tmap_3d(&mq, a.q, C::ATOM_E, a.q_rows_cap, a.kv / C::ATOM_E, (uint64_t)a.kv * 2,
@@ -727,11 +887,12 @@ static cudaError_t launch_pp_hd(const vlc_attn_args& a, cudaStream_t stream, boo
   if (e != cudaSuccess) return e;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_pp_kernel<HD, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaFuncSetAttribute(attn_pp_kernel<HD, KT, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     attr = true;
   }
   const int smem = C::SMEM > g_attn_min_smem ? C::SMEM : g_attn_min_smem;
-  return launch_chain(attn_pp_kernel<HD, KT>, dim3(a.n_items), dim3(PP_THREADS), smem, stream, coop, mq, mk, mv, a);
+  return launch_chain(attn_pp_kernel<HD, KT, VAR>, dim3(a.n_items), dim3(PP_THREADS), smem, stream, coop, mq, mk, mv, a,
+                      h_attn_dbg, h_attn_trace);
 }
 
 cudaError_t launch_attention_pp(const vlc_attn_args& a, cudaStream_t stream, bool coop) {
@@ -740,7 +901,26 @@ cudaError_t launch_attention_pp(const vlc_attn_args& a, cudaStream_t stream, boo
     case 16: return launch_pp_hd<16, 64>(a, stream, coop);
     case 32: return launch_pp_hd<32, 64>(a, stream, coop);
     case 64: return launch_pp_hd<64, 64>(a, stream, coop);
-    case 128: return g_attn_kt == 128 ? launch_pp_hd<128, 128>(a, stream, coop) : launch_pp_hd<128, 64>(a, stream, coop);
+    case 128:
+      if (g_attn_kt == 64) return launch_pp_hd<128, 64>(a, stream, coop);
+      switch (g_attn_var) {
+        case 1: return launch_pp_hd<128, 128, 0x01>(a, stream, coop);
+        case 2: return launch_pp_hd<128, 128, 0x21>(a, stream, coop);
+        case 3: return launch_pp_hd<128, 128, 0x31>(a, stream, coop);
+        case 4: return launch_pp_hd<128, 128, 0x41>(a, stream, coop);
+        case 5: return launch_pp_hd<128, 128, 0x03>(a, stream, coop);
+        case 6: return launch_pp_hd<128, 128, 0x05>(a, stream, coop);
+        case 7: return launch_pp_hd<128, 128, 0x07>(a, stream, coop);
+        case 8: return launch_pp_hd<128, 128, 0x100>(a, stream, coop);
+        case 9: return launch_pp_hd<128, 128, 0x200>(a, stream, coop);
+        case 10: return launch_pp_hd<128, 128, 0x300>(a, stream, coop);
+        case 11: return launch_pp_hd<128, 128, 0x400>(a, stream, coop);
+        case 16: return launch_pp_hd<128, 128, 0x1000>(a, stream, coop);
+        case 17: return launch_pp_hd<128, 128, 0x1001>(a, stream, coop);
+        case 18: return launch_pp_hd<128, 128, 0x1100>(a, stream, coop);
+        case 19: return launch_pp_hd<128, 128, 0x1400>(a, stream, coop);
+        default: return launch_pp_hd<128, 128>(a, stream, coop);
+      }
     default: return cudaErrorInvalidValue;
   }
 }

@@ -36,6 +36,9 @@ struct SkSched {
   int KB;        // k-blocks per tile
   int m_tiles;
   int red;       // RESID split partials reduced with red.add (1) or through the ordered fix-up (0)
+  unsigned long long* dbg;   // phase timestamps (experiments; nullptr)
+  int mc;        // cluster size: k-block kb's activation block is loaded once, by CTA kb % mc of the
+                 // cluster, and multicast to all (1 = no cluster)
   __device__ __forceinline__ long long u0(int g) const { return U * g / G; }
   __device__ __forceinline__ int cta_of(long long u) const {
     int g = (int)((u * G) / U);
@@ -47,13 +50,13 @@ struct SkSched {
 
 constexpr int SK_MAX_PART = 8;  // participants per split tile
 
-__device__ unsigned long long* g_dbg = nullptr;  // phase timestamps (experiments only)
+static unsigned long long* h_dbg = nullptr;  // phase timestamps (experiments only; kernel parameter sk.dbg)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-#define DBG(slot) do { if (g_dbg) g_dbg[blockIdx.x * 8 + (slot)] = gtimer(); } while (0)
+#define DBG(slot) do { if (sk.dbg) sk.dbg[blockIdx.x * 8 + (slot)] = gtimer(); } while (0)
 
 // H = 1: 128 weight rows per tile, 128-wide k-blocks (two swizzle atoms), double-buffered TMEM
 //        accumulator.
@@ -98,7 +101,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     DBG(0);
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], sk.mc);   // every CTA of the cluster has consumed the stage
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&acc_full[s], 1);
@@ -108,9 +111,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  if (sk.mc > 1) cluster_sync_all();   // peers' barriers initialised before any multicast
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int crank = sk.mc > 1 ? (int)cluster_ctarank() : 0;
+  const uint16_t cmask = (uint16_t)((1u << sk.mc) - 1);
 
   // source of the weight half h of k-block kb of weight tile mt (PACKED layout, include/vlcache.h)
   auto a_src = [&](int mt, int kb, int h) -> const uint8_t* {
@@ -157,7 +163,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               bulk_load(sa + stage * a_bytes + h * (a_bytes / H), a_src(mt, kb, h), a_bytes / H, &full[stage],
                         pol_w);
           }
-          bulk_load(sb + stage * b_bytes, b_src(tt, kb), b_bytes, &full[stage], pol_x);
+          if (sk.mc == 1) {
+            bulk_load(sb + stage * b_bytes, b_src(tt, kb), b_bytes, &full[stage], pol_x);
+          } else if (kb % sk.mc == crank) {
+            // the stage is free in every CTA: the empty[stage] wait above counts all mc consumers
+            // (first ring pass: every stage is fresh)
+            bulk_load_mc(sb + stage * b_bytes, b_src(tt, kb), b_bytes, &full[stage], cmask, pol_x);
+          }
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
       }
@@ -201,7 +213,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               }
             }
           }
-          tc_commit(&empty[stage]);
+          if (sk.mc > 1) tc_commit_mc(&empty[stage], cmask);
+          else tc_commit(&empty[stage]);
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
         tc_commit(&acc_full[slot]);
@@ -319,11 +332,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
+  if (sk.mc > 1) cluster_sync_all();   // peers' last commits / multicasts target this CTA's smem
   if (threadIdx.x == 0) DBG(7);
 }
 
 int g_stage_override = 0;
-void set_debug_buffer(unsigned long long* p) { cudaMemcpyToSymbol(g_dbg, &p, sizeof(p)); }
+void set_debug_buffer(unsigned long long* p) { h_dbg = p; }
 
 int g_coop = 1;
 int g_pdl = 1;
@@ -332,6 +346,7 @@ int g_deterministic = 0;  // tuning key 13: 1 = RESID split-K partials through t
 int g_pair = 96;          // tuning key 10: CTA-pair GEMM for non-RESID kinds when n_tile >= this (0 = off)
 int g_unsplit_min = 64;   // tuning key 9: tile count from which each tile gets its own CTA (no split-K)
 int g_wide = 1;   // tuning key 7: 0 auto, 1 never use 256-row tiles (default: measured slower), 2 always
+int g_mc = 1;     // tuning key 16: cluster size of the one-tile-per-CTA schedule (multicast activations)
 
 static int gemm_pick_stages(int n_tile, int H) {
   if (g_stage_override > 0) return g_stage_override;
@@ -413,7 +428,12 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   }
   const int stages = gemm_pick_stages(n_tile, H);
   const int smem = gemm_smem_bytes(n_tile, stages, H);
-  SkSched sk{U, G, KB, m_tiles, red ? 1 : 0};
+  // cluster multicast of the activation blocks: one tile per CTA, all CTAs on one token tile
+  int mc = 1;
+  if (g_mc > 1 && H == 1 && tok_tiles == 1 && G == (int)tiles && tiles * KB == U && m_tiles % g_mc == 0 &&
+      !(rl && rl->n_blocks > 0) && KB >= g_mc)
+    mc = g_mc;
+  SkSched sk{U, G, KB, m_tiles, red ? 1 : 0, h_dbg, mc};
   const uint8_t* wpp = reinterpret_cast<const uint8_t*>(W);
   const uint8_t* xpp = reinterpret_cast<const uint8_t*>(X);
   RelocArgs rla{};
@@ -437,6 +457,9 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
       cudaFuncSetAttribute(gemm_bf16_tc<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);  \
       attr = true;                                                                                    \
     }                                                                                                 \
+    if (mc > 1)                                                                                       \
+      return launch_chain_cluster(gemm_bf16_tc<K, 1>, dim3(grid), dim3(GEMM_THREADS), smem, stream, mc, wpp, \
+                                  xpp, epi, sk, n_tile, stages, ws, counters, rla);                   \
     if (H == 2)                                                                                       \
       return launch_chain(gemm_bf16_tc<K, 2>, dim3(grid), dim3(GEMM_THREADS), smem, stream, g_coop != 0, wpp,    \
                           xpp, epi, sk, n_tile, stages, ws, counters, rla);                           \

@@ -22,6 +22,7 @@ enum EpiKind {
 using GemmEpi = vlc_epilogue;
 
 extern int g_stage_override;  // experiment knob (vlc_set_tuning key 1)
+extern int g_attn_var;        // key 15: softmax variant of the hd-128 attention kernel
 extern int g_attn_kt;         // key 12: key tile of the hd-128 attention kernel (64 / 128)
 extern int g_attn_min_smem;   // key 5: lower bound on the attention kernel's dynamic smem
 extern int g_coop;            // key 2: cooperative launch of the stream-K GEMM
@@ -30,6 +31,7 @@ extern int g_reloc_wide;      // key 14: idle-SM relocation variant (smem bytes 
 extern int g_pair;            // key 10: CTA-pair GEMM threshold on the token tile (0 = off)
 extern int g_unsplit_min;     // key 9: tiles >= this (and <= #SMs) -> one CTA per tile
 extern int g_wide;            // key 7: 256-row GEMM tiles (0 auto, 1 never, 2 always)
+extern int g_mc;              // key 16: GEMM cluster size for multicast activation loads (1 = off)
 extern int g_pdl;             // key 6: programmatic dependent launch of the chain kernels (default 1)
 void set_debug_buffer(unsigned long long* p);
 
@@ -54,6 +56,32 @@ cudaError_t launch_chain(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t s
     at[n].val.cooperative = 1;
     ++n;
   }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+// launch_chain with a thread-block cluster of `cluster` CTAs along x (PDL as above; no cooperative
+// attribute: clustered kernels do not rely on grid-wide co-residency)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_chain_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                 int cluster, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (g_pdl) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  at[n].id = cudaLaunchAttributeClusterDimension;
+  at[n].val.clusterDim.x = cluster;
+  at[n].val.clusterDim.y = 1;
+  at[n].val.clusterDim.z = 1;
+  ++n;
   cfg.attrs = at;
   cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);

@@ -290,6 +290,28 @@ def test_attention_pp_matches_torch(nat, hd, heads, nkeys, nq, causal):
     assert torch.equal(nat.unpack(outp, nq, kv, R), out)
 
 
+@pytest.mark.parametrize("var", [0, 1, 16, 17])
+@pytest.mark.parametrize("heads,nkeys,nq", [(28, 4128, 236), (2, 1000, 150), (4, 300, 300), (1, 4128, 600)])
+def test_attention_pp_softmax_variants(nat, var, heads, nkeys, nq):
+    """hd-128 / 128-key softmax variants (tuning key 15): three-input max, P staged in smem."""
+    nat.load().vlc_set_tuning(15, var)
+    try:
+        test_attention_pp_matches_torch(nat, 128, heads, nkeys, nq, True)
+    finally:
+        nat.load().vlc_set_tuning(15, 0)
+
+
+@pytest.mark.parametrize("mc", [2, 4])
+@pytest.mark.parametrize("n_pad,k_pad,m", [(10752, 3584, 236), (1024, 512, 100), (512, 1024, 40)])
+def test_gemm_cluster_multicast(nat, mc, n_pad, k_pad, m):
+    """Tuning key 16: clusters of mc CTAs share each activation k-block through one multicast copy."""
+    nat.load().vlc_set_tuning(16, mc)
+    try:
+        test_gemm_f32_matches_torch(nat, n_pad, k_pad, m, 0)
+    finally:
+        nat.load().vlc_set_tuning(16, 1)
+
+
 @pytest.fixture
 def gemm_mode(nat):
     yield lambda mode: nat.load().vlc_set_tuning(7, mode)

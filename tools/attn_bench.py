@@ -67,7 +67,40 @@ def run(max_ctas):
             print(f"   {nm:14s} min {col.min():7.2f} med {np.median(col):7.2f} max {col.max():7.2f}")
 
 
+def phases(var=11):
+    """VAR 0x400 (tuning 15 = 11): per-phase clock64 cycles summed over all CTAs (one thread per
+    query tile for the softmax phases, the MMA thread for its phases)."""
+    lib.vlc_set_tuning(15, var)
+    a, keep, n = setup(max_ctas=148)
+    s = torch.cuda.current_stream().cuda_stream
+    N.check(lib.vlc_attn_pp(a, s), "pp")
+    buf = torch.zeros(512, dtype=torch.int64, device="cuda")
+    lib.vlc_set_trace_buffer(buf.data_ptr())
+    N.check(lib.vlc_attn_pp(a, s), "pp")
+    torch.cuda.synchronize()
+    lib.vlc_set_trace_buffer(None)
+    b = buf.cpu().numpy()[256:]
+    names = ["wait_s", "tmem_ld", "mask_max", "rescale", "exp_pack", "st_arrive"]
+    for x in range(2):
+        it = max(int(b[x * 8 + 7]), 1)
+        print(f"softmax tile {'AB'[x]} ({it} iterations): " +
+              " ".join(f"{nm}={b[x * 8 + k] / it:.0f}" for k, nm in enumerate(names)), flush=True)
+    for x in range(2):
+        print(f"mma tile {'AB'[x]}: " + " ".join(f"{nm}={b[16 + x * 4 + k] / 140:.0f}"
+                                              for k, nm in enumerate(["wait_p", "issue_pv", "wait_kv_issue_s"])))
+    lib.vlc_set_tuning(15, 0)
+
+
 if __name__ == "__main__":
+  if len(sys.argv) > 1 and sys.argv[1] == "phases":
+    phases(int(sys.argv[2]) if len(sys.argv) > 2 else 11)
+    sys.exit(0)
+  if len(sys.argv) > 1 and sys.argv[1] == "vars":   # softmax variants of the 128-key kernel (key 15)
+    for v in [int(x) for x in sys.argv[2:]]:
+      lib.vlc_set_tuning(15, v)
+      print(f"== softmax variant {v}", flush=True)
+      run(148)
+    sys.exit(0)
   for kt in (64, 128):
     lib.vlc_set_tuning(12, kt)
     print(f"== key tile {kt}", flush=True)

@@ -91,16 +91,18 @@ __global__ void mma_probe(int n, int groups, int variant, unsigned long long* ou
     tc_commit(&bar);
     mbar_wait(&bar, (variant & 1) ? (groups & 1) : 0);
     long long t2 = clock64();
-    out[0] = t1 - t0;  // issue loop
-    out[1] = t2 - t0;  // until all MMAs complete
+    if (blockIdx.x == 0) {
+      out[0] = t1 - t0;  // issue loop
+      out[1] = t2 - t0;  // until all MMAs complete
+    }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tmem); }
 }
 
-extern "C" int probe_mma(int n, int groups, int variant, void* out, cudaStream_t s) {
-  cudaFuncSetAttribute(mma_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  mma_probe<<<1, 128, 100 * 1024, s>>>(n, groups, variant, (unsigned long long*)out);
+extern "C" int probe_mma(int n, int groups, int variant, void* out, cudaStream_t s, int ctas) {
+  cudaFuncSetAttribute(mma_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  mma_probe<<<ctas, 128, 200 * 1024, s>>>(n, groups, variant, (unsigned long long*)out);
   return (int)cudaGetLastError();
 }
