@@ -74,6 +74,16 @@ typedef struct vlc_epilogue {
   const float* add;  int ld_add;
   int pk_rows;       /* > 0: BF16 / SWIGLU output written PACKED (row tile pk_rows, pk_kb blocks) */
   int pk_kb;
+  /* RESID only, optional (norm_gamma = NULL: off): once every CTA's contribution to the fp32
+   * residual `out` has landed (grid barrier on `counters`), RMSNorm of its first norm_rows rows
+   * (model.py:257-259) -> norm_out, bf16 PACKED with row tile norm_pk_rows / norm_pk_kb blocks.
+   * Replaces the vlc_rmsnorm launch that would follow the projection.                    */
+  const float* norm_gamma;
+  void* norm_out;
+  float norm_eps;
+  int norm_rows;
+  int norm_pk_rows;
+  int norm_pk_kb;
 } vlc_epilogue;
 
 /* Mixed attention over cached + recomputed KV (engine.py:181-182, model.py:268-291).
@@ -151,7 +161,8 @@ int vlc_store_write_pages(const void* src, int src_f32, int layers, int tokens, 
  * Stream-K schedule over (128-row weight tile x token tile x 64-wide k-block) units on
  * max_ctas co-resident CTAs (0 = one per SM); tiles shared by several CTAs are reduced in
  * parallel through `ws` (>= ctas*8*128*256 floats) with `counters` (>= 2*ctas ints, zeroed
- * once; the kernel leaves them zeroed).  Replaces engine.py:176-178, 183-185, 187. */
+ * once; the kernel leaves them zeroed; >= 4098 ints when epi->norm_gamma is set: the fused norm's
+ * grid barrier uses counters[4096..4097]).  Replaces engine.py:176-178, 183-185, 187. */
 int vlc_gemm_bf16(const void* w, int n_pad, int k_pad, const void* x, int x_rows_cap,
                   int m_tokens, const vlc_epilogue* epi, int max_ctas, float* ws, size_t ws_bytes,
                   int* counters, cudaStream_t stream);

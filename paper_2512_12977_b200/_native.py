@@ -32,7 +32,9 @@ class Epilogue(C.Structure):
                 ("map1", C.c_void_p), ("map2", C.c_void_p), ("pos", C.c_void_p),
                 ("cos_tab", C.c_void_p), ("sin_tab", C.c_void_p), ("tab_ld", C.c_int),
                 ("hd", C.c_int), ("seg", C.c_int), ("bias", C.c_void_p), ("add", C.c_void_p),
-                ("ld_add", C.c_int), ("pk_rows", C.c_int), ("pk_kb", C.c_int)]
+                ("ld_add", C.c_int), ("pk_rows", C.c_int), ("pk_kb", C.c_int),
+                ("norm_gamma", C.c_void_p), ("norm_out", C.c_void_p), ("norm_eps", C.c_float),
+                ("norm_rows", C.c_int), ("norm_pk_rows", C.c_int), ("norm_pk_kb", C.c_int)]
 
 
 class AttnArgs(C.Structure):

@@ -341,10 +341,10 @@ __device__ __forceinline__ void adbg(unsigned long long* dbgp, int slot) {
   }
 }
 void set_attn_debug_buffer(unsigned long long* p) { h_attn_dbg = p; }
-__device__ __forceinline__ void atrace(unsigned long long* trc, int slot) {
+__device__ __forceinline__ void atrace(unsigned long long* trc, int slot) {   // SM clock (CTA 0 only)
   if (trc && blockIdx.x == 0) {
     unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
     trc[slot] = t;
   }
 }
@@ -382,11 +382,19 @@ struct PPCfg {
   static constexpr int KV_ATOM = KT * SWZ;
   // K/V ring as deep as shared memory allows (<= 8): the softmax warps wait on S, i.e. on K/V
   // loads, when the ring is shallow (ncu: s_full wait was the top stall at 3 stages)
-  static constexpr int ST_FIT = (232448 - 1024 - 320 - 2 * Q_BYTES - P_BYTES) / (2 * KV_BYTES);
-  static constexpr int ST = ST_FIT > 8 ? 8 : ST_FIT;
-  static constexpr int SMEM = 1024 + 2 * Q_BYTES + ST * 2 * KV_BYTES + P_BYTES + 320;
-  static_assert(ST * 2 * KV_BYTES >= 2 * 128 * HD * 4, "split partials are staged in the K/V ring");
-  static_assert(ST * 2 * KV_BYTES >= 256 * 8 * 12 + 256 * 4, "merge tables live in the K/V ring");
+  // Separate K and V rings: K(j) is consumed by S(j), a softmax ahead of PV(j), so K gets the
+  // extra stage (KT = 128: K 3 deep, V 2 deep) -- with one shared 2-deep ring the S issue waited
+  // on the HBM latency of K(j+1), loaded only once PV(j-1) had freed its slot.
+  static constexpr int BAR_BYTES = 512;
+  static constexpr int RING = 232448 - 1024 - BAR_BYTES - 2 * Q_BYTES - P_BYTES;
+  static constexpr int VST_FIT = RING / (2 * KV_BYTES);
+  static constexpr int VST = VST_FIT > 8 ? 8 : VST_FIT;
+  static constexpr int KST_FIT = (RING - VST * KV_BYTES) / KV_BYTES;
+  static constexpr int KST = KST_FIT > 8 ? 8 : KST_FIT;
+  static constexpr int SMEM = 1024 + 2 * Q_BYTES + (KST + VST) * KV_BYTES + P_BYTES + BAR_BYTES;
+  static_assert(VST >= 2 && KST >= VST, "K / V rings");
+  static_assert((KST + VST) * KV_BYTES >= 2 * 128 * HD * 4, "split partials are staged in the K/V ring");
+  static_assert((KST + VST) * KV_BYTES >= 256 * 8 * 12 + 256 * 4, "merge tables live in the K/V ring");
   // TMEM: S[x][buf] (KT fp32 cols; P bf16 pairs aliased in its first KT/2 cols), O[x] (HD cols)
   __device__ static constexpr uint32_t s_col(int x, int b) { return DB ? 64u * (2 * x + b) : 128u * x; }
   __device__ static constexpr uint32_t o_col(int x) { return 256u + (uint32_t)(HD > 64 ? HD : 64) * x; }
@@ -410,13 +418,15 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                                   // [2][Q_BYTES]
   uint8_t* sK = sQ + 2 * C::Q_BYTES;                    // [ST][KV_BYTES]
-  uint8_t* sV = sK + C::ST * C::KV_BYTES;               // [ST][KV_BYTES]
-  uint8_t* sP = sV + C::ST * C::KV_BYTES;               // [P_BYTES] (PSM)
+  uint8_t* sV = sK + C::KST * C::KV_BYTES;              // [VST][KV_BYTES]
+  uint8_t* sP = sV + C::VST * C::KV_BYTES;              // [P_BYTES] (PSM)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::P_BYTES);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;
-  uint64_t* kv_empty = kv_full + C::ST;
-  uint64_t* s_full = kv_empty + C::ST;   // [2 tiles][2 buffers]
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = k_full + C::KST;
+  uint64_t* v_full = k_empty + C::KST;
+  uint64_t* v_empty = v_full + C::VST;
+  uint64_t* s_full = v_empty + C::VST;   // [2 tiles][2 buffers]
   uint64_t* p_full = s_full + 4;         // [2 tiles][2 S buffers]: P(j) of tile x in buffer j&1
   uint64_t* o_done = p_full + 4;         // [2]
   uint64_t* all_done = o_done + 2;       // every MMA of the CTA complete (K/V ring reusable)
@@ -447,9 +457,13 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     tma_prefetch(&map_k);
     tma_prefetch(&map_v);
     mbar_init(q_full, 1);
-    for (int s = 0; s < C::ST; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+    for (int s = 0; s < C::KST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < C::VST; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
     }
     for (int x = 0; x < 4; ++x) mbar_init(&s_full[x], 1);
     for (int x = 0; x < 4; ++x) mbar_init(&p_full[x], 128);
@@ -479,14 +493,26 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       for (int x = 0; x < 2; ++x)   // one op per Q tile: 3-D view {atom elems, rows, atoms}
         if (nq_t[x] > 0)
           tma_load_3d(sQ + x * C::Q_BYTES, &map_q, q_full, 0, q_row0 + x * 128, head * C::N_ATOMS, pol_q);
-      for (int j = 0; j < nt; ++j) {
-        const int st = j % C::ST;
-        mbar_wait(&kv_empty[st], ((j / C::ST) & 1) ^ 1);
+      auto load_k = [&](int j) {   // one op per K / V tile: 4-D {elems, keys, atoms, layer}
+        const int st = j % C::KST;
+        mbar_wait(&k_empty[st], ((j / C::KST) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], C::KV_BYTES);
+        tma_load_4d(sK + st * C::KV_BYTES, &map_k, &k_full[st], 0, kv_row0 + kb + j * PP_KT, head * C::N_ATOMS,
+                    a.layer, pol_kv);
+      };
+      auto load_v = [&](int j) {
+        const int st = j % C::VST;
+        mbar_wait(&v_empty[st], ((j / C::VST) & 1) ^ 1);
         if (j < 32) atrace(trc, 128 + j);
-        mbar_expect_tx(&kv_full[st], 2 * C::KV_BYTES);
-        const int krow = kv_row0 + kb + j * PP_KT;   // one op per K / V tile: 4-D {elems, keys, atoms, layer}
-        tma_load_4d(sK + st * C::KV_BYTES, &map_k, &kv_full[st], 0, krow, head * C::N_ATOMS, a.layer, pol_kv);
-        tma_load_4d(sV + st * C::KV_BYTES, &map_v, &kv_full[st], 0, krow, head * C::N_ATOMS, a.layer, pol_kv);
+        mbar_expect_tx(&v_full[st], C::KV_BYTES);
+        tma_load_4d(sV + st * C::KV_BYTES, &map_v, &v_full[st], 0, kv_row0 + kb + j * PP_KT, head * C::N_ATOMS,
+                    a.layer, pol_kv);
+      };
+      // K runs KST-1 tiles ahead of V
+      for (int j = 0; j < C::KST - 1 && j < nt; ++j) load_k(j);
+      for (int j = 0; j < nt; ++j) {
+        if (j + C::KST - 1 < nt) load_k(j + C::KST - 1);
+        load_v(j);
       }
     }
   } else if (warp == 1) {
@@ -496,8 +522,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       mbar_wait(q_full, 0);
       adbg(dbgp, 1);
       auto issue_s = [&](int x, int j) {   // S[x][j&1] = Q_x K_j^T
-        const int st = j % C::ST;
-        mbar_wait(&kv_full[st], (j / C::ST) & 1);
+        const int st = j % C::KST;
+        mbar_wait(&k_full[st], (j / C::KST) & 1);
         tc_fence_after();
         const uint32_t q_addr = smem_u32(sQ + x * C::Q_BYTES);
         const uint32_t k_addr = smem_u32(sK + st * C::KV_BYTES);
@@ -512,7 +538,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         tc_commit(&s_full[2 * x + C::sbuf(j)]);
       };
       auto issue_pv = [&](int x, int j) {  // O_x += P_x(j) V_j, P from TMEM (aliased in S[x][j&1])
-        const int st = j % C::ST;
+        const int st = j % C::VST;
         const uint32_t v_addr = smem_u32(sV + st * C::KV_BYTES);
 #pragma unroll
         for (int k = 0; k < PP_KT / 16; ++k) {
@@ -528,6 +554,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         // written; P-buffer use u releases the buffer through p_free[u & 1]
         for (int x = 0; x < 2; ++x)
           if (0 < nt_t[x]) issue_s(x, 0);
+        tc_commit(&k_empty[0]);
         const uint32_t p_addr = smem_u32(sP);
         for (int j = 0; j < nt; ++j) {
           for (int x = 0; x < 2; ++x)
@@ -536,7 +563,10 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
               tc_fence_after();
               issue_s(x, j + 1);
             }
-          const int st = j % C::ST;
+          if (j + 1 < nt) tc_commit(&k_empty[(j + 1) % C::KST]);
+          const int st = j % C::VST;
+          mbar_wait(&v_full[st], (j / C::VST) & 1);
+          tc_fence_after();
           const uint32_t v_addr = smem_u32(sV + st * C::KV_BYTES);
           for (int x = 0; x < 2; ++x) {
             if (j >= nt_t[x]) continue;
@@ -551,7 +581,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
             tc_commit(&p_free[p_use(x, j) & 1]);
             tc_commit(&o_done[x]);
           }
-          tc_commit(&kv_empty[st]);
+          tc_commit(&v_empty[st]);
         }
         tc_commit(all_done);
         adbg(dbgp, 2);
@@ -560,10 +590,14 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       // tile ahead: S(j+1) is issued right after PV(j), which frees the single S/P buffer
       constexpr int AHEAD = C::DB ? 2 : 1;
       if (!PSM) {
-      for (int j = 0; j < AHEAD; ++j)
+      for (int j = 0; j < AHEAD; ++j) {
         for (int x = 0; x < 2; ++x)
           if (j < nt_t[x]) issue_s(x, j);
+        if (j < nt) tc_commit(&k_empty[j % C::KST]);
+      }
       for (int j = 0; j < nt; ++j) {
+        mbar_wait(&v_full[j % C::VST], (j / C::VST) & 1);
+        tc_fence_after();
         for (int x = 0; x < 2; ++x) {
           if (j >= nt_t[x]) continue;
           const bool ph = (VAR & 0x400) && trc;
@@ -578,7 +612,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
           PH(ph, 16 + x * 4 + 2, tph);
           if (j < 16) atrace(trc, 64 + j * 4 + 2 * x + 1);
         }
-        tc_commit(&kv_empty[j % C::ST]);
+        tc_commit(&v_empty[j % C::VST]);
+        if (j + AHEAD < nt) tc_commit(&k_empty[(j + AHEAD) % C::KST]);
       }
       tc_commit(all_done);
       adbg(dbgp, 2);
@@ -679,6 +714,19 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       const float nm = any ? -m_run : NEG_INF;     // all-masked row: every p = exp2(-inf) = 0
       // P packed in place into s[0, KT/2) (slot i is free once pairs 2i, 2i+1 are read)
       float ls4[4] = {0.f, 0.f, 0.f, 0.f};
+      if constexpr ((VAR & 0x2000) != 0) {     // packed-pair FFMA2 / FADD2
+        const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nm2 = make_float2(nm, nm);
+        float2 l2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int i = 0; i < PP_KT / 2; ++i) {
+          const float2 xx = ffma2(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2);
+          const float2 pp = make_float2(fast_exp2(xx.x), fast_exp2(xx.y));
+          l2[i & 3] = fadd2(l2[i & 3], pp);
+          s[i] = __uint_as_float(pack_bf16(pp.x, pp.y));
+        }
+        const float2 la = fadd2(l2[0], l2[1]), lb = fadd2(l2[2], l2[3]);
+        ls4[0] = la.x; ls4[1] = la.y; ls4[2] = lb.x; ls4[3] = lb.y;
+      } else
 #pragma unroll
       for (int i = 0; i < PP_KT / 2; ++i) {
         // POLY of every 8 pairs on the FMA pipe, the rest on the MUFU (both pipes busy)
@@ -915,6 +963,8 @@ cudaError_t launch_attention_pp(const vlc_attn_args& a, cudaStream_t stream, boo
         case 9: return launch_pp_hd<128, 128, 0x200>(a, stream, coop);
         case 10: return launch_pp_hd<128, 128, 0x300>(a, stream, coop);
         case 11: return launch_pp_hd<128, 128, 0x400>(a, stream, coop);
+        case 20: return launch_pp_hd<128, 128, 0x2001>(a, stream, coop);
+        case 21: return launch_pp_hd<128, 128, 0x2401>(a, stream, coop);
         case 16: return launch_pp_hd<128, 128, 0x1000>(a, stream, coop);
         case 17: return launch_pp_hd<128, 128, 0x1001>(a, stream, coop);
         case 18: return launch_pp_hd<128, 128, 0x1100>(a, stream, coop);

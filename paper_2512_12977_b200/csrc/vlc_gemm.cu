@@ -64,6 +64,70 @@ __device__ __forceinline__ unsigned long long gtimer() {
 //        k-blocks: the activation bytes per weight byte halve, which keeps the L2 traffic of
 //        c ~ 240-token GEMMs under the LTS cap.  Single accumulator of 2 x n_tile columns.
 // The A (weight) bytes of a stage are 32 KB in both cases.
+// Grid-wide barrier of the first G CTAs (all co-resident: <= 1 CTA per SM, G <= #SMs).
+// cnt / gen: two ints of the counters buffer; the last arriver resets cnt and bumps gen.
+__device__ __forceinline__ void grid_barrier(int* cnt, int* gen, int G) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile int* vg = gen;
+    const int g0 = *vg;
+    __threadfence();
+    if (atomicAdd(cnt, 1) == G - 1) {
+      *cnt = 0;
+      __threadfence();
+      atomicAdd(gen, 1);
+    } else {
+      while (*vg == g0) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+constexpr int NORM_BAR = 4096;   // counters[NORM_BAR], [NORM_BAR + 1]: the fused-norm grid barrier
+
+// RMSNorm of residual rows g, g + G, ... (< epi.norm_rows) -> packed bf16 (model.py:257-259;
+// same arithmetic as rmsnorm_kernel: y = (x / sqrt(mean(x^2) + eps)) * gamma).  All GEMM_THREADS
+// threads; the residual is read from L2 (__ldcg: the red.add results live there).
+// red: GEMM_THREADS / 32 floats of (dynamic) shared memory -- a static array would push the
+// kernel past the 227 KB per-block limit its dynamic-smem attribute is set to.
+__device__ __forceinline__ void fused_norm_rows(const GemmEpi& epi, int g, int G, float* red) {
+  constexpr int NV = 8;   // float4 per thread: d <= 8 * 4 * GEMM_THREADS
+  const int d = epi.n_valid, n4 = d >> 2;
+  const float4* g4 = reinterpret_cast<const float4*>(epi.norm_gamma);
+  for (int row = g; row < epi.norm_rows; row += G) {
+    const float4* xr = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(epi.out) + (long)row * epi.ldo);
+    float4 v[NV], gg[NV];
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int i = threadIdx.x + GEMM_THREADS * k;
+      v[k] = i < n4 ? __ldcg(xr + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      gg[k] = i < n4 ? __ldg(g4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < GEMM_THREADS / 32; ++w) tot += red[w];
+    const float denom = sqrtf(tot / (float)d + epi.norm_eps);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int i = threadIdx.x + GEMM_THREADS * k;
+      if (i >= n4) break;
+      const uint2 pk = make_uint2(pack_bf16((v[k].x / denom) * gg[k].x, (v[k].y / denom) * gg[k].y),
+                                  pack_bf16((v[k].z / denom) * gg[k].z, (v[k].w / denom) * gg[k].w));
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(epi.norm_out) +
+                                packed_off(row, 4 * i, epi.norm_pk_rows, epi.norm_pk_kb)) = pk;
+    }
+    __syncthreads();   // red[] reused by the next row
+  }
+}
+
 template <int KIND, int H>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc(const uint8_t* __restrict__ wp, const uint8_t* __restrict__ xp, GemmEpi epi, SkSched sk,
@@ -333,6 +397,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tmem_dealloc<512>(tmem);
   }
   if (sk.mc > 1) cluster_sync_all();   // peers' last commits / multicasts target this CTA's smem
+  if constexpr (KIND == EPI_RESID) {
+    if (epi.norm_gamma != nullptr) {     // every residual update of every CTA lands, then the norm
+      __threadfence();
+      grid_barrier(counters + NORM_BAR, counters + NORM_BAR + 1, sk.G);
+      fused_norm_rows(epi, g, sk.G, stage_all);   // epilogue staging tile: free by now
+    }
+  }
   if (threadIdx.x == 0) DBG(7);
 }
 
@@ -385,6 +456,10 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
                         int m_tokens, const GemmEpi& epi, int max_ctas, float* ws, size_t ws_bytes,
                         int* counters, cudaStream_t stream, const RelocArgs* rl) {
   if (m_tokens <= 0) return cudaSuccess;
+  if (epi.norm_gamma != nullptr &&
+      (epi.kind != EPI_RESID || counters == nullptr || epi.n_valid % 4 != 0 || epi.n_valid > 32 * GEMM_THREADS ||
+       epi.norm_pk_rows <= 0 || epi.norm_rows > epi.m_tokens || epi.norm_rows < 0))
+    return cudaErrorInvalidValue;
   const int n_tile = gemm_row_tile(m_tokens);
   // token-heavy non-residual GEMMs: CTA-pair kernel (halves the activation bytes per SM)
   // (multi-wave GEMMs only -- the LM head: measured 7% faster there, no gain at <= 1 wave)

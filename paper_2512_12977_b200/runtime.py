@@ -18,7 +18,13 @@ N_SMS = 148
 _DEBUG_SYNC = bool(int(__import__("os").environ.get("VLC_DEBUG_SYNC", "0")))  # sync + log every launch
 _OVERLAP_RELOC = bool(int(__import__("os").environ.get("VLC_RELOC_OVERLAP", "1")))
 _FUSE_RELOC = bool(int(__import__("os").environ.get("VLC_RELOC_FUSED", "0")))
+# RMSNorm fused into the preceding residual projection's tail (vlc_epilogue.norm_*): one launch
+# per norm less (VLC_FUSED_NORM=1; measured neutral on C3: the norm stays on the critical path
+# either way, so the separate vlc_rmsnorm launches are the default)
+_FUSED_NORM = bool(int(__import__("os").environ.get("VLC_FUSED_NORM", "0")))
 _SKIP_RELOC_EXPERIMENT = bool(int(__import__("os").environ.get("VLC_EXPERIMENT_SKIP_RELOC", "0")))
+# timing experiments only (wrong results): kernel names (Runner._run) not launched at all
+_SKIP_EXPERIMENT = {k for k in __import__("os").environ.get("VLC_EXPERIMENT_SKIP", "").split(",") if k}
 
 
 def _torch():
@@ -174,6 +180,8 @@ class Runner:
 
     def _run(self, name, fn, nbytes=0, flops=0, kernels=1):
         """Issue one C-ABI call; optionally bracket it with CUDA events on the current stream."""
+        if name in _SKIP_EXPERIMENT:
+            return
         if _DEBUG_SYNC:
             import sys
             import time
@@ -533,11 +541,21 @@ class Runner:
                     side_ev.append(ev)
         elif nb:
             relocate(0, nb)
+        fuse_norm = _FUSED_NORM
+
+        def norm_kw(gamma, rows):
+            """RESID epilogue fields: RMSNorm of the first `rows` residual rows fused into the GEMM."""
+            if not fuse_norm or rows <= 0:
+                return {}
+            return dict(norm_gamma=gamma.data_ptr(), norm_out=xn.data_ptr(), norm_eps=RMS_EPS, norm_rows=rows,
+                        norm_pk_rows=N.row_tile(rows), norm_pk_kb=dw.kd // 128)
+        normed = False                     # xn already holds this layer's attn-normed rows
         for i in range(L):
             ci = int(c[i])
             W = dw.layers[i]
             Ri = N.row_tile(ci)
-            self.rmsnorm(x, W["attn_norm"], xn, ci, pk=(Ri, dw.kd // 128))
+            if not normed:
+                self.rmsnorm(x, W["attn_norm"], xn, ci, pk=(Ri, dw.kd // 128))
             self.gemm(W["wqkv"], dw.kd, xn, ci, _epi(
                 kind=N.EPI_QKV_ROPE, n_valid=3 * kv, out=q.data_ptr(), ldo=kv,
                 out2=kc[i].data_ptr(), ld2=kv, out3=vc[i].data_ptr(), ld3=kv, out4=kpre[i].data_ptr(), ld4=kv,
@@ -570,9 +588,11 @@ class Runner:
                     x.data_ptr(), d, cap.data_ptr(), d, W["mlp_norm"].data_ptr(), xn.data_ptr(), d, ci, d, RMS_EPS,
                     Ri, dw.kd // 128, _stream()), "vlc_add_rmsnorm"))
             elif self.tp_group is None:
-                self.gemm(W["wo"], dw.kkv, att, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d),
-                          name="gemm_o", k_valid=kv)
-                self.rmsnorm(x, W["mlp_norm"], xn, ci, pk=(Ri, dw.kd // 128))
+                nk = norm_kw(W["mlp_norm"], ci)
+                self.gemm(W["wo"], dw.kkv, att, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d,
+                                                         **nk), name="gemm_o", k_valid=kv)
+                if not nk:
+                    self.rmsnorm(x, W["mlp_norm"], xn, ci, pk=(Ri, dw.kd // 128))
             else:
                 # head-parallel: row-parallel O projection of this rank's heads -> y, one all-reduce
                 # of y over the group (NCCL / NVLink), then x += y fused into the MLP norm
@@ -588,8 +608,11 @@ class Runner:
                       _epi(kind=N.EPI_SWIGLU, n_valid=2 * cfg.mlp_hidden, out=hb.data_ptr(), ldo=dw.kh,
                            pk_rows=Ri, pk_kb=dw.kh // 128),
                       name="gemm_gate_up", k_valid=d)
-            self.gemm(W["wd"], dw.kh, hb, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d),
+            # the next layer's attention norm rides on this projection (its rows: the first c[i+1])
+            nk = norm_kw(dw.layers[i + 1]["attn_norm"], int(c[i + 1])) if i + 1 < L else {}
+            self.gemm(W["wd"], dw.kh, hb, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d, **nk),
                       name="gemm_down", k_valid=cfg.mlp_hidden)
+            normed = bool(nk)
         if side_ev is not None:
             _torch().cuda.current_stream().wait_stream(self._side)
         self.rmsnorm(x, dw.final_norm, xn, cL, row_map=pack.ptr("final"), pk=(N.row_tile(cL), dw.kd // 128))

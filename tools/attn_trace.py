@@ -16,8 +16,8 @@ torch.cuda.synchronize()
 ab.lib.vlc_set_trace_buffer(None)
 t = buf.cpu().numpy().astype(np.float64)
 t0 = t[t > 0].min()
-us = np.where(t > 0, (t - t0) / 1e3, np.nan)
-print("iter | softmaxA: s_ready ld_done exp_done arrived | MMA: pA_ok A_issued pB_ok B_issued | load_go | "
+us = np.where(t > 0, (t - t0) / 1e3, np.nan)   # k-cycles of SM clock
+print("(k-cycles)\niter | softmaxA: s_ready ld_done exp_done arrived | MMA: pA_ok A_issued pB_ok B_issued | load_go | "
       "softmaxB: s_ready ld_done exp_done arrived")
 for j in range(16):
     sa = us[j * 4:j * 4 + 4]
