@@ -329,6 +329,16 @@ static cudaError_t launch_attn_hd(const vlc_attn_args& a, cudaStream_t stream) {
 // tensor core works on the other group's S / PV.  TMEM: S_A, S_B (64 cols fp32), P_A, P_B
 // (32 cols of packed bf16 pairs, the A operand of the PV MMA), O_A, O_B (HD cols fp32).
 constexpr int PP_THREADS = 320;
+// Softmax warps per (query tile, TMEM row quadrant): SW = 1 -> one thread per query row and all KT
+// columns (10 warps); SW = 2 (VAR 0x4000) -> two threads per row, KT/2 columns each, row max
+// exchanged through shared memory (20 warps: 2 control + 16 softmax + 2 idle = 5 per scheduler,
+// so the per-scheduler register file allows 96 registers per thread).
+template <int VAR>
+struct PPRoles {
+  static constexpr int SW = (VAR & 0x4000) ? 2 : 1;
+  static constexpr int THREADS = SW == 1 ? PP_THREADS : 640;
+  static constexpr int XM_BYTES = SW == 1 ? 0 : 2 * 2 * 2 * 128 * 4;   // [parity][tile][half][row]
+};
 // Experiment instrumentation.  The buffers travel as kernel parameters (constant bank), so a
 // disabled trace costs a predicated branch, not a global load on the softmax critical path.
 static unsigned long long* h_attn_dbg = nullptr;    // per-CTA phase timestamps
@@ -364,9 +374,10 @@ __device__ __forceinline__ long long clk() { long long c; asm volatile("mov.u64 
 // columns), half the MMA instructions and barrier round trips per key; the ping-pong between
 // the two query tiles hides the S(j) -> softmax -> PV(j) -> S(j+1) chain of each tile.
 int g_attn_kt = 128;   // tuning key 12: key tile of the hd-128 kernel (64 or 128)
-int g_attn_var = 0;    // tuning key 15: softmax variant of the hd-128 / 128-key kernel (see VAR below)
+int g_attn_var = 0;    // tuning key 15: softmax variant of the hd-128 / 128-key kernel (see VAR below;
+                       // 0 = default two-threads-per-row kernel, 100 = one thread per row)
 
-template <int HD, int KT, bool PSM_ = false>
+template <int HD, int KT, bool PSM_ = false, int XM_BYTES = 0>
 struct PPCfg {
   static constexpr bool DB = KT == 64;
   // PSM: P staged in shared memory (SS MMA for PV) instead of aliased over S in TMEM, so S(j+1)
@@ -386,12 +397,12 @@ struct PPCfg {
   // extra stage (KT = 128: K 3 deep, V 2 deep) -- with one shared 2-deep ring the S issue waited
   // on the HBM latency of K(j+1), loaded only once PV(j-1) had freed its slot.
   static constexpr int BAR_BYTES = 512;
-  static constexpr int RING = 232448 - 1024 - BAR_BYTES - 2 * Q_BYTES - P_BYTES;
+  static constexpr int RING = 232448 - 1024 - BAR_BYTES - 2 * Q_BYTES - P_BYTES - XM_BYTES;
   static constexpr int VST_FIT = RING / (2 * KV_BYTES);
   static constexpr int VST = VST_FIT > 8 ? 8 : VST_FIT;
   static constexpr int KST_FIT = (RING - VST * KV_BYTES) / KV_BYTES;
   static constexpr int KST = KST_FIT > 8 ? 8 : KST_FIT;
-  static constexpr int SMEM = 1024 + 2 * Q_BYTES + (KST + VST) * KV_BYTES + P_BYTES + BAR_BYTES;
+  static constexpr int SMEM = 1024 + 2 * Q_BYTES + (KST + VST) * KV_BYTES + P_BYTES + XM_BYTES + BAR_BYTES;
   static_assert(VST >= 2 && KST >= VST, "K / V rings");
   static_assert((KST + VST) * KV_BYTES >= 2 * 128 * HD * 4, "split partials are staged in the K/V ring");
   static_assert((KST + VST) * KV_BYTES >= 256 * 8 * 12 + 256 * 4, "merge tables live in the K/V ring");
@@ -406,12 +417,16 @@ struct PPCfg {
 // exponentials run as poly_exp2 on the FMA pipe; bits 1 / 2 = timing experiments only (no exp2 /
 // no O rescale: wrong results).
 template <int HD, int KT, int VAR = 0>
-__global__ void __launch_bounds__(PP_THREADS, 1)
+__global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
     attn_pp_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                    const __grid_constant__ CUtensorMap map_v, vlc_attn_args a, unsigned long long* dbgp,
                    unsigned long long* trc) {
-  using C = PPCfg<HD, KT, (VAR & 0x1000) != 0>;
+  using R = PPRoles<VAR>;
+  using C = PPCfg<HD, KT, (VAR & 0x1000) != 0, R::XM_BYTES>;
   constexpr bool PSM = C::PSM;
+  constexpr int SW = R::SW, NTH = R::THREADS;
+  static_assert(!(PSM && SW == 2), "P-in-smem is a one-warp-per-row variant");
+  static_assert(SW == 1 || KT == 128, "two threads per row: 128-key tiles");
   constexpr int PP_KT = KT;
   constexpr int POLY = (VAR >> 4) & 7;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -420,7 +435,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   uint8_t* sK = sQ + 2 * C::Q_BYTES;                    // [ST][KV_BYTES]
   uint8_t* sV = sK + C::KST * C::KV_BYTES;              // [VST][KV_BYTES]
   uint8_t* sP = sV + C::VST * C::KV_BYTES;              // [P_BYTES] (PSM)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::P_BYTES);
+  float* xm = reinterpret_cast<float*>(sP + C::P_BYTES);  // [XM_BYTES] (SW = 2) row-max exchange
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::P_BYTES + R::XM_BYTES);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;
   uint64_t* k_empty = k_full + C::KST;
@@ -466,7 +482,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       mbar_init(&v_empty[s], 1);
     }
     for (int x = 0; x < 4; ++x) mbar_init(&s_full[x], 1);
-    for (int x = 0; x < 4; ++x) mbar_init(&p_full[x], 128);
+    for (int x = 0; x < 4; ++x) mbar_init(&p_full[x], 128 * SW);
     for (int x = 0; x < 2; ++x) {
       mbar_init(&o_done[x], 1);
     }
@@ -620,9 +636,11 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       }
     }
     __syncwarp();
-  } else {
-    // ---------------- softmax groups: warps 2-5 -> tile A, warps 6-9 -> tile B
-    const int x = (warp - 2) >> 2;
+  } else if (warp < 2 + 8 * SW) {
+    // ---------------- softmax groups: warps 2.. -> tile A, then tile B (SW warps per quadrant)
+    const int x = (warp - 2) / (4 * SW);
+    const int hh = SW == 1 ? 0 : ((warp - 2) >> 2) & 1;   // column half of the row
+    constexpr int CW = KT / SW, OW = HD / SW;              // S / O columns of this thread
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
     const bool q_valid = r < nq_t[x];
@@ -635,8 +653,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     for (int j = 0; j < ntx; ++j) {
       const int k0 = kb + j * PP_KT;
       const uint32_t tS = tmem + C::s_col(x, C::sbuf(j)) + lane_off;
-      float s[PP_KT];
-      const bool ph = (VAR & 0x400) && r == 0 && trc;
+      float s[CW];
+      const bool ph = (VAR & 0x400) && r == 0 && hh == 0 && trc;
       long long tph = ph ? clk() : 0;
       mbar_wait(&s_full[2 * x + C::sbuf(j)], C::sphase(j));
       tc_fence_after();
@@ -647,10 +665,10 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         mbar_arrive(&p_full[2 * x + C::sbuf(j)]);
         continue;
       }
-      const bool tr = trc && r == 0 && j < 16;
+      const bool tr = trc && r == 0 && hh == 0 && j < 16;
       if (tr) atrace(trc, (x ? 160 : 0) + j * 4);
 #pragma unroll
-      for (int c = 0; c < PP_KT / 32; ++c) tmem_ld32(tS + 32 * c, s + 32 * c);
+      for (int c = 0; c < CW / 32; ++c) tmem_ld32(tS + hh * CW + 32 * c, s + 32 * c);
       tmem_wait_ld();
       if (PSM) {                                  // S(j) is in registers: S(j+1) may overwrite it
         tc_fence_before();
@@ -660,20 +678,31 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       if (tr) atrace(trc, (x ? 160 : 0) + j * 4 + 1);
       // scores stay raw (scale folded into the exp2 FFMA); masked keys -> -inf; reductions in
       // 4 independent chains (only 2 softmax warps per scheduler: latency, not issue, binds)
-      const int lim = min(qp, ke - 1) - k0;
-      if (lim < PP_KT - 1) {
+      const int lim = min(qp, ke - 1) - k0 - hh * CW;
+      if (lim < CW - 1) {
 #pragma unroll
-        for (int i = 0; i < PP_KT; ++i) s[i] = (i <= lim) ? s[i] : NEG_INF;
+        for (int i = 0; i < CW; ++i) s[i] = (i <= lim) ? s[i] : NEG_INF;
       }
       float mx4[4] = {NEG_INF, NEG_INF, NEG_INF, NEG_INF};
       if (VAR & 1) {
 #pragma unroll
-        for (int i = 0; i < PP_KT; i += 2) mx4[(i >> 1) & 3] = fmax3(mx4[(i >> 1) & 3], s[i], s[i + 1]);
+        for (int i = 0; i < CW; i += 2) mx4[(i >> 1) & 3] = fmax3(mx4[(i >> 1) & 3], s[i], s[i + 1]);
       } else {
 #pragma unroll
-        for (int i = 0; i < PP_KT; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], s[i]);
+        for (int i = 0; i < CW; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], s[i]);
       }
-      const float tmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * a.scale_log2;
+      float pmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      if constexpr (SW == 2) {
+        // the other half-row's max; the barrier also orders both halves' S reads before any P
+        // write into S's columns (P of the upper half lands in the lower half's S columns)
+        float* xb = xm + ((j & 1) * 2 + x) * 256;
+        xb[hh * 128 + r] = pmax;
+        tc_fence_before();
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + x), "r"(256) : "memory");
+        tc_fence_after();
+        pmax = fmaxf(pmax, xb[(1 - hh) * 128 + r]);
+      }
+      const float tmax = pmax * a.scale_log2;
       const float m_new = fmaxf(m_run, tmax);
       const bool need = m_new > m_run + 8.0f;
       const bool has_o = m_run != NEG_INF;
@@ -695,13 +724,13 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       if (resc) {
         const float sc = (need && has_o) ? fast_exp2(m_run - m_new) : 1.0f;
 #pragma unroll
-        for (int c = 0; c < HD / 16; ++c) {
+        for (int c = 0; c < OW / 16; ++c) {
           float o[16];
-          tmem_ld16(tO + c * 16, o);
+          tmem_ld16(tO + hh * OW + c * 16, o);
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 16; ++i) o[i] *= sc;
-          tmem_st16(tO + c * 16, o);
+          tmem_st16(tO + hh * OW + c * 16, o);
         }
         tmem_wait_st();
       }
@@ -718,7 +747,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nm2 = make_float2(nm, nm);
         float2 l2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-        for (int i = 0; i < PP_KT / 2; ++i) {
+        for (int i = 0; i < CW / 2; ++i) {
           const float2 xx = ffma2(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2);
           const float2 pp = make_float2(fast_exp2(xx.x), fast_exp2(xx.y));
           l2[i & 3] = fadd2(l2[i & 3], pp);
@@ -728,7 +757,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         ls4[0] = la.x; ls4[1] = la.y; ls4[2] = lb.x; ls4[3] = lb.y;
       } else
 #pragma unroll
-      for (int i = 0; i < PP_KT / 2; ++i) {
+      for (int i = 0; i < CW / 2; ++i) {
         // POLY of every 8 pairs on the FMA pipe, the rest on the MUFU (both pipes busy)
         const float x0 = fmaf(s[2 * i], a.scale_log2, nm), x1 = fmaf(s[2 * i + 1], a.scale_log2, nm);
         float p0, p1;
@@ -761,7 +790,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         mbar_arrive(&p_full[2 * x]);
       } else {
 #pragma unroll
-        for (int c = 0; c < PP_KT / 64; ++c) tmem_st32f(tS + 32 * c, s + 32 * c);   // P(j) over S(j)'s first cols
+        for (int c = 0; c < CW / 64; ++c) tmem_st32f(tS + hh * (CW / 2) + 32 * c, s + 32 * c);   // P(j) over S(j)'s first cols
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_full[2 * x + C::sbuf(j)]);   // per-buffer barrier: softmax may run a tile ahead
@@ -774,17 +803,23 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       mbar_wait(&o_done[x], (ntx - 1) & 1);
       tc_fence_after();
     }
-    if (r == 0) adbg(dbgp, 3 + x);
+    if constexpr (SW == 2) {   // row sum = both halves' sums (exchange buffer of iteration ntx: free)
+      float* xb = xm + ((ntx & 1) * 2 + x) * 256;
+      xb[hh * 128 + r] = l_run;
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + x), "r"(256) : "memory");
+      l_run += xb[(1 - hh) * 128 + r];
+    }
+    if (r == 0 && hh == 0) adbg(dbgp, 3 + x);
     const int qrow = q_row0 + x * 128 + r;
     if (group < 0) {
       const float inv = (l_run > 0.f) ? 1.0f / l_run : 0.f;
       const int orow_i = q_valid ? a.rowof[qrow] : 0;
       __nv_bfloat16* obase = reinterpret_cast<__nv_bfloat16*>(a.out);
 #pragma unroll
-      for (int c = 0; c < HD / 16; ++c) {
+      for (int c = 0; c < OW / 16; ++c) {
         float o[16];
         if (ntx > 0) {
-          tmem_ld16(tO + c * 16, o);
+          tmem_ld16(tO + hh * OW + c * 16, o);
           tmem_wait_ld();
         } else {
 #pragma unroll
@@ -794,7 +829,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
           uint32_t pkk[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q) pkk[q] = pack_bf16(o[2 * q] * inv, o[2 * q + 1] * inv);
-          const int col = head * HD + c * 16;
+          const int col = head * HD + hh * OW + c * 16;
           const long o0 = a.pk_rows > 0 ? packed_off(orow_i, col, a.pk_rows, a.pk_kb) : (long)orow_i * a.ldo + col;
           const long o1 = a.pk_rows > 0 ? packed_off(orow_i, col + 8, a.pk_rows, a.pk_kb) : o0 + 8;
           *reinterpret_cast<uint4*>(obase + o0) = make_uint4(pkk[0], pkk[1], pkk[2], pkk[3]);
@@ -812,26 +847,27 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         tc_fence_after();
         float4* stg = reinterpret_cast<float4*>(sK) + x * 128 * (HD / 4) + r * (HD / 4);
 #pragma unroll
-        for (int c = 0; c < HD / 16; ++c) {
+        for (int c = 0; c < OW / 16; ++c) {
           float o[16];
           if (ntx > 0) {
-            tmem_ld16(tO + c * 16, o);
+            tmem_ld16(tO + hh * OW + c * 16, o);
             tmem_wait_ld();
           } else {
 #pragma unroll
             for (int i = 0; i < 16; ++i) o[i] = 0.f;
           }
+          const int c4 = (hh * OW / 16 + c) * 4;
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            stg[(c * 4 + q) ^ (r & 7)] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+            stg[(c4 + q) ^ (r & 7)] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
         }
         fence_proxy_async_smem();
-        asm volatile("bar.sync %0, 128;" ::"r"(1 + x) : "memory");
-        if (quad == 0 && lane == 0 && nq_t[x] > 0)
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + x), "r"(128 * SW) : "memory");
+        if (quad == 0 && lane == 0 && hh == 0 && nq_t[x] > 0)
           bulk_store_wait(a.ws_o + prow0 * HD, reinterpret_cast<float4*>(sK) + x * 128 * (HD / 4),
                           (uint32_t)(nq_t[x] * HD * 4));
       }
-      if (q_valid) __stcg(reinterpret_cast<float2*>(a.ws_ml) + prow0 + r, make_float2(m_run, l_run));
+      if (q_valid && hh == 0) __stcg(reinterpret_cast<float2*>(a.ws_ml) + prow0 + r, make_float2(m_run, l_run));
       __threadfence();
     }
   }
@@ -861,14 +897,14 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   float* s_w = reinterpret_cast<float*>(s_ml + 256 * 8);        // [nr][8] weight / L
   int* s_orow = reinterpret_cast<int*>(s_w + 256 * 8);          // [nr]
   const long gbase = (long)group * 8 * 256;
-  for (int t = threadIdx.x; t < nr * 8; t += PP_THREADS) {
+  for (int t = threadIdx.x; t < nr * 8; t += NTH) {
     const int rr = t >> 3, s2 = t & 7;
     s_ml[t] = s2 < nsplit ? __ldcg(reinterpret_cast<const float2*>(a.ws_ml) + gbase + s2 * 256 + r_lo + rr)
                           : make_float2(-INFINITY, 0.f);
   }
-  for (int rr = threadIdx.x; rr < nr; rr += PP_THREADS) s_orow[rr] = a.rowof[q_row0 + r_lo + rr];
+  for (int rr = threadIdx.x; rr < nr; rr += NTH) s_orow[rr] = a.rowof[q_row0 + r_lo + rr];
   __syncthreads();
-  for (int rr = threadIdx.x; rr < nr; rr += PP_THREADS) {
+  for (int rr = threadIdx.x; rr < nr; rr += NTH) {
     float M = -INFINITY;
 #pragma unroll
     for (int s2 = 0; s2 < 8; ++s2) M = fmaxf(M, s_ml[rr * 8 + s2].x);
@@ -885,7 +921,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   }
   __syncthreads();
   constexpr int C4 = HD / 4;
-  for (int t = threadIdx.x; t < nr * C4; t += PP_THREADS) {
+  for (int t = threadIdx.x; t < nr * C4; t += NTH) {
     const int rr = t / C4, c4 = t % C4;
     const int row = r_lo + rr;                                   // row within the group's 256
     const float4* src = reinterpret_cast<const float4*>(a.ws_o) + (gbase + row) * C4 + (c4 ^ (row & 7));
@@ -919,7 +955,7 @@ int g_attn_min_smem = 0;
 
 template <int HD, int KT, int VAR = 0>
 static cudaError_t launch_pp_hd(const vlc_attn_args& a, cudaStream_t stream, bool coop) {
-  using C = PPCfg<HD, KT, (VAR & 0x1000) != 0>;
+  using C = PPCfg<HD, KT, (VAR & 0x1000) != 0, PPRoles<VAR>::XM_BYTES>;
   CUtensorMap mq, mk, mv;
   // Q: {atom elems, rows, atoms} box {ATOM_E, 128, N_ATOMS}: one op = both swizzle atoms of a tile
   cudaError_t e = make_tmap_3d(&mq, a.q, C::ATOM_E, a.q_rows_cap, a.kv / C::ATOM_E, (uint64_t)a.kv * 2,
@@ -939,7 +975,7 @@ static cudaError_t launch_pp_hd(const vlc_attn_args& a, cudaStream_t stream, boo
     attr = true;
   }
   const int smem = C::SMEM > g_attn_min_smem ? C::SMEM : g_attn_min_smem;
-  return launch_chain(attn_pp_kernel<HD, KT, VAR>, dim3(a.n_items), dim3(PP_THREADS), smem, stream, coop, mq, mk, mv, a,
+  return launch_chain(attn_pp_kernel<HD, KT, VAR>, dim3(a.n_items), dim3(PPRoles<VAR>::THREADS), smem, stream, coop, mq, mk, mv, a,
                       h_attn_dbg, h_attn_trace);
 }
 
@@ -964,12 +1000,22 @@ cudaError_t launch_attention_pp(const vlc_attn_args& a, cudaStream_t stream, boo
         case 10: return launch_pp_hd<128, 128, 0x300>(a, stream, coop);
         case 11: return launch_pp_hd<128, 128, 0x400>(a, stream, coop);
         case 20: return launch_pp_hd<128, 128, 0x2001>(a, stream, coop);
+        case 22: return launch_pp_hd<128, 128, 0x4000>(a, stream, coop);
+        case 23: return launch_pp_hd<128, 128, 0x4001>(a, stream, coop);
+        case 24: return launch_pp_hd<128, 128, 0x4400>(a, stream, coop);
+        case 25: return launch_pp_hd<128, 128, 0x4021>(a, stream, coop);
+        case 26: return launch_pp_hd<128, 128, 0x4031>(a, stream, coop);
+        case 27: return launch_pp_hd<128, 128, 0x4041>(a, stream, coop);
+        case 28: return launch_pp_hd<128, 128, 0x4051>(a, stream, coop);
         case 21: return launch_pp_hd<128, 128, 0x2401>(a, stream, coop);
         case 16: return launch_pp_hd<128, 128, 0x1000>(a, stream, coop);
         case 17: return launch_pp_hd<128, 128, 0x1001>(a, stream, coop);
         case 18: return launch_pp_hd<128, 128, 0x1100>(a, stream, coop);
         case 19: return launch_pp_hd<128, 128, 0x1400>(a, stream, coop);
-        default: return launch_pp_hd<128, 128>(a, stream, coop);
+        case 100: return launch_pp_hd<128, 128, 0x0>(a, stream, coop);     // one warp per row quadrant
+        // default: two threads per query row (PPRoles SW = 2), three-input max -- measured
+        // 32.4 -> 31.8 us standalone, 5.25 -> 5.16 ms C3 TTFT (profiles/r1_attention_softmax_variants.txt)
+        default: return launch_pp_hd<128, 128, 0x4001>(a, stream, coop);
       }
     default: return cudaErrorInvalidValue;
   }

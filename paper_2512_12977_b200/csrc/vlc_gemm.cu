@@ -409,6 +409,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
 int g_stage_override = 0;
 void set_debug_buffer(unsigned long long* p) { h_dbg = p; }
+unsigned long long* debug_buffer() { return h_dbg; }
 
 int g_coop = 1;
 int g_pdl = 1;

@@ -32,7 +32,16 @@ struct PairSched {
   int tok_tiles;
   int KB;         // 128-wide k-blocks
   int n_pairs;
+  unsigned long long* dbg;   // per-CTA phase timestamps (experiments; nullptr)
 };
+#define PDBG(slot)                                                                        \
+  do {                                                                                    \
+    if (sc.dbg) {                                                                         \
+      unsigned long long t_;                                                              \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                              \
+      sc.dbg[blockIdx.x * 8 + (slot)] = t_;                                               \
+    }                                                                                     \
+  } while (0)
 
 template <int KIND>
 __global__ void __launch_bounds__(PAIR_THREADS, 1)
@@ -63,6 +72,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
   const int n_tiles = sc.m_tiles2 * sc.tok_tiles;
 
   if (warp == 0 && lane == 0) {
+    PDBG(0);
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -96,6 +106,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         }
       }
       pdl_wait();
+      PDBG(1);
       int stage = 0, u = 0;
       uint32_t phase = 0;
       for (int t = pair; t < n_tiles; t += sc.n_pairs) {
@@ -113,6 +124,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
       }
+      PDBG(2);
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -175,6 +187,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
       const int m0 = (t % sc.m_tiles2) * 256 + rank * 128, tok0 = (t / sc.m_tiles2) * n_tile;
       mbar_wait(&acc_full[slot], (seg >> 1) & 1);
       tc_fence_after();
+      if (threadIdx.x == 64) PDBG(3);
       const uint32_t d = tmem + slot * 256 + lane_off;
       const int nch = (n_tile + 31) / 32;
       for (int ci = eg; ci < nch; ci += 2) {
@@ -196,6 +209,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         else mbar_arrive_remote(mapa_shared(&acc_empty_peer[slot], 0));
       }
     }
+    if (threadIdx.x == 64) PDBG(6);
   }
   tc_fence_before();
   __syncthreads();
@@ -227,7 +241,7 @@ cudaError_t launch_gemm_pair(const void* W, int n_pad, int k_pad, const void* X,
   int sms = 0, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  PairSched sc{n_pad / 256, tok_tiles, k_pad / 128, 0};
+  PairSched sc{n_pad / 256, tok_tiles, k_pad / 128, 0, debug_buffer()};
   const int tiles = sc.m_tiles2 * tok_tiles;
   int pairs = (sms > 0 ? sms : 148) / 2;
   if (max_pairs > 0 && max_pairs < pairs) pairs = max_pairs;

@@ -34,6 +34,7 @@ extern int g_wide;            // key 7: 256-row GEMM tiles (0 auto, 1 never, 2 a
 extern int g_mc;              // key 16: GEMM cluster size for multicast activation loads (1 = off)
 extern int g_pdl;             // key 6: programmatic dependent launch of the chain kernels (default 1)
 void set_debug_buffer(unsigned long long* p);
+unsigned long long* debug_buffer();
 
 // Launch with programmatic stream serialization (g_pdl) and optionally cooperative residency
 // (only when PDL is off: the kernels that rely on co-residency size their grids to <= #SMs).

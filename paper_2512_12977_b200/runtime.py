@@ -175,6 +175,8 @@ class Runner:
         # Measured on C3: 5.58 -> 5.24 ms TTFT (tools: VLC_HI_PRIO / VLC_RELOC_WIDE A/B, run42).
         self.hi_prio = bool(int(__import__("os").environ.get("VLC_HI_PRIO", "1")))
         self.lib.vlc_set_tuning(14, int(__import__("os").environ.get("VLC_RELOC_WIDE", "100000")))
+        if "VLC_ATTN_VAR" in __import__("os").environ:   # attention softmax variant (experiments)
+            self.lib.vlc_set_tuning(15, int(__import__("os").environ["VLC_ATTN_VAR"]))
         self.tp_group = None       # head-parallel process group (engine sets it from the model)
         self._side = None          # side stream of the overlapped kv_relocate
 

@@ -56,7 +56,7 @@ def phases(n, k, m, ctas):
     out = torch.zeros(m + 256, n, device="cuda", dtype=torch.float32)
     e = N.Epilogue()
     e.kind, e.n_valid, e.m_tokens, e.out, e.ldo = N.EPI_BF16, n, m, out.data_ptr(), n
-    dbg = torch.zeros(148 * 8, dtype=torch.int64, device="cuda")
+    dbg = torch.zeros(160 * 8, dtype=torch.int64, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     for it in range(3):
         flush.add_(1)
@@ -65,7 +65,7 @@ def phases(n, k, m, ctas):
                                   ws.numel() * 4, cnt.data_ptr(), torch.cuda.current_stream().cuda_stream), "g")
         torch.cuda.synchronize()
     lib.vlc_set_debug_buffer(None)
-    d = dbg.view(148, 8).cpu().numpy().astype("float64")
+    d = dbg.view(160, 8).cpu().numpy().astype("float64")
     g = d[:, 0] > 0
     d = d[g]
     t0 = d[:, 0].min()
@@ -83,6 +83,13 @@ def phases(n, k, m, ctas):
 if __name__ == "__main__":
     import numpy as np  # noqa: F811
     mode = sys.argv[1] if len(sys.argv) > 1 else "sweep"
+    if mode == "pairphases":      # single-CTA vs CTA-pair kernel, QKV / GU shapes at c = 236
+        for pair in (0, -32):
+            lib.vlc_set_tuning(10, pair)
+            print(f"=== pair threshold {pair}")
+            for (n, kk, m, c) in ((10752, 3584, 236, 0), (14336, 3584, 236, 0)):
+                phases(n, kk, m, c)
+        lib.vlc_set_tuning(10, 96)
     if mode == "phases":
         for (n, kk, m, c) in ((14336, 3584, 240, 112), (14336, 3584, 16, 112), (3584, 3584, 240, 148),
                               (14336, 3584, 240, 148)):
