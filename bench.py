@@ -234,6 +234,7 @@ def main():
 
     import paper_2512_12977_b200 as P
     from paper_2512_12977_b200.engine import _runner, prefill_with_reuse
+    from paper_2512_12977_b200 import runtime as RT
     if args.workload == "C5":
         run_c5(args, wl, P, rank, world, local, dist)
         return
@@ -380,6 +381,26 @@ def main():
                 a = fl_k / (ms_k / 1e3) / 1e12
                 others[k] = {"bound": "tensor", "achieved": round(a, 2), "peak": tf_burst, "unit": "TFLOP/s",
                              "frac": round(a / tf_burst, 4), "note": "causal-effective FLOPs"}
+    # kv_relocate against its own roofline: the production chain runs it per layer on a low-priority
+    # side stream as wide CTAs that only fill idle SMs (its event times above include that
+    # sharing); here the same relocation runs as ONE launch of the full-rate kernel, alone.
+    try:
+        runner.tracer, runner.overlap_reloc = [], False
+        runner.lib.vlc_set_tuning(14, 0)
+        for _ in range(3):
+            _flush_l2(flush)
+            prefill_with_reuse(model, req, store)
+        torch.cuda.synchronize()
+        rl = [(e0.elapsed_time(e1), nb) for name, e0, e1, nb, fl in runner.tracer if name == "kv_relocate"]
+        if rl:
+            ms_r, nb_r = statistics.median(x[0] for x in rl), rl[0][1]
+            a = nb_r / (ms_r / 1e3) / 1e9
+            others["kv_relocate_single_launch"] = {
+                "bound": "hbm", "achieved": round(a, 1), "peak": hbm, "unit": "GB/s", "frac": round(a / hbm, 4),
+                "us": round(ms_r * 1e3, 1), "algorithmic": f"{nb_r / 1e6:.1f} MB (all layers; K+V read + write)"}
+    finally:
+        runner.tracer, runner.overlap_reloc = None, RT._OVERLAP_RELOC
+        runner.lib.vlc_set_tuning(14, int(os.environ.get("VLC_RELOC_WIDE", "100000")))
     if args.trace:
         with open(args.trace, "w") as fh:
             json.dump({"kernels": kernels, "agg": {k: v for k, v in agg.items()}}, fh, indent=1)
