@@ -84,6 +84,11 @@ typedef struct vlc_epilogue {
   int norm_rows;
   int norm_pk_rows;
   int norm_pk_kb;
+  /* optional: bytes [l2_prefetch, l2_prefetch + l2_prefetch_bytes) are prefetched into L2 (evict-last)
+   * while this GEMM runs -- the next projection's weights, so that they stream from HBM in this
+   * GEMM's spare bandwidth instead of on the critical path.  NULL / 0 = off.                  */
+  const void* l2_prefetch;
+  unsigned long long l2_prefetch_bytes;
 } vlc_epilogue;
 
 /* Mixed attention over cached + recomputed KV (engine.py:181-182, model.py:268-291).

@@ -34,7 +34,8 @@ class Epilogue(C.Structure):
                 ("hd", C.c_int), ("seg", C.c_int), ("bias", C.c_void_p), ("add", C.c_void_p),
                 ("ld_add", C.c_int), ("pk_rows", C.c_int), ("pk_kb", C.c_int),
                 ("norm_gamma", C.c_void_p), ("norm_out", C.c_void_p), ("norm_eps", C.c_float),
-                ("norm_rows", C.c_int), ("norm_pk_rows", C.c_int), ("norm_pk_kb", C.c_int)]
+                ("norm_rows", C.c_int), ("norm_pk_rows", C.c_int), ("norm_pk_kb", C.c_int),
+                ("l2_prefetch", C.c_void_p), ("l2_prefetch_bytes", C.c_ulonglong)]
 
 
 class AttnArgs(C.Structure):

@@ -333,11 +333,16 @@ constexpr int PP_THREADS = 320;
 // columns (10 warps); SW = 2 (VAR 0x4000) -> two threads per row, KT/2 columns each, row max
 // exchanged through shared memory (20 warps: 2 control + 16 softmax + 2 idle = 5 per scheduler,
 // so the per-scheduler register file allows 96 registers per thread).
+// ONE (VAR 0x8000): a single query tile per CTA with S double-buffered in TMEM (S(j+1) is computed
+// while the softmax works on S(j)) and SW = 4 threads per row (32 columns each).
 template <int VAR>
 struct PPRoles {
-  static constexpr int SW = (VAR & 0x4000) ? 2 : 1;
-  static constexpr int THREADS = SW == 1 ? PP_THREADS : 640;
-  static constexpr int XM_BYTES = SW == 1 ? 0 : 2 * 2 * 2 * 128 * 4;   // [parity][tile][half][row]
+  static constexpr bool ONE = (VAR & 0x8000) != 0;
+  static constexpr int SW = ONE ? 4 : ((VAR & 0x4000) ? 2 : 1);
+  static constexpr int NTILE = ONE ? 1 : 2;
+  static constexpr int SOFT_WARPS = 4 * SW * NTILE;
+  static constexpr int THREADS = SOFT_WARPS <= 8 ? PP_THREADS : 640;   // 10 or 20 warps
+  static constexpr int XM_BYTES = SW == 1 ? 0 : 2 * NTILE * SW * 128 * 4;   // [parity][tile][part][row]
 };
 // Experiment instrumentation.  The buffers travel as kernel parameters (constant bank), so a
 // disabled trace costs a predicated branch, not a global load on the softmax critical path.
@@ -377,9 +382,9 @@ int g_attn_kt = 128;   // tuning key 12: key tile of the hd-128 kernel (64 or 12
 int g_attn_var = 0;    // tuning key 15: softmax variant of the hd-128 / 128-key kernel (see VAR below;
                        // 0 = default two-threads-per-row kernel, 100 = one thread per row)
 
-template <int HD, int KT, bool PSM_ = false, int XM_BYTES = 0>
+template <int HD, int KT, bool PSM_ = false, int XM_BYTES = 0, bool ONE = false>
 struct PPCfg {
-  static constexpr bool DB = KT == 64;
+  static constexpr bool DB = KT == 64 || ONE;
   // PSM: P staged in shared memory (SS MMA for PV) instead of aliased over S in TMEM, so S(j+1)
   // can be issued as soon as the softmax has read S(j) into registers (KT = 128 only)
   static constexpr bool PSM = PSM_ && KT == 128;
@@ -407,7 +412,9 @@ struct PPCfg {
   static_assert((KST + VST) * KV_BYTES >= 2 * 128 * HD * 4, "split partials are staged in the K/V ring");
   static_assert((KST + VST) * KV_BYTES >= 256 * 8 * 12 + 256 * 4, "merge tables live in the K/V ring");
   // TMEM: S[x][buf] (KT fp32 cols; P bf16 pairs aliased in its first KT/2 cols), O[x] (HD cols)
-  __device__ static constexpr uint32_t s_col(int x, int b) { return DB ? 64u * (2 * x + b) : 128u * x; }
+  __device__ static constexpr uint32_t s_col(int x, int b) {
+    return ONE ? 128u * b : (DB ? 64u * (2 * x + b) : 128u * x);
+  }
   __device__ static constexpr uint32_t o_col(int x) { return 256u + (uint32_t)(HD > 64 ? HD : 64) * x; }
   __device__ static constexpr int sbuf(int j) { return DB ? (j & 1) : 0; }          // S buffer of tile j
   __device__ static constexpr uint32_t sphase(int j) { return DB ? ((j >> 1) & 1) : (j & 1); }
@@ -422,9 +429,10 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
                    const __grid_constant__ CUtensorMap map_v, vlc_attn_args a, unsigned long long* dbgp,
                    unsigned long long* trc) {
   using R = PPRoles<VAR>;
-  using C = PPCfg<HD, KT, (VAR & 0x1000) != 0, R::XM_BYTES>;
+  using C = PPCfg<HD, KT, (VAR & 0x1000) != 0, R::XM_BYTES, R::ONE>;
   constexpr bool PSM = C::PSM;
   constexpr int SW = R::SW, NTH = R::THREADS;
+  static_assert(!R::ONE || KT == 128, "single-tile mode: 128-key tiles");
   static_assert(!(PSM && SW == 2), "P-in-smem is a one-warp-per-row variant");
   static_assert(SW == 1 || KT == 128, "two threads per row: 128-key tiles");
   constexpr int PP_KT = KT;
@@ -454,7 +462,7 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
   const int q_row0 = it[0], nq = it[1], head = it[2], kv_row0 = it[3];
   const int kb = it[4], ke = it[5], group = it[6];
   const int part = it[7] >> 8, nsplit = it[7] & 0xff;
-  const int nq_t[2] = {min(nq, 128), max(0, nq - 128)};
+  const int nq_t[2] = {min(nq, 128), R::ONE ? 0 : max(0, nq - 128)};   // ONE: items carry <= 128 queries
   int nt_t[2];
 #pragma unroll
   for (int x = 0; x < 2; ++x) {
@@ -636,10 +644,10 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
       }
     }
     __syncwarp();
-  } else if (warp < 2 + 8 * SW) {
+  } else if (warp < 2 + R::SOFT_WARPS) {
     // ---------------- softmax groups: warps 2.. -> tile A, then tile B (SW warps per quadrant)
     const int x = (warp - 2) / (4 * SW);
-    const int hh = SW == 1 ? 0 : ((warp - 2) >> 2) & 1;   // column half of the row
+    const int hh = SW == 1 ? 0 : ((warp - 2) >> 2) % SW;   // column part of the row
     constexpr int CW = KT / SW, OW = HD / SW;              // S / O columns of this thread
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
@@ -692,15 +700,16 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
         for (int i = 0; i < CW; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], s[i]);
       }
       float pmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-      if constexpr (SW == 2) {
-        // the other half-row's max; the barrier also orders both halves' S reads before any P
-        // write into S's columns (P of the upper half lands in the lower half's S columns)
-        float* xb = xm + ((j & 1) * 2 + x) * 256;
+      if constexpr (SW > 1) {
+        // the other row parts' maxima; the barrier also orders every part's S reads before any P
+        // write into S's columns (P of an upper part lands in a lower part's S columns)
+        float* xb = xm + ((j & 1) * R::NTILE + x) * (SW * 128);
         xb[hh * 128 + r] = pmax;
         tc_fence_before();
-        asm volatile("bar.sync %0, %1;" ::"r"(1 + x), "r"(256) : "memory");
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + x), "r"(128 * SW) : "memory");
         tc_fence_after();
-        pmax = fmaxf(pmax, xb[(1 - hh) * 128 + r]);
+#pragma unroll
+        for (int o = 1; o < SW; ++o) pmax = fmaxf(pmax, xb[((hh + o) % SW) * 128 + r]);
       }
       const float tmax = pmax * a.scale_log2;
       const float m_new = fmaxf(m_run, tmax);
@@ -789,8 +798,12 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
         fence_proxy_async_smem();
         mbar_arrive(&p_full[2 * x]);
       } else {
+        if constexpr (CW >= 64) {
 #pragma unroll
-        for (int c = 0; c < CW / 64; ++c) tmem_st32f(tS + hh * (CW / 2) + 32 * c, s + 32 * c);   // P(j) over S(j)'s first cols
+          for (int c = 0; c < CW / 64; ++c) tmem_st32f(tS + hh * (CW / 2) + 32 * c, s + 32 * c);   // P(j) over S(j)'s first cols
+        } else {
+          tmem_st16(tS + hh * (CW / 2), s);
+        }
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_full[2 * x + C::sbuf(j)]);   // per-buffer barrier: softmax may run a tile ahead
@@ -803,11 +816,14 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
       mbar_wait(&o_done[x], (ntx - 1) & 1);
       tc_fence_after();
     }
-    if constexpr (SW == 2) {   // row sum = both halves' sums (exchange buffer of iteration ntx: free)
-      float* xb = xm + ((ntx & 1) * 2 + x) * 256;
+    if constexpr (SW > 1) {   // row sum = all parts' sums (exchange buffer of iteration ntx: free)
+      float* xb = xm + ((ntx & 1) * R::NTILE + x) * (SW * 128);
       xb[hh * 128 + r] = l_run;
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + x), "r"(256) : "memory");
-      l_run += xb[(1 - hh) * 128 + r];
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + x), "r"(128 * SW) : "memory");
+      float lt = l_run;
+#pragma unroll
+      for (int o = 1; o < SW; ++o) lt += xb[((hh + o) % SW) * 128 + r];
+      l_run = lt;
     }
     if (r == 0 && hh == 0) adbg(dbgp, 3 + x);
     const int qrow = q_row0 + x * 128 + r;
@@ -891,7 +907,7 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
   __syncthreads();
   __threadfence();
   if (threadIdx.x == 0) adbg(dbgp, 5);
-  const int r_lo = 256 * part / nsplit, r_hi = min(nq, 256 * (part + 1) / nsplit);
+  const int r_lo = nq * part / nsplit, r_hi = nq * (part + 1) / nsplit;
   const int nr = max(0, r_hi - r_lo);
   float2* s_ml = reinterpret_cast<float2*>(sK);                 // [nr][8]
   float* s_w = reinterpret_cast<float*>(s_ml + 256 * 8);        // [nr][8] weight / L
@@ -955,7 +971,7 @@ int g_attn_min_smem = 0;
 
 template <int HD, int KT, int VAR = 0>
 static cudaError_t launch_pp_hd(const vlc_attn_args& a, cudaStream_t stream, bool coop) {
-  using C = PPCfg<HD, KT, (VAR & 0x1000) != 0, PPRoles<VAR>::XM_BYTES>;
+  using C = PPCfg<HD, KT, (VAR & 0x1000) != 0, PPRoles<VAR>::XM_BYTES, PPRoles<VAR>::ONE>;
   CUtensorMap mq, mk, mv;
   // Q: {atom elems, rows, atoms} box {ATOM_E, 128, N_ATOMS}: one op = both swizzle atoms of a tile
   cudaError_t e = make_tmap_3d(&mq, a.q, C::ATOM_E, a.q_rows_cap, a.kv / C::ATOM_E, (uint64_t)a.kv * 2,
@@ -1013,6 +1029,8 @@ cudaError_t launch_attention_pp(const vlc_attn_args& a, cudaStream_t stream, boo
         case 18: return launch_pp_hd<128, 128, 0x1100>(a, stream, coop);
         case 19: return launch_pp_hd<128, 128, 0x1400>(a, stream, coop);
         case 100: return launch_pp_hd<128, 128, 0x0>(a, stream, coop);     // one warp per row quadrant
+        case 30: return launch_pp_hd<128, 128, 0x8001>(a, stream, coop);   // single tile, S double-buffered
+        case 31: return launch_pp_hd<128, 128, 0x8401>(a, stream, coop);
         // default: two threads per query row (PPRoles SW = 2), three-input max -- measured
         // 32.4 -> 31.8 us standalone, 5.25 -> 5.16 ms C3 TTFT (profiles/r1_attention_softmax_variants.txt)
         default: return launch_pp_hd<128, 128, 0x4001>(a, stream, coop);

@@ -211,6 +211,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             bulk_load(sa + pre * a_bytes + h * (a_bytes / H), a_src(mt, kb, h), a_bytes / H, &full[pre], pol_w);
         }
       }
+      if (epi.l2_prefetch_bytes > 0) {
+        // this CTA's share of the next projection's weights -> L2 (evict-last), 64 KB per op
+        const unsigned long long per = ((epi.l2_prefetch_bytes / sk.G + 65535) >> 16) << 16;
+        const unsigned long long lo = per * g;
+        const unsigned long long hi = min(epi.l2_prefetch_bytes, lo + per);
+        const uint64_t pol_pf = policy_evict_last();
+        for (unsigned long long o = lo; o < hi; o += 65536)
+          bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(epi.l2_prefetch) + o, (uint32_t)min(65536ull, hi - o),
+                           pol_pf);
+      }
       pdl_wait();
       int stage = 0, u = 0;
       uint32_t phase = 0;

@@ -18,6 +18,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 
 SRC_TEXT, SRC_STORE, SRC_SCRATCH = 0, 1, 2
@@ -145,6 +147,61 @@ def attention_work(q_ranges, qpos, n_req, heads, target_items: int):
     return it, cb, slot
 
 
+# Attention work decomposition (and the matching vlc_attn_pp kernel, tuning key 15): single 128-query
+# tiles per CTA with S double-buffered (default; measured 31.7 -> 26.8 us per C3 layer) or the
+# two-tile ping-pong kernel (VLC_ATTN_ONE=0).  The two must agree: two-tile items (up to 256 queries)
+# on the single-tile kernel would drop queries 128..255.
+ATTN_ONE_TILE = bool(int(os.environ.get("VLC_ATTN_ONE", "1")))
+
+
+def attn_kernel_variant() -> int:
+    """vlc_set_tuning(15, .) value matching ATTN_ONE_TILE (30: single tile, 0: ping-pong)."""
+    return 30 if ATTN_ONE_TILE else 0
+
+
+def attention_work(q_ranges, qpos, n_req, heads, max_ctas: int = 148):
+    """Work items for vlc_attn_pp in the configured decomposition (ATTN_ONE_TILE)."""
+    fn = attention_work_one if ATTN_ONE_TILE else attention_work_pp
+    return fn(q_ranges, qpos, n_req, heads, max_ctas)
+
+
+def attention_work_one(q_ranges, qpos, n_req, heads, max_ctas: int = 148):
+    """Work items of the single-query-tile attention kernel (vlc_attn_pp, tuning 15 = 30): one CTA
+    per (request, head, <= 128 sorted queries, key range).  Key ranges are split so every CTA gets
+    about the same number of 128-key tiles (a query tile's keys end at its last query's position, so
+    late tiles get more splits); <= 8 splits per tile, all CTAs co-resident when anything is split.
+
+    Returns (items int32 [n, 9], n_groups)."""
+    units = []
+    for h in range(heads):
+        for req, q0, cnt in q_ranges:
+            for t0 in range(q0, q0 + cnt, 128):
+                nq = min(128, q0 + cnt - t0)
+                kend = min(int(qpos[t0 + nq - 1]) + 1, int(n_req[req]))
+                units.append((req, t0, nq, kend, h, max(1, -(-kend // 128))))
+    total = sum(u[5] for u in units)
+    if len(units) >= max_ctas:
+        ns = [1] * len(units)
+    else:
+        target = max(1, -(-total // max_ctas))
+        while True:
+            ns = [max(1, min(8, -(-u[5] // target))) for u in units]
+            if sum(ns) <= max_ctas:
+                break
+            target += 1
+    items, group = [], 0
+    for (req, t0, nq, kend, h, tiles), n in zip(units, ns):
+        n = min(n, tiles)
+        if n == 1:
+            items.append([t0, nq, h, 0, 0, kend, -1, (0 << 8) | 1, req])
+            continue
+        bounds = [min(kend, (tiles * sidx // n) * 128) for sidx in range(n)] + [kend]
+        for sidx in range(n):
+            items.append([t0, nq, h, 0, bounds[sidx], bounds[sidx + 1], group, (sidx << 8) | n, req])
+        group += 1
+    return np.array(items, dtype=np.int32).reshape(-1, 9), group
+
+
 def attention_work_pp(q_ranges, qpos, n_req, heads, max_ctas: int = 148):
     """Work items of the ping-pong attention kernel (include/vlcache.h vlc_attn_pp): one CTA per
     (request, head, <=256 sorted queries, key range).  When there are few (query-pair, head)
@@ -217,7 +274,7 @@ def build_layout(specs: list[RequestSpec], L: int, heads: int, target_items: int
             if len(sel):
                 ranges.append((r, int(sel[0]), len(sel)))
         q_ranges.append(ranges)
-        it9, groups = attention_work_pp(ranges, qpos[i], n_req, heads)
+        it9, groups = attention_work(ranges, qpos[i], n_req, heads)
         it9[:, 3] = kvoff[it9[:, 8]]
         attn_items.append(np.ascontiguousarray(it9[:, :8]))
         comb_items.append(np.zeros((0, 8), dtype=np.int32))

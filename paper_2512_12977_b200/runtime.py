@@ -11,7 +11,7 @@ import weakref
 import numpy as np
 
 from . import _native as N
-from .layout import Layout, attention_work_pp
+from .layout import Layout, attention_work, attn_kernel_variant
 from .model import RMS_EPS, DeviceWeights
 
 N_SMS = 148
@@ -175,8 +175,8 @@ class Runner:
         # Measured on C3: 5.58 -> 5.24 ms TTFT (tools: VLC_HI_PRIO / VLC_RELOC_WIDE A/B, run42).
         self.hi_prio = bool(int(__import__("os").environ.get("VLC_HI_PRIO", "1")))
         self.lib.vlc_set_tuning(14, int(__import__("os").environ.get("VLC_RELOC_WIDE", "100000")))
-        if "VLC_ATTN_VAR" in __import__("os").environ:   # attention softmax variant (experiments)
-            self.lib.vlc_set_tuning(15, int(__import__("os").environ["VLC_ATTN_VAR"]))
+        # attention kernel variant matching the layout's work decomposition (layout.ATTN_ONE_TILE)
+        self.lib.vlc_set_tuning(15, attn_kernel_variant())
         self.tp_group = None       # head-parallel process group (engine sets it from the model)
         self._side = None          # side stream of the overlapped kv_relocate
 
@@ -303,7 +303,7 @@ class Runner:
                        out3=ve.data_ptr(), ld3=kv, seg=kv, hd=cfg.head_dim))
         ranges = [(m, m * T, T) for m in range(k)]
         qpos = np.full(M, T - 1, dtype=np.int32)
-        it9, slots = attention_work_pp(ranges, qpos, np.full(k, T), cfg.num_heads)
+        it9, slots = attention_work(ranges, qpos, np.full(k, T), cfg.num_heads)
         it9[:, 3] = it9[:, 8] * T
         items = np.ascontiguousarray(it9[:, :8])
         pack = IntPack()
@@ -670,7 +670,7 @@ class DeviceDecoder:
         L, d, kv, V = cfg.num_layers, cfg.model_dim, dw.kv, cfg.vocab_size
         pos = self.n
         R = N.row_tile(1)
-        it9, groups = attention_work_pp([(0, 0, 1)], np.array([pos], np.int32), np.array([pos + 1]), dw.heads)
+        it9, groups = attention_work([(0, 0, 1)], np.array([pos], np.int32), np.array([pos + 1]), dw.heads)
         items = np.ascontiguousarray(it9[:, :8])
         pack = IntPack()
         pack.add("src", np.array([[0, token]]))

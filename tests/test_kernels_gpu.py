@@ -246,8 +246,11 @@ def test_kv_relocate_matches_torch(nat):
                                                       (64, 2, 513, 200, True), (32, 8, 288, 44, True),
                                                       (16, 2, 26, 10, True), (128, 4, 300, 300, True),
                                                       (128, 3, 256, 256, False), (128, 1, 4128, 600, True)])
-def test_attention_pp_matches_torch(nat, hd, heads, nkeys, nq, causal):
-    from paper_2512_12977_b200.layout import attention_work_pp
+def test_attention_pp_matches_torch(nat, hd, heads, nkeys, nq, causal, var=None):
+    from paper_2512_12977_b200.layout import attention_work_one, attention_work_pp, attn_kernel_variant
+    var = attn_kernel_variant() if var is None else var
+    nat.load().vlc_set_tuning(15, var)
+    work = attention_work_one if var in (30, 31) else attention_work_pp
     kv = heads * hd
     g = torch.Generator(device="cuda").manual_seed(nkeys + nq)
     layers, layer, kv_rows = 2, 1, nkeys + 64
@@ -262,7 +265,7 @@ def test_attention_pp_matches_torch(nat, hd, heads, nkeys, nq, causal):
     q[:nq] = torch.randn(nq, kv, device="cuda", generator=g).bfloat16()
     rowof = torch.randperm(nq, device="cuda", generator=g).int()
     out = torch.zeros(nq, kv, device="cuda", dtype=torch.bfloat16)
-    it9, groups = attention_work_pp([(0, 0, nq)], qpos.cpu().numpy(), np.array([nkeys]), heads)
+    it9, groups = work([(0, 0, nq)], qpos.cpu().numpy(), np.array([nkeys]), heads)
     it = torch.from_numpy(np.ascontiguousarray(it9[:, :8])).cuda()
     ws_o = torch.zeros(max(groups, 1) * 8 * 256 * hd, device="cuda")
     ws_ml = torch.zeros(max(groups, 1) * 8 * 256 * 2, device="cuda")
@@ -290,15 +293,16 @@ def test_attention_pp_matches_torch(nat, hd, heads, nkeys, nq, causal):
     assert torch.equal(nat.unpack(outp, nq, kv, R), out)
 
 
-@pytest.mark.parametrize("var", [0, 100, 1, 16, 17, 20, 22])
+@pytest.mark.parametrize("var", [0, 30, 31, 100, 1, 16, 17, 20, 22])
 @pytest.mark.parametrize("heads,nkeys,nq", [(28, 4128, 236), (2, 1000, 150), (4, 300, 300), (1, 4128, 600)])
 def test_attention_pp_softmax_variants(nat, var, heads, nkeys, nq):
-    """hd-128 / 128-key softmax variants (tuning key 15): three-input max, P staged in smem."""
-    nat.load().vlc_set_tuning(15, var)
+    """hd-128 / 128-key kernel variants (tuning key 15): ping-pong with 1 or 2 threads per row,
+    three-input max, P staged in smem, single query tile with S double-buffered (30 / 31)."""
+    from paper_2512_12977_b200.layout import attn_kernel_variant
     try:
-        test_attention_pp_matches_torch(nat, 128, heads, nkeys, nq, True)
+        test_attention_pp_matches_torch(nat, 128, heads, nkeys, nq, True, var=var)
     finally:
-        nat.load().vlc_set_tuning(15, 0)
+        nat.load().vlc_set_tuning(15, attn_kernel_variant())
 
 
 @pytest.mark.parametrize("mc", [2, 4])

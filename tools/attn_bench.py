@@ -13,6 +13,9 @@ from paper_2512_12977_b200.layout import attention_work_pp  # noqa: E402
 lib = N.load()
 
 
+ONE = False   # single-query-tile items (attention_work_one) for the tuning-15 = 30/31 kernels
+
+
 def setup(hd=128, heads=28, nkeys=4128, nq=236, max_ctas=148):
     kv = heads * hd
     g = torch.Generator(device="cuda").manual_seed(1)
@@ -25,7 +28,9 @@ def setup(hd=128, heads=28, nkeys=4128, nq=236, max_ctas=148):
     q = torch.randn(512, kv, device="cuda", generator=g).bfloat16()
     rowof = torch.arange(nq, dtype=torch.int32, device="cuda")
     out = torch.zeros(nq, kv, device="cuda", dtype=torch.bfloat16)
-    it9, groups = attention_work_pp([(0, 0, nq)], qpos, np.array([nkeys]), heads, max_ctas)
+    from paper_2512_12977_b200.layout import attention_work_one
+    work = attention_work_one if ONE else attention_work_pp
+    it9, groups = work([(0, 0, nq)], qpos, np.array([nkeys]), heads, max_ctas)
     it = torch.from_numpy(np.ascontiguousarray(it9[:, :8])).cuda()
     ws_o = torch.zeros(max(groups, 1) * 8 * 256 * hd, device="cuda")
     ws_ml = torch.zeros(max(groups, 1) * 8 * 256 * 2, device="cuda")
@@ -97,6 +102,7 @@ if __name__ == "__main__":
     sys.exit(0)
   if len(sys.argv) > 1 and sys.argv[1] == "vars":   # softmax variants of the 128-key kernel (key 15)
     for v in [int(x) for x in sys.argv[2:]]:
+      ONE = v in (30, 31)
       lib.vlc_set_tuning(15, v)
       print(f"== softmax variant {v}", flush=True)
       run(148)
