@@ -1031,6 +1031,10 @@ cudaError_t launch_attention_pp(const vlc_attn_args& a, cudaStream_t stream, boo
         case 100: return launch_pp_hd<128, 128, 0x0>(a, stream, coop);     // one warp per row quadrant
         case 30: return launch_pp_hd<128, 128, 0x8001>(a, stream, coop);   // single tile, S double-buffered
         case 31: return launch_pp_hd<128, 128, 0x8401>(a, stream, coop);
+        case 32: return launch_pp_hd<128, 128, 0x8021>(a, stream, coop);
+        case 33: return launch_pp_hd<128, 128, 0x8031>(a, stream, coop);
+        case 34: return launch_pp_hd<128, 128, 0x8041>(a, stream, coop);
+        case 35: return launch_pp_hd<128, 128, 0xA001>(a, stream, coop);
         // default: two threads per query row (PPRoles SW = 2), three-input max -- measured
         // 32.4 -> 31.8 us standalone, 5.25 -> 5.16 ms C3 TTFT (profiles/r1_attention_softmax_variants.txt)
         default: return launch_pp_hd<128, 128, 0x4001>(a, stream, coop);

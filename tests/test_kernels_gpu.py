@@ -250,7 +250,7 @@ def test_attention_pp_matches_torch(nat, hd, heads, nkeys, nq, causal, var=None)
     from paper_2512_12977_b200.layout import attention_work_one, attention_work_pp, attn_kernel_variant
     var = attn_kernel_variant() if var is None else var
     nat.load().vlc_set_tuning(15, var)
-    work = attention_work_one if var in (30, 31) else attention_work_pp
+    work = attention_work_one if 30 <= var < 40 else attention_work_pp
     kv = heads * hd
     g = torch.Generator(device="cuda").manual_seed(nkeys + nq)
     layers, layer, kv_rows = 2, 1, nkeys + 64
