@@ -315,6 +315,42 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int gf = sk.cta_of(tb), gl = sk.cta_of(tb + sk.KB - 1);
       const int m0 = (t % sk.m_tiles) * BM, tok0 = (t / sk.m_tiles) * n_tile;
       const int slot = H == 1 ? (seg & 1) : 0;
+      const bool split_t = gf != gl && !(KIND == EPI_RESID && sk.red);
+      if constexpr (KIND == EPI_QKV_ROPE && H == 1) {
+        if (!split_t) {
+          // metadata + RoPE tables of chunk c+1 load while chunk c is stored; chunk 0's before the
+          // accumulator is ready (all independent of it)
+          const int nch = (n_tile + 31) / 32;
+          RopeMeta ma, mb;   // two register-resident sets, roles alternate (no copies, no local memory)
+          if (eg < nch)
+            rope_prefetch(epi, m0 + 4 * lane, tok0 + eg * 32, quad, min(32, epi.m_tokens - tok0 - eg * 32), ma);
+          mbar_wait(&acc_full[slot], (seg >> 1) & 1);
+          tc_fence_after();
+          if (leader) DBG(3);
+          const uint32_t d = tmem + slot * 256 + lane_off;
+          auto step = [&](int ci, const RopeMeta& cur, RopeMeta& nxt) {
+            const int c = ci * 32;
+            float v[32];
+            tmem_ld32(d + c, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) stage_buf[jj * 128 + row] = v[jj];
+            asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+            if (ci + 2 < nch)
+              rope_prefetch(epi, m0 + 4 * lane, tok0 + c + 64, quad, min(32, epi.m_tokens - tok0 - c - 64), nxt);
+            rope_store(epi, m0 + 4 * lane, tok0 + c, quad, min(32, epi.m_tokens - tok0 - c), cur,
+                       stage_buf + 4 * lane);
+            asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+          };
+          for (int ci = eg; ci < nch; ci += 4) {
+            step(ci, ma, mb);
+            if (ci + 2 < nch) step(ci + 2, mb, ma);
+          }
+          tc_fence_before();
+          mbar_arrive(&acc_empty[slot]);
+          continue;
+        }
+      }
       mbar_wait(&acc_full[slot], H == 1 ? ((seg >> 1) & 1) : (seg & 1));
       tc_fence_after();
       if (leader) DBG(3);

@@ -103,6 +103,76 @@ __device__ __forceinline__ void write_group(const GemmEpi& e, int F, int j, floa
   }
 }
 
+// QKV_ROPE epilogue split in two: the per-token metadata and RoPE table entries of a 32-token chunk
+// (rope_prefetch: independent of the accumulator, so the GEMM issues chunk c+1's -- and, before the
+// accumulator is ready, chunk 0's -- while it stores chunk c) and the rotation + stores (rope_store).
+struct RopeMeta {
+  int dr[8];        // destination row (q: map1, k / v: KV-cache row)
+  float2 c[8], s[8];
+};
+__device__ __forceinline__ void rope_prefetch(const GemmEpi& e, int F, int j0, int quad, int jv, RopeMeta& m) {
+  if (F >= e.n_valid) return;
+  const int sec = F / e.seg, r = F - sec * e.seg;
+  const int t = (r - (r / e.hd) * e.hd) >> 1;
+  int p[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int jj = quad + 4 * q;
+    if (jj < jv) {
+      const int j = j0 + jj;
+      if (sec != 2) p[q] = __ldg(e.pos + j);
+      m.dr[q] = sec == 0 ? (e.map1 ? __ldg(e.map1 + j) : j) : __ldg(e.map2 + j);
+    }
+  }
+  if (sec == 2) return;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (quad + 4 * q < jv) {
+      const long tab = (long)p[q] * e.tab_ld + t;
+      m.c[q] = __ldg(reinterpret_cast<const float2*>(e.cos_tab + tab));
+      m.s[q] = __ldg(reinterpret_cast<const float2*>(e.sin_tab + tab));
+    }
+  }
+}
+__device__ __forceinline__ void rope_store(const GemmEpi& e, int F, int j0, int quad, int jv, const RopeMeta& m,
+                                           const float* sb) {
+  if (F >= e.n_valid) return;
+  const int sec = F / e.seg, r = F - sec * e.seg;
+  if (sec == 2) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int jj = quad + 4 * q;
+      if (jj < jv) {
+        const float4 x = *reinterpret_cast<const float4*>(sb + jj * 128);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(e.out3) + (long)m.dr[q] * e.ld3 + r) =
+            pack4_bf16(x.x, x.y, x.z, x.w);
+      }
+    }
+    return;
+  }
+  const int half = e.hd >> 1;
+  const int head = r / e.hd, t = (r - head * e.hd) >> 1;   // pairs (t, t+half), (t+1, t+1+half)
+  const int fa = head * e.hd + t;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int jj = quad + 4 * q;
+    if (jj >= jv) continue;
+    const float2 c = m.c[q], sn = m.s[q];
+    const float4 x = *reinterpret_cast<const float4*>(sb + jj * 128);
+    const uint32_t lo = pack_bf16(x.x * c.x - x.y * sn.x, x.z * c.y - x.w * sn.y);
+    const uint32_t hi = pack_bf16(x.y * c.x + x.x * sn.x, x.w * c.y + x.z * sn.y);
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(sec == 0 ? e.out : e.out2) +
+                       (long)m.dr[q] * (sec == 0 ? e.ldo : e.ld2);
+    *reinterpret_cast<uint32_t*>(o + fa) = lo;
+    *reinterpret_cast<uint32_t*>(o + fa + half) = hi;
+    if (sec == 1 && e.out4) {
+      __nv_bfloat16* kp = reinterpret_cast<__nv_bfloat16*>(e.out4) + (long)(j0 + jj) * e.ld4;
+      *reinterpret_cast<uint32_t*>(kp + fa) = pack_bf16(x.x, x.z);
+      *reinterpret_cast<uint32_t*>(kp + fa + half) = pack_bf16(x.y, x.w);
+    }
+  }
+}
+
 // The up-to-8 tokens jj = quad + 4q (q < 8, jj < jv) of one 32-token chunk, features [F, F+4):
 // loads of per-token metadata / RoPE tables are issued for all tokens before any store, so the
 // epilogue is not a chain of dependent global-load latencies.  sb = stage + 4*lane (token stride
