@@ -232,6 +232,33 @@ __device__ __forceinline__ void write_chunk(const GemmEpi& e, int F, int j0, int
       }
     }
   } else {
+    if constexpr (KIND == EPI_BF16 || KIND == EPI_SWIGLU) {
+      // PACKED output, chunk inside one row tile: one division per chunk instead of one per token
+      // (packed_off's row / R) -- the packed store path was ~3.5 us of the gate/up epilogue
+      const int R = e.pk_rows;
+      if (R > 0 && F < e.n_valid && F + 4 <= e.n_valid) {
+        const int rt = j0 / R, r0 = j0 - rt * R;
+        if (r0 + 32 <= R) {
+          const int k = KIND == EPI_SWIGLU ? (F >> 1) : F;
+          const long base = ((((long)rt * e.pk_kb + (k >> 7)) * 2 + ((k >> 6) & 1)) * R) * 64 + (k & 7);
+          const int c = (k >> 3) & 7;
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(e.out);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int jj = quad + 4 * q;
+            if (jj >= jv) continue;
+            const int r = r0 + jj;
+            const long off = base + (long)r * 64 + ((c ^ (r & 7)) << 3);
+            const float4 v = *reinterpret_cast<const float4*>(sb + jj * 128);
+            if constexpr (KIND == EPI_SWIGLU)
+              *reinterpret_cast<uint32_t*>(o + off) = pack_bf16(silu_f(v.x) * v.y, silu_f(v.z) * v.w);
+            else
+              *reinterpret_cast<uint2*>(o + off) = pack4_bf16(v.x, v.y, v.z, v.w);
+          }
+          return;
+        }
+      }
+    }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int jj = quad + 4 * q;

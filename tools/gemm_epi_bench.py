@@ -62,6 +62,8 @@ def main():
     X = N.pack(torch.randn(m, k, device="cuda").bfloat16(), R, rows_cap=-(-m // R) * R)
     # QKV
     n = 3 * kv
+    if os.environ.get("GU_ONLY"):
+        return gu(m, k, R, X)
     Ws = [N.pack(torch.randn(n, k, device="cuda").bfloat16(), 128) for _ in range(4)]
     q = torch.zeros(m + 256, kv, device="cuda", dtype=torch.bfloat16)
     kc = torch.zeros(n_keys + 64, kv, device="cuda", dtype=torch.bfloat16)
@@ -89,6 +91,13 @@ def main():
             print(f"{name} unsplit_min={um}: {timed(Ws, n, k, X, R, e):.2f} us", flush=True)
             phases(Ws[0], n, k, X, R, e)
         lib.vlc_set_tuning(9, 64)
+    gu(m, k, R, X)
+
+
+def gu(m, k, R, X):
+    plain = N.Epilogue()
+    out0 = torch.zeros(m + 256, 14336, device="cuda", dtype=torch.bfloat16)
+    plain.kind, plain.n_valid, plain.m_tokens, plain.out, plain.ldo = N.EPI_BF16, 14336, m, out0.data_ptr(), 14336
     # gate/up
     n = 14336
     Ws = [N.pack(torch.randn(n, k, device="cuda").bfloat16(), 128) for _ in range(3)]
@@ -97,6 +106,17 @@ def main():
     plain.n_valid, plain.out, plain.ldo = n, out.data_ptr(), n
     sw = N.Epilogue()
     sw.kind, sw.n_valid, sw.m_tokens, sw.out, sw.ldo, sw.pk_rows, sw.pk_kb = N.EPI_SWIGLU, n, m, h.data_ptr(), n // 2, R, n // 256
+    sw_rm = N.Epilogue()   # SwiGLU written row-major (isolates the packed-layout store cost)
+    sw_rm.kind, sw_rm.n_valid, sw_rm.m_tokens, sw_rm.out, sw_rm.ldo = N.EPI_SWIGLU, n, m, out.data_ptr(), n // 2
+    bf_pk = N.Epilogue()   # plain BF16 written packed
+    hp = torch.zeros(N.packed_numel(m, n, R), device="cuda", dtype=torch.bfloat16)
+    bf_pk.kind, bf_pk.n_valid, bf_pk.m_tokens, bf_pk.out, bf_pk.ldo, bf_pk.pk_rows, bf_pk.pk_kb = \
+        N.EPI_BF16, n, m, hp.data_ptr(), n, R, n // 128
+    if os.environ.get("GU_ONLY"):
+        for name, e in (("gu bf16", plain), ("gu bf16 packed", bf_pk), ("gu swiglu", sw), ("gu swiglu rowmajor", sw_rm)):
+            print(f"{name}: {timed(Ws, n, k, X, R, e):.2f} us", flush=True)
+            phases(Ws[0], n, k, X, R, e)
+        return
     for name, e in (("gu bf16", plain), ("gu swiglu", sw)):
         for um in (64, 1000):
             lib.vlc_set_tuning(9, um)
