@@ -48,14 +48,14 @@ def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1, packed=Fals
           f"{gbs:7.1f} GB/s  {tf:7.1f} TF/s", flush=True)
 
 
-def phases(n, k, m, ctas):
+def phases(n, k, m, ctas, kind=None):
     """Per-CTA phase timestamps of one launch (DRAM-cold weights)."""
     R = N.row_tile(m)
     W = N.pack(torch.randn(n, k, device="cuda").bfloat16(), 128)
     X = N.pack(torch.randn(m, k, device="cuda").bfloat16(), R, rows_cap=-(-m // R) * R)
     out = torch.zeros(m + 256, n, device="cuda", dtype=torch.float32)
     e = N.Epilogue()
-    e.kind, e.n_valid, e.m_tokens, e.out, e.ldo = N.EPI_BF16, n, m, out.data_ptr(), n
+    e.kind, e.n_valid, e.m_tokens, e.out, e.ldo = N.EPI_BF16 if kind is None else kind, n, m, out.data_ptr(), n
     dbg = torch.zeros(160 * 8, dtype=torch.int64, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     for it in range(3):
@@ -90,6 +90,14 @@ if __name__ == "__main__":
             for (n, kk, m, c) in ((10752, 3584, 236, 0), (14336, 3584, 236, 0)):
                 phases(n, kk, m, c)
         lib.vlc_set_tuning(10, 96)
+    if mode == "residctas":       # stream-K RESID GEMMs at fewer CTAs (fewer split segments -> less red.add)
+        for c in (148, 128, 112, 96, 74):
+            for (n, kk, m) in ((3584, 3584, 236), (3584, 7168, 236)):
+                run(n, kk, m, c, kind=N.EPI_RESID)
+    if mode == "residphases":     # the stream-K O / down projections (red.add into an fp32 residual)
+        for (n, kk, m) in ((3584, 3584, 236), (3584, 7168, 236)):
+            run(n, kk, m, 0, kind=N.EPI_RESID)
+            phases(n, kk, m, 0, kind=N.EPI_RESID)
     if mode == "phases":
         for (n, kk, m, c) in ((14336, 3584, 240, 112), (14336, 3584, 16, 112), (3584, 3584, 240, 148),
                               (14336, 3584, 240, 148)):

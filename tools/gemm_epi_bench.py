@@ -85,6 +85,20 @@ def main():
                       map2=pos.data_ptr(), pos=pos.data_ptr(), cos_tab=cos.data_ptr(), sin_tab=sin.data_ptr(),
                       tab_ld=half, hd=hd, seg=kv).items():
         setattr(rope, kk, v)
+    if os.environ.get("ROPE_ONLY"):
+        rope_nk = N.Epilogue()
+        for f, _ in rope._fields_:
+            setattr(rope_nk, f, getattr(rope, f))
+        rope_nk.out4 = None
+        rope_id = N.Epilogue()     # identity Q/K destination maps (map1 = None: q row = token)
+        for f, _ in rope._fields_:
+            setattr(rope_id, f, getattr(rope, f))
+        rope_id.map1 = None
+        for name, e in (("qkv bf16", plain), ("qkv rope", rope), ("qkv rope no kpre", rope_nk),
+                        ("qkv rope q identity", rope_id)):
+            print(f"{name}: {timed(Ws, n, k, X, R, e):.2f} us", flush=True)
+            phases(Ws[0], n, k, X, R, e)
+        return
     for name, e in (("qkv bf16", plain), ("qkv rope", rope)):
         for um in (64, 1000):
             lib.vlc_set_tuning(9, um)
