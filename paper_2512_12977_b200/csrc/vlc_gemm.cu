@@ -39,6 +39,9 @@ struct SkSched {
   unsigned long long* dbg;   // phase timestamps (experiments; nullptr)
   int mc;        // cluster size: k-block kb's activation block is loaded once, by CTA kb % mc of the
                  // cluster, and multicast to all (1 = no cluster)
+  int sw, sx;    // > 0: decoupled rings (one tile per CTA, H = 1): sw weight stages fed by warp 0 with
+                 // no dependence on the previous kernel, sx activation stages fed by warp 2; the
+                 // epilogue staging aliases the weight ring (free once the accumulator is complete)
   __device__ __forceinline__ long long u0(int g) const { return U * g / G; }
   __device__ __forceinline__ int cta_of(long long u) const {
     int g = (int)((u * G) / U);
@@ -145,14 +148,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int a_bytes = BM * BK * 2;          // 32 KB
   const int b_bytes = n_tile * BK * 2;
+  const bool dec = H == 1 && sk.sw > 0;
+  const int wst = dec ? sk.sw : stages, xst = dec ? sk.sx : stages;   // weight / activation ring depth
   uint8_t* sa = smem;
-  uint8_t* sb = smem + stages * a_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sb + stages * b_bytes);
-  uint64_t* empty = full + stages;
-  uint64_t* acc_full = empty + stages;   // [2]
+  uint8_t* sb = smem + wst * a_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + xst * b_bytes);   // [wst] (coupled: both operands)
+  uint64_t* empty = full + wst;
+  uint64_t* xfull = empty + wst;                                       // [xst] decoupled only
+  uint64_t* xempty = xfull + (dec ? xst : 0);
+  uint64_t* acc_full = xempty + (dec ? xst : 0);   // [2]
   uint64_t* acc_empty = acc_full + 2;    // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  float* stage_all = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(acc_empty) + 64);  // [2][32][128] fp32
+  float* stage_all = dec ? reinterpret_cast<float*>(smem)   // [2][32][128] fp32
+                         : reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(acc_empty) + 64);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int g = blockIdx.x;
@@ -163,10 +171,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     DBG(0);
-    for (int s = 0; s < stages; ++s) {
+    for (int s = 0; s < wst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], sk.mc);   // every CTA of the cluster has consumed the stage
     }
+    if (dec)
+      for (int s = 0; s < xst; ++s) {
+        mbar_init(&xfull[s], 1);
+        mbar_init(&xempty[s], 1);
+      }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_empty[s], 32 * GEMM_EPI_WARPS);
@@ -192,7 +205,47 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     return xp + (((long)tt * kb128 + (kb >> 1)) * 2 + (kb & 1)) * (long)b_bytes;
   };
 
-  if (warp == 0) {
+  if (dec && warp == 0) {
+    // decoupled: weight ring only; weights never depend on the previous kernel (no pdl_wait), so
+    // the ring fills while the predecessor drains and stays wst deep ahead of the MMA
+    if (lane == 0) {
+      DBG(1);
+      const uint64_t pol_w = policy_evict_first();
+      const int mt = t_first % sk.m_tiles;
+      for (int kb = 0; kb < sk.KB; ++kb) {
+        const int st = kb % wst;
+        if (kb >= wst) mbar_wait(&empty[st], ((kb / wst) & 1) ^ 1);
+        mbar_expect_tx(&full[st], a_bytes);
+        bulk_load(sa + st * a_bytes, a_src(mt, kb, 0), a_bytes, &full[st], pol_w);
+      }
+      DBG(2);
+    }
+  } else if (dec && warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc_bf16(GEMM_BM, n_tile, 0, 0);
+      mbar_wait(&acc_empty[0], 1);
+      tc_fence_after();
+      for (int kb = 0; kb < sk.KB; ++kb) {
+        const int ws_ = kb % wst, xs = kb % xst;
+        mbar_wait(&full[ws_], (kb / wst) & 1);
+        mbar_wait(&xfull[xs], (kb / xst) & 1);
+        tc_fence_after();
+        const uint32_t a_addr = smem_u32(sa + ws_ * a_bytes);
+        const uint32_t b_addr = smem_u32(sb + xs * b_bytes);
+#pragma unroll
+        for (int k = 0; k < GEMM_BK / 16; ++k) {
+          const int at = k >> 2;
+          const uint64_t ad = make_sdesc(a_addr + at * (GEMM_BM * 128) + (k & 3) * 32, 16, 1024, 128);
+          const uint64_t bd = make_sdesc(b_addr + at * (n_tile * 128) + (k & 3) * 32, 16, 1024, 128);
+          tc_mma_f16(tmem, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+        }
+        tc_commit(&empty[ws_]);
+        tc_commit(&xempty[xs]);
+      }
+      tc_commit(&acc_full[0]);
+    }
+    __syncwarp();
+  } else if (warp == 0) {
     if (lane == 0) {
       DBG(1);
       const uint64_t pol_w = policy_evict_first();
@@ -298,6 +351,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else {
     pdl_wait();                     // outputs / residual rows belong to the previous kernels
     if (threadIdx.x == 64) pdl_trigger();
+    if (dec && warp == 2) {
+      // decoupled: the activation ring (the previous kernel's output), xst deep ahead of the MMA
+      if (lane == 0) {
+        const uint64_t pol_x = policy_evict_last();
+        const int tt = t_first / sk.m_tiles;
+        for (int kb = 0; kb < sk.KB; ++kb) {
+          const int st = kb % xst;
+          if (kb >= xst) mbar_wait(&xempty[st], ((kb / xst) & 1) ^ 1);
+          mbar_expect_tx(&xfull[st], b_bytes);
+          bulk_load(sb + st * b_bytes, b_src(tt, kb), b_bytes, &xfull[st], pol_x);
+        }
+      }
+      __syncwarp();
+    }
     // ---------------- epilogue warps 2..9 (quad = TMEM lane quadrant).  H == 1: group eg = 0/1
     // takes alternate 32-column chunks; H == 2: group eg drains weight half eg.
     // TMEM (thread = weight row) -> smem stage [32 tokens][128 rows] -> token-major float4
@@ -466,6 +533,8 @@ int g_unsplit_min = 64;   // tuning key 9: tile count from which each tile gets 
 int g_wide = 1;   // tuning key 7: 0 auto, 1 never use 256-row tiles (default: measured slower), 2 always
 int g_mc = 1;     // tuning key 16: cluster size of the one-tile-per-CTA schedule (multicast activations)
 int g_aligned_split = 1;   // tuning key 17: tile-aligned split-K instead of stream-K when it fills >= 70% of SMs
+int g_decoupled = 2;       // tuning key 18: decoupled weight / activation rings (one tile per CTA);
+                           // value = activation stages (>= 2), 0 = off
 
 static int gemm_pick_stages(int n_tile, int H) {
   if (g_stage_override > 0) return g_stage_override;
@@ -559,13 +628,27 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
     else return cudaErrorInvalidValue;
   }
   const int stages = gemm_pick_stages(n_tile, H);
-  const int smem = gemm_smem_bytes(n_tile, stages, H);
   // cluster multicast of the activation blocks: one tile per CTA, all CTAs on one token tile
   int mc = 1;
   if (g_mc > 1 && H == 1 && tok_tiles == 1 && G == (int)tiles && tiles * KB == U && m_tiles % g_mc == 0 &&
       !(rl && rl->n_blocks > 0) && KB >= g_mc)
     mc = g_mc;
-  SkSched sk{U, G, KB, m_tiles, red ? 1 : 0, h_dbg, mc};
+  SkSched sk{U, G, KB, m_tiles, red ? 1 : 0, h_dbg, mc, 0, 0};
+  // decoupled weight / activation rings for the one-tile-per-CTA schedule: the weight ring
+  // (HBM-latency bound) gets every byte the activation ring (L2, 2 stages) leaves
+  // (measured: QKV / gate-up at c = 236: 31.5 / 32.0 -> 29.9 / 29.6 us; slower at c = 112, where the
+  // coupled ring already holds 3 stages -> only for token tiles >= 160)
+  if (g_decoupled && H == 1 && mc == 1 && n_tile >= 160 && G == (int)tiles && tiles * KB == U &&
+      !(rl && rl->n_blocks > 0)) {
+    const int a_b = GEMM_BM * GEMM_BK * 2, b_b = n_tile * GEMM_BK * 2;
+    const int budget = 232448 - 1024 - 512;
+    const int sx = g_decoupled >= 2 ? g_decoupled : 2;   // key 18 value >= 2: activation stages
+    const int sw = (budget - sx * b_b) / a_b;
+    if (sw >= 2 && sw * a_b >= 2 * 32 * 128 * 4) { sk.sw = sw > 8 ? 8 : sw; sk.sx = sx; }
+  }
+  const int smem = sk.sw > 0 ? 1024 + sk.sw * GEMM_BM * GEMM_BK * 2 + sk.sx * n_tile * GEMM_BK * 2 +
+                                   (2 * sk.sw + 2 * sk.sx + 4) * 8 + 64
+                             : gemm_smem_bytes(n_tile, stages, H);
   const uint8_t* wpp = reinterpret_cast<const uint8_t*>(W);
   const uint8_t* xpp = reinterpret_cast<const uint8_t*>(X);
   RelocArgs rla{};

@@ -90,6 +90,17 @@ if __name__ == "__main__":
             for (n, kk, m, c) in ((10752, 3584, 236, 0), (14336, 3584, 236, 0)):
                 phases(n, kk, m, c)
         lib.vlc_set_tuning(10, 96)
+    if mode == "decoupled":       # one-tile GEMMs with decoupled weight / activation rings (key 18)
+        for dec in (0, 2, 3, 4, 0, 2, 3, 4):
+            lib.vlc_set_tuning(18, dec)
+            print(f"-- decoupled {dec}", flush=True)
+            for (n, kk, m) in ((10752, 3584, 236), (14336, 3584, 236), (14336, 3584, 112)):
+                run(n, kk, m, 0)
+        lib.vlc_set_tuning(18, 0)
+        lib.vlc_set_tuning(18, 1)
+        for (n, kk, m) in ((10752, 3584, 236),):
+            phases(n, kk, m, 0)
+        lib.vlc_set_tuning(18, 0)
     if mode == "residctas":       # stream-K RESID GEMMs at fewer CTAs (fewer split segments -> less red.add)
         for c in (148, 128, 112, 96, 74):
             for (n, kk, m) in ((3584, 3584, 236), (3584, 7168, 236)):
