@@ -334,11 +334,11 @@ constexpr int PP_THREADS = 320;
 // exchanged through shared memory (20 warps: 2 control + 16 softmax + 2 idle = 5 per scheduler,
 // so the per-scheduler register file allows 96 registers per thread).
 // ONE (VAR 0x8000): a single query tile per CTA with S double-buffered in TMEM (S(j+1) is computed
-// while the softmax works on S(j)) and SW = 4 threads per row (32 columns each).
+// while the softmax works on S(j)) and SW = 4 threads per row (32 columns each; 0x4000: 2).
 template <int VAR>
 struct PPRoles {
   static constexpr bool ONE = (VAR & 0x8000) != 0;
-  static constexpr int SW = ONE ? 4 : ((VAR & 0x4000) ? 2 : 1);
+  static constexpr int SW = ONE ? ((VAR & 0x4000) ? 2 : 4) : ((VAR & 0x4000) ? 2 : 1);
   static constexpr int NTILE = ONE ? 1 : 2;
   static constexpr int SOFT_WARPS = 4 * SW * NTILE;
   static constexpr int THREADS = SOFT_WARPS <= 8 ? PP_THREADS : 640;   // 10 or 20 warps
@@ -1035,6 +1035,7 @@ cudaError_t launch_attention_pp(const vlc_attn_args& a, cudaStream_t stream, boo
         case 33: return launch_pp_hd<128, 128, 0x8031>(a, stream, coop);
         case 34: return launch_pp_hd<128, 128, 0x8041>(a, stream, coop);
         case 35: return launch_pp_hd<128, 128, 0xA001>(a, stream, coop);
+        case 36: return launch_pp_hd<128, 128, 0xC001>(a, stream, coop);   // single tile, two threads per row
         // default: two threads per query row (PPRoles SW = 2), three-input max -- measured
         // 32.4 -> 31.8 us standalone, 5.25 -> 5.16 ms C3 TTFT (profiles/r1_attention_softmax_variants.txt)
         default: return launch_pp_hd<128, 128, 0x4001>(a, stream, coop);

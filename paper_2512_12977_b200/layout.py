@@ -155,8 +155,9 @@ ATTN_ONE_TILE = bool(int(os.environ.get("VLC_ATTN_ONE", "1")))
 
 
 def attn_kernel_variant() -> int:
-    """vlc_set_tuning(15, .) value matching ATTN_ONE_TILE (30: single tile, 0: ping-pong)."""
-    return 30 if ATTN_ONE_TILE else 0
+    """vlc_set_tuning(15, .) value matching ATTN_ONE_TILE (36: single tile, two softmax threads per row;
+    0: ping-pong)."""
+    return 36 if ATTN_ONE_TILE else 0
 
 
 def attention_work(q_ranges, qpos, n_req, heads, max_ctas: int = 148):
