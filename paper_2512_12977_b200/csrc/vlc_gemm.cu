@@ -39,6 +39,7 @@ struct SkSched {
   unsigned long long* dbg;   // phase timestamps (experiments; nullptr)
   int mc;        // cluster size: k-block kb's activation block is loaded once, by CTA kb % mc of the
                  // cluster, and multicast to all (1 = no cluster)
+  int xh;        // decoupled: activation slots hold one 64-k atom (half a k-block) instead of a k-block
   int sw, sx;    // > 0: decoupled rings (one tile per CTA, H = 1): sw weight stages fed by warp 0 with
                  // no dependence on the previous kernel, sx activation stages fed by warp 2; the
                  // epilogue staging aliases the weight ring (free once the accumulator is complete)
@@ -150,9 +151,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int b_bytes = n_tile * BK * 2;
   const bool dec = H == 1 && sk.sw > 0;
   const int wst = dec ? sk.sw : stages, xst = dec ? sk.sx : stages;   // weight / activation ring depth
+  const int x_unit = (dec && sk.xh) ? b_bytes / 2 : b_bytes;          // activation slot bytes
   uint8_t* sa = smem;
   uint8_t* sb = smem + wst * a_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sb + xst * b_bytes);   // [wst] (coupled: both operands)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + xst * x_unit);    // [wst] (coupled: both operands)
   uint64_t* empty = full + wst;
   uint64_t* xfull = empty + wst;                                       // [xst] decoupled only
   uint64_t* xempty = xfull + (dec ? xst : 0);
@@ -225,24 +227,41 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint32_t idesc = make_idesc_bf16(GEMM_BM, n_tile, 0, 0);
       mbar_wait(&acc_empty[0], 1);
       tc_fence_after();
+      const int xper = sk.xh ? 2 : 1;   // activation slots per k-block
+      long long c0 = 0;
+      if (sk.dbg) { asm volatile("mov.u64 %0, %%clock64;" : "=l"(c0)); DBG(5); }
       for (int kb = 0; kb < sk.KB; ++kb) {
-        const int ws_ = kb % wst, xs = kb % xst;
+        const int ws_ = kb % wst;
         mbar_wait(&full[ws_], (kb / wst) & 1);
-        mbar_wait(&xfull[xs], (kb / xst) & 1);
-        tc_fence_after();
         const uint32_t a_addr = smem_u32(sa + ws_ * a_bytes);
-        const uint32_t b_addr = smem_u32(sb + xs * b_bytes);
 #pragma unroll
-        for (int k = 0; k < GEMM_BK / 16; ++k) {
-          const int at = k >> 2;
-          const uint64_t ad = make_sdesc(a_addr + at * (GEMM_BM * 128) + (k & 3) * 32, 16, 1024, 128);
-          const uint64_t bd = make_sdesc(b_addr + at * (n_tile * 128) + (k & 3) * 32, 16, 1024, 128);
-          tc_mma_f16(tmem, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+        for (int hx = 0; hx < 2; ++hx) {
+          if (hx >= xper) break;
+          const int u = kb * xper + hx, xs = u % xst;
+          mbar_wait(&xfull[xs], (u / xst) & 1);
+          tc_fence_after();
+          const uint32_t b_addr = smem_u32(sb + xs * x_unit);
+#pragma unroll
+          for (int k = 0; k < GEMM_BK / 16; ++k) {
+            const int at = k >> 2;
+            if (xper == 2 && at != hx) continue;   // half slots: atom hx of the k-block only
+            const uint64_t ad = make_sdesc(a_addr + at * (GEMM_BM * 128) + (k & 3) * 32, 16, 1024, 128);
+            const uint64_t bd = make_sdesc(b_addr + (xper == 2 ? 0 : at * (n_tile * 128)) + (k & 3) * 32, 16,
+                                           1024, 128);
+            tc_mma_f16(tmem, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          }
+          tc_commit(&xempty[xs]);
         }
         tc_commit(&empty[ws_]);
-        tc_commit(&xempty[xs]);
       }
       tc_commit(&acc_full[0]);
+      if (sk.dbg) {   // mainloop SM cycles next to globaltimer slots 5 / 6: the SM clock under load
+        mbar_wait(&acc_full[0], 0);
+        long long c1;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(c1));
+        DBG(6);
+        sk.dbg[(160 + blockIdx.x) * 8] = (unsigned long long)(c1 - c0);   // buffers >= 320 x 8 entries
+      }
     }
     __syncwarp();
   } else if (warp == 0) {
@@ -356,11 +375,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (lane == 0) {
         const uint64_t pol_x = policy_evict_last();
         const int tt = t_first / sk.m_tiles;
-        for (int kb = 0; kb < sk.KB; ++kb) {
-          const int st = kb % xst;
-          if (kb >= xst) mbar_wait(&xempty[st], ((kb / xst) & 1) ^ 1);
-          mbar_expect_tx(&xfull[st], b_bytes);
-          bulk_load(sb + st * b_bytes, b_src(tt, kb), b_bytes, &xfull[st], pol_x);
+        const int xper = sk.xh ? 2 : 1;
+        for (int u = 0; u < sk.KB * xper; ++u) {
+          const int st = u % xst;
+          if (u >= xst) mbar_wait(&xempty[st], ((u / xst) & 1) ^ 1);
+          mbar_expect_tx(&xfull[st], x_unit);
+          const uint8_t* src = xper == 2 ? b_src(tt, u >> 1) + (u & 1) * (n_tile * 128) : b_src(tt, u);
+          bulk_load(sb + st * x_unit, src, x_unit, &xfull[st], pol_x);
         }
       }
       __syncwarp();
@@ -633,7 +654,7 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   if (g_mc > 1 && H == 1 && tok_tiles == 1 && G == (int)tiles && tiles * KB == U && m_tiles % g_mc == 0 &&
       !(rl && rl->n_blocks > 0) && KB >= g_mc)
     mc = g_mc;
-  SkSched sk{U, G, KB, m_tiles, red ? 1 : 0, h_dbg, mc, 0, 0};
+  SkSched sk{U, G, KB, m_tiles, red ? 1 : 0, h_dbg, mc, 0, 0, 0};
   // decoupled weight / activation rings for the one-tile-per-CTA schedule: the weight ring
   // (HBM-latency bound) gets every byte the activation ring (L2, 2 stages) leaves
   // (measured: QKV / gate-up at c = 236: 31.5 / 32.0 -> 29.9 / 29.6 us; slower at c = 112, where the
@@ -642,11 +663,14 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
       !(rl && rl->n_blocks > 0)) {
     const int a_b = GEMM_BM * GEMM_BK * 2, b_b = n_tile * GEMM_BK * 2;
     const int budget = 232448 - 1024 - 512;
-    const int sx = g_decoupled >= 2 ? g_decoupled : 2;   // key 18 value >= 2: activation stages
-    const int sw = (budget - sx * b_b) / a_b;
-    if (sw >= 2 && sw * a_b >= 2 * 32 * 128 * 4) { sk.sw = sw > 8 ? 8 : sw; sk.sx = sx; }
+    // key 18 value v: v in [2, 9] activation k-block stages; v >= 10: (v - 10) half-k-block stages
+    const int xh = g_decoupled >= 10 ? 1 : 0;
+    const int sx = xh ? (g_decoupled - 10 >= 2 ? g_decoupled - 10 : 2) : (g_decoupled >= 2 ? g_decoupled : 2);
+    const int xu = xh ? b_b / 2 : b_b;
+    const int sw = (budget - sx * xu) / a_b;
+    if (sw >= 2 && sw * a_b >= 2 * 32 * 128 * 4) { sk.sw = sw > 8 ? 8 : sw; sk.sx = sx; sk.xh = xh; }
   }
-  const int smem = sk.sw > 0 ? 1024 + sk.sw * GEMM_BM * GEMM_BK * 2 + sk.sx * n_tile * GEMM_BK * 2 +
+  const int smem = sk.sw > 0 ? 1024 + sk.sw * GEMM_BM * GEMM_BK * 2 + sk.sx * n_tile * GEMM_BK * (sk.xh ? 1 : 2) +
                                    (2 * sk.sw + 2 * sk.sx + 4) * 8 + 64
                              : gemm_smem_bytes(n_tile, stages, H);
   const uint8_t* wpp = reinterpret_cast<const uint8_t*>(W);

@@ -56,7 +56,7 @@ def phases(n, k, m, ctas, kind=None):
     out = torch.zeros(m + 256, n, device="cuda", dtype=torch.float32)
     e = N.Epilogue()
     e.kind, e.n_valid, e.m_tokens, e.out, e.ldo = N.EPI_BF16 if kind is None else kind, n, m, out.data_ptr(), n
-    dbg = torch.zeros(160 * 8, dtype=torch.int64, device="cuda")
+    dbg = torch.zeros(320 * 8, dtype=torch.int64, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     for it in range(3):
         flush.add_(1)
@@ -65,7 +65,7 @@ def phases(n, k, m, ctas, kind=None):
                                   ws.numel() * 4, cnt.data_ptr(), torch.cuda.current_stream().cuda_stream), "g")
         torch.cuda.synchronize()
     lib.vlc_set_debug_buffer(None)
-    d = dbg.view(160, 8).cpu().numpy().astype("float64")
+    d = dbg.view(320, 8)[:160].cpu().numpy().astype("float64")
     g = d[:, 0] > 0
     d = d[g]
     t0 = d[:, 0].min()
@@ -91,7 +91,7 @@ if __name__ == "__main__":
                 phases(n, kk, m, c)
         lib.vlc_set_tuning(10, 96)
     if mode == "decoupled":       # one-tile GEMMs with decoupled weight / activation rings (key 18)
-        for dec in (0, 2, 3, 4, 0, 2, 3, 4):
+        for dec in (2, 12, 13, 14, 2, 13):
             lib.vlc_set_tuning(18, dec)
             print(f"-- decoupled {dec}", flush=True)
             for (n, kk, m) in ((10752, 3584, 236), (14336, 3584, 236), (14336, 3584, 112)):
@@ -101,6 +101,29 @@ if __name__ == "__main__":
         for (n, kk, m) in ((10752, 3584, 236),):
             phases(n, kk, m, 0)
         lib.vlc_set_tuning(18, 0)
+    if mode == "clock":           # SM clock during the decoupled QKV / GU mainloop (cycles / ns)
+        for (n, kk, m) in ((10752, 3584, 236), (14336, 3584, 236)):
+            R = N.row_tile(m)
+            W = N.pack(torch.randn(n, kk, device="cuda").bfloat16(), 128)
+            X = N.pack(torch.randn(m, kk, device="cuda").bfloat16(), R, rows_cap=-(-m // R) * R)
+            out = torch.zeros(m + 256, n, device="cuda", dtype=torch.float32)
+            e = N.Epilogue()
+            e.kind, e.n_valid, e.m_tokens, e.out, e.ldo = N.EPI_BF16, n, m, out.data_ptr(), n
+            dbg = torch.zeros(320 * 8, dtype=torch.int64, device="cuda")
+            for it in range(4):
+                lib.vlc_set_debug_buffer(dbg.data_ptr() if it == 3 else None)
+                N.check(lib.vlc_gemm_bf16(W.data_ptr(), n, kk, X.data_ptr(), -(-m // R) * R, m, e, 0, ws.data_ptr(),
+                                          ws.numel() * 4, cnt.data_ptr(), torch.cuda.current_stream().cuda_stream), "g")
+                torch.cuda.synchronize()
+            lib.vlc_set_debug_buffer(None)
+            dd = dbg.view(320, 8).cpu().numpy().astype("float64")
+            cyc = dd[160:, 0]
+            d = dd[:160]
+            ok = cyc > 0
+            d, cyc = d[ok], cyc[ok]
+            mhz = cyc / (d[:, 6] - d[:, 5]) * 1e3
+            print(f"N={n}: mainloop {np.median(d[:, 6] - d[:, 5]) / 1e3:.2f} us, {np.median(cyc):.0f} cycles, "
+                  f"SM clock {np.median(mhz):.0f} MHz (min {mhz.min():.0f})", flush=True)
     if mode == "residctas":       # stream-K RESID GEMMs at fewer CTAs (fewer split segments -> less red.add)
         for c in (148, 128, 112, 96, 74):
             for (n, kk, m) in ((3584, 3584, 236), (3584, 7168, 236)):
