@@ -308,7 +308,7 @@ def main():
         res = prefill_with_reuse(model, req, store)
         last = res.last_logits()
         e2e.append((time.perf_counter() - t0) * 1e3)
-        bytes_h2d = int(runner.ws.bufs["ints"].numel() * 4)
+        bytes_h2d = int(getattr(runner.ws, "last_h2d_bytes", runner.ws.bufs["ints"].numel() * 4))
     clocks = sampler.stop()
     if dist:
         t = torch.tensor([p50, mean, statistics.median(e2e)], device="cuda")

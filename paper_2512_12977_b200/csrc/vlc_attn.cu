@@ -752,7 +752,19 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
       const float nm = any ? -m_run : NEG_INF;     // all-masked row: every p = exp2(-inf) = 0
       // P packed in place into s[0, KT/2) (slot i is free once pairs 2i, 2i+1 are read)
       float ls4[4] = {0.f, 0.f, 0.f, 0.f};
-      if constexpr ((VAR & 0x2000) != 0) {     // packed-pair FFMA2 / FADD2
+      if constexpr ((VAR & 0x10000) != 0) {    // two exponentials per MUFU op (f16x2), fp32 sums
+        const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nm2 = make_float2(nm, nm);
+        float2 l2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int i = 0; i < CW / 2; ++i) {
+          const float2 xx = ffma2(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2);
+          const float2 pp = exp2_f16x2(xx.x, xx.y);
+          l2[i & 3] = fadd2(l2[i & 3], pp);
+          s[i] = __uint_as_float(pack_bf16(pp.x, pp.y));
+        }
+        const float2 la = fadd2(l2[0], l2[1]), lb = fadd2(l2[2], l2[3]);
+        ls4[0] = la.x; ls4[1] = la.y; ls4[2] = lb.x; ls4[3] = lb.y;
+      } else if constexpr ((VAR & 0x2000) != 0) {     // packed-pair FFMA2 / FADD2
         const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nm2 = make_float2(nm, nm);
         float2 l2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
@@ -1036,6 +1048,8 @@ cudaError_t launch_attention_pp(const vlc_attn_args& a, cudaStream_t stream, boo
         case 34: return launch_pp_hd<128, 128, 0x8041>(a, stream, coop);
         case 35: return launch_pp_hd<128, 128, 0xA001>(a, stream, coop);
         case 36: return launch_pp_hd<128, 128, 0xC001>(a, stream, coop);   // single tile, two threads per row
+        case 37: return launch_pp_hd<128, 128, 0x1C001>(a, stream, coop);  // + f16x2 exponentials
+        case 38: return launch_pp_hd<128, 128, 0x18001>(a, stream, coop);  // single tile, SW 4, f16x2
         // default: two threads per query row (PPRoles SW = 2), three-input max -- measured
         // 32.4 -> 31.8 us standalone, 5.25 -> 5.16 ms C3 TTFT (profiles/r1_attention_softmax_variants.txt)
         default: return launch_pp_hd<128, 128, 0x4001>(a, stream, coop);

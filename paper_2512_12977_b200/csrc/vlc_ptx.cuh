@@ -375,6 +375,18 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
       : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
   return *reinterpret_cast<float2*>(&rd);
 }
+// two exponentials per MUFU op: 2^x for an (x0, x1) pair rounded to f16, results widened to fp32
+// (f16 input spacing <= 2^-7 for |x| < 16 -> <= 0.27% relative on p, below bf16's 0.39% rounding of P)
+__device__ __forceinline__ float2 exp2_f16x2(float x0, float x1) {
+  uint32_t h, e;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(x1), "f"(x0));   // x0 -> low half
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(e) : "r"(h));
+  float lo, hi;
+  asm("{\n\t.reg .f16 l, u;\n\tmov.b32 {l, u}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, u;\n\t}"
+      : "=f"(lo), "=f"(hi)
+      : "r"(e));
+  return make_float2(lo, hi);
+}
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float d;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));

@@ -106,6 +106,7 @@ class IntPack:
         ev = torch.cuda.Event()
         ev.record()
         ws.pinned[key] = (pin, ev)
+        ws.last_h2d_bytes = 4 * int(host.size)
         self.dev = dev
         return self
 
@@ -118,10 +119,13 @@ class IntPack:
             ev.synchronize()
         dev = ws.bufs[key]
         pn = pin.numpy()
+        nbytes = 0
         for name in names:
             o, n = self.off[name]
             pn[o:o + n] = self.host[o:o + n]
             dev[o:o + n].copy_(pin[o:o + n], non_blocking=True)
+            nbytes += 4 * n
+        ws.last_h2d_bytes = nbytes
         ev = torch.cuda.Event()
         ev.record()
         ws.pinned[key] = (pin, ev)
