@@ -39,12 +39,21 @@ __global__ void __launch_bounds__(128) rmsnorm_kernel(float* __restrict__ x, int
                                                       const int* __restrict__ row_map, float eps,
                                                       int pk_rows, int pk_kb, const float* __restrict__ add,
                                                       int ld_add) {
+  const int n4 = d >> 2;
+  // gamma does not depend on the previous kernel: load it before griddepcontrol.wait, so only the
+  // residual row's load + reduction + store stay on the critical path
+  float4 gg[VPT];
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int i = threadIdx.x + 128 * k;
+    gg[k] = i < n4 ? __ldg(g4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   pdl_wait();
   pdl_trigger();
   const int r = blockIdx.x;
   const int sr = row_map ? __ldg(row_map + r) : r;
   float4* xr = reinterpret_cast<float4*>(x + (long)sr * ldx);
-  const int n4 = d >> 2;
   float4 v[VPT];
   float acc = 0.f;
 #pragma unroll
@@ -72,14 +81,12 @@ __global__ void __launch_bounds__(128) rmsnorm_kernel(float* __restrict__ x, int
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
   const float denom = sqrtf((red[0] + red[1] + red[2] + red[3]) / (float)d + eps);
-  const float4* g4 = reinterpret_cast<const float4*>(g);
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
     const int i = threadIdx.x + 128 * k;
     if (i >= n4) break;
-    const float4 gg = __ldg(g4 + i);
-    const float4 y = make_float4((v[k].x / denom) * gg.x, (v[k].y / denom) * gg.y, (v[k].z / denom) * gg.z,
-                                 (v[k].w / denom) * gg.w);
+    const float4 y = make_float4((v[k].x / denom) * gg[k].x, (v[k].y / denom) * gg[k].y,
+                                 (v[k].z / denom) * gg[k].z, (v[k].w / denom) * gg[k].w);
     if (OUT_F32) {
       reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + (long)r * ldo)[i] = y;
     } else {
