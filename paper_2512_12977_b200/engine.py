@@ -63,9 +63,20 @@ def flops_from_masks(masks: ComputationMask, seq_len: int, cfg: ModelConfig,
                           sum(_mlp_flops(c, cfg) for c in counts))
 
 
+_FLOPS_CACHE: dict = {}
+
+
 def _flops_from_counts(counts, n, cfg, encoded):
-    return FlopsBreakdown(encoded * encoder_flops(cfg), sum(_attn_flops(c, n, cfg) for c in counts),
-                          sum(_mlp_flops(c, cfg) for c in counts))
+    """FlopsBreakdown of per-layer computed-row counts (memoised: pure in its arguments)."""
+    key = (tuple(counts), n, encoded, cfg.num_layers, cfg.model_dim, cfg.kv_dim, cfg.mlp_hidden,
+           cfg.tokens_per_image, cfg.patch_size)
+    fb = _FLOPS_CACHE.get(key)
+    if fb is None:
+        fb = FlopsBreakdown(encoded * encoder_flops(cfg), sum(_attn_flops(c, n, cfg) for c in counts),
+                            sum(_mlp_flops(c, cfg) for c in counts))
+        if len(_FLOPS_CACHE) < 4096:
+            _FLOPS_CACHE[key] = fb
+    return fb   # frozen dataclass: safe to share
 
 
 def count_flops(request, plan: RecomputePlan, config: ModelConfig, encoder_cached: bool = True) -> FlopsBreakdown:

@@ -119,9 +119,14 @@ class IntPack:
             ev.synchronize()
         dev = ws.bufs[key]
         pn = pin.numpy()
+        # the named segments as one contiguous span when they are adjacent (the pack puts the
+        # per-call segments first): one H2D copy instead of one per segment
+        spans = sorted(self.off[name] for name in names)
+        lo, hi = spans[0][0], max(o + n for o, n in spans)
+        if sum(n for _, n in spans) >= (hi - lo) * 3 // 4:
+            spans = [(lo, hi - lo)]
         nbytes = 0
-        for name in names:
-            o, n = self.off[name]
+        for o, n in spans:
             pn[o:o + n] = self.host[o:o + n]
             dev[o:o + n].copy_(pin[o:o + n], non_blocking=True)
             nbytes += 4 * n
@@ -447,7 +452,8 @@ class Runner:
         tpl = getattr(lay, "_pack_tpl", None)
         if tpl is None:
             pk = IntPack()
-            pk.add("src", lay.row_src)
+            pk.add("src", lay.row_src)            # per-call segments first and adjacent: one copy
+            pk.add("pages", lay.page_table)
             pk.add("row_pos", lay.row_pos)
             pk.add("row_kv", lay.row_kv)
             for i in range(lay.L):
@@ -458,7 +464,6 @@ class Runner:
                 pk.add(f"comb{i}", lay.comb_items[i] if len(lay.comb_items[i]) else np.zeros(8))
             pk.add("descs", lay.reloc_descs if len(lay.reloc_descs) else np.zeros(8))
             pk.add("blocks", lay.reloc_blocks if len(lay.reloc_blocks) else np.zeros(2))
-            pk.add("pages", lay.page_table)
             pk.add("final", lay.final_rows)
             tpl = lay._pack_tpl = (np.concatenate(pk.parts), dict(pk.off))
         host, off = tpl

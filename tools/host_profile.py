@@ -37,4 +37,4 @@ pr.enable()
 for _ in range(10):
     P.prefill_with_reuse(model, req, store).last_logits()
 pr.disable()
-pstats.Stats(pr).sort_stats("cumulative").print_stats(35)
+pstats.Stats(pr).sort_stats(os.environ.get("SORT", "cumulative")).print_stats(35)
