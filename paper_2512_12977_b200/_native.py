@@ -35,7 +35,7 @@ class Epilogue(C.Structure):
                 ("ld_add", C.c_int), ("pk_rows", C.c_int), ("pk_kb", C.c_int),
                 ("norm_gamma", C.c_void_p), ("norm_out", C.c_void_p), ("norm_eps", C.c_float),
                 ("norm_rows", C.c_int), ("norm_pk_rows", C.c_int), ("norm_pk_kb", C.c_int),
-                ("l2_prefetch", C.c_void_p), ("l2_prefetch_bytes", C.c_ulonglong)]
+                ("l2_prefetch", C.c_void_p), ("l2_prefetch_bytes", C.c_ulonglong), ("red_scratch", C.c_void_p)]
 
 
 class AttnArgs(C.Structure):

@@ -89,6 +89,7 @@ __device__ __forceinline__ void grid_barrier(int* cnt, int* gen, int G) {
 }
 
 constexpr int NORM_BAR = 4096;   // counters[NORM_BAR], [NORM_BAR + 1]: the fused-norm grid barrier
+constexpr int REDX_CNT = 8192;   // counters[REDX_CNT + gf]: arrivals at split tile (first CTA gf) in red mode
 
 // RMSNorm of residual rows g, g + G, ... (< epi.norm_rows) -> packed bf16 (model.py:257-259;
 // same arithmetic as rmsnorm_kernel: y = (x / sqrt(mean(x^2) + eps)) * gamma).  All GEMM_THREADS
@@ -445,7 +446,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint32_t d = tmem + slot * 256 + (H == 2 ? eg * 256 : 0) + lane_off;
       const int hoff = H == 2 ? eg * 128 : 0;                 // weight-row offset of this group
       const bool split = gf != gl && !(KIND == EPI_RESID && sk.red);   // RESID partials: red.add in L2
-      float* part = split ? ws + (2L * g + (t == t_first ? 0 : 1)) * (long)n_tile * BM : nullptr;
+      // red mode: the split tile's partials meet in the zero-maintained scratch slot of its first CTA
+      const bool redx = split && KIND != EPI_RESID && epi.red_scratch != nullptr;
+      float* rslot = redx ? epi.red_scratch + (long)gf * BM * n_tile : nullptr;   // [n_tile][BM]
+      float* part = split && !redx ? ws + (2L * g + (t == t_first ? 0 : 1)) * (long)n_tile * BM : nullptr;
       const int nch = (n_tile + 31) / 32;
       for (int ci = (H == 1 ? eg : 0); ci < nch; ci += (H == 1 ? 2 : 1)) {
         const int c = ci * 32;
@@ -456,7 +460,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int jj = 0; jj < 32; ++jj) stage_buf[jj * 128 + row] = v[jj];
         asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
         const int jmax = min(32, n_tile - c);
-        if (split) {
+        if (redx) {
+          for (int jj = quad; jj < jmax; jj += 4) {
+            const float4 x4 = *reinterpret_cast<const float4*>(stage_buf + jj * 128 + 4 * lane);
+            float* o = rslot + (long)(c + jj) * BM + hoff + 4 * lane;
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(o), "f"(x4.x), "f"(x4.y), "f"(x4.z),
+                         "f"(x4.w)
+                         : "memory");
+          }
+        } else if (split) {
           for (int jj = quad; jj < jmax; jj += 4)
             __stcg(reinterpret_cast<float4*>(part + (long)(c + jj) * BM + hoff) + lane,
                    *reinterpret_cast<const float4*>(stage_buf + jj * 128 + 4 * lane));
@@ -468,7 +480,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[slot]);   // this thread's TMEM reads of the accumulator are done
-      if (split) {
+      if (redx) {
+        // every participant's red.adds land before its arrival; the last arrival finishes the tile:
+        // scratch -> stage (re-zeroing the scratch) -> the fused epilogue, chunk by chunk
+        const int nseg = gl - gf + 1;
+        __threadfence();
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+        if (leader) tmem_slot[1] = (atomicAdd(&counters[REDX_CNT + gf], 1) == nseg - 1) ? 1u : 0u;
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+        if (tmem_slot[1]) {
+          __threadfence();
+          for (int ci = eg; ci < nch; ci += 2) {
+            const int c = ci * 32;
+            const int jmax = min(32, n_tile - c);
+            for (int jj = quad; jj < jmax; jj += 4) {
+              float4* src = reinterpret_cast<float4*>(rslot + (long)(c + jj) * BM + hoff) + lane;
+              *reinterpret_cast<float4*>(stage_buf + jj * 128 + 4 * lane) = __ldcg(src);
+              __stcg(src, make_float4(0.f, 0.f, 0.f, 0.f));
+            }
+            asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+            const int jv = min(jmax, epi.m_tokens - tok0 - c);
+            write_chunk<KIND>(epi, m0 + hoff + 4 * lane, tok0 + c, quad, jv, stage_buf + 4 * lane);
+            asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+          }
+          if (leader) counters[REDX_CNT + gf] = 0;
+        }
+      } else if (split) {
         __threadfence();
         asm volatile("bar.sync 3, 256;" ::: "memory");
         if (leader) atomicAdd(&counters[2 * gf], 1);
@@ -482,7 +519,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int t = t_first; t <= t_last; ++t) {
       const long long tb = (long long)t * sk.KB;
       const int gf = sk.cta_of(tb), gl = sk.cta_of(tb + sk.KB - 1);
-      if (gf == gl || (KIND == EPI_RESID && sk.red)) continue;
+      if (gf == gl || (KIND == EPI_RESID && sk.red) || (KIND != EPI_RESID && epi.red_scratch != nullptr)) continue;
       const int nseg = gl - gf + 1, p = g - gf;
       if (leader) {
         volatile int* cnt = counters + 2 * gf;
@@ -554,6 +591,7 @@ int g_unsplit_min = 64;   // tuning key 9: tile count from which each tile gets 
 int g_wide = 1;   // tuning key 7: 0 auto, 1 never use 256-row tiles (default: measured slower), 2 always
 int g_mc = 1;     // tuning key 16: cluster size of the one-tile-per-CTA schedule (multicast activations)
 int g_aligned_split = 1;   // tuning key 17: tile-aligned split-K instead of stream-K when it fills >= 70% of SMs
+int g_redx = 1;            // tuning key 19: honour epi.red_scratch (red.add split tiles + last-arriver epilogue)
 int g_decoupled = 2;       // tuning key 18: decoupled weight / activation rings (one tile per CTA);
                            // value = activation stages (>= 2), 0 = off
 
@@ -627,7 +665,13 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   // automatic schedule: enough weight tiles -> one CTA per tile (no split-K fixup); few tiles
   // (the d x d projections) -> stream-K over every SM
   const long long tiles = (long long)m_tiles * tok_tiles;
-  if (max_ctas == 0 && tiles >= g_unsplit_min && tiles <= G) G = (int)tiles;
+  // red mode (epi.red_scratch): split tiles need no fix-up wait, so one-wave projections keep
+  // stream-K over every SM instead of one CTA per tile
+  const bool redx_ok = epi.red_scratch != nullptr && epi.kind != EPI_RESID && !g_deterministic && g_redx &&
+                       H == 1 && counters != nullptr;
+  GemmEpi ep = epi;                       // what the kernel sees: red mode only where usable
+  if (!redx_ok) ep.red_scratch = nullptr;
+  if (max_ctas == 0 && tiles >= g_unsplit_min && tiles <= G && !redx_ok) G = (int)tiles;
   // split tiles reduce through the workspace with <= 8 participants, except RESID (red.add into
   // the residual, any number of participants; >= 2 k-blocks per CTA)
   const bool red = epi.kind == EPI_RESID && !g_deterministic;
@@ -698,12 +742,12 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
     }                                                                                                 \
     if (mc > 1)                                                                                       \
       return launch_chain_cluster(gemm_bf16_tc<K, 1>, dim3(grid), dim3(GEMM_THREADS), smem, stream, mc, wpp, \
-                                  xpp, epi, sk, n_tile, stages, ws, counters, rla);                   \
+                                  xpp, ep, sk, n_tile, stages, ws, counters, rla);                    \
     if (H == 2)                                                                                       \
       return launch_chain(gemm_bf16_tc<K, 2>, dim3(grid), dim3(GEMM_THREADS), smem, stream, g_coop != 0, wpp,    \
-                          xpp, epi, sk, n_tile, stages, ws, counters, rla);                           \
+                          xpp, ep, sk, n_tile, stages, ws, counters, rla);                            \
     return launch_chain(gemm_bf16_tc<K, 1>, dim3(grid), dim3(GEMM_THREADS), smem, stream, g_coop != 0, wpp, xpp, \
-                        epi, sk, n_tile, stages, ws, counters, rla);                                  \
+                        ep, sk, n_tile, stages, ws, counters, rla);                                   \
   }
   switch (epi.kind) {
     VLC_GEMM_KIND(EPI_F32)

@@ -34,7 +34,7 @@ def _epi(nat, **kw):
 def _gemm(nat, W, X, m, epi, splits=1):
     """W [n_pad, k_pad] and X [rows, k_pad] row-major bf16 -> packed operands -> vlc_gemm_bf16."""
     ws = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
-    cnt = torch.zeros(4096, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(16384, dtype=torch.int32, device="cuda")
     R = nat.row_tile(m)
     Wp = nat.pack(W, 128)
     Xp = nat.pack(X[:m], R, rows_cap=-(-m // R) * R)
@@ -303,6 +303,36 @@ def test_attention_pp_softmax_variants(nat, var, heads, nkeys, nq):
         test_attention_pp_matches_torch(nat, 128, heads, nkeys, nq, True, var=var)
     finally:
         nat.load().vlc_set_tuning(15, attn_kernel_variant())
+
+
+@pytest.mark.parametrize("n_pad,k_pad,m,splits", [(10752, 3584, 236, 0), (14336, 3584, 236, 0), (1024, 512, 100, 0),
+                                                  (384, 512, 100, 3), (1280, 768, 600, 7)])
+def test_gemm_red_scratch_f32_swiglu(nat, n_pad, k_pad, m, splits):
+    """epi.red_scratch: split tiles reduced by red.add into a zero-maintained scratch, finished by the
+    last-arriving CTA (fp32 logits-style and packed SwiGLU outputs); the scratch is left zero."""
+    g = torch.Generator(device="cuda").manual_seed(n_pad + 7 * m)
+    W = torch.randn(n_pad, k_pad, device="cuda", generator=g).bfloat16()
+    X = torch.randn(max(256, m), k_pad, device="cuda", generator=g).bfloat16()
+    scratch = torch.zeros(148 * 128 * 256, device="cuda")
+    out = torch.full((m, n_pad), float("nan"), device="cuda")
+    epi = _epi(nat, kind=nat.EPI_F32, n_valid=n_pad, m_tokens=m, out=out.data_ptr(), ldo=n_pad,
+               red_scratch=scratch.data_ptr())
+    for _ in range(2):   # twice: scratch and counters must be left clean
+        _gemm(nat, W, X, m, epi, splits)
+        ref = X[:m].float() @ W.float().t()
+        assert (out - ref).abs().max().item() / ref.abs().max().item() < 1e-5
+    assert scratch.abs().sum().item() == 0
+    R = nat.row_tile(m)
+    hp = torch.zeros(nat.packed_numel(m, n_pad // 2, R), device="cuda", dtype=torch.bfloat16)
+    sw = _epi(nat, kind=nat.EPI_SWIGLU, n_valid=n_pad, m_tokens=m, out=hp.data_ptr(), ldo=n_pad // 2, pk_rows=R,
+              pk_kb=-(-(n_pad // 2) // 128), red_scratch=scratch.data_ptr())
+    _gemm(nat, W, X, m, sw, splits)
+    acc = X[:m].float() @ W.float().t()
+    gate, up = acc[:, 0::2], acc[:, 1::2]
+    ref = (torch.nn.functional.silu(gate) * up)
+    got = nat.unpack(hp, m, n_pad // 2, R).float()
+    assert (got - ref).abs().max().item() / ref.abs().max().item() < 2e-2
+    assert scratch.abs().sum().item() == 0
 
 
 @pytest.mark.parametrize("mc", [2, 4])

@@ -12,7 +12,10 @@ ws = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 cnt = torch.zeros(1 << 16, dtype=torch.int32, device="cuda")
 
 
-def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1, packed=False, mode=0):
+RED = torch.zeros(148 * 128 * 256, device="cuda")
+
+
+def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1, packed=False, mode=0, red=False):
     nw = max(2, min(8, (1 << 30) // (n * k * 2)))   # rotate > L2 worth of weights
     Ws = [N.pack(torch.randn(n, k, device="cuda").bfloat16(), 128) for _ in range(nw)]
     R = N.row_tile(m)
@@ -21,6 +24,8 @@ def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1, packed=Fals
     out = torch.zeros(m + 256, n, device="cuda", dtype=torch.float32)
     e = N.Epilogue()
     e.kind, e.n_valid, e.m_tokens, e.out, e.ldo = kind, n, m, out.data_ptr(), n
+    if red:
+        e.red_scratch = RED.data_ptr()
     lib.vlc_set_tuning(1, stages)
     lib.vlc_set_tuning(2, coop)
     s = torch.cuda.current_stream().cuda_stream
@@ -124,6 +129,21 @@ if __name__ == "__main__":
             mhz = cyc / (d[:, 6] - d[:, 5]) * 1e3
             print(f"N={n}: mainloop {np.median(d[:, 6] - d[:, 5]) / 1e3:.2f} us, {np.median(cyc):.0f} cycles, "
                   f"SM clock {np.median(mhz):.0f} MHz (min {mhz.min():.0f})", flush=True)
+    if mode == "wide":            # 256-row tiles (H = 2) under stream-K over every SM (fix-up path)
+        for wide, um in ((1, 64), (2, 64), (1, 1000), (2, 1000)):
+            lib.vlc_set_tuning(7, wide)
+            lib.vlc_set_tuning(9, um)
+            print(f"-- wide {wide} unsplit_min {um}", flush=True)
+            for (n, kk, m) in ((10752, 3584, 236), (14336, 3584, 236)):
+                run(n, kk, m, 0)
+                phases(n, kk, m, 0)
+        lib.vlc_set_tuning(7, 1)
+        lib.vlc_set_tuning(9, 64)
+    if mode == "redx":            # one-wave projections: one CTA per tile vs stream-K with red.add split tiles
+        for red in (False, True, False, True):
+            print(f"-- red_scratch {red}", flush=True)
+            for (n, kk, m) in ((10752, 3584, 236), (14336, 3584, 236), (14336, 3584, 112), (3584, 3584, 236)):
+                run(n, kk, m, 0, red=red)
     if mode == "residctas":       # stream-K RESID GEMMs at fewer CTAs (fewer split segments -> less red.add)
         for c in (148, 128, 112, 96, 74):
             for (n, kk, m) in ((3584, 3584, 236), (3584, 7168, 236)):
