@@ -89,7 +89,7 @@ typedef struct vlc_epilogue {
    * GEMM's spare bandwidth instead of on the critical path.  NULL / 0 = off.                  */
   const void* l2_prefetch;
   unsigned long long l2_prefetch_bytes;
-  /* optional (non-RESID kinds): zero-maintained fp32 scratch of >= max_ctas * 128 * 256 floats (all
+  /* optional (kinds other than RESID / QKV_ROPE): zero-maintained fp32 scratch of >= max_ctas * 128 * 256 floats (all
    * zero on entry; the kernel leaves it zero).  With it, a weight tile whose k-range is split across
    * CTAs is reduced with red.add into the scratch and finished by its last-arriving CTA (no partial
    * workspace, no waiting), which lets one-wave projections (QKV: 84 tiles) use every SM.      */

@@ -447,7 +447,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int hoff = H == 2 ? eg * 128 : 0;                 // weight-row offset of this group
       const bool split = gf != gl && !(KIND == EPI_RESID && sk.red);   // RESID partials: red.add in L2
       // red mode: the split tile's partials meet in the zero-maintained scratch slot of its first CTA
-      const bool redx = split && KIND != EPI_RESID && epi.red_scratch != nullptr;
+      // (not compiled for QKV_ROPE: its second epilogue instance spilled the hot one's registers)
+      const bool redx = KIND != EPI_RESID && KIND != EPI_QKV_ROPE && split && epi.red_scratch != nullptr;
       float* rslot = redx ? epi.red_scratch + (long)gf * BM * n_tile : nullptr;   // [n_tile][BM]
       float* part = split && !redx ? ws + (2L * g + (t == t_first ? 0 : 1)) * (long)n_tile * BM : nullptr;
       const int nch = (n_tile + 31) / 32;
@@ -519,7 +520,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int t = t_first; t <= t_last; ++t) {
       const long long tb = (long long)t * sk.KB;
       const int gf = sk.cta_of(tb), gl = sk.cta_of(tb + sk.KB - 1);
-      if (gf == gl || (KIND == EPI_RESID && sk.red) || (KIND != EPI_RESID && epi.red_scratch != nullptr)) continue;
+      if (gf == gl || (KIND == EPI_RESID && sk.red) ||
+          (KIND != EPI_RESID && KIND != EPI_QKV_ROPE && epi.red_scratch != nullptr))
+        continue;
       const int nseg = gl - gf + 1, p = g - gf;
       if (leader) {
         volatile int* cnt = counters + 2 * gf;
@@ -667,8 +670,8 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   const long long tiles = (long long)m_tiles * tok_tiles;
   // red mode (epi.red_scratch): split tiles need no fix-up wait, so one-wave projections keep
   // stream-K over every SM instead of one CTA per tile
-  const bool redx_ok = epi.red_scratch != nullptr && epi.kind != EPI_RESID && !g_deterministic && g_redx &&
-                       H == 1 && counters != nullptr;
+  const bool redx_ok = epi.red_scratch != nullptr && epi.kind != EPI_RESID && epi.kind != EPI_QKV_ROPE &&
+                       !g_deterministic && g_redx && H == 1 && counters != nullptr;
   GemmEpi ep = epi;                       // what the kernel sees: red mode only where usable
   if (!redx_ok) ep.red_scratch = nullptr;
   if (max_ctas == 0 && tiles >= g_unsplit_min && tiles <= G && !redx_ok) G = (int)tiles;
