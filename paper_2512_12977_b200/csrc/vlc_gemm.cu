@@ -593,7 +593,8 @@ int g_pair = 96;          // tuning key 10: CTA-pair GEMM for non-RESID kinds wh
 int g_unsplit_min = 64;   // tuning key 9: tile count from which each tile gets its own CTA (no split-K)
 int g_wide = 1;   // tuning key 7: 0 auto, 1 never use 256-row tiles (default: measured slower), 2 always
 int g_mc = 1;     // tuning key 16: cluster size of the one-tile-per-CTA schedule (multicast activations)
-int g_aligned_split = 1;   // tuning key 17: tile-aligned split-K instead of stream-K when it fills >= 70% of SMs
+int g_aligned_split = 2;   // tuning key 17: tile-aligned split-K instead of stream-K when it fills >= 70% of SMs
+                           // (1: split count divides the k-blocks, 2: any split count -- 140 CTAs on C3)
 int g_redx = 1;            // tuning key 19: honour epi.red_scratch (red.add split tiles + last-arriver epilogue)
 int g_decoupled = 2;       // tuning key 18: decoupled weight / activation rings (one tile per CTA);
                            // value = activation stages (>= 2), 0 = off
@@ -682,10 +683,12 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   // Tile-aligned split-K when it keeps >= 70% of the SMs: every CTA then owns exactly one k-range
   // of one tile (one epilogue, no CTA waiting on a second tile's partial) -- measured on the C3
   // O / down projections: 148 stream-K CTAs 16.4 / 21.8 us, 112 aligned CTAs 14.0 / 19.9 us.
+  // (g_aligned_split == 2: the split count need not divide the k-blocks -- G = tiles * s still puts
+  // every CTA boundary of a tile on a tile boundary, ranges of floor / ceil(KB / s) k-blocks)
   if (max_ctas == 0 && g_aligned_split && tiles < G) {
     int best = 0;
     for (int sp = 2; sp <= KB / min_units; ++sp)
-      if (KB % sp == 0 && tiles * sp <= G) best = sp;
+      if ((KB % sp == 0 || g_aligned_split == 2) && tiles * sp <= G) best = sp;
     if (best > 0 && tiles * best * 10 >= 7LL * G) G = (int)(tiles * best);
   }
   if ((long long)G * min_units > U) G = (int)(U / min_units);

@@ -186,6 +186,11 @@ class Runner:
         self.lib.vlc_set_tuning(14, int(__import__("os").environ.get("VLC_RELOC_WIDE", "100000")))
         # attention kernel variant matching the layout's work decomposition (layout.ATTN_ONE_TILE)
         self.lib.vlc_set_tuning(15, attn_kernel_variant())
+        # experiments: VLC_TUNING="key=value,..." applied last (vlc_set_tuning)
+        for kv_ in __import__("os").environ.get("VLC_TUNING", "").split(","):
+            if "=" in kv_:
+                k_, v_ = kv_.split("=", 1)
+                self.lib.vlc_set_tuning(int(k_), int(v_))
         self.tp_group = None       # head-parallel process group (engine sets it from the model)
         self._side = None          # side stream of the overlapped kv_relocate
 

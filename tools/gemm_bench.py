@@ -144,6 +144,13 @@ if __name__ == "__main__":
             print(f"-- red_scratch {red}", flush=True)
             for (n, kk, m) in ((10752, 3584, 236), (14336, 3584, 236), (14336, 3584, 112), (3584, 3584, 236)):
                 run(n, kk, m, 0, red=red)
+    if mode == "aligned":         # tile-aligned split-K: divisor splits (key 17 = 1) vs any split (2)
+        for al in (1, 2, 1, 2):
+            lib.vlc_set_tuning(17, al)
+            print(f"-- aligned {al}", flush=True)
+            for (n, kk, m) in ((3584, 3584, 236), (3584, 7168, 236)):
+                run(n, kk, m, 0, kind=N.EPI_RESID)
+        lib.vlc_set_tuning(17, 1)
     if mode == "residctas":       # stream-K RESID GEMMs at fewer CTAs (fewer split segments -> less red.add)
         for c in (148, 128, 112, 96, 74):
             for (n, kk, m) in ((3584, 3584, 236), (3584, 7168, 236)):
