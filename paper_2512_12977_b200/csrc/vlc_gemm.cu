@@ -684,11 +684,12 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   // of one tile (one epilogue, no CTA waiting on a second tile's partial) -- measured on the C3
   // O / down projections: 148 stream-K CTAs 16.4 / 21.8 us, 112 aligned CTAs 14.0 / 19.9 us.
   // (g_aligned_split == 2: the split count need not divide the k-blocks -- G = tiles * s still puts
-  // every CTA boundary of a tile on a tile boundary, ranges of floor / ceil(KB / s) k-blocks)
+  // every CTA boundary of a tile on a tile boundary, ranges of floor / ceil(KB / s) k-blocks; only for
+  // token tiles >= 160: at c = 112 the extra CTAs cost more than they bring, 3.64 -> 3.85 ms TTFT)
   if (max_ctas == 0 && g_aligned_split && tiles < G) {
     int best = 0;
     for (int sp = 2; sp <= KB / min_units; ++sp)
-      if ((KB % sp == 0 || g_aligned_split == 2) && tiles * sp <= G) best = sp;
+      if ((KB % sp == 0 || (g_aligned_split == 2 && n_tile >= 160)) && tiles * sp <= G) best = sp;
     if (best > 0 && tiles * best * 10 >= 7LL * G) G = (int)(tiles * best);
   }
   if ((long long)G * min_units > U) G = (int)(U / min_units);
