@@ -433,6 +433,11 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
   constexpr bool PSM = C::PSM;
   constexpr int SW = R::SW, NTH = R::THREADS;
   static_assert(!R::ONE || KT == 128, "single-tile mode: 128-key tiles");
+  // OSPLIT (VAR 0x20000, single tile, two threads per row): each column half of the row keeps its
+  // own running max / sum and its own O accumulator (O0, O1 in the TMEM columns the second tile
+  // would use), so the per-iteration row-max exchange disappears; the halves merge once at the end.
+  constexpr bool OSPLIT = (VAR & 0x20000) != 0;
+  static_assert(!OSPLIT || (R::ONE && SW == 2 && HD == 128), "O split: single tile, two threads per row");
   static_assert(!(PSM && SW == 2), "P-in-smem is a one-warp-per-row variant");
   static_assert(SW == 1 || KT == 128, "two threads per row: 128-key tiles");
   constexpr int PP_KT = KT;
@@ -567,9 +572,14 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
 #pragma unroll
         for (int k = 0; k < PP_KT / 16; ++k) {
           const uint64_t bd = make_sdesc(v_addr + k * 16 * C::SWZ, C::KV_ATOM, 8 * C::SWZ, C::SWZ);
-          if (!(VAR & 0x200))
-            tc_mma_f16_ts(tmem + C::o_col(x), tmem + C::s_col(x, C::sbuf(j)) + k * 8, bd, idesc_o,
-                          (j > 0 || k > 0) ? 1u : 0u);
+          if (!(VAR & 0x200)) {
+            if (OSPLIT)   // keys of column half k>>2 accumulate into O_(k>>2); P of half h at S cols 64h..
+              tc_mma_f16_ts(tmem + C::o_col(k >> 2), tmem + C::s_col(x, C::sbuf(j)) + k * 8 + (k >> 2) * 32, bd,
+                            idesc_o, (j > 0 || (k & 3) > 0) ? 1u : 0u);
+            else
+              tc_mma_f16_ts(tmem + C::o_col(x), tmem + C::s_col(x, C::sbuf(j)) + k * 8, bd, idesc_o,
+                            (j > 0 || k > 0) ? 1u : 0u);
+          }
         }
         tc_commit(&o_done[x]);
       };
@@ -655,7 +665,7 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
     const int qp = q_valid ? a.qpos[q_row0 + x * 128 + r] : -1;
     const int ntx = nt_t[x];
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const uint32_t tO = tmem + C::o_col(x) + lane_off;
+    const uint32_t tO = tmem + C::o_col(OSPLIT ? hh : x) + lane_off;   // OSPLIT: this half's O
     const float NEG_INF = -INFINITY;
     float m_run = NEG_INF, l_run = 0.f;
     for (int j = 0; j < ntx; ++j) {
@@ -700,7 +710,7 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
         for (int i = 0; i < CW; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], s[i]);
       }
       float pmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-      if constexpr (SW > 1) {
+      if constexpr (SW > 1 && !OSPLIT) {
         // the other row parts' maxima; the barrier also orders every part's S reads before any P
         // write into S's columns (P of an upper part lands in a lower part's S columns)
         float* xb = xm + ((j & 1) * R::NTILE + x) * (SW * 128);
@@ -732,14 +742,16 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
       }
       if (resc) {
         const float sc = (need && has_o) ? fast_exp2(m_run - m_new) : 1.0f;
+        constexpr int RW = OSPLIT ? HD : OW;          // O columns this thread rescales
+        const uint32_t tR = OSPLIT ? tO : tO + hh * OW;
 #pragma unroll
-        for (int c = 0; c < OW / 16; ++c) {
+        for (int c = 0; c < RW / 16; ++c) {
           float o[16];
-          tmem_ld16(tO + hh * OW + c * 16, o);
+          tmem_ld16(tR + c * 16, o);
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 16; ++i) o[i] *= sc;
-          tmem_st16(tO + hh * OW + c * 16, o);
+          tmem_st16(tR + c * 16, o);
         }
         tmem_wait_st();
       }
@@ -812,7 +824,9 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
       } else {
         if constexpr (CW >= 64) {
 #pragma unroll
-          for (int c = 0; c < CW / 64; ++c) tmem_st32f(tS + hh * (CW / 2) + 32 * c, s + 32 * c);   // P(j) over S(j)'s first cols
+          // P(j) over S(j)'s first cols (OSPLIT: over this half's own S columns -- no exchange barrier
+          // orders the other half's S reads)
+          for (int c = 0; c < CW / 64; ++c) tmem_st32f(tS + hh * (OSPLIT ? CW : CW / 2) + 32 * c, s + 32 * c);
         } else {
           tmem_st16(tS + hh * (CW / 2), s);
         }
@@ -828,7 +842,19 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
       mbar_wait(&o_done[x], (ntx - 1) & 1);
       tc_fence_after();
     }
-    if constexpr (SW > 1) {   // row sum = all parts' sums (exchange buffer of iteration ntx: free)
+    float w_own = 1.f, w_oth = 0.f;   // OSPLIT: weights of O_own / O_other in the merged row
+    if constexpr (OSPLIT) {
+      // merge the two halves' (max, sum): M = max, w_h = 2^(m_h - M), L = w0 l0 + w1 l1
+      xm[hh * 128 + r] = m_run;
+      xm[256 + hh * 128 + r] = l_run;
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + x), "r"(256) : "memory");
+      const float m_o = xm[(1 - hh) * 128 + r], l_o = xm[256 + (1 - hh) * 128 + r];
+      const float M = fmaxf(m_run, m_o);
+      w_own = m_run == -INFINITY ? 0.f : fast_exp2(m_run - M);
+      w_oth = m_o == -INFINITY ? 0.f : fast_exp2(m_o - M);
+      l_run = w_own * l_run + w_oth * l_o;
+      m_run = M;
+    } else if constexpr (SW > 1) {   // row sum = all parts' sums (exchange buffer of iteration ntx: free)
       float* xb = xm + ((ntx & 1) * R::NTILE + x) * (SW * 128);
       xb[hh * 128 + r] = l_run;
       asm volatile("bar.sync %0, %1;" ::"r"(1 + x), "r"(128 * SW) : "memory");
@@ -839,6 +865,20 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
     }
     if (r == 0 && hh == 0) adbg(dbgp, 3 + x);
     const int qrow = q_row0 + x * 128 + r;
+    // 16 O columns (chunk c of this thread's OW) of the row: OSPLIT merges O_own and O_other
+    auto load_o = [&](int c, float* o) {
+      if constexpr (OSPLIT) {
+        float o2[16];
+        tmem_ld16(tmem + C::o_col(hh) + lane_off + hh * OW + c * 16, o);
+        tmem_ld16(tmem + C::o_col(1 - hh) + lane_off + hh * OW + c * 16, o2);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) o[i] = w_own * o[i] + w_oth * o2[i];
+      } else {
+        tmem_ld16(tO + hh * OW + c * 16, o);
+        tmem_wait_ld();
+      }
+    };
     if (group < 0) {
       const float inv = (l_run > 0.f) ? 1.0f / l_run : 0.f;
       const int orow_i = q_valid ? a.rowof[qrow] : 0;
@@ -847,8 +887,7 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
       for (int c = 0; c < OW / 16; ++c) {
         float o[16];
         if (ntx > 0) {
-          tmem_ld16(tO + hh * OW + c * 16, o);
-          tmem_wait_ld();
+          load_o(c, o);
         } else {
 #pragma unroll
           for (int i = 0; i < 16; ++i) o[i] = 0.f;
@@ -878,8 +917,7 @@ __global__ void __launch_bounds__(PPRoles<VAR>::THREADS, 1)
         for (int c = 0; c < OW / 16; ++c) {
           float o[16];
           if (ntx > 0) {
-            tmem_ld16(tO + hh * OW + c * 16, o);
-            tmem_wait_ld();
+            load_o(c, o);
           } else {
 #pragma unroll
             for (int i = 0; i < 16; ++i) o[i] = 0.f;
@@ -1050,6 +1088,7 @@ cudaError_t launch_attention_pp(const vlc_attn_args& a, cudaStream_t stream, boo
         case 36: return launch_pp_hd<128, 128, 0xC001>(a, stream, coop);   // single tile, two threads per row
         case 37: return launch_pp_hd<128, 128, 0x1C001>(a, stream, coop);  // + f16x2 exponentials
         case 38: return launch_pp_hd<128, 128, 0x18001>(a, stream, coop);  // single tile, SW 4, f16x2
+        case 39: return launch_pp_hd<128, 128, 0x2C001>(a, stream, coop);  // single tile, SW 2, O per half
         // default: two threads per query row (PPRoles SW = 2), three-input max -- measured
         // 32.4 -> 31.8 us standalone, 5.25 -> 5.16 ms C3 TTFT (profiles/r1_attention_softmax_variants.txt)
         default: return launch_pp_hd<128, 128, 0x4001>(a, stream, coop);

@@ -155,9 +155,10 @@ ATTN_ONE_TILE = bool(int(os.environ.get("VLC_ATTN_ONE", "1")))
 
 
 def attn_kernel_variant() -> int:
-    """vlc_set_tuning(15, .) value matching ATTN_ONE_TILE (36: single tile, two softmax threads per row;
+    """vlc_set_tuning(15, .) value matching ATTN_ONE_TILE (39: single tile, two softmax threads per row,
+    each column half with its own max / sum / O accumulator;
     0: ping-pong)."""
-    return 36 if ATTN_ONE_TILE else 0
+    return 39 if ATTN_ONE_TILE else 0
 
 
 def attention_work(q_ranges, qpos, n_req, heads, max_ctas: int = 148):

@@ -293,7 +293,7 @@ def test_attention_pp_matches_torch(nat, hd, heads, nkeys, nq, causal, var=None)
     assert torch.equal(nat.unpack(outp, nq, kv, R), out)
 
 
-@pytest.mark.parametrize("var", [0, 30, 31, 36, 37, 100, 1, 16, 17, 20, 22])
+@pytest.mark.parametrize("var", [0, 30, 31, 36, 37, 39, 100, 1, 16, 17, 20, 22])
 @pytest.mark.parametrize("heads,nkeys,nq", [(28, 4128, 236), (2, 1000, 150), (4, 300, 300), (1, 4128, 600)])
 def test_attention_pp_softmax_variants(nat, var, heads, nkeys, nq):
     """hd-128 / 128-key kernel variants (tuning key 15): ping-pong with 1 or 2 threads per row,

@@ -76,7 +76,7 @@ def phases(var=11):
     """VAR 0x400 (tuning 15 = 11): per-phase clock64 cycles summed over all CTAs (one thread per
     query tile for the softmax phases, the MMA thread for its phases)."""
     global ONE
-    ONE = var in (30, 31, 32, 33, 34, 35, 36, 37, 38)
+    ONE = var in (30, 31, 32, 33, 34, 35, 36, 37, 38, 39)
     lib.vlc_set_tuning(15, var)
     a, keep, n = setup(max_ctas=148)
     s = torch.cuda.current_stream().cuda_stream
@@ -104,7 +104,7 @@ if __name__ == "__main__":
     sys.exit(0)
   if len(sys.argv) > 1 and sys.argv[1] == "vars":   # softmax variants of the 128-key kernel (key 15)
     for v in [int(x) for x in sys.argv[2:]]:
-      ONE = v in (30, 31, 32, 33, 34, 35, 36, 37, 38)
+      ONE = v in (30, 31, 32, 33, 34, 35, 36, 37, 38, 39)
       lib.vlc_set_tuning(15, v)
       print(f"== softmax variant {v}", flush=True)
       run(148)

@@ -10,7 +10,7 @@ import attn_bench as ab  # noqa: E402  (runs its own timing first)
 
 if len(sys.argv) > 1:
     ab.lib.vlc_set_tuning(15, int(sys.argv[1]))
-    ab.ONE = int(sys.argv[1]) in (30, 31, 32, 33, 34, 35, 36, 37, 38)
+    ab.ONE = int(sys.argv[1]) in (30, 31, 32, 33, 34, 35, 36, 37, 38, 39)
 a, keep, n = ab.setup()
 buf = torch.zeros(256, dtype=torch.int64, device="cuda")
 ab.lib.vlc_set_trace_buffer(buf.data_ptr())
