@@ -291,7 +291,7 @@ def _resolve(model: ToyVLM, request: ReuseRequest, store: CacheStore, miss_base:
                 metrics.fallback_images += 1
                 keep[:, m] = T
     text_pos, text_ids = _text_tokens(seq, cfg)
-    counts = [len(text_pos) + int(keep[i].sum()) for i in range(L)]
+    counts = (len(text_pos) + keep.sum(axis=1)).tolist()   # one numpy reduction, not one per layer
     metrics.computed_per_layer = counts
     metrics.flops = _flops_from_counts(counts, len(seq), cfg, metrics.encoder_misses)
     spec = RequestSpec(n=len(seq), text_pos=text_pos, text_ids=text_ids,

@@ -86,13 +86,25 @@ class IntPack:
         if (-a.size) % 4:
             self.parts.append(np.zeros((-a.size) % 4, np.int32))
 
+    def _full_host(self):
+        """The whole int32 buffer: the (shared, read-only) template with the per-call patches."""
+        host = getattr(self, "host", None)
+        if host is None:
+            return np.concatenate(self.parts) if self.parts else np.zeros(4, np.int32)
+        patches = getattr(self, "patches", None)
+        if not patches:
+            return host
+        host = host.copy()
+        for name, arr in patches.items():
+            o, n = self.off[name]
+            host[o:o + n] = arr
+        return host
+
     def upload(self, ws: Workspace, key: str):
         """One async H2D copy through a persistent pinned staging buffer of the workspace (no
         per-call pinned allocation); the staging buffer is reused once its last copy completed."""
         torch = _torch()
-        host = getattr(self, "host", None)
-        if host is None:
-            host = np.concatenate(self.parts) if self.parts else np.zeros(4, np.int32)
+        host = self._full_host()
         n = max(4, host.size)
         dev = ws.get(key, (n,), torch.int32, zero=False)
         pin, ev = ws.pinned.get(key, (None, None))
@@ -126,8 +138,13 @@ class IntPack:
         if sum(n for _, n in spans) >= (hi - lo) * 3 // 4:
             spans = [(lo, hi - lo)]
         nbytes = 0
+        patches = getattr(self, "patches", None) or {}
         for o, n in spans:
-            pn[o:o + n] = self.host[o:o + n]
+            pn[o:o + n] = self.host[o:o + n]          # template (structural values)
+            for name, arr in patches.items():          # per-call segments inside the span
+                po, pn_ = self.off[name]
+                if o <= po and po + pn_ <= o + n:
+                    pn[po:po + pn_] = arr
             dev[o:o + n].copy_(pin[o:o + n], non_blocking=True)
             nbytes += 4 * n
         ws.last_h2d_bytes = nbytes
@@ -472,13 +489,12 @@ class Runner:
             pk.add("final", lay.final_rows)
             tpl = lay._pack_tpl = (np.concatenate(pk.parts), dict(pk.off))
         host, off = tpl
-        host = host.copy()
-        o, n = off["src"]
-        host[o:o + n] = lay.row_src.reshape(-1)
-        o, n = off["pages"]
-        host[o:o + n] = lay.page_table.reshape(-1)
         pk = IntPack()
+        # the template stays shared and unmodified; the per-call segments travel as patches (the
+        # structure-resident path uploads only them, no copy of the whole ~0.5 MB template)
         pk.host, pk.off = host, off
+        pk.patches = {"src": lay.row_src.reshape(-1).astype(np.int32, copy=False),
+                      "pages": lay.page_table.reshape(-1).astype(np.int32, copy=False)}
         return pk
 
     def _allreduce(self, t):
