@@ -126,8 +126,12 @@ typedef struct vlc_attn_args {
 
 const char* vlc_last_error(void);
 int vlc_version(void);
-/* Tuning knobs for experiments: key 1 = GEMM pipeline stages (0 = automatic); keys 2-15 see
-   vlc_capi.cu (e.g. 15 = softmax variant of the hd-128 attention). */
+/* Asynchronous host -> device copy on `stream` (the per-call metadata upload of the host runtime:
+ * a direct cudaMemcpyAsync without a framework dispatch).  host should be pinned.            */
+int vlc_copy_h2d_async(void* device_dst, const void* host_src, size_t bytes, cudaStream_t stream);
+
+/* Tuning knobs for experiments: key 1 = GEMM pipeline stages (0 = automatic); keys 2-19 see
+   vlc_capi.cu and INTEGRATION.md (e.g. 15 = attention kernel variant). */
 int vlc_set_tuning(int key, int value);
 int vlc_set_debug_buffer(void* device_ptr);
 int vlc_set_trace_buffer(void* device_ptr);   /* experiments: attention CTA-0 event trace (>= 224 u64) */

@@ -107,6 +107,12 @@ int vlc_patchify_impl(const float*, int, int, void*, int, int, int, cudaStream_t
 const char* vlc_last_error(void) { return g_err; }
 
 /* Experiment knobs (not part of the stable ABI): key 1 = GEMM pipeline stages (0 = auto). */
+int vlc_copy_h2d_async(void* device_dst, const void* host_src, size_t bytes, cudaStream_t stream) {
+  if (bytes == 0) return VLC_OK;
+  if (!device_dst || !host_src) return fail(VLC_ERR_INVALID, "copy_h2d: null pointer");
+  return cuda_status(cudaMemcpyAsync(device_dst, host_src, bytes, cudaMemcpyHostToDevice, stream), "copy_h2d");
+}
+
 int vlc_set_tuning(int key, int value) {
   if (key == 1) { vlc::g_stage_override = value; return VLC_OK; }
   if (key == 2) { vlc::g_coop = value; return VLC_OK; }
