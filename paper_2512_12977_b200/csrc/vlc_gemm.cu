@@ -171,6 +171,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int t_first = (int)(u_begin / sk.KB);
   const int t_last = (u_end > u_begin) ? (int)((u_end - 1) / sk.KB) : t_first - 1;
   const int kb128 = H == 1 ? sk.KB : sk.KB / 2;   // 128-wide blocks per packed row tile
+  // decoupled mode: every CTA owns exactly one k-range [dkb0, dkb0 + dnkb) of one tile
+  const int dkb0 = (int)(u_begin - (long long)t_first * sk.KB), dnkb = (int)(u_end - u_begin);
 
   if (warp == 0 && lane == 0) {
     DBG(0);
@@ -215,11 +217,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       DBG(1);
       const uint64_t pol_w = policy_evict_first();
       const int mt = t_first % sk.m_tiles;
-      for (int kb = 0; kb < sk.KB; ++kb) {
-        const int st = kb % wst;
-        if (kb >= wst) mbar_wait(&empty[st], ((kb / wst) & 1) ^ 1);
+      for (int i = 0; i < dnkb; ++i) {
+        const int st = i % wst;
+        if (i >= wst) mbar_wait(&empty[st], ((i / wst) & 1) ^ 1);
         mbar_expect_tx(&full[st], a_bytes);
-        bulk_load(sa + st * a_bytes, a_src(mt, kb, 0), a_bytes, &full[st], pol_w);
+        bulk_load(sa + st * a_bytes, a_src(mt, dkb0 + i, 0), a_bytes, &full[st], pol_w);
       }
       DBG(2);
     }
@@ -231,7 +233,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int xper = sk.xh ? 2 : 1;   // activation slots per k-block
       long long c0 = 0;
       if (sk.dbg) { asm volatile("mov.u64 %0, %%clock64;" : "=l"(c0)); DBG(5); }
-      for (int kb = 0; kb < sk.KB; ++kb) {
+      for (int kb = 0; kb < dnkb; ++kb) {   // kb: index within this CTA's single k-range
         const int ws_ = kb % wst;
         mbar_wait(&full[ws_], (kb / wst) & 1);
         const uint32_t a_addr = smem_u32(sa + ws_ * a_bytes);
@@ -377,11 +379,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const uint64_t pol_x = policy_evict_last();
         const int tt = t_first / sk.m_tiles;
         const int xper = sk.xh ? 2 : 1;
-        for (int u = 0; u < sk.KB * xper; ++u) {
+        for (int u = 0; u < dnkb * xper; ++u) {
           const int st = u % xst;
           if (u >= xst) mbar_wait(&xempty[st], ((u / xst) & 1) ^ 1);
           mbar_expect_tx(&xfull[st], x_unit);
-          const uint8_t* src = xper == 2 ? b_src(tt, u >> 1) + (u & 1) * (n_tile * 128) : b_src(tt, u);
+          const int kbu = dkb0 + (xper == 2 ? (u >> 1) : u);
+          const uint8_t* src = xper == 2 ? b_src(tt, kbu) + (u & 1) * (n_tile * 128) : b_src(tt, kbu);
           bulk_load(sb + st * x_unit, src, x_unit, &xfull[st], pol_x);
         }
       }
@@ -710,8 +713,9 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   // (HBM-latency bound) gets every byte the activation ring (L2, 2 stages) leaves
   // (measured: QKV / gate-up at c = 236: 31.5 / 32.0 -> 29.9 / 29.6 us; slower at c = 112, where the
   // coupled ring already holds 3 stages -> only for token tiles >= 160)
-  if (g_decoupled && H == 1 && mc == 1 && n_tile >= 160 && G == (int)tiles && tiles * KB == U &&
-      !(rl && rl->n_blocks > 0)) {
+  // (also for tile-aligned split-K: G a multiple of the tile count -> one k-range of one tile per CTA)
+  if (g_decoupled && H == 1 && mc == 1 && n_tile >= 160 && G >= (int)tiles && G % (int)tiles == 0 &&
+      tiles * KB == U && U / G >= 2 && !(rl && rl->n_blocks > 0)) {
     const int a_b = GEMM_BM * GEMM_BK * 2, b_b = n_tile * GEMM_BK * 2;
     const int budget = 232448 - 1024 - 512;
     // key 18 value v: v in [2, 9] activation k-block stages; v >= 10: (v - 10) half-k-block stages
