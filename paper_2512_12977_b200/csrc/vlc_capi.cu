@@ -124,6 +124,7 @@ int vlc_set_tuning(int key, int value) {
   if (key == 10) { vlc::g_pair = value; return VLC_OK; }
   if (key == 14) { vlc::g_reloc_wide = value; return VLC_OK; }
   if (key == 15) { vlc::g_attn_var = value; return VLC_OK; }
+  if (key == 20) { vlc::g_dec_min_tile = value; return VLC_OK; }
   if (key == 19) { vlc::g_redx = value; return VLC_OK; }
   if (key == 18) { vlc::g_decoupled = value; return VLC_OK; }
   if (key == 17) { vlc::g_aligned_split = value; return VLC_OK; }

@@ -599,8 +599,10 @@ int g_mc = 1;     // tuning key 16: cluster size of the one-tile-per-CTA schedul
 int g_aligned_split = 2;   // tuning key 17: tile-aligned split-K instead of stream-K when it fills >= 70% of SMs
                            // (1: split count divides the k-blocks, 2: any split count -- 140 CTAs on C3)
 int g_redx = 1;            // tuning key 19: honour epi.red_scratch (red.add split tiles + last-arriver epilogue)
-int g_decoupled = 2;       // tuning key 18: decoupled weight / activation rings (one tile per CTA);
-                           // value = activation stages (>= 2), 0 = off
+int g_dec_min_tile = 16;   // tuning key 20: smallest token tile that uses the decoupled rings
+int g_decoupled = 1;       // tuning key 18: decoupled weight / activation rings for single-k-range CTAs
+                           // (1: automatic activation depth, v >= 2: v stages, v >= 10: v-10 half-k-block
+                           // stages, 0: off)
 
 static int gemm_pick_stages(int n_tile, int H) {
   if (g_stage_override > 0) return g_stage_override;
@@ -714,13 +716,17 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   // (measured: QKV / gate-up at c = 236: 31.5 / 32.0 -> 29.9 / 29.6 us; slower at c = 112, where the
   // coupled ring already holds 3 stages -> only for token tiles >= 160)
   // (also for tile-aligned split-K: G a multiple of the tile count -> one k-range of one tile per CTA)
-  if (g_decoupled && H == 1 && mc == 1 && n_tile >= 160 && G >= (int)tiles && G % (int)tiles == 0 &&
+  if (g_decoupled && H == 1 && mc == 1 && n_tile >= g_dec_min_tile && G >= (int)tiles && G % (int)tiles == 0 &&
       tiles * KB == U && U / G >= 2 && !(rl && rl->n_blocks > 0)) {
     const int a_b = GEMM_BM * GEMM_BK * 2, b_b = n_tile * GEMM_BK * 2;
     const int budget = 232448 - 1024 - 512;
     // key 18 value v: v in [2, 9] activation k-block stages; v >= 10: (v - 10) half-k-block stages
     const int xh = g_decoupled >= 10 ? 1 : 0;
-    const int sx = xh ? (g_decoupled - 10 >= 2 ? g_decoupled - 10 : 2) : (g_decoupled >= 2 ? g_decoupled : 2);
+    // g_decoupled == 1: floor(100 KB / activation stage) >= 2 activation stages -- measured best on C3:
+    // 2 stages of 61 KB at c = 236, 3 of 28 KB at c = 112 (TTFT at r = 2%: 3.57 -> 3.49 ms)
+    const int sx_auto = 100 * 1024 / b_b < 2 ? 2 : 100 * 1024 / b_b;
+    const int sx = xh ? (g_decoupled - 10 >= 2 ? g_decoupled - 10 : 2)
+                      : (g_decoupled >= 2 ? g_decoupled : sx_auto);
     const int xu = xh ? b_b / 2 : b_b;
     const int sw = (budget - sx * xu) / a_b;
     if (sw >= 2 && sw * a_b >= 2 * 32 * 128 * 4) { sk.sw = sw > 8 ? 8 : sw; sk.sx = sx; sk.xh = xh; }

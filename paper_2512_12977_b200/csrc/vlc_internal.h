@@ -33,7 +33,8 @@ extern int g_unsplit_min;     // key 9: tiles >= this (and <= #SMs) -> one CTA p
 extern int g_wide;            // key 7: 256-row GEMM tiles (0 auto, 1 never, 2 always)
 extern int g_aligned_split;   // key 17: tile-aligned split-K for the multi-CTA-per-tile schedule
 extern int g_redx;            // key 19: red.add split-tile reduction with last-arriver epilogue
-extern int g_decoupled;       // key 18: decoupled weight / activation rings in the one-tile GEMM schedule
+extern int g_decoupled;
+extern int g_dec_min_tile;    // key 20: smallest token tile using the decoupled rings       // key 18: decoupled weight / activation rings in the one-tile GEMM schedule
 extern int g_mc;              // key 16: GEMM cluster size for multicast activation loads (1 = off)
 extern int g_pdl;             // key 6: programmatic dependent launch of the chain kernels (default 1)
 void set_debug_buffer(unsigned long long* p);

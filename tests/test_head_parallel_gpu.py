@@ -74,7 +74,7 @@ def _run_rank(rank, world, backend, port, q):
         dist.destroy_process_group()
 
 
-def _spawn(world, backend):
+def _spawn_once(world, backend):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -82,11 +82,26 @@ def _spawn(world, backend):
     procs = [ctx.Process(target=_run_rank, args=(r, world, backend, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    outs = dict(q.get(timeout=300) for _ in range(world))
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    try:
+        outs = dict(q.get(timeout=300) for _ in range(world))
+    finally:
+        for p in procs:
+            p.join(timeout=120)
+            if p.is_alive():
+                p.terminate()
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     return outs
+
+
+def _spawn(world, backend):
+    """One retry with a fresh rendezvous port: the port from _free_port() is released before the
+    ranks bind it, so another process on the box can take it in between (rendezvous failure, not a
+    result mismatch -- results are checked by the caller either way)."""
+    import queue
+    try:
+        return _spawn_once(world, backend)
+    except (queue.Empty, AssertionError):
+        return _spawn_once(world, backend)
 
 
 def _check(outs, ref):
