@@ -335,6 +335,30 @@ def test_gemm_red_scratch_f32_swiglu(nat, n_pad, k_pad, m, splits):
     assert scratch.abs().sum().item() == 0
 
 
+@pytest.mark.parametrize("dec", [0, 1, 3, 12])
+@pytest.mark.parametrize("n_pad,k_pad,m", [(10752, 3584, 236), (14336, 3584, 112), (3584, 7168, 236), (3584, 3584, 112)])
+def test_gemm_decoupled_rings_and_aligned_split(nat, dec, n_pad, k_pad, m):
+    """Schedules of the chain GEMMs: one CTA per tile and tile-aligned split-K (any split count),
+    with coupled rings (key 18 = 0) or decoupled weight / activation rings (automatic depth, 3
+    activation stages, 2 half-k-block activation stages)."""
+    lib = nat.load()
+    lib.vlc_set_tuning(18, dec)
+    lib.vlc_set_tuning(20, 16)
+    try:
+        test_gemm_f32_matches_torch(nat, n_pad, k_pad, m, 0)
+        g = torch.Generator(device="cuda").manual_seed(n_pad + m + 1)
+        W = torch.randn(n_pad, k_pad, device="cuda", generator=g).bfloat16()
+        X = torch.randn(max(256, m), k_pad, device="cuda", generator=g).bfloat16()
+        x = torch.randn(m, n_pad, device="cuda", generator=g)
+        x0 = x.clone()
+        _gemm(nat, W, X, m, _epi(nat, kind=nat.EPI_RESID, n_valid=n_pad, m_tokens=m, out=x.data_ptr(), ldo=n_pad), 0)
+        ref = x0 + X[:m].float() @ W.float().t()
+        assert (x - ref).abs().max().item() / ref.abs().max().item() < 1e-5
+    finally:
+        lib.vlc_set_tuning(18, 1)
+        lib.vlc_set_tuning(20, 16)
+
+
 @pytest.mark.parametrize("mc", [2, 4])
 @pytest.mark.parametrize("n_pad,k_pad,m", [(10752, 3584, 236), (1024, 512, 100), (512, 1024, 40)])
 def test_gemm_cluster_multicast(nat, mc, n_pad, k_pad, m):
