@@ -113,25 +113,29 @@ int vlc_copy_h2d_async(void* device_dst, const void* host_src, size_t bytes, cud
   return cuda_status(cudaMemcpyAsync(device_dst, host_src, bytes, cudaMemcpyHostToDevice, stream), "copy_h2d");
 }
 
+// Process-wide schedule / variant switches (experiments and tests; defaults = measured best,
+// INTEGRATION.md lists them).
 int vlc_set_tuning(int key, int value) {
-  if (key == 1) { vlc::g_stage_override = value; return VLC_OK; }
-  if (key == 2) { vlc::g_coop = value; return VLC_OK; }
-  if (key == 4) { vlc::set_attn_debug_buffer(nullptr); return VLC_OK; }
-  if (key == 5) { vlc::g_attn_min_smem = value; return VLC_OK; }
-  if (key == 6) { vlc::g_pdl = value; return VLC_OK; }
-  if (key == 7) { vlc::g_wide = value; return VLC_OK; }
-  if (key == 9) { vlc::g_unsplit_min = value; return VLC_OK; }
-  if (key == 10) { vlc::g_pair = value; return VLC_OK; }
-  if (key == 14) { vlc::g_reloc_wide = value; return VLC_OK; }
-  if (key == 15) { vlc::g_attn_var = value; return VLC_OK; }
-  if (key == 20) { vlc::g_dec_min_tile = value; return VLC_OK; }
-  if (key == 19) { vlc::g_redx = value; return VLC_OK; }
-  if (key == 18) { vlc::g_decoupled = value; return VLC_OK; }
-  if (key == 17) { vlc::g_aligned_split = value; return VLC_OK; }
-  if (key == 16) { vlc::g_mc = value >= 1 && value <= 8 ? value : 1; return VLC_OK; }
-  if (key == 13) { vlc::g_deterministic = value != 0; return VLC_OK; }
-  if (key == 12) { vlc::g_attn_kt = value == 64 ? 64 : 128; return VLC_OK; }
-  return fail(VLC_ERR_INVALID, "set_tuning: unknown key");
+  switch (key) {
+    case 1: vlc::g_stage_override = value; return VLC_OK;        // GEMM pipeline stages (0 = auto)
+    case 2: vlc::g_coop = value; return VLC_OK;                  // cooperative launch when PDL is off
+    case 4: vlc::set_attn_debug_buffer(nullptr); return VLC_OK;  // detach the attention debug buffer
+    case 5: vlc::g_attn_min_smem = value; return VLC_OK;         // attention smem lower bound (occupancy tests)
+    case 6: vlc::g_pdl = value; return VLC_OK;                   // programmatic dependent launch
+    case 7: vlc::g_wide = value; return VLC_OK;                  // 256-row GEMM tiles
+    case 9: vlc::g_unsplit_min = value; return VLC_OK;           // one-CTA-per-tile threshold
+    case 10: vlc::g_pair = value; return VLC_OK;                 // CTA-pair GEMM threshold
+    case 12: vlc::g_attn_kt = value == 64 ? 64 : 128; return VLC_OK;   // attention key tile (two-tile kernel)
+    case 13: vlc::g_deterministic = value != 0; return VLC_OK;   // bitwise-reproducible RESID reduction
+    case 14: vlc::g_reloc_wide = value; return VLC_OK;           // idle-SM relocation CTA smem (0 = plain)
+    case 15: vlc::g_attn_var = value; return VLC_OK;             // attention kernel variant
+    case 16: vlc::g_mc = value >= 1 && value <= 8 ? value : 1; return VLC_OK;   // GEMM cluster multicast
+    case 17: vlc::g_aligned_split = value; return VLC_OK;        // tile-aligned split-K
+    case 18: vlc::g_decoupled = value; return VLC_OK;            // decoupled weight / activation rings
+    case 19: vlc::g_redx = value; return VLC_OK;                 // honour vlc_epilogue.red_scratch
+    case 20: vlc::g_dec_min_tile = value; return VLC_OK;         // smallest token tile using key 18
+    default: return fail(VLC_ERR_INVALID, "set_tuning: unknown key");
+  }
 }
 /* Experiments only: device buffer (>= 224 u64) receiving per-iteration event times of attention CTA 0. */
 int vlc_set_trace_buffer(void* p) {
