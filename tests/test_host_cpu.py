@@ -268,3 +268,55 @@ def test_layout_rows_match_masks(pre, T, nimg, suf, ratios, hits):
     # every reused (layer, token) is relocated exactly once
     want = int((~masks).sum())
     assert lay.reloc_tokens == want
+
+
+@pytest.mark.parametrize("work", ["one", "pp"])
+@pytest.mark.parametrize("nq,nkeys,heads,reqs", [(236, 4128, 28, 1), (62, 1056, 12, 1), (44, 288, 8, 1),
+                                                 (600, 4128, 1, 1), (300, 300, 4, 1), (40, 300, 8, 3)])
+def test_attention_work_items_cover_every_visible_key(work, nq, nkeys, heads, reqs):
+    """Work decompositions of vlc_attn_pp: every (query, head) sees exactly its causal key range
+    [0, pos + 1) once across the splits of its unit; query tiles are <= 128 (single-tile kernel) /
+    <= 256 (ping-pong); split groups fit the co-residency budget (<= 148 CTAs) and <= 8 parts; the
+    parts of a group have consecutive indices with the group size in every item."""
+    import numpy as np
+    from paper_2512_12977_b200.layout import attention_work_one, attention_work_pp
+    rng = np.random.default_rng(nq + nkeys)
+    ranges, qpos, n_req, q0 = [], [], [], 0
+    for r in range(reqs):
+        n = nkeys
+        pos = np.sort(rng.permutation(n)[:nq]).astype(np.int32)
+        pos[-1] = n - 1
+        ranges.append((r, q0, nq))
+        qpos.append(pos)
+        n_req.append(n)
+        q0 += nq
+    qpos = np.concatenate(qpos)
+    fn = attention_work_one if work == "one" else attention_work_pp
+    it, groups = fn(ranges, qpos, np.array(n_req), heads)
+    tile = 128 if work == "one" else 256
+    assert (it[:, 1] <= tile).all() and (it[:, 1] > 0).all()
+    if groups:
+        assert len(it) <= 148
+    parts = {}
+    for row in it:
+        t0, nqt, h, _, kb, ke, grp, pk, req = (int(v) for v in row)
+        p, ns = pk >> 8, pk & 0xFF
+        assert 1 <= ns <= 8 and 0 <= p < ns
+        assert (grp < 0) == (ns == 1)
+        parts.setdefault((req, t0, h), []).append((kb, ke, p, ns, nqt))
+    for (req, t0, h), lst in parts.items():
+        lst.sort()
+        ns = lst[0][3]
+        assert len(lst) == ns and [x[2] for x in lst] == list(range(ns))
+        # contiguous, gap-free key cover from 0 to the tile's last visible key
+        assert lst[0][0] == 0
+        for a, b in zip(lst, lst[1:]):
+            assert a[1] == b[0]
+        nqt = lst[0][4]
+        assert lst[-1][1] == min(int(qpos[t0 + nqt - 1]) + 1, n_req[req])
+    # every query row of every request is covered by exactly one tile per head
+    for r, q0_, cnt in ranges:
+        for h in range(heads):
+            rows = sorted(t0 + i for (req, t0, hh), lst in parts.items() if req == r and hh == h
+                          for i in range(lst[0][4]))
+            assert rows == list(range(q0_, q0_ + cnt))
