@@ -320,3 +320,28 @@ def test_attention_work_items_cover_every_visible_key(work, nq, nkeys, heads, re
             rows = sorted(t0 + i for (req, t0, hh), lst in parts.items() if req == r and hh == h
                           for i in range(lst[0][4]))
             assert rows == list(range(q0_, q0_ + cnt))
+
+
+def test_int_pack_template_and_patches():
+    """Per-call metadata: the structural template is shared and left unmodified; the per-call
+    segments (token ids / page ids) travel as patches that the full upload applies."""
+    import numpy as np
+    from paper_2512_12977_b200.runtime import IntPack
+    pk = IntPack()
+    pk.add("src", np.arange(10))
+    pk.add("pages", np.arange(5) + 100)
+    pk.add("rest", np.arange(7) + 1000)
+    tpl = np.concatenate(pk.parts)
+    q = IntPack()
+    q.host, q.off = tpl, dict(pk.off)
+    q.patches = {"src": np.full(10, -1, np.int32), "pages": np.full(5, -2, np.int32)}
+    full = q._full_host()
+    o, n = q.off["src"]
+    assert (full[o:o + n] == -1).all()
+    o, n = q.off["pages"]
+    assert (full[o:o + n] == -2).all()
+    o, n = q.off["rest"]
+    assert (full[o:o + n] == np.arange(7) + 1000).all()
+    assert (tpl == np.concatenate(pk.parts)).all()          # template untouched
+    # every view keeps 16-byte alignment
+    assert all(off % 4 == 0 for off, _ in q.off.values())
