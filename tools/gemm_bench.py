@@ -139,6 +139,12 @@ if __name__ == "__main__":
                 phases(n, kk, m, 0)
         lib.vlc_set_tuning(7, 1)
         lib.vlc_set_tuning(9, 64)
+    if mode == "head":            # LM head: CTA pair (9 waves, last one holds 2 of 594 tiles) vs stream-K
+        for pair, red in ((96, False), (0, False), (0, True), (96, False)):
+            lib.vlc_set_tuning(10, pair)
+            print(f"-- pair {pair} red {red}", flush=True)
+            run(152064, 3584, 236, 0, kind=N.EPI_F32, red=red, reps=6)
+        lib.vlc_set_tuning(10, 96)
     if mode == "redx":            # one-wave projections: one CTA per tile vs stream-K with red.add split tiles
         for red in (False, True, False, True):
             print(f"-- red_scratch {red}", flush=True)
