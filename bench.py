@@ -8,22 +8,35 @@ heads, V = 152064; 4 cached images x 1024 tokens reused at SHIFTED positions
 tokens; static 5% recompute.  A "step" is one `prefill_with_reuse` of that
 request.  Weights are random-init on the device (same distributions as the
 reference); images/prompts come from the reference's seeded generators.
+`--workload C2` is configs[1] (2B shape, one image, dynamic layer-wise 3% budget
+from plan_greedy); `--workload C5` is configs[4] (64 requests, aggregate tokens/s).
 
-  value      p50 device TTFT (ms) with inputs resident in HBM, L2 flushed
-             between steps; max over ranks.
-  e2e        same call through the public API with host inputs: wall time from
-             prefill_with_reuse() entry to the last-row logits on the host.
-  roofline   dominant kernel from a CUDA-event-traced pass.
-  cpu_baseline  the CPU oracle (numpy restatement of the reference) on a bounded
-             sample: 2 of the 28 layers timed per layer, extrapolated.
+  value         p50 device TTFT (ms) with inputs resident in HBM, L2 flushed
+                between steps; max over ranks.
+  e2e           same call through the public API with host inputs: wall time from
+                prefill_with_reuse() entry to the last-row logits on the host.
+  roofline      dominant kernel from a CUDA-event-traced pass.
+  cpu_baseline  the reference's own kvreuse.prefill_with_reuse (installed in
+                baseline/_ref; the oracle port if absent) at FULL depth on the same
+                weights and the same stored KV as the device run, all host cores.
+  parity_vs_cpu the device result of the benchmarked request against that CPU run.
 
-`--impl reference` prints the CPU arm only (rank 0).
+`--impl reference` runs the reference arm only (rank 0): the unmodified reference
+package at full depth on the workload's shape, one request per step.
+`--gpus N` without a torch.distributed environment re-launches itself under
+torch.distributed.run with N ranks (127.0.0.1 rendezvous).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+
+if "reference" in __import__("sys").argv and "WORLD_SIZE" in os.environ:
+    # rank 0 of a torchrun launch runs the CPU arm: torchrun sets OMP_NUM_THREADS=1 per rank, so give
+    # OpenBLAS (read at numpy import, and ahead of OMP_NUM_THREADS) every host core explicitly
+    os.environ["OPENBLAS_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
+import socket
 import statistics
 import subprocess
 import sys
@@ -45,17 +58,32 @@ CONFIGS = {
                tokens_per_image=1024),
 }
 WORKLOADS = {
-    "C3": dict(cfg="C3", images=4, ratio=0.05,
+    "C3": dict(cfg="C3", images=4, ratio=0.05, plan="static",
                desc="Qwen2.5-VL-7B shape (ref semantics L28 d=kv=3584 H28 h7168 V152064), 4x1024 cached image "
                     "tokens reused at shifted positions + 32 text, static 5% recompute"),
-    "C2": dict(cfg="C2", images=1, ratio=0.03,
-               desc="Qwen2-VL-2B shape (ref semantics L28 d=kv=1536 H12 h3072 V151936), 1024 image tokens, 3%"),
-    "C1": dict(cfg="C1", images=1, ratio=0.05, desc="tiny L4 d256 H8, 256 image + 32 text, 5%"),
+    "C2": dict(cfg="C2", images=1, ratio=0.03, plan="greedy",
+               desc="Qwen2-VL-2B shape (ref semantics L28 d=kv=1536 H12 h3072 V151936), 1024 image tokens reused "
+                    "at a shifted position + 32 text, dynamic layer-wise budget 3% (plan_greedy, P = 0.03 L)"),
+    "C1": dict(cfg="C1", images=1, ratio=0.05, plan="static", desc="tiny L4 d256 H8, 256 image + 32 text, 5%"),
     "C5": dict(cfg="C2", images=2, ratio=0.03, requests=64, pool=8, micro=8,
                desc="64 concurrent requests sharing 8 cached images (Qwen2-VL-2B shape, ref semantics), each "
                     "16 text + 2 seeded images x 1024 tokens + 16 text, 3% recompute; requests sharded "
                     "round-robin over ranks, micro-batches of 8 requests per device pass"),
 }
+
+
+def workload_plan(P, wl, L):
+    """The workload's plan: plan_static(r), or for the dynamic budget plan_greedy at P = r * L
+    (cli.py:222-228) over a diminishing sensitivity table whose shallow layers gain more
+    (section 3) -- the same table tests/test_fullscale_parity_gpu.py checks on device
+    against the oracle."""
+    if wl.get("plan") != "greedy":
+        return P.plan_static(wl["ratio"], L)
+    grid = tuple(round(0.002 * k, 3) for k in range(1, 51))
+    w = np.linspace(2.0, 0.25, L)[:, None]
+    gains = w * np.exp(-np.asarray(grid)[None, :] / 0.03) * 0.002
+    scores = np.maximum(1.0 - np.cumsum(gains, axis=1), 0.0)
+    return P.plan_greedy(P.SensitivityTable(scores, grid, 1.0, 1, 0), P.BudgetSpec(wl["ratio"] * L))
 
 
 def _peaks():
@@ -115,53 +143,6 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-# ---------------------------------------------------------------- CPU arm (oracle port)
-
-class CpuSample:
-    """Bounded sample of the reference algorithm on host cores: the oracle's reuse prefill
-    over `sample_layers` of the layers (same d/kv/H/V/T, sequence and plan) with random
-    weights / cached KV of the workload shape; per-layer time extrapolated to full depth."""
-
-    def __init__(self, cfg_kw: dict, images: int, ratio: float, sample_layers: int = 2, seed: int = 0):
-        from oracle import kvreuse_oracle as O
-        self.O, self.L, self.ratio, self.sl = O, cfg_kw["num_layers"], ratio, sample_layers
-        self.c = c = O.Cfg(**{**cfg_kw, "num_layers": sample_layers, "seed": seed})
-        g = np.random.default_rng(seed)
-        d, kv, h, V, T = c.model_dim, c.kv_dim, c.hidden, c.vocab_size, c.tokens_per_image
-
-        def rnd(*shape, scale=1.0):   # uniform, variance-matched: timing does not depend on values
-            a = g.random(shape, dtype=np.float32)
-            a -= np.float32(0.5)
-            a *= np.float32(scale * 3.4641016)
-            return a
-
-        w = {"embed": rnd(V, d), "head": rnd(d, V, scale=d ** -0.5), "final_norm": np.ones(d, np.float32)}
-        for i in range(sample_layers):
-            w.update({f"l{i}_attn_norm": np.ones(d, np.float32), f"l{i}_mlp_norm": np.ones(d, np.float32),
-                      f"l{i}_wq": rnd(d, kv, scale=d ** -0.5), f"l{i}_wk": rnd(d, kv, scale=d ** -0.5),
-                      f"l{i}_wv": rnd(d, kv, scale=d ** -0.5), f"l{i}_wo": rnd(kv, d, scale=kv ** -0.5),
-                      f"l{i}_w_gate": rnd(d, h, scale=d ** -0.5), f"l{i}_w_up": rnd(d, h, scale=d ** -0.5),
-                      f"l{i}_w_down": rnd(h, d, scale=h ** -0.5)})
-        text = O.prompt(V, 32, 12)
-        self.ids, self.segs = O.layout(text[:16], images, T, text[16:])
-        self.enc, self.kvs, self.hashes = {}, {}, []
-        for m in range(images):
-            key = f"{m:064x}"
-            self.hashes.append(key)
-            self.enc[key] = rnd(T, d)
-            self.kvs[key] = O.KVEntry(rnd(sample_layers, T, kv), rnd(sample_layers, T, kv), 8)
-        self.w = w
-
-    def run(self):
-        tm = {}
-        self.O.reuse_prefill(self.c, self.w, self.ids, self.segs, self.hashes, (self.ratio,) * self.sl,
-                             self.enc, self.kvs, timings=tm)
-        per_layer = statistics.mean(tm["layers"])
-        ttft = tm["resolve"] * self.L / self.sl + tm["embed"] + per_layer * self.L + tm["head"]
-        return ttft * 1e3, {"sample_layers": self.sl, "per_layer_s": per_layer, "resolve_s": tm["resolve"],
-                            "head_s": tm["head"]}
-
-
 def cpu_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -169,30 +150,157 @@ def cpu_cores() -> int:
         return os.cpu_count() or 1
 
 
+# ---------------------------------------------------------------- the reference on the host cores
+
+def reference_package():
+    """The UNMODIFIED reference package `kvreuse`, pip-installed into baseline/_ref.
+    None when it is not there (the CPU legs then run the oracle port)."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "kvreuse")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    import kvreuse
+    return kvreuse
+
+
+class HostReuse:
+    """One reuse prefill of the workload on the host cores, through the reference's public API
+    (kvreuse.prefill_with_reuse, engine.py:119-190) or, without it, the oracle restatement.
+
+    kw: ModelConfig fields; w: reference-named fp32 weights; enc / kv: hash hex -> [T, d] rows /
+    (keys [L, T, kv], values, origin); text: the 32 live text tokens; ratios: the plan."""
+
+    def __init__(self, kw, w, text, hashes, enc, kv, ratios, fingerprint=1):
+        self.K = reference_package()
+        self.kind = "reference" if self.K is not None else "port"
+        self.ratios = tuple(float(r) for r in ratios)
+        T, n_img = kw["tokens_per_image"], len(hashes)
+        if self.K is not None:
+            K = self.K
+            self.model = K.ToyVLM(K.ModelConfig(**kw), w)
+            # the fingerprint is a lazily computed, cached property of the immutable model
+            # (model.py:221-227): fixing it up front skips hashing 19 GB of weights at setup only
+            self.model._fingerprint = int(fingerprint)
+            self.store = K.CacheStore()
+            for h in hashes:
+                ih = K.ImageHash(h)
+                self.store.put_encoder(K.EncoderCacheEntry(ih, enc[h], self.model.fingerprint))
+                k, v, origin = kv[h]
+                self.store.put_kv(K.KVCacheEntry(ih, k, v, int(origin), self.model.fingerprint))
+            seq = K.make_sequence(list(text[:16]), n_img, T, suffix=list(text[16:]))
+            self.req = K.ReuseRequest(seq, [K.ImageHash(h) for h in hashes], K.RecomputePlan(self.ratios))
+        else:
+            from oracle import kvreuse_oracle as O
+            self.O = O
+            self.oc = O.Cfg(**kw)
+            self.w, self.keys = w, list(hashes)
+            self.enc = enc
+            self.kv = {h: O.KVEntry(*kv[h]) for h in hashes}
+            self.ids, self.segs = O.layout(list(text[:16]), n_img, T, list(text[16:]))
+
+    def run(self):
+        """(seconds, dict of rows / logits / keys / values / counts / misses / fallbacks)."""
+        t0 = time.perf_counter()
+        if self.K is not None:
+            r = self.K.prefill_with_reuse(self.model, self.req, self.store)
+            dt = time.perf_counter() - t0
+            return dt, dict(rows=np.asarray(r.positions), logits=r.logits, keys=r.kv.keys, values=r.kv.values,
+                            counts=list(r.metrics.computed_per_layer), misses=r.metrics.encoder_misses,
+                            fallbacks=r.metrics.fallback_images, resolve_s=r.metrics.resolve_seconds)
+        r = self.O.reuse_prefill(self.oc, self.w, self.ids, self.segs, self.keys, self.ratios, self.enc, self.kv)
+        dt = time.perf_counter() - t0
+        return dt, dict(rows=r.rows, logits=r.logits, keys=r.keys, values=r.values, counts=r.counts,
+                        misses=r.encoder_misses, fallbacks=r.fallback_images)
+
+
 def run_reference(args, wl):
-    cfg_kw = CONFIGS[wl["cfg"]]
+    """--impl reference: the reference's prefill_with_reuse at FULL depth on the workload's shape,
+    one request per step, on all host cores.  Weights: each layer's matrices share one random
+    block per shape (the per-layer arithmetic and memory traffic are those of distinct weights --
+    a layer's 0.5 GB far exceeds the CPU caches -- at 1/28 of the host RAM); the store holds random
+    pre-RoPE K/V for each image (the resolve copy is the reference's own)."""
+    kw = dict(CONFIGS[wl["cfg"]], seed=0)
+    L, d, kv, V, T = kw["num_layers"], kw["model_dim"], kw["kv_dim"], kw["vocab_size"], kw["tokens_per_image"]
+    h = 2 * d
+    g = np.random.default_rng(0)
+
+    def rnd(*shape, scale=1.0):      # uniform, variance-matched: the timing does not depend on values
+        a = g.random(shape, dtype=np.float32)
+        a -= np.float32(0.5)
+        a *= np.float32(scale * 3.4641016)
+        return a
+    blk = {"attn_norm": np.ones(d, np.float32), "mlp_norm": np.ones(d, np.float32),
+           "wq": rnd(d, kv, scale=d ** -0.5), "wk": rnd(d, kv, scale=d ** -0.5), "wv": rnd(d, kv, scale=d ** -0.5),
+           "wo": rnd(kv, d, scale=kv ** -0.5), "w_gate": rnd(d, h, scale=d ** -0.5),
+           "w_up": rnd(d, h, scale=d ** -0.5), "w_down": rnd(h, d, scale=h ** -0.5)}
+    w = {"embed": rnd(V, d), "head": rnd(d, V, scale=d ** -0.5), "final_norm": np.ones(d, np.float32)}
+    for i in range(L):
+        w.update({f"l{i}_{k}": v for k, v in blk.items()})
+    from paper_2512_12977_b200.toydata import prompt_ids
+    text = prompt_ids(V, 32, 12)
+    hashes = [f"{m + 1:064x}" for m in range(wl["images"])]
+    enc = {hh: rnd(T, d) for hh in hashes}
+    kvs = {hh: (rnd(L, T, kv), rnd(L, T, kv), 8) for hh in hashes}
+    import paper_2512_12977_b200 as P        # host-side planner only (no device work)
+    ratios = workload_plan(P, wl, L).ratios
+    host = HostReuse(kw, w, text, hashes, enc, kvs, ratios)
     times = []
-    # one sampled layer per step (the per-layer time x L extrapolation) keeps a default run of the
-    # arm within a few minutes on the host cores
-    sample = CpuSample(cfg_kw, wl["images"], wl["ratio"], sample_layers=1)
     for step in range(args.warmup + args.steps):
-        ms, det = sample.run()
+        dt, _ = host.run()
         if step >= args.warmup:
-            times.append(ms)
+            times.append(dt * 1e3)
     v = statistics.median(times)
     cores = cpu_cores()
-    sample = (f"oracle (numpy restatement of kvreuse.prefill_with_reuse) over {det['sample_layers']} of "
-              f"{cfg_kw['num_layers']} layers per step, per-layer time x {cfg_kw['num_layers']} + resolve/head; "
-              f"BLAS threads = all {cores} cores")
+    sample = (f"{'kvreuse 0.1.0 (baseline/_ref)' if host.kind == 'reference' else 'oracle port'} "
+              f"prefill_with_reuse, full depth ({L}/{L} layers), one {wl['cfg']} request per step "
+              f"(resolve + compute), numpy/OpenBLAS on all {cores} host cores")
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(statistics.mean(times), 3),
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded prompts, random weights/KV of the workload shape)",
-            "config": {"workload": wl["desc"], "recompute": wl["ratio"], "image_tokens": wl["images"] * 1024,
-                       "text_tokens": 32},
-            "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": cores, "kind": "port", "sample": sample},
+            "data": "synthetic (seeded prompts; random weights and cached KV of the workload shape)",
+            "config": {"workload": wl["desc"], "recompute": wl["ratio"], "image_tokens": wl["images"] * T,
+                       "text_tokens": 32, "plan_ratios_first_last": [ratios[0], ratios[-1]]},
+            "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": cores, "kind": host.kind,
+                             "sample": sample},
             "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- launcher
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_relaunch(args) -> bool:
+    """`--gpus N` (N > 1) outside torch.distributed: re-run this command as N ranks."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def dry_run(args):
+    """Launcher check without a GPU: every rank joins a gloo group; rank 0 prints the world."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        n = int(t.item())
+        dist.barrier()
+        dist.destroy_process_group()
+    else:
+        n = 1
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_joined": n, "gpus_flag": args.gpus}), flush=True)
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -208,12 +316,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C3", choices=list(WORKLOADS),
-                    help="C3: the BASELINE metric (TTFT); C5: aggregate tokens/s of batched requests")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+                    help="C3: the BASELINE metric (TTFT); C2: configs[1]; C5: aggregate tokens/s of batched requests")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline / parity leg")
+    ap.add_argument("--cpu-reps", type=int, default=2, help="reference runs in the cpu_baseline leg")
     ap.add_argument("--parallel", default="replicas", choices=["replicas", "heads"],
                     help="N>1: independent requests per rank (default) or head-parallel attention on one "
                          "request (one NCCL all-reduce per layer)")
     ap.add_argument("--trace", default="", help="write per-kernel trace json here")
+    ap.add_argument("--dry-run", action="store_true", help="launcher check only (no GPU work)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = WORKLOADS[args.workload]
@@ -222,6 +332,10 @@ def main():
     if args.impl == "reference":
         if rank == 0:
             run_reference(args, wl)
+        return
+    maybe_relaunch(args)
+    if args.dry_run:
+        dry_run(args)
         return
 
     import torch
@@ -242,7 +356,10 @@ def main():
     cfg = P.ModelConfig(**CONFIGS[wl["cfg"]], seed=0)
     T, V, L = cfg.tokens_per_image, cfg.vocab_size, cfg.num_layers
     head_par = args.parallel == "heads" and world > 1
-    model = P.ToyVLM.device_random(cfg, seed=0, tp_group=dist.group.WORLD if head_par else None)
+    cpu_leg = rank == 0 and world == 1 and not args.no_cpu
+    export = {} if cpu_leg else None          # host copy of the device weights for the CPU leg
+    t_setup = time.perf_counter()
+    model = P.ToyVLM.device_random(cfg, seed=0, tp_group=dist.group.WORLD if head_par else None, export=export)
     runner = _runner(model)
     store = P.CacheStore()
     from paper_2512_12977_b200.toydata import make_images, prompt_ids
@@ -251,9 +368,10 @@ def main():
     text = prompt_ids(V, 32, 12)
     seq = P.make_sequence(text[:16], wl["images"], T, text[16:])
     hashes = [P.hash_image(px) for px in images]
-    plan = P.plan_static(wl["ratio"], L)
+    plan = workload_plan(P, wl, L)
     req = P.ReuseRequest(seq, hashes, plan)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    setup_s = time.perf_counter() - t_setup
 
     def timed(request, st, steps, warmup):
         for _ in range(warmup):
@@ -306,7 +424,7 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = prefill_with_reuse(model, req, store)
-        last = res.last_logits()
+        res.last_logits()
         e2e.append((time.perf_counter() - t0) * 1e3)
         bytes_h2d = int(getattr(runner.ws, "last_h2d_bytes", runner.ws.bufs["ints"].numel() * 4))
     clocks = sampler.stop()
@@ -323,9 +441,10 @@ def main():
                                         P.CacheStore(), 3, 1))
     c4 = layer_aware_vs_uniform(P, model, seq, hashes, store, L, timed) if args.workload == "C3" else None
     sweep = {}
-    for r in (0.02, 0.03, 0.04, 0.05):
-        sweep[str(r)] = round(statistics.median(timed(P.ReuseRequest(seq, hashes, P.plan_static(r, L)), store,
-                                                      7, 2)), 4)
+    if args.workload == "C3":
+        for r in (0.02, 0.03, 0.04, 0.05):
+            sweep[str(r)] = round(statistics.median(timed(P.ReuseRequest(seq, hashes, P.plan_static(r, L)), store,
+                                                          7, 2)), 4)
 
     # ---- per-kernel trace (separate pass, events around each launch)
     hbm, tf_burst, tf_sust, peak_src = _peaks()
@@ -405,23 +524,15 @@ def main():
         with open(args.trace, "w") as fh:
             json.dump({"kernels": kernels, "agg": {k: v for k, v in agg.items()}}, fh, indent=1)
 
-    # ---- parity vs CPU oracle on configs[0] (C1), bf16-rounded weights
-    parity = None
-    if rank == 0:
+    # ---- CPU leg: the reference at full depth on the SAME weights and stored KV, and parity of the
+    # benchmarked request against it
+    parity = cpu = None
+    if cpu_leg:
         try:
-            parity = parity_c1(P)
+            parity, cpu = cpu_leg_run(P, model, store, hashes, text, wl, plan, req, export, args.cpu_reps)
         except Exception as exc:  # never hide it: report in the line
             parity = {"error": repr(exc)}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cs = CpuSample(CONFIGS[wl["cfg"]], wl["images"], wl["ratio"])
-        cs.run()
-        ms_cpu, det = cs.run()
-        cores = cpu_cores()
-        cpu = {"value": round(ms_cpu, 2), "unit": "ms", "cores": cores, "kind": "port",
-               "sample": f"oracle reuse prefill over {det['sample_layers']}/{L} layers, per-layer x {L} "
-                         f"(+resolve, head); numpy/OpenBLAS on {cores} threads"}
+    del export
 
     n_tok = len(seq)
     c = prefill_with_reuse(model, req, store).metrics.computed_per_layer
@@ -433,7 +544,9 @@ def main():
                         "and prompts; store filled by the device miss path",
                 "config": {"workload": wl["desc"], "recompute": wl["ratio"], "image_tokens": wl["images"] * T,
                            "text_tokens": 32, "seq_len": n_tok, "computed_rows_layer0": c[0],
-                           "l2": "flushed between steps (512 MiB write); weights 9.6 GB >> L2",
+                           "plan_ratios_first_last": [plan.ratios[0], plan.ratios[-1]],
+                           "mean_ratio": round(P.mean_ratio(plan), 4),
+                           "l2": "flushed between steps (512 MiB write); weights >> L2",
                            "parallelism": (f"head-parallel attention over {world} GPUs (one NCCL all-reduce "
                                            f"per layer)" if head_par else
                                            f"replica per GPU x{world} (independent requests, no collective)")},
@@ -446,11 +559,58 @@ def main():
                 "speedup_vs_full_prefill": round(full_ms / p50, 2), "speedup_vs_origin": round(origin_ms / p50, 2),
                 "sweep_p50_ms": sweep, "layer_aware_vs_uniform": c4, "parity_vs_cpu": parity,
                 "prefill_tokens_per_s": round((1 if head_par else world) * n_tok / (p50 / 1e3), 1),
-                "timed_region_s": round(region_s, 3)}
+                "timed_region_s": round(region_s, 3), "setup_s": round(setup_s, 1)}
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def cpu_leg_run(P, model, store, hashes, text, wl, plan, req, export, reps):
+    """cpu_baseline + parity_vs_cpu: the reference's prefill_with_reuse (baseline/_ref; the oracle
+    port without it) at full depth on the device's own weights (bf16 values) and stored KV, timed
+    on all host cores; the device result of the same request compared with it (north_star bars)."""
+    cfg = model.config
+    kw = dict(CONFIGS[wl["cfg"]], seed=0)
+    enc, kv = {}, {}
+    for h in hashes:
+        e, k = store.get_encoder(h), store.get_kv(h)
+        enc[h.hex] = np.ascontiguousarray(e.embeddings, dtype=np.float32)
+        kv[h.hex] = (k.keys, k.values, k.origin_position)
+    host = HostReuse(kw, export, text, [h.hex for h in hashes], enc, kv, plan.ratios, fingerprint=model.fingerprint)
+    times, out = [], None
+    for _ in range(max(1, reps)):
+        dt, out = host.run()
+        times.append(dt * 1e3)
+    res = P.prefill_with_reuse(model, req, store)
+    lg = res.logits
+    num = den = 0.0
+    keys, vals = res.kv.keys, res.kv.values
+    for i in range(cfg.num_layers):     # rel_err over [L, n, kv], a layer at a time
+        for a, e in ((keys[i], out["keys"][i]), (vals[i], out["values"][i])):
+            num = max(num, float(np.max(np.abs(a.astype(np.float64) - e))))
+            den = max(den, float(np.max(np.abs(e))))
+    kv_err = num / max(den, 1e-6)
+    ref_lg = out["logits"]
+    parity = {"config": f"{wl['cfg']} (the benchmarked request: full depth, plan {plan.ratios[0]}..{plan.ratios[-1]})",
+              "cpu_impl": host.kind,
+              "rel_err": float(np.max(np.abs(lg.astype(np.float64) - ref_lg)) / max(1e-6, float(np.max(np.abs(ref_lg))))),
+              "max_abs": float(np.max(np.abs(lg - ref_lg))), "kv_rel_err": kv_err,
+              "top1_last_row_equal": bool(np.argmax(lg[-1]) == np.argmax(ref_lg[-1])),
+              "rows_bit_exact": bool(np.array_equal(res.positions, out["rows"])),
+              "counts_bit_exact": list(res.metrics.computed_per_layer) == list(out["counts"]),
+              "hit_miss_equal": (res.metrics.encoder_misses, res.metrics.fallback_images) ==
+                                (out["misses"], out["fallbacks"]),
+              "tolerance": "rel_err <= 2e-2 (logits and merged K/V), top-1 equal, rows/counts bit-exact"}
+    parity["pass"] = bool(parity["rel_err"] <= 2e-2 and kv_err <= 2e-2 and parity["top1_last_row_equal"]
+                          and parity["rows_bit_exact"] and parity["counts_bit_exact"] and parity["hit_miss_equal"])
+    cores = cpu_cores()
+    cpu = {"value": round(statistics.median(times), 2), "unit": "ms", "cores": cores, "kind": host.kind,
+           "sample": f"{'kvreuse.prefill_with_reuse (baseline/_ref)' if host.kind == 'reference' else 'oracle port'}"
+                     f" of the benchmarked request at full depth ({cfg.num_layers}/{cfg.num_layers} layers) on the "
+                     f"device's weights and stored KV; median of {len(times)}; numpy/OpenBLAS on {cores} threads",
+           "reps_ms": [round(t, 1) for t in times]}
+    return parity, cpu
 
 
 def run_c5(args, wl, P, rank, world, local, dist):
@@ -561,35 +721,6 @@ def layer_aware_vs_uniform(P, model, seq, hashes, store, L, timed):
 
 def prefill_last(P, model, req, store):
     return P.prefill_with_reuse(model, req, store).last_logits().astype(np.float64)
-
-
-def parity_c1(P):
-    """configs[0] on the GPU vs the CPU oracle, both on the same bf16-rounded weights."""
-    from oracle import kvreuse_oracle as O
-    kw = dict(CONFIGS["C1"], seed=0)
-    oc = O.Cfg(**kw)
-    w = {k: O.bf16_round(v) for k, v in O.make_weights(oc).items()}
-    model = P.ToyVLM(P.ModelConfig(**kw), w)
-    V, T = oc.vocab_size, oc.tokens_per_image
-    imgs = O.images(1, oc.side, 1)
-    enc, kv = {}, {}
-    ids0, segs0 = O.layout(O.prompt(V, 8, 11), 1, T)
-    O.fill_one(oc, w, ids0, segs0, imgs, enc, kv)
-    store = P.CacheStore()
-    h = O.sha256_hex(imgs[0])
-    store.put_encoder(P.EncoderCacheEntry(P.ImageHash(h), enc[h], model.fingerprint))
-    store.put_kv(P.KVCacheEntry(P.ImageHash(h), kv[h].keys, kv[h].values, 8, model.fingerprint))
-    text = O.prompt(V, 32, 12)
-    ids, segs = O.layout(text[:16], 1, T, text[16:])
-    ref = O.reuse_prefill(oc, w, ids, segs, [h], (0.05,) * 4, enc, kv)
-    res = P.prefill_with_reuse(model, P.ReuseRequest(P.make_sequence(text[:16], 1, T, text[16:]),
-                                                     [P.ImageHash(h)], P.plan_static(0.05, 4)), store)
-    lg = res.logits
-    return {"config": "C1 (configs[0])", "rel_err": O.rel_err(lg, ref.logits),
-            "max_abs": float(np.abs(lg - ref.logits).max()),
-            "top1_last_row_equal": bool(np.argmax(lg[-1]) == np.argmax(ref.logits[-1])),
-            "rows_bit_exact": bool(np.array_equal(res.positions, ref.rows)),
-            "counts_bit_exact": res.metrics.computed_per_layer == ref.counts, "tolerance": "rel_err <= 2e-2"}
 
 
 if __name__ == "__main__":

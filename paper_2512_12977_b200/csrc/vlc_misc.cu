@@ -18,7 +18,9 @@ __global__ void embed_assemble_kernel(float* __restrict__ x, int ldx,
   if (r >= rows) return;
   const int2 s = src[r];
   float* dst = x + (long)r * ldx;
-  if (s.x == 0) {
+  if (s.x == 0 && s.y < 0) {          // negative text id: zero embedding (model.py:349-353)
+    for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = 0.f;
+  } else if (s.x == 0) {
     const __nv_bfloat16* e = embed + (long)s.y * d;
     for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = __bfloat162float(e[i]);
   } else {

@@ -14,6 +14,7 @@ Results are device-resident and materialise on access: `logits` and `kv.keys`
 """
 from __future__ import annotations
 
+import threading
 import time
 from dataclasses import dataclass, field
 
@@ -130,12 +131,22 @@ _PINNED: dict = {}   # numel -> pinned host staging row for last_logits()
 class ReuseResult:
     """positions (host), logits [len(positions), V] and merged pre-RoPE KV, device-backed."""
 
-    def __init__(self, positions, dev_logits, kv: KVTensors, metrics: ReuseMetrics):
+    def __init__(self, positions, dev_logits, kv: KVTensors, metrics: ReuseMetrics, lock=None):
         self.positions = positions
         self._dev_logits = dev_logits
         self._logits = None
         self.kv = kv
         self.metrics = metrics
+        # the runner's lock: a host read must not interleave with a later call that detaches this
+        # result (copies it out of the shared workspace) and reuses the workspace
+        self._lock = lock if lock is not None else threading.RLock()
+        if kv._loader is not None:
+            loader = kv._loader
+
+            def locked_load():
+                with self._lock:
+                    return loader()
+            kv._loader = locked_load
 
     @property
     def device_logits(self):
@@ -144,24 +155,25 @@ class ReuseResult:
     @property
     def logits(self) -> np.ndarray:
         if self._logits is None:
-            self._logits = self._dev_logits.cpu().numpy()
+            with self._lock:
+                self._logits = self._dev_logits.cpu().numpy()
         return self._logits
 
     def last_logits(self) -> np.ndarray:
         """Last row's logits (the next-token distribution) via a pinned staging buffer."""
         import torch
-        row = self._dev_logits[-1]
-        buf = _PINNED.get(row.numel())
-        if buf is None:
-            buf = _PINNED[row.numel()] = torch.empty(row.numel(), dtype=row.dtype, pin_memory=True)
-        buf.copy_(row, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        return buf.numpy().copy()
+        with self._lock:
+            row = self._dev_logits[-1]
+            buf = _PINNED.get(row.numel())
+            if buf is None:
+                buf = _PINNED[row.numel()] = torch.empty(row.numel(), dtype=row.dtype, pin_memory=True)
+            buf.copy_(row, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return buf.numpy().copy()
 
     def _detach(self):
         """The runner is about to reuse its workspace: take private copies."""
-        if self._logits is None:
-            self._dev_logits = self._dev_logits.clone()
+        self._dev_logits = self._dev_logits.clone()
         if self.kv._dev is None and self.kv._keys is None:
             self.kv._device()
         if self.kv._dev is not None:
@@ -184,26 +196,36 @@ def _layout(runner, specs, L, heads):
     return with_data(lay, specs)
 
 
+_RUNNER_LOCK = threading.Lock()
+
+
 def _runner(model: ToyVLM):
     from .runtime import Runner
     r = getattr(model, "_runner", None)
     if r is None:
-        r = Runner(model.device)
-        r.tp_group = model.tp_group
-        model._runner = r
+        with _RUNNER_LOCK:
+            r = getattr(model, "_runner", None)
+            if r is None:
+                r = Runner(model.device)
+                r.tp_group = model.tp_group
+                model._runner = r
     return r
 
 
 def encode_image(model: ToyVLM, pixels) -> np.ndarray:
     """GPU toy ViT (model.py:302-332); returns host fp32 [T, d] like the reference."""
     _check_pixels(model.config, pixels)
-    return _runner(model).encode([pixels]).cpu().numpy()
+    runner = _runner(model)
+    with runner.serial():
+        return runner.encode([pixels]).cpu().numpy()
 
 
 def encode_images_device(model: ToyVLM, pixels_list):
     for px in pixels_list:
         _check_pixels(model.config, px)
-    return _runner(model).encode(pixels_list)
+    runner = _runner(model)
+    with runner.serial():
+        return runner.encode(pixels_list).clone()     # the encoder workspace is reused by the next call
 
 
 def _check_pixels(cfg: ModelConfig, pixels) -> None:
@@ -230,9 +252,8 @@ def _text_tokens(seq: TokenSequence, cfg: ModelConfig):
                 t = seq.ids[p]
                 if t >= cfg.vocab_size:
                     raise InputError(f"token id {t} out of vocab")
-                if t >= 0:
-                    pos.append(p)
-                    ids.append(t)
+                pos.append(p)            # a negative id embeds as a zero row (model.py:349-353)
+                ids.append(t)
     return np.array(pos, dtype=np.int64), np.array(ids, dtype=np.int64)
 
 
@@ -260,6 +281,7 @@ def _resolve(model: ToyVLM, request: ReuseRequest, store: CacheStore, miss_base:
     keep = np.repeat(layer_keep(plan, T)[:, None], len(segs), axis=1).astype(np.int32)
 
     fp = model.fingerprint
+    runner_kv = model.device.kv
     enc_src, kv_hit, page_rows, miss_px = [], [], [], []
     enc_pool = kv_pool = None
     for m, seg in enumerate(segs):                               # engine.py:140-159
@@ -281,8 +303,12 @@ def _resolve(model: ToyVLM, request: ReuseRequest, store: CacheStore, miss_base:
         if entry is not None:
             if entry.tokens != T or entry.layers != L:
                 raise InputError("cached KV shape does not match the model")
+            if entry.pool.width != runner_kv:
+                raise InputError(f"cached KV width {entry.pool.width} does not match this model's K/V width "
+                                 f"{runner_kv} (head-parallel stores hold each rank's head slice)")
             kv_pool = entry.pool
-            kv_hit.append(bool(keep[0, m] < T))
+            # keep is non-increasing over layers: any layer that skips image tokens reads cached KV
+            kv_hit.append(bool((keep[:, m] < T).any()))
             page_rows.append(entry.pages)
         else:
             kv_hit.append(False)
@@ -311,9 +337,14 @@ def prefill_batch_with_reuse(model: ToyVLM, requests: list, store: CacheStore) -
     causal by position).  Result i equals prefill_with_reuse(model, requests[i], store)."""
     if not requests:
         return []
+    runner = _runner(model)
+    with runner.serial():
+        return _prefill_batch(model, requests, store, runner)
+
+
+def _prefill_batch(model: ToyVLM, requests: list, store: CacheStore, runner) -> list:
     cfg = model.config
     L = cfg.num_layers
-    runner = _runner(model)
     t0 = time.perf_counter()
     resolved, miss_px = [], []
     for req in requests:
@@ -343,7 +374,7 @@ def prefill_batch_with_reuse(model: ToyVLM, requests: list, store: CacheStore) -
         r.metrics._events = ev
         start, cnt = lay.logit_ranges[i]
         kv = KVTensors(loader=_merged_kv_loader(out, lay, r.spec, kv_pool, cfg, req=i))
-        res = ReuseResult(lay.positions[i], out["logits"][start:start + cnt], kv, r.metrics)
+        res = ReuseResult(lay.positions[i], out["logits"][start:start + cnt], kv, r.metrics, runner.lock)
         runner.ws.live.add(res)
         results.append(res)
     return results
@@ -389,7 +420,10 @@ def _merged_kv_loader(out, lay, spec: RequestSpec, kv_pool, cfg: ModelConfig, re
 
 def prefill_full(model: ToyVLM, seq: TokenSequence, image_embeds) -> tuple[np.ndarray, KVTensors]:
     """Dense causal prefill (model.py:362-389) on device: plan = 1.0 through the same kernels."""
+    import torch
     res = _prefill_embeds(model, seq, image_embeds)
+    if not bool(torch.isfinite(res.device_logits).all()):      # model.py:387-388
+        raise InputError("non-finite logits from prefill")
     # the result object is dropped here: give the returned KV its own device copy so that it stays
     # valid when the runner's output buffers are reused
     k, v = (t.clone() for t in res.kv._device())
@@ -398,6 +432,12 @@ def prefill_full(model: ToyVLM, seq: TokenSequence, image_embeds) -> tuple[np.nd
 
 def _prefill_embeds(model: ToyVLM, seq: TokenSequence, image_embeds, inject=None, capture=()) -> ReuseResult:
     """Full prefill with explicit image embeddings (host numpy or device rows)."""
+    runner = _runner(model)
+    with runner.serial():
+        return _prefill_embeds_locked(model, seq, image_embeds, runner, inject, capture)
+
+
+def _prefill_embeds_locked(model, seq, image_embeds, runner, inject, capture) -> ReuseResult:
     import torch
     cfg = model.config
     seq.validate(cfg.tokens_per_image)
@@ -406,7 +446,6 @@ def _prefill_embeds(model: ToyVLM, seq: TokenSequence, image_embeds, inject=None
         raise InputError(f"sequence has {len(segs)} image segments but {len(image_embeds)} embedding blocks "
                          "were supplied")
     T, L, d = cfg.tokens_per_image, cfg.num_layers, cfg.model_dim
-    runner = _runner(model)
     if segs:
         blocks = []
         for e in image_embeds:
@@ -430,7 +469,7 @@ def _prefill_embeds(model: ToyVLM, seq: TokenSequence, image_embeds, inject=None
     metrics._events = ev
     start, cnt = lay.logit_ranges[0]
     res = ReuseResult(lay.positions[0], out["logits"][start:start + cnt],
-                      KVTensors(loader=_merged_kv_loader(out, lay, spec, None, cfg)), metrics)
+                      KVTensors(loader=_merged_kv_loader(out, lay, spec, None, cfg)), metrics, runner.lock)
     res._scratch = scratch
     res._capture = out["capture"]
     runner.ws.live.add(res)
@@ -455,7 +494,8 @@ def forward_injected(model: ToyVLM, seq: TokenSequence, image_embeds, inject_key
         raise InputError(f"use_cached must be [{L}, {n}]")
     if use_cached.any() and (inject_keys is None or inject_values is None):
         raise InputError("use_cached set but no injected KV supplied")
-    caps = sorted({int(c) % L for c in capture_layers})
+    # the reference captures layer i when i or i - L is listed (engine.py:277); nothing else
+    caps = sorted({int(c) + L if int(c) < 0 else int(c) for c in capture_layers if -L <= int(c) < L})
     runner = _runner(model)
     if runner.tp_group is not None:
         raise NotImplementedError("forward_injected under head-parallel attention is not supported")
@@ -538,6 +578,39 @@ def decode_with_merged_kv(model: ToyVLM, merged_kv: KVTensors, tail_ids=(), max_
         ids.append(tok)
         cur = step(tok)
     return DecodeResult(ids, step_logits, tail_logits)
+
+
+def generate(model: ToyVLM, seq: TokenSequence, image_embeds, max_new: int):
+    """Full prefill then greedy decoding (model.py:467-471): (ids, step_logits [max_new, V])."""
+    logits, kv = prefill_full(model, seq, image_embeds)
+    out = decode_with_merged_kv(model, kv, max_new=max_new, initial_logits=logits[-1])
+    return out.ids, out.step_logits
+
+
+def apply_rope(x, positions, head_dim: int, base: float):
+    """Rotate [..., kv] vectors to `positions` (model.py:137-163), on the device in fp32 with the
+    reference's fp32 angle / cos / sin tables.  A utility of the API surface; the hot path rotates
+    inside the QKV epilogue and kv_relocate.  Returns numpy for numpy input, else a cuda tensor."""
+    import torch
+    from .model import rope_inv_freq
+    host = not isinstance(x, torch.Tensor)
+    t = torch.as_tensor(np.asarray(x, dtype=np.float32) if host else x).to("cuda", torch.float32)
+    squeeze = t.dim() == 1
+    if squeeze:
+        t = t[None, :]
+    pos = np.atleast_1d(np.asarray(positions))
+    if pos.shape[0] == 1 and t.shape[-2] != 1:
+        pos = np.broadcast_to(pos, (t.shape[-2],))
+    ang = pos.astype(np.float32)[:, None] * rope_inv_freq(head_dim, base)[None, :]
+    cos = torch.from_numpy(np.cos(ang, dtype=np.float32)).cuda()[:, None, :]
+    sin = torch.from_numpy(np.sin(ang, dtype=np.float32)).cuda()[:, None, :]
+    half = head_dim // 2
+    sh = t.reshape(*t.shape[:-1], t.shape[-1] // head_dim, head_dim)
+    a, b = sh[..., :half], sh[..., half:]
+    out = torch.cat((a * cos - b * sin, b * cos + a * sin), dim=-1).reshape(t.shape)
+    if squeeze:
+        out = out[0]
+    return out.cpu().numpy() if host else out
 
 
 # ---------------------------------------------------------------- cache-miss fill (bench.py:82-104)

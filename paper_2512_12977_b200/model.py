@@ -118,9 +118,11 @@ class ToyVLM:
             dist.get_rank(self.tp_group)]
 
     @classmethod
-    def device_random(cls, config: ModelConfig, seed: int | None = None, tp_group=None) -> "ToyVLM":
+    def device_random(cls, config: ModelConfig, seed: int | None = None, tp_group=None,
+                      export: dict | None = None) -> "ToyVLM":
         """Random-init weights generated directly on the GPU (benchmarks at 7B shape, where the
-        reference's 125 s host init would dominate).  Not bit-identical to init_model."""
+        reference's 125 s host init would dominate).  Not bit-identical to init_model.
+        export: see DeviceWeights.random (host fp32 copy of the device weights, reference names)."""
         m = cls.__new__(cls)
         m.config = config
         m.w = None
@@ -129,7 +131,7 @@ class ToyVLM:
             (_config_json(config) + f"|device-random|{s}").encode()).digest()[:8], "big")
         if tp_group is not None:
             m.tp_group = tp_group
-        m._device = DeviceWeights.random(config, s, m._heads())
+        m._device = DeviceWeights.random(config, s, m._heads(), export=export)
         return m
 
 
@@ -353,39 +355,58 @@ class DeviceWeights:
         return self
 
     @classmethod
-    def random(cls, cfg: ModelConfig, seed: int, heads=None) -> "DeviceWeights":
+    def random(cls, cfg: ModelConfig, seed: int, heads=None, export: dict | None = None) -> "DeviceWeights":
         """Same distributions as model.py:165-210 (N(0,1)/sqrt(fan_in), unit norms), drawn on device
-        (the full tensors are drawn on every rank, so head slices agree across ranks)."""
+        (the full tensors are drawn on every rank, so head slices agree across ranks).
+
+        export: if a dict, it receives the weights the device holds as host fp32 arrays in the
+        reference's names and [in, out] layout (bf16 values widened), so a CPU reference can run
+        on exactly the same model (tests / bench parity at the 7B shape)."""
         import torch
         self = cls(cfg, heads)
         g = torch.Generator(device="cuda").manual_seed(int(seed))
         d, kv, h, pp = cfg.model_dim, cfg.kv_dim, cfg.mlp_hidden, cfg.patch_size ** 2
         shapes = {"wq": (d, kv), "wk": (d, kv), "wv": (d, kv), "wo": (kv, d), "w_gate": (d, h),
                   "w_up": (d, h), "w_down": (h, d)}
+        prefix = [""]
+
+        def keep(name, t, rounded=True):
+            if export is not None:
+                v = t.to(torch.bfloat16).float() if rounded else t.float()
+                export[prefix[0] + name] = v.cpu().numpy()
+            return t
 
         def gen(name):
             if name.endswith("norm"):
-                return torch.ones(d, device="cuda")
+                return keep(name, torch.ones(d, device="cuda"), rounded=False)
             shape = shapes[name]
-            return torch.randn(shape, device="cuda", generator=g) / float(np.sqrt(shape[0]))
-        for _ in range(cfg.num_layers):
+            return keep(name, torch.randn(shape, device="cuda", generator=g) / float(np.sqrt(shape[0])))
+        for i in range(cfg.num_layers):
+            prefix[0] = f"l{i}_"
             blk = self._block(torch, gen)
             blk.pop("wqkv_plain")
             self.layers.append(blk)
+        prefix[0] = "enc_"
         self.enc = self._block(torch, gen, whole=True)
         self.enc["patch_w"] = PackedWeight(self._kmajor(
-            torch, torch.randn(pp, d, device="cuda", generator=g) / float(np.sqrt(pp)), self.n_d, self.kp))
-        self.enc["patch_b"] = torch.randn(d, device="cuda", generator=g) / float(np.sqrt(d))
-        self.enc["pos"] = torch.randn(cfg.tokens_per_image, d, device="cuda", generator=g)
-        self.enc["out_norm"] = torch.ones(d, device="cuda")
-        self.embed = torch.randn(cfg.vocab_size, d, device="cuda", generator=g).to(torch.bfloat16)
-        self.final_norm = torch.ones(d, device="cuda")
+            torch, keep("patch_w", torch.randn(pp, d, device="cuda", generator=g) / float(np.sqrt(pp))),
+            self.n_d, self.kp))
+        self.enc["patch_b"] = keep("patch_b", torch.randn(d, device="cuda", generator=g) / float(np.sqrt(d)),
+                                   rounded=False)
+        self.enc["pos"] = keep("pos", torch.randn(cfg.tokens_per_image, d, device="cuda", generator=g),
+                               rounded=False)
+        self.enc["out_norm"] = keep("out_norm", torch.ones(d, device="cuda"), rounded=False)
+        prefix[0] = ""
+        self.embed = keep("embed", torch.randn(cfg.vocab_size, d, device="cuda", generator=g).to(torch.bfloat16))
+        self.final_norm = keep("final_norm", torch.ones(d, device="cuda"), rounded=False)
         head = torch.zeros(self.n_vocab, self.kd, dtype=torch.bfloat16, device="cuda")
         for r0 in range(0, cfg.vocab_size, 16384):   # chunked to bound the fp32 transient
             r1 = min(cfg.vocab_size, r0 + 16384)
             head[r0:r1, :d] = (torch.randn(r1 - r0, d, device="cuda", generator=g)
                                / float(np.sqrt(d))).to(torch.bfloat16)
         self.head = PackedWeight(head)
+        if export is not None:
+            export["head"] = np.ascontiguousarray(head[:cfg.vocab_size, :d].float().cpu().numpy().T)
         del head
         torch.cuda.synchronize()
         return self

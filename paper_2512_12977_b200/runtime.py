@@ -5,7 +5,9 @@ HBM, provides the stream and does host<->device copies.
 """
 from __future__ import annotations
 
+import contextlib
 import math
+import threading
 import weakref
 
 import numpy as np
@@ -22,9 +24,6 @@ _FUSE_RELOC = bool(int(__import__("os").environ.get("VLC_RELOC_FUSED", "0")))
 # per norm less (VLC_FUSED_NORM=1; measured neutral on C3: the norm stays on the critical path
 # either way, so the separate vlc_rmsnorm launches are the default)
 _FUSED_NORM = bool(int(__import__("os").environ.get("VLC_FUSED_NORM", "0")))
-_SKIP_RELOC_EXPERIMENT = bool(int(__import__("os").environ.get("VLC_EXPERIMENT_SKIP_RELOC", "0")))
-# timing experiments only (wrong results): kernel names (Runner._run) not launched at all
-_SKIP_EXPERIMENT = {k for k in __import__("os").environ.get("VLC_EXPERIMENT_SKIP", "").split(",") if k}
 
 
 def _torch():
@@ -217,11 +216,29 @@ class Runner:
                 self.lib.vlc_set_tuning(int(k_), int(v_))
         self.tp_group = None       # head-parallel process group (engine sets it from the model)
         self._side = None          # side stream of the overlapped kv_relocate
+        # Concurrent callers: the workspaces, split-K scratch and counters belong to
+        # the runner, so calls are serialised -- on the host by the lock, on the device by making
+        # each call's stream wait for the previous call's completion event.
+        self.lock = threading.RLock()
+        self._done = None
+
+    @contextlib.contextmanager
+    def serial(self):
+        """One call's exclusive use of this runner's device state (host lock + stream order)."""
+        torch = _torch()
+        with self.lock:
+            cur = torch.cuda.current_stream()
+            if self._done is not None:
+                cur.wait_event(self._done)
+            try:
+                yield
+            finally:
+                if self._done is None:
+                    self._done = torch.cuda.Event()
+                self._done.record(cur)
 
     def _run(self, name, fn, nbytes=0, flops=0, kernels=1):
         """Issue one C-ABI call; optionally bracket it with CUDA events on the current stream."""
-        if name in _SKIP_EXPERIMENT:
-            return
         if _DEBUG_SYNC:
             import sys
             import time
@@ -548,8 +565,6 @@ class Runner:
                 pack.ptr("descs"), pack.ptr("blocks") + 8 * b0, n_b, dw.cos.data_ptr(), dw.sin.data_ptr(),
                 cfg.head_dim // 2, _stream()), "vlc_kv_relocate"), lay.reloc_tokens * kv * 2 * 4 * n_b // nb)
 
-        if _SKIP_RELOC_EXPERIMENT:
-            nb = 0                    # timing experiment only: wrong results
         lb = lay.reloc_layer_blocks
         fused_reloc = bool(nb) and self.fuse_reloc and "inject" not in buf
 
@@ -700,6 +715,10 @@ class DeviceDecoder:
 
     def step(self, token: int):
         """Append `token` at the next position; device logits row [1, V] (model.py:413-439)."""
+        with self.r.serial():
+            return self._step(token)
+
+    def _step(self, token: int):
         torch = _torch()
         r, cfg, dw = self.r, self.r.cfg, self.r.dw
         if self.n >= self.cap:

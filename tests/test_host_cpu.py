@@ -235,7 +235,7 @@ def _spec(pre, T, nimg, suf, ratios, hits=None):
              for m, h in enumerate(hits)]
     spec = RequestSpec(n=len(seq), text_pos=tpos, text_ids=tpos % 7,
                        images=[(s.start, s.length) for s in segs], keep=keep,
-                       kv_hit=[bool(h and keep[0, m] < T) for m, h in enumerate(hits)],
+                       kv_hit=[bool(h and (keep[:, m] < T).any()) for m, h in enumerate(hits)],
                        enc_src=[(SRC_STORE, m * T) for m in range(nimg)], page_rows=pages)
     return seq, plan, spec
 
@@ -246,6 +246,7 @@ def _spec(pre, T, nimg, suf, ratios, hits=None):
     (16, 64, 3, 16, (0.3, 0.1, 0.1, 0.0), [True, False, True]),
     (0, 64, 2, 0, (1.0, 1.0), None),
     (5, 16, 0, 0, (0.0, 0.0), None),
+    (4, 32, 2, 4, (1.0, 0.1, 0.1, 0.0), None),     # full first layer, reuse below it
 ])
 def test_layout_rows_match_masks(pre, T, nimg, suf, ratios, hits):
     seq, plan, spec = _spec(pre, T, nimg, suf, ratios, hits)
