@@ -128,6 +128,13 @@ class ReuseMetrics:
 _PINNED: dict = {}   # numel -> pinned host staging row for last_logits()
 
 
+def _locked(fn, lock):
+    def call():
+        with lock:
+            return fn()
+    return call
+
+
 class ReuseResult:
     """positions (host), logits [len(positions), V] and merged pre-RoPE KV, device-backed."""
 
@@ -141,12 +148,7 @@ class ReuseResult:
         # result (copies it out of the shared workspace) and reuses the workspace
         self._lock = lock if lock is not None else threading.RLock()
         if kv._loader is not None:
-            loader = kv._loader
-
-            def locked_load():
-                with self._lock:
-                    return loader()
-            kv._loader = locked_load
+            kv._loader = _locked(kv._loader, self._lock)   # no reference back to self (no cycle)
 
     @property
     def device_logits(self):

@@ -307,9 +307,12 @@ class DeviceWeights:
         else:
             kv, n_qkv, kkv, perm, c0, c1 = self.kv, self.n_qkv, self.kkv, self.perm, self.c0, self.c1
         full_get = get
+        drawn = {}
 
         def get(name):                      # noqa: F811 -- head slice of the attention weights
-            w = full_get(name)
+            if name not in drawn:           # one draw per tensor (get() may be asked twice)
+                drawn[name] = full_get(name)
+            w = drawn[name]
             if name in ("wq", "wk", "wv"):
                 return w[:, c0:c1]
             if name == "wo":

@@ -346,3 +346,24 @@ def test_int_pack_template_and_patches():
     assert (tpl == np.concatenate(pk.parts)).all()          # template untouched
     # every view keeps 16-byte alignment
     assert all(off % 4 == 0 for off, _ in q.off.values())
+
+
+def test_reuse_result_is_freed_without_gc():
+    """A dropped ReuseResult must die by reference count: the runner keeps only weak references
+    to live results and copies out (detaches) those still alive when their workspace set comes
+    round again -- a reference cycle would keep every result alive until a GC pass and make each
+    call copy the previous result's logits and merged KV."""
+    import gc
+    import threading
+    import weakref
+    from paper_2512_12977_b200.engine import ReuseMetrics, ReuseResult
+    from paper_2512_12977_b200.model import KVTensors
+    gc.disable()
+    try:
+        res = ReuseResult(np.arange(3), object(), KVTensors(loader=lambda: (None, None)), ReuseMetrics(),
+                          threading.RLock())
+        ref = weakref.ref(res)
+        del res
+        assert ref() is None
+    finally:
+        gc.enable()
