@@ -348,7 +348,6 @@ def main():
 
     import paper_2512_12977_b200 as P
     from paper_2512_12977_b200.engine import _runner, prefill_with_reuse
-    from paper_2512_12977_b200 import runtime as RT
     if args.workload == "C5":
         run_c5(args, wl, P, rank, world, local, dist)
         return
@@ -500,26 +499,11 @@ def main():
                 a = fl_k / (ms_k / 1e3) / 1e12
                 others[k] = {"bound": "tensor", "achieved": round(a, 2), "peak": tf_burst, "unit": "TFLOP/s",
                              "frac": round(a / tf_burst, 4), "note": "causal-effective FLOPs"}
-    # kv_relocate against its own roofline: the production chain runs it per layer on a low-priority
-    # side stream as wide CTAs that only fill idle SMs (its event times above include that
-    # sharing); here the same relocation runs as ONE launch of the full-rate kernel, alone.
-    try:
-        runner.tracer, runner.overlap_reloc = [], False
-        runner.lib.vlc_set_tuning(14, 0)
-        for _ in range(3):
-            _flush_l2(flush)
-            prefill_with_reuse(model, req, store)
-        torch.cuda.synchronize()
-        rl = [(e0.elapsed_time(e1), nb) for name, e0, e1, nb, fl in runner.tracer if name == "kv_relocate"]
-        if rl:
-            ms_r, nb_r = statistics.median(x[0] for x in rl), rl[0][1]
-            a = nb_r / (ms_r / 1e3) / 1e9
-            others["kv_relocate_single_launch"] = {
-                "bound": "hbm", "achieved": round(a, 1), "peak": hbm, "unit": "GB/s", "frac": round(a / hbm, 4),
-                "us": round(ms_r * 1e3, 1), "algorithmic": f"{nb_r / 1e6:.1f} MB (all layers; K+V read + write)"}
-    finally:
-        runner.tracer, runner.overlap_reloc = None, RT._OVERLAP_RELOC
-        runner.lib.vlc_set_tuning(14, int(os.environ.get("VLC_RELOC_WIDE", "100000")))
+    # kv_relocate against its own roofline: the prefill chain reads cached chunks straight from the
+    # store (the gather + re-rotation fused into the attention) and relocates only the rows sharing
+    # a chunk with recomputed ones; here the UNFUSED kernel moves every cached row of the request
+    # (read K, V from the store + write rotated K, V into request rows) as one launch, alone.
+    others["kv_relocate_single_launch"] = relocate_standalone(P, model, req, store, runner, flush, hbm)
     if args.trace:
         with open(args.trace, "w") as fh:
             json.dump({"kernels": kernels, "agg": {k: v for k, v in agg.items()}}, fh, indent=1)
@@ -564,6 +548,43 @@ def main():
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def relocate_standalone(P, model, req, store, runner, flush, hbm, reps=5):
+    """vlc_kv_relocate of every cached (layer, token) row of the request, timed alone (CUDA events,
+    L2 flushed before each launch); algorithmic bytes = rows x kv x 2 B x 4 (K, V read + written)."""
+    import torch
+    from paper_2512_12977_b200 import _native as N
+    from paper_2512_12977_b200.engine import _resolve
+    from paper_2512_12977_b200.layout import full_relocation
+    cfg, dw = model.config, model.device
+    res = _resolve(model, req, store)
+    descs, blocks, ptab, rows = full_relocation([res.spec], cfg.num_layers)
+    if not rows:
+        return None
+    pool = res.kv_pool
+    dd, bb, pt = (torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (descs, blocks, ptab))
+    n, kv = res.spec.n, dw.kv
+    kc = torch.empty(cfg.num_layers, n, kv, dtype=torch.bfloat16, device="cuda")
+    vc = torch.empty_like(kc)
+    dw.ensure_positions(n + 1)
+    times = []
+    for _ in range(reps + 1):
+        _flush_l2(flush)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        N.call("vlc_kv_relocate", pool.k.data_ptr(), pool.v.data_ptr(), pool.P, pt.data_ptr(), kv, cfg.head_dim,
+               kc.data_ptr(), vc.data_ptr(), n, dd.data_ptr(), bb.data_ptr(), len(blocks), dw.cos.data_ptr(),
+               dw.sin.data_ptr(), cfg.head_dim // 2, torch.cuda.current_stream().cuda_stream)
+        e1.record()
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = statistics.median(times[1:])
+    nb = rows * kv * 2 * 4
+    a = nb / (ms / 1e3) / 1e9
+    return {"bound": "hbm", "achieved": round(a, 1), "peak": hbm, "unit": "GB/s", "frac": round(a / hbm, 4),
+            "us": round(ms * 1e3, 1), "algorithmic": f"{nb / 1e6:.1f} MB (all layers; K+V read + write)",
+            "note": "unfused kernel, measured alone; the chain reads these rows in the attention instead"}
 
 
 def cpu_leg_run(P, model, store, hashes, text, wl, plan, req, export, reps):

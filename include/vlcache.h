@@ -96,33 +96,37 @@ typedef struct vlc_epilogue {
   float* red_scratch;
 } vlc_epilogue;
 
-/* Mixed attention over cached + recomputed KV (engine.py:181-182, model.py:268-291).
- * Work items: int32[n_items][8] = {q_row0, n_q<=128, head, kv_row0, key_begin,
- * key_end, slot, 0}; slot<0 writes normalised bf16 rows to out[rowof[q]], slot>=0
- * writes an unnormalised fp32 partial to ws_o/ws_ml for vlc_attn_combine.
- * Combine items: int32[n_comb][8] = {q_row0, n_q, head, slot0, nslots, 0,0,0}.   */
-typedef struct vlc_attn_args {
-  const void* q; int q_rows_cap;                 /* bf16 [q_rows_cap][kv]            */
-  const void* kc; const void* vc;                /* bf16 [layers][kv_rows_cap][kv]   */
+/* Paged attention (vlc_attn_paged; model.py:274-291, engine.py:179-182): the recomputed queries of
+ * one layer over all keys of their request.  The keys are a list of 64-key CHUNKS (contiguous
+ * positions) per (request, layer): chunks int32[n][4] = {pos0, len <= 64, a, b}
+ *   b <  0: request rows a .. a+63 of kc / vc (K already rotated: text / recomputed tokens);
+ *   b >= 0: store rows page_table[a] * page_rows + b .. +63 of pool_k / pool_v (cached image tokens,
+ *           K pre-RoPE: rotated to positions pos0 .. pos0+63 in shared memory with the fp32 tables).
+ * A 128-key tile = two consecutive chunks (lists padded to an even length with len = 0 chunks).
+ * items int32[n][8] = {q_row0, n_q <= 128, head, chunk0, tile_begin, tile_end, group,
+ * (part << 8) | nsplit}: queries q_row0 .. (position-sorted, positions qpos, output rows rowof)
+ * over tiles [tile_begin, tile_end) of the chunk list starting at chunk0.  group < 0 writes
+ * normalised rows; otherwise the nsplit CTAs of a group merge their fp32 partials (ws_o >= groups*8*256*hd
+ * floats, ws_ml >= groups*8*256*2) in-kernel -- every CTA must be co-resident (n_items <= #SMs),
+ * counters >= 2*ws_slots ints, zero, left zero. */
+typedef struct vlc_attn_paged_args {
+  const void* q; int q_rows_cap;                 /* bf16 [q_rows_cap][kv] rotated queries        */
+  const void* kc; const void* vc;                /* bf16 [layers][kv_rows_cap][kv] request K / V */
   int layers_cap; int kv_rows_cap; int layer;
+  const void* pool_k; const void* pool_v;        /* bf16 [pool_rows][kv] store pages (or NULL)   */
+  int pool_rows; const int* page_table; int page_rows;
+  const float* cos_tab; const float* sin_tab; int tab_ld;   /* fp32 [pos][head_dim/2]           */
   int kv; int heads; int head_dim;
+  const int* chunks;
   const int* items; int n_items;
-  const int* qpos;                               /* [q] position within request       */
-  const int* rowof;                              /* [q] packed output row             */
-  void* out; int ldo;                            /* bf16 [rows][ldo]                  */
+  const int* qpos;                               /* [q] position within request                  */
+  const int* rowof;                              /* [q] output row                               */
+  void* out; int ldo;                            /* bf16 [rows][ldo], PACKED when pk_rows > 0    */
+  int pk_rows; int pk_kb;
   float* ws_o; float* ws_ml; int ws_slots;
-  const int* comb; int n_comb;
-  float scale_log2;                              /* log2(e) / sqrt(head_dim)          */
-  int* counters;                                 /* >= 2*ws_slots ints, zeroed (pp)   */
-  int pk_rows; int pk_kb;                        /* > 0: output rows written PACKED   */
-} vlc_attn_args;
-
-/* Ping-pong attention (vlc_attn_pp): one CTA = up to 256 queries of one request and head
- * (two 128-query tiles with their own softmax warpgroups sharing each K/V tile) over a key
- * range.  Items int32[n][8] = {q_row0, n_q<=256, head, kv_row0, key_begin, key_end, group,
- * (part << 8) | nsplit}; group < 0 writes normalised rows directly, otherwise the nsplit
- * CTAs of a group merge their partials in parallel (all CTAs must be co-resident: the
- * launch is cooperative when any group is split, so n_items <= #SMs then). */
+  int* counters;
+  float scale_log2;                              /* log2(e) / sqrt(head_dim)                     */
+} vlc_attn_paged_args;
 
 const char* vlc_last_error(void);
 int vlc_version(void);
@@ -134,7 +138,6 @@ int vlc_copy_h2d_async(void* device_dst, const void* host_src, size_t bytes, cud
    vlc_capi.cu and INTEGRATION.md (e.g. 15 = attention kernel variant). */
 int vlc_set_tuning(int key, int value);
 int vlc_set_debug_buffer(void* device_ptr);
-int vlc_set_trace_buffer(void* device_ptr);   /* experiments: attention CTA-0 event trace (>= 224 u64) */
 
 /* Layer-0 hidden rows of the computed set (model.py:339-359, engine.py:167).
  * src int32[rows][2] = {kind, index}: kind 0 -> bf16 embed row `index` (text token id),
@@ -192,9 +195,7 @@ int vlc_gemm_bf16_relocate(const void* w, int n_pad, int k_pad, const void* x, i
                            int n_blocks, const float* cos_tab, const float* sin_tab, int tab_ld,
                            cudaStream_t stream);
 
-int vlc_attn_mixed(const vlc_attn_args* args, cudaStream_t stream);
-int vlc_attn_combine(const vlc_attn_args* args, cudaStream_t stream);
-int vlc_attn_pp(const vlc_attn_args* args, cudaStream_t stream);
+int vlc_attn_paged(const vlc_attn_paged_args* args, cudaStream_t stream);
 
 /* Patchify (model.py:312-314): pixels f32 [side][side] -> bf16 patches, PACKED with row tile
  * pk_rows (patch rows start at row `row0`), K = patch^2 (kb blocks pk_kb). */

@@ -10,7 +10,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libvlcache.so")
-SOURCES = ["vlc_misc.cu", "vlc_gemm.cu", "vlc_gemm_pair.cu", "vlc_attn.cu", "vlc_capi.cu"]
+SOURCES = ["vlc_misc.cu", "vlc_gemm.cu", "vlc_gemm_pair.cu", "vlc_attn_paged.cu", "vlc_capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include")]

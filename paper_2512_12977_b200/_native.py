@@ -17,8 +17,8 @@ VLC_OK, VLC_ERR_INVALID, VLC_ERR_UNSUPPORTED, VLC_ERR_CUDA = 0, 1, 2, 3
 EPI_F32, EPI_RESID, EPI_BF16, EPI_BIAS_ADD, EPI_SWIGLU, EPI_QKV_PLAIN, EPI_QKV_ROPE = range(7)
 
 EXPORTS = ("vlc_last_error", "vlc_version", "vlc_embed_assemble", "vlc_rmsnorm", "vlc_add_rmsnorm", "vlc_kv_relocate",
-           "vlc_store_write_pages", "vlc_gemm_bf16", "vlc_gemm_bf16_relocate", "vlc_gemm_row_tile", "vlc_pack_operand", "vlc_attn_mixed", "vlc_attn_combine", "vlc_attn_pp",
-           "vlc_patchify", "vlc_set_tuning", "vlc_set_debug_buffer", "vlc_set_trace_buffer", "vlc_copy_h2d_async")
+           "vlc_store_write_pages", "vlc_gemm_bf16", "vlc_gemm_bf16_relocate", "vlc_gemm_row_tile", "vlc_pack_operand", "vlc_attn_paged",
+           "vlc_patchify", "vlc_set_tuning", "vlc_set_debug_buffer", "vlc_copy_h2d_async")
 
 
 class NativeError(KVReuseError):
@@ -38,15 +38,19 @@ class Epilogue(C.Structure):
                 ("l2_prefetch", C.c_void_p), ("l2_prefetch_bytes", C.c_ulonglong), ("red_scratch", C.c_void_p)]
 
 
-class AttnArgs(C.Structure):
+class AttnPagedArgs(C.Structure):
+    """include/vlcache.h vlc_attn_paged_args."""
     _fields_ = [("q", C.c_void_p), ("q_rows_cap", C.c_int), ("kc", C.c_void_p), ("vc", C.c_void_p),
                 ("layers_cap", C.c_int), ("kv_rows_cap", C.c_int), ("layer", C.c_int),
+                ("pool_k", C.c_void_p), ("pool_v", C.c_void_p), ("pool_rows", C.c_int),
+                ("page_table", C.c_void_p), ("page_rows", C.c_int),
+                ("cos_tab", C.c_void_p), ("sin_tab", C.c_void_p), ("tab_ld", C.c_int),
                 ("kv", C.c_int), ("heads", C.c_int), ("head_dim", C.c_int),
-                ("items", C.c_void_p), ("n_items", C.c_int), ("qpos", C.c_void_p),
-                ("rowof", C.c_void_p), ("out", C.c_void_p), ("ldo", C.c_int),
+                ("chunks", C.c_void_p), ("items", C.c_void_p), ("n_items", C.c_int),
+                ("qpos", C.c_void_p), ("rowof", C.c_void_p), ("out", C.c_void_p), ("ldo", C.c_int),
+                ("pk_rows", C.c_int), ("pk_kb", C.c_int),
                 ("ws_o", C.c_void_p), ("ws_ml", C.c_void_p), ("ws_slots", C.c_int),
-                ("comb", C.c_void_p), ("n_comb", C.c_int), ("scale_log2", C.c_float),
-                ("counters", C.c_void_p), ("pk_rows", C.c_int), ("pk_kb", C.c_int)]
+                ("counters", C.c_void_p), ("scale_log2", C.c_float)]
 
 
 _lib = None
@@ -72,14 +76,11 @@ def load():
         lib.vlc_gemm_bf16_relocate.argtypes = [vp, i, i, vp, i, i, C.POINTER(Epilogue), i, vp, C.c_size_t, vp,
                                                vp, vp, i, vp, i, i, vp, vp, i, vp, vp, i, vp, vp, i, vp]
         lib.vlc_pack_operand.argtypes = [vp, i, i, i, vp, i, i, vp]
-        lib.vlc_attn_mixed.argtypes = [C.POINTER(AttnArgs), vp]
-        lib.vlc_attn_combine.argtypes = [C.POINTER(AttnArgs), vp]
-        lib.vlc_attn_pp.argtypes = [C.POINTER(AttnArgs), vp]
+        lib.vlc_attn_paged.argtypes = [C.POINTER(AttnPagedArgs), vp]
         lib.vlc_patchify.argtypes = [vp, i, i, vp, i, i, i, vp]
         lib.vlc_set_tuning.argtypes = [i, i]
         lib.vlc_copy_h2d_async.argtypes = [vp, vp, C.c_size_t, vp]
         lib.vlc_set_debug_buffer.argtypes = [vp]
-        lib.vlc_set_trace_buffer.argtypes = [vp]
         for name in EXPORTS:
             getattr(lib, name).restype = C.c_char_p if name == "vlc_last_error" else i
         _lib = lib

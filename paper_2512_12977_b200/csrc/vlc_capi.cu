@@ -119,16 +119,12 @@ int vlc_set_tuning(int key, int value) {
   switch (key) {
     case 1: vlc::g_stage_override = value; return VLC_OK;        // GEMM pipeline stages (0 = auto)
     case 2: vlc::g_coop = value; return VLC_OK;                  // cooperative launch when PDL is off
-    case 4: vlc::set_attn_debug_buffer(nullptr); return VLC_OK;  // detach the attention debug buffer
-    case 5: vlc::g_attn_min_smem = value; return VLC_OK;         // attention smem lower bound (occupancy tests)
     case 6: vlc::g_pdl = value; return VLC_OK;                   // programmatic dependent launch
     case 7: vlc::g_wide = value; return VLC_OK;                  // 256-row GEMM tiles
     case 9: vlc::g_unsplit_min = value; return VLC_OK;           // one-CTA-per-tile threshold
     case 10: vlc::g_pair = value; return VLC_OK;                 // CTA-pair GEMM threshold
-    case 12: vlc::g_attn_kt = value == 64 ? 64 : 128; return VLC_OK;   // attention key tile (two-tile kernel)
     case 13: vlc::g_deterministic = value != 0; return VLC_OK;   // bitwise-reproducible RESID reduction
     case 14: vlc::g_reloc_wide = value; return VLC_OK;           // idle-SM relocation CTA smem (0 = plain)
-    case 15: vlc::g_attn_var = value; return VLC_OK;             // attention kernel variant
     case 16: vlc::g_mc = value >= 1 && value <= 8 ? value : 1; return VLC_OK;   // GEMM cluster multicast
     case 17: vlc::g_aligned_split = value; return VLC_OK;        // tile-aligned split-K
     case 18: vlc::g_decoupled = value; return VLC_OK;            // decoupled weight / activation rings
@@ -137,17 +133,10 @@ int vlc_set_tuning(int key, int value) {
     default: return fail(VLC_ERR_INVALID, "set_tuning: unknown key");
   }
 }
-/* Experiments only: device buffer (>= 224 u64) receiving per-iteration event times of attention CTA 0. */
-int vlc_set_trace_buffer(void* p) {
-  vlc::set_attn_trace_buffer(reinterpret_cast<unsigned long long*>(p));
-  return VLC_OK;
-}
 /* Experiments only: device buffer receiving per-CTA phase timestamps of the GEMM (NULL = off). */
 int vlc_set_debug_buffer(void* p) {
   vlc::set_debug_buffer(reinterpret_cast<unsigned long long*>(p));
-  vlc::set_attn_debug_buffer(reinterpret_cast<unsigned long long*>(p));
   return VLC_OK;
-  return fail(VLC_ERR_INVALID, "set_tuning: unknown key");
 }
 int vlc_version(void) { return 100; }
 
@@ -255,28 +244,19 @@ int vlc_gemm_bf16_relocate(const void* w, int n_pad, int k_pad, const void* x, i
                      "gemm_relocate");
 }
 
-int vlc_attn_mixed(const vlc_attn_args* a, cudaStream_t stream) {
-  if (!a || !a->q || !a->kc || !a->vc || !a->items) return fail(VLC_ERR_INVALID, "attn: null pointer");
+int vlc_attn_paged(const vlc_attn_paged_args* a, cudaStream_t stream) {
+  if (!a || !a->q || !a->kc || !a->vc || !a->items || !a->chunks || !a->qpos || !a->rowof || !a->out)
+    return fail(VLC_ERR_INVALID, "attn_paged: null pointer");
   if (a->head_dim != 16 && a->head_dim != 32 && a->head_dim != 64 && a->head_dim != 128)
-    return fail(VLC_ERR_UNSUPPORTED, "attn: head_dim must be 16/32/64/128");
-  if (a->kv != a->heads * a->head_dim) return fail(VLC_ERR_INVALID, "attn: kv != heads*head_dim");
-  return cuda_status(launch_attention(*a, stream), "attn_mixed");
-}
-
-int vlc_attn_pp(const vlc_attn_args* a, cudaStream_t stream) {
-  if (!a || !a->q || !a->kc || !a->vc || !a->items) return fail(VLC_ERR_INVALID, "attn_pp: null pointer");
-  if (a->head_dim != 16 && a->head_dim != 32 && a->head_dim != 64 && a->head_dim != 128)
-    return fail(VLC_ERR_UNSUPPORTED, "attn_pp: head_dim must be 16/32/64/128");
-  if (a->kv != a->heads * a->head_dim) return fail(VLC_ERR_INVALID, "attn_pp: kv != heads*head_dim");
-  // split groups need every CTA resident at once (parallel merge); cooperative launch checks it
-  const bool coop = a->ws_slots > 0;
-  if (coop && !a->counters) return fail(VLC_ERR_INVALID, "attn_pp: split groups need counters");
-  return cuda_status(launch_attention_pp(*a, stream, coop), "attn_pp");
-}
-
-int vlc_attn_combine(const vlc_attn_args* a, cudaStream_t stream) {
-  if (!a) return fail(VLC_ERR_INVALID, "attn_combine: null");
-  return cuda_status(launch_attn_combine(*a, stream), "attn_combine");
+    return fail(VLC_ERR_UNSUPPORTED, "attn_paged: head_dim must be 16/32/64/128");
+  if (a->kv != a->heads * a->head_dim) return fail(VLC_ERR_INVALID, "attn_paged: kv != heads*head_dim");
+  if (a->pool_k && (!a->pool_v || !a->page_table || a->page_rows <= 0 || !a->cos_tab || !a->sin_tab ||
+                    a->tab_ld != a->head_dim / 2))
+    return fail(VLC_ERR_INVALID, "attn_paged: store chunks need pools, page table and RoPE tables");
+  // split groups merge in-kernel: every CTA of the launch must be resident at once
+  if (a->ws_slots > 0 && (!a->counters || !a->ws_o || !a->ws_ml || a->n_items > 148))
+    return fail(VLC_ERR_INVALID, "attn_paged: split groups need counters / workspaces and <= 148 items");
+  return cuda_status(launch_attention_paged(*a, stream), "attn_paged");
 }
 
 int vlc_patchify(const float* pixels, int side, int patch, void* out, int row0, int pk_rows, int pk_kb,

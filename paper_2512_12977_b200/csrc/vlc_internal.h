@@ -22,9 +22,6 @@ enum EpiKind {
 using GemmEpi = vlc_epilogue;
 
 extern int g_stage_override;  // experiment knob (vlc_set_tuning key 1)
-extern int g_attn_var;        // key 15: softmax variant of the hd-128 attention kernel
-extern int g_attn_kt;         // key 12: key tile of the hd-128 attention kernel (64 / 128)
-extern int g_attn_min_smem;   // key 5: lower bound on the attention kernel's dynamic smem
 extern int g_coop;            // key 2: cooperative launch of the stream-K GEMM
 extern int g_deterministic;   // key 13: bitwise run-to-run reproducible RESID GEMMs (slower)
 extern int g_reloc_wide;      // key 14: idle-SM relocation variant (smem bytes requested; 0 = off)
@@ -116,8 +113,6 @@ cudaError_t launch_gemm_pair(const void* W, int n_pad, int k_pad, const void* X,
                              const GemmEpi& epi, int max_pairs, cudaStream_t stream);
 cudaError_t launch_pack(const void* src, int rows, int cols, int ld, void* dst, int R, int KB, cudaStream_t s);
 
-cudaError_t launch_attention(const vlc_attn_args& a, cudaStream_t stream);
-cudaError_t launch_attn_combine(const vlc_attn_args& a, cudaStream_t stream);
-cudaError_t launch_attention_pp(const vlc_attn_args& a, cudaStream_t stream, bool coop);
+cudaError_t launch_attention_paged(const vlc_attn_paged_args& a, cudaStream_t stream);
 
 }  // namespace vlc

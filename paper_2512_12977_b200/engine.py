@@ -324,7 +324,7 @@ def _resolve(model: ToyVLM, request: ReuseRequest, store: CacheStore, miss_base:
     metrics.flops = _flops_from_counts(counts, len(seq), cfg, metrics.encoder_misses)
     spec = RequestSpec(n=len(seq), text_pos=text_pos, text_ids=text_ids,
                        images=[(s.start, s.length) for s in segs], keep=keep, kv_hit=kv_hit,
-                       enc_src=enc_src, page_rows=page_rows)
+                       enc_src=enc_src, page_rows=page_rows, page_tokens=kv_pool.P if kv_pool is not None else 64)
     return _Resolved(spec, metrics, enc_pool, kv_pool, miss_px)
 
 

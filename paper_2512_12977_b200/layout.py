@@ -35,6 +35,7 @@ class RequestSpec:
     kv_hit: list                  # per image: True if cached KV is reused (relocated)
     enc_src: list                 # per image: (SRC_STORE|SRC_SCRATCH, row base)
     page_rows: list = field(default_factory=list)  # per image: int32 [L, ppl] page ids (kv_hit only)
+    page_tokens: int = 64         # token rows per store page
 
 
 @dataclass
@@ -54,10 +55,10 @@ class Layout:
     qpos: np.ndarray
     rowof: np.ndarray
     q_ranges: list                # per layer: list of (req, q0, count)
-    # attention work (per layer) + combine entries
+    # attention work (per layer): key chunks + work items of vlc_attn_paged
+    attn_chunks: list             # per layer: int32 [n_chunks, 4] {pos0, len, a, b} (all requests)
     attn_items: list              # per layer: int32 [n, 8]
-    comb_items: list              # per layer: int32 [m, 8]
-    attn_slots: int               # max partial slots over layers
+    attn_slots: int               # max split groups over layers
     # relocation
     reloc_descs: np.ndarray       # int32 [d, 8]
     reloc_blocks: np.ndarray      # int32 [b, 2]
@@ -80,7 +81,7 @@ class Layout:
                   self.reloc_descs, self.reloc_blocks, self.final_rows, self.row_src[:, 0]):
             h.update(np.ascontiguousarray(a).tobytes())
             h.update(b"|")
-        for a in self.attn_items + self.comb_items:
+        for a in self.attn_items + self.attn_chunks:
             h.update(np.ascontiguousarray(a).tobytes())
         h.update(f"{len(self.page_table)}|{self.kv_rows}|{self.attn_slots}".encode())
         return h.digest()
@@ -116,126 +117,150 @@ def _depths(spec: RequestSpec, L: int, text_base: int, img_base: int):
     return tuple(np.concatenate(a) for a in (pos, dep, kind, idx, tref, iref, tt))
 
 
-def attention_work(q_ranges, qpos, n_req, heads, target_items: int):
-    """Split (request, head, 128-query tile) key ranges into <= target_items CTAs.
-
-    Returns (items int32 [n, 8], comb int32 [m, 8], slots)."""
-    tiles = []
-    for req, q0, cnt in q_ranges:
-        for t0 in range(q0, q0 + cnt, 128):
-            nq = min(128, q0 + cnt - t0)
-            kend = int(qpos[t0 + nq - 1]) + 1
-            kend = min(kend, int(n_req[req]))
-            tiles.append((req, t0, nq, kend))
-    total = sum((kend + 127) // 128 for _, _, _, kend in tiles) * heads
-    chunk = max(2, -(-total // max(1, target_items)))
-    items, comb, slot = [], [], 0
-    for h in range(heads):
-        for req, t0, nq, kend in tiles:
-            nt = (kend + 127) // 128
-            ns = -(-nt // chunk)
-            if ns <= 1:
-                items.append([t0, nq, h, 0, 0, kend, -1, req])
-                continue
-            bounds = [min(kend, (nt * s // ns) * 128) for s in range(ns)] + [kend]
-            for s in range(ns):
-                items.append([t0, nq, h, 0, bounds[s], bounds[s + 1], slot + s, req])
-            comb.append([t0, nq, h, slot, ns, 0, 0, 0])
-            slot += ns
-    it = np.array(items, dtype=np.int32).reshape(-1, 8)
-    cb = np.array(comb, dtype=np.int32).reshape(-1, 8)
-    return it, cb, slot
+CHUNK = 64        # keys per attention chunk (vlc_attn_paged); a 128-key tile is two chunks
 
 
-# Attention work decomposition (and the matching vlc_attn_pp kernel, tuning key 15): single 128-query
-# tiles per CTA with S double-buffered (default; measured 31.7 -> 26.8 us per C3 layer) or the
-# two-tile ping-pong kernel (VLC_ATTN_ONE=0).  The two must agree: two-tile items (up to 256 queries)
-# on the single-tile kernel would drop queries 128..255.
-ATTN_ONE_TILE = bool(int(os.environ.get("VLC_ATTN_ONE", "1")))
+def contiguous_chunks(row0: int, n: int) -> np.ndarray:
+    """Chunks of a request whose n keys (positions 0..n-1) all sit in request rows row0.. ."""
+    out = [[c, min(CHUNK, n - c), row0 + c, -1] for c in range(0, n, CHUNK)]
+    return _pad_even(out)
 
 
-def attn_kernel_variant() -> int:
-    """vlc_set_tuning(15, .) value matching ATTN_ONE_TILE (39: single tile, two softmax threads per row,
-    each column half with its own max / sum / O accumulator;
-    0: ping-pong)."""
-    return 39 if ATTN_ONE_TILE else 0
+def _pad_even(out):
+    if len(out) % 2:          # a masked (len 0) chunk that reads valid memory: the previous source
+        last = out[-1]
+        out.append([last[0] + CHUNK, 0, last[2], last[3]])
+    return np.array(out, dtype=np.int32).reshape(-1, 4)
 
 
-def attention_work(q_ranges, qpos, n_req, heads, max_ctas: int = 148):
-    """Work items for vlc_attn_pp in the configured decomposition (ATTN_ONE_TILE)."""
-    fn = attention_work_one if ATTN_ONE_TILE else attention_work_pp
-    return fn(q_ranges, qpos, n_req, heads, max_ctas)
+def store_chunks_ok(T: int, P: int) -> bool:
+    """A 64-key chunk of an image lies inside one store page (else the layer's cached rows are
+    relocated into the request rows instead of being read from the store)."""
+    return P % CHUNK == 0 or T <= P
 
 
-def attention_work_one(q_ranges, qpos, n_req, heads, max_ctas: int = 148):
-    """Work items of the single-query-tile attention kernel (vlc_attn_pp, tuning 15 = 30): one CTA
-    per (request, head, <= 128 sorted queries, key range).  Key ranges are split so every CTA gets
-    about the same number of 128-key tiles (a query tile's keys end at its last query's position, so
-    late tiles get more splits); <= 8 splits per tile, all CTAs co-resident when anything is split.
+def request_chunks(spec: RequestSpec, i: int, kvoff: int, page_base: dict) -> np.ndarray:
+    """Key chunks of one request at layer i, in position order (vlc_attn_paged, include/vlcache.h):
+    text runs and recomputed image chunks from the request rows; image chunks at or past the
+    layer's keep count straight from the store page (a = page-table index, b = row offset); the
+    chunk holding the keep boundary from the request rows (its cached rows relocated there)."""
+    spans = sorted(spec.images)
+    out, cur = [], 0
 
-    Returns (items int32 [n, 9], n_groups)."""
+    def text_run(a, b):
+        for c in range(a, b, CHUNK):
+            out.append([c, min(CHUNK, b - c), kvoff + c, -1])
+    for m, (start, T) in sorted(enumerate(spec.images), key=lambda e: e[1][0]):
+        text_run(cur, start)
+        k = int(spec.keep[i, m])
+        hit = bool(spec.kv_hit[m])
+        P = int(spec.page_tokens)
+        direct = hit and store_chunks_ok(T, P)
+        ppl = np.asarray(spec.page_rows[m]).shape[1] if hit else 0
+        for t0 in range(0, T, CHUNK):
+            ln = min(CHUNK, T - t0)
+            if direct and t0 >= k:
+                out.append([start + t0, ln, page_base[m] + i * ppl + t0 // P, t0 % P])
+            else:
+                out.append([start + t0, ln, kvoff + start + t0, -1])
+        cur = start + T
+    text_run(cur, spec.n)
+    del spans
+    return _pad_even(out)
+
+
+def relocated_ranges(spec: RequestSpec, i: int):
+    """Per image: the cached token range [k, e) of layer i that goes through vlc_kv_relocate into
+    the request rows -- the rest of the keep boundary's chunk (the chunk is read from the request
+    rows), or every cached row when the page size does not allow direct store chunks."""
+    out = []
+    for m, (start, T) in enumerate(spec.images):
+        if not spec.kv_hit[m]:
+            continue
+        k = int(spec.keep[i, m])
+        if k >= T:
+            continue
+        if not store_chunks_ok(T, int(spec.page_tokens)):
+            e = T
+        else:
+            e = min(T, -(-k // CHUNK) * CHUNK)
+        if e > k:
+            out.append((m, k, e))
+    return out
+
+
+def full_relocation(specs: list, L: int):
+    """vlc_kv_relocate descriptors that move EVERY cached (layer, token) row of the batch into the
+    request rows -- the unfused gather + re-rotation + scatter, used to measure that kernel against
+    its own HBM roofline (bench.py); the prefill chain itself reads cached chunks from the store.
+    Returns (descs int32 [d, 8], blocks int32 [b, 2], page_table, rows)."""
+    n_req = [s.n for s in specs]
+    kvoff = np.concatenate([[0], np.cumsum(n_req)[:-1]]).astype(np.int64)
+    pages, base = [], {}
+    for r, spec in enumerate(specs):
+        for m in range(len(spec.images)):
+            if spec.kv_hit[m]:
+                base[(r, m)] = sum(len(p) for p in pages)
+                pages.append(np.asarray(spec.page_rows[m], dtype=np.int32).reshape(-1))
+    descs, blocks, rows = [], [], 0
+    for i in range(L):
+        for r, spec in enumerate(specs):
+            for m, (start, T) in enumerate(spec.images):
+                k = int(spec.keep[i, m])
+                if not spec.kv_hit[m] or k >= T:
+                    continue
+                ppl = np.asarray(spec.page_rows[m]).shape[1]
+                for off in range(0, T - k, RELOC_TOK):
+                    blocks.append([len(descs), off])
+                descs.append([i, base[(r, m)] + i * ppl, k, T - k, int(kvoff[r]) + start + k, start + k, 0, 0])
+                rows += T - k
+    return (np.array(descs, np.int32).reshape(-1, 8), np.array(blocks, np.int32).reshape(-1, 2),
+            (np.concatenate(pages) if pages else np.zeros(1, np.int32)).astype(np.int32), rows)
+
+
+def attention_work(q_ranges, qpos, tiles_of, chunk0, heads, max_ctas: int = 148):
+    """Work items of vlc_attn_paged: one CTA per (request, head, <= 128 position-sorted queries,
+    range of 128-key tiles).  tiles_of(req, max query position) = 128-key tiles the query tile
+    needs (causal); chunk0[req] = the request's chunk-list offset.  Tile ranges are split so that
+    every CTA gets about the same number of tiles (late query tiles see more keys, so they get more
+    splits); <= 8 splits per query tile, and at most max_ctas CTAs (co-resident: split groups merge
+    in-kernel) whenever anything is split.
+
+    Returns (items int32 [n, 8], number of split groups)."""
     units = []
     for h in range(heads):
         for req, q0, cnt in q_ranges:
             for t0 in range(q0, q0 + cnt, 128):
                 nq = min(128, q0 + cnt - t0)
-                kend = min(int(qpos[t0 + nq - 1]) + 1, int(n_req[req]))
-                units.append((req, t0, nq, kend, h, max(1, -(-kend // 128))))
-    total = sum(u[5] for u in units)
+                units.append((req, t0, nq, h, max(1, int(tiles_of(req, int(qpos[t0 + nq - 1]))))))
+    total = sum(u[4] for u in units)
     if len(units) >= max_ctas:
         ns = [1] * len(units)
     else:
         target = max(1, -(-total // max_ctas))
         while True:
-            ns = [max(1, min(8, -(-u[5] // target))) for u in units]
+            ns = [max(1, min(8, -(-u[4] // target))) for u in units]
             if sum(ns) <= max_ctas:
                 break
             target += 1
     items, group = [], 0
-    for (req, t0, nq, kend, h, tiles), n in zip(units, ns):
+    for (req, t0, nq, h, tiles), n in zip(units, ns):
         n = min(n, tiles)
+        c0 = int(chunk0[req])
         if n == 1:
-            items.append([t0, nq, h, 0, 0, kend, -1, (0 << 8) | 1, req])
+            items.append([t0, nq, h, c0, 0, tiles, -1, 1])
             continue
-        bounds = [min(kend, (tiles * sidx // n) * 128) for sidx in range(n)] + [kend]
+        bounds = [tiles * sidx // n for sidx in range(n)] + [tiles]
         for sidx in range(n):
-            items.append([t0, nq, h, 0, bounds[sidx], bounds[sidx + 1], group, (sidx << 8) | n, req])
+            items.append([t0, nq, h, c0, bounds[sidx], bounds[sidx + 1], group, (sidx << 8) | n])
         group += 1
-    return np.array(items, dtype=np.int32).reshape(-1, 9), group
+    return np.array(items, dtype=np.int32).reshape(-1, 8), group
 
 
-def attention_work_pp(q_ranges, qpos, n_req, heads, max_ctas: int = 148):
-    """Work items of the ping-pong attention kernel (include/vlcache.h vlc_attn_pp): one CTA per
-    (request, head, <=256 sorted queries, key range).  When there are few (query-pair, head)
-    units the key range is split so the grid fills the SMs; split groups merge in-kernel, which
-    requires every CTA co-resident, hence total CTAs <= max_ctas whenever anything is split.
-
-    Returns (items int32 [n, 8], n_groups)."""
-    pairs = []
-    for req, q0, cnt in q_ranges:
-        for t0 in range(q0, q0 + cnt, 256):
-            nq = min(256, q0 + cnt - t0)
-            kend = min(int(qpos[t0 + nq - 1]) + 1, int(n_req[req]))
-            pairs.append((req, t0, nq, kend))
-    units = len(pairs) * heads
-    ns_max = max(1, min(8, max_ctas // max(1, units)))
-    items, group = [], 0
-    for h in range(heads):
-        for req, t0, nq, kend in pairs:
-            tiles = (kend + 63) // 64
-            ns = max(1, min(ns_max, tiles // 2))
-            if ns == 1:
-                items.append([t0, nq, h, 0, 0, kend, -1, (0 << 8) | 1, req])
-                continue
-            # even key-tile split: a CTA's time follows its key-tile count (each iteration serves
-            # both query tiles), not the query-tile x key-tile work (measured: work-balanced splits
-            # leave the single-tile tail CTAs 1.7x slower)
-            bounds = [min(kend, (tiles * s // ns) * 64) for s in range(ns)] + [kend]
-            for s in range(ns):
-                items.append([t0, nq, h, 0, bounds[s], bounds[s + 1], group, (s << 8) | ns, req])
-            group += 1
-    it = np.array(items, dtype=np.int32).reshape(-1, 9)
-    return it, group
+def tiles_needed(chunks: np.ndarray, max_pos: int) -> int:
+    """128-key tiles of a position-ordered chunk list that hold keys <= max_pos."""
+    need = int(np.searchsorted(chunks[:, 0], max_pos, side="right"))
+    return -(-need // 2)
 
 
 def build_layout(specs: list[RequestSpec], L: int, heads: int, target_items: int = 296) -> Layout:
@@ -261,7 +286,14 @@ def build_layout(specs: list[RequestSpec], L: int, heads: int, target_items: int
     qdst = np.zeros((L, c0), dtype=np.int32)
     qpos = np.zeros((L, c0), dtype=np.int32)
     rowof = np.zeros((L, c0), dtype=np.int32)
-    q_ranges, attn_items, comb_items = [], [], []
+    # store pages referenced by this batch: one flat page table (per-call data), per image a base
+    pages, page_base = [], {}
+    for r, spec in enumerate(specs):
+        for m, (start, T) in enumerate(spec.images):
+            if spec.kv_hit[m]:
+                page_base[(r, m)] = sum(len(p) for p in pages)
+                pages.append(np.asarray(spec.page_rows[m], dtype=np.int32).reshape(-1))
+    q_ranges, attn_items, attn_chunks = [], [], []
     slots = 0
     for i in range(L):
         ci = int(c[i])
@@ -276,29 +308,23 @@ def build_layout(specs: list[RequestSpec], L: int, heads: int, target_items: int
             if len(sel):
                 ranges.append((r, int(sel[0]), len(sel)))
         q_ranges.append(ranges)
-        it9, groups = attention_work(ranges, qpos[i], n_req, heads)
-        it9[:, 3] = kvoff[it9[:, 8]]
-        attn_items.append(np.ascontiguousarray(it9[:, :8]))
-        comb_items.append(np.zeros((0, 8), dtype=np.int32))
+        lists = [request_chunks(spec, i, int(kvoff[r]), {m: page_base[(r, m)] for m in range(len(spec.images))
+                                                         if (r, m) in page_base})
+                 for r, spec in enumerate(specs)]
+        chunk0 = np.concatenate([[0], np.cumsum([len(x) for x in lists])[:-1]]).astype(np.int64)
+        items, groups = attention_work(ranges, qpos[i], lambda r, p: tiles_needed(lists[r], p), chunk0, heads)
+        attn_items.append(np.ascontiguousarray(items))
+        attn_chunks.append(np.ascontiguousarray(np.concatenate(lists).astype(np.int32)))
         slots = max(slots, groups)
 
-    # relocation descriptors, grouped by layer
-    descs, blocks, layer_blocks, pages, ntok_total = [], [], [0], [], 0
-    page_base = {}
-    for r, spec in enumerate(specs):
-        for m, (start, T) in enumerate(spec.images):
-            if spec.kv_hit[m]:
-                page_base[(r, m)] = sum(len(p) for p in pages)
-                pages.append(np.asarray(spec.page_rows[m], dtype=np.int32).reshape(-1))
+    # relocation descriptors (vlc_kv_relocate), grouped by layer: only the cached rows that share a
+    # key chunk with recomputed ones (attention reads every other cached chunk from the store)
+    descs, blocks, layer_blocks, ntok_total = [], [], [0], 0
     for i in range(L):
         for r, spec in enumerate(specs):
-            for m, (start, T) in enumerate(spec.images):
-                if not spec.kv_hit[m]:
-                    continue
-                k = int(spec.keep[i, m])
-                ntok = T - k
-                if ntok <= 0:
-                    continue
+            for m, k, e in relocated_ranges(spec, i):
+                start = spec.images[m][0]
+                ntok = e - k
                 ppl = np.asarray(spec.page_rows[m]).shape[1]
                 d = [i, page_base[(r, m)] + i * ppl, k, ntok, int(kvoff[r]) + start + k, start + k, 0, 0]
                 for off in range(0, ntok, RELOC_TOK):
@@ -321,7 +347,7 @@ def build_layout(specs: list[RequestSpec], L: int, heads: int, target_items: int
     return Layout(L=L, heads=heads, c=c, kv_rows=int(n_req.sum()), kvoff=kvoff.astype(np.int32),
                   row_req=req.astype(np.int32), row_pos=pos.astype(np.int32), row_kv=row_kv.astype(np.int32),
                   row_src=src, qdst=qdst, qpos=qpos, rowof=rowof, q_ranges=q_ranges,
-                  attn_items=attn_items, comb_items=comb_items, attn_slots=slots,
+                  attn_chunks=attn_chunks, attn_items=attn_items, attn_slots=slots,
                   reloc_descs=np.array(descs, dtype=np.int32).reshape(-1, 8),
                   reloc_blocks=np.array(blocks, dtype=np.int32).reshape(-1, 2),
                   reloc_layer_blocks=np.array(layer_blocks, dtype=np.int32), reloc_tokens=ntok_total,
@@ -337,7 +363,7 @@ def structure_of(specs: list[RequestSpec], L: int, heads: int):
         key.append((s.n, np.asarray(s.text_pos, np.int64).tobytes(), tuple(s.images),
                      np.asarray(s.keep, np.int32).tobytes(), tuple(bool(h) for h in s.kv_hit),
                      tuple(int(k) for k, _ in s.enc_src),
-                     tuple(0 if p is None else np.asarray(p).shape[1] for p in s.page_rows)))
+                     tuple(0 if p is None else np.asarray(p).shape[1] for p in s.page_rows), int(s.page_tokens)))
     return tuple(key)
 
 

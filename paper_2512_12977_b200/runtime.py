@@ -13,7 +13,7 @@ import weakref
 import numpy as np
 
 from . import _native as N
-from .layout import Layout, attention_work, attn_kernel_variant
+from .layout import Layout, attention_work, contiguous_chunks, tiles_needed
 from .model import RMS_EPS, DeviceWeights
 
 N_SMS = 148
@@ -207,8 +207,6 @@ class Runner:
         # Measured on C3: 5.58 -> 5.24 ms TTFT (tools: VLC_HI_PRIO / VLC_RELOC_WIDE A/B, run42).
         self.hi_prio = bool(int(__import__("os").environ.get("VLC_HI_PRIO", "1")))
         self.lib.vlc_set_tuning(14, int(__import__("os").environ.get("VLC_RELOC_WIDE", "100000")))
-        # attention kernel variant matching the layout's work decomposition (layout.ATTN_ONE_TILE)
-        self.lib.vlc_set_tuning(15, attn_kernel_variant())
         # experiments: VLC_TUNING="key=value,..." applied last (vlc_set_tuning)
         for kv_ in __import__("os").environ.get("VLC_TUNING", "").split(","):
             if "=" in kv_:
@@ -295,24 +293,31 @@ class Runner:
             x.data_ptr(), x.shape[1], gamma.data_ptr(), out.data_ptr(), ldo, int(out_f32), rows, d,
             row_map, RMS_EPS, pk[0], pk[1], _stream()), "vlc_rmsnorm"), rows * d * (4 + (4 if out_f32 else 2)))
 
-    def attention(self, q, kc, vc, layer, items_ptr, n_items, comb_ptr, n_comb, qpos_ptr, rowof_ptr, out,
-                  slots, nbytes=0, flops=0, pk=(0, 0), kv=None, heads=None):
-        """kv / heads: this rank's K/V width and head count (default: the decoder's, head-split)."""
+    def attention(self, q, kc, vc, layer, chunks_ptr, items_ptr, n_items, qpos_ptr, rowof_ptr, out, slots,
+                  nbytes=0, flops=0, pk=(0, 0), kv=None, heads=None, pool=None, page_table=0):
+        """vlc_attn_paged over one layer.  pool: the store's _PagePool whose pages the chunk list
+        references (None: every chunk is request rows).  kv / heads: this rank's K/V width and head
+        count (default: the decoder's, head-split)."""
         torch = _torch()
-        cfg = self.cfg
+        cfg, dw = self.cfg, self.dw
         hd = cfg.head_dim
-        kv = kv or self.dw.kv
-        heads = heads or self.dw.heads
+        kv = kv or dw.kv
+        heads = heads or dw.heads
         ws_o = self.shared.get("attn_ws_o", (max(1, slots) * 8 * 256 * hd,), torch.float32, zero=False)
         ws_ml = self.shared.get("attn_ws_ml", (max(1, slots) * 8 * 256 * 2,), torch.float32, zero=False)
-        a = N.AttnArgs(q=q.data_ptr(), q_rows_cap=q.shape[0], kc=kc.data_ptr(), vc=vc.data_ptr(),
-                       layers_cap=kc.shape[0], kv_rows_cap=kc.shape[1], layer=layer, kv=kv,
-                       heads=heads, head_dim=hd, items=items_ptr, n_items=n_items, qpos=qpos_ptr,
-                       rowof=rowof_ptr, out=out.data_ptr(), ldo=kv, ws_o=ws_o.data_ptr(),
-                       ws_ml=ws_ml.data_ptr(), ws_slots=slots, comb=comb_ptr, n_comb=n_comb,
-                       scale_log2=math.log2(math.e) / math.sqrt(hd), counters=self.attn_counters.data_ptr(),
-                       pk_rows=pk[0], pk_kb=pk[1])
-        self._run("attention", lambda: N.check(self.lib.vlc_attn_pp(a, _stream()), "vlc_attn_pp"),
+        a = N.AttnPagedArgs(
+            q=q.data_ptr(), q_rows_cap=q.shape[0], kc=kc.data_ptr(), vc=vc.data_ptr(), layers_cap=kc.shape[0],
+            kv_rows_cap=kc.shape[1], layer=layer,
+            pool_k=pool.k.data_ptr() if pool is not None else None,
+            pool_v=pool.v.data_ptr() if pool is not None else None,
+            pool_rows=pool.k.shape[0] if pool is not None else 0, page_table=page_table or None,
+            page_rows=pool.P if pool is not None else 0,
+            cos_tab=dw.cos.data_ptr(), sin_tab=dw.sin.data_ptr(), tab_ld=hd // 2,
+            kv=kv, heads=heads, head_dim=hd, chunks=chunks_ptr, items=items_ptr, n_items=n_items,
+            qpos=qpos_ptr, rowof=rowof_ptr, out=out.data_ptr(), ldo=kv, pk_rows=pk[0], pk_kb=pk[1],
+            ws_o=ws_o.data_ptr(), ws_ml=ws_ml.data_ptr(), ws_slots=slots, counters=self.attn_counters.data_ptr(),
+            scale_log2=math.log2(math.e) / math.sqrt(hd))
+        self._run("attention", lambda: N.check(self.lib.vlc_attn_paged(a, _stream()), "vlc_attn_paged"),
                   nbytes, flops)
 
     # ---------------------------------------------------------------- vision encoder (miss path)
@@ -356,19 +361,21 @@ class Runner:
         self.gemm(E["wqkv_plain"], dw.kd, xn, M,
                   _epi(kind=N.EPI_QKV_PLAIN, n_valid=3 * kv, out=qe.data_ptr(), ldo=kv, out2=ke.data_ptr(), ld2=kv,
                        out3=ve.data_ptr(), ld3=kv, seg=kv, hd=cfg.head_dim))
+        # bidirectional (model.py:325): every query sees all T keys of its image (position T - 1)
         ranges = [(m, m * T, T) for m in range(k)]
         qpos = np.full(M, T - 1, dtype=np.int32)
-        it9, slots = attention_work(ranges, qpos, np.full(k, T), cfg.num_heads)
-        it9[:, 3] = it9[:, 8] * T
-        items = np.ascontiguousarray(it9[:, :8])
+        chunks = [contiguous_chunks(m * T, T) for m in range(k)]
+        chunk0 = np.arange(k) * len(chunks[0])
+        items, slots = attention_work(ranges, qpos, lambda r, p: tiles_needed(chunks[r], p), chunk0,
+                                      cfg.num_heads)
         pack = IntPack()
         pack.add("items", items)
-        pack.add("comb", np.zeros((1, 8)))
+        pack.add("chunks", np.concatenate(chunks))
         pack.add("qpos", qpos)
         pack.add("rowof", np.arange(M))
         pack.upload(ws, "enc_ints")
-        self.attention(qe, ke, ve, 0, pack.ptr("items"), len(items), pack.ptr("comb"), 0,
-                       pack.ptr("qpos"), pack.ptr("rowof"), att, slots, pk=pkkv, kv=kv, heads=cfg.num_heads)
+        self.attention(qe, ke, ve, 0, pack.ptr("chunks"), pack.ptr("items"), len(items), pack.ptr("qpos"),
+                       pack.ptr("rowof"), att, slots, pk=pkkv, kv=kv, heads=cfg.num_heads)
         self.gemm(E["wo"], dw.kkv_enc, att, M, _epi(kind=N.EPI_RESID, n_valid=d, out=xe.data_ptr(), ldo=d))
         self.rmsnorm(xe, E["mlp_norm"], xn, M, pk=pkd)
         self.gemm(E["wgu"], dw.kd, xn, M,
@@ -442,6 +449,7 @@ class Runner:
                 pack.dev.data_ptr(), dw.cos.data_ptr(), self.splitk.data_ptr(),
                 self.shared.bufs["attn_ws_o"].data_ptr(), self.shared.bufs["attn_ws_ml"].data_ptr()) + tuple(
                     t.data_ptr() for t in buf.values())
+        buf["kv_pool"] = kv_pool                      # cached chunks are read from its pages
         if inject is not None or capture:
             # measurement path (forward_injected): per-layer KV substitution after the QKV GEMM and
             # captured attention-block outputs; eager launches
@@ -507,7 +515,7 @@ class Runner:
                 pk.add(f"qpos{i}", lay.qpos[i])
                 pk.add(f"rowof{i}", lay.rowof[i])
                 pk.add(f"items{i}", lay.attn_items[i])
-                pk.add(f"comb{i}", lay.comb_items[i] if len(lay.comb_items[i]) else np.zeros(8))
+                pk.add(f"chunks{i}", lay.attn_chunks[i])
             pk.add("descs", lay.reloc_descs if len(lay.reloc_descs) else np.zeros(8))
             pk.add("blocks", lay.reloc_blocks if len(lay.reloc_blocks) else np.zeros(2))
             pk.add("final", lay.final_rows)
@@ -548,6 +556,7 @@ class Runner:
         c = lay.c
         c0, cL = int(c[0]), int(c[L - 1])
         enc_a, enc_b, kpool, vpool, P = ptrs[:5]
+        kv_pool_obj = buf.get("kv_pool")
         s = _stream()
         # layer-0 rows: text embeddings + cached / freshly encoded image rows
         self._run("embed", lambda: N.check(self.lib.vlc_embed_assemble(
@@ -628,10 +637,10 @@ class Runner:
             vis = int(lay.qpos[i, :ci].astype(np.int64).sum()) + ci
             if side_ev is not None:
                 _torch().cuda.current_stream().wait_event(side_ev[i])
-            self.attention(q, kc, vc, i, pack.ptr(f"items{i}"), len(lay.attn_items[i]), pack.ptr(f"comb{i}"),
-                           len(lay.comb_items[i]), pack.ptr(f"qpos{i}"), pack.ptr(f"rowof{i}"), att, lay.attn_slots,
+            self.attention(q, kc, vc, i, pack.ptr(f"chunks{i}"), pack.ptr(f"items{i}"), len(lay.attn_items[i]),
+                           pack.ptr(f"qpos{i}"), pack.ptr(f"rowof{i}"), att, lay.attn_slots,
                            nbytes=lay.kv_rows * kv * 4 + ci * kv * 4, flops=4 * cfg.head_dim * dw.heads * vis,
-                           pk=(Ri, dw.kkv // 128))
+                           pk=(Ri, dw.kkv // 128), pool=kv_pool_obj, page_table=pack.ptr("pages"))
             if i in buf.get("capture", {}):
                 # captured attention block output (engine.py:273-275): O projection alone, then
                 # x += it fused with the MLP norm
@@ -726,13 +735,15 @@ class DeviceDecoder:
         L, d, kv, V = cfg.num_layers, cfg.model_dim, dw.kv, cfg.vocab_size
         pos = self.n
         R = N.row_tile(1)
-        it9, groups = attention_work([(0, 0, 1)], np.array([pos], np.int32), np.array([pos + 1]), dw.heads)
-        items = np.ascontiguousarray(it9[:, :8])
+        chunks = contiguous_chunks(0, pos + 1)
+        items, groups = attention_work([(0, 0, 1)], np.array([pos], np.int32), lambda q, p: tiles_needed(chunks, p),
+                                       [0], dw.heads)
         pack = IntPack()
         pack.add("src", np.array([[0, token]]))
         pack.add("pos", np.array([pos]))
         pack.add("zero", np.array([0]))
         pack.add("items", items)
+        pack.add("chunks", chunks)
         pack.upload(r.shared, "dec_ints")
         s = _stream()
         r._run("embed", lambda: N.check(r.lib.vlc_embed_assemble(
@@ -746,7 +757,7 @@ class DeviceDecoder:
                 map1=pack.ptr("zero"), map2=pack.ptr("pos"), pos=pack.ptr("pos"),
                 cos_tab=dw.cos.data_ptr(), sin_tab=dw.sin.data_ptr(), tab_ld=cfg.head_dim // 2,
                 hd=cfg.head_dim, seg=kv), name="gemm_qkv", k_valid=d)
-            r.attention(self.q, self.kc, self.vc, i, pack.ptr("items"), len(items), pack.ptr("zero"), 0,
+            r.attention(self.q, self.kc, self.vc, i, pack.ptr("chunks"), pack.ptr("items"), len(items),
                         pack.ptr("pos"), pack.ptr("zero"), self.att, groups, pk=(R, dw.kkv // 128))
             r.gemm(W["wo"], dw.kkv, self.att, 1, _epi(kind=N.EPI_RESID, n_valid=d, out=self.x.data_ptr(), ldo=d),
                    name="gemm_o", k_valid=kv)

@@ -266,61 +266,109 @@ def test_layout_rows_match_masks(pre, T, nimg, suf, ratios, hits):
         qp = lay.qpos[i, :ci]
         assert (np.diff(qp) >= 0).all()
     assert np.array_equal(lay.positions[0], np.flatnonzero(masks[-1]))
-    # every reused (layer, token) is relocated exactly once
-    want = int((~masks).sum())
+    # reused (layer, token) rows: the store chunks' rows are read in place by the attention, the
+    # rest of each keep boundary's chunk is relocated (exactly once)
+    from paper_2512_12977_b200.layout import relocated_ranges
+    want = sum(e - k for i in range(L) for _, k, e in relocated_ranges(spec, i))
     assert lay.reloc_tokens == want
+    store = sum(int(c[1]) for ch in lay.attn_chunks for c in ch if c[3] >= 0 and c[1] > 0)
+    assert store + want == int((~masks).sum())
 
 
-@pytest.mark.parametrize("work", ["one", "pp"])
 @pytest.mark.parametrize("nq,nkeys,heads,reqs", [(236, 4128, 28, 1), (62, 1056, 12, 1), (44, 288, 8, 1),
-                                                 (600, 4128, 1, 1), (300, 300, 4, 1), (40, 300, 8, 3)])
-def test_attention_work_items_cover_every_visible_key(work, nq, nkeys, heads, reqs):
-    """Work decompositions of vlc_attn_pp: every (query, head) sees exactly its causal key range
-    [0, pos + 1) once across the splits of its unit; query tiles are <= 128 (single-tile kernel) /
-    <= 256 (ping-pong); split groups fit the co-residency budget (<= 148 CTAs) and <= 8 parts; the
-    parts of a group have consecutive indices with the group size in every item."""
+                                            (600, 4128, 1, 1), (300, 300, 4, 1), (40, 300, 8, 3)])
+def test_attention_work_items_cover_every_visible_key(nq, nkeys, heads, reqs):
+    """Work items of vlc_attn_paged: every (query tile, head) covers the 128-key tiles holding its
+    causal keys [0, last query position] exactly once across its splits; query tiles are <= 128
+    rows; split groups fit the co-residency budget (<= 148 CTAs) and <= 8 parts; the parts of a
+    group have consecutive indices with the group size in every item."""
     import numpy as np
-    from paper_2512_12977_b200.layout import attention_work_one, attention_work_pp
+    from paper_2512_12977_b200.layout import attention_work, contiguous_chunks, tiles_needed
     rng = np.random.default_rng(nq + nkeys)
-    ranges, qpos, n_req, q0 = [], [], [], 0
+    ranges, qpos, q0, lists = [], [], 0, []
     for r in range(reqs):
-        n = nkeys
-        pos = np.sort(rng.permutation(n)[:nq]).astype(np.int32)
-        pos[-1] = n - 1
+        pos = np.sort(rng.permutation(nkeys)[:nq]).astype(np.int32)
+        pos[-1] = nkeys - 1
         ranges.append((r, q0, nq))
         qpos.append(pos)
-        n_req.append(n)
+        lists.append(contiguous_chunks(r * nkeys, nkeys))
         q0 += nq
     qpos = np.concatenate(qpos)
-    fn = attention_work_one if work == "one" else attention_work_pp
-    it, groups = fn(ranges, qpos, np.array(n_req), heads)
-    tile = 128 if work == "one" else 256
-    assert (it[:, 1] <= tile).all() and (it[:, 1] > 0).all()
+    chunk0 = np.cumsum([0] + [len(x) for x in lists[:-1]])
+    it, groups = attention_work(ranges, qpos, lambda r, p: tiles_needed(lists[r], p), chunk0, heads)
+    assert (it[:, 1] <= 128).all() and (it[:, 1] > 0).all()
     if groups:
         assert len(it) <= 148
     parts = {}
     for row in it:
-        t0, nqt, h, _, kb, ke, grp, pk, req = (int(v) for v in row)
+        t0, nqt, h, c0, tb, te, grp, pk = (int(v) for v in row)
         p, ns = pk >> 8, pk & 0xFF
         assert 1 <= ns <= 8 and 0 <= p < ns
         assert (grp < 0) == (ns == 1)
-        parts.setdefault((req, t0, h), []).append((kb, ke, p, ns, nqt))
-    for (req, t0, h), lst in parts.items():
+        parts.setdefault((c0, t0, h), []).append((tb, te, p, ns, nqt))
+    for (c0, t0, h), lst in parts.items():
+        req = int(np.searchsorted(chunk0, c0, side="right") - 1)
         lst.sort()
         ns = lst[0][3]
         assert len(lst) == ns and [x[2] for x in lst] == list(range(ns))
-        # contiguous, gap-free key cover from 0 to the tile's last visible key
         assert lst[0][0] == 0
         for a, b in zip(lst, lst[1:]):
             assert a[1] == b[0]
         nqt = lst[0][4]
-        assert lst[-1][1] == min(int(qpos[t0 + nqt - 1]) + 1, n_req[req])
-    # every query row of every request is covered by exactly one tile per head
+        last = int(qpos[t0 + nqt - 1])
+        ch = lists[req]
+        te = lst[-1][1]
+        # the tiles reach the last visible key and stop at the first tile wholly past it
+        assert ch[2 * te - 2:2 * te, 0].min() <= last
+        assert 2 * te >= len(ch) or ch[2 * te, 0] > last
     for r, q0_, cnt in ranges:
         for h in range(heads):
-            rows = sorted(t0 + i for (req, t0, hh), lst in parts.items() if req == r and hh == h
+            rows = sorted(t0 + i for (c0, t0, hh), lst in parts.items() if c0 == chunk0[r] and hh == h
                           for i in range(lst[0][4]))
             assert rows == list(range(q0_, q0_ + cnt))
+
+
+@pytest.mark.parametrize("pre,T,nimg,suf,ratios,P", [
+    (16, 1024, 4, 16, (0.05, 0.02, 0.0), 64), (16, 256, 2, 16, (0.3, 0.1, 0.0), 64),
+    (6, 16, 1, 4, (0.3, 0.2, 0.1, 0.0), 16), (16, 256, 1, 16, (1.0, 0.25, 0.1), 128),
+    (3, 300, 2, 5, (0.5, 0.2, 0.0), 64), (16, 256, 1, 16, (0.1, 0.0), 48)])
+def test_key_chunks_cover_every_key_once(pre, T, nimg, suf, ratios, P):
+    """vlc_attn_paged's key chunks of each layer: positions 0 .. n-1 exactly once, in order; a store
+    chunk only for cached rows (t >= keep) that sit inside one page; every cached row of a hit
+    image is either read from the store or relocated into the request rows -- never both, never
+    neither -- and the relocated rows are exactly the cached rows of request-row chunks."""
+    import numpy as np
+    from paper_2512_12977_b200.layout import relocated_ranges, request_chunks
+    seq, plan, spec = _spec(pre, T, nimg, suf, ratios, None)
+    spec.page_tokens = P
+    ppl = -(-T // P)
+    spec.page_rows = [np.arange(len(ratios) * ppl, dtype=np.int32).reshape(len(ratios), ppl) for _ in range(nimg)]
+    base = {m: m * len(ratios) * ppl for m in range(nimg)}
+    for i in range(len(ratios)):
+        ch = request_chunks(spec, i, 1000, base)
+        assert len(ch) % 2 == 0
+        real = ch[ch[:, 1] > 0]
+        covered = np.concatenate([np.arange(c[0], c[0] + c[1]) for c in real])
+        assert np.array_equal(covered, np.arange(spec.n))
+        reloc = {m: (k, e) for m, k, e in relocated_ranges(spec, i)}
+        for m, (start, Tm) in enumerate(spec.images):
+            k = int(spec.keep[i, m])
+            store_rows, req_rows = set(), set()
+            for c in real:
+                if not (start <= c[0] < start + Tm):
+                    continue
+                t = set(range(c[0] - start, c[0] - start + c[1]))
+                if c[3] >= 0:
+                    assert min(t) >= k and c[3] + c[1] <= P
+                    assert c[2] == base[m] + i * ppl + (c[0] - start) // P
+                    store_rows |= t
+                else:
+                    assert c[2] == 1000 + c[0]
+                    req_rows |= t
+            cached = set(range(k, Tm))
+            relocated = set(range(*reloc[m])) if m in reloc else set()
+            assert store_rows.isdisjoint(relocated) and store_rows | relocated == cached
+            assert relocated == cached & req_rows
 
 
 def test_int_pack_template_and_patches():

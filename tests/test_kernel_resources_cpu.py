@@ -15,7 +15,7 @@ BUDGET = {
     "gemm_bf16_tcILi6ELi1E": 64,       # QKV GEMM + RoPE epilogue
     "gemm_bf16_tcILi4ELi1E": 0,        # gate/up GEMM + SwiGLU epilogue
     "gemm_bf16_tcILi1ELi1E": 0,        # O / down GEMMs (residual red.add)
-    "attn_pp_kernelILi128ELi128ELi180225E": 64,  # default single-tile attention (O split per half)
+    "attn_paged_kernelILi128E": 64,    # paged attention (store chunks rotated in smem)
     "rmsnorm_kernelILb0ELi8E": 0,
 }
 

@@ -156,55 +156,6 @@ def _attn_ref(q, k, v, qpos, heads, hd, nkeys):
     return (torch.softmax(s, -1) @ vh).transpose(0, 1).reshape(nq, -1)
 
 
-@pytest.mark.parametrize("hd,heads,nkeys,nq,split", [(128, 2, 1000, 150, 3), (128, 4, 300, 60, 1),
-                                                      (64, 2, 513, 200, 2), (32, 8, 288, 44, 1),
-                                                      (16, 2, 26, 10, 1), (128, 1, 4128, 236, 6)])
-def test_attention_matches_torch(nat, hd, heads, nkeys, nq, split):
-    kv = heads * hd
-    g = torch.Generator(device="cuda").manual_seed(nkeys)
-    layers, layer, kv_rows = 3, 1, nkeys + 64
-    kc = torch.randn(layers, kv_rows, kv, device="cuda", generator=g).bfloat16()
-    vc = torch.randn(layers, kv_rows, kv, device="cuda", generator=g).bfloat16()
-    qpos = torch.sort(torch.randperm(nkeys, device="cuda", generator=g)[:nq]).values.int()
-    qpos[-1] = nkeys - 1
-    q = torch.zeros(max(256, nq + 128), kv, device="cuda", dtype=torch.bfloat16)
-    q[:nq] = torch.randn(nq, kv, device="cuda", generator=g).bfloat16()
-    rowof = torch.randperm(nq, device="cuda", generator=g).int()
-    out = torch.zeros(nq, kv, device="cuda", dtype=torch.bfloat16)
-    items, comb, slot = [], [], 0
-    for h in range(heads):
-        for q0 in range(0, nq, 128):
-            n_q = min(128, nq - q0)
-            kend = int(qpos[q0 + n_q - 1]) + 1
-            ntile = (kend + 127) // 128
-            ns = min(split, ntile)
-            if ns == 1:
-                items.append([q0, n_q, h, 0, 0, kend, -1, 0])
-                continue
-            bounds = [round(ntile * i / ns) * 128 for i in range(ns + 1)]
-            bounds[-1] = kend
-            for s in range(ns):
-                items.append([q0, n_q, h, 0, bounds[s], bounds[s + 1], slot + s, 0])
-            comb.append([q0, n_q, h, slot, ns, 0, 0, 0])
-            slot += ns
-    it = torch.tensor(items, dtype=torch.int32, device="cuda")
-    cb = torch.tensor(comb or [[0] * 8], dtype=torch.int32, device="cuda")
-    ws_o = torch.zeros(max(slot, 1) * 128 * hd, device="cuda")
-    ws_ml = torch.zeros(max(slot, 1) * 256, device="cuda")
-    a = nat.AttnArgs(q=q.data_ptr(), q_rows_cap=q.shape[0], kc=kc.data_ptr(), vc=vc.data_ptr(),
-                     layers_cap=layers, kv_rows_cap=kv_rows, layer=layer, kv=kv, heads=heads, head_dim=hd,
-                     items=it.data_ptr(), n_items=len(items), qpos=qpos.data_ptr(), rowof=rowof.data_ptr(),
-                     out=out.data_ptr(), ldo=kv, ws_o=ws_o.data_ptr(), ws_ml=ws_ml.data_ptr(), ws_slots=slot,
-                     comb=cb.data_ptr(), n_comb=len(comb), scale_log2=math.log2(math.e) / math.sqrt(hd))
-    nat.check(nat.load().vlc_attn_mixed(a, _stream()), "attn")
-    nat.check(nat.load().vlc_attn_combine(a, _stream()), "comb")
-    torch.cuda.synchronize()
-    ref = _attn_ref(q[:nq], kc[layer], vc[layer], qpos, heads, hd, nkeys)
-    got = out[rowof.long()].float()
-    err = (got - ref).abs().max().item()
-    assert err < 2e-2, err
-
-
 def test_kv_relocate_matches_torch(nat):
     g = torch.Generator(device="cuda").manual_seed(5)
     L, T, kv, hd, P = 3, 100, 256, 128, 16
@@ -242,20 +193,44 @@ def test_kv_relocate_matches_torch(nat):
         assert kc[layer, :start + keeps[layer]].abs().sum().item() == 0
 
 
-@pytest.mark.parametrize("hd,heads,nkeys,nq,causal", [(128, 28, 4128, 236, True), (128, 2, 1000, 150, True),
-                                                      (64, 2, 513, 200, True), (32, 8, 288, 44, True),
-                                                      (16, 2, 26, 10, True), (128, 4, 300, 300, True),
-                                                      (128, 3, 256, 256, False), (128, 1, 4128, 600, True)])
-def test_attention_pp_matches_torch(nat, hd, heads, nkeys, nq, causal, var=None):
-    from paper_2512_12977_b200.layout import attention_work_one, attention_work_pp, attn_kernel_variant
-    var = attn_kernel_variant() if var is None else var
-    nat.load().vlc_set_tuning(15, var)
-    work = attention_work_one if 30 <= var < 40 else attention_work_pp
+def _paged_case(nat, hd, heads, nkeys, nq, causal, store_every, seed, page_rows=64):
+    """Request K/V rows plus a store pool; every `store_every`-th 64-key chunk (0: none) is read from
+    a randomly placed store page holding PRE-RoPE K (the kernel rotates it to the chunk's
+    positions).  Returns the kernel arguments and the fp32 torch reference of the attention."""
+    from paper_2512_12977_b200.layout import attention_work, tiles_needed
     kv = heads * hd
-    g = torch.Generator(device="cuda").manual_seed(nkeys + nq)
+    g = torch.Generator(device="cuda").manual_seed(seed)
     layers, layer, kv_rows = 2, 1, nkeys + 64
     kc = torch.randn(layers, kv_rows, kv, device="cuda", generator=g).bfloat16()
     vc = torch.randn(layers, kv_rows, kv, device="cuda", generator=g).bfloat16()
+    n_chunks = -(-nkeys // 64)
+    npages = n_chunks * 64 // page_rows + 3
+    kpool = torch.randn(npages * page_rows, kv, device="cuda", generator=g).bfloat16()
+    vpool = torch.randn(npages * page_rows, kv, device="cuda", generator=g).bfloat16()
+    ptab = torch.randperm(npages, device="cuda", generator=g).int()
+    cos, sin = _tables(hd, nkeys + 64)
+    ref_k, ref_v = kc[layer, :nkeys].float().clone(), vc[layer, :nkeys].float().clone()
+    chunks = []
+    for ci, c in enumerate(range(0, nkeys, 64)):
+        ln = min(64, nkeys - c)
+        if store_every and ci % store_every == store_every - 1:
+            pti, off = ci * 64 // page_rows, (ci * 64) % page_rows
+            rows = ptab[pti].long() * page_rows + off + torch.arange(ln, device="cuda")
+            pos = torch.arange(c, c + ln, device="cuda")
+            # the kernel rotates in fp32 with the fp32 tables and rounds the result to bf16
+            kf = kpool[rows].float().reshape(ln, heads, hd)
+            half = hd // 2
+            cc, ss = cos[pos][:, None, :], sin[pos][:, None, :]
+            a_, b_ = kf[..., :half], kf[..., half:]
+            rot = torch.cat([a_ * cc - b_ * ss, b_ * cc + a_ * ss], -1).reshape(ln, kv)
+            ref_k[c:c + ln] = rot.bfloat16().float()
+            ref_v[c:c + ln] = vpool[rows].float()
+            chunks.append([c, ln, pti, off])
+        else:
+            chunks.append([c, ln, c, -1])
+    if len(chunks) % 2:
+        chunks.append([chunks[-1][0] + 64, 0, chunks[-1][2], chunks[-1][3]])
+    chunks = np.array(chunks, np.int32)
     if causal:
         qpos = torch.sort(torch.randperm(nkeys, device="cuda", generator=g)[:nq]).values.int()
         qpos[-1] = nkeys - 1
@@ -265,44 +240,62 @@ def test_attention_pp_matches_torch(nat, hd, heads, nkeys, nq, causal, var=None)
     q[:nq] = torch.randn(nq, kv, device="cuda", generator=g).bfloat16()
     rowof = torch.randperm(nq, device="cuda", generator=g).int()
     out = torch.zeros(nq, kv, device="cuda", dtype=torch.bfloat16)
-    it9, groups = work([(0, 0, nq)], qpos.cpu().numpy(), np.array([nkeys]), heads)
-    it = torch.from_numpy(np.ascontiguousarray(it9[:, :8])).cuda()
-    ws_o = torch.zeros(max(groups, 1) * 8 * 256 * hd, device="cuda")
-    ws_ml = torch.zeros(max(groups, 1) * 8 * 256 * 2, device="cuda")
-    cnt = torch.zeros(4096, dtype=torch.int32, device="cuda")
-    a = nat.AttnArgs(q=q.data_ptr(), q_rows_cap=q.shape[0], kc=kc.data_ptr(), vc=vc.data_ptr(),
-                     layers_cap=layers, kv_rows_cap=kv_rows, layer=layer, kv=kv, heads=heads, head_dim=hd,
-                     items=it.data_ptr(), n_items=it.shape[0], qpos=qpos.data_ptr(), rowof=rowof.data_ptr(),
-                     out=out.data_ptr(), ldo=kv, ws_o=ws_o.data_ptr(), ws_ml=ws_ml.data_ptr(), ws_slots=groups,
-                     comb=0, n_comb=0, scale_log2=math.log2(math.e) / math.sqrt(hd), counters=cnt.data_ptr())
-    for _ in range(2):   # twice: counters must be left zeroed for the next launch
+    items, groups = attention_work([(0, 0, nq)], qpos.cpu().numpy(), lambda r, p: tiles_needed(chunks, p), [0],
+                                   heads)
+    keep = dict(it=torch.from_numpy(items).cuda(), ch=torch.from_numpy(chunks).cuda(),
+                ws_o=torch.zeros(max(groups, 1) * 8 * 256 * hd, device="cuda"),
+                ws_ml=torch.zeros(max(groups, 1) * 8 * 256 * 2, device="cuda"),
+                cnt=torch.zeros(4096, dtype=torch.int32, device="cuda"),
+                kc=kc, vc=vc, kpool=kpool, vpool=vpool, ptab=ptab, cos=cos, sin=sin, q=q, qpos=qpos, rowof=rowof)
+    use_pool = bool(store_every)
+    a = nat.AttnPagedArgs(q=q.data_ptr(), q_rows_cap=q.shape[0], kc=kc.data_ptr(), vc=vc.data_ptr(),
+                          layers_cap=layers, kv_rows_cap=kv_rows, layer=layer,
+                          pool_k=kpool.data_ptr() if use_pool else None, pool_v=vpool.data_ptr() if use_pool else None,
+                          pool_rows=kpool.shape[0], page_table=ptab.data_ptr(), page_rows=page_rows,
+                          cos_tab=cos.data_ptr(), sin_tab=sin.data_ptr(), tab_ld=hd // 2, kv=kv, heads=heads,
+                          head_dim=hd, chunks=keep["ch"].data_ptr(), items=keep["it"].data_ptr(),
+                          n_items=len(items), qpos=qpos.data_ptr(), rowof=rowof.data_ptr(), out=out.data_ptr(),
+                          ldo=kv, pk_rows=0, pk_kb=0, ws_o=keep["ws_o"].data_ptr(), ws_ml=keep["ws_ml"].data_ptr(),
+                          ws_slots=groups, counters=keep["cnt"].data_ptr(),
+                          scale_log2=math.log2(math.e) / math.sqrt(hd))
+    ref = _attn_ref(q[:nq], ref_k, ref_v, qpos, heads, hd, nkeys)
+    return a, out, ref, keep
+
+
+@pytest.mark.parametrize("hd,heads,nkeys,nq,causal,store_every",
+                         [(128, 28, 4128, 236, True, 1), (128, 28, 4128, 236, True, 3), (128, 2, 1000, 150, True, 2),
+                          (64, 2, 513, 200, True, 2), (32, 8, 288, 44, True, 1), (16, 2, 26, 10, True, 1),
+                          (128, 4, 300, 300, True, 0), (128, 3, 256, 256, False, 2), (128, 1, 4128, 600, True, 4),
+                          (32, 8, 288, 288, False, 0), (16, 2, 40, 40, True, 0)])
+def test_attention_paged_matches_torch(nat, hd, heads, nkeys, nq, causal, store_every):
+    """vlc_attn_paged against fp32 torch: request chunks and store chunks (pre-RoPE K rotated in
+    shared memory) mixed, causal and bidirectional, split key ranges merged in-kernel."""
+    a, out, ref, keep = _paged_case(nat, hd, heads, nkeys, nq, causal, store_every, nkeys + nq + store_every)
+    rowof = keep["rowof"]
+    for _ in range(2):   # twice: the split-merge counters must be left zeroed for the next launch
         out.zero_()
-        nat.check(nat.load().vlc_attn_pp(a, _stream()), "attn_pp")
+        nat.check(nat.load().vlc_attn_paged(a, _stream()), "attn_paged")
         torch.cuda.synchronize()
-        ref = _attn_ref(q[:nq], kc[layer], vc[layer], qpos, heads, hd, nkeys)
         got = out[rowof.long()].float()
         err = (got - ref).abs().max().item()
         assert err < 2e-2, err
-    assert int(cnt.abs().sum()) == 0
+    assert int(keep["cnt"].abs().sum()) == 0
     # packed output (the O-projection's input layout)
+    nq, kv = out.shape
     R = nat.row_tile(nq)
     outp = torch.zeros(nat.packed_numel(nq, kv, R), device="cuda", dtype=torch.bfloat16)
     a.out, a.pk_rows, a.pk_kb = outp.data_ptr(), R, -(-kv // 128)
-    nat.check(nat.load().vlc_attn_pp(a, _stream()), "attn_pp packed")
+    nat.check(nat.load().vlc_attn_paged(a, _stream()), "attn_paged packed")
     torch.cuda.synchronize()
     assert torch.equal(nat.unpack(outp, nq, kv, R), out)
 
 
-@pytest.mark.parametrize("var", [0, 30, 31, 36, 37, 39, 100, 1, 16, 17, 20, 22])
-@pytest.mark.parametrize("heads,nkeys,nq", [(28, 4128, 236), (2, 1000, 150), (4, 300, 300), (1, 4128, 600)])
-def test_attention_pp_softmax_variants(nat, var, heads, nkeys, nq):
-    """hd-128 / 128-key kernel variants (tuning key 15): ping-pong with 1 or 2 threads per row,
-    three-input max, P staged in smem, single query tile with S double-buffered (30 / 31)."""
-    from paper_2512_12977_b200.layout import attn_kernel_variant
-    try:
-        test_attention_pp_matches_torch(nat, 128, heads, nkeys, nq, True, var=var)
-    finally:
-        nat.load().vlc_set_tuning(15, attn_kernel_variant())
+def test_attention_paged_store_page_size_128(nat):
+    """Store pages of 128 rows: a chunk starts mid-page (row offset 64)."""
+    a, out, ref, keep = _paged_case(nat, 128, 4, 700, 90, True, 1, 11, page_rows=128)
+    nat.check(nat.load().vlc_attn_paged(a, _stream()), "attn_paged")
+    torch.cuda.synchronize()
+    assert (out[keep["rowof"].long()].float() - ref).abs().max().item() < 2e-2
 
 
 @pytest.mark.parametrize("n_pad,k_pad,m,splits", [(10752, 3584, 236, 0), (14336, 3584, 236, 0), (1024, 512, 100, 0),

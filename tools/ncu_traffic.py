@@ -28,7 +28,7 @@ for rep in reps:
             resid_seen += 1
         elif "gemm_pair_tc<0" in k or "gemm_bf16_tc<0" in k:
             name = "gemm_head"
-        elif "attn_pp" in k:
+        elif "attn_paged" in k:
             name = "attention"
         elif "kv_relocate" in k:
             name = "kv_relocate"
