@@ -246,47 +246,98 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
     __syncwarp();
   } else if (warp >= 2 + PA_SOFT_WARPS) {
     // ---------------- rotation warps: store K chunks -> rotated at their new positions
-    const int rt = threadIdx.x - 32 * (2 + PA_SOFT_WARPS);     // 0 .. 127
-    constexpr int G = HD / 16;                                  // 16-byte groups per half row
-    const int half = HD / 2;
-    for (int j = 0; j < nt; ++j) {
-      const int st = j % C::KST;
-      mbar_wait(&k_full[st], (j / C::KST) & 1);
-      uint8_t* tile = sK + st * C::KV_BYTES;
+    // Lane -> two adjacent frequencies (f0, f0 + 1) of the head: one 4-byte word of the lower half row
+    // (dims f0, f0 + 1) and one of the upper half (f0 + HD/2, ...); a warp covers RPW whole rows per
+    // step (conflict-free: one 128-byte wavefront per access) and walks a 16-row block of the chunk.
+    // The angle advances by RPW positions per step with the complex recurrence
+    //   (c, s) <- (c cos(RPW f) - s sin(RPW f), s cos(RPW f) + c sin(RPW f)),
+    // starting from the fp32 table row of the block's first position (reference fp32 tables,
+    // model.py:129-134) and stepping with table row RPW: no per-row table traffic (L2 latency),
+    // a <= 16-step recurrence error (~1e-6) far below both the table's own fp32 angle rounding
+    // and the bf16 rounding of the rotated key.
+    constexpr int LPR = HD / 4;                               // lanes per row
+    constexpr int RPW = 32 / LPR;                             // rows per warp step
+    constexpr int RB = PA_CHUNK / PA_ROT_WARPS;               // rows per warp block (16)
+    constexpr int STEPS = RB / RPW;
+    constexpr int HALF = HD / 2;
+    const int wr = (int)warp - (2 + PA_SOFT_WARPS);
+    const int f0 = 2 * ((int)lane % LPR);
+    const int r0 = wr * RB + (int)lane / LPR;                 // first row of this lane in a chunk
+    const float2 stc = __ldg(reinterpret_cast<const float2*>(a.cos_tab + (long)RPW * a.tab_ld + f0));
+    const float2 sts = __ldg(reinterpret_cast<const float2*>(a.sin_tab + (long)RPW * a.tab_ld + f0));
+    const float2 nsts = make_float2(-sts.x, -sts.y);
+    // byte offset of element e of tile row `row` in the [atom][128][SWZ] swizzled layout
+    auto eoff = [](int row, int e) -> uint32_t {
+      const uint32_t lin = (uint32_t)((e / C::ATOM_E) * C::KV_ATOM + row * C::SWZ + (e % C::ATOM_E) * 2);
+      return lin ^ (((lin >> 7) & ((1u << C::SWZ_B) - 1)) << 4);
+    };
+    // base (cos, sin) of both chunks of tile j: the chunk descriptors are loaded two tiles ahead and
+    // the table entries one tile ahead, so neither dependent global load sits on the rotation path
+    auto load_base = [&](const int4* ch, float2* bc, float2* bs) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int4 ch = chunks[2 * j + h];
-        if (ch.w < 0) continue;                                 // request rows: already rotated
-        const int rows = min(ch.y, PA_CHUNK);
-        for (int t = rt; t < rows * G; t += 32 * PA_ROT_WARPS) {
-          const int r = t / G, q = t % G;
-          const int row = h * PA_CHUNK + r;
-          const uint32_t o_lo = pa_swz_off<HD>(row, q), o_hi = pa_swz_off<HD>(row, q + G);
-          uint4 lo = *reinterpret_cast<const uint4*>(tile + o_lo);
-          uint4 hi = *reinterpret_cast<const uint4*>(tile + o_hi);
-          const float* cs = a.cos_tab + (long)(ch.x + r) * a.tab_ld + 8 * q;
-          const float* sn = a.sin_tab + (long)(ch.x + r) * a.tab_ld + 8 * q;
-          const float4 c0 = __ldg(reinterpret_cast<const float4*>(cs));
-          const float4 c1 = __ldg(reinterpret_cast<const float4*>(cs + 4));
-          const float4 s0 = __ldg(reinterpret_cast<const float4*>(sn));
-          const float4 s1 = __ldg(reinterpret_cast<const float4*>(sn + 4));
-          const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-          const float ss[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-          uint32_t* lw = reinterpret_cast<uint32_t*>(&lo);
-          uint32_t* hw = reinterpret_cast<uint32_t*>(&hi);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float a0 = bf16_lo(lw[e]), a1 = bf16_hi(lw[e]);
-            const float b0 = bf16_lo(hw[e]), b1 = bf16_hi(hw[e]);
-            const float c_0 = cc[2 * e], c_1 = cc[2 * e + 1], s_0 = ss[2 * e], s_1 = ss[2 * e + 1];
-            lw[e] = pack_bf16(a0 * c_0 - b0 * s_0, a1 * c_1 - b1 * s_1);
-            hw[e] = pack_bf16(b0 * c_0 + a0 * s_0, b1 * c_1 + a1 * s_1);
-          }
-          *reinterpret_cast<uint4*>(tile + o_lo) = lo;
-          *reinterpret_cast<uint4*>(tile + o_hi) = hi;
+        if (ch[h].w >= 0) {
+          const long o = (long)(ch[h].x + r0) * a.tab_ld + f0;
+          bc[h] = __ldg(reinterpret_cast<const float2*>(a.cos_tab + o));
+          bs[h] = __ldg(reinterpret_cast<const float2*>(a.sin_tab + o));
         }
       }
-      (void)half;
+    };
+    int4 d_cur[2], d_nxt[2], d_nn[2];
+    float2 bc[2] = {}, bs[2] = {};
+    if (nt > 0) {
+      d_cur[0] = chunks[0];
+      d_cur[1] = chunks[1];
+      load_base(d_cur, bc, bs);
+    }
+    if (nt > 1) {
+      d_nxt[0] = chunks[2];
+      d_nxt[1] = chunks[3];
+    }
+    for (int j = 0; j < nt; ++j) {
+      const int st = j % C::KST;
+      float2 cc[2] = {bc[0], bc[1]}, ss[2] = {bs[0], bs[1]};
+      const int4 d0 = d_cur[0], d1 = d_cur[1];
+      if (j + 2 < nt) {
+        d_nn[0] = chunks[2 * (j + 2)];
+        d_nn[1] = chunks[2 * (j + 2) + 1];
+      }
+      if (j + 1 < nt) load_base(d_nxt, bc, bs);
+      d_cur[0] = d_nxt[0];
+      d_cur[1] = d_nxt[1];
+      d_nxt[0] = d_nn[0];
+      d_nxt[1] = d_nn[1];
+      mbar_wait(&k_full[st], (j / C::KST) & 1);
+      const uint32_t tile = smem_u32(sK + st * C::KV_BYTES);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if ((h ? d1.w : d0.w) < 0) continue;                  // request rows: already rotated
+#if defined(VLC_PA_EXP) && VLC_PA_EXP == 1
+        continue;                                             // timing experiment: no rotation work
+#endif
+        float2 c = cc[h], s = ss[h];
+#pragma unroll
+        for (int k = 0; k < STEPS; ++k) {
+          const int row = h * PA_CHUNK + r0 + k * RPW;
+          const uint32_t plo = tile + eoff(row, f0), phi = tile + eoff(row, f0 + HALF);
+          const uint32_t lo = lds32(plo), hi = lds32(phi);
+#if defined(VLC_PA_EXP) && VLC_PA_EXP == 2
+          sts32(plo, lo ^ hi);                                // timing experiment: smem traffic only
+          sts32(phi, hi);
+          continue;
+#endif
+          // packed fp32 pairs (FMUL2 / FFMA2): lo' = a c + b (-s), hi' = b c + a s
+          const float2 av = make_float2(bf16_lo(lo), bf16_hi(lo)), bv = make_float2(bf16_lo(hi), bf16_hi(hi));
+          const float2 ns = fmul2(s, make_float2(-1.f, -1.f));
+          const float2 ro = ffma2(bv, ns, fmul2(av, c)), rh = ffma2(av, s, fmul2(bv, c));
+          sts32(plo, pack_bf16(ro.x, ro.y));
+          sts32(phi, pack_bf16(rh.x, rh.y));
+          // advance RPW positions: (c, s) <- (c cos - s sin, s cos + c sin)
+          const float2 cn = ffma2(s, nsts, fmul2(c, stc));
+          s = ffma2(c, sts, fmul2(s, stc));
+          c = cn;
+        }
+      }
       fence_proxy_async_smem();      // generic-proxy writes -> visible to the tensor core's reads
       mbar_arrive(&k_ready[st]);
     }

@@ -411,11 +411,13 @@ def _merged_kv_loader(out, lay, spec: RequestSpec, kv_pool, cfg: ModelConfig, re
         a = torch.from_numpy(np.concatenate(kpre_idx)).cuda()
         b = torch.from_numpy(np.concatenate(kpre_dst)).cuda()
         K[b] = kpre.view(-1, kvd)[a]
+        V = vc[:, kvoff:kvoff + n].clone()     # computed rows (and relocated boundary rows)
         if pool_idx:
+            # reused rows straight from the store pages (the attention reads them there too)
             a = torch.from_numpy(np.concatenate(pool_idx)).cuda()
             b = torch.from_numpy(np.concatenate(pool_dst)).cuda()
             K[b] = kv_pool.k[a]
-        V = vc[:, kvoff:kvoff + n].clone()
+            V.view(L * n, kvd)[b] = kv_pool.v[a]
         return K.view(L, n, kvd), V
     return load
 

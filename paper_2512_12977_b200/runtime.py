@@ -303,7 +303,9 @@ class Runner:
         hd = cfg.head_dim
         kv = kv or dw.kv
         heads = heads or dw.heads
-        ws_o = self.shared.get("attn_ws_o", (max(1, slots) * 8 * 256 * hd,), torch.float32, zero=False)
+        if pool is None and dw.cos is None:
+            dw.ensure_positions(2)     # tables only read for store chunks; the pointer must be valid
+        ws_o =self.shared.get("attn_ws_o", (max(1, slots) * 8 * 256 * hd,), torch.float32, zero=False)
         ws_ml = self.shared.get("attn_ws_ml", (max(1, slots) * 8 * 256 * 2,), torch.float32, zero=False)
         a = N.AttnPagedArgs(
             q=q.data_ptr(), q_rows_cap=q.shape[0], kc=kc.data_ptr(), vc=vc.data_ptr(), layers_cap=kc.shape[0],
