@@ -179,7 +179,11 @@ int vlc_store_write_pages(const void* src, int src_f32, int layers, int tokens, 
  * max_ctas co-resident CTAs (0 = one per SM); tiles shared by several CTAs are reduced in
  * parallel through `ws` (>= ctas*8*128*256 floats) with `counters` (>= 2*ctas ints, zeroed
  * once; the kernel leaves them zeroed; >= 4098 ints when epi->norm_gamma is set: the fused norm's
- * grid barrier uses counters[4096..4097]).  Replaces engine.py:176-178, 183-185, 187. */
+ * grid barrier uses counters[4096..4097]).  Token tiles >= 32 run the CTA-pair (cta_group::2)
+ * stream-K schedule over 256-row tiles x 128-wide k-blocks on every SM pair: its split tiles
+ * exchange fp32 partials through ws (2 * 74 * 128 * 256 floats) and per-tile flags in
+ * counters[12288 .. 12288 + 2 * tiles) -- pass counters of >= 16384 ints (<= 2048 tiles; else
+ * whole-tile pairs only).  Replaces engine.py:176-178, 183-185, 187. */
 int vlc_gemm_bf16(const void* w, int n_pad, int k_pad, const void* x, int x_rows_cap,
                   int m_tokens, const vlc_epilogue* epi, int max_ctas, float* ws, size_t ws_bytes,
                   int* counters, cudaStream_t stream);

@@ -592,7 +592,7 @@ int g_coop = 1;
 int g_pdl = 1;
 
 int g_deterministic = 0;  // tuning key 13: 1 = RESID split-K partials through the ordered fix-up
-int g_pair = 96;          // tuning key 10: CTA-pair GEMM for non-RESID kinds when n_tile >= this (0 = off)
+int g_pair = 160;         // tuning key 10: CTA-pair stream-K GEMM (multi-wave) when the token tile >= this (0 = off)
 int g_unsplit_min = 64;   // tuning key 9: tile count from which each tile gets its own CTA (no split-K)
 int g_wide = 1;   // tuning key 7: 0 auto, 1 never use 256-row tiles (default: measured slower), 2 always
 int g_mc = 1;     // tuning key 16: cluster size of the one-tile-per-CTA schedule (multicast activations)
@@ -646,19 +646,23 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
        epi.norm_pk_rows <= 0 || epi.norm_rows > epi.m_tokens || epi.norm_rows < 0))
     return cudaErrorInvalidValue;
   const int n_tile = gemm_row_tile(m_tokens);
-  // token-heavy non-residual GEMMs: CTA-pair kernel (halves the activation bytes per SM)
-  // (multi-wave GEMMs only -- the LM head: measured 7% faster there, no gain at <= 1 wave)
-  //  g_pair < 0: force the pair kernel from n_tile >= -g_pair (tests)
+  // Multi-wave GEMMs (the LM head) with token tiles >= pair_min: the CTA-pair stream-K kernel
+  // (vlc_gemm_pair.cu; head at c = 236: 282 -> 258 us, profiles/r2_gemm_pair_streamk.txt).  The
+  // one-wave projections stay on the single-CTA kernel: under stream-K over all 74 pairs they are
+  // L2-throughput bound like it (146 vs 219 MB through L2 but ~8 vs ~10 TB/s) and pay the exposed
+  // last-segment epilogue on every SM (QKV 31.2 -> 32.9 us, gate/up 32.4 -> 38.3 us at c = 236).
+  //  g_pair < 0: force the pair kernel from n_tile >= -g_pair (tests); 0: off
   const int pair_min = g_pair < 0 ? -g_pair : g_pair;
-  if (g_pair != 0 && epi.kind != EPI_RESID && n_tile >= pair_min &&
-      (g_pair < 0 || (long long)(n_pad / 128) * ((m_tokens + n_tile - 1) / n_tile) >= 2LL * num_sms())) {
+  const long long tiles128 = (long long)(n_pad / 128) * ((m_tokens + n_tile - 1) / n_tile);
+  if (g_pair != 0 && n_tile >= pair_min && (g_pair < 0 || tiles128 >= 2LL * num_sms()) &&
+      !(epi.kind == EPI_RESID && g_deterministic) && epi.norm_gamma == nullptr && epi.red_scratch == nullptr) {
     if (rl && rl->n_blocks > 0) {                      // the pair kernel has no spare CTAs
       const cudaError_t e = launch_relocate(*rl, stream);
       if (e != cudaSuccess) return e;
       rl = nullptr;
     }
     const cudaError_t e = launch_gemm_pair(W, n_pad, k_pad, X, x_rows_cap, m_tokens, epi,
-                                           max_ctas > 0 ? max_ctas / 2 : 0, stream);
+                                           max_ctas > 0 ? max_ctas / 2 : 0, ws, ws_bytes, counters, stream);
     if (e != cudaErrorNotSupported) return e;
   }
   const bool wide_ok = n_pad % 256 == 0;

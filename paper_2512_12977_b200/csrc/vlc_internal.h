@@ -110,7 +110,8 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
                         int* counters, cudaStream_t stream, const RelocArgs* rl = nullptr);
 int gemm_row_tile(int m_tokens);
 cudaError_t launch_gemm_pair(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap, int m_tokens,
-                             const GemmEpi& epi, int max_pairs, cudaStream_t stream);
+                             const GemmEpi& epi, int max_pairs, float* ws, size_t ws_bytes, int* counters,
+                             cudaStream_t stream);
 cudaError_t launch_pack(const void* src, int rows, int cols, int ld, void* dst, int R, int KB, cudaStream_t s);
 
 cudaError_t launch_attention_paged(const vlc_attn_paged_args& a, cudaStream_t stream);

@@ -60,7 +60,7 @@ def phases(n, k, m, ctas, kind=None):
     X = N.pack(torch.randn(m, k, device="cuda").bfloat16(), R, rows_cap=-(-m // R) * R)
     out = torch.zeros(m + 256, n, device="cuda", dtype=torch.float32)
     e = N.Epilogue()
-    e.kind, e.n_valid, e.m_tokens, e.out, e.ldo = N.EPI_BF16 if kind is None else kind, n, m, out.data_ptr(), n
+    e.kind, e.n_valid, e.m_tokens, e.out, e.ldo = N.EPI_BF16 if kind in (None, "pair") else kind, n, m, out.data_ptr(), n
     dbg = torch.zeros(320 * 8, dtype=torch.int64, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     for it in range(3):
@@ -75,7 +75,9 @@ def phases(n, k, m, ctas, kind=None):
     d = d[g]
     t0 = d[:, 0].min()
     d = np.where(d > 0, (d - t0) / 1e3, -1.0)
-    names = ["start", "prod_go", "prod_done", "acc_full(last)", "partials_done", "fixup_go", "epi_end", "exit"]
+    names = (["start", "prod_go", "prod_done", "acc_full(last)", "owner_go", "acc_full(seg0)", "epi_end", "exit"]
+             if kind == "pair" else
+             ["start", "prod_go", "prod_done", "acc_full(last)", "partials_done", "fixup_go", "epi_end", "exit"])
     print(f"--- N={n} K={k} M={m} ctas={ctas}: {len(d)} CTAs; us rel. to first start")
     for i, nm in enumerate(names):
         col = d[:, i]
@@ -89,11 +91,11 @@ if __name__ == "__main__":
     import numpy as np  # noqa: F811
     mode = sys.argv[1] if len(sys.argv) > 1 else "sweep"
     if mode == "pairphases":      # single-CTA vs CTA-pair kernel, QKV / GU shapes at c = 236
-        for pair in (0, -32):
+        for pair in (0, 32):
             lib.vlc_set_tuning(10, pair)
             print(f"=== pair threshold {pair}")
             for (n, kk, m, c) in ((10752, 3584, 236, 0), (14336, 3584, 236, 0)):
-                phases(n, kk, m, c)
+                phases(n, kk, m, c, kind="pair" if pair else None)
         lib.vlc_set_tuning(10, 96)
     if mode == "decoupled":       # one-tile GEMMs with decoupled weight / activation rings (key 18)
         for dec in (2, 12, 13, 14, 2, 13):
