@@ -126,6 +126,7 @@ typedef struct vlc_attn_paged_args {
   float* ws_o; float* ws_ml; int ws_slots;
   int* counters;
   float scale_log2;                              /* log2(e) / sqrt(head_dim)                     */
+  unsigned long long* trace;                     /* NULL, or [n_items][64] globaltimer stamps    */
 } vlc_attn_paged_args;
 
 const char* vlc_last_error(void);

@@ -50,7 +50,7 @@ class AttnPagedArgs(C.Structure):
                 ("qpos", C.c_void_p), ("rowof", C.c_void_p), ("out", C.c_void_p), ("ldo", C.c_int),
                 ("pk_rows", C.c_int), ("pk_kb", C.c_int),
                 ("ws_o", C.c_void_p), ("ws_ml", C.c_void_p), ("ws_slots", C.c_int),
-                ("counters", C.c_void_p), ("scale_log2", C.c_float)]
+                ("counters", C.c_void_p), ("scale_log2", C.c_float), ("trace", C.c_void_p)]
 
 
 _lib = None

@@ -86,6 +86,16 @@ __device__ __forceinline__ void tmem_ld_n(uint32_t taddr, float* v) {
   }
 }
 
+// timing trace (a.trace != NULL only in timing studies): slot s of this CTA's 64 stamps
+#define PA_TRACE(s)                                                                        \
+  do {                                                                                     \
+    if (a.trace) {                                                                         \
+      unsigned long long t_;                                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                               \
+      a.trace[blockIdx.x * 64 + (s)] = t_;                                                 \
+    }                                                                                      \
+  } while (0)
+
 template <int HD>
 __global__ void __launch_bounds__(PA_THREADS, 1)
     attn_paged_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kc,
@@ -153,6 +163,7 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_wait();                 // Q / K / V / work lists come from the previous kernels
   if (threadIdx.x == 0) pdl_trigger();
+  if (threadIdx.x == 0) PA_TRACE(0);
 
   if (warp == 0) {
     // ---------------- TMA producer
@@ -201,6 +212,7 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
       const uint32_t idesc_s = make_idesc_bf16(128, PA_KT, 0, 0);
       const uint32_t idesc_o = make_idesc_bf16(128, HD, 0, 1);
       mbar_wait(q_full, 0);
+      PA_TRACE(1);
       auto issue_s = [&](int j) {   // S[j & 1] = Q K_j^T
         const int st = j % C::KST;
         mbar_wait(&k_ready[st], (j / C::KST) & 1);
@@ -308,38 +320,46 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
       d_nxt[0] = d_nn[0];
       d_nxt[1] = d_nn[1];
       mbar_wait(&k_full[st], (j / C::KST) & 1);
+      if (wr == 0 && lane == 0 && j < 16) PA_TRACE(18 + j);
       const uint32_t tile = smem_u32(sK + st * C::KV_BYTES);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         if ((h ? d1.w : d0.w) < 0) continue;                  // request rows: already rotated
-#if defined(VLC_PA_EXP) && VLC_PA_EXP == 1
-        continue;                                             // timing experiment: no rotation work
-#endif
         float2 c = cc[h], s = ss[h];
+        // all loads of the chunk first, then the math, then the stores: the shared-memory accesses
+        // are volatile asm (ordered), so interleaving them per step would serialise every step on
+        // the load latency (1.82 -> 1.61 us per 128-key tile at the C3 layout)
+        uint32_t lo[STEPS], hi[STEPS];
 #pragma unroll
         for (int k = 0; k < STEPS; ++k) {
           const int row = h * PA_CHUNK + r0 + k * RPW;
-          const uint32_t plo = tile + eoff(row, f0), phi = tile + eoff(row, f0 + HALF);
-          const uint32_t lo = lds32(plo), hi = lds32(phi);
-#if defined(VLC_PA_EXP) && VLC_PA_EXP == 2
-          sts32(plo, lo ^ hi);                                // timing experiment: smem traffic only
-          sts32(phi, hi);
-          continue;
-#endif
+          lo[k] = lds32(tile + eoff(row, f0));
+          hi[k] = lds32(tile + eoff(row, f0 + HALF));
+        }
+#pragma unroll
+        for (int k = 0; k < STEPS; ++k) {
           // packed fp32 pairs (FMUL2 / FFMA2): lo' = a c + b (-s), hi' = b c + a s
-          const float2 av = make_float2(bf16_lo(lo), bf16_hi(lo)), bv = make_float2(bf16_lo(hi), bf16_hi(hi));
+          const float2 av = make_float2(bf16_lo(lo[k]), bf16_hi(lo[k]));
+          const float2 bv = make_float2(bf16_lo(hi[k]), bf16_hi(hi[k]));
           const float2 ns = fmul2(s, make_float2(-1.f, -1.f));
           const float2 ro = ffma2(bv, ns, fmul2(av, c)), rh = ffma2(av, s, fmul2(bv, c));
-          sts32(plo, pack_bf16(ro.x, ro.y));
-          sts32(phi, pack_bf16(rh.x, rh.y));
+          lo[k] = pack_bf16(ro.x, ro.y);
+          hi[k] = pack_bf16(rh.x, rh.y);
           // advance RPW positions: (c, s) <- (c cos - s sin, s cos + c sin)
           const float2 cn = ffma2(s, nsts, fmul2(c, stc));
           s = ffma2(c, sts, fmul2(s, stc));
           c = cn;
         }
+#pragma unroll
+        for (int k = 0; k < STEPS; ++k) {
+          const int row = h * PA_CHUNK + r0 + k * RPW;
+          sts32(tile + eoff(row, f0), lo[k]);
+          sts32(tile + eoff(row, f0 + HALF), hi[k]);
+        }
       }
       fence_proxy_async_smem();      // generic-proxy writes -> visible to the tensor core's reads
       mbar_arrive(&k_ready[st]);
+      if (wr == 0 && lane == 0 && j < 16) PA_TRACE(34 + j);
     }
   } else {
     // ---------------- softmax: warp w -> TMEM lane quadrant w & 3, chunk half hh
@@ -358,6 +378,7 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
       float s[CW];
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
+      if (warp == 2 && lane == 0 && j < 16) PA_TRACE(2 + j);
 #pragma unroll
       for (int c = 0; c < CW / 32; ++c) tmem_ld32(tS + 32 * c, s + 32 * c);
       tmem_wait_ld();
@@ -419,6 +440,7 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
       mbar_wait(o_done, (nt - 1) & 1);
       tc_fence_after();
     }
+    if (warp == 2 && lane == 0) PA_TRACE(50);
     // merge the two halves' (max, sum): M = max, w_h = 2^(m_h - M), L = w0 l0 + w1 l1
     xm[hh * 128 + r] = m_run;
     xm[256 + hh * 128 + r] = l_run;
@@ -501,6 +523,7 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
+  if (threadIdx.x == 0) PA_TRACE(51);
   if (group < 0) return;
   // ---------------- parallel merge of the nsplit partials (all CTAs of the group co-resident).
   // This CTA merges rows [r_lo, r_hi) of the group: pass 1 turns each row's (m, l) per split into
@@ -513,6 +536,7 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
   }
   __syncthreads();
   __threadfence();
+  if (threadIdx.x == 0) PA_TRACE(52);
   const int r_lo = nq * part / nsplit, r_hi = nq * (part + 1) / nsplit;
   const int nr = max(0, r_hi - r_lo);
   float2* s_ml = reinterpret_cast<float2*>(sK);                 // [nr][8]
@@ -564,6 +588,7 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
         make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
   }
   __syncthreads();
+  if (threadIdx.x == 0) PA_TRACE(53);
   if (threadIdx.x == 0) {
     // the last CTA of the group to finish merging re-zeroes both counters for the next launch
     if (atomicAdd(&a.counters[a.ws_slots + group], 1) == nsplit - 1) {
