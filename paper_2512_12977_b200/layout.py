@@ -142,8 +142,11 @@ def store_chunks_ok(T: int, P: int) -> bool:
 def request_chunks(spec: RequestSpec, i: int, kvoff: int, page_base: dict) -> np.ndarray:
     """Key chunks of one request at layer i, in position order (vlc_attn_paged, include/vlcache.h):
     text runs and recomputed image chunks from the request rows; image chunks at or past the
-    layer's keep count straight from the store page (a = page-table index, b = row offset); the
-    chunk holding the keep boundary from the request rows (its cached rows relocated there)."""
+    layer's keep count straight from the store page (a = page-table index, b = row offset).  The
+    64-token block holding the keep boundary k is split in two chunks: [t0, k) from the request rows
+    (recomputed) and [k, t0 + 64) from the store page at row offset k mod P (inside one page since
+    P is a multiple of 64), so no cached row goes through vlc_kv_relocate.  Store pages whose size is
+    not a multiple of 64 (and T > P) fall back to relocating every cached row (relocated_ranges)."""
     spans = sorted(spec.images)
     out, cur = [], 0
 
@@ -161,6 +164,9 @@ def request_chunks(spec: RequestSpec, i: int, kvoff: int, page_base: dict) -> np
             ln = min(CHUNK, T - t0)
             if direct and t0 >= k:
                 out.append([start + t0, ln, page_base[m] + i * ppl + t0 // P, t0 % P])
+            elif direct and t0 < k < t0 + ln:          # the keep boundary splits this block
+                out.append([start + t0, k - t0, kvoff + start + t0, -1])
+                out.append([start + k, t0 + ln - k, page_base[m] + i * ppl + k // P, k % P])
             else:
                 out.append([start + t0, ln, kvoff + start + t0, -1])
         cur = start + T
@@ -170,9 +176,9 @@ def request_chunks(spec: RequestSpec, i: int, kvoff: int, page_base: dict) -> np
 
 
 def relocated_ranges(spec: RequestSpec, i: int):
-    """Per image: the cached token range [k, e) of layer i that goes through vlc_kv_relocate into
-    the request rows -- the rest of the keep boundary's chunk (the chunk is read from the request
-    rows), or every cached row when the page size does not allow direct store chunks."""
+    """Per image: the cached token range [k, T) of layer i that goes through vlc_kv_relocate into
+    the request rows -- only when the page size does not allow direct store chunks (the chain's
+    attention otherwise reads every cached row from its store page)."""
     out = []
     for m, (start, T) in enumerate(spec.images):
         if not spec.kv_hit[m]:
@@ -181,11 +187,7 @@ def relocated_ranges(spec: RequestSpec, i: int):
         if k >= T:
             continue
         if not store_chunks_ok(T, int(spec.page_tokens)):
-            e = T
-        else:
-            e = min(T, -(-k // CHUNK) * CHUNK)
-        if e > k:
-            out.append((m, k, e))
+            out.append((m, k, T))
     return out
 
 
