@@ -74,26 +74,9 @@ typedef struct vlc_epilogue {
   const float* add;  int ld_add;
   int pk_rows;       /* > 0: BF16 / SWIGLU output written PACKED (row tile pk_rows, pk_kb blocks) */
   int pk_kb;
-  /* RESID only, optional (norm_gamma = NULL: off): once every CTA's contribution to the fp32
-   * residual `out` has landed (grid barrier on `counters`), RMSNorm of its first norm_rows rows
-   * (model.py:257-259) -> norm_out, bf16 PACKED with row tile norm_pk_rows / norm_pk_kb blocks.
-   * Replaces the vlc_rmsnorm launch that would follow the projection.                    */
-  const float* norm_gamma;
-  void* norm_out;
-  float norm_eps;
-  int norm_rows;
-  int norm_pk_rows;
-  int norm_pk_kb;
-  /* optional: bytes [l2_prefetch, l2_prefetch + l2_prefetch_bytes) are prefetched into L2 (evict-last)
-   * while this GEMM runs -- the next projection's weights, so that they stream from HBM in this
-   * GEMM's spare bandwidth instead of on the critical path.  NULL / 0 = off.                  */
-  const void* l2_prefetch;
-  unsigned long long l2_prefetch_bytes;
-  /* optional (kinds other than RESID / QKV_ROPE): zero-maintained fp32 scratch of >= max_ctas * 128 * 256 floats (all
-   * zero on entry; the kernel leaves it zero).  With it, a weight tile whose k-range is split across
-   * CTAs is reduced with red.add into the scratch and finished by its last-arriving CTA (no partial
-   * workspace, no waiting), which lets one-wave projections (QKV: 84 tiles) use every SM.      */
-  float* red_scratch;
+  /* RESID: split-K partials reduced in a fixed order through `ws` (bitwise reproducible runs)
+   * instead of red.add in arrival order (faster).  0 = red.add.                               */
+  int deterministic;
 } vlc_epilogue;
 
 /* Paged attention (vlc_attn_paged; model.py:274-291, engine.py:179-182): the recomputed queries of
@@ -135,8 +118,8 @@ int vlc_version(void);
  * a direct cudaMemcpyAsync without a framework dispatch).  host should be pinned.            */
 int vlc_copy_h2d_async(void* device_dst, const void* host_src, size_t bytes, cudaStream_t stream);
 
-/* Tuning knobs for experiments: key 1 = GEMM pipeline stages (0 = automatic); keys 2-19 see
-   vlc_capi.cu and INTEGRATION.md (e.g. 15 = attention kernel variant). */
+/* Schedule overrides for experiments and tests ONLY (process-global, not re-entrant; nothing in
+   the drop-in calls it): key 1 = GEMM pipeline stages (0 = automatic); other keys see vlc_capi.cu. */
 int vlc_set_tuning(int key, int value);
 int vlc_set_debug_buffer(void* device_ptr);
 
@@ -146,6 +129,7 @@ int vlc_set_debug_buffer(void* device_ptr);
  * (freshly encoded images of a cache miss). */
 int vlc_embed_assemble(float* x, int ldx, const void* embed_bf16, int d, const float* enc_a,
                        const float* enc_b, const int* src, int rows, cudaStream_t stream);
+
 
 /* RMSNorm eps (model.py:257-259) of rows (optionally gathered via row_map) -> bf16 or f32;
  * bf16 output is PACKED when pk_rows > 0 (then ldo is ignored). */
@@ -179,8 +163,7 @@ int vlc_store_write_pages(const void* src, int src_f32, int layers, int tokens, 
  * Stream-K schedule over (128-row weight tile x token tile x 64-wide k-block) units on
  * max_ctas co-resident CTAs (0 = one per SM); tiles shared by several CTAs are reduced in
  * parallel through `ws` (>= ctas*8*128*256 floats) with `counters` (>= 2*ctas ints, zeroed
- * once; the kernel leaves them zeroed; >= 4098 ints when epi->norm_gamma is set: the fused norm's
- * grid barrier uses counters[4096..4097]).  Token tiles >= 32 run the CTA-pair (cta_group::2)
+ * once; the kernel leaves them zeroed).  Token tiles >= 32 run the CTA-pair (cta_group::2)
  * stream-K schedule over 256-row tiles x 128-wide k-blocks on every SM pair: its split tiles
  * exchange fp32 partials through ws (2 * 74 * 128 * 256 floats) and per-tile flags in
  * counters[12288 .. 12288 + 2 * tiles) -- pass counters of >= 16384 ints (<= 2048 tiles; else
@@ -188,17 +171,6 @@ int vlc_store_write_pages(const void* src, int src_f32, int layers, int tokens, 
 int vlc_gemm_bf16(const void* w, int n_pad, int k_pad, const void* x, int x_rows_cap,
                   int m_tokens, const vlc_epilogue* epi, int max_ctas, float* ws, size_t ws_bytes,
                   int* counters, cudaStream_t stream);
-
-/* The QKV GEMM fused with the same layer's kv_relocate: CTAs beyond the GEMM's own (the SMs a
- * one-tile-per-CTA projection leaves idle) gather + re-rotate + scatter the layer's cached K/V
- * (arguments as vlc_gemm_bf16 followed by vlc_kv_relocate's); falls back to two launches when the
- * GEMM occupies every SM.  Replaces engine.py:153-155 + 176-180 for one layer. */
-int vlc_gemm_bf16_relocate(const void* w, int n_pad, int k_pad, const void* x, int x_rows_cap, int m_tokens,
-                           const vlc_epilogue* epi, int max_ctas, float* ws, size_t ws_bytes, int* counters,
-                           const void* kpool, const void* vpool, int page_tokens, const int* page_table, int kv,
-                           int head_dim, void* kc, void* vc, int kv_rows_cap, const int* descs, const int* blocks,
-                           int n_blocks, const float* cos_tab, const float* sin_tab, int tab_ld,
-                           cudaStream_t stream);
 
 int vlc_attn_paged(const vlc_attn_paged_args* args, cudaStream_t stream);
 

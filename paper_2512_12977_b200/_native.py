@@ -16,8 +16,9 @@ LIB_PATH = os.path.join(_PKG, "libvlcache.so")
 VLC_OK, VLC_ERR_INVALID, VLC_ERR_UNSUPPORTED, VLC_ERR_CUDA = 0, 1, 2, 3
 EPI_F32, EPI_RESID, EPI_BF16, EPI_BIAS_ADD, EPI_SWIGLU, EPI_QKV_PLAIN, EPI_QKV_ROPE = range(7)
 
-EXPORTS = ("vlc_last_error", "vlc_version", "vlc_embed_assemble", "vlc_rmsnorm", "vlc_add_rmsnorm", "vlc_kv_relocate",
-           "vlc_store_write_pages", "vlc_gemm_bf16", "vlc_gemm_bf16_relocate", "vlc_gemm_row_tile", "vlc_pack_operand", "vlc_attn_paged",
+EXPORTS = ("vlc_last_error", "vlc_version", "vlc_embed_assemble", "vlc_rmsnorm",
+           "vlc_add_rmsnorm", "vlc_kv_relocate", "vlc_store_write_pages", "vlc_gemm_bf16", "vlc_gemm_row_tile",
+           "vlc_pack_operand", "vlc_attn_paged",
            "vlc_patchify", "vlc_set_tuning", "vlc_set_debug_buffer", "vlc_copy_h2d_async")
 
 
@@ -33,9 +34,7 @@ class Epilogue(C.Structure):
                 ("cos_tab", C.c_void_p), ("sin_tab", C.c_void_p), ("tab_ld", C.c_int),
                 ("hd", C.c_int), ("seg", C.c_int), ("bias", C.c_void_p), ("add", C.c_void_p),
                 ("ld_add", C.c_int), ("pk_rows", C.c_int), ("pk_kb", C.c_int),
-                ("norm_gamma", C.c_void_p), ("norm_out", C.c_void_p), ("norm_eps", C.c_float),
-                ("norm_rows", C.c_int), ("norm_pk_rows", C.c_int), ("norm_pk_kb", C.c_int),
-                ("l2_prefetch", C.c_void_p), ("l2_prefetch_bytes", C.c_ulonglong), ("red_scratch", C.c_void_p)]
+                ("deterministic", C.c_int)]
 
 
 class AttnPagedArgs(C.Structure):
@@ -73,8 +72,6 @@ def load():
         lib.vlc_store_write_pages.argtypes = [vp, i, i, i, i, vp, i, vp, i, vp]
         lib.vlc_gemm_bf16.argtypes = [vp, i, i, vp, i, i, C.POINTER(Epilogue), i, vp, C.c_size_t, vp, vp]
         lib.vlc_gemm_row_tile.argtypes = [i]
-        lib.vlc_gemm_bf16_relocate.argtypes = [vp, i, i, vp, i, i, C.POINTER(Epilogue), i, vp, C.c_size_t, vp,
-                                               vp, vp, i, vp, i, i, vp, vp, i, vp, vp, i, vp, vp, i, vp]
         lib.vlc_pack_operand.argtypes = [vp, i, i, i, vp, i, i, vp]
         lib.vlc_attn_paged.argtypes = [C.POINTER(AttnPagedArgs), vp]
         lib.vlc_patchify.argtypes = [vp, i, i, vp, i, i, i, vp]

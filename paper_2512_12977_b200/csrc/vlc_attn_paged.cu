@@ -161,8 +161,15 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  pdl_wait();                 // Q / K / V / work lists come from the previous kernels
-  if (threadIdx.x == 0) pdl_trigger();
+  // Programmatic dependent launch: Q and the request K / V rows come from the QKV GEMM before this
+  // kernel, so the producer waits for it (griddepcontrol.wait) -- but only after it has issued the
+  // loads of the leading tiles whose chunks are all store pages (cached K / V, independent of it),
+  // and the rotation warps work on those while the GEMM drains.  The softmax warps wait as well
+  // (they write the attention output); the MMA warp only consumes shared memory / TMEM.
+  if (warp >= 2 && warp < 2 + PA_SOFT_WARPS) {
+    pdl_wait();
+    if (threadIdx.x == 64) pdl_trigger();
+  }
   if (threadIdx.x == 0) PA_TRACE(0);
 
   if (warp == 0) {
@@ -170,8 +177,6 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
     if (lane == 0 && nt > 0) {
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_normal();
-      mbar_expect_tx(q_full, C::Q_BYTES);
-      tma_load_3d(sQ, &map_q, q_full, 0, q_row0, head * C::N_ATOMS, pol_q);
       // one op per (chunk, atom): [atom][128 rows][SWZ] with chunk h in rows 64h .. 64h + 63
       auto load_tile = [&](uint8_t* dst, uint64_t* bar, int j, bool is_k) {
         mbar_expect_tx(bar, C::KV_BYTES);
@@ -199,11 +204,19 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
         mbar_wait(&v_empty[st], ((j / C::VST) & 1) ^ 1);
         load_tile(sV + st * C::KV_BYTES, &v_full[st], j, false);
       };
+      // leading store-only tiles before griddepcontrol.wait (their K / V do not depend on the GEMM)
+      auto store_only = [&](int j) { return chunks[2 * j].w >= 0 && chunks[2 * j + 1].w >= 0; };
+      int jk = 0, jv = 0;
+      while (jk < C::KST - 1 && jk < nt && store_only(jk)) load_k(jk++);
+      while (jv < C::VST && jv < jk) load_v(jv++);
+      pdl_wait();
+      mbar_expect_tx(q_full, C::Q_BYTES);
+      tma_load_3d(sQ, &map_q, q_full, 0, q_row0, head * C::N_ATOMS, pol_q);
       // K runs KST - 1 tiles ahead of V (S(j) needs K(j) a softmax before PV(j) needs V(j))
-      for (int j = 0; j < C::KST - 1 && j < nt; ++j) load_k(j);
+      for (; jk < C::KST - 1 && jk < nt; ++jk) load_k(jk);
       for (int j = 0; j < nt; ++j) {
         if (j + C::KST - 1 < nt) load_k(j + C::KST - 1);
-        load_v(j);
+        if (j >= jv) load_v(j);
       }
     }
   } else if (warp == 1) {
@@ -398,8 +411,10 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
       const bool has_o = m_run != NEG_INF;
       const bool resc = __any_sync(0xffffffffu, need && has_o);
       // P(j) goes over S buffer j & 1, whose previous P (PV(j-2)) is complete: S(j) was issued after
-      // it.  O is touched only when some row rescales, and then PV(j-1) must be complete too.
-      if (j > 0 && (resc || j == nt - 1)) {
+      // it.  O is touched only when some row rescales, and then PV(j-1) must be complete first;
+      // otherwise PV(j-1)'s phase is still observed below, before P(j) is published (every o_done
+      // phase gets a waiter before the next one can complete -- compute-sanitizer synccheck)
+      if (j > 0 && resc) {
         mbar_wait(o_done, (j - 1) & 1);
         tc_fence_after();
       }
@@ -431,6 +446,7 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
         s[i] = __uint_as_float(pack_bf16(p0, p1));
       }
       l_run += (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
+      if (j > 0 && !resc) mbar_wait(o_done, (j - 1) & 1);   // PV(j-1): issued a softmax ago, done
       tmem_st32f(tS, s);                               // P over this half's own S columns
       tmem_wait_st();
       tc_fence_before();

@@ -106,7 +106,6 @@ int vlc_patchify_impl(const float*, int, int, void*, int, int, int, cudaStream_t
 
 const char* vlc_last_error(void) { return g_err; }
 
-/* Experiment knobs (not part of the stable ABI): key 1 = GEMM pipeline stages (0 = auto). */
 int vlc_copy_h2d_async(void* device_dst, const void* host_src, size_t bytes, cudaStream_t stream) {
   if (bytes == 0) return VLC_OK;
   if (!device_dst || !host_src) return fail(VLC_ERR_INVALID, "copy_h2d: null pointer");
@@ -123,12 +122,8 @@ int vlc_set_tuning(int key, int value) {
     case 7: vlc::g_wide = value; return VLC_OK;                  // 256-row GEMM tiles
     case 9: vlc::g_unsplit_min = value; return VLC_OK;           // one-CTA-per-tile threshold
     case 10: vlc::g_pair = value; return VLC_OK;                 // CTA-pair GEMM threshold
-    case 13: vlc::g_deterministic = value != 0; return VLC_OK;   // bitwise-reproducible RESID reduction
-    case 14: vlc::g_reloc_wide = value; return VLC_OK;           // idle-SM relocation CTA smem (0 = plain)
-    case 16: vlc::g_mc = value >= 1 && value <= 8 ? value : 1; return VLC_OK;   // GEMM cluster multicast
     case 17: vlc::g_aligned_split = value; return VLC_OK;        // tile-aligned split-K
     case 18: vlc::g_decoupled = value; return VLC_OK;            // decoupled weight / activation rings
-    case 19: vlc::g_redx = value; return VLC_OK;                 // honour vlc_epilogue.red_scratch
     case 20: vlc::g_dec_min_tile = value; return VLC_OK;         // smallest token tile using key 18
     default: return fail(VLC_ERR_INVALID, "set_tuning: unknown key");
   }
@@ -215,33 +210,6 @@ int vlc_gemm_bf16(const void* w, int n_pad, int k_pad, const void* x, int x_rows
   return cuda_status(launch_gemm(w, n_pad, k_pad, x, x_rows_cap, m_tokens, *epi, max_ctas, ws, ws_bytes, counters,
                                  stream),
                      "gemm_bf16");
-}
-
-int vlc_gemm_bf16_relocate(const void* w, int n_pad, int k_pad, const void* x, int x_rows_cap, int m_tokens,
-                           const vlc_epilogue* epi, int max_ctas, float* ws, size_t ws_bytes, int* counters,
-                           const void* kpool, const void* vpool, int page_tokens, const int* page_table, int kv,
-                           int head_dim, void* kc, void* vc, int kv_rows_cap, const int* descs, const int* blocks,
-                           int n_blocks, const float* cos_tab, const float* sin_tab, int tab_ld,
-                           cudaStream_t stream) {
-  if (!w || !x || !epi) return fail(VLC_ERR_INVALID, "gemm_relocate: null pointer");
-  if (n_pad % 128 || k_pad % 128 || n_pad <= 0 || k_pad <= 0)
-    return fail(VLC_ERR_UNSUPPORTED, "gemm_relocate: n_pad and k_pad must be multiples of 128");
-  const int rt = gemm_row_tile(m_tokens);
-  if (m_tokens > 0 && x_rows_cap < (m_tokens + rt - 1) / rt * rt)
-    return fail(VLC_ERR_INVALID, "gemm_relocate: x_rows_cap must cover whole row tiles");
-  if (epi->m_tokens != m_tokens) return fail(VLC_ERR_INVALID, "gemm_relocate: epilogue m_tokens mismatch");
-  if (epi->kind == VLC_EPI_QKV_ROPE && (!epi->map2 || !epi->pos || !epi->cos_tab || epi->hd % 2))
-    return fail(VLC_ERR_INVALID, "gemm_relocate: QKV_ROPE needs map2/pos/tables");
-  if (n_blocks < 0 || page_tokens <= 0 || head_dim < 16 || head_dim % 16 || kv % head_dim || tab_ld != head_dim / 2)
-    return fail(VLC_ERR_INVALID, "gemm_relocate: bad relocation arguments");
-  RelocArgs r{reinterpret_cast<const __nv_bfloat16*>(kpool), reinterpret_cast<const __nv_bfloat16*>(vpool),
-              page_tokens, page_table, kv, head_dim, reinterpret_cast<__nv_bfloat16*>(kc),
-              reinterpret_cast<__nv_bfloat16*>(vc), kv_rows_cap, descs, reinterpret_cast<const int2*>(blocks),
-              n_blocks, cos_tab, sin_tab, tab_ld};
-  if (m_tokens <= 0) return cuda_status(launch_relocate(r, stream), "gemm_relocate");
-  return cuda_status(launch_gemm(w, n_pad, k_pad, x, x_rows_cap, m_tokens, *epi, max_ctas, ws, ws_bytes, counters,
-                                 stream, &r),
-                     "gemm_relocate");
 }
 
 int vlc_attn_paged(const vlc_attn_paged_args* a, cudaStream_t stream) {

@@ -19,7 +19,6 @@
 //   QKV_PLAIN encoder projections (model.py:318)
 #include "vlc_internal.h"
 #include "vlc_gemm_epi.cuh"
-#include "vlc_reloc.cuh"
 
 namespace vlc {
 
@@ -37,8 +36,6 @@ struct SkSched {
   int m_tiles;
   int red;       // RESID split partials reduced with red.add (1) or through the ordered fix-up (0)
   unsigned long long* dbg;   // phase timestamps (experiments; nullptr)
-  int mc;        // cluster size: k-block kb's activation block is loaded once, by CTA kb % mc of the
-                 // cluster, and multicast to all (1 = no cluster)
   int xh;        // decoupled: activation slots hold one 64-k atom (half a k-block) instead of a k-block
   int sw, sx;    // > 0: decoupled rings (one tile per CTA, H = 1): sw weight stages fed by warp 0 with
                  // no dependence on the previous kernel, sx activation stages fed by warp 2; the
@@ -68,82 +65,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 //        k-blocks: the activation bytes per weight byte halve, which keeps the L2 traffic of
 //        c ~ 240-token GEMMs under the LTS cap.  Single accumulator of 2 x n_tile columns.
 // The A (weight) bytes of a stage are 32 KB in both cases.
-// Grid-wide barrier of the first G CTAs (all co-resident: <= 1 CTA per SM, G <= #SMs).
-// cnt / gen: two ints of the counters buffer; the last arriver resets cnt and bumps gen.
-__device__ __forceinline__ void grid_barrier(int* cnt, int* gen, int G) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile int* vg = gen;
-    const int g0 = *vg;
-    __threadfence();
-    if (atomicAdd(cnt, 1) == G - 1) {
-      *cnt = 0;
-      __threadfence();
-      atomicAdd(gen, 1);
-    } else {
-      while (*vg == g0) __nanosleep(64);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-constexpr int NORM_BAR = 4096;   // counters[NORM_BAR], [NORM_BAR + 1]: the fused-norm grid barrier
-constexpr int REDX_CNT = 8192;   // counters[REDX_CNT + gf]: arrivals at split tile (first CTA gf) in red mode
-
-// RMSNorm of residual rows g, g + G, ... (< epi.norm_rows) -> packed bf16 (model.py:257-259;
-// same arithmetic as rmsnorm_kernel: y = (x / sqrt(mean(x^2) + eps)) * gamma).  All GEMM_THREADS
-// threads; the residual is read from L2 (__ldcg: the red.add results live there).
-// red: GEMM_THREADS / 32 floats of (dynamic) shared memory -- a static array would push the
-// kernel past the 227 KB per-block limit its dynamic-smem attribute is set to.
-__device__ __forceinline__ void fused_norm_rows(const GemmEpi& epi, int g, int G, float* red) {
-  constexpr int NV = 8;   // float4 per thread: d <= 8 * 4 * GEMM_THREADS
-  const int d = epi.n_valid, n4 = d >> 2;
-  const float4* g4 = reinterpret_cast<const float4*>(epi.norm_gamma);
-  for (int row = g; row < epi.norm_rows; row += G) {
-    const float4* xr = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(epi.out) + (long)row * epi.ldo);
-    float4 v[NV], gg[NV];
-    float acc = 0.f;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const int i = threadIdx.x + GEMM_THREADS * k;
-      v[k] = i < n4 ? __ldcg(xr + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-      gg[k] = i < n4 ? __ldg(g4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int k = 0; k < NV; ++k) acc += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    float tot = 0.f;
-#pragma unroll
-    for (int w = 0; w < GEMM_THREADS / 32; ++w) tot += red[w];
-    const float denom = sqrtf(tot / (float)d + epi.norm_eps);
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const int i = threadIdx.x + GEMM_THREADS * k;
-      if (i >= n4) break;
-      const uint2 pk = make_uint2(pack_bf16((v[k].x / denom) * gg[k].x, (v[k].y / denom) * gg[k].y),
-                                  pack_bf16((v[k].z / denom) * gg[k].z, (v[k].w / denom) * gg[k].w));
-      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(epi.norm_out) +
-                                packed_off(row, 4 * i, epi.norm_pk_rows, epi.norm_pk_kb)) = pk;
-    }
-    __syncthreads();   // red[] reused by the next row
-  }
-}
-
 template <int KIND, int H>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc(const uint8_t* __restrict__ wp, const uint8_t* __restrict__ xp, GemmEpi epi, SkSched sk,
-                 int n_tile, int stages, float* ws, int* counters, RelocArgs rl) {
-  // CTAs past the GEMM's own (sk.G) relocate cached KV (vlc_reloc.cuh) on the SMs the projection
-  // leaves idle: independent of the previous kernel's output and of this GEMM's (disjoint rows)
-  if ((int)blockIdx.x >= sk.G) {
-    if (threadIdx.x < RELOC_THREADS)
-      for (int b = blockIdx.x - sk.G; b < rl.n_blocks; b += gridDim.x - sk.G) relocate_block(rl, b, threadIdx.x);
-    return;
-  }
+                 int n_tile, int stages, float* ws, int* counters) {
   constexpr int BM = GEMM_BM * H;
   constexpr int BK = GEMM_BK / H;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -178,7 +103,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     DBG(0);
     for (int s = 0; s < wst; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], sk.mc);   // every CTA of the cluster has consumed the stage
+      mbar_init(&empty[s], 1);
     }
     if (dec)
       for (int s = 0; s < xst; ++s) {
@@ -193,12 +118,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
-  if (sk.mc > 1) cluster_sync_all();   // peers' barriers initialised before any multicast
-  else __syncthreads();
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int crank = sk.mc > 1 ? (int)cluster_ctarank() : 0;
-  const uint16_t cmask = (uint16_t)((1u << sk.mc) - 1);
 
   // source of the weight half h of k-block kb of weight tile mt (PACKED layout, include/vlcache.h)
   auto a_src = [&](int mt, int kb, int h) -> const uint8_t* {
@@ -286,16 +208,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             bulk_load(sa + pre * a_bytes + h * (a_bytes / H), a_src(mt, kb, h), a_bytes / H, &full[pre], pol_w);
         }
       }
-      if (epi.l2_prefetch_bytes > 0) {
-        // this CTA's share of the next projection's weights -> L2 (evict-last), 64 KB per op
-        const unsigned long long per = ((epi.l2_prefetch_bytes / sk.G + 65535) >> 16) << 16;
-        const unsigned long long lo = per * g;
-        const unsigned long long hi = min(epi.l2_prefetch_bytes, lo + per);
-        const uint64_t pol_pf = policy_evict_last();
-        for (unsigned long long o = lo; o < hi; o += 65536)
-          bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(epi.l2_prefetch) + o, (uint32_t)min(65536ull, hi - o),
-                           pol_pf);
-      }
       pdl_wait();
       int stage = 0, u = 0;
       uint32_t phase = 0;
@@ -312,13 +224,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               bulk_load(sa + stage * a_bytes + h * (a_bytes / H), a_src(mt, kb, h), a_bytes / H, &full[stage],
                         pol_w);
           }
-          if (sk.mc == 1) {
-            bulk_load(sb + stage * b_bytes, b_src(tt, kb), b_bytes, &full[stage], pol_x);
-          } else if (kb % sk.mc == crank) {
-            // the stage is free in every CTA: the empty[stage] wait above counts all mc consumers
-            // (first ring pass: every stage is fresh)
-            bulk_load_mc(sb + stage * b_bytes, b_src(tt, kb), b_bytes, &full[stage], cmask, pol_x);
-          }
+          bulk_load(sb + stage * b_bytes, b_src(tt, kb), b_bytes, &full[stage], pol_x);
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
       }
@@ -362,8 +268,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               }
             }
           }
-          if (sk.mc > 1) tc_commit_mc(&empty[stage], cmask);
-          else tc_commit(&empty[stage]);
+          tc_commit(&empty[stage]);
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
         tc_commit(&acc_full[slot]);
@@ -449,11 +354,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint32_t d = tmem + slot * 256 + (H == 2 ? eg * 256 : 0) + lane_off;
       const int hoff = H == 2 ? eg * 128 : 0;                 // weight-row offset of this group
       const bool split = gf != gl && !(KIND == EPI_RESID && sk.red);   // RESID partials: red.add in L2
-      // red mode: the split tile's partials meet in the zero-maintained scratch slot of its first CTA
-      // (not compiled for QKV_ROPE: its second epilogue instance spilled the hot one's registers)
-      const bool redx = KIND != EPI_RESID && KIND != EPI_QKV_ROPE && split && epi.red_scratch != nullptr;
-      float* rslot = redx ? epi.red_scratch + (long)gf * BM * n_tile : nullptr;   // [n_tile][BM]
-      float* part = split && !redx ? ws + (2L * g + (t == t_first ? 0 : 1)) * (long)n_tile * BM : nullptr;
+      float* part = split ? ws + (2L * g + (t == t_first ? 0 : 1)) * (long)n_tile * BM : nullptr;
       const int nch = (n_tile + 31) / 32;
       for (int ci = (H == 1 ? eg : 0); ci < nch; ci += (H == 1 ? 2 : 1)) {
         const int c = ci * 32;
@@ -464,15 +365,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int jj = 0; jj < 32; ++jj) stage_buf[jj * 128 + row] = v[jj];
         asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
         const int jmax = min(32, n_tile - c);
-        if (redx) {
-          for (int jj = quad; jj < jmax; jj += 4) {
-            const float4 x4 = *reinterpret_cast<const float4*>(stage_buf + jj * 128 + 4 * lane);
-            float* o = rslot + (long)(c + jj) * BM + hoff + 4 * lane;
-            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(o), "f"(x4.x), "f"(x4.y), "f"(x4.z),
-                         "f"(x4.w)
-                         : "memory");
-          }
-        } else if (split) {
+        if (split) {
           for (int jj = quad; jj < jmax; jj += 4)
             __stcg(reinterpret_cast<float4*>(part + (long)(c + jj) * BM + hoff) + lane,
                    *reinterpret_cast<const float4*>(stage_buf + jj * 128 + 4 * lane));
@@ -484,32 +377,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[slot]);   // this thread's TMEM reads of the accumulator are done
-      if (redx) {
-        // every participant's red.adds land before its arrival; the last arrival finishes the tile:
-        // scratch -> stage (re-zeroing the scratch) -> the fused epilogue, chunk by chunk
-        const int nseg = gl - gf + 1;
-        __threadfence();
-        asm volatile("bar.sync 3, 256;" ::: "memory");
-        if (leader) tmem_slot[1] = (atomicAdd(&counters[REDX_CNT + gf], 1) == nseg - 1) ? 1u : 0u;
-        asm volatile("bar.sync 3, 256;" ::: "memory");
-        if (tmem_slot[1]) {
-          __threadfence();
-          for (int ci = eg; ci < nch; ci += 2) {
-            const int c = ci * 32;
-            const int jmax = min(32, n_tile - c);
-            for (int jj = quad; jj < jmax; jj += 4) {
-              float4* src = reinterpret_cast<float4*>(rslot + (long)(c + jj) * BM + hoff) + lane;
-              *reinterpret_cast<float4*>(stage_buf + jj * 128 + 4 * lane) = __ldcg(src);
-              __stcg(src, make_float4(0.f, 0.f, 0.f, 0.f));
-            }
-            asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
-            const int jv = min(jmax, epi.m_tokens - tok0 - c);
-            write_chunk<KIND>(epi, m0 + hoff + 4 * lane, tok0 + c, quad, jv, stage_buf + 4 * lane);
-            asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
-          }
-          if (leader) counters[REDX_CNT + gf] = 0;
-        }
-      } else if (split) {
+      if (split) {
         __threadfence();
         asm volatile("bar.sync 3, 256;" ::: "memory");
         if (leader) atomicAdd(&counters[2 * gf], 1);
@@ -523,9 +391,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int t = t_first; t <= t_last; ++t) {
       const long long tb = (long long)t * sk.KB;
       const int gf = sk.cta_of(tb), gl = sk.cta_of(tb + sk.KB - 1);
-      if (gf == gl || (KIND == EPI_RESID && sk.red) ||
-          (KIND != EPI_RESID && KIND != EPI_QKV_ROPE && epi.red_scratch != nullptr))
-        continue;
+      if (gf == gl || (KIND == EPI_RESID && sk.red)) continue;
       const int nseg = gl - gf + 1, p = g - gf;
       if (leader) {
         volatile int* cnt = counters + 2 * gf;
@@ -573,14 +439,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
-  if (sk.mc > 1) cluster_sync_all();   // peers' last commits / multicasts target this CTA's smem
-  if constexpr (KIND == EPI_RESID) {
-    if (epi.norm_gamma != nullptr) {     // every residual update of every CTA lands, then the norm
-      __threadfence();
-      grid_barrier(counters + NORM_BAR, counters + NORM_BAR + 1, sk.G);
-      fused_norm_rows(epi, g, sk.G, stage_all);   // epilogue staging tile: free by now
-    }
-  }
   if (threadIdx.x == 0) DBG(7);
 }
 
@@ -591,14 +449,11 @@ unsigned long long* debug_buffer() { return h_dbg; }
 int g_coop = 1;
 int g_pdl = 1;
 
-int g_deterministic = 0;  // tuning key 13: 1 = RESID split-K partials through the ordered fix-up
 int g_pair = 160;         // tuning key 10: CTA-pair stream-K GEMM (multi-wave) when the token tile >= this (0 = off)
 int g_unsplit_min = 64;   // tuning key 9: tile count from which each tile gets its own CTA (no split-K)
 int g_wide = 1;   // tuning key 7: 0 auto, 1 never use 256-row tiles (default: measured slower), 2 always
-int g_mc = 1;     // tuning key 16: cluster size of the one-tile-per-CTA schedule (multicast activations)
 int g_aligned_split = 2;   // tuning key 17: tile-aligned split-K instead of stream-K when it fills >= 70% of SMs
                            // (1: split count divides the k-blocks, 2: any split count -- 140 CTAs on C3)
-int g_redx = 1;            // tuning key 19: honour epi.red_scratch (red.add split tiles + last-arriver epilogue)
 int g_dec_min_tile = 16;   // tuning key 20: smallest token tile that uses the decoupled rings
 int g_decoupled = 1;       // tuning key 18: decoupled weight / activation rings for single-k-range CTAs
                            // (1: automatic activation depth, v >= 2: v stages, v >= 10: v-10 half-k-block
@@ -639,12 +494,8 @@ int gemm_row_tile(int m_tokens) {
 // ws must hold G * 2 * BM * n_tile floats; counters 2 * G ints (zero).
 cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap,
                         int m_tokens, const GemmEpi& epi, int max_ctas, float* ws, size_t ws_bytes,
-                        int* counters, cudaStream_t stream, const RelocArgs* rl) {
+                        int* counters, cudaStream_t stream) {
   if (m_tokens <= 0) return cudaSuccess;
-  if (epi.norm_gamma != nullptr &&
-      (epi.kind != EPI_RESID || counters == nullptr || epi.n_valid % 4 != 0 || epi.n_valid > 32 * GEMM_THREADS ||
-       epi.norm_pk_rows <= 0 || epi.norm_rows > epi.m_tokens || epi.norm_rows < 0))
-    return cudaErrorInvalidValue;
   const int n_tile = gemm_row_tile(m_tokens);
   // Multi-wave GEMMs (the LM head) with token tiles >= pair_min: the CTA-pair stream-K kernel
   // (vlc_gemm_pair.cu; head at c = 236: 282 -> 258 us, profiles/r2_gemm_pair_streamk.txt).  The
@@ -655,12 +506,7 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   const int pair_min = g_pair < 0 ? -g_pair : g_pair;
   const long long tiles128 = (long long)(n_pad / 128) * ((m_tokens + n_tile - 1) / n_tile);
   if (g_pair != 0 && n_tile >= pair_min && (g_pair < 0 || tiles128 >= 2LL * num_sms()) &&
-      !(epi.kind == EPI_RESID && g_deterministic) && epi.norm_gamma == nullptr && epi.red_scratch == nullptr) {
-    if (rl && rl->n_blocks > 0) {                      // the pair kernel has no spare CTAs
-      const cudaError_t e = launch_relocate(*rl, stream);
-      if (e != cudaSuccess) return e;
-      rl = nullptr;
-    }
+      !(epi.kind == EPI_RESID && epi.deterministic)) {
     const cudaError_t e = launch_gemm_pair(W, n_pad, k_pad, X, x_rows_cap, m_tokens, epi,
                                            max_ctas > 0 ? max_ctas / 2 : 0, ws, ws_bytes, counters, stream);
     if (e != cudaErrorNotSupported) return e;
@@ -678,16 +524,10 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   // automatic schedule: enough weight tiles -> one CTA per tile (no split-K fixup); few tiles
   // (the d x d projections) -> stream-K over every SM
   const long long tiles = (long long)m_tiles * tok_tiles;
-  // red mode (epi.red_scratch): split tiles need no fix-up wait, so one-wave projections keep
-  // stream-K over every SM instead of one CTA per tile
-  const bool redx_ok = epi.red_scratch != nullptr && epi.kind != EPI_RESID && epi.kind != EPI_QKV_ROPE &&
-                       !g_deterministic && g_redx && H == 1 && counters != nullptr;
-  GemmEpi ep = epi;                       // what the kernel sees: red mode only where usable
-  if (!redx_ok) ep.red_scratch = nullptr;
-  if (max_ctas == 0 && tiles >= g_unsplit_min && tiles <= G && !redx_ok) G = (int)tiles;
+  if (max_ctas == 0 && tiles >= g_unsplit_min && tiles <= G) G = (int)tiles;
   // split tiles reduce through the workspace with <= 8 participants, except RESID (red.add into
   // the residual, any number of participants; >= 2 k-blocks per CTA)
-  const bool red = epi.kind == EPI_RESID && !g_deterministic;
+  const bool red = epi.kind == EPI_RESID && !epi.deterministic;
   const int min_units = red ? 2 : (KB + 5) / 6;
   // Tile-aligned split-K when it keeps >= 70% of the SMs: every CTA then owns exactly one k-range
   // of one tile (one epilogue, no CTA waiting on a second tile's partial) -- measured on the C3
@@ -709,19 +549,14 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
     else return cudaErrorInvalidValue;
   }
   const int stages = gemm_pick_stages(n_tile, H);
-  // cluster multicast of the activation blocks: one tile per CTA, all CTAs on one token tile
-  int mc = 1;
-  if (g_mc > 1 && H == 1 && tok_tiles == 1 && G == (int)tiles && tiles * KB == U && m_tiles % g_mc == 0 &&
-      !(rl && rl->n_blocks > 0) && KB >= g_mc)
-    mc = g_mc;
-  SkSched sk{U, G, KB, m_tiles, red ? 1 : 0, h_dbg, mc, 0, 0, 0};
+  SkSched sk{U, G, KB, m_tiles, red ? 1 : 0, h_dbg, 0, 0, 0};
   // decoupled weight / activation rings for the one-tile-per-CTA schedule: the weight ring
   // (HBM-latency bound) gets every byte the activation ring (L2, 2 stages) leaves
   // (measured: QKV / gate-up at c = 236: 31.5 / 32.0 -> 29.9 / 29.6 us; slower at c = 112, where the
   // coupled ring already holds 3 stages -> only for token tiles >= 160)
   // (also for tile-aligned split-K: G a multiple of the tile count -> one k-range of one tile per CTA)
-  if (g_decoupled && H == 1 && mc == 1 && n_tile >= g_dec_min_tile && G >= (int)tiles && G % (int)tiles == 0 &&
-      tiles * KB == U && U / G >= 2 && !(rl && rl->n_blocks > 0)) {
+  if (g_decoupled && H == 1 && n_tile >= g_dec_min_tile && G >= (int)tiles && G % (int)tiles == 0 &&
+      tiles * KB == U && U / G >= 2) {
     const int a_b = GEMM_BM * GEMM_BK * 2, b_b = n_tile * GEMM_BK * 2;
     const int budget = 232448 - 1024 - 512;
     // key 18 value v: v in [2, 9] activation k-block stages; v >= 10: (v - 10) half-k-block stages
@@ -740,19 +575,7 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
                              : gemm_smem_bytes(n_tile, stages, H);
   const uint8_t* wpp = reinterpret_cast<const uint8_t*>(W);
   const uint8_t* xpp = reinterpret_cast<const uint8_t*>(X);
-  RelocArgs rla{};
-  int grid = G;
-  if (rl && rl->n_blocks > 0) {       // relocation CTAs on the SMs this GEMM leaves idle
-    rla = *rl;
-    const int extra = num_sms() - G;
-    if (extra <= 0) {
-      cudaError_t e = launch_relocate(rla, stream);
-      if (e != cudaSuccess) return e;
-      rla.n_blocks = 0;
-    } else {
-      grid = G + extra;
-    }
-  }
+  const int grid = G;
 #define VLC_GEMM_KIND(K)                                                                              \
   case K: {                                                                                           \
     static bool attr = false;                                                                         \
@@ -761,14 +584,11 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
       cudaFuncSetAttribute(gemm_bf16_tc<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);  \
       attr = true;                                                                                    \
     }                                                                                                 \
-    if (mc > 1)                                                                                       \
-      return launch_chain_cluster(gemm_bf16_tc<K, 1>, dim3(grid), dim3(GEMM_THREADS), smem, stream, mc, wpp, \
-                                  xpp, ep, sk, n_tile, stages, ws, counters, rla);                    \
     if (H == 2)                                                                                       \
       return launch_chain(gemm_bf16_tc<K, 2>, dim3(grid), dim3(GEMM_THREADS), smem, stream, g_coop != 0, wpp,    \
-                          xpp, ep, sk, n_tile, stages, ws, counters, rla);                            \
+                          xpp, epi, sk, n_tile, stages, ws, counters);                            \
     return launch_chain(gemm_bf16_tc<K, 1>, dim3(grid), dim3(GEMM_THREADS), smem, stream, g_coop != 0, wpp, xpp, \
-                        ep, sk, n_tile, stages, ws, counters, rla);                                   \
+                        epi, sk, n_tile, stages, ws, counters);                                   \
   }
   switch (epi.kind) {
     VLC_GEMM_KIND(EPI_F32)

@@ -316,7 +316,6 @@ cudaError_t launch_gemm_pair(const void* W, int n_pad, int k_pad, const void* X,
                              cudaStream_t stream) {
   const int n_tile = gemm_row_tile(m_tokens);
   if (n_pad % 256 || k_pad % 128 || n_tile % 16 || n_tile < 32) return cudaErrorNotSupported;
-  if (epi.norm_gamma != nullptr || epi.red_scratch != nullptr) return cudaErrorNotSupported;
   const int tok_tiles = (m_tokens + n_tile - 1) / n_tile;
   if (x_rows_cap < tok_tiles * n_tile) return cudaErrorInvalidValue;
   const int stages = pair_stages(n_tile);

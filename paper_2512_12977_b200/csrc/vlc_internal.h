@@ -23,16 +23,12 @@ using GemmEpi = vlc_epilogue;
 
 extern int g_stage_override;  // experiment knob (vlc_set_tuning key 1)
 extern int g_coop;            // key 2: cooperative launch of the stream-K GEMM
-extern int g_deterministic;   // key 13: bitwise run-to-run reproducible RESID GEMMs (slower)
-extern int g_reloc_wide;      // key 14: idle-SM relocation variant (smem bytes requested; 0 = off)
 extern int g_pair;            // key 10: CTA-pair GEMM threshold on the token tile (0 = off)
 extern int g_unsplit_min;     // key 9: tiles >= this (and <= #SMs) -> one CTA per tile
 extern int g_wide;            // key 7: 256-row GEMM tiles (0 auto, 1 never, 2 always)
 extern int g_aligned_split;   // key 17: tile-aligned split-K for the multi-CTA-per-tile schedule
-extern int g_redx;            // key 19: red.add split-tile reduction with last-arriver epilogue
-extern int g_decoupled;
-extern int g_dec_min_tile;    // key 20: smallest token tile using the decoupled rings       // key 18: decoupled weight / activation rings in the one-tile GEMM schedule
-extern int g_mc;              // key 16: GEMM cluster size for multicast activation loads (1 = off)
+extern int g_decoupled;       // key 18: decoupled weight / activation rings in the one-tile GEMM schedule
+extern int g_dec_min_tile;    // key 20: smallest token tile using the decoupled rings
 extern int g_pdl;             // key 6: programmatic dependent launch of the chain kernels (default 1)
 void set_debug_buffer(unsigned long long* p);
 unsigned long long* debug_buffer();
@@ -62,34 +58,6 @@ cudaError_t launch_chain(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t s
   cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
-// launch_chain with a thread-block cluster of `cluster` CTAs along x (PDL as above; no cooperative
-// attribute: clustered kernels do not rely on grid-wide co-residency)
-template <typename... KArgs, typename... Args>
-cudaError_t launch_chain_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                                 int cluster, Args&&... args) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[2];
-  int n = 0;
-  if (g_pdl) {
-    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[n].val.programmaticStreamSerializationAllowed = 1;
-    ++n;
-  }
-  at[n].id = cudaLaunchAttributeClusterDimension;
-  at[n].val.clusterDim.x = cluster;
-  at[n].val.clusterDim.y = 1;
-  at[n].val.clusterDim.z = 1;
-  ++n;
-  cfg.attrs = at;
-  cfg.numAttrs = n;
-  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
-}
-void set_attn_debug_buffer(unsigned long long* p);
-void set_attn_trace_buffer(unsigned long long* p);
 
 
 // tensor maps (driver entry point resolved through the runtime, no -lcuda)
@@ -107,7 +75,7 @@ struct RelocArgs;   // vlc_reloc.cuh
 cudaError_t launch_relocate(const RelocArgs& r, cudaStream_t stream);
 cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap,
                         int m_tokens, const GemmEpi& epi, int max_ctas, float* ws, size_t ws_bytes,
-                        int* counters, cudaStream_t stream, const RelocArgs* rl = nullptr);
+                        int* counters, cudaStream_t stream);
 int gemm_row_tile(int m_tokens);
 cudaError_t launch_gemm_pair(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap, int m_tokens,
                              const GemmEpi& epi, int max_pairs, float* ws, size_t ws_bytes, int* counters,

@@ -143,27 +143,8 @@ __global__ void __launch_bounds__(RELOC_THREADS) kv_relocate_kernel(RelocArgs r)
   relocate_block(r, blockIdx.x, threadIdx.x);
 }
 
-// "Idle-SM" variant (g_reloc_wide): 4 blocks per 1024-thread CTA with a large (unused) shared
-// memory request, so that relocation CTAs never co-reside with a GEMM / attention CTA (whose L1 /
-// shared-memory bandwidth they would steal) and instead fill the SMs a projection leaves idle.
-__global__ void __launch_bounds__(4 * RELOC_THREADS) kv_relocate_wide_kernel(RelocArgs r) {
-  const int b = blockIdx.x * 4 + (threadIdx.x / RELOC_THREADS);
-  if (b < r.n_blocks) relocate_block(r, b, threadIdx.x % RELOC_THREADS);
-}
-
-int g_reloc_wide = 0;   // tuning key 14: shared memory bytes requested by the idle-SM variant (0 = off)
-
 cudaError_t launch_relocate(const RelocArgs& r, cudaStream_t stream) {
   if (r.n_blocks <= 0) return cudaSuccess;
-  if (g_reloc_wide > 0) {
-    static int attr = 0;
-    if (attr != g_reloc_wide) {
-      cudaFuncSetAttribute(kv_relocate_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, g_reloc_wide);
-      attr = g_reloc_wide;
-    }
-    kv_relocate_wide_kernel<<<(r.n_blocks + 3) / 4, 4 * RELOC_THREADS, g_reloc_wide, stream>>>(r);
-    return cudaGetLastError();
-  }
   return launch_chain(kv_relocate_kernel, dim3(r.n_blocks), dim3(RELOC_THREADS), 0, stream, false, r);
 }
 

@@ -1,7 +1,6 @@
 // Gather + RoPE re-rotation + scatter of cached pre-RoPE K and copy of V (engine.py:153-155 +
-// engine.py:180), one RELOC_TOK-token block of one (layer, image) descriptor per call.  Shared by
-// the standalone kv_relocate kernel (vlc_misc.cu) and the QKV GEMM, whose otherwise idle CTAs
-// relocate the same layer's cached KV while the projection runs (vlc_gemm.cu).
+// engine.py:180), one RELOC_TOK-token block of one (layer, image) descriptor per call, for the
+// kv_relocate kernel (vlc_misc.cu).
 #pragma once
 #include "vlc_internal.h"
 

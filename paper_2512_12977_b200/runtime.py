@@ -18,12 +18,6 @@ from .model import RMS_EPS, DeviceWeights
 
 N_SMS = 148
 _DEBUG_SYNC = bool(int(__import__("os").environ.get("VLC_DEBUG_SYNC", "0")))  # sync + log every launch
-_OVERLAP_RELOC = bool(int(__import__("os").environ.get("VLC_RELOC_OVERLAP", "1")))
-_FUSE_RELOC = bool(int(__import__("os").environ.get("VLC_RELOC_FUSED", "0")))
-# RMSNorm fused into the preceding residual projection's tail (vlc_epilogue.norm_*): one launch
-# per norm less (VLC_FUSED_NORM=1; measured neutral on C3: the norm stays on the critical path
-# either way, so the separate vlc_rmsnorm launches are the default)
-_FUSED_NORM = bool(int(__import__("os").environ.get("VLC_FUSED_NORM", "0")))
 
 
 def _torch():
@@ -186,9 +180,10 @@ class Runner:
         self.shared = Workspace()    # per-call scratch (split-K partials, counters, attention merge)
         self.enc_ws = Workspace()
         self.lib = N.load()
-        # VLC_DETERMINISTIC=1: split-K partials of the residual GEMMs reduced in a fixed order
-        # (bitwise reproducible runs) instead of red.add in arrival order (faster)
-        self.lib.vlc_set_tuning(13, int(__import__("os").environ.get("VLC_DETERMINISTIC", "0")))
+        # deterministic: split-K partials of the residual GEMMs reduced in a fixed order (bitwise
+        # reproducible runs; per call through vlc_epilogue.deterministic) instead of red.add in
+        # arrival order (faster).
+        self.deterministic = False
         torch = _torch()
         self.splitk = self.shared.get("splitk", (64 << 20,), torch.float32, zero=False)
         self.counters = self.shared.get("counters", (1 << 16,), torch.int32)
@@ -198,22 +193,7 @@ class Runner:
         self.layouts: dict = {}    # structure key -> Layout (engine._layout)
         self.graph_launches: dict = {}
         self.tracer = None         # list -> (name, ev0, ev1, algo_bytes, algo_flops) per launch
-        self.overlap_reloc = _OVERLAP_RELOC
-        self.fuse_reloc = _FUSE_RELOC    # relocate layer i's cached KV inside its QKV GEMM launch
-        # The cached-KV relocation runs on a low-priority side stream as 1024-thread CTAs that request
-        # ~100 KB of shared memory, so they cannot co-reside with GEMM / attention CTAs (whose L1 /
-        # shared-memory bandwidth they would steal) and fill the SMs a projection leaves idle; the
-        # layer chain is captured at high priority so its CTAs win the SMs that free up.
-        # Measured on C3: 5.58 -> 5.24 ms TTFT (tools: VLC_HI_PRIO / VLC_RELOC_WIDE A/B, run42).
-        self.hi_prio = bool(int(__import__("os").environ.get("VLC_HI_PRIO", "1")))
-        self.lib.vlc_set_tuning(14, int(__import__("os").environ.get("VLC_RELOC_WIDE", "100000")))
-        # experiments: VLC_TUNING="key=value,..." applied last (vlc_set_tuning)
-        for kv_ in __import__("os").environ.get("VLC_TUNING", "").split(","):
-            if "=" in kv_:
-                k_, v_ = kv_.split("=", 1)
-                self.lib.vlc_set_tuning(int(k_), int(v_))
         self.tp_group = None       # head-parallel process group (engine sets it from the model)
-        self._side = None          # side stream of the overlapped kv_relocate
         # Concurrent callers: the workspaces, split-K scratch and counters belong to
         # the runner, so calls are serialised -- on the host by the lock, on the device by making
         # each call's stream wait for the previous call's completion event.
@@ -259,29 +239,22 @@ class Runner:
         self.launches += kernels
 
     # ---------------------------------------------------------------- primitives
-    def gemm(self, w, k_pad, x, m, epi: N.Epilogue, splits: int | None = None, name="gemm", k_valid=None,
-             reloc=None):
-        """w: PackedWeight; x: packed activations (row tile N.row_tile(m)), flat bf16 tensor.
-        reloc: vlc_kv_relocate arguments (after `kv`... see vlc_gemm_bf16_relocate) to run on the
-        CTAs this GEMM leaves idle."""
+    def gemm(self, w, k_pad, x, m, epi: N.Epilogue, splits: int | None = None, name="gemm", k_valid=None):
+        """w: PackedWeight; x: packed activations (row tile N.row_tile(m)), flat bf16 tensor."""
         if m <= 0:
             return
         if splits is None:
             splits = 0                       # stream-K over all SMs
         epi.m_tokens = m
+        if epi.kind == N.EPI_RESID and self.deterministic:
+            epi.deterministic = 1
         R = N.row_tile(m)
         kv_ = k_valid or k_pad
         nbytes = 2 * epi.n_valid * kv_ + 2 * m * kv_
-        if reloc is None:
-            self._run(name, lambda: N.check(self.lib.vlc_gemm_bf16(
-                w.data_ptr(), w.n, w.k, x.data_ptr(), -(-m // R) * R, m, epi, splits, self.splitk.data_ptr(),
-                self.splitk.numel() * 4, self.counters.data_ptr(), _stream()), "vlc_gemm_bf16"),
-                nbytes, 2 * m * epi.n_valid * kv_)
-        else:
-            self._run(name, lambda: N.check(self.lib.vlc_gemm_bf16_relocate(
-                w.data_ptr(), w.n, w.k, x.data_ptr(), -(-m // R) * R, m, epi, splits, self.splitk.data_ptr(),
-                self.splitk.numel() * 4, self.counters.data_ptr(), *reloc, _stream()), "vlc_gemm_bf16_relocate"),
-                nbytes, 2 * m * epi.n_valid * kv_)
+        self._run(name, lambda: N.check(self.lib.vlc_gemm_bf16(
+            w.data_ptr(), w.n, w.k, x.data_ptr(), -(-m // R) * R, m, epi, splits, self.splitk.data_ptr(),
+            self.splitk.numel() * 4, self.counters.data_ptr(), _stream()), "vlc_gemm_bf16"),
+            nbytes, 2 * m * epi.n_valid * kv_)
 
     def rmsnorm(self, x, gamma, out, rows, out_f32=False, row_map=0, pk=(0, 0)):
         """out: fp32 row-major [rows, ld] (out_f32) or flat packed bf16 with geometry pk=(R, KB)."""
@@ -471,22 +444,20 @@ class Runner:
             skey = getattr(lay, "_skey", None)
             if skey is None:
                 skey = lay._skey = lay.structure_key()
-            key = (skey, ptrs)
+            key = (skey, ptrs, self.deterministic)
             g = self.graphs.get(key)
             if g is None:
                 chain()                                   # eager run serves this call
                 g = torch.cuda.CUDAGraph()
-                # the layer chain is captured at high priority, the side-stream relocation at the
-                # default (lowest) one: when SMs free up, chain CTAs are dispatched first
-                side = torch.cuda.Stream(priority=-1 if self.hi_prio else 0)
-                side.wait_stream(torch.cuda.current_stream())
-                with torch.cuda.stream(side):
-                    with torch.cuda.graph(g, stream=side):
+                cap = torch.cuda.Stream()           # captured off the caller's stream
+                cap.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(cap):
+                    with torch.cuda.graph(g, stream=cap):
                         launches = self.launches
                         chain()
                         self.graph_launches[key] = self.launches - launches
                         self.launches = launches
-                torch.cuda.current_stream().wait_stream(side)
+                torch.cuda.current_stream().wait_stream(cap)
                 if len(self.graphs) >= 16:
                     self.graphs.pop(next(iter(self.graphs)))
                 self.graphs[key] = g
@@ -560,73 +531,31 @@ class Runner:
         enc_a, enc_b, kpool, vpool, P = ptrs[:5]
         kv_pool_obj = buf.get("kv_pool")
         s = _stream()
+        kd = dw.kd // 128
         # layer-0 rows: text embeddings + cached / freshly encoded image rows
         self._run("embed", lambda: N.check(self.lib.vlc_embed_assemble(
             x.data_ptr(), d, dw.embed.data_ptr(), d, enc_a, enc_b, pack.ptr("src"), c0, s), "vlc_embed_assemble"),
             c0 * d * 6)
-        # cached K/V of every reused image token, re-rotated to the new positions.  The relocation
-        # is a pure HBM stream while the layer GEMMs are latency-bound, so by default it runs per
-        # layer on a side stream, overlapped with the layer chain; attention i waits for layer i.
+        # cached K/V rows that share a 64-key chunk with recomputed ones when the store's page size
+        # does not allow reading them in place (attention reads every other cached chunk from the store)
         nb = len(lay.reloc_blocks)
-        side_ev = None
-
-        def relocate(b0, n_b):
+        if nb:
             self._run("kv_relocate", lambda: N.check(self.lib.vlc_kv_relocate(
                 kpool, vpool, P, pack.ptr("pages"), kv, cfg.head_dim, kc.data_ptr(), vc.data_ptr(), kc.shape[1],
-                pack.ptr("descs"), pack.ptr("blocks") + 8 * b0, n_b, dw.cos.data_ptr(), dw.sin.data_ptr(),
-                cfg.head_dim // 2, _stream()), "vlc_kv_relocate"), lay.reloc_tokens * kv * 2 * 4 * n_b // nb)
+                pack.ptr("descs"), pack.ptr("blocks"), nb, dw.cos.data_ptr(), dw.sin.data_ptr(),
+                cfg.head_dim // 2, _stream()), "vlc_kv_relocate"), lay.reloc_tokens * kv * 2 * 4)
 
-        lb = lay.reloc_layer_blocks
-        fused_reloc = bool(nb) and self.fuse_reloc and "inject" not in buf
-
-        def reloc_args(i):
-            """Layer i's relocation, run by the QKV GEMM's spare CTAs (vlc_gemm_bf16_relocate)."""
-            if not fused_reloc or lb[i + 1] <= lb[i]:
-                return None
-            return (kpool, vpool, P, pack.ptr("pages"), kv, cfg.head_dim, kc.data_ptr(), vc.data_ptr(), kc.shape[1],
-                    pack.ptr("descs"), pack.ptr("blocks") + 8 * int(lb[i]), int(lb[i + 1] - lb[i]), dw.cos.data_ptr(),
-                    dw.sin.data_ptr(), cfg.head_dim // 2)
-        if fused_reloc:
-            pass
-        elif nb and self.overlap_reloc:
-            torch = _torch()
-            main = torch.cuda.current_stream()
-            if self._side is None:
-                self._side = torch.cuda.Stream()
-            side = self._side
-            side.wait_stream(main)
-            side_ev = []
-            lb = lay.reloc_layer_blocks
-            with torch.cuda.stream(side):
-                for i in range(L):
-                    if lb[i + 1] > lb[i]:
-                        relocate(int(lb[i]), int(lb[i + 1] - lb[i]))
-                    ev = torch.cuda.Event()
-                    ev.record(side)
-                    side_ev.append(ev)
-        elif nb:
-            relocate(0, nb)
-        fuse_norm = _FUSED_NORM
-
-        def norm_kw(gamma, rows):
-            """RESID epilogue fields: RMSNorm of the first `rows` residual rows fused into the GEMM."""
-            if not fuse_norm or rows <= 0:
-                return {}
-            return dict(norm_gamma=gamma.data_ptr(), norm_out=xn.data_ptr(), norm_eps=RMS_EPS, norm_rows=rows,
-                        norm_pk_rows=N.row_tile(rows), norm_pk_kb=dw.kd // 128)
-        normed = False                     # xn already holds this layer's attn-normed rows
         for i in range(L):
             ci = int(c[i])
             W = dw.layers[i]
             Ri = N.row_tile(ci)
-            if not normed:
-                self.rmsnorm(x, W["attn_norm"], xn, ci, pk=(Ri, dw.kd // 128))
+            self.rmsnorm(x, W["attn_norm"], xn, ci, pk=(Ri, kd))
             self.gemm(W["wqkv"], dw.kd, xn, ci, _epi(
                 kind=N.EPI_QKV_ROPE, n_valid=3 * kv, out=q.data_ptr(), ldo=kv,
                 out2=kc[i].data_ptr(), ld2=kv, out3=vc[i].data_ptr(), ld3=kv, out4=kpre[i].data_ptr(), ld4=kv,
                 map1=pack.ptr(f"qdst{i}"), map2=pack.ptr("row_kv"), pos=pack.ptr("row_pos"),
                 cos_tab=dw.cos.data_ptr(), sin_tab=dw.sin.data_ptr(), tab_ld=cfg.head_dim // 2,
-                hd=cfg.head_dim, seg=kv), name="gemm_qkv", k_valid=d, reloc=reloc_args(i))
+                hd=cfg.head_dim, seg=kv), name="gemm_qkv", k_valid=d)
             if "inject" in buf:
                 inj, ipk = buf["inject"]
                 lb = inj["layer_blocks"]
@@ -637,8 +566,6 @@ class Runner:
                         ipk.ptr("blocks") + 8 * int(lb[i]), int(lb[i + 1] - lb[i]), dw.cos.data_ptr(),
                         dw.sin.data_ptr(), cfg.head_dim // 2, _stream()), "vlc_kv_relocate"))
             vis = int(lay.qpos[i, :ci].astype(np.int64).sum()) + ci
-            if side_ev is not None:
-                _torch().cuda.current_stream().wait_event(side_ev[i])
             self.attention(q, kc, vc, i, pack.ptr(f"chunks{i}"), pack.ptr(f"items{i}"), len(lay.attn_items[i]),
                            pack.ptr(f"qpos{i}"), pack.ptr(f"rowof{i}"), att, lay.attn_slots,
                            nbytes=lay.kv_rows * kv * 4 + ci * kv * 4, flops=4 * cfg.head_dim * dw.heads * vis,
@@ -651,13 +578,11 @@ class Runner:
                           name="gemm_o", k_valid=kv)
                 self._run("rmsnorm", lambda cap=cap, W=W: N.check(self.lib.vlc_add_rmsnorm(
                     x.data_ptr(), d, cap.data_ptr(), d, W["mlp_norm"].data_ptr(), xn.data_ptr(), d, ci, d, RMS_EPS,
-                    Ri, dw.kd // 128, _stream()), "vlc_add_rmsnorm"))
+                    Ri, kd, _stream()), "vlc_add_rmsnorm"))
             elif self.tp_group is None:
-                nk = norm_kw(W["mlp_norm"], ci)
-                self.gemm(W["wo"], dw.kkv, att, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d,
-                                                         **nk), name="gemm_o", k_valid=kv)
-                if not nk:
-                    self.rmsnorm(x, W["mlp_norm"], xn, ci, pk=(Ri, dw.kd // 128))
+                self.gemm(W["wo"], dw.kkv, att, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d),
+                          name="gemm_o", k_valid=kv)
+                self.rmsnorm(x, W["mlp_norm"], xn, ci, pk=(Ri, kd))
             else:
                 # head-parallel: row-parallel O projection of this rank's heads -> y, one all-reduce
                 # of y over the group (NCCL / NVLink), then x += y fused into the MLP norm
@@ -668,19 +593,14 @@ class Runner:
                 self._allreduce(y[:ci])
                 self._run("rmsnorm", lambda: N.check(self.lib.vlc_add_rmsnorm(
                     x.data_ptr(), d, y.data_ptr(), d, W["mlp_norm"].data_ptr(), xn.data_ptr(), d, ci, d, RMS_EPS,
-                    Ri, dw.kd // 128, _stream()), "vlc_add_rmsnorm"), ci * d * 14)
+                    Ri, kd, _stream()), "vlc_add_rmsnorm"), ci * d * 14)
             self.gemm(W["wgu"], dw.kd, xn, ci,
                       _epi(kind=N.EPI_SWIGLU, n_valid=2 * cfg.mlp_hidden, out=hb.data_ptr(), ldo=dw.kh,
                            pk_rows=Ri, pk_kb=dw.kh // 128),
                       name="gemm_gate_up", k_valid=d)
-            # the next layer's attention norm rides on this projection (its rows: the first c[i+1])
-            nk = norm_kw(dw.layers[i + 1]["attn_norm"], int(c[i + 1])) if i + 1 < L else {}
-            self.gemm(W["wd"], dw.kh, hb, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d, **nk),
+            self.gemm(W["wd"], dw.kh, hb, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d),
                       name="gemm_down", k_valid=cfg.mlp_hidden)
-            normed = bool(nk)
-        if side_ev is not None:
-            _torch().cuda.current_stream().wait_stream(self._side)
-        self.rmsnorm(x, dw.final_norm, xn, cL, row_map=pack.ptr("final"), pk=(N.row_tile(cL), dw.kd // 128))
+        self.rmsnorm(x, dw.final_norm, xn, cL, row_map=pack.ptr("final"), pk=(N.row_tile(cL), kd))
         self.gemm(dw.head, dw.kd, xn, cL, _epi(kind=N.EPI_F32, n_valid=V, out=logits.data_ptr(), ldo=V),
                   name="gemm_head", k_valid=d)
 

@@ -1,7 +1,7 @@
 """Concurrent callers ("Multiple calls may run concurrently against one immutable
 model and one store"): host threads issuing prefill_with_reuse on one model, each on its own CUDA
 stream, get exactly the results of the same calls made one after another.  The run uses the
-deterministic split-K reduction (vlc_set_tuning(13, 1)): without it, red.add arrival order makes
+deterministic split-K reduction (Runner.deterministic): without it, red.add arrival order makes
 runs differ at bf16-rounding scale, which would hide a real race."""
 import threading
 
@@ -22,7 +22,7 @@ def test_two_threads_match_serial_results(cuda_ok):
     sc = Scene(P, "C1", 2, export=False)
     L = sc.cfg.num_layers
     runner = _runner(sc.model)
-    N.load().vlc_set_tuning(13, 1)
+    runner.deterministic = True
     runner.graphs.clear()
     plans = [P.plan_static(0.05, L), P.RecomputePlan((0.3, 0.2, 0.1, 0.0)), P.plan_static(0.0, L),
              P.RecomputePlan((1.0, 0.1, 0.1, 0.0))]
@@ -48,7 +48,7 @@ def test_two_threads_match_serial_results(cuda_ok):
         for t in th:
             t.join()
     finally:
-        N.load().vlc_set_tuning(13, 0)
+        runner.deterministic = False
         runner.graphs.clear()
     assert not errors, errors
     for (tid, rep), (k, lg, last) in out.items():

@@ -121,19 +121,17 @@ def test_c3_page_placement_invariance(c3):
 
 @pytest.mark.timeout(900)
 def test_c3_deterministic_mode_is_bitwise_reproducible(c3):
-    """vlc_set_tuning(13, 1) (env VLC_DETERMINISTIC=1): residual split-K partials reduced in a fixed
-    order -> two runs (and two page placements) give identical logits."""
-    from paper_2512_12977_b200 import _native as N
+    """Runner.deterministic (vlc_epilogue.deterministic): residual split-K partials reduced in a
+    fixed order -> two runs (and two page placements) give identical logits."""
     P, cfg, model, imgs, store = c3
     req = _req(P, cfg, imgs, 12, 0.05)
-    lib = N.load()
-    lib.vlc_set_tuning(13, 1)
+    model._runner.deterministic = True
     try:
         model._runner.graphs.clear()          # re-capture with the deterministic kernels
         a = P.prefill_with_reuse(model, req, store).logits
         b = P.prefill_with_reuse(model, req, store).logits
         c = P.prefill_with_reuse(model, req, store).logits
     finally:
-        lib.vlc_set_tuning(13, 0)
+        model._runner.deterministic = False
         model._runner.graphs.clear()
     assert np.array_equal(a, b) and np.array_equal(b, c)

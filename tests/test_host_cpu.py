@@ -415,3 +415,32 @@ def test_reuse_result_is_freed_without_gc():
         assert ref() is None
     finally:
         gc.enable()
+
+
+def test_query_tiles_minimise_scanned_key_tiles():
+    """layout.query_tiles: exact minimum of sum(key tiles of each tile's last query) + 1 per tile
+    over every cut into <= rows-row tiles (brute force on small cases); C3 at 5% cuts at the gap
+    before image 2 instead of at row 128 (45 instead of 53 key tiles per head)."""
+    import itertools
+
+    import numpy as np
+    from paper_2512_12977_b200.layout import query_tiles
+    rng = np.random.default_rng(5)
+    for _ in range(40):
+        n, rows = int(rng.integers(1, 11)), int(rng.integers(1, 5))
+        pos = np.sort(rng.choice(200, n, replace=False))
+        tiles = lambda p: p // 16 + 1          # noqa: E731
+        got = query_tiles(pos, tiles, rows=rows)
+        assert got[0][0] == 0 and got[-1][1] == n and all(b - a <= rows for a, b in got)
+        assert all(x[1] == y[0] for x, y in zip(got, got[1:]))
+        best = min(sum(tiles(pos[b - 1]) + 1 for a, b in zip((0,) + c, c + (n,)))
+                   for k in range(n) for c in itertools.combinations(range(1, n), k)
+                   if all(b - a <= rows for a, b in zip((0,) + c, c + (n,))))
+        assert sum(tiles(pos[b - 1]) + 1 for a, b in got) == best
+    # C3: 16 text + 4 images x 51 leading tokens (+ their store / request split chunk) + 16 text
+    pos = np.concatenate([np.arange(16), 16 + np.arange(51), 1040 + np.arange(51), 2064 + np.arange(51),
+                          3088 + np.arange(51), 4112 + np.arange(16)])
+    tiles = lambda p: -(-(p // 64 + 1 + (p > 66) + (p > 1090) + (p > 2114) + (p > 3138)) // 2)   # noqa: E731
+    got = query_tiles(pos, tiles)
+    assert sum(tiles(pos[b - 1]) for a, b in got) == 44 and len(got) == 2
+    assert tiles(pos[127]) + tiles(pos[-1]) == 53

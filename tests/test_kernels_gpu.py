@@ -298,36 +298,6 @@ def test_attention_paged_store_page_size_128(nat):
     assert (out[keep["rowof"].long()].float() - ref).abs().max().item() < 2e-2
 
 
-@pytest.mark.parametrize("n_pad,k_pad,m,splits", [(10752, 3584, 236, 0), (14336, 3584, 236, 0), (1024, 512, 100, 0),
-                                                  (384, 512, 100, 3), (1280, 768, 600, 7)])
-def test_gemm_red_scratch_f32_swiglu(nat, n_pad, k_pad, m, splits):
-    """epi.red_scratch: split tiles reduced by red.add into a zero-maintained scratch, finished by the
-    last-arriving CTA (fp32 logits-style and packed SwiGLU outputs); the scratch is left zero."""
-    g = torch.Generator(device="cuda").manual_seed(n_pad + 7 * m)
-    W = torch.randn(n_pad, k_pad, device="cuda", generator=g).bfloat16()
-    X = torch.randn(max(256, m), k_pad, device="cuda", generator=g).bfloat16()
-    scratch = torch.zeros(148 * 128 * 256, device="cuda")
-    out = torch.full((m, n_pad), float("nan"), device="cuda")
-    epi = _epi(nat, kind=nat.EPI_F32, n_valid=n_pad, m_tokens=m, out=out.data_ptr(), ldo=n_pad,
-               red_scratch=scratch.data_ptr())
-    for _ in range(2):   # twice: scratch and counters must be left clean
-        _gemm(nat, W, X, m, epi, splits)
-        ref = X[:m].float() @ W.float().t()
-        assert (out - ref).abs().max().item() / ref.abs().max().item() < 1e-5
-    assert scratch.abs().sum().item() == 0
-    R = nat.row_tile(m)
-    hp = torch.zeros(nat.packed_numel(m, n_pad // 2, R), device="cuda", dtype=torch.bfloat16)
-    sw = _epi(nat, kind=nat.EPI_SWIGLU, n_valid=n_pad, m_tokens=m, out=hp.data_ptr(), ldo=n_pad // 2, pk_rows=R,
-              pk_kb=-(-(n_pad // 2) // 128), red_scratch=scratch.data_ptr())
-    _gemm(nat, W, X, m, sw, splits)
-    acc = X[:m].float() @ W.float().t()
-    gate, up = acc[:, 0::2], acc[:, 1::2]
-    ref = (torch.nn.functional.silu(gate) * up)
-    got = nat.unpack(hp, m, n_pad // 2, R).float()
-    assert (got - ref).abs().max().item() / ref.abs().max().item() < 2e-2
-    assert scratch.abs().sum().item() == 0
-
-
 @pytest.mark.parametrize("dec", [0, 1, 3, 12])
 @pytest.mark.parametrize("n_pad,k_pad,m", [(10752, 3584, 236), (14336, 3584, 112), (3584, 7168, 236), (3584, 3584, 112)])
 def test_gemm_decoupled_rings_and_aligned_split(nat, dec, n_pad, k_pad, m):
@@ -350,17 +320,6 @@ def test_gemm_decoupled_rings_and_aligned_split(nat, dec, n_pad, k_pad, m):
     finally:
         lib.vlc_set_tuning(18, 1)
         lib.vlc_set_tuning(20, 16)
-
-
-@pytest.mark.parametrize("mc", [2, 4])
-@pytest.mark.parametrize("n_pad,k_pad,m", [(10752, 3584, 236), (1024, 512, 100), (512, 1024, 40)])
-def test_gemm_cluster_multicast(nat, mc, n_pad, k_pad, m):
-    """Tuning key 16: clusters of mc CTAs share each activation k-block through one multicast copy."""
-    nat.load().vlc_set_tuning(16, mc)
-    try:
-        test_gemm_f32_matches_torch(nat, n_pad, k_pad, m, 0)
-    finally:
-        nat.load().vlc_set_tuning(16, 1)
 
 
 @pytest.fixture

@@ -1,0 +1,72 @@
+"""A/B of chain variants on the C3 bench request (same process, same weights / store): p50 device
+TTFT per variant, alternating rounds.  Variants are Runner attributes: defer_norm (deferred RMSNorm)
+and env-free schedule toggles passed as NAME=attr:value,... on the command line.
+
+  python tools/ab_ttft.py base= nonorm=defer_norm:0
+"""
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2512_12977_b200 as P  # noqa: E402
+from paper_2512_12977_b200.engine import _runner, prefill_with_reuse  # noqa: E402
+from paper_2512_12977_b200.toydata import make_images, prompt_ids  # noqa: E402
+
+wl = bench.WORKLOADS[os.environ.get("WL", "C3")]
+cfg = P.ModelConfig(**bench.CONFIGS[wl["cfg"]], seed=0)
+T, V, L = cfg.tokens_per_image, cfg.vocab_size, cfg.num_layers
+model = P.ToyVLM.device_random(cfg, seed=0)
+runner = _runner(model)
+store = P.CacheStore()
+images = make_images(wl["images"], cfg.image_side, 1)
+P.fill_store(model, store, images, prompt_ids(V, 8, 11))
+text = prompt_ids(V, 32, 12)
+seq = P.make_sequence(text[:16], wl["images"], T, text[16:])
+hashes = [P.hash_image(px) for px in images]
+ratio = float(os.environ.get("RATIO", wl["ratio"]))
+req = P.ReuseRequest(seq, hashes, P.plan_static(ratio, L))
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+variants = {}
+for a in sys.argv[1:]:
+    name, _, spec = a.partition("=")
+    variants[name] = [(k, int(v)) for k, v in (kv.split(":") for kv in spec.split(",") if kv)]
+if not variants:
+    variants = {"base": []}
+defaults = {k: getattr(runner, k) for v in variants.values() for k, _ in v}
+
+
+def apply(v):
+    for k, val in defaults.items():
+        setattr(runner, k, val)
+    for k, val in v:
+        setattr(runner, k, bool(val) if isinstance(defaults[k], bool) else val)
+
+
+res = {n: [] for n in variants}
+last = {}
+for rnd in range(4):
+    for n, v in variants.items():
+        apply(v)
+        for _ in range(3):
+            prefill_with_reuse(model, req, store)
+        torch.cuda.synchronize()
+        for _ in range(10):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r = prefill_with_reuse(model, req, store)
+            e1.record()
+            e1.synchronize()
+            res[n].append(e0.elapsed_time(e1))
+        last[n] = r.last_logits().copy()
+base = next(iter(variants))
+for n in variants:
+    d = float(abs(last[n] - last[base]).max())
+    print(f"{n:12s} p50 {statistics.median(res[n]):.4f} ms  min {min(res[n]):.4f}  "
+          f"max|last - {base}| {d:.3e}", flush=True)

@@ -12,7 +12,6 @@ ws = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 cnt = torch.zeros(1 << 16, dtype=torch.int32, device="cuda")
 
 
-RED = torch.zeros(148 * 128 * 256, device="cuda")
 
 
 def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1, packed=False, mode=0, red=False):
@@ -24,8 +23,6 @@ def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1, packed=Fals
     out = torch.zeros(m + 256, n, device="cuda", dtype=torch.float32)
     e = N.Epilogue()
     e.kind, e.n_valid, e.m_tokens, e.out, e.ldo = kind, n, m, out.data_ptr(), n
-    if red:
-        e.red_scratch = RED.data_ptr()
     lib.vlc_set_tuning(1, stages)
     lib.vlc_set_tuning(2, coop)
     s = torch.cuda.current_stream().cuda_stream
@@ -142,16 +139,11 @@ if __name__ == "__main__":
         lib.vlc_set_tuning(7, 1)
         lib.vlc_set_tuning(9, 64)
     if mode == "head":            # LM head: CTA pair (9 waves, last one holds 2 of 594 tiles) vs stream-K
-        for pair, red in ((96, False), (0, False), (0, True), (96, False)):
+        for pair in (96, 0, 96):
             lib.vlc_set_tuning(10, pair)
-            print(f"-- pair {pair} red {red}", flush=True)
-            run(152064, 3584, 236, 0, kind=N.EPI_F32, red=red, reps=6)
+            print(f"-- pair {pair}", flush=True)
+            run(152064, 3584, 236, 0, kind=N.EPI_F32, reps=6)
         lib.vlc_set_tuning(10, 96)
-    if mode == "redx":            # one-wave projections: one CTA per tile vs stream-K with red.add split tiles
-        for red in (False, True, False, True):
-            print(f"-- red_scratch {red}", flush=True)
-            for (n, kk, m) in ((10752, 3584, 236), (14336, 3584, 236), (14336, 3584, 112), (3584, 3584, 236)):
-                run(n, kk, m, 0, red=red)
     if mode == "aligned":         # tile-aligned split-K: divisor splits (key 17 = 1) vs any split (2)
         for al in (1, 2, 1, 2):
             lib.vlc_set_tuning(17, al)
