@@ -152,6 +152,12 @@ int vlc_kv_relocate(const void* kpool, const void* vpool, int page_tokens, const
                     const int* blocks, int n_blocks, const float* cos_tab, const float* sin_tab,
                     int tab_ld, cudaStream_t stream);
 
+/* Row gather: dst row dst_rows[r] = src row src_rows[r] for r < n (rows of row_bytes bytes, a multiple
+ * of 16; 16-byte aligned buffers).  Assembles ReuseResult.kv, the merged pre-RoPE K / V [L, n, kv] of
+ * a request (engine.py:153-155, 177-178), from the QKV epilogue's computed rows and the store pages. */
+int vlc_gather_rows(void* dst, const int* dst_rows, const void* src, const int* src_rows, int n, int row_bytes,
+                    cudaStream_t stream);
+
 /* Store write (store.py:140-147 put_kv): src [layers][T][kv] (f32 or bf16) -> bf16 pages. */
 int vlc_store_write_pages(const void* src, int src_f32, int layers, int tokens, int kv,
                           const int* page_table, int pages_per_layer, void* pool,

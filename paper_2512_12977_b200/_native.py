@@ -18,7 +18,7 @@ EPI_F32, EPI_RESID, EPI_BF16, EPI_BIAS_ADD, EPI_SWIGLU, EPI_QKV_PLAIN, EPI_QKV_R
 
 EXPORTS = ("vlc_last_error", "vlc_version", "vlc_embed_assemble", "vlc_rmsnorm",
            "vlc_add_rmsnorm", "vlc_kv_relocate", "vlc_store_write_pages", "vlc_gemm_bf16", "vlc_gemm_row_tile",
-           "vlc_pack_operand", "vlc_attn_paged",
+           "vlc_pack_operand", "vlc_attn_paged", "vlc_gather_rows",
            "vlc_patchify", "vlc_set_tuning", "vlc_set_debug_buffer", "vlc_copy_h2d_async")
 
 
@@ -75,6 +75,7 @@ def load():
         lib.vlc_pack_operand.argtypes = [vp, i, i, i, vp, i, i, vp]
         lib.vlc_attn_paged.argtypes = [C.POINTER(AttnPagedArgs), vp]
         lib.vlc_patchify.argtypes = [vp, i, i, vp, i, i, i, vp]
+        lib.vlc_gather_rows.argtypes = [vp, vp, vp, vp, i, i, vp]
         lib.vlc_set_tuning.argtypes = [i, i]
         lib.vlc_copy_h2d_async.argtypes = [vp, vp, C.c_size_t, vp]
         lib.vlc_set_debug_buffer.argtypes = [vp]

@@ -103,6 +103,7 @@ int vlc_kv_relocate_impl(const void*, const void*, int, const int*, int, int, vo
                          const int*, int, const float*, const float*, int, cudaStream_t);
 int vlc_store_write_pages_impl(const void*, int, int, int, int, const int*, int, void*, int, cudaStream_t);
 int vlc_patchify_impl(const float*, int, int, void*, int, int, int, cudaStream_t);
+int vlc_gather_rows_impl(void*, const int*, const void*, const int*, int, int, cudaStream_t);
 
 const char* vlc_last_error(void) { return g_err; }
 
@@ -225,6 +226,15 @@ int vlc_attn_paged(const vlc_attn_paged_args* a, cudaStream_t stream) {
   if (a->ws_slots > 0 && (!a->counters || !a->ws_o || !a->ws_ml || a->n_items > 148))
     return fail(VLC_ERR_INVALID, "attn_paged: split groups need counters / workspaces and <= 148 items");
   return cuda_status(launch_attention_paged(*a, stream), "attn_paged");
+}
+
+int vlc_gather_rows(void* dst, const int* dst_rows, const void* src, const int* src_rows, int n, int row_bytes,
+                    cudaStream_t stream) {
+  if (n < 0 || (n > 0 && (!dst || !dst_rows || !src || !src_rows)) || row_bytes <= 0 || row_bytes % 16 ||
+      (reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) % 16)
+    return fail(VLC_ERR_INVALID, "gather_rows: bad args");
+  return cuda_status((cudaError_t)vlc_gather_rows_impl(dst, dst_rows, src, src_rows, n, row_bytes, stream),
+                     "gather_rows");
 }
 
 int vlc_patchify(const float* pixels, int side, int patch, void* out, int row0, int pk_rows, int pk_kb,

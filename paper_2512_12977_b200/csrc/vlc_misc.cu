@@ -166,6 +166,17 @@ __global__ void store_pages_kernel(const void* __restrict__ src, int layers, int
   }
 }
 
+// ------------------------------------------------------------------ row gather (merged KV)
+__global__ void __launch_bounds__(256) gather_rows_kernel(uint4* __restrict__ dst, const int* __restrict__ drow,
+                                                          const uint4* __restrict__ src, const int* __restrict__ srow,
+                                                          int n, int row16) {
+  for (long r = blockIdx.x; r < n; r += gridDim.x) {
+    const uint4* s = src + (long)__ldg(srow + r) * row16;
+    uint4* d = dst + (long)__ldg(drow + r) * row16;
+    for (int i = threadIdx.x; i < row16; i += blockDim.x) d[i] = __ldcs(s + i);
+  }
+}
+
 // ------------------------------------------------------------------ patchify
 __global__ void patchify_kernel(const float* __restrict__ px, int side, int p,
                                 __nv_bfloat16* __restrict__ out, int row0, int pk_rows, int pk_kb) {
@@ -245,6 +256,15 @@ int vlc_store_write_pages_impl(const void* src, int src_f32, int layers, int tok
                                                                   pages_per_layer,
                                                                   reinterpret_cast<__nv_bfloat16*>(pool),
                                                                   page_tokens);
+  return (int)cudaGetLastError();
+}
+
+int vlc_gather_rows_impl(void* dst, const int* dst_rows, const void* src, const int* src_rows, int n, int row_bytes,
+                         cudaStream_t stream) {
+  if (n <= 0) return 0;
+  const int blocks = n < 148 * 16 ? n : 148 * 16;
+  gather_rows_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<uint4*>(dst), dst_rows,
+                                                 reinterpret_cast<const uint4*>(src), src_rows, n, row_bytes / 16);
   return (int)cudaGetLastError();
 }
 

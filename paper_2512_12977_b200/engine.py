@@ -20,6 +20,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import _native as N
 from .config import ModelConfig
 from .exceptions import InputError
 from .layout import SRC_SCRATCH, SRC_STORE, RequestSpec, build_layout, structure_of, with_data
@@ -407,17 +408,31 @@ def _merged_kv_loader(out, lay, spec: RequestSpec, kv_pool, cfg: ModelConfig, re
                     pages = spec.page_rows[m]
                     pool_idx.append(pages[i, t // kv_pool.P].astype(np.int64) * kv_pool.P + t % kv_pool.P)
                     pool_dst.append(i * n + start + t)
+        # one int32 upload of the row maps, then vlc_gather_rows: K rows from the QKV epilogue's pre-RoPE
+        # copy (computed) and the store pages (reused); V rows from the request cache and the store
+        KVR = vc.shape[1]
+        v_src = (np.arange(L, dtype=np.int64)[:, None] * KVR + kvoff + np.arange(n)[None, :]).reshape(-1)
+        v_dst = np.arange(L * n, dtype=np.int64)
+        pk = [np.concatenate(kpre_idx), np.concatenate(kpre_dst), v_src, v_dst]
+        if pool_idx:
+            pk += [np.concatenate(pool_idx), np.concatenate(pool_dst)]
+        sizes = [len(a) for a in pk]
+        idx = torch.from_numpy(np.concatenate(pk).astype(np.int32)).cuda()
+        offs = np.concatenate([[0], np.cumsum(sizes)])
         K = torch.zeros(L * n, kvd, dtype=torch.bfloat16, device="cuda")
-        a = torch.from_numpy(np.concatenate(kpre_idx)).cuda()
-        b = torch.from_numpy(np.concatenate(kpre_dst)).cuda()
-        K[b] = kpre.view(-1, kvd)[a]
-        V = vc[:, kvoff:kvoff + n].clone()     # computed rows (and relocated boundary rows)
+        V = torch.zeros(L * n, kvd, dtype=torch.bfloat16, device="cuda")
+        stream = torch.cuda.current_stream().cuda_stream
+
+        def gather(dst, src, j):        # pairs (src rows pk[j], dst rows pk[j + 1])
+            N.check(N.load().vlc_gather_rows(dst.data_ptr(), idx[offs[j + 1]:].data_ptr(), src.data_ptr(),
+                                             idx[offs[j]:].data_ptr(), sizes[j], kvd * 2, stream), "vlc_gather_rows")
+        gather(K, kpre, 0)
+        gather(V, vc, 2)
         if pool_idx:
             # reused rows straight from the store pages (the attention reads them there too)
-            a = torch.from_numpy(np.concatenate(pool_idx)).cuda()
-            b = torch.from_numpy(np.concatenate(pool_dst)).cuda()
-            K[b] = kv_pool.k[a]
-            V.view(L * n, kvd)[b] = kv_pool.v[a]
+            gather(K, kv_pool.k, 4)
+            gather(V, kv_pool.v, 4)
+        K, V = K.view(L, n, kvd), V.view(L, n, kvd)
         return K.view(L, n, kvd), V
     return load
 

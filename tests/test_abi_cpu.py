@@ -26,7 +26,7 @@ def lib():
 
 def test_header_declares_the_minimum_set():
     names = _declared()
-    for n in ("vlc_last_error", "vlc_embed_assemble", "vlc_kv_relocate", "vlc_rmsnorm", "vlc_gemm_bf16",
+    for n in ("vlc_last_error", "vlc_embed_assemble", "vlc_gather_rows", "vlc_kv_relocate", "vlc_rmsnorm", "vlc_gemm_bf16",
               "vlc_attn_paged", "vlc_store_write_pages"):
         assert n in names
 

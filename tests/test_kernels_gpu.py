@@ -400,3 +400,19 @@ def test_gemm_cta_pair_swiglu_packed(nat, pair_mode):
     gate, up = acc[:, 0::2], acc[:, 1::2]
     ref = gate / (1 + torch.exp(-gate)) * up
     assert (h - ref).abs().max().item() <= 2e-2 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("rows,width", [(1, 8), (300, 3584), (5000, 256)])
+def test_gather_rows(nat, rows, width):
+    """vlc_gather_rows: dst[dst_rows[r]] = src[src_rows[r]] (the merged-KV assembly of ReuseResult.kv)."""
+    g = torch.Generator(device="cuda").manual_seed(rows + width)
+    src = torch.randn(2 * rows + 3, width, device="cuda", generator=g).bfloat16()
+    dst = torch.zeros(rows + 5, width, device="cuda", dtype=torch.bfloat16)
+    s_idx = torch.randperm(2 * rows + 3, device="cuda", generator=g)[:rows].int()
+    d_idx = torch.randperm(rows + 5, device="cuda", generator=g)[:rows].int()
+    nat.check(nat.load().vlc_gather_rows(dst.data_ptr(), d_idx.data_ptr(), src.data_ptr(), s_idx.data_ptr(), rows,
+                                         width * 2, _stream()), "gather_rows")
+    torch.cuda.synchronize()
+    want = torch.zeros_like(dst)
+    want[d_idx.long()] = src[s_idx.long()]
+    assert torch.equal(dst, want)
