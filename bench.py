@@ -782,8 +782,12 @@ def layer_aware_vs_uniform(P, model, seq, hashes, store, L, timed):
     for name, plan in plans.items():
         req = P.ReuseRequest(seq, hashes, plan)
         last = prefill_last(P, model, req, store)
+        try:
+            obj = round(P.objective(table, plan), 6)
+        except P.InputError:                   # a ratio off the profiled grid (uniform 5%)
+            obj = None
         out[name] = {"mean_ratio": round(P.mean_ratio(plan), 4), "ratios": list(plan.ratios),
-                     "objective": round(P.objective(table, plan), 6),
+                     "objective": obj, "objective_fit": round(P.objective(fit, plan), 6) if obj is not None else None,
                      "p50_ms": round(statistics.median(timed(req, store, 7, 2)), 4),
                      "last_row_mse_vs_full": float(np.mean((last.astype(np.float64) - full) ** 2)),
                      "last_row_max_abs_vs_full": float(np.abs(last - full).max()),

@@ -146,7 +146,8 @@ int vlc_add_rmsnorm(float* x, int ldx, const float* add, int ld_add, const float
 /* Fused gather + RoPE re-rotation + scatter of cached pre-RoPE K and copy of V from
  * the paged store into the request KV cache (engine.py:153-155 + engine.py:180).
  * descs int32[n][8] = {layer, page_tab_off, tok0, ntok, dst_row0, pos0, 0, 0};
- * blocks int32[n_blocks][2] = {desc, token offset}; kc/vc bf16 [layers][kv_rows_cap][kv]. */
+ * blocks int32[n_blocks][2] = {desc, token offset}; kc/vc bf16 [layers][kv_rows_cap][kv].
+ * vpool / vc NULL: K only (the store builds its rotated-at-origin K pages with it). */
 int vlc_kv_relocate(const void* kpool, const void* vpool, int page_tokens, const int* page_table,
                     int kv, int head_dim, void* kc, void* vc, int kv_rows_cap, const int* descs,
                     const int* blocks, int n_blocks, const float* cos_tab, const float* sin_tab,

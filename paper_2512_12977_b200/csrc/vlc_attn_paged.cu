@@ -5,20 +5,26 @@
 //   * the request's K/V rows (kc / vc, [layer][row][kv]): text and recomputed tokens, whose K the
 //     QKV epilogue already rotated to its position -- and the few cached rows that share a chunk
 //     with recomputed ones (relocated there by vlc_kv_relocate);
-//   * a page of the store's pool (pool_k / pool_v, [row][kv]): cached image tokens, K pre-RoPE.
-//     Four ROTATION warps turn such a K chunk, in shared memory, into K rotated at the chunk's new
-//     positions (the reference's engine.py:180 re-rotation: (a cos - b sin, b cos + a sin) in
-//     fp32 with the fp32 cos / sin tables of model.py:129-134), before the MMA reads it.
-// So the cached K/V of an image cross HBM once per layer, read-only, straight from the store:
-// the gather + re-rotation of vlc_kv_relocate is fused into its consumer and the scatter into the
-// request cache (and its re-read) disappears.
+//   * a page of the store's pool (pool_k / pool_v, [row][kv]): cached image tokens, K rotated at the
+//     position it was CACHED at (o + t).  At its new position s + t the reference re-rotates the
+//     pre-RoPE key (engine.py:180); since RoPE rotations compose, R(s + t) k = R(D) R(o + t) k with
+//     D = s - o the image's shift, and q . R(D) K = (R(-D) q) . K.  So instead of re-rotating every
+//     cached key (per layer, per key), the CTA rotates its 128 queries ONCE by -D (four ROTATION
+//     warps, fp32 tables of model.py:129-134) into a second Q buffer and multiplies the store chunks
+//     against it; request chunks use the queries as they are.  A chunk's D rides in the upper bits
+//     of its length word; a tile never pairs store chunks of two images (host padding), and when the
+//     CTA's key range reaches the next image the rotation warps redo the rotation for its D once the
+//     MMAs on the previous one are complete (q1_free / q1_ready).
+// So the cached K/V of an image cross HBM once per layer, read-only, straight from the store: the
+// gather + re-rotation + scatter of vlc_kv_relocate disappears into the consumer.
 //
 // CTA = (request, head, <= 128 position-sorted queries, range of 128-key tiles); tile j of an item
 // = chunks chunk0 + 2j, 2j + 1 (the host pads every list to an even length).  Warp 0 issues the
 // TMA loads (Q once; per K / V tile 2 chunks x the head's swizzle atoms), warp 1 the tcgen05.mma
 // chain, warps 2-9 run the online softmax (two threads per query row, one per 64-key chunk, each
 // with its own running max / sum and O accumulator in TMEM, merged once at the end), warps 10-13
-// rotate store K chunks.  S is double-buffered in TMEM: S(j+2) is issued after PV(j), so the
+// rotate the queries for the store chunks.  A 128-key tile whose two chunks need different query
+// buffers is multiplied as two N = 64 halves.  S is double-buffered in TMEM: S(j+2) is issued after PV(j), so the
 // tensor pipe computes S(j+1) while the softmax works on S(j).  P (bf16) overwrites S in TMEM and
 // feeds O += P V as a TS-MMA.  Key ranges of long query tiles are split over co-resident CTAs that
 // merge their fp32 partials in-kernel (group >= 0).
@@ -46,13 +52,14 @@ struct PaCfg {
   static constexpr int KV_ATOM = PA_KT * SWZ;            // [atom][128 rows][SWZ]
   static constexpr int CH_ATOM_BYTES = PA_CHUNK * SWZ;   // one chunk's rows of one atom
   static constexpr int BAR_BYTES = 512;
-  static constexpr int XM_BYTES = 2 * 2 * 128 * 4;       // merge exchange: [m | l][half][row]
-  static constexpr int RING = PA_SMEM_MAX - 1024 - BAR_BYTES - Q_BYTES - XM_BYTES;
+  static constexpr int XM_BYTES = 2 * 2 * 128 * 4;       // merge exchange: [m | l][half][row] (in the V ring)
+  static constexpr int RING = PA_SMEM_MAX - 1024 - BAR_BYTES - 2 * Q_BYTES;
   static constexpr int VST_FIT = RING / (2 * KV_BYTES);
   static constexpr int VST = VST_FIT > 6 ? 6 : VST_FIT;
   static constexpr int KST_FIT = (RING - VST * KV_BYTES) / KV_BYTES;
   static constexpr int KST = KST_FIT > 6 ? 6 : KST_FIT;
-  static constexpr int SMEM = 1024 + Q_BYTES + (KST + VST) * KV_BYTES + XM_BYTES + BAR_BYTES;
+  static constexpr int SMEM = 1024 + 2 * Q_BYTES + (KST + VST) * KV_BYTES + BAR_BYTES;
+  static_assert(VST * KV_BYTES >= XM_BYTES, "merge exchange lives in the V ring");
   static_assert(VST >= 2 && KST >= VST, "K / V rings");
   static_assert((KST + VST) * KV_BYTES >= 128 * HD * 4, "split partials are staged in the K/V ring");
   static_assert((KST + VST) * KV_BYTES >= 256 * 8 * 12 + 256 * 4, "merge tables live in the K/V ring");
@@ -108,14 +115,16 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sK = sQ + C::Q_BYTES;
+  uint8_t* sQ1 = sQ + C::Q_BYTES;         // queries rotated by -D for the store chunks
+  uint8_t* sK = sQ1 + C::Q_BYTES;
   uint8_t* sV = sK + C::KST * C::KV_BYTES;
-  float* xm = reinterpret_cast<float*>(sV + C::VST * C::KV_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xm) + C::XM_BYTES);
+  float* xm = reinterpret_cast<float*>(sV);   // used once every PV has completed
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + C::VST * C::KV_BYTES);
   uint64_t* q_full = bars;
   uint64_t* k_full = q_full + 1;          // [KST] TMA landed
-  uint64_t* k_ready = k_full + C::KST;    // [KST] store chunks rotated
-  uint64_t* k_empty = k_ready + C::KST;   // [KST] S MMA done with the slot
+  uint64_t* q1_ready = k_full + C::KST;   // rotated queries written (one phase per image run)
+  uint64_t* q1_free = q1_ready + 1;       // every MMA on the previous run's rotated queries complete
+  uint64_t* k_empty = q1_free + 1;        // [KST] S MMA done with the slot
   uint64_t* v_full = k_empty + C::KST;    // [VST]
   uint64_t* v_empty = v_full + C::VST;    // [VST]
   uint64_t* s_full = v_empty + C::VST;    // [2] S buffer b complete
@@ -139,9 +148,10 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
     tma_prefetch(&map_pk);
     tma_prefetch(&map_pv);
     mbar_init(q_full, 1);
+    mbar_init(q1_ready, 32 * PA_ROT_WARPS);
+    mbar_init(q1_free, 1);
     for (int s = 0; s < C::KST; ++s) {
       mbar_init(&k_full[s], 1);
-      mbar_init(&k_ready[s], 32 * PA_ROT_WARPS);
       mbar_init(&k_empty[s], 1);
     }
     for (int s = 0; s < C::VST; ++s) {
@@ -223,22 +233,52 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
     // ---------------- MMA issue (one thread)
     if (lane == 0 && nt > 0) {
       const uint32_t idesc_s = make_idesc_bf16(128, PA_KT, 0, 0);
+      const uint32_t idesc_h = make_idesc_bf16(128, PA_CHUNK, 0, 0);
       const uint32_t idesc_o = make_idesc_bf16(128, HD, 0, 1);
       mbar_wait(q_full, 0);
       PA_TRACE(1);
-      auto issue_s = [&](int j) {   // S[j & 1] = Q K_j^T
+      int run = -1, run_d = 0;      // image run of the rotated queries in use
+      auto issue_s = [&](int j) {   // S[j & 1] = Q K_j^T (store chunks against the rotated queries)
         const int st = j % C::KST;
-        mbar_wait(&k_ready[st], (j / C::KST) & 1);
+        const int4 c0 = chunks[2 * j], c1 = chunks[2 * j + 1];
+        const bool s0 = c0.w >= 0, s1 = c1.w >= 0;
+        if (s0 || s1) {
+          const int dj = (s0 ? c0.y : c1.y) >> 8;
+          if (run < 0 || dj != run_d) {          // a new image: its rotation, after the old one's MMAs
+            if (run >= 0) tc_commit(q1_free);
+            ++run;
+            run_d = dj;
+            mbar_wait(q1_ready, run & 1);
+          }
+        }
+        mbar_wait(&k_full[st], (j / C::KST) & 1);
         tc_fence_after();
-        const uint32_t q_addr = smem_u32(sQ);
         const uint32_t k_addr = smem_u32(sK + st * C::KV_BYTES);
+        if (s0 == s1) {
+          const uint32_t q_addr = smem_u32(s0 ? sQ1 : sQ);
 #pragma unroll
-        for (int k = 0; k < HD / 16; ++k) {
-          const int at = (k * 16) / C::ATOM_E;
-          const uint32_t eoff = ((k * 16) % C::ATOM_E) * 2;
-          const uint64_t ad = make_sdesc(q_addr + at * C::Q_ATOM + eoff, 16, 8 * C::SWZ, C::SWZ);
-          const uint64_t bd = make_sdesc(k_addr + at * C::KV_ATOM + eoff, 16, 8 * C::SWZ, C::SWZ);
-          tc_mma_f16(tmem + C::s_col(j & 1), ad, bd, idesc_s, k > 0 ? 1u : 0u);
+          for (int k = 0; k < HD / 16; ++k) {
+            const int at = (k * 16) / C::ATOM_E;
+            const uint32_t eoff = ((k * 16) % C::ATOM_E) * 2;
+            const uint64_t ad = make_sdesc(q_addr + at * C::Q_ATOM + eoff, 16, 8 * C::SWZ, C::SWZ);
+            const uint64_t bd = make_sdesc(k_addr + at * C::KV_ATOM + eoff, 16, 8 * C::SWZ, C::SWZ);
+            tc_mma_f16(tmem + C::s_col(j & 1), ad, bd, idesc_s, k > 0 ? 1u : 0u);
+          }
+        } else {
+          // mixed tile: chunk h (key rows 64h ..) against its own query buffer, N = 64 each
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t q_addr = smem_u32((h ? s1 : s0) ? sQ1 : sQ);
+#pragma unroll
+            for (int k = 0; k < HD / 16; ++k) {
+              const int at = (k * 16) / C::ATOM_E;
+              const uint32_t eoff = ((k * 16) % C::ATOM_E) * 2;
+              const uint64_t ad = make_sdesc(q_addr + at * C::Q_ATOM + eoff, 16, 8 * C::SWZ, C::SWZ);
+              const uint64_t bd = make_sdesc(k_addr + at * C::KV_ATOM + h * C::CH_ATOM_BYTES + eoff, 16,
+                                             8 * C::SWZ, C::SWZ);
+              tc_mma_f16(tmem + C::s_col(j & 1) + h * PA_CHUNK, ad, bd, idesc_h, k > 0 ? 1u : 0u);
+            }
+          }
         }
         tc_commit(&s_full[j & 1]);
         if (j + C::KST < nt) tc_commit(&k_empty[st]);   // the slot's next load waits on this
@@ -270,109 +310,66 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
     }
     __syncwarp();
   } else if (warp >= 2 + PA_SOFT_WARPS) {
-    // ---------------- rotation warps: store K chunks -> rotated at their new positions
+    // ---------------- rotation warps: the queries rotated by -D for the store chunks (sQ1)
+    // D = the shift of the image whose store chunks the tile reads; redone per image run of the range.
     // Lane -> two adjacent frequencies (f0, f0 + 1) of the head: one 4-byte word of the lower half row
     // (dims f0, f0 + 1) and one of the upper half (f0 + HD/2, ...); a warp covers RPW whole rows per
-    // step (conflict-free: one 128-byte wavefront per access) and walks a 16-row block of the chunk.
-    // The angle advances by RPW positions per step with the complex recurrence
-    //   (c, s) <- (c cos(RPW f) - s sin(RPW f), s cos(RPW f) + c sin(RPW f)),
-    // starting from the fp32 table row of the block's first position (reference fp32 tables,
-    // model.py:129-134) and stepping with table row RPW: no per-row table traffic (L2 latency),
-    // a <= 16-step recurrence error (~1e-6) far below both the table's own fp32 angle rounding
-    // and the bf16 rounding of the rotated key.
+    // step (one 128-byte wavefront per access).  R(-D): (a, b) -> (a cos + b sin, b cos - a sin) with
+    // cos / sin of D * theta from the fp32 tables (row |D|; sin flips sign for D < 0), in fp32, one
+    // bf16 rounding.
     constexpr int LPR = HD / 4;                               // lanes per row
     constexpr int RPW = 32 / LPR;                             // rows per warp step
-    constexpr int RB = PA_CHUNK / PA_ROT_WARPS;               // rows per warp block (16)
-    constexpr int STEPS = RB / RPW;
     constexpr int HALF = HD / 2;
+    constexpr int STEPS = 128 / (PA_ROT_WARPS * RPW);
+    constexpr int B = STEPS < 8 ? STEPS : 8;                  // rows per batch: loads, math, stores
     const int wr = (int)warp - (2 + PA_SOFT_WARPS);
     const int f0 = 2 * ((int)lane % LPR);
-    const int r0 = wr * RB + (int)lane / LPR;                 // first row of this lane in a chunk
-    const float2 stc = __ldg(reinterpret_cast<const float2*>(a.cos_tab + (long)RPW * a.tab_ld + f0));
-    const float2 sts = __ldg(reinterpret_cast<const float2*>(a.sin_tab + (long)RPW * a.tab_ld + f0));
-    const float2 nsts = make_float2(-sts.x, -sts.y);
-    // byte offset of element e of tile row `row` in the [atom][128][SWZ] swizzled layout
     auto eoff = [](int row, int e) -> uint32_t {
-      const uint32_t lin = (uint32_t)((e / C::ATOM_E) * C::KV_ATOM + row * C::SWZ + (e % C::ATOM_E) * 2);
+      const uint32_t lin = (uint32_t)((e / C::ATOM_E) * C::Q_ATOM + row * C::SWZ + (e % C::ATOM_E) * 2);
       return lin ^ (((lin >> 7) & ((1u << C::SWZ_B) - 1)) << 4);
     };
-    // base (cos, sin) of both chunks of tile j: the chunk descriptors are loaded two tiles ahead and
-    // the table entries one tile ahead, so neither dependent global load sits on the rotation path
-    auto load_base = [&](const int4* ch, float2* bc, float2* bs) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (ch[h].w >= 0) {
-          const long o = (long)(ch[h].x + r0) * a.tab_ld + f0;
-          bc[h] = __ldg(reinterpret_cast<const float2*>(a.cos_tab + o));
-          bs[h] = __ldg(reinterpret_cast<const float2*>(a.sin_tab + o));
-        }
-      }
-    };
-    int4 d_cur[2], d_nxt[2], d_nn[2];
-    float2 bc[2] = {}, bs[2] = {};
-    if (nt > 0) {
-      d_cur[0] = chunks[0];
-      d_cur[1] = chunks[1];
-      load_base(d_cur, bc, bs);
-    }
-    if (nt > 1) {
-      d_nxt[0] = chunks[2];
-      d_nxt[1] = chunks[3];
-    }
+    const uint32_t q0 = smem_u32(sQ), q1 = smem_u32(sQ1);
+    int run = -1, run_d = 0;
     for (int j = 0; j < nt; ++j) {
-      const int st = j % C::KST;
-      float2 cc[2] = {bc[0], bc[1]}, ss[2] = {bs[0], bs[1]};
-      const int4 d0 = d_cur[0], d1 = d_cur[1];
-      if (j + 2 < nt) {
-        d_nn[0] = chunks[2 * (j + 2)];
-        d_nn[1] = chunks[2 * (j + 2) + 1];
-      }
-      if (j + 1 < nt) load_base(d_nxt, bc, bs);
-      d_cur[0] = d_nxt[0];
-      d_cur[1] = d_nxt[1];
-      d_nxt[0] = d_nn[0];
-      d_nxt[1] = d_nn[1];
-      mbar_wait(&k_full[st], (j / C::KST) & 1);
-      if (wr == 0 && lane == 0 && j < 16) PA_TRACE(18 + j);
-      const uint32_t tile = smem_u32(sK + st * C::KV_BYTES);
+      const int4 c0 = chunks[2 * j], c1 = chunks[2 * j + 1];
+      if (c0.w < 0 && c1.w < 0) continue;
+      const int d = (c0.w >= 0 ? c0.y : c1.y) >> 8;
+      if (run >= 0 && d == run_d) continue;
+      if (run < 0) mbar_wait(q_full, 0);
+      else mbar_wait(q1_free, run & 1);      // the MMAs on the previous image's rotation are complete
+      ++run;
+      run_d = d;
+      const int ad = d < 0 ? -d : d;
+      const float2 c = __ldg(reinterpret_cast<const float2*>(a.cos_tab + (long)ad * a.tab_ld + f0));
+      float2 sn = __ldg(reinterpret_cast<const float2*>(a.sin_tab + (long)ad * a.tab_ld + f0));
+      if (d < 0) sn = make_float2(-sn.x, -sn.y);
+      const float2 nsn = make_float2(-sn.x, -sn.y);
+      for (int k0 = 0; k0 < STEPS; k0 += B) {
+        uint32_t lo[B], hi[B];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if ((h ? d1.w : d0.w) < 0) continue;                  // request rows: already rotated
-        float2 c = cc[h], s = ss[h];
-        // all loads of the chunk first, then the math, then the stores: the shared-memory accesses
-        // are volatile asm (ordered), so interleaving them per step would serialise every step on
-        // the load latency (1.82 -> 1.61 us per 128-key tile at the C3 layout)
-        uint32_t lo[STEPS], hi[STEPS];
-#pragma unroll
-        for (int k = 0; k < STEPS; ++k) {
-          const int row = h * PA_CHUNK + r0 + k * RPW;
-          lo[k] = lds32(tile + eoff(row, f0));
-          hi[k] = lds32(tile + eoff(row, f0 + HALF));
+        for (int k = 0; k < B; ++k) {
+          const int row = (k0 + k) * PA_ROT_WARPS * RPW + wr * RPW + (int)lane / LPR;
+          lo[k] = lds32(q0 + eoff(row, f0));
+          hi[k] = lds32(q0 + eoff(row, f0 + HALF));
         }
 #pragma unroll
-        for (int k = 0; k < STEPS; ++k) {
-          // packed fp32 pairs (FMUL2 / FFMA2): lo' = a c + b (-s), hi' = b c + a s
+        for (int k = 0; k < B; ++k) {
           const float2 av = make_float2(bf16_lo(lo[k]), bf16_hi(lo[k]));
           const float2 bv = make_float2(bf16_lo(hi[k]), bf16_hi(hi[k]));
-          const float2 ns = fmul2(s, make_float2(-1.f, -1.f));
-          const float2 ro = ffma2(bv, ns, fmul2(av, c)), rh = ffma2(av, s, fmul2(bv, c));
+          const float2 ro = ffma2(bv, sn, fmul2(av, c));      // a cos + b sin
+          const float2 rh = ffma2(av, nsn, fmul2(bv, c));     // b cos - a sin
           lo[k] = pack_bf16(ro.x, ro.y);
           hi[k] = pack_bf16(rh.x, rh.y);
-          // advance RPW positions: (c, s) <- (c cos - s sin, s cos + c sin)
-          const float2 cn = ffma2(s, nsts, fmul2(c, stc));
-          s = ffma2(c, sts, fmul2(s, stc));
-          c = cn;
         }
 #pragma unroll
-        for (int k = 0; k < STEPS; ++k) {
-          const int row = h * PA_CHUNK + r0 + k * RPW;
-          sts32(tile + eoff(row, f0), lo[k]);
-          sts32(tile + eoff(row, f0 + HALF), hi[k]);
+        for (int k = 0; k < B; ++k) {
+          const int row = (k0 + k) * PA_ROT_WARPS * RPW + wr * RPW + (int)lane / LPR;
+          sts32(q1 + eoff(row, f0), lo[k]);
+          sts32(q1 + eoff(row, f0 + HALF), hi[k]);
         }
       }
       fence_proxy_async_smem();      // generic-proxy writes -> visible to the tensor core's reads
-      mbar_arrive(&k_ready[st]);
-      if (wr == 0 && lane == 0 && j < 16) PA_TRACE(34 + j);
+      mbar_arrive(q1_ready);
     }
   } else {
     // ---------------- softmax: warp w -> TMEM lane quadrant w & 3, chunk half hh
@@ -396,7 +393,7 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
       for (int c = 0; c < CW / 32; ++c) tmem_ld32(tS + 32 * c, s + 32 * c);
       tmem_wait_ld();
       // column c is key position ch.x + c, valid for c < len and position <= the query's
-      const int lim = min(qp - ch.x, ch.y - 1);
+      const int lim = min(qp - ch.x, (ch.y & 0xff) - 1);
       if (lim < CW - 1) {
 #pragma unroll
         for (int i = 0; i < CW; ++i) s[i] = (i <= lim) ? s[i] : NEG_INF;

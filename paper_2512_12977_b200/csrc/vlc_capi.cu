@@ -171,6 +171,9 @@ int vlc_kv_relocate(const void* kpool, const void* vpool, int page_tokens, const
   if (n_blocks < 0 || page_tokens <= 0 || head_dim < 16 || head_dim % 16 || kv % head_dim || kv_rows_cap <= 0)
     return fail(VLC_ERR_UNSUPPORTED, "kv_relocate: head_dim must be a multiple of 16 dividing kv");
   if (tab_ld != head_dim / 2) return fail(VLC_ERR_INVALID, "kv_relocate: tab_ld must be head_dim/2");
+  if (n_blocks > 0 && (!kpool || !kc || !page_table || !descs || !blocks || !cos_tab || !sin_tab ||
+                       (vc != nullptr && vpool == nullptr)))
+    return fail(VLC_ERR_INVALID, "kv_relocate: null pointer");
   return cuda_status((cudaError_t)vlc_kv_relocate_impl(kpool, vpool, page_tokens, page_table, kv, head_dim, kc, vc,
                                                        kv_rows_cap, descs, blocks, n_blocks, cos_tab, sin_tab,
                                                        tab_ld, stream),

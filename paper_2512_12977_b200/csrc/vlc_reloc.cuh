@@ -97,6 +97,7 @@ __device__ __forceinline__ void relocate_block(const RelocArgs& r, int b, int ti
       }
     }
   }
+  if (r.vc == nullptr) return;   // K only (the store's rotated-at-origin copy)
   const int vec_per_row = kv / 8;
   const int total = t_count * vec_per_row;
 #pragma unroll 4

@@ -285,7 +285,7 @@ def _resolve(model: ToyVLM, request: ReuseRequest, store: CacheStore, miss_base:
 
     fp = model.fingerprint
     runner_kv = model.device.kv
-    enc_src, kv_hit, page_rows, miss_px = [], [], [], []
+    enc_src, kv_hit, page_rows, miss_px, origin = [], [], [], [], []
     enc_pool = kv_pool = None
     for m, seg in enumerate(segs):                               # engine.py:140-159
         h = request.image_hashes[m]
@@ -313,9 +313,13 @@ def _resolve(model: ToyVLM, request: ReuseRequest, store: CacheStore, miss_base:
             # keep is non-increasing over layers: any layer that skips image tokens reads cached KV
             kv_hit.append(bool((keep[:, m] < T).any()))
             page_rows.append(entry.pages)
+            origin.append(int(entry.origin_position))
+            if kv_hit[-1]:
+                _ensure_rotated(model, entry)
         else:
             kv_hit.append(False)
             page_rows.append(None)
+            origin.append(0)
             if (keep[:, m] < T).any():                            # reuse requested, nothing to reuse
                 metrics.fallback_images += 1
                 keep[:, m] = T
@@ -325,8 +329,49 @@ def _resolve(model: ToyVLM, request: ReuseRequest, store: CacheStore, miss_base:
     metrics.flops = _flops_from_counts(counts, len(seq), cfg, metrics.encoder_misses)
     spec = RequestSpec(n=len(seq), text_pos=text_pos, text_ids=text_ids,
                        images=[(s.start, s.length) for s in segs], keep=keep, kv_hit=kv_hit,
-                       enc_src=enc_src, page_rows=page_rows, page_tokens=kv_pool.P if kv_pool is not None else 64)
+                       enc_src=enc_src, page_rows=page_rows, page_tokens=kv_pool.P if kv_pool is not None else 64,
+                       origin=origin)
     return _Resolved(spec, metrics, enc_pool, kv_pool, miss_px)
+
+
+def _ensure_rotated(model: ToyVLM, entry) -> None:
+    """The store entry's K rotated at the positions it was cached at (origin + t), into its pool's kr
+    pages (same page ids): once per entry and RoPE configuration, on the caller's stream.  The attention
+    reads these pages for reused rows and rotates its queries by -(new start - origin) instead of
+    re-rotating every cached key (engine.py:180 algebra: R(s + t) k = R(s - o) R(o + t) k)."""
+    cfg = model.config
+    sig = (cfg.head_dim, float(cfg.rope_base))
+    if getattr(entry, "rotated_for", None) == sig:
+        return
+    import torch
+    from .layout import RELOC_TOK
+    pool, P = entry.pool, entry.pool.P
+    L, T = entry.layers, entry.tokens
+    dw = model.device
+    dw.ensure_positions(int(entry.origin_position) + T + 1)
+    pages = np.asarray(entry.pages, dtype=np.int32)
+    ppl = pages.shape[1]
+    j = np.arange(ppl)
+    ntok = np.minimum(P, T - j * P)
+    descs = np.zeros((L, ppl, 8), dtype=np.int32)
+    descs[:, :, 1] = np.arange(L * ppl).reshape(L, ppl)
+    descs[:, :, 3] = ntok[None, :]
+    descs[:, :, 4] = pages * P
+    descs[:, :, 5] = int(entry.origin_position) + j[None, :] * P
+    descs = descs.reshape(-1, 8)
+    nt = descs[:, 3]
+    nblk = -(-nt // RELOC_TOK)
+    blocks = np.stack([np.repeat(np.arange(len(descs)), nblk),
+                       np.concatenate([np.arange(k) * RELOC_TOK for k in nblk])], axis=1).astype(np.int32)
+    pad = np.zeros((-pages.size) % 4, dtype=np.int32)          # blocks are read as int2: 8-byte aligned
+    ints = torch.from_numpy(np.concatenate([pages.reshape(-1), pad, descs.reshape(-1), blocks.reshape(-1)])).cuda()
+    o_d = pages.size + pad.size
+    o_b = o_d + descs.size
+    N.check(N.load().vlc_kv_relocate(pool.k.data_ptr(), None, P, ints.data_ptr(), pool.width, cfg.head_dim,
+                                     pool.kr.data_ptr(), None, pool.kr.shape[0], ints[o_d:].data_ptr(),
+                                     ints[o_b:].data_ptr(), len(blocks), dw.cos.data_ptr(), dw.sin.data_ptr(),
+                                     cfg.head_dim // 2, torch.cuda.current_stream().cuda_stream), "vlc_kv_relocate")
+    entry.rotated_for = sig
 
 
 def prefill_with_reuse(model: ToyVLM, request: ReuseRequest, store: CacheStore) -> ReuseResult:

@@ -36,6 +36,7 @@ class RequestSpec:
     enc_src: list                 # per image: (SRC_STORE|SRC_SCRATCH, row base)
     page_rows: list = field(default_factory=list)  # per image: int32 [L, ppl] page ids (kv_hit only)
     page_tokens: int = 64         # token rows per store page
+    origin: list = field(default_factory=list)     # per image: position its cached KV was computed at
 
 
 @dataclass
@@ -129,8 +130,13 @@ def contiguous_chunks(row0: int, n: int) -> np.ndarray:
 def _pad_even(out):
     if len(out) % 2:          # a masked (len 0) chunk that reads valid memory: the previous source
         last = out[-1]
-        out.append([last[0] + CHUNK, 0, last[2], last[3]])
+        out.append([last[0] + CHUNK, last[1] & ~0xFF, last[2], last[3]])
     return np.array(out, dtype=np.int32).reshape(-1, 4)
+
+
+def chunk_shift(ch) -> int:
+    """D of a store chunk (its image's new start - cached start), packed above the 8-bit length."""
+    return int(ch[1]) >> 8
 
 
 def store_chunks_ok(T: int, P: int) -> bool:
@@ -160,15 +166,25 @@ def request_chunks(spec: RequestSpec, i: int, kvoff: int, page_base: dict) -> np
         P = int(spec.page_tokens)
         direct = hit and store_chunks_ok(T, P)
         ppl = np.asarray(spec.page_rows[m]).shape[1] if hit else 0
+        # D = new start - cached start (the attention rotates its queries by -D for these chunks)
+        dsh = (start - int(spec.origin[m] if spec.origin else start)) << 8 if direct else 0
+        first_store = True
         for t0 in range(0, T, CHUNK):
             ln = min(CHUNK, T - t0)
             if direct and t0 >= k:
-                out.append([start + t0, ln, page_base[m] + i * ppl + t0 // P, t0 % P])
+                store = [start + t0, ln | dsh, page_base[m] + i * ppl + t0 // P, t0 % P]
             elif direct and t0 < k < t0 + ln:          # the keep boundary splits this block
                 out.append([start + t0, k - t0, kvoff + start + t0, -1])
-                out.append([start + k, t0 + ln - k, page_base[m] + i * ppl + k // P, k % P])
+                store = [start + k, (t0 + ln - k) | dsh, page_base[m] + i * ppl + k // P, k % P]
             else:
                 out.append([start + t0, ln, kvoff + start + t0, -1])
+                continue
+            if first_store and len(out) % 2 and out[-1][3] >= 0 and (out[-1][1] >> 8) != (dsh >> 8):
+                # a 128-key tile never pairs store chunks of two images (one query rotation per tile)
+                last = out[-1]
+                out.append([store[0], last[1] & ~0xFF, last[2], last[3]])
+            first_store = False
+            out.append(store)
         cur = start + T
     text_run(cur, spec.n)
     del spans
@@ -389,7 +405,8 @@ def structure_of(specs: list[RequestSpec], L: int, heads: int):
         key.append((s.n, np.asarray(s.text_pos, np.int64).tobytes(), tuple(s.images),
                      np.asarray(s.keep, np.int32).tobytes(), tuple(bool(h) for h in s.kv_hit),
                      tuple(int(k) for k, _ in s.enc_src),
-                     tuple(0 if p is None else np.asarray(p).shape[1] for p in s.page_rows), int(s.page_tokens)))
+                     tuple(0 if p is None else np.asarray(p).shape[1] for p in s.page_rows), int(s.page_tokens),
+                     tuple(int(o) for o in s.origin)))
     return tuple(key)
 
 

@@ -283,7 +283,7 @@ class Runner:
         a = N.AttnPagedArgs(
             q=q.data_ptr(), q_rows_cap=q.shape[0], kc=kc.data_ptr(), vc=vc.data_ptr(), layers_cap=kc.shape[0],
             kv_rows_cap=kc.shape[1], layer=layer,
-            pool_k=pool.k.data_ptr() if pool is not None else None,
+            pool_k=pool.kr.data_ptr() if pool is not None else None,
             pool_v=pool.v.data_ptr() if pool is not None else None,
             pool_rows=pool.k.shape[0] if pool is not None else 0, page_table=page_table or None,
             page_rows=pool.P if pool is not None else 0,

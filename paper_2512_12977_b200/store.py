@@ -96,13 +96,16 @@ def _torch():
 
 
 class _PagePool:
-    """bf16 [capacity * page_tokens, width] rows; page p = rows [p*P, (p+1)*P)."""
+    """bf16 [capacity * page_tokens, width] rows; page p = rows [p*P, (p+1)*P).  k holds pre-RoPE K
+    (the reference's stored form, store.py:140-147); kr the same keys rotated at the position they were
+    cached at (filled per entry by engine._ensure_rotated), which the attention reads."""
 
     def __init__(self, width: int, page_tokens: int, pages: int):
         torch = _torch()
         self.width, self.P = width, page_tokens
         self.k = torch.zeros(pages * page_tokens, width, dtype=torch.bfloat16, device="cuda")
         self.v = torch.zeros_like(self.k)
+        self.kr = torch.zeros_like(self.k)
         self.free = list(range(pages - 1, -1, -1))
 
     @property
@@ -121,10 +124,11 @@ class _PagePool:
         torch = _torch()
         old = self.capacity
         k = torch.zeros(pages * self.P, self.width, dtype=torch.bfloat16, device="cuda")
-        v = torch.zeros_like(k)
+        v, kr = torch.zeros_like(k), torch.zeros_like(k)
         k[:self.k.shape[0]] = self.k
         v[:self.v.shape[0]] = self.v
-        self.k, self.v = k, v
+        kr[:self.kr.shape[0]] = self.kr
+        self.k, self.v, self.kr = k, v, kr
         self.free = list(range(pages - 1, old - 1, -1)) + self.free
 
 
@@ -176,6 +180,7 @@ class StoredKV:
         self.layers, self.tokens = layers, tokens
         self.origin_position, self.model_fingerprint = origin, fp
         self._host_k = self._host_v = None
+        self.rotated_for = None     # (head_dim, rope_base) whose rotation pool.kr holds for these pages
 
     def _rows(self):
         torch = _torch()

@@ -271,7 +271,7 @@ def test_layout_rows_match_masks(pre, T, nimg, suf, ratios, hits):
     from paper_2512_12977_b200.layout import relocated_ranges
     want = sum(e - k for i in range(L) for _, k, e in relocated_ranges(spec, i))
     assert lay.reloc_tokens == want
-    store = sum(int(c[1]) for ch in lay.attn_chunks for c in ch if c[3] >= 0 and c[1] > 0)
+    store = sum(int(c[1]) & 0xFF for ch in lay.attn_chunks for c in ch if c[3] >= 0 and c[1] & 0xFF > 0)
     assert store + want == int((~masks).sum())
 
 
@@ -336,7 +336,9 @@ def test_key_chunks_cover_every_key_once(pre, T, nimg, suf, ratios, P):
     """vlc_attn_paged's key chunks of each layer: positions 0 .. n-1 exactly once, in order; a store
     chunk only for cached rows (t >= keep) that sit inside one page; every cached row of a hit
     image is either read from the store or relocated into the request rows -- never both, never
-    neither -- and the relocated rows are exactly the cached rows of request-row chunks."""
+    neither -- and the relocated rows are exactly the cached rows of request-row chunks.  A store
+    chunk carries its image's shift D = new start - cached start above the 8-bit length, and no 128-key
+    tile pairs store chunks of two different shifts (the kernel rotates its queries once per tile)."""
     import numpy as np
     from paper_2512_12977_b200.layout import relocated_ranges, request_chunks
     seq, plan, spec = _spec(pre, T, nimg, suf, ratios, None)
@@ -344,21 +346,30 @@ def test_key_chunks_cover_every_key_once(pre, T, nimg, suf, ratios, P):
     ppl = -(-T // P)
     spec.page_rows = [np.arange(len(ratios) * ppl, dtype=np.int32).reshape(len(ratios), ppl) for _ in range(nimg)]
     base = {m: m * len(ratios) * ppl for m in range(nimg)}
+    spec.origin = [8 + 5 * m for m in range(nimg)]
     for i in range(len(ratios)):
-        ch = request_chunks(spec, i, 1000, base)
+        ch = request_chunks(spec, i, 1000, base).copy()
         assert len(ch) % 2 == 0
+        shift = ch[:, 1] >> 8
+        ch[:, 1] &= 0xFF
+        for a, b, sa, sb in zip(ch[0::2], ch[1::2], shift[0::2], shift[1::2]):
+            if a[3] >= 0 and b[3] >= 0:
+                assert sa == sb
+        assert (np.diff(ch[:, 0]) >= 0).all()
         real = ch[ch[:, 1] > 0]
+        rshift = shift[ch[:, 1] > 0]
         covered = np.concatenate([np.arange(c[0], c[0] + c[1]) for c in real])
         assert np.array_equal(covered, np.arange(spec.n))
         reloc = {m: (k, e) for m, k, e in relocated_ranges(spec, i)}
         for m, (start, Tm) in enumerate(spec.images):
             k = int(spec.keep[i, m])
             store_rows, req_rows = set(), set()
-            for c in real:
+            for c, sh in zip(real, rshift):
                 if not (start <= c[0] < start + Tm):
                     continue
                 t = set(range(c[0] - start, c[0] - start + c[1]))
                 if c[3] >= 0:
+                    assert sh == start - spec.origin[m]
                     assert min(t) >= k and c[3] + c[1] <= P
                     assert c[2] == base[m] + i * ppl + (c[0] - start) // P
                     store_rows |= t

@@ -195,8 +195,10 @@ def test_kv_relocate_matches_torch(nat):
 
 def _paged_case(nat, hd, heads, nkeys, nq, causal, store_every, seed, page_rows=64):
     """Request K/V rows plus a store pool; every `store_every`-th 64-key chunk (0: none) is read from
-    a randomly placed store page holding PRE-RoPE K (the kernel rotates it to the chunk's
-    positions).  Returns the kernel arguments and the fp32 torch reference of the attention."""
+    a randomly placed store page holding K rotated at the position it was CACHED at, pos - D, with a
+    shift D that changes every other 128-key tile (negative ones included); the kernel multiplies such
+    chunks against its queries rotated by -D.  The reference rotates the pre-RoPE key straight to its
+    position (engine.py:180).  Returns the kernel arguments and the fp32 torch reference."""
     from paper_2512_12977_b200.layout import attention_work, tiles_needed
     kv = heads * hd
     g = torch.Generator(device="cuda").manual_seed(seed)
@@ -210,6 +212,16 @@ def _paged_case(nat, hd, heads, nkeys, nq, causal, store_every, seed, page_rows=
     ptab = torch.randperm(npages, device="cuda", generator=g).int()
     cos, sin = _tables(hd, nkeys + 64)
     ref_k, ref_v = kc[layer, :nkeys].float().clone(), vc[layer, :nkeys].float().clone()
+    kr = kpool.clone()                      # the store's rotated-at-cache-position copy
+    half = hd // 2
+    inv = 10000.0 ** (-torch.arange(half, device="cuda", dtype=torch.float32) * (2.0 / hd))
+
+    def rope(kf, p):                        # fp32 rotation of [ln, kv] rows to positions p (any sign)
+        ang = p.float()[:, None] * inv[None, :]
+        cc, ss = torch.cos(ang)[:, None, :], torch.sin(ang)[:, None, :]
+        k3 = kf.reshape(len(p), heads, hd)
+        a_, b_ = k3[..., :half], k3[..., half:]
+        return torch.cat([a_ * cc - b_ * ss, b_ * cc + a_ * ss], -1).reshape(len(p), kv)
     chunks = []
     for ci, c in enumerate(range(0, nkeys, 64)):
         ln = min(64, nkeys - c)
@@ -217,19 +229,16 @@ def _paged_case(nat, hd, heads, nkeys, nq, causal, store_every, seed, page_rows=
             pti, off = ci * 64 // page_rows, (ci * 64) % page_rows
             rows = ptab[pti].long() * page_rows + off + torch.arange(ln, device="cuda")
             pos = torch.arange(c, c + ln, device="cuda")
-            # the kernel rotates in fp32 with the fp32 tables and rounds the result to bf16
-            kf = kpool[rows].float().reshape(ln, heads, hd)
-            half = hd // 2
-            cc, ss = cos[pos][:, None, :], sin[pos][:, None, :]
-            a_, b_ = kf[..., :half], kf[..., half:]
-            rot = torch.cat([a_ * cc - b_ * ss, b_ * cc + a_ * ss], -1).reshape(ln, kv)
-            ref_k[c:c + ln] = rot.bfloat16().float()
+            shift = ((ci // 4) % 3) * 37 - 40       # constant over a 128-key tile, new every other tile
+            kf = kpool[rows].float()
+            ref_k[c:c + ln] = rope(kf, pos).bfloat16().float()
+            kr[rows] = rope(kf, pos - shift).bfloat16()
             ref_v[c:c + ln] = vpool[rows].float()
-            chunks.append([c, ln, pti, off])
+            chunks.append([c, ln | (shift << 8), pti, off])
         else:
             chunks.append([c, ln, c, -1])
     if len(chunks) % 2:
-        chunks.append([chunks[-1][0] + 64, 0, chunks[-1][2], chunks[-1][3]])
+        chunks.append([chunks[-1][0] + 64, chunks[-1][1] & ~0xFF, chunks[-1][2], chunks[-1][3]])
     chunks = np.array(chunks, np.int32)
     if causal:
         qpos = torch.sort(torch.randperm(nkeys, device="cuda", generator=g)[:nq]).values.int()
@@ -246,11 +255,12 @@ def _paged_case(nat, hd, heads, nkeys, nq, causal, store_every, seed, page_rows=
                 ws_o=torch.zeros(max(groups, 1) * 8 * 256 * hd, device="cuda"),
                 ws_ml=torch.zeros(max(groups, 1) * 8 * 256 * 2, device="cuda"),
                 cnt=torch.zeros(4096, dtype=torch.int32, device="cuda"),
-                kc=kc, vc=vc, kpool=kpool, vpool=vpool, ptab=ptab, cos=cos, sin=sin, q=q, qpos=qpos, rowof=rowof)
+                kc=kc, vc=vc, kpool=kpool, kr=kr, vpool=vpool, ptab=ptab, cos=cos, sin=sin, q=q, qpos=qpos,
+                rowof=rowof)
     use_pool = bool(store_every)
     a = nat.AttnPagedArgs(q=q.data_ptr(), q_rows_cap=q.shape[0], kc=kc.data_ptr(), vc=vc.data_ptr(),
                           layers_cap=layers, kv_rows_cap=kv_rows, layer=layer,
-                          pool_k=kpool.data_ptr() if use_pool else None, pool_v=vpool.data_ptr() if use_pool else None,
+                          pool_k=kr.data_ptr() if use_pool else None, pool_v=vpool.data_ptr() if use_pool else None,
                           pool_rows=kpool.shape[0], page_table=ptab.data_ptr(), page_rows=page_rows,
                           cos_tab=cos.data_ptr(), sin_tab=sin.data_ptr(), tab_ld=hd // 2, kv=kv, heads=heads,
                           head_dim=hd, chunks=keep["ch"].data_ptr(), items=keep["it"].data_ptr(),

@@ -39,8 +39,8 @@ def c3_case(hd=128, heads=28, T=1024, imgs=4, keep=51, pre=16, post=16, seed=0):
         s0 = pre + m * T
         qpos += list(range(s0, s0 + keep))
         for t0 in range(0, T, 64):
-            if t0 >= keep:
-                chunks.append([s0 + t0, 64, m * (T // 64) + t0 // 64, 0])
+            if t0 >= keep:     # K rotated at its cached position (start 8): shift D = s0 - 8
+                chunks.append([s0 + t0, 64 | ((s0 - 8) << 8), m * (T // 64) + t0 // 64, 0])
             else:
                 chunks.append([s0 + t0, 64, s0 + t0, -1])
     s1 = pre + imgs * T
