@@ -18,6 +18,31 @@ __global__ void embed_assemble_kernel(float* __restrict__ x, int ldx,
   if (r >= rows) return;
   const int2 s = src[r];
   float* dst = x + (long)r * ldx;
+  if ((d & 3) == 0 && (ldx & 3) == 0) {
+    // 128-bit loads / stores, all of a thread's loads issued before its stores
+    constexpr int U = 4;
+    const int d4 = d >> 2;
+    float4* o = reinterpret_cast<float4*>(dst);
+    for (int i0 = threadIdx.x; i0 < d4; i0 += U * blockDim.x) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * blockDim.x;
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i >= d4 || (s.x == 0 && s.y < 0)) continue;   // negative text id: zero embedding (model.py:349-353)
+        if (s.x == 0) {
+          const uint2 e = __ldg(reinterpret_cast<const uint2*>(embed + (long)s.y * d) + i);
+          v[u] = make_float4(bf16_lo(e.x), bf16_hi(e.x), bf16_lo(e.y), bf16_hi(e.y));
+        } else {
+          v[u] = __ldg(reinterpret_cast<const float4*>((s.x == 1 ? enc_a : enc_b) + (long)s.y * d) + i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i0 + u * blockDim.x < d4) o[i0 + u * blockDim.x] = v[u];
+    }
+    return;
+  }
   if (s.x == 0 && s.y < 0) {          // negative text id: zero embedding (model.py:349-353)
     for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = 0.f;
   } else if (s.x == 0) {
