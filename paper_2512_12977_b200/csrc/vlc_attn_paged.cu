@@ -61,6 +61,8 @@ struct PaCfg {
   static constexpr int SMEM = 1024 + 2 * Q_BYTES + (KST + VST) * KV_BYTES + BAR_BYTES;
   static_assert(VST * KV_BYTES >= XM_BYTES, "merge exchange lives in the V ring");
   static_assert(VST >= 2 && KST >= VST, "K / V rings");
+  static_assert((KST + VST) * KV_BYTES >= 128 * HD * 4, "split partials are staged in the K/V ring");
+  static_assert((KST + VST) * KV_BYTES >= 256 * 8 * 12 + 256 * 4, "merge tables live in the K/V ring");
   // TMEM: S[b] at 128 b (b = 0, 1: KT fp32 columns, P bf16 pairs over its first half of each chunk's
   // columns); O_h (h = chunk half) at 256 + 128 h (HD columns)
   __device__ static constexpr uint32_t s_col(int b) { return 128u * b; }
@@ -128,7 +130,8 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
   uint64_t* s_full = v_empty + C::VST;    // [2] S buffer b complete
   uint64_t* p_full = s_full + 2;          // [2] P written over S buffer b (all 256 softmax threads)
   uint64_t* o_done = p_full + 2;          // PV(j) complete (one phase per tile)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
+  uint64_t* all_done = o_done + 1;        // every MMA of the CTA complete (K/V ring reusable)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(all_done + 1);
 
   const int* it = a.items + blockIdx.x * 8;
   const int q_row0 = it[0], nq = it[1], head = it[2], chunk0 = it[3];
@@ -160,6 +163,7 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
       mbar_init(&p_full[b], 32 * PA_SOFT_WARPS);
     }
     mbar_init(o_done, 1);
+    mbar_init(all_done, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -302,6 +306,7 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
         issue_pv(j);
         if (j + 2 < nt) issue_s(j + 2);       // in order after PV(j): reuses P(j)'s TMEM columns
       }
+      tc_commit(all_done);
     }
     __syncwarp();
   } else if (warp >= 2 + PA_SOFT_WARPS) {
@@ -495,11 +500,13 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
         }
       }
     } else {
-      // Split partial: the row's unnormalised fp32 O (this thread's half of the head dims) straight
-      // from registers to ws_o (row-major [row][HD]; each thread writes whole 32-byte sectors), plus
-      // the row's (max, sum).
+      // Split partial: once every MMA of the CTA is complete the K/V ring is free; stage the tile's
+      // fp32 O rows there (row-major, float4 slot c4 at c4 ^ (row & 7): bank-conflict free, same
+      // layout in ws_o) and write them with one bulk copy.
       const long prow0 = ((long)group * 8 + part) * 256;
-      float4* dst = reinterpret_cast<float4*>(a.ws_o + (prow0 + r) * HD) + hh * (OW / 4);
+      if (nt > 0) mbar_wait(all_done, 0);
+      tc_fence_after();
+      float4* stg = reinterpret_cast<float4*>(sK) + r * (HD / 4);
 #pragma unroll
       for (int c = 0; c < OW / OC; ++c) {
         float o[OC];
@@ -509,12 +516,16 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < OC; ++i) o[i] = 0.f;
         }
-        if (q_valid) {
 #pragma unroll
-          for (int q = 0; q < OC / 4; ++q)
-            __stcg(dst + c * (OC / 4) + q, make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]));
+        for (int q = 0; q < OC / 4; ++q) {
+          const int c4 = (hh * OW + c * OC) / 4 + q;
+          stg[c4 ^ (r & 7) % (HD / 4)] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
         }
       }
+      fence_proxy_async_smem();
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (quad == 0 && lane == 0 && hh == 0 && nq > 0)
+        bulk_store_wait(a.ws_o + prow0 * HD, sK, (uint32_t)(nq * HD * 4));
       if (q_valid && hh == 0) __stcg(reinterpret_cast<float2*>(a.ws_ml) + prow0 + r, make_float2(m_run, l_run));
       __threadfence();
     }
@@ -528,7 +539,9 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
   if (threadIdx.x == 0) PA_TRACE(51);
   if (group < 0) return;
   // ---------------- parallel merge of the nsplit partials (all CTAs of the group co-resident).
-  // This CTA merges rows [r_lo, r_hi) of the group.
+  // This CTA merges rows [r_lo, r_hi) of the group: pass 1 turns each row's (m, l) per split into
+  // normalised weights (smem, in the K/V ring, free once this CTA's partial is written); pass 2 is
+  // one thread per (row, float4 of the head) with every split's load independent.
   if (threadIdx.x == 0) {
     atomicAdd(&a.counters[group], 1);
     volatile int* cnt = a.counters + group;
@@ -539,41 +552,53 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
   if (threadIdx.x == 0) PA_TRACE(52);
   const int r_lo = nq * part / nsplit, r_hi = nq * (part + 1) / nsplit;
   const int nr = max(0, r_hi - r_lo);
+  float2* s_ml = reinterpret_cast<float2*>(sK);                 // [nr][8]
+  float* s_w = reinterpret_cast<float*>(s_ml + 256 * 8);        // [nr][8] weight / L
+  int* s_orow = reinterpret_cast<int*>(s_w + 256 * 8);          // [nr]
   const long gbase = (long)group * 8 * 256;
-  // one thread per (row, float4 of the head): every split's (max, sum) and O float4 and the row's
-  // output index load together (one dependent round trip), then the weighted sum
+  for (int t = threadIdx.x; t < nr * 8; t += PA_THREADS) {
+    const int rr = t >> 3, s2 = t & 7;
+    s_ml[t] = s2 < nsplit ? __ldcg(reinterpret_cast<const float2*>(a.ws_ml) + gbase + s2 * 256 + r_lo + rr)
+                          : make_float2(-INFINITY, 0.f);
+  }
+  for (int rr = threadIdx.x; rr < nr; rr += PA_THREADS) s_orow[rr] = a.rowof[q_row0 + r_lo + rr];
+  __syncthreads();
+  for (int rr = threadIdx.x; rr < nr; rr += PA_THREADS) {
+    float M = -INFINITY;
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2) M = fmaxf(M, s_ml[rr * 8 + s2].x);
+    float w[8], L = 0.f;
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2) {
+      const float2 ml = s_ml[rr * 8 + s2];
+      w[s2] = ml.x == -INFINITY ? 0.f : exp2f(ml.x - M);
+      L += w[s2] * ml.y;
+    }
+    const float inv = L > 0.f ? 1.0f / L : 0.f;
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2) s_w[rr * 8 + s2] = w[s2] * inv;
+  }
+  __syncthreads();
   constexpr int C4 = HD / 4;
   for (int t = threadIdx.x; t < nr * C4; t += PA_THREADS) {
     const int rr = t / C4, c4 = t % C4;
     const int row = r_lo + rr;
-    float2 ml[8];
+    const float4* src = reinterpret_cast<const float4*>(a.ws_o) + (gbase + row) * C4 + ((c4 ^ (row & 7)) % C4);
     float4 xs[8];
 #pragma unroll
-    for (int s2 = 0; s2 < 8; ++s2) {
-      if (s2 < nsplit) {
-        ml[s2] = __ldcg(reinterpret_cast<const float2*>(a.ws_ml) + gbase + s2 * 256 + row);
-        xs[s2] = __ldcg(reinterpret_cast<const float4*>(a.ws_o) + (gbase + s2 * 256 + row) * C4 + c4);
-      }
-    }
-    const int orow_i = a.rowof[q_row0 + row];
-    float M = -INFINITY;
-#pragma unroll
     for (int s2 = 0; s2 < 8; ++s2)
-      if (s2 < nsplit) M = fmaxf(M, ml[s2].x);
-    float L = 0.f;
+      if (s2 < nsplit) xs[s2] = __ldcg(src + (long)s2 * 256 * C4);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int s2 = 0; s2 < 8; ++s2) {
       if (s2 >= nsplit) break;
-      const float w = ml[s2].x == -INFINITY ? 0.f : exp2f(ml[s2].x - M);
-      L += w * ml[s2].y;
+      const float w = s_w[rr * 8 + s2];
       acc.x += w * xs[s2].x; acc.y += w * xs[s2].y; acc.z += w * xs[s2].z; acc.w += w * xs[s2].w;
     }
-    const float inv = L > 0.f ? 1.0f / L : 0.f;
-    const int col = head * HD + c4 * 4;
+    const int orow_i = s_orow[rr], col = head * HD + c4 * 4;
     const long off = a.pk_rows > 0 ? packed_off(orow_i, col, a.pk_rows, a.pk_kb) : (long)orow_i * a.ldo + col;
     *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.out) + off) =
-        make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
+        make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
   }
   __syncthreads();
   if (threadIdx.x == 0) PA_TRACE(53);
