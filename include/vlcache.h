@@ -81,11 +81,13 @@ typedef struct vlc_epilogue {
 
 /* Paged attention (vlc_attn_paged; model.py:274-291, engine.py:179-182): the recomputed queries of
  * one layer over all keys of their request.  The keys are a list of 64-key CHUNKS (contiguous
- * positions) per (request, layer): chunks int32[n][4] = {pos0, len <= 64, a, b}
+ * positions) per (request, layer): chunks int32[n][4] = {pos0, len <= 64 | D << 8, a, b}
  *   b <  0: request rows a .. a+63 of kc / vc (K already rotated: text / recomputed tokens);
  *   b >= 0: store rows page_table[a] * page_rows + b .. +63 of pool_k / pool_v (cached image tokens,
- *           K pre-RoPE: rotated to positions pos0 .. pos0+63 in shared memory with the fp32 tables).
- * A 128-key tile = two consecutive chunks (lists padded to an even length with len = 0 chunks).
+ *           K rotated at the position it was cached at, pos - D): the kernel multiplies them against its
+ *           queries rotated by -D (fp32 tables, row |D|), since q . R(D) k_cached = (R(-D) q) . k_cached.
+ * A 128-key tile = two consecutive chunks (lists padded to an even length with len = 0 chunks); its
+ * store chunks share one D.
  * items int32[n][8] = {q_row0, n_q <= 128, head, chunk0, tile_begin, tile_end, group,
  * (part << 8) | nsplit}: queries q_row0 .. (position-sorted, positions qpos, output rows rowof)
  * over tiles [tile_begin, tile_end) of the chunk list starting at chunk0.  group < 0 writes

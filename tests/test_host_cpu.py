@@ -346,7 +346,8 @@ def test_key_chunks_cover_every_key_once(pre, T, nimg, suf, ratios, P):
     ppl = -(-T // P)
     spec.page_rows = [np.arange(len(ratios) * ppl, dtype=np.int32).reshape(len(ratios), ppl) for _ in range(nimg)]
     base = {m: m * len(ratios) * ppl for m in range(nimg)}
-    spec.origin = [8 + 5 * m for m in range(nimg)]
+    # cached starts before and after the new ones: positive and negative shifts D
+    spec.origin = [s0 + (8 - 13 * m) for m, (s0, _) in enumerate(spec.images)]
     for i in range(len(ratios)):
         ch = request_chunks(spec, i, 1000, base).copy()
         assert len(ch) % 2 == 0
