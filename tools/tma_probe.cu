@@ -5,7 +5,8 @@
 #include "../paper_2512_12977_b200/csrc/vlc_ptx.cuh"
 using namespace vlc;
 
-__global__ void bulk_stream(const uint8_t* src, long bytes_per_cta, int chunk, int stages, unsigned long long* sink) {
+__global__ void bulk_stream(const uint8_t* src, long bytes_per_cta, int chunk, int stages, unsigned long long* sink,
+                            long wrap = 0, int shared = 0) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + stages * chunk);
   if (threadIdx.x == 0) {
@@ -14,14 +15,17 @@ __global__ void bulk_stream(const uint8_t* src, long bytes_per_cta, int chunk, i
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
-  const uint8_t* base = src + (long)blockIdx.x * bytes_per_cta;
+  // wrap > 0: the CTA re-reads a window of `wrap` bytes (L2-resident after the first pass); shared: all
+  // CTAs read the same window
+  const uint8_t* base = src + (wrap > 0 ? (shared ? 0 : (long)blockIdx.x * wrap) : (long)blockIdx.x * bytes_per_cta);
+  auto at = [&](long i) { return base + (wrap > 0 ? (i * chunk) % wrap : i * chunk); };
   const long n = bytes_per_cta / chunk;
-  const uint64_t pol = policy_evict_first();
+  const uint64_t pol = wrap > 0 ? policy_evict_normal() : policy_evict_first();
   unsigned long long acc = 0;
   long issued = 0;
   for (; issued < n && issued < stages; ++issued) {
     mbar_expect_tx(&full[issued], chunk);
-    bulk_load(sm + issued * chunk, base + issued * chunk, chunk, &full[issued], pol);
+    bulk_load(sm + issued * chunk, at(issued), chunk, &full[issued], pol);
   }
   for (long i = 0; i < n; ++i) {
     const int s = i % stages;
@@ -29,7 +33,7 @@ __global__ void bulk_stream(const uint8_t* src, long bytes_per_cta, int chunk, i
     acc += sm[s * chunk + (i & 63)];
     if (issued < n) {
       mbar_expect_tx(&full[s], chunk);
-      bulk_load(sm + s * chunk, base + issued * chunk, chunk, &full[s], pol);
+      bulk_load(sm + s * chunk, at(issued), chunk, &full[s], pol);
       ++issued;
     }
   }
@@ -104,5 +108,14 @@ __global__ void mma_probe(int n, int groups, int variant, unsigned long long* ou
 extern "C" int probe_mma(int n, int groups, int variant, void* out, cudaStream_t s, int ctas) {
   cudaFuncSetAttribute(mma_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   mma_probe<<<ctas, 128, 200 * 1024, s>>>(n, groups, variant, (unsigned long long*)out);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int probe_bulk_l2(const void* src, long bytes_per_cta, int chunk, int stages, int ctas, long wrap, int shared,
+                             void* sink, cudaStream_t s) {
+  const int smem = stages * chunk + stages * 8 + 64;
+  cudaFuncSetAttribute(bulk_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+  bulk_stream<<<ctas, 32, smem, s>>>((const uint8_t*)src, bytes_per_cta, chunk, stages, (unsigned long long*)sink,
+                                     wrap, shared);
   return (int)cudaGetLastError();
 }
