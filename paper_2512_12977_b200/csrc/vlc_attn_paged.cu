@@ -335,13 +335,14 @@ __global__ void __launch_bounds__(PA_THREADS, 1)
       if (c0.w < 0 && c1.w < 0) continue;
       const int d = (c0.w >= 0 ? c0.y : c1.y) >> 8;
       if (run >= 0 && d == run_d) continue;
+      // the rotation's table entries load while the queries land / the previous run's MMAs drain
+      const int ad = d < 0 ? -d : d;
+      const float2 c = __ldg(reinterpret_cast<const float2*>(a.cos_tab + (long)ad * a.tab_ld + f0));
+      float2 sn = __ldg(reinterpret_cast<const float2*>(a.sin_tab + (long)ad * a.tab_ld + f0));
       if (run < 0) mbar_wait(q_full, 0);
       else mbar_wait(q1_free, run & 1);      // the MMAs on the previous image's rotation are complete
       ++run;
       run_d = d;
-      const int ad = d < 0 ? -d : d;
-      const float2 c = __ldg(reinterpret_cast<const float2*>(a.cos_tab + (long)ad * a.tab_ld + f0));
-      float2 sn = __ldg(reinterpret_cast<const float2*>(a.sin_tab + (long)ad * a.tab_ld + f0));
       if (d < 0) sn = make_float2(-sn.x, -sn.y);
       const float2 nsn = make_float2(-sn.x, -sn.y);
       for (int k0 = 0; k0 < STEPS; k0 += B) {

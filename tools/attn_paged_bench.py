@@ -121,6 +121,15 @@ def trace(a, items):
         k = int(np.median(nt))
         row = np.nanmedian(rel[nt >= k, base:base + min(k, 16)], axis=0)
         print(f"  {lab:10s} per tile (median CTA): " + " ".join(f"{x:5.2f}" for x in row))
+    # per split part (items[:, 7] = part << 8 | nsplit): when each part starts, ends its loop, posts its partial
+    part, nsp = items[:, 7] >> 8, items[:, 7] & 0xFF
+    for ns_ in sorted(set(nsp.tolist())):
+        for p_ in range(ns_):
+            sel = (nsp == ns_) & (part == p_)
+            if sel.any():
+                print(f"  nsplit {ns_} part {p_}: n={sel.sum():3d} tiles {np.median(nt[sel]):4.1f}  S(0) "
+                      f"{np.nanmedian(rel[sel, 2]):5.2f}  loop_end {np.nanmedian(rel[sel, 50]):5.2f}  partial "
+                      f"{np.nanmedian(rel[sel, 51]):5.2f} (max {np.nanmax(rel[sel, 51]):5.2f})")
     print(f"  per-tile     med {np.median(it):.3f} us  min {np.min(it):.3f} max {np.max(it):.3f}  "
           f"tiles/CTA med {np.median(nt):.0f} max {nt.max()}  total {nt.sum()}")
 
