@@ -38,14 +38,20 @@ for a in sys.argv[1:]:
     variants[name] = [(k, int(v)) for k, v in (kv.split(":") for kv in spec.split(",") if kv)]
 if not variants:
     variants = {"base": []}
-defaults = {k: getattr(runner, k) for v in variants.values() for k, _ in v}
+# NAME=attr:value sets a Runner attribute; NAME=@key:value a vlc_set_tuning key (default from TUNE_DEFAULTS)
+TUNE_DEFAULTS = {16: 1, 17: 2, 18: 1, 9: 64, 10: 160, 7: 1}
+defaults = {k: (TUNE_DEFAULTS[int(k[1:])] if k.startswith("@") else getattr(runner, k))
+            for v in variants.values() for k, _ in v}
 
 
 def apply(v):
-    for k, val in defaults.items():
-        setattr(runner, k, val)
-    for k, val in v:
-        setattr(runner, k, bool(val) if isinstance(defaults[k], bool) else val)
+    from paper_2512_12977_b200 import _native as N
+    for k, val in list(defaults.items()) + list(v):
+        if k.startswith("@"):
+            N.load().vlc_set_tuning(int(k[1:]), int(val))
+        else:
+            setattr(runner, k, bool(val) if isinstance(defaults[k], bool) else val)
+    runner.graphs.clear()              # launch configurations are captured with the graph
 
 
 res = {n: [] for n in variants}

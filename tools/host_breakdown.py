@@ -67,3 +67,24 @@ for _ in range(N):
 print(f"prefill_with_reuse host {1e3 * tot / N:.3f} ms per call")
 for k, v in sorted(acc.items(), key=lambda kv: -kv[1]):
     print(f"  {k:32s} {1e3 * v / N:.3f} ms")
+# end to end as the bench measures it: API call -> last-row logits on the host
+e2e, host = [], []
+for _ in range(N):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = P.prefill_with_reuse(model, req, store)
+    t1 = time.perf_counter()
+    r.last_logits()
+    t2 = time.perf_counter()
+    e2e.append(t2 - t0)
+    host.append(t1 - t0)
+ev = []
+for _ in range(N):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    P.prefill_with_reuse(model, req, store)
+    e1.record()
+    e1.synchronize()
+    ev.append(e0.elapsed_time(e1))
+print(f"e2e p50 {1e3 * np.median(e2e):.3f} ms (host issue {1e3 * np.median(host):.3f} ms), device events p50 "
+      f"{np.median(ev):.3f} ms (no L2 flush)")
