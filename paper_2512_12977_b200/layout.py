@@ -18,8 +18,6 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
-import os
-
 import numpy as np
 
 SRC_TEXT, SRC_STORE, SRC_SCRATCH = 0, 1, 2

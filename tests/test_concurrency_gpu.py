@@ -17,7 +17,6 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.timeout(600)
 def test_two_threads_match_serial_results(cuda_ok):
     import paper_2512_12977_b200 as P
-    from paper_2512_12977_b200 import _native as N
     from paper_2512_12977_b200.engine import _runner
     sc = Scene(P, "C1", 2, export=False)
     L = sc.cfg.num_layers
