@@ -37,9 +37,11 @@ extern "C" {
  * (the SWIZZLE_128B image UMMA expects).  Element (row, k), KB = ceil(K/128):
  *   ((((rt*KB + kb)*2 + atom)*R + r)*64 + ((c ^ (r&7)) << 3) + e),
  *   rt = row/R, r = row%R, kb = k>>7, atom = (k>>6)&1, c = (k>>3)&7, e = k&7.
- * Weights use R = 128; activations use R = vlc_gemm_row_tile(m_tokens) of the consuming GEMM.
+ * Weights use R = 128; activations use R = vlc_gemm_row_tile(n_pad, m_tokens) of the consuming GEMM.
  * One (rt, kb) block is one cp.async.bulk copy, which is what lets a CTA stream at HBM speed. */
-int vlc_gemm_row_tile(int m_tokens);
+/* <= 256 tokens per row tile, except a one-wave GEMM (n_pad / 128 <= #SMs) keeps 257..512 tokens in one
+ * wide tile (two UMMA N chunks into one TMEM accumulator). */
+int vlc_gemm_row_tile(int n_pad, int m_tokens);
 /* Row-major bf16 [rows][cols] (leading dimension ld) -> packed (R, KB); padding is untouched. */
 int vlc_pack_operand(const void* src, int rows, int cols, int ld, void* dst, int R, int KB,
                      cudaStream_t stream);
@@ -167,7 +169,7 @@ int vlc_store_write_pages(const void* src, int src_f32, int layers, int tokens, 
                           int page_tokens, cudaStream_t stream);
 
 /* Fused-epilogue tcgen05 GEMM: acc[f][j] = sum_k W[f][k] X[j][k]; W PACKED (R = 128) with
- * n_pad rows, X PACKED with R = vlc_gemm_row_tile(m_tokens) and >= ceil(m/R)*R rows (x_rows_cap),
+ * n_pad rows, X PACKED with R = vlc_gemm_row_tile(n_pad, m_tokens) and >= ceil(m/R)*R rows (x_rows_cap),
  * both with K = k_pad (% 128 == 0).  n_pad % 128 == 0.
  * Stream-K schedule over (128-row weight tile x token tile x 64-wide k-block) units on
  * max_ctas co-resident CTAs (0 = one per SM); tiles shared by several CTAs are reduced in

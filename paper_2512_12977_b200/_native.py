@@ -71,7 +71,7 @@ def load():
         lib.vlc_kv_relocate.argtypes = [vp, vp, i, vp, i, i, vp, vp, i, vp, vp, i, vp, vp, i, vp]
         lib.vlc_store_write_pages.argtypes = [vp, i, i, i, i, vp, i, vp, i, vp]
         lib.vlc_gemm_bf16.argtypes = [vp, i, i, vp, i, i, C.POINTER(Epilogue), i, vp, C.c_size_t, vp, vp]
-        lib.vlc_gemm_row_tile.argtypes = [i]
+        lib.vlc_gemm_row_tile.argtypes = [i, i]
         lib.vlc_pack_operand.argtypes = [vp, i, i, i, vp, i, i, vp]
         lib.vlc_attn_paged.argtypes = [C.POINTER(AttnPagedArgs), vp]
         lib.vlc_patchify.argtypes = [vp, i, i, vp, i, i, i, vp]
@@ -103,9 +103,20 @@ def ptr(t) -> int:
     return 0 if t is None else int(t.data_ptr())
 
 
-def row_tile(m_tokens: int) -> int:
-    """Row tile R of the packed activations consumed by a GEMM over m_tokens rows."""
-    return 256 if m_tokens >= 256 else max(16, (m_tokens + 15) // 16 * 16)
+_ROW_TILES: dict = {}
+
+
+def row_tile(m_tokens: int, n_pad: int | None = None) -> int:
+    """Row tile R of the packed activations consumed by a GEMM of n_pad weight rows over m_tokens rows
+    (vlc_gemm_row_tile: <= 256, except 257..512 tokens stay one wide tile in a one-wave GEMM).  Without
+    n_pad: the <= 256 rule (kernels other than the GEMM's activation input)."""
+    if n_pad is None or m_tokens <= 256 or m_tokens > 512:
+        return 256 if m_tokens >= 256 else max(16, (m_tokens + 15) // 16 * 16)
+    key = (int(n_pad), int(m_tokens))
+    r = _ROW_TILES.get(key)
+    if r is None:
+        r = _ROW_TILES[key] = int(load().vlc_gemm_row_tile(int(n_pad), int(m_tokens)))
+    return r
 
 
 def packed_numel(rows: int, K: int, R: int) -> int:

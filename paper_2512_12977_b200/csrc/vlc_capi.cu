@@ -189,7 +189,7 @@ int vlc_store_write_pages(const void* src, int src_f32, int layers, int tokens, 
                      "store_write_pages");
 }
 
-int vlc_gemm_row_tile(int m_tokens) { return gemm_row_tile(m_tokens); }
+int vlc_gemm_row_tile(int n_pad, int m_tokens) { return gemm_row_tile(n_pad, m_tokens); }
 
 int vlc_pack_operand(const void* src, int rows, int cols, int ld, void* dst, int R, int KB, cudaStream_t stream) {
   if (!src || !dst || rows < 0 || cols <= 0 || ld < cols || R <= 0 || R % 8 || KB * 128 < cols)
@@ -203,7 +203,7 @@ int vlc_gemm_bf16(const void* w, int n_pad, int k_pad, const void* x, int x_rows
   if (!w || !x || !epi) return fail(VLC_ERR_INVALID, "gemm: null pointer");
   if (n_pad % 128 || k_pad % 128 || n_pad <= 0 || k_pad <= 0)
     return fail(VLC_ERR_UNSUPPORTED, "gemm: n_pad and k_pad must be multiples of 128");
-  const int rt = gemm_row_tile(m_tokens);
+  const int rt = gemm_row_tile(n_pad, m_tokens);
   if (m_tokens > 0 && x_rows_cap < (m_tokens + rt - 1) / rt * rt)
     return fail(VLC_ERR_INVALID, "gemm: x_rows_cap must cover whole row tiles of the packed activations");
   if ((epi->kind == VLC_EPI_BF16 || epi->kind == VLC_EPI_SWIGLU) && epi->pk_rows > 0 && epi->pk_rows % 8)

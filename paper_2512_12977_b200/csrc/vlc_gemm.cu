@@ -17,6 +17,8 @@
 //   F32       logits (engine.py:187)
 //   BIAS_ADD  encoder patch embedding + bias + positional rows (model.py:316)
 //   QKV_PLAIN encoder projections (model.py:318)
+#include <type_traits>
+
 #include "vlc_internal.h"
 #include "vlc_gemm_epi.cuh"
 
@@ -149,36 +151,47 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (dec && warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = make_idesc_bf16(GEMM_BM, n_tile, 0, 0);
+      // N chunks: <= 256 tokens per UMMA; a wide tile (257..512) is two halves into adjacent columns
+      const int nw0 = n_tile > 256 ? ((n_tile / 2 + 15) & ~15) : n_tile, nw1 = n_tile - nw0;
+      const uint32_t idesc = make_idesc_bf16(GEMM_BM, nw0, 0, 0);
+      const uint32_t idesc1 = make_idesc_bf16(GEMM_BM, nw1 > 0 ? nw1 : 16, 0, 0);
       mbar_wait(&acc_empty[0], 1);
       tc_fence_after();
       const int xper = sk.xh ? 2 : 1;   // activation slots per k-block
       long long c0 = 0;
       if (sk.dbg) { asm volatile("mov.u64 %0, %%clock64;" : "=l"(c0)); DBG(5); }
-      for (int kb = 0; kb < dnkb; ++kb) {   // kb: index within this CTA's single k-range
-        const int ws_ = kb % wst;
-        mbar_wait(&full[ws_], (kb / wst) & 1);
-        const uint32_t a_addr = smem_u32(sa + ws_ * a_bytes);
+      // the narrow loop keeps the code of a single N chunk; wide tiles issue both chunks per K step
+      auto mainloop = [&](auto wide_tag) {
+        constexpr bool WIDE = decltype(wide_tag)::value;
+        for (int kb = 0; kb < dnkb; ++kb) {   // kb: index within this CTA's single k-range
+          const int ws_ = kb % wst;
+          mbar_wait(&full[ws_], (kb / wst) & 1);
+          const uint32_t a_addr = smem_u32(sa + ws_ * a_bytes);
 #pragma unroll
-        for (int hx = 0; hx < 2; ++hx) {
-          if (hx >= xper) break;
-          const int u = kb * xper + hx, xs = u % xst;
-          mbar_wait(&xfull[xs], (u / xst) & 1);
-          tc_fence_after();
-          const uint32_t b_addr = smem_u32(sb + xs * x_unit);
+          for (int hx = 0; hx < 2; ++hx) {
+            if (hx >= xper) break;
+            const int u = kb * xper + hx, xs = u % xst;
+            mbar_wait(&xfull[xs], (u / xst) & 1);
+            tc_fence_after();
+            const uint32_t b_addr = smem_u32(sb + xs * x_unit);
 #pragma unroll
-          for (int k = 0; k < GEMM_BK / 16; ++k) {
-            const int at = k >> 2;
-            if (xper == 2 && at != hx) continue;   // half slots: atom hx of the k-block only
-            const uint64_t ad = make_sdesc(a_addr + at * (GEMM_BM * 128) + (k & 3) * 32, 16, 1024, 128);
-            const uint64_t bd = make_sdesc(b_addr + (xper == 2 ? 0 : at * (n_tile * 128)) + (k & 3) * 32, 16,
-                                           1024, 128);
-            tc_mma_f16(tmem, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < GEMM_BK / 16; ++k) {
+              const int at = k >> 2;
+              if (xper == 2 && at != hx) continue;   // half slots: atom hx of the k-block only
+              const uint64_t ad = make_sdesc(a_addr + at * (GEMM_BM * 128) + (k & 3) * 32, 16, 1024, 128);
+              const uint32_t b0 = b_addr + (xper == 2 ? 0 : at * (n_tile * 128)) + (k & 3) * 32;
+              tc_mma_f16(tmem, ad, make_sdesc(b0, 16, 1024, 128), idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              if constexpr (WIDE)   // tokens nw0 .. n_tile: rows nw0.. of the same activation block
+                tc_mma_f16(tmem + nw0, ad, make_sdesc(b0 + nw0 * 128, 16, 1024, 128), idesc1,
+                           (kb > 0 || k > 0) ? 1u : 0u);
+            }
+            tc_commit(&xempty[xs]);
           }
-          tc_commit(&xempty[xs]);
+          tc_commit(&empty[ws_]);
         }
-        tc_commit(&empty[ws_]);
-      }
+      };
+      if (nw1 > 0) mainloop(std::true_type{});
+      else mainloop(std::false_type{});
       tc_commit(&acc_full[0]);
       if (sk.dbg) {   // mainloop SM cycles next to globaltimer slots 5 / 6: the SM clock under load
         mbar_wait(&acc_full[0], 0);
@@ -485,9 +498,14 @@ static int num_sms() {
   return n;
 }
 
-int gemm_row_tile(int m_tokens) {
+// Token (row) tile of a GEMM's packed activations: <= 256 rows per UMMA N, except that a one-wave GEMM
+// (<= #SMs weight tiles) keeps 257..512 tokens in ONE wide tile -- two N chunks into one 512-column TMEM
+// accumulator -- rather than two token tiles (which would double the CTAs past one wave: C3 at 6%
+// recompute, c = 276 rows, ran at 1.9x the TTFT of 5%).
+int gemm_row_tile(int n_pad, int m_tokens) {
+  const int t = ((m_tokens + 15) / 16) * 16;
+  if (m_tokens > 256 && m_tokens <= 512 && n_pad > 0 && n_pad / 128 <= num_sms()) return t;
   if (m_tokens >= 256) return 256;
-  int t = ((m_tokens + 15) / 16) * 16;
   return t < 16 ? 16 : t;
 }
 
@@ -496,7 +514,8 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
                         int m_tokens, const GemmEpi& epi, int max_ctas, float* ws, size_t ws_bytes,
                         int* counters, cudaStream_t stream) {
   if (m_tokens <= 0) return cudaSuccess;
-  const int n_tile = gemm_row_tile(m_tokens);
+  const int n_tile = gemm_row_tile(n_pad, m_tokens);
+  const bool wide = n_tile > 256;   // one wide token tile: one k-range of one weight tile per CTA, decoupled rings
   // Multi-wave GEMMs (the LM head) with token tiles >= pair_min: the CTA-pair stream-K kernel
   // (vlc_gemm_pair.cu; head at c = 236: 282 -> 258 us, profiles/r2_gemm_pair_streamk.txt).  The
   // one-wave projections stay on the single-CTA kernel: under stream-K over all 74 pairs they are
@@ -511,7 +530,7 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
                                            max_ctas > 0 ? max_ctas / 2 : 0, ws, ws_bytes, counters, stream);
     if (e != cudaErrorNotSupported) return e;
   }
-  const bool wide_ok = n_pad % 256 == 0;
+  const bool wide_ok = n_pad % 256 == 0 && !wide;
   const int H = (g_wide == 2 && wide_ok) || (g_wide == 0 && wide_ok && n_tile >= 96) ? 2 : 1;
   const int BM = GEMM_BM * H, BK = GEMM_BK / H;
   const int KB = k_pad / BK;
@@ -539,9 +558,14 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
     int best = 0;
     for (int sp = 2; sp <= KB / min_units; ++sp)
       if ((KB % sp == 0 || (g_aligned_split == 2 && n_tile >= 160)) && tiles * sp <= G) best = sp;
-    if (best > 0 && tiles * best * 10 >= 7LL * G) G = (int)(tiles * best);
+    if (best > 0 && (tiles * best * 10 >= 7LL * G || wide)) G = (int)(tiles * best);
   }
-  if ((long long)G * min_units > U) G = (int)(U / min_units);
+  if (wide) {
+    // a single accumulator of n_tile columns: every CTA owns exactly one k-range of one weight tile
+    if (tiles > num_sms()) return cudaErrorInvalidValue;
+    if ((long long)G < tiles || G % tiles != 0 || G > num_sms()) G = (int)tiles;
+  }
+  if (!wide && (long long)G * min_units > U) G = (int)(U / min_units);
   if (G < 1) G = 1;
   const size_t need = (size_t)G * 2 * BM * n_tile * sizeof(float);
   if (!red && (need > ws_bytes || counters == nullptr)) {
@@ -555,21 +579,23 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   // (measured: QKV / gate-up at c = 236: 31.5 / 32.0 -> 29.9 / 29.6 us; slower at c = 112, where the
   // coupled ring already holds 3 stages -> only for token tiles >= 160)
   // (also for tile-aligned split-K: G a multiple of the tile count -> one k-range of one tile per CTA)
-  if (g_decoupled && H == 1 && n_tile >= g_dec_min_tile && G >= (int)tiles && G % (int)tiles == 0 &&
-      tiles * KB == U && U / G >= 2) {
+  if ((g_decoupled || wide) && H == 1 && n_tile >= g_dec_min_tile && G >= (int)tiles && G % (int)tiles == 0 &&
+      tiles * KB == U && (U / G >= 2 || wide)) {
     const int a_b = GEMM_BM * GEMM_BK * 2, b_b = n_tile * GEMM_BK * 2;
     const int budget = 232448 - 1024 - 512;
     // key 18 value v: v in [2, 9] activation k-block stages; v >= 10: (v - 10) half-k-block stages
-    const int xh = g_decoupled >= 10 ? 1 : 0;
+    // wide tiles: half-k-block activation slots when whole ones would leave < 2 weight stages
+    const int xh = g_decoupled >= 10 || (wide && budget - 2 * b_b < 2 * a_b) ? 1 : 0;
     // g_decoupled == 1: floor(100 KB / activation stage) >= 2 activation stages -- measured best on C3:
     // 2 stages of 61 KB at c = 236, 3 of 28 KB at c = 112 (TTFT at r = 2%: 3.57 -> 3.49 ms)
     const int sx_auto = 100 * 1024 / b_b < 2 ? 2 : 100 * 1024 / b_b;
     const int sx = xh ? (g_decoupled - 10 >= 2 ? g_decoupled - 10 : 2)
-                      : (g_decoupled >= 2 ? g_decoupled : sx_auto);
+                      : (g_decoupled >= 2 && !wide ? g_decoupled : sx_auto);
     const int xu = xh ? b_b / 2 : b_b;
     const int sw = (budget - sx * xu) / a_b;
     if (sw >= 2 && sw * a_b >= 2 * 32 * 128 * 4) { sk.sw = sw > 8 ? 8 : sw; sk.sx = sx; sk.xh = xh; }
   }
+  if (wide && sk.sw <= 0) return cudaErrorInvalidValue;   // wide tiles run only on the decoupled rings
   const int smem = sk.sw > 0 ? 1024 + sk.sw * GEMM_BM * GEMM_BK * 2 + sk.sx * n_tile * GEMM_BK * (sk.xh ? 1 : 2) +
                                    (2 * sk.sw + 2 * sk.sx + 4) * 8 + 64
                              : gemm_smem_bytes(n_tile, stages, H);

@@ -314,7 +314,8 @@ static int pair_smem(int n_tile, int stages) {
 cudaError_t launch_gemm_pair(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap, int m_tokens,
                              const GemmEpi& epi, int max_pairs, float* ws, size_t ws_bytes, int* counters,
                              cudaStream_t stream) {
-  const int n_tile = gemm_row_tile(m_tokens);
+  const int n_tile = gemm_row_tile(n_pad, m_tokens);
+  if (n_tile > 256) return cudaErrorNotSupported;
   if (n_pad % 256 || k_pad % 128 || n_tile % 16 || n_tile < 32) return cudaErrorNotSupported;
   const int tok_tiles = (m_tokens + n_tile - 1) / n_tile;
   if (x_rows_cap < tok_tiles * n_tile) return cudaErrorInvalidValue;

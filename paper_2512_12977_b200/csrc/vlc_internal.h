@@ -76,7 +76,7 @@ cudaError_t launch_relocate(const RelocArgs& r, cudaStream_t stream);
 cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap,
                         int m_tokens, const GemmEpi& epi, int max_ctas, float* ws, size_t ws_bytes,
                         int* counters, cudaStream_t stream);
-int gemm_row_tile(int m_tokens);
+int gemm_row_tile(int n_pad, int m_tokens);
 cudaError_t launch_gemm_pair(const void* W, int n_pad, int k_pad, const void* X, int x_rows_cap, int m_tokens,
                              const GemmEpi& epi, int max_pairs, float* ws, size_t ws_bytes, int* counters,
                              cudaStream_t stream);

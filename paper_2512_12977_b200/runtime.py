@@ -240,7 +240,7 @@ class Runner:
 
     # ---------------------------------------------------------------- primitives
     def gemm(self, w, k_pad, x, m, epi: N.Epilogue, splits: int | None = None, name="gemm", k_valid=None):
-        """w: PackedWeight; x: packed activations (row tile N.row_tile(m)), flat bf16 tensor."""
+        """w: PackedWeight; x: packed activations (row tile N.row_tile(m, w.n)), flat bf16 tensor."""
         if m <= 0:
             return
         if splits is None:
@@ -248,7 +248,7 @@ class Runner:
         epi.m_tokens = m
         if epi.kind == N.EPI_RESID and self.deterministic:
             epi.deterministic = 1
-        R = N.row_tile(m)
+        R = N.row_tile(m, w.n)
         kv_ = k_valid or k_pad
         nbytes = 2 * epi.n_valid * kv_ + 2 * m * kv_
         self._run(name, lambda: N.check(self.lib.vlc_gemm_bf16(
@@ -305,9 +305,9 @@ class Runner:
         k = len(pixels_list)
         M = k * T
         cap = -(-max(256, M) // 256) * 256
-        Rp = N.row_tile(T)
+        E = dw.enc
+        Rp = N.row_tile(T, E["patch_w"].n)
         rows_img = -(-T // Rp) * Rp
-        RM = N.row_tile(M)
         patches = ws.get("patches", (k * rows_img * dw.kp,), torch.bfloat16)
         xe = ws.get("xe", (cap, d), torch.float32)
         xn = ws.get("xn", (cap * dw.kd,), torch.bfloat16)
@@ -321,7 +321,6 @@ class Runner:
         host = np.stack([np.asarray(px, dtype=np.float32).reshape(side, side) for px in pixels_list])
         dev_px = ws.get("pixels", (k, side, side), torch.float32, zero=False)
         dev_px[:k].copy_(torch.from_numpy(host).pin_memory(), non_blocking=True)
-        E = dw.enc
         for m in range(k):
             self._run("patchify", lambda m=m: N.check(self.lib.vlc_patchify(
                 dev_px[m].data_ptr(), side, p, patches.data_ptr(), m * rows_img, Rp, dw.kp // 128, _stream()),
@@ -331,8 +330,12 @@ class Runner:
             self.gemm(E["patch_w"], dw.kp, patches[m * rows_img * dw.kp:], T,
                       _epi(kind=N.EPI_BIAS_ADD, n_valid=d, out=xe[m * T].data_ptr(), ldo=d,
                            bias=E["patch_b"].data_ptr(), add=E["pos"].data_ptr(), ld_add=d))
-        pkd, pkkv, pkh = (RM, dw.kd // 128), (RM, dw.kkv_enc // 128), (RM, dw.kh // 128)
-        self.rmsnorm(xe, E["attn_norm"], xn, M, pk=pkd)
+        # each GEMM input packed with that GEMM's row tile
+        pkq = (N.row_tile(M, E["wqkv_plain"].n), dw.kd // 128)
+        pkkv = (N.row_tile(M, E["wo"].n), dw.kkv_enc // 128)
+        pkg = (N.row_tile(M, E["wgu"].n), dw.kd // 128)
+        pkh = (N.row_tile(M, E["wd"].n), dw.kh // 128)
+        self.rmsnorm(xe, E["attn_norm"], xn, M, pk=pkq)
         self.gemm(E["wqkv_plain"], dw.kd, xn, M,
                   _epi(kind=N.EPI_QKV_PLAIN, n_valid=3 * kv, out=qe.data_ptr(), ldo=kv, out2=ke.data_ptr(), ld2=kv,
                        out3=ve.data_ptr(), ld3=kv, seg=kv, hd=cfg.head_dim))
@@ -352,7 +355,7 @@ class Runner:
         self.attention(qe, ke, ve, 0, pack.ptr("chunks"), pack.ptr("items"), len(items), pack.ptr("qpos"),
                        pack.ptr("rowof"), att, slots, pk=pkkv, kv=kv, heads=cfg.num_heads)
         self.gemm(E["wo"], dw.kkv_enc, att, M, _epi(kind=N.EPI_RESID, n_valid=d, out=xe.data_ptr(), ldo=d))
-        self.rmsnorm(xe, E["mlp_norm"], xn, M, pk=pkd)
+        self.rmsnorm(xe, E["mlp_norm"], xn, M, pk=pkg)
         self.gemm(E["wgu"], dw.kd, xn, M,
                   _epi(kind=N.EPI_SWIGLU, n_valid=2 * cfg.mlp_hidden, out=hb.data_ptr(), ldo=dw.kh,
                        pk_rows=pkh[0], pk_kb=pkh[1]))
@@ -548,8 +551,10 @@ class Runner:
         for i in range(L):
             ci = int(c[i])
             W = dw.layers[i]
-            Ri = N.row_tile(ci)
-            self.rmsnorm(x, W["attn_norm"], xn, ci, pk=(Ri, kd))
+            # each GEMM input packed with that GEMM's row tile (one wide tile for 257..512 rows)
+            Rq, Ro = N.row_tile(ci, W["wqkv"].n), N.row_tile(ci, W["wo"].n)
+            Rg, Rd = N.row_tile(ci, W["wgu"].n), N.row_tile(ci, W["wd"].n)
+            self.rmsnorm(x, W["attn_norm"], xn, ci, pk=(Rq, kd))
             self.gemm(W["wqkv"], dw.kd, xn, ci, _epi(
                 kind=N.EPI_QKV_ROPE, n_valid=3 * kv, out=q.data_ptr(), ldo=kv,
                 out2=kc[i].data_ptr(), ld2=kv, out3=vc[i].data_ptr(), ld3=kv, out4=kpre[i].data_ptr(), ld4=kv,
@@ -569,7 +574,7 @@ class Runner:
             self.attention(q, kc, vc, i, pack.ptr(f"chunks{i}"), pack.ptr(f"items{i}"), len(lay.attn_items[i]),
                            pack.ptr(f"qpos{i}"), pack.ptr(f"rowof{i}"), att, lay.attn_slots,
                            nbytes=lay.kv_rows * kv * 4 + ci * kv * 4, flops=4 * cfg.head_dim * dw.heads * vis,
-                           pk=(Ri, dw.kkv // 128), pool=kv_pool_obj, page_table=pack.ptr("pages"))
+                           pk=(Ro, dw.kkv // 128), pool=kv_pool_obj, page_table=pack.ptr("pages"))
             if i in buf.get("capture", {}):
                 # captured attention block output (engine.py:273-275): O projection alone, then
                 # x += it fused with the MLP norm
@@ -578,11 +583,11 @@ class Runner:
                           name="gemm_o", k_valid=kv)
                 self._run("rmsnorm", lambda cap=cap, W=W: N.check(self.lib.vlc_add_rmsnorm(
                     x.data_ptr(), d, cap.data_ptr(), d, W["mlp_norm"].data_ptr(), xn.data_ptr(), d, ci, d, RMS_EPS,
-                    Ri, kd, _stream()), "vlc_add_rmsnorm"))
+                    Rg, kd, _stream()), "vlc_add_rmsnorm"))
             elif self.tp_group is None:
                 self.gemm(W["wo"], dw.kkv, att, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d),
                           name="gemm_o", k_valid=kv)
-                self.rmsnorm(x, W["mlp_norm"], xn, ci, pk=(Ri, kd))
+                self.rmsnorm(x, W["mlp_norm"], xn, ci, pk=(Rg, kd))
             else:
                 # head-parallel: row-parallel O projection of this rank's heads -> y, one all-reduce
                 # of y over the group (NCCL / NVLink), then x += y fused into the MLP norm
@@ -593,14 +598,14 @@ class Runner:
                 self._allreduce(y[:ci])
                 self._run("rmsnorm", lambda: N.check(self.lib.vlc_add_rmsnorm(
                     x.data_ptr(), d, y.data_ptr(), d, W["mlp_norm"].data_ptr(), xn.data_ptr(), d, ci, d, RMS_EPS,
-                    Ri, kd, _stream()), "vlc_add_rmsnorm"), ci * d * 14)
+                    Rg, kd, _stream()), "vlc_add_rmsnorm"), ci * d * 14)
             self.gemm(W["wgu"], dw.kd, xn, ci,
                       _epi(kind=N.EPI_SWIGLU, n_valid=2 * cfg.mlp_hidden, out=hb.data_ptr(), ldo=dw.kh,
-                           pk_rows=Ri, pk_kb=dw.kh // 128),
+                           pk_rows=Rd, pk_kb=dw.kh // 128),
                       name="gemm_gate_up", k_valid=d)
             self.gemm(W["wd"], dw.kh, hb, ci, _epi(kind=N.EPI_RESID, n_valid=d, out=x.data_ptr(), ldo=d),
                       name="gemm_down", k_valid=cfg.mlp_hidden)
-        self.rmsnorm(x, dw.final_norm, xn, cL, row_map=pack.ptr("final"), pk=(N.row_tile(cL), kd))
+        self.rmsnorm(x, dw.final_norm, xn, cL, row_map=pack.ptr("final"), pk=(N.row_tile(cL, dw.head.n), kd))
         self.gemm(dw.head, dw.kd, xn, cL, _epi(kind=N.EPI_F32, n_valid=V, out=logits.data_ptr(), ldo=V),
                   name="gemm_head", k_valid=d)
 

@@ -35,7 +35,7 @@ def _gemm(nat, W, X, m, epi, splits=1):
     """W [n_pad, k_pad] and X [rows, k_pad] row-major bf16 -> packed operands -> vlc_gemm_bf16."""
     ws = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
     cnt = torch.zeros(16384, dtype=torch.int32, device="cuda")
-    R = nat.row_tile(m)
+    R = nat.row_tile(m, W.shape[0])
     Wp = nat.pack(W, 128)
     Xp = nat.pack(X[:m], R, rows_cap=-(-m // R) * R)
     nat.check(nat.load().vlc_gemm_bf16(Wp.data_ptr(), W.shape[0], W.shape[1], Xp.data_ptr(), -(-m // R) * R, m,
@@ -306,6 +306,23 @@ def test_attention_paged_store_page_size_128(nat):
     nat.check(nat.load().vlc_attn_paged(a, _stream()), "attn_paged")
     torch.cuda.synchronize()
     assert (out[keep["rowof"].long()].float() - ref).abs().max().item() < 2e-2
+
+
+@pytest.mark.parametrize("n_pad,k_pad,m", [(10752, 3584, 276), (1024, 512, 400), (256, 128, 300), (3584, 7168, 512),
+                                           (14336, 3584, 260)])
+def test_gemm_wide_token_tile(nat, n_pad, k_pad, m):
+    """257..512 tokens of a one-wave GEMM stay ONE wide token tile (two UMMA N chunks into one TMEM
+    accumulator, decoupled rings, one k-range per CTA): F32 and RESID (split-K red.add) epilogues."""
+    assert nat.row_tile(m, n_pad) == -(-m // 16) * 16
+    test_gemm_f32_matches_torch(nat, n_pad, k_pad, m, 0)
+    g = torch.Generator(device="cuda").manual_seed(n_pad + m + 5)
+    W = torch.randn(n_pad, k_pad, device="cuda", generator=g).bfloat16()
+    X = torch.randn(max(512, m), k_pad, device="cuda", generator=g).bfloat16()
+    x = torch.randn(m, n_pad, device="cuda", generator=g)
+    x0 = x.clone()
+    _gemm(nat, W, X, m, _epi(nat, kind=nat.EPI_RESID, n_valid=n_pad, m_tokens=m, out=x.data_ptr(), ldo=n_pad), 0)
+    ref = x0 + X[:m].float() @ W.float().t()
+    assert (x - ref).abs().max().item() / ref.abs().max().item() < 1e-5
 
 
 @pytest.mark.parametrize("dec", [0, 1, 3, 12])

@@ -17,7 +17,7 @@ cnt = torch.zeros(1 << 16, dtype=torch.int32, device="cuda")
 def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1, packed=False, mode=0, red=False):
     nw = max(2, min(8, (1 << 30) // (n * k * 2)))   # rotate > L2 worth of weights
     Ws = [N.pack(torch.randn(n, k, device="cuda").bfloat16(), 128) for _ in range(nw)]
-    R = N.row_tile(m)
+    R = N.row_tile(m, n)
     fn = lib.vlc_gemm_bf16
     X = N.pack(torch.randn(m, k, device="cuda").bfloat16(), R, rows_cap=-(-m // R) * R)
     out = torch.zeros(m + 256, n, device="cuda", dtype=torch.float32)
@@ -52,7 +52,7 @@ def run(n, k, m, splits, kind=N.EPI_BF16, stages=0, reps=20, coop=1, packed=Fals
 
 def phases(n, k, m, ctas, kind=None):
     """Per-CTA phase timestamps of one launch (DRAM-cold weights)."""
-    R = N.row_tile(m)
+    R = N.row_tile(m, n)
     W = N.pack(torch.randn(n, k, device="cuda").bfloat16(), 128)
     X = N.pack(torch.randn(m, k, device="cuda").bfloat16(), R, rows_cap=-(-m // R) * R)
     out = torch.zeros(m + 256, n, device="cuda", dtype=torch.float32)
@@ -107,7 +107,7 @@ if __name__ == "__main__":
         lib.vlc_set_tuning(18, 0)
     if mode == "clock":           # SM clock during the decoupled QKV / GU mainloop (cycles / ns)
         for (n, kk, m) in ((10752, 3584, 236), (14336, 3584, 236)):
-            R = N.row_tile(m)
+            R = N.row_tile(m, n)
             W = N.pack(torch.randn(n, kk, device="cuda").bfloat16(), 128)
             X = N.pack(torch.randn(m, kk, device="cuda").bfloat16(), R, rows_cap=-(-m // R) * R)
             out = torch.zeros(m + 256, n, device="cuda", dtype=torch.float32)
