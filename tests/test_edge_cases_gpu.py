@@ -84,3 +84,11 @@ def test_hit_next_to_miss(env):
 @pytest.mark.parametrize("r", [0.002, 0.3])
 def test_grid_extremes(env, r):
     _run(env, O.prompt(501, 9, 8), [0], O.prompt(501, 9, 9), (r,) * 3)
+
+
+@pytest.mark.parametrize("npre,nsuf", [(150, 100), (300, 260)])
+def test_wide_and_multi_token_tiles(env, npre, nsuf):
+    """Long text around repeated cached images: 257..512 computed rows run every one-wave GEMM as ONE
+    wide token tile (two UMMA N chunks), > 512 rows as several token tiles; parity with the oracle."""
+    got = _run(env, O.prompt(501, npre, 11), [0, 0, 0], O.prompt(501, nsuf, 12), (0.3, 0.3, 0.1))
+    assert max(got.metrics.computed_per_layer) > 256
