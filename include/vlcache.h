@@ -79,6 +79,9 @@ typedef struct vlc_epilogue {
   /* RESID: split-K partials reduced in a fixed order through `ws` (bitwise reproducible runs)
    * instead of red.add in arrival order (faster).  0 = red.add.                               */
   int deterministic;
+  /* QKV_ROPE, optional: the RoPE tables interleaved, rows of head_dim floats (cos t, cos t+1, sin t,
+   * sin t+1 for even t) -- one 16-byte load per token instead of two (NULL: cos_tab / sin_tab). */
+  const float* cs_tab;
 } vlc_epilogue;
 
 /* Paged attention (vlc_attn_paged; model.py:274-291, engine.py:179-182): the recomputed queries of

@@ -34,7 +34,7 @@ class Epilogue(C.Structure):
                 ("cos_tab", C.c_void_p), ("sin_tab", C.c_void_p), ("tab_ld", C.c_int),
                 ("hd", C.c_int), ("seg", C.c_int), ("bias", C.c_void_p), ("add", C.c_void_p),
                 ("ld_add", C.c_int), ("pk_rows", C.c_int), ("pk_kb", C.c_int),
-                ("deterministic", C.c_int)]
+                ("deterministic", C.c_int), ("cs_tab", C.c_void_p)]
 
 
 class AttnPagedArgs(C.Structure):

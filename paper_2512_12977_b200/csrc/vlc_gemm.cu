@@ -67,6 +67,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 //        k-blocks: the activation bytes per weight byte halve, which keeps the L2 traffic of
 //        c ~ 240-token GEMMs under the LTS cap.  Single accumulator of 2 x n_tile columns.
 // The A (weight) bytes of a stage are 32 KB in both cases.
+// decoupled rings: the QKV_ROPE token tile's staged positions / destination rows + their barrier
+constexpr int ROPE_STAGE_BYTES = 4096 + 64;
 template <int KIND, int H>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_tc(const uint8_t* __restrict__ wp, const uint8_t* __restrict__ xp, GemmEpi epi, SkSched sk,
@@ -91,6 +93,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   float* stage_all = dec ? reinterpret_cast<float*>(smem)   // [2][32][128] fp32
                          : reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(acc_empty) + 64);
+  // decoupled rings, QKV_ROPE: the token tile's positions and destination rows ([512] + [512] int32, 4 KB)
+  int* s_rope = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(acc_empty) + 64);
+  uint64_t* rope_bar = reinterpret_cast<uint64_t*>(s_rope + 1024);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int g = blockIdx.x;
@@ -116,6 +121,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_empty[s], 32 * GEMM_EPI_WARPS);
     }
+    if (dec) mbar_init(rope_bar, 32 * (GEMM_EPI_WARPS - 1));
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -331,9 +337,30 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           // metadata + RoPE tables of chunk c+1 load while chunk c is stored; chunk 0's before the
           // accumulator is ready (all independent of it)
           const int nch = (n_tile + 31) / 32;
+          // decoupled rings (one tile per CTA): the tile's positions / destination rows go to shared memory
+          // while the mainloop runs -- warps 3..9 stage them (warp 2 is feeding the activation ring), every
+          // epilogue warp waits on rope_bar
+          const int* s_pos = nullptr;
+          const int* s_dr = nullptr;
+          if (dec) {
+            if (warp != 2) {
+              const int sec = m0 / epi.seg;
+              for (int i = threadIdx.x - 96; i < n_tile; i += 32 * (GEMM_EPI_WARPS - 1)) {
+                const int j = tok0 + i;
+                const bool ok = j < epi.m_tokens;
+                s_rope[i] = ok && sec != 2 ? __ldg(epi.pos + j) : 0;
+                s_rope[512 + i] = !ok ? 0 : sec == 0 ? (epi.map1 ? __ldg(epi.map1 + j) : j) : __ldg(epi.map2 + j);
+              }
+              mbar_arrive(rope_bar);
+            }
+            mbar_wait(rope_bar, 0);
+            s_pos = s_rope - tok0;
+            s_dr = s_rope + 512 - tok0;
+          }
           RopeMeta ma, mb;   // two register-resident sets, roles alternate (no copies, no local memory)
           if (eg < nch)
-            rope_prefetch(epi, m0 + 4 * lane, tok0 + eg * 32, quad, min(32, epi.m_tokens - tok0 - eg * 32), ma);
+            rope_prefetch(epi, m0 + 4 * lane, tok0 + eg * 32, quad, min(32, epi.m_tokens - tok0 - eg * 32), ma,
+                          s_pos, s_dr);
           mbar_wait(&acc_full[slot], (seg >> 1) & 1);
           tc_fence_after();
           if (leader) DBG(3);
@@ -346,8 +373,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj) stage_buf[jj * 128 + row] = v[jj];
             asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
-            if (ci + 2 < nch)
-              rope_prefetch(epi, m0 + 4 * lane, tok0 + c + 64, quad, min(32, epi.m_tokens - tok0 - c - 64), nxt);
+            if (ci + 2 < nch)     // the chunk after next's tables load while this chunk is stored
+              rope_prefetch(epi, m0 + 4 * lane, tok0 + c + 64, quad, min(32, epi.m_tokens - tok0 - c - 64), nxt,
+                            s_pos, s_dr);
             rope_store(epi, m0 + 4 * lane, tok0 + c, quad, min(32, epi.m_tokens - tok0 - c), cur,
                        stage_buf + 4 * lane);
             asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
@@ -582,7 +610,7 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   if ((g_decoupled || wide) && H == 1 && n_tile >= g_dec_min_tile && G >= (int)tiles && G % (int)tiles == 0 &&
       tiles * KB == U && (U / G >= 2 || wide)) {
     const int a_b = GEMM_BM * GEMM_BK * 2, b_b = n_tile * GEMM_BK * 2;
-    const int budget = 232448 - 1024 - 512;
+    const int budget = 232448 - 1024 - 512 - ROPE_STAGE_BYTES;   // align, barriers, QKV_ROPE token metadata
     // key 18 value v: v in [2, 9] activation k-block stages; v >= 10: (v - 10) half-k-block stages
     // wide tiles: half-k-block activation slots when whole ones would leave < 2 weight stages
     const int xh = g_decoupled >= 10 || (wide && budget - 2 * b_b < 2 * a_b) ? 1 : 0;
@@ -597,7 +625,7 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   }
   if (wide && sk.sw <= 0) return cudaErrorInvalidValue;   // wide tiles run only on the decoupled rings
   const int smem = sk.sw > 0 ? 1024 + sk.sw * GEMM_BM * GEMM_BK * 2 + sk.sx * n_tile * GEMM_BK * (sk.xh ? 1 : 2) +
-                                   (2 * sk.sw + 2 * sk.sx + 4) * 8 + 64
+                                   (2 * sk.sw + 2 * sk.sx + 4) * 8 + 64 + ROPE_STAGE_BYTES
                              : gemm_smem_bytes(n_tile, stages, H);
   const uint8_t* wpp = reinterpret_cast<const uint8_t*>(W);
   const uint8_t* xpp = reinterpret_cast<const uint8_t*>(X);

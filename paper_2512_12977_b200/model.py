@@ -423,6 +423,10 @@ class DeviceWeights:
         c, s = rope_tables_np(rows, self.cfg.head_dim, self.cfg.rope_base)
         self.cos = torch.from_numpy(c).cuda()
         self.sin = torch.from_numpy(s).cuda()
+        # interleaved copy for the QKV epilogue: per row, (cos t, cos t+1, sin t, sin t+1) for even t
+        h2 = c.shape[1]
+        cs = np.stack([c.reshape(rows, h2 // 2, 2), s.reshape(rows, h2 // 2, 2)], axis=2).reshape(rows, 2 * h2)
+        self.cs = torch.from_numpy(np.ascontiguousarray(cs)).cuda()
         self.tab_rows = rows
 
     def bytes_per_layer(self) -> int:

@@ -560,6 +560,7 @@ class Runner:
                 out2=kc[i].data_ptr(), ld2=kv, out3=vc[i].data_ptr(), ld3=kv, out4=kpre[i].data_ptr(), ld4=kv,
                 map1=pack.ptr(f"qdst{i}"), map2=pack.ptr("row_kv"), pos=pack.ptr("row_pos"),
                 cos_tab=dw.cos.data_ptr(), sin_tab=dw.sin.data_ptr(), tab_ld=cfg.head_dim // 2,
+                cs_tab=dw.cs.data_ptr() if cfg.head_dim % 4 == 0 else None,
                 hd=cfg.head_dim, seg=kv), name="gemm_qkv", k_valid=d)
             if "inject" in buf:
                 inj, ipk = buf["inject"]
@@ -683,6 +684,7 @@ class DeviceDecoder:
                 out2=self.kc[i].data_ptr(), ld2=kv, out3=self.vc[i].data_ptr(), ld3=kv,
                 map1=pack.ptr("zero"), map2=pack.ptr("pos"), pos=pack.ptr("pos"),
                 cos_tab=dw.cos.data_ptr(), sin_tab=dw.sin.data_ptr(), tab_ld=cfg.head_dim // 2,
+                cs_tab=dw.cs.data_ptr() if cfg.head_dim % 4 == 0 else None,
                 hd=cfg.head_dim, seg=kv), name="gemm_qkv", k_valid=d)
             r.attention(self.q, self.kc, self.vc, i, pack.ptr("chunks"), pack.ptr("items"), len(items),
                         pack.ptr("pos"), pack.ptr("zero"), self.att, groups, pk=(R, dw.kkv // 128))

@@ -56,6 +56,10 @@ def _run_rank(rank, world, backend, port, q):
         from paper_2512_12977_b200.sharding import head_split
         O, oc, w, enc, kv, h, text, ref = _scene()
         model = P.ToyVLM(P.ModelConfig(**KW), w).head_parallel()
+        # the ranks must agree bitwise: the replicated residual GEMMs reduce their split-K partials
+        # in a fixed order (red.add arrival order differs run to run, and so between the ranks)
+        from paper_2512_12977_b200.engine import _runner
+        _runner(model).deterministic = True
         h0, hk = head_split(KW["num_heads"], world)[rank]
         c0, c1 = h0 * oc.head_dim, (h0 + hk) * oc.head_dim
         store = P.CacheStore()

@@ -110,21 +110,26 @@ def _perm_rows(kv, hd):
     return torch.tensor(idx)
 
 
-@pytest.mark.parametrize("hd,heads", [(128, 3), (32, 8), (16, 2)])
-def test_gemm_qkv_rope_epilogue(nat, hd, heads):
+@pytest.mark.parametrize("hd,heads,m,cs_tab", [(128, 3, 37, False), (32, 8, 37, False), (16, 2, 37, False),
+                                              (128, 3, 37, True), (32, 8, 37, True), (128, 4, 300, True),
+                                              (128, 2, 200, False)])
+def test_gemm_qkv_rope_epilogue(nat, hd, heads, m, cs_tab):
+    """cs_tab: the interleaved (c0 c1 s0 s1) per-position table the model passes; without it the
+    epilogue reads the split cos/sin tables."""
     kv = hd * heads
-    d, m = 128, 37
+    d = 128
     g = torch.Generator(device="cuda").manual_seed(hd)
     Wq, Wk, Wv = (torch.randn(kv, d, device="cuda", generator=g).bfloat16() for _ in range(3))
     perm = _perm_rows(kv, hd).cuda()
     n_pad = ((3 * kv + 127) // 128) * 128
     W = torch.zeros(n_pad, d, device="cuda", dtype=torch.bfloat16)
     W[:kv], W[kv:2 * kv], W[2 * kv:3 * kv] = Wq[perm], Wk[perm], Wv
-    X = torch.randn(256, d, device="cuda", generator=g).bfloat16()
+    X = torch.randn(max(256, m), d, device="cuda", generator=g).bfloat16()
     pos = torch.randperm(500, device="cuda", generator=g)[:m].int()
     qmap = torch.randperm(m, device="cuda", generator=g).int()
     kvmap = (pos + 3).int()
     cos, sin = _tables(hd, 600)
+    cs = torch.stack([cos.reshape(600, hd // 4, 2), sin.reshape(600, hd // 4, 2)], 2).reshape(600, hd).contiguous()
     q = torch.zeros(m, kv, device="cuda", dtype=torch.bfloat16)
     kc = torch.zeros(600, kv, device="cuda", dtype=torch.bfloat16)
     vc = torch.zeros_like(kc)
@@ -132,7 +137,8 @@ def test_gemm_qkv_rope_epilogue(nat, hd, heads):
     epi = _epi(nat, kind=nat.EPI_QKV_ROPE, n_valid=3 * kv, m_tokens=m, out=q.data_ptr(), ldo=kv,
                out2=kc.data_ptr(), ld2=kv, out3=vc.data_ptr(), ld3=kv, out4=kpre.data_ptr(), ld4=kv,
                map1=qmap.data_ptr(), map2=kvmap.data_ptr(), pos=pos.data_ptr(), cos_tab=cos.data_ptr(),
-               sin_tab=sin.data_ptr(), tab_ld=hd // 2, hd=hd, seg=kv)
+               sin_tab=sin.data_ptr(), tab_ld=hd // 2, hd=hd, seg=kv,
+               cs_tab=cs.data_ptr() if cs_tab else None)
     _gemm(nat, W, X, m, epi, 2)
     Xf = X[:m].float()
     qr = _rope_ref(Xf @ Wq.float().t(), pos, hd)

@@ -8,6 +8,8 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2512_12977_b200 import _native as N  # noqa: E402
+if os.environ.get("VLC_LIB_VARIANT"):          # experiment builds (tools/build_variant.py)
+    N.LIB_PATH = os.environ["VLC_LIB_VARIANT"]
 
 lib = N.load()
 ws = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
@@ -45,9 +47,16 @@ def phases(W, n, k, X, R, e):
     torch.cuda.synchronize()
     lib.vlc_set_debug_buffer(None)
     d = dbg.view(148, 8).cpu().numpy().astype("float64")
-    d = d[d[:, 0] > 0]
+    alive = d[:, 0] > 0
+    d = d[alive]
     t0 = d[:, 0].min()
     d = np.where(d > 0, (d - t0) / 1e3, np.nan)
+    if n == 3 * kv and alive.sum() == n // 128:    # one tile per CTA: the section of CTA g is g * 128 // kv
+        sec = (np.arange(len(d)) * 128) // kv
+        for sidx, nm in enumerate("QKV"):
+            sel = sec == sidx
+            print(f"     section {nm}: acc_full med {np.nanmedian(d[sel, 3]):6.2f}  epilogue end med "
+                  f"{np.nanmedian(d[sel, 4]):6.2f} max {np.nanmax(d[sel, 4]):6.2f}")
     for i, nm in enumerate(["start", "prod_go", "prod_done", "acc_full", "partials_done", "fixup_go", "epi_end",
                             "exit"]):
         col = d[:, i]
@@ -76,6 +85,10 @@ def main():
     ang = np.arange(n_keys + 64, dtype=np.float32)[:, None] * inv
     cos = torch.from_numpy(np.cos(ang)).cuda()
     sin = torch.from_numpy(np.sin(ang)).cuda()
+    c_, s_ = np.cos(ang), np.sin(ang)
+    cs = torch.from_numpy(np.ascontiguousarray(np.stack([c_.reshape(len(ang), half // 2, 2),
+                                                         s_.reshape(len(ang), half // 2, 2)], axis=2)
+                                              .reshape(len(ang), hd))).cuda()
     out = torch.zeros(m + 256, n, device="cuda", dtype=torch.bfloat16)
     plain = N.Epilogue()
     plain.kind, plain.n_valid, plain.m_tokens, plain.out, plain.ldo = N.EPI_BF16, n, m, out.data_ptr(), n
@@ -83,7 +96,7 @@ def main():
     for kk, v in dict(kind=N.EPI_QKV_ROPE, n_valid=n, m_tokens=m, out=q.data_ptr(), ldo=kv, out2=kc.data_ptr(), ld2=kv,
                       out3=vc.data_ptr(), ld3=kv, out4=kpre.data_ptr(), ld4=kv, map1=qmap.data_ptr(),
                       map2=pos.data_ptr(), pos=pos.data_ptr(), cos_tab=cos.data_ptr(), sin_tab=sin.data_ptr(),
-                      tab_ld=half, hd=hd, seg=kv).items():
+                      tab_ld=half, hd=hd, seg=kv, cs_tab=cs.data_ptr() if os.environ.get("CS", "1") == "1" else None).items():
         setattr(rope, kk, v)
     if os.environ.get("ROPE_ONLY"):
         rope_nk = N.Epilogue()
