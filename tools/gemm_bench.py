@@ -94,6 +94,16 @@ if __name__ == "__main__":
             for (n, kk, m, c) in ((10752, 3584, 236, 0), (14336, 3584, 236, 0)):
                 phases(n, kk, m, c, kind="pair" if pair else None)
         lib.vlc_set_tuning(10, 96)
+    if mode == "pairtile":        # CTA-pair kernel with one 256-row tile per pair (no stream-K) vs single-CTA
+        for pair in (0, -16, 0, -16):
+            lib.vlc_set_tuning(10, pair)
+            print(f"=== pair {pair}", flush=True)
+            for (n, kk, m) in ((10752, 3584, 236), (14336, 3584, 236)):
+                c = n // 128 if pair else 0
+                run(n, kk, m, c)
+                if pair:
+                    phases(n, kk, m, c, kind="pair")
+        lib.vlc_set_tuning(10, 160)
     if mode == "decoupled":       # one-tile GEMMs with decoupled weight / activation rings (key 18)
         for dec in (2, 12, 13, 14, 2, 13):
             lib.vlc_set_tuning(18, dec)
