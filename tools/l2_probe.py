@@ -15,11 +15,15 @@ lib.probe_bulk_l2.argtypes = [C.c_void_p, C.c_long, C.c_int, C.c_int, C.c_int, C
 buf = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
 sink = torch.zeros(1024, dtype=torch.int64, device="cuda")
 s = torch.cuda.current_stream().cuda_stream
-for ctas in (84, 148):
+import sys
+SHARED = [int(a) for a in sys.argv[1:]] or [1]
+for shared in SHARED:
+  print(f"-- shared window {shared} (1: every CTA reads the same 3 MB window; 0: a private window per CTA)")
+  for ctas in (84, 148):
     for chunk, stages in ((4096, 32), (8192, 16), (16384, 12), (32768, 6), (49152, 4), (65536, 3), (98304, 2)):
         per = 32 << 20
-        wrap = 3 << 20
-        f = lambda: lib.probe_bulk_l2(buf.data_ptr(), per, chunk, stages, ctas, wrap, 1, sink.data_ptr(), s)  # noqa
+        wrap = 3 << 20 if shared else 512 << 10
+        f = lambda: lib.probe_bulk_l2(buf.data_ptr(), per, chunk, stages, ctas, wrap, shared, sink.data_ptr(), s)  # noqa
         f()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)

@@ -1,6 +1,7 @@
 // Calibration probe: per-SM streaming bandwidth of 1-D bulk copies (cp.async.bulk) with a
 // ring of `stages` x `chunk` bytes in flight, versus plain 128-bit vector loads.
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include "../paper_2512_12977_b200/csrc/vlc_ptx.cuh"
 using namespace vlc;
@@ -50,6 +51,71 @@ __global__ void ldg_stream(const uint4* src, long vec_per_cta, unsigned long lon
     acc ^= v.x ^ v.w;
   }
   if (acc == 0x12345) sink[blockIdx.x] = acc;
+}
+
+
+// Tensor-map (cp.async.bulk.tensor.2d) variant: rows of 128 B (64 bf16), box of chunk / 128 rows (<= 256),
+// 128-byte swizzle; `issuers` warps each run an independent ring of stages / issuers slots over their own
+// rows (issuers > 1 also for the 1-D variant below: does the SM's TMA unit overlap ops of several issuers?)
+__global__ void tensor_stream(const __grid_constant__ CUtensorMap map, long rows_per_cta, int box_rows, int stages,
+                              int issuers, int tensor, const uint8_t* src, unsigned long long* sink, long wrap_rows) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const int chunk = box_rows * 128;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + stages * chunk);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) != 0 || w >= issuers) return;
+  const int per = stages / issuers;                 // this issuer's slots [w * per, (w + 1) * per)
+  const long n = rows_per_cta / box_rows / issuers; // ops of this issuer
+  const uint64_t pol = policy_evict_normal();
+  auto row_of = [&](long i) { return ((long)blockIdx.x * 0 + (i * issuers + w) * box_rows) % wrap_rows; };
+  auto issue = [&](int s, long i) {
+    mbar_expect_tx(&full[s], chunk);
+    if (tensor) tma_load_2d(sm + s * chunk, &map, &full[s], 0, (int)row_of(i), pol);
+    else bulk_load(sm + s * chunk, src + row_of(i) * 128, chunk, &full[s], pol);
+  };
+  long issued = 0;
+  for (; issued < n && issued < per; ++issued) issue(w * per + (int)issued, issued);
+  unsigned long long acc = 0;
+  for (long i = 0; i < n; ++i) {
+    const int s = w * per + (int)(i % per);
+    mbar_wait(&full[s], (i / per) & 1);
+    acc += sm[s * chunk + (i & 63)];
+    if (issued < n) issue(s, issued++);
+  }
+  sink[blockIdx.x * 8 + w] = acc;
+}
+
+typedef CUresult (*EncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                          const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                          CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+extern "C" int probe_tensor(const void* src, long rows_total, long rows_per_cta, int box_rows, int stages, int issuers,
+                            int tensor, int ctas, void* sink, cudaStream_t s) {
+  static EncFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess) return -1;
+    fn = reinterpret_cast<EncFn>(p);
+  }
+  CUtensorMap m;
+  cuuint64_t dims[2] = {64, (cuuint64_t)rows_total};
+  cuuint64_t strides[1] = {128};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(src), dims, strides, box, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -2;
+  const int smem = stages * box_rows * 128 + stages * 8 + 64;
+  cudaFuncSetAttribute(tensor_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+  tensor_stream<<<ctas, 32 * issuers, smem, s>>>(m, rows_per_cta, box_rows, stages, issuers, tensor,
+                                                 (const uint8_t*)src, (unsigned long long*)sink, rows_total);
+  return (int)cudaGetLastError();
 }
 
 extern "C" int probe_bulk(const void* src, long bytes_per_cta, int chunk, int stages, int ctas, void* sink, cudaStream_t s) {
