@@ -498,11 +498,13 @@ def main():
                         "TFps": round(fl / s / 1e12, 2) if fl else None})
     dom = kernels[0]
     dname = dom["name"]
-    try:   # DRAM bytes per launch from the committed ncu --set full capture (tools/ncu_traffic.py)
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            traffic = json.load(fh)
-    except (OSError, ValueError):
-        traffic = {}
+    traffic = {}
+    if args.workload == "C3":   # DRAM bytes per launch from the committed ncu --set full capture of the C3
+        try:                    # layer (tools/ncu_traffic.py); other workloads: no capture, traffic null
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+                traffic = json.load(fh)
+        except (OSError, ValueError):
+            traffic = {}
     ms_d, cnt_d, nb_d, fl_d = agg[dname]
     if dname.startswith("gemm") or dname in ("kv_relocate", "rmsnorm", "embed"):
         ach = nb_d / (ms_d / 1e3) / 1e9
