@@ -185,3 +185,51 @@ extern "C" int probe_bulk_l2(const void* src, long bytes_per_cta, int chunk, int
                                      wrap, shared);
   return (int)cudaGetLastError();
 }
+
+// ---------------------------------------------------------------- tcgen05 cta_group::2 issue-rate probe
+// One cluster of 2 CTAs (an SM pair), operands = whatever is in smem (timing only): the leader issues
+// groups of 8 UMMAs M = 256 (128 rows per SM), N = n split over the pair, K = 16 each.
+__global__ void __cluster_dims__(2, 1, 1) mma2_probe(int n, int groups, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  if (warp == 0) tmem_alloc2<512>(&tslot);
+  if (threadIdx.x == 32) { mbar_init(&bar, 1); fence_barrier_init(); }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (rank == 0 && warp == 1 && lane == 0) {
+    const uint32_t idesc = make_idesc_bf16(256, n, 0, 0);
+    const uint32_t a = smem_u32(sm), b = smem_u32(sm + 32768);
+    const int atom_b = (n / 2) * 128;
+    long long t0 = clock64();
+    for (int g = 0; g < groups; ++g) {
+      for (int k = 0; k < 8; ++k) {
+        const uint64_t ad = make_sdesc(a + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, 128);
+        const uint64_t bd = make_sdesc(b + (k >> 2) * atom_b + (k & 3) * 32, 16, 1024, 128);
+        tc_mma2_f16(tmem, ad, bd, idesc, (g | k) ? 1u : 0u);
+      }
+    }
+    long long t1 = clock64();
+    tc_commit2_mc(&bar, 3);
+    mbar_wait(&bar, 0);
+    long long t2 = clock64();
+    out[0] = t1 - t0;
+    out[1] = t2 - t0;
+  }
+  if (rank == 1 && threadIdx.x == 32) mbar_wait(&bar, 0);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc2<512>(tmem); }
+}
+
+extern "C" int probe_mma2(int n, int groups, void* out, cudaStream_t s) {
+  cudaFuncSetAttribute(mma2_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  mma2_probe<<<2, 128, 200 * 1024, s>>>(n, groups, (unsigned long long*)out);
+  return (int)cudaGetLastError();
+}
