@@ -419,6 +419,19 @@ def test_gemm_cta_pair_f32(nat, pair_mode, n_pad, k_pad, m):
     assert (out - ref).abs().max().item() / ref.abs().max().item() < 1e-5
 
 
+@pytest.mark.parametrize("n_pad,k_pad,m", [(38016, 1024, 278), (38144, 512, 500), (76032, 256, 236)])
+def test_gemm_multiwave_head_token_tiles(nat, n_pad, k_pad, m):
+    """Multi-wave (LM-head-like) GEMM on the default schedule, the CTA-pair stream-K kernel: more than
+    256 rows take several token tiles, a weight tile's token tiles being consecutive units."""
+    g = torch.Generator(device="cuda").manual_seed(n_pad + m)
+    W = torch.randn(n_pad, k_pad, device="cuda", generator=g).bfloat16()
+    X = torch.randn(max(256, m), k_pad, device="cuda", generator=g).bfloat16()
+    ref = X[:m].float() @ W.float().t()
+    out = torch.full((m, n_pad), float("nan"), device="cuda")
+    _gemm(nat, W, X, m, _epi(nat, kind=nat.EPI_F32, n_valid=n_pad, m_tokens=m, out=out.data_ptr(), ldo=n_pad), 0)
+    assert (out - ref).abs().max().item() / ref.abs().max().item() < 1e-5
+
+
 def test_gemm_cta_pair_swiglu_packed(nat, pair_mode):
     g = torch.Generator(device="cuda").manual_seed(9)
     n, k, m = 1024, 512, 236
