@@ -14,6 +14,9 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 import paper_2512_12977_b200 as P  # noqa: E402
+from paper_2512_12977_b200 import _native as N  # noqa: E402
+if os.environ.get("VLC_LIB_VARIANT"):          # experiment builds (tools/build_variant.py)
+    N.LIB_PATH = os.environ["VLC_LIB_VARIANT"]
 from paper_2512_12977_b200.engine import _runner, prefill_with_reuse  # noqa: E402
 from paper_2512_12977_b200.toydata import make_images, prompt_ids  # noqa: E402
 

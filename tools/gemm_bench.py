@@ -6,6 +6,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 from paper_2512_12977_b200 import _native as N  # noqa: E402
+if os.environ.get("VLC_LIB_VARIANT"):          # experiment builds (tools/build_variant.py)
+    N.LIB_PATH = os.environ["VLC_LIB_VARIANT"]
 
 lib = N.load()
 ws = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
