@@ -1,0 +1,80 @@
+"""Seeded random reuse-prefill scenes on the device vs the CPU oracle (bf16-rounded weights): 1-3 images
+drawn (with repeats) from a store whose entries were cached at different positions (origins 0, 3, 11),
+sometimes one uncached image supplied as pixels (encoder miss + KV fallback), random text before / after
+the images, and a random valid plan (non-increasing grid ratios, 0 and 1 included).  Same bars as
+test_engine_gpu.py: rows / counts / hit-miss bit-exact, logits and merged K/V rel_err <= 2e-2, last-row
+top-1 equal."""
+import numpy as np
+import pytest
+
+from conftest import rel_err
+from oracle import kvreuse_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+KW = dict(num_layers=4, num_heads=4, model_dim=128, kv_dim=128, vocab_size=509, patch_size=4,
+          tokens_per_image=64, seed=21)
+ORIGINS = (0, 3, 11)
+GRID = [round(0.002 * k, 3) for k in range(1, 151)]
+
+
+@pytest.fixture(scope="module")
+def world(cuda_ok):
+    import paper_2512_12977_b200 as P
+    oc = O.Cfg(**KW)
+    w = {k: O.bf16_round(v) for k, v in O.make_weights(oc).items()}
+    model = P.ToyVLM(P.ModelConfig(**KW), w)
+    imgs = O.images(4, oc.side, 17)                    # images 0-2 cached, image 3 never
+    enc, kv = {}, {}
+    store = P.CacheStore()
+    for px, o in zip(imgs[:3], ORIGINS):
+        ids0, segs0 = O.layout(O.prompt(509, o, 40 + o), 1, 64)
+        O.fill_one(oc, w, ids0, segs0, [px], enc, kv)
+        h = O.sha256_hex(px)
+        store.put_encoder(P.EncoderCacheEntry(P.ImageHash(h), enc[h], model.fingerprint))
+        store.put_kv(P.KVCacheEntry(P.ImageHash(h), kv[h].keys, kv[h].values, kv[h].origin_position,
+                                    model.fingerprint))
+    return P, oc, w, model, imgs, enc, kv, store
+
+
+def _plan(rng, L):
+    first = rng.choice([1.0, 0.3, 0.1, 0.05, 0.01, 0.002, 0.0, -1.0])
+    if first < 0:                                       # any grid value, then non-increasing
+        first = GRID[int(rng.integers(len(GRID)))]
+    ratios = [float(first)]
+    for _ in range(L - 1):
+        prev = ratios[-1]
+        cands = [0.0] + [g for g in GRID if g <= prev + 1e-12] + ([1.0] if prev == 1.0 else [])
+        ratios.append(float(cands[int(rng.integers(len(cands)))]) if rng.random() < 0.6 else prev)
+    return tuple(ratios)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_scene_matches_oracle(world, seed):
+    P, oc, w, model, imgs, enc, kv, store = world
+    rng = np.random.default_rng(seed)
+    T = oc.tokens_per_image
+    n_img = int(rng.integers(1, 4))
+    idx = [int(rng.integers(3)) for _ in range(n_img)]
+    miss = seed % 4 == 3                                # one uncached image, pixels supplied
+    if miss:
+        idx[int(rng.integers(n_img))] = 3
+    prefix = O.prompt(509, int(rng.integers(0, 40)), 100 + seed)
+    suffix = O.prompt(509, int(rng.integers(1, 24)), 200 + seed)
+    ratios = _plan(rng, oc.num_layers)
+    ims = [imgs[i] for i in idx]
+    hs = [O.sha256_hex(px) for px in ims]
+    px = ims if miss else None
+    ids, segs = O.layout(prefix, n_img, T, suffix)
+    ref = O.reuse_prefill(oc, w, ids, segs, hs, ratios, dict(enc), dict(kv), images=px)
+    seq = P.make_sequence(prefix, n_img, T, suffix)
+    got = P.prefill_with_reuse(model, P.ReuseRequest(seq, [P.ImageHash(h) for h in hs], P.RecomputePlan(ratios),
+                                                     images=px), store)
+    assert np.array_equal(got.positions, ref.rows), (ratios, idx)
+    assert got.metrics.computed_per_layer == ref.counts
+    assert (got.metrics.encoder_misses, got.metrics.fallback_images) == (ref.encoder_misses, ref.fallback_images)
+    e = rel_err(got.logits, ref.logits)
+    assert e <= 2e-2, (e, ratios, idx)
+    assert int(np.argmax(got.logits[-1])) == int(np.argmax(ref.logits[-1]))
+    assert rel_err(got.kv.keys, ref.keys) <= 2e-2 and rel_err(got.kv.values, ref.values) <= 2e-2
