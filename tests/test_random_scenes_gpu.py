@@ -13,15 +13,18 @@ from oracle import kvreuse_oracle as O
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-KW = dict(num_layers=4, num_heads=4, model_dim=128, kv_dim=128, vocab_size=509, patch_size=4,
-          tokens_per_image=64, seed=21)
+KWS = {"hd32": dict(num_layers=4, num_heads=4, model_dim=128, kv_dim=128, vocab_size=509, patch_size=4,
+                   tokens_per_image=64, seed=21),
+       "hd64": dict(num_layers=3, num_heads=4, model_dim=256, kv_dim=256, vocab_size=509, patch_size=4,
+                   tokens_per_image=64, seed=22)}
 ORIGINS = (0, 3, 11)
 GRID = [round(0.002 * k, 3) for k in range(1, 151)]
 
 
-@pytest.fixture(scope="module")
-def world(cuda_ok):
+@pytest.fixture(scope="module", params=list(KWS))
+def world(cuda_ok, request):
     import paper_2512_12977_b200 as P
+    KW = KWS[request.param]
     oc = O.Cfg(**KW)
     w = {k: O.bf16_round(v) for k, v in O.make_weights(oc).items()}
     model = P.ToyVLM(P.ModelConfig(**KW), w)
@@ -50,10 +53,9 @@ def _plan(rng, L):
     return tuple(ratios)
 
 
-@pytest.mark.parametrize("seed", range(40))
-def test_random_scene_matches_oracle(world, seed):
+def _scene(world, rng, seed):
+    """(oracle result, device ReuseRequest) of one random request."""
     P, oc, w, model, imgs, enc, kv, store = world
-    rng = np.random.default_rng(seed)
     T = oc.tokens_per_image
     n_img = int(rng.integers(1, 4))
     idx = [int(rng.integers(3)) for _ in range(n_img)]
@@ -69,12 +71,37 @@ def test_random_scene_matches_oracle(world, seed):
     ids, segs = O.layout(prefix, n_img, T, suffix)
     ref = O.reuse_prefill(oc, w, ids, segs, hs, ratios, dict(enc), dict(kv), images=px)
     seq = P.make_sequence(prefix, n_img, T, suffix)
-    got = P.prefill_with_reuse(model, P.ReuseRequest(seq, [P.ImageHash(h) for h in hs], P.RecomputePlan(ratios),
-                                                     images=px), store)
-    assert np.array_equal(got.positions, ref.rows), (ratios, idx)
+    return ref, P.ReuseRequest(seq, [P.ImageHash(h) for h in hs], P.RecomputePlan(ratios), images=px)
+
+
+def _check(ref, got):
+    assert np.array_equal(got.positions, ref.rows)
     assert got.metrics.computed_per_layer == ref.counts
     assert (got.metrics.encoder_misses, got.metrics.fallback_images) == (ref.encoder_misses, ref.fallback_images)
     e = rel_err(got.logits, ref.logits)
-    assert e <= 2e-2, (e, ratios, idx)
-    assert int(np.argmax(got.logits[-1])) == int(np.argmax(ref.logits[-1]))
+    assert e <= 2e-2, e
+    a, b = int(np.argmax(got.logits[-1])), int(np.argmax(ref.logits[-1]))
+    # top-1 equal, unless the reference's own top-1 / that token gap is inside the logits tolerance
+    # (a near-tie: random small-vocab scenes produce them)
+    gap = float(ref.logits[-1][b] - ref.logits[-1][a])
+    assert a == b or gap <= 2e-2 * float(np.max(np.abs(ref.logits))), (a, b, gap)
     assert rel_err(got.kv.keys, ref.keys) <= 2e-2 and rel_err(got.kv.values, ref.values) <= 2e-2
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_scene_matches_oracle(world, seed):
+    P, model, store = world[0], world[3], world[7]
+    ref, req = _scene(world, np.random.default_rng(seed), seed)
+    _check(ref, P.prefill_with_reuse(model, req, store))
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_batch_matches_oracle(world, seed):
+    """prefill_batch_with_reuse over 2-4 random requests (varlen rows, one device pass): each result
+    against its own oracle run."""
+    P, model, store = world[0], world[3], world[7]
+    rng = np.random.default_rng(1000 + seed)
+    scenes = [_scene(world, rng, 1000 + 7 * seed + k) for k in range(int(rng.integers(2, 5)))]
+    outs = P.prefill_batch_with_reuse(model, [req for _, req in scenes], store)
+    for (ref, _), got in zip(scenes, outs):
+        _check(ref, got)
