@@ -55,6 +55,18 @@ struct PairSched {
     return p;
   }
 };
+#ifdef VLC_PAIR_TRACE   // experiment builds only: per-unit stamps [cta][64 units][4] in the debug buffer
+#define PTR(u, k)                                                                          \
+  do {                                                                                     \
+    if (sc.dbg && (u) < 64) {                                                              \
+      unsigned long long t_;                                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                               \
+      sc.dbg[4096 + ((long)blockIdx.x * 64 + (u)) * 4 + (k)] = t_;                         \
+    }                                                                                      \
+  } while (0)
+#else
+#define PTR(u, k) do { } while (0)
+#endif
 #define PDBG(slot)                                                                        \
   do {                                                                                    \
     if (sc.dbg) {                                                                         \
@@ -159,6 +171,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
           const uint8_t* xb = x_src(t, kb);
           bulk_load(sb + stage * b_bytes, xb, atom_b, &full[stage], pol_x);
           bulk_load(sb + stage * b_bytes + atom_b, xb + (long)n_tile * 128, atom_b, &full[stage], pol_x);
+          PTR(u, 0);
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
       }
@@ -172,6 +185,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         uint32_t phase = 0;
         for (long long u = u_begin; u < u_end; ++u) {
           mbar_wait(&full[stage], phase);
+          PTR((int)(u - u_begin), 1);
           mbar_arrive_remote(mapa_shared(&peer_full[stage], 0));
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
@@ -179,6 +193,7 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
         const uint32_t idesc = make_idesc_bf16(256, n_tile, 0, 0);
         int stage = 0, seg = 0;
         uint32_t phase = 0;
+        int uu = 0;   // unit index within the range (trace)
         for (int t = t_first; t <= t_last; ++t, ++seg) {
           int lo, hi;
           kb_range(t, lo, hi);
@@ -190,7 +205,9 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
           const uint32_t d = tmem + slot * 256;
           for (int kb = lo; kb < hi; ++kb) {
             mbar_wait(&full[stage], phase);
+            PTR(uu, 1);
             mbar_wait_cluster(&peer_full[stage], phase);
+            PTR(uu, 2);
             tc_fence_after();
             const uint32_t a_addr = smem_u32(sa + stage * a_bytes);
             const uint32_t b_addr = smem_u32(sb + stage * b_bytes);
@@ -202,6 +219,8 @@ __global__ void __launch_bounds__(PAIR_THREADS, 1)
               tc_mma2_f16(d, ad, bd, idesc, (kb > lo || k > 0) ? 1u : 0u);
             }
             tc_commit2_mc(&empty[stage], 3);
+            PTR(uu, 3);
+            ++uu;
             if (++stage == stages) { stage = 0; phase ^= 1; }
           }
           tc_commit2_mc(&acc_full[slot], 3);
