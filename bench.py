@@ -534,6 +534,20 @@ def main():
     # a chunk with recomputed ones; here the UNFUSED kernel moves every cached row of the request
     # (read K, V from the store + write rotated K, V into request rows) as one launch, alone.
     others["kv_relocate_single_launch"] = relocate_standalone(P, model, req, store, runner, flush, hbm)
+    # attention against HBM as well (its K/V bytes per launch; the tensor fraction above is capped at ~0.37
+    # by its 94 F/B arithmetic intensity) and the whole request against HBM: every launch's algorithmic
+    # bytes (weights + activations + K/V) at the measured copy bandwidth vs the p50 TTFT
+    if "attention" in agg:
+        ms_k, c_k, nb_k, fl_k = agg["attention"]
+        a = nb_k / (ms_k / 1e3) / 1e9
+        others["attention_hbm"] = {"bound": "hbm", "achieved": round(a, 1), "peak": hbm, "unit": "GB/s",
+                                   "frac": round(a / hbm, 4),
+                                   "algorithmic": f"{nb_k / c_k / 1e6:.2f} MB per launch (K/V read once)"}
+    req_bytes = sum(v[2] for v in agg.values()) / ntrace
+    t_hbm_ms = req_bytes / (hbm * 1e9) * 1e3
+    others["request_hbm"] = {"bound": "hbm", "algorithmic_gb": round(req_bytes / 1e9, 3),
+                             "t_hbm_ms": round(t_hbm_ms, 3), "ttft_ms": round(p50, 4),
+                             "frac": round(t_hbm_ms / p50, 4), "peak": hbm, "unit": "GB/s"}
     if args.trace:
         with open(args.trace, "w") as fh:
             json.dump({"kernels": kernels, "agg": {k: v for k, v in agg.items()}}, fh, indent=1)
