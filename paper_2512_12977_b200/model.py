@@ -281,7 +281,7 @@ class DeviceWeights:
         self.n_qkv_enc = _round_up(3 * cfg.kv_dim, 128)
         self.kkv_enc = _round_up(cfg.kv_dim, 128)
         self.layers: list[dict] = []
-        self.cos = self.sin = None
+        self.cos = self.sin = self.cs = None
         self.tab_rows = 0
 
     # -- construction

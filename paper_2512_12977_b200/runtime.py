@@ -424,7 +424,7 @@ class Runner:
                 enc_scratch_rows.data_ptr() if enc_scratch_rows is not None else 0,
                 kv_pool.k.data_ptr() if kv_pool is not None else 0,
                 kv_pool.v.data_ptr() if kv_pool is not None else 0, kv_pool.P if kv_pool is not None else 0,
-                pack.dev.data_ptr(), dw.cos.data_ptr(), self.splitk.data_ptr(),
+                pack.dev.data_ptr(), dw.cos.data_ptr(), dw.cs.data_ptr(), self.splitk.data_ptr(),
                 self.shared.bufs["attn_ws_o"].data_ptr(), self.shared.bufs["attn_ws_ml"].data_ptr()) + tuple(
                     t.data_ptr() for t in buf.values())
         buf["kv_pool"] = kv_pool                      # cached chunks are read from its pages
