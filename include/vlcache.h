@@ -54,7 +54,8 @@ int vlc_pack_operand(const void* src, int rows, int cols, int ld, void* dst, int
 #define VLC_EPI_SWIGLU 4    /* rows interleaved gate/up: out[j][f/2] = silu(g)*u (model.py:262)  */
 #define VLC_EPI_QKV_PLAIN 5 /* q/k/v sections -> out/out2/out3          (model.py:318)           */
 #define VLC_EPI_QKV_ROPE 6  /* q rot -> out[map1[j]], k -> out4[j] (pre-RoPE) and rot -> out2
-                               [map2[j]], v -> out3[map2[j]]            (engine.py:176-180)       */
+                               [map2[j]], v -> out3[map2[j]]            (engine.py:176-180);
+                               head_dim % 8 == 0, else VLC_ERR_UNSUPPORTED                         */
 
 typedef struct vlc_epilogue {
   int kind;

@@ -211,6 +211,8 @@ int vlc_gemm_bf16(const void* w, int n_pad, int k_pad, const void* x, int x_rows
   if (epi->m_tokens != m_tokens) return fail(VLC_ERR_INVALID, "gemm: epilogue m_tokens mismatch");
   if (epi->kind == VLC_EPI_QKV_ROPE && (!epi->map2 || !epi->pos || !epi->cos_tab || epi->hd % 2))
     return fail(VLC_ERR_INVALID, "gemm: QKV_ROPE needs map2/pos/tables");
+  if (epi->kind == VLC_EPI_QKV_ROPE && epi->hd % 8)   // the epilogue rotates 4 pairs per lane
+    return fail(VLC_ERR_UNSUPPORTED, "gemm: QKV_ROPE needs head_dim % 8 == 0");
   return cuda_status(launch_gemm(w, n_pad, k_pad, x, x_rows_cap, m_tokens, *epi, max_ctas, ws, ws_bytes, counters,
                                  stream),
                      "gemm_bf16");

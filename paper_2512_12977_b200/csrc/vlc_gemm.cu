@@ -357,15 +357,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             s_pos = s_rope - tok0;
             s_dr = s_rope + 512 - tok0;
           }
-          RopeMeta ma, mb;   // two register-resident sets, roles alternate (no copies, no local memory)
+          // eight features per lane (head_dim % 8 == 0, validated by vlc_gemm_bf16): lanes 0-15 / 16-31 take
+          // two tokens per step, each rotated half one 8-byte store (vlc_gemm_epi.cuh)
+          const int Fl = m0 + 8 * (lane & 15), bl = quad + 4 * (lane >> 4);
+          const float* sbl = stage_buf + 8 * (lane & 15);
+          RopeMeta8 ma, mb;   // two register-resident sets, roles alternate (no copies, no local memory)
           if (eg < nch)
-            rope_prefetch(epi, m0 + 4 * lane, tok0 + eg * 32, quad, min(32, epi.m_tokens - tok0 - eg * 32), ma,
-                          s_pos, s_dr);
+            rope8_prefetch(epi, Fl, tok0 + eg * 32, bl, min(32, epi.m_tokens - tok0 - eg * 32), ma, s_pos, s_dr);
           mbar_wait(&acc_full[slot], (seg >> 1) & 1);
           tc_fence_after();
           if (leader) DBG(3);
           const uint32_t d = tmem + slot * 256 + lane_off;
-          auto step = [&](int ci, const RopeMeta& cur, RopeMeta& nxt) {
+          auto step = [&](int ci, const RopeMeta8& cur, RopeMeta8& nxt) {
             const int c = ci * 32;
             float v[32];
             tmem_ld32(d + c, v);
@@ -374,10 +377,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             for (int jj = 0; jj < 32; ++jj) stage_buf[jj * 128 + row] = v[jj];
             asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
             if (ci + 2 < nch)     // the chunk after next's tables load while this chunk is stored
-              rope_prefetch(epi, m0 + 4 * lane, tok0 + c + 64, quad, min(32, epi.m_tokens - tok0 - c - 64), nxt,
-                            s_pos, s_dr);
-            rope_store(epi, m0 + 4 * lane, tok0 + c, quad, min(32, epi.m_tokens - tok0 - c), cur,
-                       stage_buf + 4 * lane);
+              rope8_prefetch(epi, Fl, tok0 + c + 64, bl, min(32, epi.m_tokens - tok0 - c - 64), nxt, s_pos, s_dr);
+            rope8_store(epi, Fl, tok0 + c, bl, min(32, epi.m_tokens - tok0 - c), cur, sbl);
             asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
           };
           for (int ci = eg; ci < nch; ci += 4) {

@@ -104,94 +104,102 @@ __device__ __forceinline__ void write_group(const GemmEpi& e, int F, int j, floa
 }
 
 // QKV_ROPE epilogue split in two: the per-token metadata and RoPE table entries of a 32-token chunk
-// (rope_prefetch: independent of the accumulator, so the GEMM issues chunk c+1's -- and, before the
-// accumulator is ready, chunk 0's -- while it stores chunk c) and the rotation + stores (rope_store).
-struct RopeMeta {
-  int dr[8];        // destination row (q: map1, k / v: KV-cache row)
-  float2 c[8], s[8];
+// (rope8_prefetch: independent of the accumulator, so the GEMM issues the next chunk's -- and, before the
+// accumulator is ready, the first chunk's -- while it stores the current one) and the rotation + stores
+// (rope8_store).  s_pos / s_dr: the tile's per-token positions and destination rows staged in shared
+// memory (indexed by token), so a chunk's RoPE-table loads are one global round trip; NULL: global.
+// Eight features per lane (F multiple of 8: RoPE pairs t .. t+3 of one head, t a multiple of 4): lanes
+// 0-15 and 16-31 cover the 128 rows for two tokens at a time, tokens jj = b + 8q (q < 4) of the chunk with
+// b = quad + 4 (lane / 16).  Each rotated half (4 bf16) is one 8-byte store and a V row segment one 16-byte
+// store -- half the store instructions of the 4-feature mapping.  Needs head_dim % 8 == 0.
+struct RopeMeta8 {
+  int dr[4];
+  float4 c[4], s[4];   // cos / sin of pairs t .. t+3 for each token
 };
-// s_pos / s_dr: the tile's per-token positions and destination rows staged in shared memory (indexed by
-// token), so a chunk's RoPE-table loads are one global round trip, not two dependent ones; NULL: global
-__device__ __forceinline__ void rope_prefetch(const GemmEpi& e, int F, int j0, int quad, int jv, RopeMeta& m,
-                                              const int* s_pos, const int* s_dr) {
+__device__ __forceinline__ void rope8_prefetch(const GemmEpi& e, int F, int j0, int b, int jv, RopeMeta8& m,
+                                               const int* s_pos, const int* s_dr) {
   if (F >= e.n_valid) return;
   const int sec = F / e.seg, r = F - sec * e.seg;
   const int t = (r - (r / e.hd) * e.hd) >> 1;
-  int p[8];
+  int p[4];
   if (s_pos) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int j = j0 + quad + 4 * q;
-      if (quad + 4 * q < jv) p[q] = s_pos[j], m.dr[q] = s_dr[j];
+    for (int q = 0; q < 4; ++q) {
+      const int jj = b + 8 * q;
+      if (jj < jv) p[q] = s_pos[j0 + jj], m.dr[q] = s_dr[j0 + jj];
     }
   } else {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int j = j0 + quad + 4 * q;
-      if (quad + 4 * q < jv) {
+    for (int q = 0; q < 4; ++q) {
+      const int jj = b + 8 * q, j = j0 + jj;
+      if (jj < jv) {
         if (sec != 2) p[q] = __ldg(e.pos + j);
         m.dr[q] = sec == 0 ? (e.map1 ? __ldg(e.map1 + j) : j) : __ldg(e.map2 + j);
       }
     }
   }
   if (sec == 2) return;
-  if (e.cs_tab) {   // interleaved (cos t, cos t+1, sin t, sin t+1): one 16-byte load per token
+  if (e.cs_tab) {   // interleaved (cos t, cos t+1, sin t, sin t+1): two 16-byte loads per token
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      if (quad + 4 * q < jv) {
-        const float4 cs = __ldg(reinterpret_cast<const float4*>(e.cs_tab + (long)p[q] * e.hd + 2 * t));
-        m.c[q] = make_float2(cs.x, cs.y);
-        m.s[q] = make_float2(cs.z, cs.w);
+    for (int q = 0; q < 4; ++q) {
+      if (b + 8 * q < jv) {
+        const float4* cs = reinterpret_cast<const float4*>(e.cs_tab + (long)p[q] * e.hd + 2 * t);
+        const float4 u0 = __ldg(cs), u1 = __ldg(cs + 1);
+        m.c[q] = make_float4(u0.x, u0.y, u1.x, u1.y);
+        m.s[q] = make_float4(u0.z, u0.w, u1.z, u1.w);
       }
     }
     return;
   }
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    if (quad + 4 * q < jv) {
+  for (int q = 0; q < 4; ++q) {
+    if (b + 8 * q < jv) {
       const long tab = (long)p[q] * e.tab_ld + t;
-      m.c[q] = __ldg(reinterpret_cast<const float2*>(e.cos_tab + tab));
-      m.s[q] = __ldg(reinterpret_cast<const float2*>(e.sin_tab + tab));
+      m.c[q] = __ldg(reinterpret_cast<const float4*>(e.cos_tab + tab));
+      m.s[q] = __ldg(reinterpret_cast<const float4*>(e.sin_tab + tab));
     }
   }
 }
-__device__ __forceinline__ void rope_store(const GemmEpi& e, int F, int j0, int quad, int jv, const RopeMeta& m,
-                                           const float* sb) {
+__device__ __forceinline__ void rope8_store(const GemmEpi& e, int F, int j0, int b, int jv, const RopeMeta8& m,
+                                            const float* sb) {
   if (F >= e.n_valid) return;
   const int sec = F / e.seg, r = F - sec * e.seg;
   if (sec == 2) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int jj = quad + 4 * q;
+    for (int q = 0; q < 4; ++q) {
+      const int jj = b + 8 * q;
       if (jj < jv) {
-        const float4 x = *reinterpret_cast<const float4*>(sb + jj * 128);
-        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(e.out3) + (long)m.dr[q] * e.ld3 + r) =
-            pack4_bf16(x.x, x.y, x.z, x.w);
+        const float4 x0 = *reinterpret_cast<const float4*>(sb + jj * 128);
+        const float4 x1 = *reinterpret_cast<const float4*>(sb + jj * 128 + 4);
+        const uint2 a = pack4_bf16(x0.x, x0.y, x0.z, x0.w), c = pack4_bf16(x1.x, x1.y, x1.z, x1.w);
+        *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.out3) + (long)m.dr[q] * e.ld3 + r) =
+            make_uint4(a.x, a.y, c.x, c.y);
       }
     }
     return;
   }
   const int half = e.hd >> 1;
-  const int head = r / e.hd, t = (r - head * e.hd) >> 1;   // pairs (t, t+half), (t+1, t+1+half)
+  const int head = r / e.hd, t = (r - head * e.hd) >> 1;   // pairs (t + i, t + i + half), i < 4
   const int fa = head * e.hd + t;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int jj = quad + 4 * q;
+  for (int q = 0; q < 4; ++q) {
+    const int jj = b + 8 * q;
     if (jj >= jv) continue;
-    const float2 c = m.c[q], sn = m.s[q];
-    const float4 x = *reinterpret_cast<const float4*>(sb + jj * 128);
-    const uint32_t lo = pack_bf16(x.x * c.x - x.y * sn.x, x.z * c.y - x.w * sn.y);
-    const uint32_t hi = pack_bf16(x.y * c.x + x.x * sn.x, x.w * c.y + x.z * sn.y);
+    const float4 c = m.c[q], sn = m.s[q];
+    const float4 x0 = *reinterpret_cast<const float4*>(sb + jj * 128);        // (t, t+h, t+1, t+1+h)
+    const float4 x1 = *reinterpret_cast<const float4*>(sb + jj * 128 + 4);    // (t+2, t+2+h, t+3, t+3+h)
+    const uint2 lo = pack4_bf16(x0.x * c.x - x0.y * sn.x, x0.z * c.y - x0.w * sn.y, x1.x * c.z - x1.y * sn.z,
+                                x1.z * c.w - x1.w * sn.w);
+    const uint2 hi = pack4_bf16(x0.y * c.x + x0.x * sn.x, x0.w * c.y + x0.z * sn.y, x1.y * c.z + x1.x * sn.z,
+                                x1.w * c.w + x1.z * sn.w);
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(sec == 0 ? e.out : e.out2) +
                        (long)m.dr[q] * (sec == 0 ? e.ldo : e.ld2);
-    // (lane-pair shuffles into one 8-byte store per lane: measured 7 us slower per QKV GEMM)
-    *reinterpret_cast<uint32_t*>(o + fa) = lo;
-    *reinterpret_cast<uint32_t*>(o + fa + half) = hi;
+    *reinterpret_cast<uint2*>(o + fa) = lo;
+    *reinterpret_cast<uint2*>(o + fa + half) = hi;
     if (sec == 1 && e.out4) {
-      const uint32_t plo = pack_bf16(x.x, x.z), phi = pack_bf16(x.y, x.w);
       __nv_bfloat16* kp = reinterpret_cast<__nv_bfloat16*>(e.out4) + (long)(j0 + jj) * e.ld4;
-      *reinterpret_cast<uint32_t*>(kp + fa) = plo;
-      *reinterpret_cast<uint32_t*>(kp + fa + half) = phi;
+      *reinterpret_cast<uint2*>(kp + fa) = pack4_bf16(x0.x, x0.z, x1.x, x1.z);
+      *reinterpret_cast<uint2*>(kp + fa + half) = pack4_bf16(x0.y, x0.w, x1.y, x1.w);
     }
   }
 }

@@ -110,12 +110,15 @@ def _perm_rows(kv, hd):
     return torch.tensor(idx)
 
 
-@pytest.mark.parametrize("hd,heads,m,cs_tab", [(128, 3, 37, False), (32, 8, 37, False), (16, 2, 37, False),
-                                              (128, 3, 37, True), (32, 8, 37, True), (128, 4, 300, True),
-                                              (128, 2, 200, False)])
-def test_gemm_qkv_rope_epilogue(nat, hd, heads, m, cs_tab):
+@pytest.mark.parametrize("hd,heads,m,cs_tab,splits", [
+    (128, 3, 37, False, 2), (32, 8, 37, False, 2), (16, 2, 37, False, 2), (128, 3, 37, True, 2),
+    (32, 8, 37, True, 2), (128, 4, 300, True, 2), (128, 2, 200, False, 2),
+    # one tile per CTA (decoupled rings, staged token metadata), C3-like widths
+    (128, 28, 236, True, 0), (128, 28, 236, False, 0), (128, 28, 141, True, 0), (64, 56, 200, True, 0),
+    (16, 64, 97, True, 0)])
+def test_gemm_qkv_rope_epilogue(nat, hd, heads, m, cs_tab, splits):
     """cs_tab: the interleaved (c0 c1 s0 s1) per-position table the model passes; without it the
-    epilogue reads the split cos/sin tables."""
+    epilogue reads the split cos/sin tables.  The epilogue rotates four pairs per lane (8 features)."""
     kv = hd * heads
     d = 128
     g = torch.Generator(device="cuda").manual_seed(hd)
@@ -139,7 +142,7 @@ def test_gemm_qkv_rope_epilogue(nat, hd, heads, m, cs_tab):
                map1=qmap.data_ptr(), map2=kvmap.data_ptr(), pos=pos.data_ptr(), cos_tab=cos.data_ptr(),
                sin_tab=sin.data_ptr(), tab_ld=hd // 2, hd=hd, seg=kv,
                cs_tab=cs.data_ptr() if cs_tab else None)
-    _gemm(nat, W, X, m, epi, 2)
+    _gemm(nat, W, X, m, epi, splits)
     Xf = X[:m].float()
     qr = _rope_ref(Xf @ Wq.float().t(), pos, hd)
     kr = _rope_ref(Xf @ Wk.float().t(), pos, hd)
@@ -149,6 +152,19 @@ def test_gemm_qkv_rope_epilogue(nat, hd, heads, m, cs_tab):
     assert (kc[kvmap.long()].float() - kr).abs().max().item() < tol(kr)
     assert (vc[kvmap.long()].float() - v).abs().max().item() < tol(v)
     assert (kpre.float() - Xf @ Wk.float().t()).abs().max().item() < tol(v)
+
+
+def test_gemm_qkv_rope_needs_head_dim_multiple_of_8(nat):
+    W = torch.zeros(128, 128, device="cuda", dtype=torch.bfloat16)
+    X = torch.zeros(16, 128, device="cuda", dtype=torch.bfloat16)
+    z = torch.zeros(64, device="cuda", dtype=torch.int32)
+    tab = torch.zeros(64 * 6, device="cuda")
+    out = torch.zeros(16, 36, device="cuda", dtype=torch.bfloat16)
+    epi = _epi(nat, kind=nat.EPI_QKV_ROPE, n_valid=108, m_tokens=16, out=out.data_ptr(), ldo=36, out2=out.data_ptr(),
+               ld2=36, out3=out.data_ptr(), ld3=36, map2=z.data_ptr(), pos=z.data_ptr(), cos_tab=tab.data_ptr(),
+               sin_tab=tab.data_ptr(), tab_ld=6, hd=12, seg=36)
+    with pytest.raises(nat.NativeError, match="head_dim % 8"):
+        _gemm(nat, W, X, 16, epi, 0)
 
 
 def _attn_ref(q, k, v, qpos, heads, hd, nkeys):
