@@ -413,7 +413,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                    *reinterpret_cast<const float4*>(stage_buf + jj * 128 + 4 * lane));
         } else {
           const int jv = min(jmax, epi.m_tokens - tok0 - c);
-          write_chunk<KIND>(epi, m0 + hoff + 4 * lane, tok0 + c, quad, jv, stage_buf + 4 * lane);
+          bool done = false;
+          if constexpr (KIND == EPI_SWIGLU && H == 1) {   // packed SwiGLU: four outputs per lane (one store)
+            done = swiglu8_packed(epi, m0 + 8 * (lane & 15), tok0 + c, quad + 4 * (lane >> 4), jv,
+                                  stage_buf + 8 * (lane & 15));
+          }
+          if (!done) write_chunk<KIND>(epi, m0 + hoff + 4 * lane, tok0 + c, quad, jv, stage_buf + 4 * lane);
         }
         asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
       }

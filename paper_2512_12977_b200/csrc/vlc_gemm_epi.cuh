@@ -204,6 +204,32 @@ __device__ __forceinline__ void rope8_store(const GemmEpi& e, int F, int j0, int
   }
 }
 
+// SwiGLU into the PACKED layout with eight features (four outputs) per lane, lanes 0-15 / 16-31 on two
+// tokens per step (b = quad + 4 (lane / 16), tokens jj = b + 8q): one 8-byte store per lane per token --
+// half the store instructions of write_chunk's four-feature mapping.  Returns false (caller falls back)
+// unless the output is packed, the 8 features are valid and the chunk sits inside one row tile.
+__device__ __forceinline__ bool swiglu8_packed(const GemmEpi& e, int F, int j0, int b, int jv, const float* sb) {
+  const int R = e.pk_rows;
+  if (R <= 0 || F + 8 > e.n_valid) return false;
+  const int rt = j0 / R, r0 = j0 - rt * R;
+  if (r0 + 32 > R) return false;
+  const int k = F >> 1;                                     // outputs k .. k+3 (k % 4 == 0)
+  const long base = ((((long)rt * e.pk_kb + (k >> 7)) * 2 + ((k >> 6) & 1)) * R) * 64 + (k & 7);
+  const int c = (k >> 3) & 7;
+  __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(e.out);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int jj = b + 8 * q;
+    if (jj >= jv) continue;
+    const int r = r0 + jj;
+    const float4 x0 = *reinterpret_cast<const float4*>(sb + jj * 128);       // (g k, u k, g k+1, u k+1)
+    const float4 x1 = *reinterpret_cast<const float4*>(sb + jj * 128 + 4);   // (g k+2, u k+2, ...)
+    *reinterpret_cast<uint2*>(o + base + (long)r * 64 + ((c ^ (r & 7)) << 3)) =
+        pack4_bf16(silu_f(x0.x) * x0.y, silu_f(x0.z) * x0.w, silu_f(x1.x) * x1.y, silu_f(x1.z) * x1.w);
+  }
+  return true;
+}
+
 // The up-to-8 tokens jj = quad + 4q (q < 8, jj < jv) of one 32-token chunk, features [F, F+4):
 // loads of per-token metadata / RoPE tables are issued for all tokens before any store, so the
 // epilogue is not a chain of dependent global-load latencies.  sb = stage + 4*lane (token stride
