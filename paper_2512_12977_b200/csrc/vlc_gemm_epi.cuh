@@ -6,7 +6,13 @@
 
 namespace vlc {
 
-__device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
+// silu(g) = g sigmoid(g) = g (1 + tanh(g / 2)) / 2: one MUFU op (tanh.approx, ~2^-11 relative) instead of
+// two (ex2 + rcp) -- the SwiGLU epilogue is MUFU-paced (gate/up 31.25 -> 30.3 us at C3)
+__device__ __forceinline__ float silu_f(float g) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * g));
+  return 0.5f * g * (1.0f + t);
+}
 
 __device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) {
   return make_uint2(pack_bf16(a, b), pack_bf16(c, d));
