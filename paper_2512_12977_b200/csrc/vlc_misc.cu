@@ -107,13 +107,15 @@ __global__ void __launch_bounds__(128) rmsnorm_kernel(float* __restrict__ x, int
   __shared__ float red[4];
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
-  const float denom = sqrtf((red[0] + red[1] + red[2] + red[3]) / (float)d + eps);
+  // one reciprocal per row, then multiplies (the reference divides, model.py:257-259; the product differs by
+  // <= 1 fp32 ulp before the bf16 rounding of the output)
+  const float inv = 1.0f / sqrtf((red[0] + red[1] + red[2] + red[3]) / (float)d + eps);
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
     const int i = threadIdx.x + 128 * k;
     if (i >= n4) break;
-    const float4 y = make_float4((v[k].x / denom) * gg[k].x, (v[k].y / denom) * gg[k].y,
-                                 (v[k].z / denom) * gg[k].z, (v[k].w / denom) * gg[k].w);
+    const float4 y = make_float4((v[k].x * inv) * gg[k].x, (v[k].y * inv) * gg[k].y,
+                                 (v[k].z * inv) * gg[k].z, (v[k].w * inv) * gg[k].w);
     if (OUT_F32) {
       reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + (long)r * ldo)[i] = y;
     } else {
