@@ -17,6 +17,8 @@ import paper_2512_12977_b200 as P  # noqa: E402
 from paper_2512_12977_b200 import _native as N  # noqa: E402
 if os.environ.get("VLC_LIB_VARIANT"):          # experiment builds (tools/build_variant.py)
     N.LIB_PATH = os.environ["VLC_LIB_VARIANT"]
+for kv in filter(None, os.environ.get("VLC_TUNING", "").split(",")):   # e.g. VLC_TUNING=17:1,10:0
+    N.load().vlc_set_tuning(*(int(x) for x in kv.split(":")))
 from paper_2512_12977_b200.engine import _runner, prefill_with_reuse  # noqa: E402
 from paper_2512_12977_b200.toydata import make_images, prompt_ids  # noqa: E402
 
