@@ -496,7 +496,7 @@ unsigned long long* debug_buffer() { return h_dbg; }
 int g_coop = 1;
 int g_pdl = 1;
 
-int g_pair = 160;         // tuning key 10: CTA-pair stream-K GEMM (multi-wave) when the token tile >= this (0 = off)
+int g_pair = 0;           // tuning key 10: CTA-pair stream-K GEMM (multi-wave) when the token tile >= this (0 = off: measured)
 int g_unsplit_min = 64;   // tuning key 9: tile count from which each tile gets its own CTA (no split-K)
 int g_wide = 1;   // tuning key 7: 0 auto, 1 never use 256-row tiles (default: measured slower), 2 always
 int g_aligned_split = 2;   // tuning key 17: tile-aligned split-K instead of stream-K when it fills >= 70% of SMs
@@ -550,9 +550,12 @@ cudaError_t launch_gemm(const void* W, int n_pad, int k_pad, const void* X, int 
   if (m_tokens <= 0) return cudaSuccess;
   const int n_tile = gemm_row_tile(n_pad, m_tokens);
   const bool wide = n_tile > 256;   // one wide token tile: one k-range of one weight tile per CTA, decoupled rings
-  // Multi-wave GEMMs (the LM head) with token tiles >= pair_min: the CTA-pair stream-K kernel
-  // (vlc_gemm_pair.cu; head at c = 236: 282 -> 258 us, profiles/r2_gemm_pair_streamk.txt).  The
-  // one-wave projections stay on the single-CTA kernel: under stream-K over all 74 pairs they are
+  // Multi-wave GEMMs (the LM head) with token tiles >= pair_min (key 10; default 0 = off): the CTA-pair
+  // stream-K kernel (vlc_gemm_pair.cu).  Alone it is faster on the head (c = 236: 282 -> 258 us,
+  // profiles/r2_gemm_pair_streamk.txt), but inside the prefill graph the single-CTA head gives the lower
+  // TTFT (C3: 3.81 -> 3.77 ms, three A/B rounds, tools/ab_ttft.py VLC_TUNING=10:160 vs default): the
+  // cluster launch starts later behind the last layer.  The one-wave projections stay on the single-CTA
+  // kernel as well: under stream-K over all 74 pairs they are
   // L2-throughput bound like it (146 vs 219 MB through L2 but ~8 vs ~10 TB/s) and pay the exposed
   // last-segment epilogue on every SM (QKV 31.2 -> 32.9 us, gate/up 32.4 -> 38.3 us at c = 236).
   //  g_pair < 0: force the pair kernel from n_tile >= -g_pair (tests); 0: off
