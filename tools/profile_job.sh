@@ -8,6 +8,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-
 python tools/launch_summary.py gpurun_out/r2_launches.csv > gpurun_out/r2_launches.txt; cat gpurun_out/r2_launches.txt
 timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -c 9 \
   -o gpurun_out/r2_full_layer0 -f python tools/profile_step.py > gpurun_out/ncu_full.log 2>&1
-timeout 600 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:gemm_pair -c 1 \
+timeout 600 ncu --set full --import-source on --clock-control none --profile-from-start off --launch-skip 198 -c 1 \
   -o gpurun_out/r2_full_head -f python tools/profile_step.py >> gpurun_out/ncu_full.log 2>&1
 tail -3 gpurun_out/ncu_full.log
