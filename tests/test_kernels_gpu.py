@@ -419,7 +419,7 @@ def test_gemm_tile_modes_swiglu_packed(nat, gemm_mode, mode):
 def pair_mode(nat):
     nat.load().vlc_set_tuning(10, -32)     # force the CTA-pair kernel from 32-token tiles
     yield
-    nat.load().vlc_set_tuning(10, 96)
+    nat.load().vlc_set_tuning(10, 0)      # the default: pair kernel off
 
 
 @pytest.mark.parametrize("n_pad,k_pad,m", [(256, 128, 32), (512, 256, 100), (10752, 3584, 236), (2048, 256, 600),

@@ -95,7 +95,7 @@ if __name__ == "__main__":
             print(f"=== pair threshold {pair}")
             for (n, kk, m, c) in ((10752, 3584, 236, 0), (14336, 3584, 236, 0)):
                 phases(n, kk, m, c, kind="pair" if pair else None)
-        lib.vlc_set_tuning(10, 96)
+        lib.vlc_set_tuning(10, 0)
     if mode == "pairtile":        # CTA-pair kernel with one 256-row tile per pair (no stream-K) vs single-CTA
         for pair in (0, -16, 0, -16):
             lib.vlc_set_tuning(10, pair)
@@ -105,7 +105,7 @@ if __name__ == "__main__":
                 run(n, kk, m, c)
                 if pair:
                     phases(n, kk, m, c, kind="pair")
-        lib.vlc_set_tuning(10, 160)
+        lib.vlc_set_tuning(10, 0)
     if mode == "decoupled":       # one-tile GEMMs with decoupled weight / activation rings (key 18)
         for dec in (2, 12, 13, 14, 2, 13):
             lib.vlc_set_tuning(18, dec)
@@ -155,7 +155,7 @@ if __name__ == "__main__":
             lib.vlc_set_tuning(10, pair)
             print(f"-- pair {pair}", flush=True)
             run(152064, 3584, 236, 0, kind=N.EPI_F32, reps=6)
-        lib.vlc_set_tuning(10, 96)
+        lib.vlc_set_tuning(10, 0)
     if mode == "aligned":         # tile-aligned split-K: divisor splits (key 17 = 1) vs any split (2)
         for al in (1, 2, 1, 2):
             lib.vlc_set_tuning(17, al)
